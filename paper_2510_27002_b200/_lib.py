@@ -1,0 +1,119 @@
+"""ctypes binding of libjz (include/jz.h).
+
+This is the only place the Python mirror touches native code.  There is no CPU
+fallback: if libjz.so is missing, or the current device is not an sm_100 GPU,
+every device entry point raises.  Status codes map back to the reference's
+exception types (ValueError / IndexError / NonFiniteGradient).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libjz.so"
+
+JZ_OK, JZ_EINVAL, JZ_EINDEX, JZ_ECUDA, JZ_EUNSUPPORTED, JZ_ENONFINITE = 0, -1, -2, -3, -4, -5
+
+EPI_F32, EPI_BF16, EPI_RESID, EPI_GELU, EPI_GELU_BWD, EPI_F32_ACC, EPI_BF16_F32 = range(7)
+
+_P, _I64, _I32, _F32, _F64, _U64 = C.c_void_p, C.c_int64, C.c_int, C.c_float, C.c_double, C.c_uint64
+
+# name -> argtypes (restype is int status unless listed in _RESTYPE)
+PROTOTYPES: dict[str, list] = {
+    "jz_device_check": [_I32],
+    "jz_gemm_workspace_bytes": [_I64, _I64, _I32],
+    "jz_gemm_bf16": [_P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I64, _I64, _I64,
+                     _I32, _P, _P, _I64, _P, _I64, _I32, _P, _P],
+}
+_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_last_error": C.c_char_p,
+            "jz_build_info": C.c_char_p}
+
+
+class NonFiniteGradient(Exception):
+    """Raised when a gradient contains NaN/Inf (mirrors deskworld.optim.NonFiniteGradient)."""
+
+
+_lib = None
+_lock = threading.Lock()
+_checked_devices: set[int] = set()
+
+
+def load() -> C.CDLL:
+    """Load libjz.so (building it first when sources are present and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists() and os.environ.get("JZ_NO_AUTOBUILD") != "1":
+            from . import build as _build
+            _build.build()
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"libjz.so not found at {LIB_PATH}; run `python -m paper_2510_27002_b200.build`")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, argtypes in PROTOTYPES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPE.get(name, _I32)
+        for name in ("jz_last_error", "jz_build_info"):
+            fn = getattr(lib, name)
+            fn.argtypes = []
+            fn.restype = C.c_char_p
+        _lib = lib
+        return lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(PROTOTYPES) + ["jz_last_error", "jz_build_info"]
+
+
+def last_error() -> str:
+    return load().jz_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = "") -> None:
+    if status == JZ_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if status == JZ_EINVAL:
+        raise ValueError(msg)
+    if status == JZ_EINDEX:
+        raise IndexError(msg)
+    if status == JZ_ENONFINITE:
+        raise NonFiniteGradient(msg)
+    raise RuntimeError(f"libjz status {status}: {msg}")
+
+
+def ensure_device(device: torch.device | int | None = None) -> int:
+    """Fail loudly unless a CUDA sm_100 device is present (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2510_27002_b200 needs a CUDA B200 (sm_100) GPU; none is visible")
+    if device is None:
+        idx = torch.cuda.current_device()
+    elif isinstance(device, int):
+        idx = device
+    else:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _checked_devices:
+        check(load().jz_device_check(idx), "device check")
+        _checked_devices.add(idx)
+    return idx
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)

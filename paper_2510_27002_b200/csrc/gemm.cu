@@ -1,0 +1,470 @@
+// K1: persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   D[M,N] = epilogue(A[M,K] . B[K,N]),  bf16 operands, fp32 accumulation in TMEM.
+//
+// Replaces deskworld nn.linear (nn.py:43-47) and the matmul forward/backward of
+// autodiff.Tensor.__matmul__ (autodiff.py:180-193): the forward (X.W), the input
+// gradient (dY.W^T) and the weight gradient (X^T.dY) are the same kernel with the
+// operand "major-ness" carried in the UMMA instruction descriptor, so no operand is
+// ever transposed in HBM.
+//
+// Roles (192 threads, one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: A/B tiles -> smem ring (128B swizzle), mbarrier tx
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=BN, K=16)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+// TMEM holds two BN-column fp32 accumulators so the epilogue of tile i overlaps the
+// main loop of tile i+1.
+#include <mutex>
+
+#include "common.h"
+#include "ptx.cuh"
+
+namespace jz {
+
+constexpr int kGemmThreads = 192;
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+struct GemmParams {
+  int M, N, K;
+  int m_tiles, n_tiles, splits, kb_total, kb_per_split;
+  int epi;
+  void* D;
+  int64_t ldd;
+  const float* bias;
+  const void* aux;
+  int64_t ldaux;
+  void* D2;
+  int64_t ldd2;
+};
+
+template <int BN>
+struct GemmShape {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+JZ_DEV float fast_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+JZ_DEV float gelu_fast(float x) {
+  const float c = 0.7978845608028654f;
+  float inner = (x + 0.044715f * (x * x * x)) * c;
+  return 0.5f * (x * (1.0f + fast_tanh(inner)));
+}
+
+JZ_DEV float gelu_grad_fast(float x) {
+  const float c = 0.7978845608028654f;
+  float x2 = x * x;
+  float t = fast_tanh((x + 0.044715f * x2 * x) * c);
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * (c * (1.0f + 0.134145f * x2));
+}
+
+// Epilogue for one thread: row m, 32 consecutive columns starting at n.
+JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], float* ws_out) {
+  const int N = p.N;
+  const bool full = (n + 32 <= N);
+  if (p.bias != nullptr && ws_out == nullptr) {
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 b = *reinterpret_cast<const float4*>(p.bias + n + j);
+        v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
+      }
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (n + j < N) v[j] += p.bias[n + j];
+    }
+  }
+  if (ws_out != nullptr) {  // split-K partial: plain fp32 [M][N]
+    float* dst = ws_out + (int64_t)m * N + n;
+    if (full && (N % 4 == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (n + j < N) dst[j] = v[j];
+    }
+    return;
+  }
+  const bool vec8 = full && (p.ldd % 8 == 0);
+  switch (p.epi) {
+    case JZ_EPI_F32:
+    case JZ_EPI_F32_ACC:
+    case JZ_EPI_RESID:
+    case JZ_EPI_BF16_F32: {
+      float* dst = reinterpret_cast<float*>(p.D) + (int64_t)m * p.ldd + n;
+      if (p.epi == JZ_EPI_RESID) {
+        const float* src = reinterpret_cast<const float*>(p.aux) + (int64_t)m * p.ldaux + n;
+        if (full && (p.ldaux % 4 == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 r = *reinterpret_cast<const float4*>(src + j);
+            v[j] += r.x; v[j + 1] += r.y; v[j + 2] += r.z; v[j + 3] += r.w;
+          }
+        } else {
+          for (int j = 0; j < 32; ++j)
+            if (n + j < N) v[j] += src[j];
+        }
+      } else if (p.epi == JZ_EPI_F32_ACC) {
+        if (full && (p.ldd % 4 == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 r = *reinterpret_cast<const float4*>(dst + j);
+            v[j] += r.x; v[j + 1] += r.y; v[j + 2] += r.z; v[j + 3] += r.w;
+          }
+        } else {
+          for (int j = 0; j < 32; ++j)
+            if (n + j < N) v[j] += dst[j];
+        }
+      }
+      if (full && (p.ldd % 4 == 0)) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n + j < N) dst[j] = v[j];
+      }
+      if (p.epi == JZ_EPI_BF16_F32) {
+        __nv_bfloat16* d2 = reinterpret_cast<__nv_bfloat16*>(p.D2) + (int64_t)m * p.ldd2 + n;
+        if (full && (p.ldd2 % 8 == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 w = make_uint4(pack_bf16(v[j], v[j + 1]), pack_bf16(v[j + 2], v[j + 3]),
+                                 pack_bf16(v[j + 4], v[j + 5]), pack_bf16(v[j + 6], v[j + 7]));
+            *reinterpret_cast<uint4*>(d2 + j) = w;
+          }
+        } else {
+          for (int j = 0; j < 32; ++j)
+            if (n + j < N) d2[j] = __float2bfloat16_rn(v[j]);
+        }
+      }
+      break;
+    }
+    case JZ_EPI_BF16:
+    case JZ_EPI_GELU:
+    case JZ_EPI_GELU_BWD: {
+      if (p.epi == JZ_EPI_GELU) {
+        __nv_bfloat16* d2 = reinterpret_cast<__nv_bfloat16*>(p.D2) + (int64_t)m * p.ldd2 + n;
+        if (full && (p.ldd2 % 8 == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 w = make_uint4(pack_bf16(v[j], v[j + 1]), pack_bf16(v[j + 2], v[j + 3]),
+                                 pack_bf16(v[j + 4], v[j + 5]), pack_bf16(v[j + 6], v[j + 7]));
+            *reinterpret_cast<uint4*>(d2 + j) = w;
+          }
+        } else {
+          for (int j = 0; j < 32; ++j)
+            if (n + j < N) d2[j] = __float2bfloat16_rn(v[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+      } else if (p.epi == JZ_EPI_GELU_BWD) {
+        const __nv_bfloat16* pre =
+            reinterpret_cast<const __nv_bfloat16*>(p.aux) + (int64_t)m * p.ldaux + n;
+        if (full && (p.ldaux % 8 == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 w = *reinterpret_cast<const uint4*>(pre + j);
+            float2 a = unpack_bf16(w.x), b = unpack_bf16(w.y), c = unpack_bf16(w.z),
+                   d = unpack_bf16(w.w);
+            v[j] *= gelu_grad_fast(a.x); v[j + 1] *= gelu_grad_fast(a.y);
+            v[j + 2] *= gelu_grad_fast(b.x); v[j + 3] *= gelu_grad_fast(b.y);
+            v[j + 4] *= gelu_grad_fast(c.x); v[j + 5] *= gelu_grad_fast(c.y);
+            v[j + 6] *= gelu_grad_fast(d.x); v[j + 7] *= gelu_grad_fast(d.y);
+          }
+        } else {
+          for (int j = 0; j < 32; ++j)
+            if (n + j < N) v[j] *= gelu_grad_fast(__bfloat162float(pre[j]));
+        }
+      }
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.D) + (int64_t)m * p.ldd + n;
+      if (vec8) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 w = make_uint4(pack_bf16(v[j], v[j + 1]), pack_bf16(v[j + 2], v[j + 3]),
+                               pack_bf16(v[j + 4], v[j + 5]), pack_bf16(v[j + 6], v[j + 7]));
+          *reinterpret_cast<uint4*>(dst + j) = w;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n + j < N) dst[j] = __float2bfloat16_rn(v[j]);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     GemmParams p, float* ws) {
+  using S = GemmShape<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + S::STAGES;
+  uint64_t* tfull_bar = empty_bar + S::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S::STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int units = p.m_tiles * p.n_tiles * p.splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tile = u / p.splits, split = u % p.splits;
+        const int m0 = (tile / p.n_tiles) * BM, n0 = (tile % p.n_tiles) * BN;
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], S::STAGE_BYTES);
+          uint8_t* a_dst = smem + stage * S::STAGE_BYTES;
+          uint8_t* b_dst = a_dst + S::A_BYTES;
+          const int k = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(a_dst, &tmA, &full_bar[stage], k, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(a_dst + j * (64 * BK * 2), &tmA, &full_bar[stage], m0 + 64 * j, k);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_dst, &tmB, &full_bar[stage], k, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(b_dst + j * (64 * BK * 2), &tmB, &full_bar[stage], n0 + 64 * j, k);
+          }
+          if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int split = u % p.splits;
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * S::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + S::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? sdesc_sw128(a_addr + kk * 2048, 64 * BK * 2, 1024)
+                                        : sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? sdesc_sw128(b_addr + kk * 2048, 64 * BK * 2, 1024)
+                                        : sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            umma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    const uint32_t quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int tile = u / p.splits, split = u % p.splits;
+      const int m0 = (tile / p.n_tiles) * BM, n0 = (tile % p.n_tiles) * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int m = m0 + quarter * 32 + lane;
+      float* ws_out = (p.splits > 1) ? ws + (int64_t)split * p.M * p.N : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + acc * BN + c * 32, r);
+        tmem_ld_wait();
+        const int n = n0 + c * 32;
+        if (m < p.M && n < p.N) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          epilogue_chunk(p, m, n, v, ws_out);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<S::TMEM_COLS>(tmem_base);
+  }
+}
+
+// Deterministic split-K reduction: fixed summation order over splits.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t MN, int N,
+                                     float* __restrict__ D, int64_t ldd, const float* bias,
+                                     int accumulate) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += ws[(int64_t)k * MN + i];
+    const int64_t m = i / N;
+    const int n = (int)(i - m * N);
+    if (bias) s += bias[n];
+    float* dst = D + m * ldd + n;
+    *dst = accumulate ? (*dst + s) : s;
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, float* ws,
+                       cudaStream_t stream) {
+  using S = GemmShape<BN>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
+  });
+  JZ_CUDA_TRY(attr_err);
+  const int units = p.m_tiles * p.n_tiles * p.splits;
+  const int grid = units < num_sms() ? units : num_sms();
+  gemm_bf16_kernel<BN, A_MN, B_MN><<<grid, kGemmThreads, S::SMEM_BYTES, stream>>>(ta, tb, p, ws);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+template <int BN>
+static int dispatch_major(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+                          const GemmParams& p, float* ws, cudaStream_t s) {
+  if (!a_mn && !b_mn) return launch_gemm<BN, false, false>(ta, tb, p, ws, s);
+  if (!a_mn && b_mn) return launch_gemm<BN, false, true>(ta, tb, p, ws, s);
+  if (a_mn && !b_mn) return launch_gemm<BN, true, false>(ta, tb, p, ws, s);
+  return launch_gemm<BN, true, true>(ta, tb, p, ws, s);
+}
+
+}  // namespace jz
+
+using namespace jz;
+
+extern "C" int64_t jz_gemm_workspace_bytes(int64_t M, int64_t N, int split_k) {
+  return split_k <= 1 ? 0 : (int64_t)split_k * M * N * (int64_t)sizeof(float);
+}
+
+extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb,
+                            int b_kmajor, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K,
+                            int epilogue, const float* bias, const void* aux, int64_t ldaux,
+                            void* D2, int64_t ldd2, int split_k, void* workspace,
+                            jz_stream_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  JZ_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem M=%lld N=%lld K=%lld", (long long)M,
+               (long long)N, (long long)K);
+  JZ_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims exceed int32");
+  JZ_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "gemm: lda/ldb must be multiples of 8 (got %lld, %lld)",
+               (long long)lda, (long long)ldb);
+  JZ_CHECK_ARG(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0, "gemm: A/B must be 16B aligned");
+  JZ_CHECK_ARG(epilogue >= JZ_EPI_F32 && epilogue <= JZ_EPI_BF16_F32, "gemm: bad epilogue %d", epilogue);
+  JZ_CHECK_ARG(D != nullptr, "gemm: null output");
+  if (epilogue == JZ_EPI_RESID || epilogue == JZ_EPI_GELU_BWD)
+    JZ_CHECK_ARG(aux != nullptr, "gemm: epilogue %d needs aux", epilogue);
+  if (epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_BF16_F32)
+    JZ_CHECK_ARG(D2 != nullptr, "gemm: epilogue %d needs D2", epilogue);
+  if (split_k < 1) split_k = 1;
+  if (split_k > 1) {
+    JZ_CHECK_ARG(epilogue == JZ_EPI_F32 || epilogue == JZ_EPI_F32_ACC,
+                 "gemm: split-K only with fp32 epilogues");
+    JZ_CHECK_ARG(workspace != nullptr, "gemm: split-K needs workspace");
+  }
+
+  const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
+  const int BN = N > 128 ? 256 : (N > 64 ? 128 : 64);
+
+  CUtensorMap ta, tb;
+  int rc;
+  if (!a_mn) rc = make_tmap_2d_bf16(&ta, A, K, M, lda, 64, 128);
+  else rc = make_tmap_2d_bf16(&ta, A, M, K, lda, 64, 64);
+  if (rc) return rc;
+  if (!b_mn) rc = make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, BN);
+  else rc = make_tmap_2d_bf16(&tb, B, N, K, ldb, 64, 64);
+  if (rc) return rc;
+
+  GemmParams p;
+  p.M = (int)M; p.N = (int)N; p.K = (int)K;
+  p.m_tiles = (int)((M + BM - 1) / BM);
+  p.n_tiles = (int)((N + BN - 1) / BN);
+  p.kb_total = (int)((K + BK - 1) / BK);
+  if (split_k > p.kb_total) split_k = p.kb_total;
+  p.kb_per_split = (p.kb_total + split_k - 1) / split_k;
+  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.epi = epilogue;
+  p.D = D; p.ldd = ldd;
+  p.bias = bias;
+  p.aux = aux; p.ldaux = ldaux;
+  p.D2 = D2; p.ldd2 = ldd2;
+
+  float* ws = p.splits > 1 ? reinterpret_cast<float*>(workspace) : nullptr;
+  if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, p, ws, stream);
+  else if (BN == 128) rc = dispatch_major<128>(a_mn, b_mn, ta, tb, p, ws, stream);
+  else rc = dispatch_major<64>(a_mn, b_mn, ta, tb, p, ws, stream);
+  if (rc) return rc;
+  if (p.splits > 1) {
+    const int64_t MN = M * N;
+    int blocks = (int)((MN + 255) / 256);
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, p.splits, MN, (int)N,
+                                                     reinterpret_cast<float*>(D), ldd, bias,
+                                                     epilogue == JZ_EPI_F32_ACC);
+    JZ_LAUNCH_CHECK();
+  }
+  return JZ_OK;
+}
