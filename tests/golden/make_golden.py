@@ -1,0 +1,213 @@
+"""Generate the golden fixtures that pin the oracle to the UNMODIFIED reference.
+
+Run in the build container (the reference is mounted read-only there; it does
+not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes small .npz files next to this script.  Every array is produced by calling
+deskworld (the reference) through its public API; nothing here re-implements it.
+"""
+from __future__ import annotations
+
+import dataclasses
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = os.environ.get("DESKWORLD_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+from deskworld import rng as R  # noqa: E402
+from deskworld.autodiff import Tensor  # noqa: E402
+from deskworld.dynamics import (ConditioningMode, DynamicsConfig, DynamicsModel,  # noqa: E402
+                                _sample_with_confidence, rollout, sample_masks)
+from deskworld.lam import LamConfig, LatentActionModel  # noqa: E402
+from deskworld.optim import adamw_init, adamw_step  # noqa: E402
+from deskworld.tokenizer import TokenizerConfig, VideoTokenizer, vq_quantize  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def save(name, **arrays):
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+    print(f"wrote {name}.npz ({sum(a.nbytes for a in map(np.asarray, arrays.values()))} B raw)")
+
+
+def grads_of(params, loss):
+    loss.backward()
+    return {f"grad.{k}": np.asarray(p.grad) for k, p in params.items() if p.grad is not None}
+
+
+def gen_rng():
+    keys = [(0,), (0, "dynamics", "step", 0), (7, "tokenizer-init"), (0, "dynamics", "step", 123456),
+            (2**63 + 5, "x"), ("a", "b", 3)]
+    folded = np.array([R.fold_key(*k) for k in keys], dtype=np.uint64)
+    g = R.stream(0, "dynamics", "step", 0)
+    words = g.integers(0, 2**64, size=64, dtype=np.uint64)
+    g = R.stream(0, "dynamics", "step", 0)
+    doubles = g.random(64)
+    m_small, p_small = sample_masks(R.stream(1, "m"), 3, 4, 16, return_p=True)
+    g = R.stream(0, "dynamics", "step", 5)
+    m_full, p_full = sample_masks(g, 2, 16, 256, return_p=True)
+    st = g.bit_generator.state
+    after = np.array([int(x) for x in st["state"]["counter"]] + [int(st["buffer_pos"])], dtype=np.uint64)
+    # a partially consumed generator (state continuation contract used by the sampler)
+    g = R.stream(9, "cont")
+    g.random(7)
+    cont = g.random((3, 5, 1))
+    save("rng_golden", folded=folded, words=words, doubles=doubles, m_small=m_small, p_small=p_small,
+         m_full=m_full, p_full=p_full, after_full=after, cont=cont,
+         key_strs=np.array(["|".join(map(str, k)) for k in keys]))
+
+
+def gen_vq():
+    out = {}
+    for dt, tag in ((np.float32, "f32"), (np.float64, "f64")):
+        g = R.stream(3, "vq", tag)
+        z = g.normal(size=(300, 8)).astype(dt) * 0.5
+        cb = g.normal(size=(32, 8)).astype(dt) * 0.5
+        z[5] = cb[7]                     # exact hit
+        cb_t = Tensor(cb, requires_grad=True)
+        z_t = Tensor(z, requires_grad=True)
+        idx, z_q, cbl, com = vq_quantize(z_t, cb_t)
+        (cbl + 0.25 * com + (z_q * z_q).sum()).backward()
+        out.update({f"{tag}.z": z, f"{tag}.cb": cb, f"{tag}.idx": idx, f"{tag}.zq": z_q.data,
+                    f"{tag}.cbl": np.asarray(cbl.data), f"{tag}.com": np.asarray(com.data),
+                    f"{tag}.gz": z_t.grad, f"{tag}.gcb": cb_t.grad})
+    # LAM-sized codebook (K=6) in f32
+    g = R.stream(4, "vq6")
+    z = g.normal(size=(45, 32)).astype(np.float32) * 0.1
+    cb = g.uniform(-1 / 6, 1 / 6, size=(6, 32)).astype(np.float32)
+    idx, _, _, _ = vq_quantize(Tensor(z), Tensor(cb))
+    out.update({"k6.z": z, "k6.cb": cb, "k6.idx": idx})
+    save("vq_golden", **out)
+
+
+DYN_SMALL = dict(model_dim=64, heads=2, ffn_dim=256, blocks=2, token_codes=64,
+                 action_latent_dim=16, patches_per_frame=16, max_frames=4)
+
+
+def gen_dynamics():
+    for mode in ("prepend", "additive"):
+        cfg = DynamicsConfig(**DYN_SMALL, mode=ConditioningMode(mode))
+        model = DynamicsModel(cfg, seed=3, dtype=np.float64)
+        g = R.stream(11, "dyn-golden", mode)
+        tokens = g.integers(0, 64, size=(2, 4, 16))
+        lat = Tensor(g.normal(size=(2, 3, 16)) * 0.5, requires_grad=True)
+        mask = sample_masks(R.stream(12, "dyn-mask", mode), 2, 4, 16)
+        logits = model.logits(tokens, lat, mask=mask)
+        loss, stats = model.loss(tokens, lat, R.stream(0, "unused"), mask=mask)
+        grads = grads_of(model.params, loss)
+        arrays = {f"param.{k}": v.data for k, v in model.params.items()}
+        save(f"dynamics_{mode}_golden", tokens=tokens, latents=lat.data, mask=mask, logits=logits.data,
+             loss=np.asarray(loss.data), grad_latents=lat.grad, **arrays, **grads)
+
+
+TOK_SMALL = dict(model_dim=32, heads=2, ffn_dim=128, blocks=1, codes=16, latent_dim=8,
+                 patch=4, height=8, width=8, max_frames=3)
+
+
+def gen_tokenizer_lam():
+    cfg = TokenizerConfig(**TOK_SMALL)
+    tok = VideoTokenizer(cfg, seed=5, dtype=np.float64)
+    g = R.stream(13, "tok-golden")
+    unit = g.uniform(-1, 1, size=(2, 3, 8, 8, 3))
+    recon, idx, losses = tok.forward(Tensor(unit))
+    grads = grads_of(tok.params, losses["total"])
+    frames_u8 = g.integers(0, 256, size=(2, 3, 8, 8, 3)).astype(np.uint8)
+    tok32 = VideoTokenizer(cfg, seed=5)
+    enc = tok32.encode(frames_u8)
+    dec = tok32.decode(enc)
+    save("tokenizer_golden", unit=unit, recon=recon.data, idx=idx,
+         **{f"loss.{k}": np.asarray(v.data) for k, v in losses.items()},
+         **{f"param.{k}": v.data for k, v in tok.params.items()}, **grads,
+         frames_u8=frames_u8, enc32=enc, dec32=dec)
+
+    lcfg = LamConfig(**{**TOK_SMALL, "codes": 6})
+    lam = LatentActionModel(lcfg, seed=6, dtype=np.float64)
+    unit = R.stream(14, "lam-golden").uniform(-1, 1, size=(2, 3, 8, 8, 3))
+    recon, idx, losses = lam.forward(Tensor(unit))
+    grads = grads_of(lam.params, losses["total"])
+    save("lam_golden", unit=unit, recon=recon.data, idx=idx,
+         **{f"loss.{k}": np.asarray(v.data) for k, v in losses.items()},
+         **{f"param.{k}": v.data for k, v in lam.params.items()}, **grads)
+
+
+def gen_sampling():
+    g = R.stream(15, "swc")
+    logits = (g.normal(size=(3, 16, 64)) * 2.0).astype(np.float32)
+    out = {"logits": logits}
+    for temp in (1.0, 0.7, 0.0):
+        s, c = _sample_with_confidence(logits, temp, R.stream(16, "swc", str(temp)))
+        out[f"sampled.{temp}"] = s
+        out[f"conf.{temp}"] = c
+    cfg = DynamicsConfig(**DYN_SMALL, mode=ConditioningMode.PREPEND)
+    for dt, tag in ((np.float32, "f32"), (np.float64, "f64")):
+        model = DynamicsModel(cfg, seed=4, dtype=dt)
+        gg = R.stream(17, "dec", tag)
+        prev = gg.integers(0, 64, size=(2, 2, 16))
+        lat = Tensor((gg.normal(size=(2, 2, 16)) * 0.5).astype(dt))
+        dec = model.decode_frame(prev, lat, steps=5, rng=R.stream(18, "dec", tag))
+        out.update({f"{tag}.prev": prev, f"{tag}.lat": lat.data, f"{tag}.decoded": dec})
+    # rollout through a real tokenizer (ground-truth action table), as test_dynamics.py:203-222
+    tcfg = TokenizerConfig(model_dim=64, heads=2, ffn_dim=256, blocks=1, codes=64, latent_dim=16,
+                           patch=4, height=16, width=16, max_frames=6)
+    tok = VideoTokenizer(tcfg, seed=6)
+    dcfg = DynamicsConfig(**{**DYN_SMALL, "max_frames": 6}, mode=ConditioningMode.GROUND_TRUTH)
+    dyn = DynamicsModel(dcfg, seed=7)
+    frames = R.stream(23, "f").integers(0, 256, size=(2, 4, 16, 16, 3)).astype(np.uint8)
+    actions = [np.array([1, 3]), np.array([2, 0])]
+    roll = rollout(tok, dyn, frames, actions, horizon=2, steps=3, rng=R.stream(9, "roll"))
+    out.update({"roll.frames": frames, "roll.out": roll})
+    save("sampling_golden", **out)
+
+
+def gen_adamw():
+    g = R.stream(19, "adam")
+    params = {n: Tensor(g.normal(size=s).astype(np.float32), requires_grad=True)
+              for n, s in (("b", (7,)), ("a", (3, 5)), ("c", (64,)))}
+    st = adamw_init(params)
+    init = {f"init.{n}": p.data.copy() for n, p in params.items()}
+    grads_all = {}
+    for step in range(3):
+        grads = {n: (g.normal(size=p.data.shape) * 10.0 ** (-step)).astype(np.float32) for n, p in params.items()}
+        for n, v in grads.items():
+            grads_all[f"grad{step}.{n}"] = v
+        adamw_step(params, grads, st, lr=3e-4 * (step + 1))
+    save("adamw_golden", **init, **grads_all, **{f"final.{n}": p.data for n, p in params.items()},
+         **{f"m.{n}": st.m[n] for n in params}, **{f"v.{n}": st.v[n] for n in params})
+
+
+def gen_jasmine_summary():
+    """Full jasmine-base dims (patch 4), B=1, fp32: loss, logits slice and gradient norms."""
+    from deskworld.configs import get_preset
+    cfg = dataclasses.replace(get_preset("jasmine-base"), patch=4, mode="pretrain_lam")
+    dcfg = cfg.dynamics_cfg()
+    t0 = time.time()
+    model = DynamicsModel(dcfg, seed=0)
+    tokens = R.stream(1, "bench-tokens").integers(0, 1024, size=(1, 16, 256))
+    lam_cb = R.stream(2, "golden-lam-cb").uniform(-1 / 6, 1 / 6, size=(6, 32)).astype(np.float32)
+    acts = R.stream(2, "bench-actions").integers(0, 6, size=(1, 15))
+    lat = Tensor(lam_cb[acts])
+    loss, stats = model.loss(tokens, lat, R.stream(0, "dynamics", "step", 0))
+    mask = sample_masks(R.stream(0, "dynamics", "step", 0), 1, 16, 256)
+    logits = model.logits(tokens, lat, mask=mask)
+    grads = grads_of(model.params, loss)
+    norms = {f"gnorm.{k[5:]}": np.float64(np.linalg.norm(v.astype(np.float64))) for k, v in grads.items()}
+    heads = {f"ghead.{k[5:]}": v.reshape(-1)[:16].copy() for k, v in grads.items()}
+    save("jasmine_b1_golden", tokens=tokens, acts=acts, lam_cb=lam_cb, mask=mask,
+         loss=np.asarray(loss.data), logits_slice=logits.data[0, :, :8, :16].copy(),
+         logits_rowsum=logits.data.sum(axis=-1)[0], **norms, **heads)
+    print(f"jasmine summary in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rng", "vq", "dynamics", "toklam", "sampling", "adamw", "jasmine"]
+    fns = {"rng": gen_rng, "vq": gen_vq, "dynamics": gen_dynamics, "toklam": gen_tokenizer_lam,
+           "sampling": gen_sampling, "adamw": gen_adamw, "jasmine": gen_jasmine_summary}
+    for w in which:
+        fns[w]()
