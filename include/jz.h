@@ -79,6 +79,121 @@ JZ_API int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void* B,
                  int epilogue, const float* bias, const void* aux, int64_t ldaux, void* D2,
                  int64_t ldd2, int split_k, void* workspace, jz_stream_t stream);
 
+
+/* ------------------------------------------------------------------------
+ * Column reductions (bias / LayerNorm-affine gradients; replaces the
+ * _unbroadcast sums of autodiff.py:22-32).  Deterministic two-stage scheme:
+ * a kernel writes `nparts` per-CTA partial rows, jz_reduce_partials sums them in
+ * index order.  jz_row_partials(rows) = the nparts the library uses.
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_row_partials(int64_t rows);
+JZ_API int jz_colsum_bf16(const void* x, int64_t rows, int cols, int64_t ld, float* part, int nparts,
+                          jz_stream_t stream);
+JZ_API int jz_reduce_partials(const float* part, int nparts, int64_t D, float* out, int accumulate,
+                              jz_stream_t stream);
+/* dst_bf16[r*ldd + c] = bf16(src[r*lds + c])  (weight shadows) */
+JZ_API int jz_cast_f32_bf16_2d(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
+                               int64_t cols, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K2  LayerNorm, eps inside the sqrt, biased variance, two-pass (nn.py:35-40).
+ * x f32 [rows, D] -> y bf16; mean/rstd f32 [rows] saved for the backward.
+ * skip_period > 0: rows r with r % skip_period == 0 are not written and the
+ * output is compacted (drops the prepended action token before to_logits,
+ * dynamics.py:135-136).  D multiple of 128, <= 1024.
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_layernorm_fwd(const float* x, int64_t rows, int D, const float* gamma, const float* beta,
+                            float eps, void* y_bf16, float* mean, float* rstd, int64_t skip_period,
+                            jz_stream_t stream);
+/* dres[r] = (accumulate ? dres[r] : 0) + LN_bwd(dy[r]); optional bf16 copy of dres;
+ * per-CTA partials of dgamma = sum dy*xhat, dbeta = sum dy, dbias = sum dres_out
+ * ([nparts, D] each, any may be NULL).  dy is compacted when skip_period > 0. */
+JZ_API int jz_layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* gamma,
+                            const float* dy, float* dres, int accumulate, void* dres_bf16,
+                            float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
+                            int64_t rows, int D, int64_t skip_period, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K7  masked softmax cross-entropy (nn.py:56-77 with weights = mask,
+ * dynamics.py:151-152), forward and backward in one pass:
+ *   row_loss[r] = mask[r] * (logsumexp(logits[r]) - logits[r, target[r]])
+ *   loss        = sum(row_loss) / count            (0 when count == 0)
+ *   dlogits     = grad_scale * mask[r]/count * (softmax - onehot)   (bf16)
+ * count is a device int (the number of masked positions, from jz_philox_mask).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_ce_fwd_bwd(const float* logits, int64_t rows, int K, const int64_t* targets,
+                         const uint8_t* mask, const int* count, float grad_scale, void* dlogits,
+                         float* row_loss, float* loss, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K13 AdamW (optim.py:34-62), f32 with numpy/NEP-50 scalar casting and no FMA
+ * contraction: bit-identical to the reference on identical inputs.
+ *   omb1 = f32(1-b1), omb2 = f32(1-b2), bc1 = f32(1-b1^t), bc2 = f32(1-b2^t),
+ *   lrwd = f32(lr*wd).  `flag` (device int, may be NULL): when non-zero the
+ *   update is skipped (a non-finite gradient was seen by jz_finite_check).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_finite_check(const float* g, int64_t n, int* flag, jz_stream_t stream);
+JZ_API int jz_adamw_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1,
+                         float b2, float omb1, float omb2, float bc1, float bc2, float eps, float lrwd,
+                         const int* flag, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K6  Bernoulli MaskGIT masks, bit-exact with dynamics.sample_masks
+ * (dynamics.py:52-62) over numpy's Philox4x64-10 stream (rng.py:38-44).
+ * The numpy bit-generator state (counter[4], key[2], buffer[4], buffer_pos) is
+ * passed in; samples [b0, b0+B_local) of a global batch of B_global are drawn by
+ * counter skip-ahead (data-parallel sharding).  mask u8 [B_local, T, N];
+ * *count += number of True entries (device int, must be zeroed by the caller).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_philox_mask(const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4,
+                          int buffer_pos, int64_t B_global, int64_t b0, int64_t B_local, int T, int N,
+                          double mask_limit, uint8_t* mask, int* count, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K5  dynamics input embedding (dynamics.py:101-133): token embed, mask-token
+ * select, latent-action conditioning (prepend: action token at s=0; additive),
+ * spatial + temporal positions.  tokens int64 [B,T,N]; mask u8 [B,T,N] or NULL;
+ * latents f32 [B,T-1,dl]; x f32 [B,T,S,D] with S = N + prepend.
+ * *err is set to 1 when a token id is out of range (the Python layer validates
+ * host inputs first and raises IndexError, autodiff.py:353-354).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, const float* latents,
+                            const float* token_embed, const float* mask_token, const float* null_action,
+                            const float* action_w, const float* action_b, const float* pos_spatial,
+                            const float* pos_temporal, int64_t B, int T, int N, int D, int dl, int K,
+                            int prepend, float* x, int* err, jz_stream_t stream);
+JZ_API int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend);
+/* Deterministic backward of jz_dyn_embed_fwd (no float atomics).  d_latents may be NULL. */
+JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_t* mask,
+                            const float* latents, const float* null_action, const float* action_w,
+                            int64_t B, int T, int N, int D, int dl, int K, int prepend,
+                            float* d_token_embed, float* d_mask_token, float* d_null_action,
+                            float* d_action_w, float* d_action_b, float* d_pos_spatial,
+                            float* d_pos_temporal, float* d_latents, float* workspace,
+                            jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K3  spatial (intra-frame) attention, tcgen05/TMEM + TMA (st.py:73,
+ * nn.py:80-110, causal=False).  qkv bf16 [frames*S, 3*H*64] (q|k|v, head h =
+ * cols 64h..), out bf16 [frames*S, H*64], lse f32 [frames, H, S] (natural-log
+ * softmax normaliser, saved for the backward).  S in {256, 257}, head_dim 64.
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
+                               float* lse, jz_stream_t stream);
+/* dqkv bf16 [frames*S, 3*H*64] (fully overwritten). */
+JZ_API int jz_attn_spatial_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                               int64_t frames, int S, int H, int head_dim, void* dqkv, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K4  causal temporal (inter-frame) attention (st.py:74-76, nn.py:103-105):
+ * for every (b, s) the T rows (b, t, s) attend causally over t.  qkv/out as
+ * above with rows ordered (b, t, s); lse f32 [B*S, H, T].  T <= 16, head_dim 64.
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, int H, int head_dim, void* out,
+                                float* lse, jz_stream_t stream);
+JZ_API int jz_attn_temporal_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                                int64_t B, int T, int S, int H, int head_dim, void* dqkv, jz_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif
