@@ -175,13 +175,16 @@ JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_
 /* ------------------------------------------------------------------------
  * K3  spatial (intra-frame) attention, tcgen05/TMEM + TMA (st.py:73,
  * nn.py:80-110, causal=False).  qkv bf16 [frames*S, 3*H*64] (q|k|v, head h =
- * cols 64h..), out bf16 [frames*S, H*64], lse f32 [frames, H, S] (natural-log
- * softmax normaliser, saved for the backward).  S in {256, 257}, head_dim 64.
+ * cols 64h..), out bf16 [frames*S, H*64], out_f32 (optional, may be NULL) the
+ * same in fp32, lse f32 [frames, H, S] (natural-log softmax normaliser).
+ * S in {256, 257}, head_dim 64.
  * ---------------------------------------------------------------------- */
 JZ_API int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
-                               float* lse, jz_stream_t stream);
-/* dqkv bf16 [frames*S, 3*H*64] (fully overwritten). */
-JZ_API int jz_attn_spatial_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                               float* out_f32, float* lse, jz_stream_t stream);
+/* dqkv bf16 [frames*S, 3*H*64] (fully overwritten).  out_f32 is the forward's fp32
+ * output: D_i = dO_i . O_i is formed from it so dP - D does not cancel against the
+ * bf16 rounding of O. */
+JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
                                int64_t frames, int S, int H, int head_dim, void* dqkv, jz_stream_t stream);
 
 /* ------------------------------------------------------------------------

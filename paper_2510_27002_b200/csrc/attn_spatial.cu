@@ -57,7 +57,8 @@ using namespace sp;
 
 __global__ void __launch_bounds__(kThreads, 1)
     spatial_fwd_kernel(const __grid_constant__ CUtensorMap tm, const __nv_bfloat16* __restrict__ qkv,
-                       __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int frames, int S, int H) {
+                       __nv_bfloat16* __restrict__ out, float* __restrict__ out_f32, float* __restrict__ lse,
+                       int frames, int S, int H) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   FwdSmallSmem& sm = *reinterpret_cast<FwdSmallSmem*>(smem + F_END);
@@ -191,8 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; j += 2) {
             const float p0 = ex2(__uint_as_float(v[j]) * c2 - mb);
             const float p1 = ex2(__uint_as_float(v[j + 1]) * c2 - mb);
-            sum += p0 + p1;
             pk[j / 2] = pack_bf16(p0, p1);
+            const float2 pr = unpack_bf16(pk[j / 2]);  // normalise with the probabilities the MMA sees
+            sum += pr.x + pr.y;
           }
           // keys 32c..32c+31 -> atom (c/2), 16B chunks (c%2)*4 .. +3
           uint8_t* atom = pbuf + (c >> 1) * TILE;
@@ -231,6 +233,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int q = 0; q < 4; ++q)
             dst[4 * c + q] = make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
                                         pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
+          if (out_f32) {
+            float4* d32 = reinterpret_cast<float4*>(out_f32 + grow * D + h * 64 + 32 * c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) d32[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          }
         }
         lse[((int64_t)f * H + h) * S + 128 * t + r] = mrow[t] * 0.125f + logf(lsum[t]);
         tc_fence_before();
@@ -326,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         o0 = (o0 + sm.tail_o[2 * dpair]) / sum;
         o1 = (o1 + sm.tail_o[2 * dpair + 1]) / sum;
         *reinterpret_cast<uint32_t*>(out + (row0 + 256) * D + h * 64 + 2 * dpair) = pack_bf16(o0, o1);
+        if (out_f32) *reinterpret_cast<float2*>(out_f32 + (row0 + 256) * D + h * 64 + 2 * dpair) = make_float2(o0, o1);
         if (tid == 0) lse[((int64_t)f * H + h) * S + 256] = mx * 0.125f + logf(sum);
       }
       named_bar(2, 64);
@@ -343,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 using namespace jz;
 
 extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
-                                   float* lse, jz_stream_t s) {
+                                   float* out_f32, float* lse, jz_stream_t s) {
   JZ_CHECK_ARG(head_dim == 64, "spatial attention: head_dim %d unsupported (64)", head_dim);
   JZ_CHECK_ARG(S == 256 || S == 257, "spatial attention: sequence length %d unsupported (256 or 257)", S);
   JZ_CHECK_ARG(frames >= 1 && frames * H < (1ll << 31), "spatial attention: frames");
@@ -359,8 +367,8 @@ extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H
   const int64_t units = frames * H;
   const int grid = (int)(units < num_sms() ? units : num_sms());
   spatial_fwd_kernel<<<grid, kThreads, F_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
-      tm, reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), lse, (int)frames,
-      S, H);
+      tm, reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out), out_f32, lse,
+      (int)frames, S, H);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
@@ -401,7 +409,7 @@ constexpr int B_SMEM = B_END + 1024 + (int)sizeof(BwdSmallSmem) + 64;
 
 __global__ void __launch_bounds__(kThreads, 1)
     spatial_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ out,
+                       const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ out,
                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
                        __nv_bfloat16* __restrict__ dqkv, int frames, int S, int H) {
   extern __shared__ uint8_t smem_raw[];
@@ -531,18 +539,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < 2; ++t) {
           const int q = 128 * t + r;
           const int64_t rr = row0 + q;
-          const uint4* op = reinterpret_cast<const uint4*>(out + rr * D + h * 64);
+          const float2* op = reinterpret_cast<const float2*>(out + rr * D + h * 64);
           const uint4* gp = reinterpret_cast<const uint4*>(dout + rr * D + h * 64);
           const uint4* qp = reinterpret_cast<const uint4*>(qkv + rr * ld3 + h * 64);
           float dd = 0.f, sk = 0.f, dpv = 0.f;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const uint4 wo = op[c], wg = gp[c], wq = qp[c];
-            const uint32_t ao[4] = {wo.x, wo.y, wo.z, wo.w}, ag[4] = {wg.x, wg.y, wg.z, wg.w},
-                           aqv[4] = {wq.x, wq.y, wq.z, wq.w};
+            const uint4 wg = gp[c], wq = qp[c];
+            const uint32_t ag[4] = {wg.x, wg.y, wg.z, wg.w}, aqv[4] = {wq.x, wq.y, wq.z, wq.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 fo = unpack_bf16(ao[e]), fg = unpack_bf16(ag[e]), fq = unpack_bf16(aqv[e]);
+              const float2 fo = op[4 * c + e], fg = unpack_bf16(ag[e]), fq = unpack_bf16(aqv[e]);
               const int d = 8 * c + 2 * e;
               dd += fo.x * fg.x + fo.y * fg.y;
               sk += fq.x * sm.k256[d] + fq.y * sm.k256[d + 1];
@@ -560,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t rr = row0 + 256;
         float dd = 0.f, sk = 0.f, dpv = 0.f;
         for (int d = 0; d < 64; ++d) {
-          dd += __bfloat162float(out[rr * D + h * 64 + d]) * sm.do256[d];
+          dd += out[rr * D + h * 64 + d] * sm.do256[d];
           sk += sm.q256[d] * sm.k256[d];
           dpv += sm.do256[d] * sm.v256[d];
         }
@@ -748,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace jz
 
-extern "C" int jz_attn_spatial_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
                                    int64_t frames, int S, int H, int head_dim, void* dqkv, jz_stream_t s) {
   using namespace jz;
   JZ_CHECK_ARG(head_dim == 64, "spatial attention bwd: head_dim %d unsupported (64)", head_dim);
@@ -767,7 +774,7 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const void* out, const void*
   const int64_t units = frames * H;
   const int grid = (int)(units < num_sms() ? units : num_sms());
   spatial_bwd_kernel<<<grid, sp::kThreads, sp::B_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
-      tq, td, reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(out),
+      tq, td, reinterpret_cast<const __nv_bfloat16*>(qkv), out_f32,
       reinterpret_cast<const __nv_bfloat16*>(dout), lse, reinterpret_cast<__nv_bfloat16*>(dqkv), (int)frames, S, H);
   JZ_LAUNCH_CHECK();
   return JZ_OK;

@@ -1,250 +1,304 @@
 // K4: causal temporal (inter-frame) attention, forward and backward.
 //
 // Replaces the temporal sub-layer's attention of st_block (st.py:74-76) =
-// multi_head_attention(causal=True) (nn.py:80-110) over the (B, S, T, D) transpose.
-// Here nothing is transposed: qkv stays in the (b, t, s) row order the GEMMs
-// produce, and one CTA gathers the T rows of one spatial slot (b, s) for all
-// heads.  With T = 16 and hd = 64 the arithmetic intensity is ~4 FLOP/B, so the
-// kernel is HBM-bound and runs on CUDA cores with 16-byte vectorised I/O
-// (SURVEY §2.3 K4); its roofline is HBM bandwidth.
+// multi_head_attention(causal=True) (nn.py:80-110, additive -1e9 mask) over the
+// (B, S, T, D) transpose.  Nothing is transposed here: qkv stays in the (b, t, s)
+// row order the GEMMs produce, and one CTA gathers the T <= 16 rows of one spatial
+// slot (b, s) with cp.async into padded shared memory; warp h owns head h.
 //
-// qkv bf16 [M, 3*D] (cols [q | k | v], head h = cols 64h..64h+63 of each),
-// out bf16 [M, D], lse f32 [(b*S + s) * H * T + h * T + t].
+// Each (b, s, head) problem is a 16x16 causal attention with hd = 64: ~4 FLOP/B,
+// HBM-bound and too small for tcgen05's M >= 64 tiles.  The
+// per-warp math uses m16n8k16 register MMAs (S = QK^T, O = PV; backward dP, dV,
+// dK, dQ) so the instruction count stays far below the memory time; the roofline
+// that bounds this kernel is HBM bandwidth.
+//
+// qkv bf16 [M, 3D] (cols [q | k | v], head h = cols 64h..64h+63 of each),
+// out bf16 [M, D], lse f32 [((b*S + s) * H + h) * T + t] (natural log).
 #include "common.h"
 #include "ptx.cuh"
 
 namespace jz {
+namespace tp {
 
 constexpr int HD = 64;
+constexpr int LDP = 24;  // padded row pitch (elements) of the per-warp 16x16 P / dS tiles
 
 JZ_DEV void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 JZ_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// 64-element dot / axpy against a bf16 smem row with 16-byte loads
-JZ_DEV float dot8x8(const float (&x)[64], const __nv_bfloat16* row) {
-  float a = 0.f;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 w = reinterpret_cast<const uint4*>(row)[c];
-    const float2 f0 = unpack_bf16(w.x), f1 = unpack_bf16(w.y), f2 = unpack_bf16(w.z), f3 = unpack_bf16(w.w);
-    a += x[8 * c] * f0.x + x[8 * c + 1] * f0.y + x[8 * c + 2] * f1.x + x[8 * c + 3] * f1.y +
-         x[8 * c + 4] * f2.x + x[8 * c + 5] * f2.y + x[8 * c + 6] * f3.x + x[8 * c + 7] * f3.y;
-  }
-  return a;
+JZ_DEV void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+JZ_DEV void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+JZ_DEV void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-JZ_DEV void axpy8x8(float (&y)[64], float a, const __nv_bfloat16* row) {
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 w = reinterpret_cast<const uint4*>(row)[c];
-    const float2 f0 = unpack_bf16(w.x), f1 = unpack_bf16(w.y), f2 = unpack_bf16(w.z), f3 = unpack_bf16(w.w);
-    y[8 * c] += a * f0.x; y[8 * c + 1] += a * f0.y; y[8 * c + 2] += a * f1.x; y[8 * c + 3] += a * f1.y;
-    y[8 * c + 4] += a * f2.x; y[8 * c + 5] += a * f2.y; y[8 * c + 6] += a * f3.x; y[8 * c + 7] += a * f3.y;
+// A fragment (16 rows x 16 k) from row-major storage (row pitch ld) at column k0
+JZ_DEV void load_a(uint32_t (&a)[4], const __nv_bfloat16* base, int ld, int k0) {
+  const int L = lane_id();
+  ldsm_x4(a, base + ((L & 7) + 8 * ((L >> 3) & 1)) * ld + k0 + 8 * (L >> 4));
+}
+// A = X^T with X stored [k rows][m cols]: A(m, k) = X[k][m]  (16 x 16)
+JZ_DEV void load_a_trans(uint32_t (&a)[4], const __nv_bfloat16* base, int ld) {
+  const int L = lane_id();
+  ldsm_x4_t(a, base + ((L & 7) + 8 * (L >> 4)) * ld + 8 * ((L >> 3) & 1));
+}
+// B for n-tiles n0..n0+15 x k16, storage [n rows][k cols]
+JZ_DEV void load_b_nk(uint32_t (&b)[4], const __nv_bfloat16* base, int ld, int n0, int k0) {
+  const int L = lane_id();
+  ldsm_x4(b, base + (n0 + (L & 7) + 8 * (L >> 4)) * ld + k0 + 8 * ((L >> 3) & 1));
+}
+// B for n-tiles n0..n0+15 x k16, storage [k rows][n cols]
+JZ_DEV void load_b_kn(uint32_t (&b)[4], const __nv_bfloat16* base, int ld, int n0) {
+  const int L = lane_id();
+  ldsm_x4_t(b, base + ((L & 7) + 8 * ((L >> 3) & 1)) * ld + n0 + 8 * (L >> 4));
+}
+
+// stage rows t = 0..15 of `src` (row (b*T + t)*S + s) into smem [16][ld]; rows >= T are zeroed
+JZ_DEV void stage_rows(__nv_bfloat16* dst, int ld, const __nv_bfloat16* src, int64_t src_ld, int cols, int64_t b,
+                       int T, int S, int64_t s) {
+  const int c16 = cols / 8;
+  for (int i = threadIdx.x; i < 16 * c16; i += blockDim.x) {
+    const int t = i / c16, c = i - t * c16;
+    if (t < T)
+      cp_async16(dst + t * ld + 8 * c, src + ((b * T + t) * S + s) * src_ld + 8 * c);
+    else
+      *reinterpret_cast<uint4*>(dst + t * ld + 8 * c) = make_uint4(0, 0, 0, 0);
   }
 }
 
-template <int T>
-__global__ void __launch_bounds__(256)
-    temporal_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, int S, int H, __nv_bfloat16* __restrict__ out,
-                        float* __restrict__ lse, float scale) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int D = H * HD;
-  const int64_t bs = blockIdx.x;  // b*S + s
-  const int64_t b = bs / S, s = bs - b * S;
-  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [T][3D]
-  const int row_u4 = 3 * D / 8;
-  for (int i = threadIdx.x; i < T * row_u4; i += blockDim.x) {
-    const int t = i / row_u4, c = i - t * row_u4;
-    const int64_t row = (b * T + t) * S + s;
-    cp_async16(reinterpret_cast<uint4*>(sq + (int64_t)t * 3 * D) + c, reinterpret_cast<const uint4*>(qkv + row * 3 * D) + c);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int h = threadIdx.x / T, t = threadIdx.x % T;
-  if (h >= H) return;
-  const __nv_bfloat16* q = sq + (int64_t)t * 3 * D + h * HD;
-  float qf[HD];
+JZ_DEV float quad_max(float v) {
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+  return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+JZ_DEV float quad_sum(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+
+// acc[n-tile][4] = X Y^T over hd (X rows pitch ldx, Y rows pitch ldy); C layout: rows L/4, L/4+8
+JZ_DEV void xyT(float (&acc)[2][4], const __nv_bfloat16* x, int ldx, const __nv_bfloat16* y, int ldy) {
 #pragma unroll
-  for (int d = 0; d < HD; d += 2) {
-    float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(q + d));
-    qf[d] = f.x; qf[d + 1] = f.y;
-  }
-  float sc[T];
-  float mx = -INFINITY;
+  for (int n = 0; n < 2; ++n)
 #pragma unroll
-  for (int j = 0; j < T; ++j) {
-    if (j <= t) {
-      const __nv_bfloat16* k = sq + (int64_t)j * 3 * D + D + h * HD;
-      float a = dot8x8(qf, k);
-      sc[j] = a * scale;
-      mx = fmaxf(mx, sc[j]);
-    } else {
-      sc[j] = -INFINITY;
+    for (int e = 0; e < 4; ++e) acc[n][e] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < HD; kk += 16) {
+    uint32_t a[4], b[4];
+    load_a(a, x, ldx, kk);
+    load_b_nk(b, y, ldy, 0, kk);
+    mma16816(acc[0], a, b[0], b[1]);
+    mma16816(acc[1], a, b[2], b[3]);
+  }
+}
+
+// C-layout 16x16 (two n-tiles) -> A fragment
+JZ_DEV void c_to_a(uint32_t (&a)[4], const float (&c)[2][4]) {
+  a[0] = pack_bf16(c[0][0], c[0][1]);
+  a[1] = pack_bf16(c[0][2], c[0][3]);
+  a[2] = pack_bf16(c[1][0], c[1][1]);
+  a[3] = pack_bf16(c[1][2], c[1][3]);
+}
+
+// C-layout 16x16 -> smem tile [16][LDP] (bf16)
+JZ_DEV void c_to_smem(__nv_bfloat16* dst, const float (&c)[2][4]) {
+  const int L = lane_id();
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+    *reinterpret_cast<uint32_t*>(dst + r0 * LDP + 8 * n + cq) = pack_bf16(c[n][0], c[n][1]);
+    *reinterpret_cast<uint32_t*>(dst + (r0 + 8) * LDP + 8 * n + cq) = pack_bf16(c[n][2], c[n][3]);
+  }
+}
+
+// out[16 rows][64] = A(16x16) . B where B rows (k) are stored [k][n] pitch ld; writes rows < T of
+// global `dst` (row index (b*T + r)*S + s, pitch dld, column offset col0) scaled by mul (per row)
+JZ_DEV void av_store(const uint32_t (&a)[4], const __nv_bfloat16* bsm, int ld, __nv_bfloat16* dst, int64_t dld,
+                     int col0, int64_t b, int T, int S, int64_t s, float mul0, float mul1) {
+  const int L = lane_id();
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+#pragma unroll
+  for (int np = 0; np < HD / 16; ++np) {
+    uint32_t bb[4];
+    load_b_kn(bb, bsm, ld, 16 * np);
+    float o0[4] = {0, 0, 0, 0}, o1[4] = {0, 0, 0, 0};
+    mma16816(o0, a, bb[0], bb[1]);
+    mma16816(o1, a, bb[2], bb[3]);
+    const int dcol = col0 + 16 * np + cq;
+    if (r0 < T) {
+      __nv_bfloat16* row = dst + ((b * T + r0) * S + s) * dld + dcol;
+      *reinterpret_cast<uint32_t*>(row) = pack_bf16(o0[0] * mul0, o0[1] * mul0);
+      *reinterpret_cast<uint32_t*>(row + 8) = pack_bf16(o1[0] * mul0, o1[1] * mul0);
+    }
+    if (r0 + 8 < T) {
+      __nv_bfloat16* row = dst + ((b * T + r0 + 8) * S + s) * dld + dcol;
+      *reinterpret_cast<uint32_t*>(row) = pack_bf16(o0[2] * mul1, o0[3] * mul1);
+      *reinterpret_cast<uint32_t*>(row + 8) = pack_bf16(o1[2] * mul1, o1[3] * mul1);
     }
   }
-  float sum = 0.f;
-#pragma unroll
-  for (int j = 0; j < T; ++j) {
-    sc[j] = j <= t ? __expf(sc[j] - mx) : 0.f;
-    sum += sc[j];
-  }
-  const float inv = 1.0f / sum;
-  float o[HD];
-#pragma unroll
-  for (int d = 0; d < HD; ++d) o[d] = 0.f;
-#pragma unroll
-  for (int j = 0; j < T; ++j) {
-    if (j <= t) {
-      const __nv_bfloat16* v = sq + (int64_t)j * 3 * D + 2 * D + h * HD;
-      axpy8x8(o, sc[j] * inv, v);
-    }
-  }
-  const int64_t row = (b * T + t) * S + s;
-  uint4* dst = reinterpret_cast<uint4*>(out + row * D + h * HD);
-#pragma unroll
-  for (int d = 0; d < HD; d += 8)
-    dst[d / 8] = make_uint4(pack_bf16(o[d], o[d + 1]), pack_bf16(o[d + 2], o[d + 3]),
-                            pack_bf16(o[d + 4], o[d + 5]), pack_bf16(o[d + 6], o[d + 7]));
-  lse[(bs * H + h) * T + t] = mx + logf(sum);
 }
 
-// Backward.  smem: qkv rows [T][3D], o rows [T][D], do rows [T][D], P and dS [H][T][T].
-template <int T>
-__global__ void __launch_bounds__(256)
-    temporal_bwd_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ o,
-                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse, int S, int H,
-                        __nv_bfloat16* __restrict__ dqkv, float scale) {
+}  // namespace tp
+
+using namespace tp;
+
+__global__ void __launch_bounds__(512) temporal_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int S, int H,
+                                                           __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                                                           float scale) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int D = H * HD;
+  const int ld = 3 * D + 8;
   const int64_t bs = blockIdx.x;
   const int64_t b = bs / S, s = bs - b * S;
-  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [T][3D]
-  __nv_bfloat16* so = sq + (int64_t)T * 3 * D;                     // [T][D]
-  __nv_bfloat16* sdo = so + (int64_t)T * D;                        // [T][D]
-  float* sp = reinterpret_cast<float*>(sdo + (int64_t)T * D);      // [H][T][T]
-  float* sds = sp + H * T * T;                                     // [H][T][T]
-  {
-    const int row_u4 = 3 * D / 8, row2 = D / 8;
-    for (int i = threadIdx.x; i < T * row_u4; i += blockDim.x) {
-      const int t = i / row_u4, c = i - t * row_u4;
-      const int64_t row = (b * T + t) * S + s;
-      cp_async16(reinterpret_cast<uint4*>(sq + (int64_t)t * 3 * D) + c, reinterpret_cast<const uint4*>(qkv + row * 3 * D) + c);
-    }
-    for (int i = threadIdx.x; i < T * row2; i += blockDim.x) {
-      const int t = i / row2, c = i - t * row2;
-      const int64_t row = (b * T + t) * S + s;
-      cp_async16(reinterpret_cast<uint4*>(so + (int64_t)t * D) + c, reinterpret_cast<const uint4*>(o + row * D) + c);
-      cp_async16(reinterpret_cast<uint4*>(sdo + (int64_t)t * D) + c, reinterpret_cast<const uint4*>(dout + row * D) + c);
-    }
-    cp_async_wait_all();
-  }
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  stage_rows(sq, ld, qkv, 3 * D, 3 * D, b, T, S, s);
+  cp_async_wait_all();
   __syncthreads();
-  const int h = threadIdx.x / T, t = threadIdx.x % T;
-  const bool active = h < H;
-  if (active) {
-    // query role: row t of head h
-    float qf[HD], dof[HD];
-    float Dt = 0.f;
+  const int h = warp_id(), L = lane_id();
+  if (h >= H) return;
+  float sc[2][4];
+  xyT(sc, sq + h * HD, ld, sq + D + h * HD, ld);
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+  float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-    for (int d = 0; d < HD; d += 2) {
-      float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sq + (int64_t)t * 3 * D + h * HD + d));
-      float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sdo + (int64_t)t * D + h * HD + d));
-      float2 w = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(so + (int64_t)t * D + h * HD + d));
-      qf[d] = a.x; qf[d + 1] = a.y;
-      dof[d] = g.x; dof[d + 1] = g.y;
-      Dt += g.x * w.x + g.y * w.y;
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int row = r0 + 8 * (e >> 1), col = 8 * n + cq + (e & 1);
+      const float x = col <= row ? sc[n][e] * scale : -INFINITY;
+      sc[n][e] = x;
+      if (e < 2) m0 = fmaxf(m0, x); else m1 = fmaxf(m1, x);
     }
-    const float L = lse[(bs * H + h) * T + t];
-#pragma unroll 1
-    for (int j = 0; j < T; ++j) {
-      float p = 0.f, ds = 0.f;
-      if (j <= t) {
-        const __nv_bfloat16* k = sq + (int64_t)j * 3 * D + D + h * HD;
-        const __nv_bfloat16* v = sq + (int64_t)j * 3 * D + 2 * D + h * HD;
-        const float a = dot8x8(qf, k);
-        const float dp = dot8x8(dof, v);
-        p = __expf(a * scale - L);
-        ds = p * (dp - Dt);
-      }
-      sp[(h * T + t) * T + j] = p;
-      sds[(h * T + t) * T + j] = ds;
+  m0 = quad_max(m0);
+  m1 = quad_max(m1);
+  float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float p = __expf(sc[n][e] - (e < 2 ? m0 : m1));
+      sc[n][e] = p;
+      if (e < 2) l0 += p; else l1 += p;
     }
-    float dq[HD];
-#pragma unroll
-    for (int d = 0; d < HD; ++d) dq[d] = 0.f;
-#pragma unroll 1
-    for (int j = 0; j <= t; ++j) axpy8x8(dq, sds[(h * T + t) * T + j], sq + (int64_t)j * 3 * D + D + h * HD);
-    const int64_t row = (b * T + t) * S + s;
-    uint4* dst = reinterpret_cast<uint4*>(dqkv + row * 3 * D + h * HD);
-#pragma unroll
-    for (int d = 0; d < HD; d += 8)
-      dst[d / 8] = make_uint4(pack_bf16(scale * dq[d], scale * dq[d + 1]), pack_bf16(scale * dq[d + 2], scale * dq[d + 3]),
-                              pack_bf16(scale * dq[d + 4], scale * dq[d + 5]), pack_bf16(scale * dq[d + 6], scale * dq[d + 7]));
-  }
-  __syncthreads();
-  if (active) {
-    // key role: key j = t of head h
-    const int j = t;
-    float dk[HD], dv[HD];
-#pragma unroll
-    for (int d = 0; d < HD; ++d) { dk[d] = 0.f; dv[d] = 0.f; }
-    for (int tq = j; tq < T; ++tq) {
-      const float p = sp[(h * T + tq) * T + j], ds = sds[(h * T + tq) * T + j];
-      axpy8x8(dk, ds, sq + (int64_t)tq * 3 * D + h * HD);
-      axpy8x8(dv, p, sdo + (int64_t)tq * D + h * HD);
-    }
-    const int64_t row = (b * T + j) * S + s;
-    uint4* dk_dst = reinterpret_cast<uint4*>(dqkv + row * 3 * D + D + h * HD);
-    uint4* dv_dst = reinterpret_cast<uint4*>(dqkv + row * 3 * D + 2 * D + h * HD);
-#pragma unroll
-    for (int d = 0; d < HD; d += 8) {
-      dk_dst[d / 8] = make_uint4(pack_bf16(scale * dk[d], scale * dk[d + 1]), pack_bf16(scale * dk[d + 2], scale * dk[d + 3]),
-                                 pack_bf16(scale * dk[d + 4], scale * dk[d + 5]), pack_bf16(scale * dk[d + 6], scale * dk[d + 7]));
-      dv_dst[d / 8] = make_uint4(pack_bf16(dv[d], dv[d + 1]), pack_bf16(dv[d + 2], dv[d + 3]),
-                                 pack_bf16(dv[d + 4], dv[d + 5]), pack_bf16(dv[d + 6], dv[d + 7]));
-    }
+  l0 = quad_sum(l0);
+  l1 = quad_sum(l1);
+  uint32_t pa[4];
+  c_to_a(pa, sc);
+  av_store(pa, sq + 2 * D + h * HD, ld, out, D, h * HD, b, T, S, s, 1.0f / l0, 1.0f / l1);
+  if ((L & 3) == 0) {
+    float* lp = lse + (bs * H + h) * T;
+    if (r0 < T) lp[r0] = m0 + logf(l0);
+    if (r0 + 8 < T) lp[r0 + 8] = m1 + logf(l1);
   }
 }
 
-template <int T>
-static int launch_temporal(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t BS,
-                           int S, int H, void* out, float scale, cudaStream_t st) {
+__global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                           const __nv_bfloat16* __restrict__ o,
+                                                           const __nv_bfloat16* __restrict__ dout,
+                                                           const float* __restrict__ lse, int T, int S, int H,
+                                                           __nv_bfloat16* __restrict__ dqkv, float scale) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
   const int D = H * HD;
-  const int threads = ((T * H + 31) / 32) * 32 < 128 ? 128 : ((T * H + 31) / 32) * 32;
-  if (!bwd) {
-    const size_t smem = (size_t)T * 3 * D * 2;
-    if (smem > 48 * 1024)
-      JZ_CUDA_TRY(cudaFuncSetAttribute(temporal_fwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    temporal_fwd_kernel<T><<<(unsigned)BS, threads, smem, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qkv), S, H, reinterpret_cast<__nv_bfloat16*>(out), lse, scale);
-  } else {
-    const size_t smem = (size_t)T * 5 * D * 2 + (size_t)2 * H * T * T * 4;
-    if (smem > 48 * 1024)
-      JZ_CUDA_TRY(cudaFuncSetAttribute(temporal_bwd_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    temporal_bwd_kernel<T><<<(unsigned)BS, threads, smem, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(o),
-        reinterpret_cast<const __nv_bfloat16*>(dout), lse, S, H, reinterpret_cast<__nv_bfloat16*>(out), scale);
+  const int ldq = 3 * D + 8, ldo = D + 8;
+  const int64_t bs = blockIdx.x;
+  const int64_t b = bs / S, s = bs - b * S;
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* so = sq + 16 * ldq;
+  __nv_bfloat16* sdo = so + 16 * ldo;
+  __nv_bfloat16* sp_all = sdo + 16 * ldo;
+  stage_rows(sq, ldq, qkv, 3 * D, 3 * D, b, T, S, s);
+  stage_rows(so, ldo, o, D, D, b, T, S, s);
+  stage_rows(sdo, ldo, dout, D, D, b, T, S, s);
+  cp_async_wait_all();
+  __syncthreads();
+  const int h = warp_id(), L = lane_id();
+  if (h >= H) return;
+  __nv_bfloat16* sP = sp_all + h * 2 * 16 * LDP;
+  __nv_bfloat16* sdS = sP + 16 * LDP;
+  const __nv_bfloat16* q = sq + h * HD;
+  const __nv_bfloat16* k = sq + D + h * HD;
+  const __nv_bfloat16* v = sq + 2 * D + h * HD;
+  const __nv_bfloat16* og = so + h * HD;
+  const __nv_bfloat16* dog = sdo + h * HD;
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+  // D_t = sum_d dO[t][d] O[t][d]: lane -> row L%16, half L/16
+  float Dp = 0.f;
+  {
+    const int t = L & 15, d0 = 32 * (L >> 4);
+#pragma unroll
+    for (int d = 0; d < 32; d += 2) {
+      const float2 a = unpack_bf16(*reinterpret_cast<const uint32_t*>(og + t * ldo + d0 + d));
+      const float2 g = unpack_bf16(*reinterpret_cast<const uint32_t*>(dog + t * ldo + d0 + d));
+      Dp += a.x * g.x + a.y * g.y;
+    }
+    Dp += __shfl_xor_sync(0xffffffffu, Dp, 16);
   }
-  JZ_LAUNCH_CHECK();
-  return JZ_OK;
+  const float D0 = __shfl_sync(0xffffffffu, Dp, r0), D1 = __shfl_sync(0xffffffffu, Dp, r0 + 8);
+  const float* lp = lse + (bs * H + h) * T;
+  const float L0 = r0 < T ? lp[r0] : 0.f, L1 = r0 + 8 < T ? lp[r0 + 8] : 0.f;
+  float P[2][4], dS[2][4];
+  xyT(P, q, ldq, k, ldq);
+  xyT(dS, dog, ldo, v, ldq);
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int row = r0 + 8 * (e >> 1), col = 8 * n + cq + (e & 1);
+      const float p = (col <= row && row < T) ? __expf(P[n][e] * scale - (e < 2 ? L0 : L1)) : 0.f;
+      P[n][e] = p;
+      dS[n][e] = p * (dS[n][e] - (e < 2 ? D0 : D1));
+    }
+  c_to_smem(sP, P);
+  c_to_smem(sdS, dS);
+  __syncwarp();
+  // dQ = scale * dS K      (A = dS from registers, B = K stored [j][d])
+  uint32_t a[4];
+  c_to_a(a, dS);
+  av_store(a, k, ldq, dqkv, 3 * D, h * HD, b, T, S, s, scale, scale);
+  // dK = scale * dS^T Q    (A = dS^T from smem, B = Q stored [t][d])
+  load_a_trans(a, sdS, LDP);
+  av_store(a, q, ldq, dqkv, 3 * D, D + h * HD, b, T, S, s, scale, scale);
+  // dV = P^T dO
+  load_a_trans(a, sP, LDP);
+  av_store(a, dog, ldo, dqkv, 3 * D, 2 * D + h * HD, b, T, S, s, 1.0f, 1.0f);
 }
 
 static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B,
                              int T, int S, int H, void* out, cudaStream_t st) {
-  JZ_CHECK_ARG(H >= 1 && H * T <= 256, "temporal attention: heads*T=%d too large (<= 256)", H * T);
+  JZ_CHECK_ARG(H >= 1 && H <= 16, "temporal attention: heads %d unsupported (<= 16)", H);
+  JZ_CHECK_ARG(T >= 1 && T <= 16, "temporal attention: T=%d unsupported (<= 16)", T);
   const float scale = 0.125f;  // 1/sqrt(64)
   const int64_t BS = B * S;
   if (BS == 0) return JZ_OK;
-  switch (T) {
-#define TC(n) case n: return launch_temporal<n>(bwd, qkv, o, dout, lse, BS, S, H, out, scale, st);
-    TC(1) TC(2) TC(3) TC(4) TC(5) TC(6) TC(7) TC(8) TC(9) TC(10) TC(11) TC(12) TC(13) TC(14) TC(15) TC(16)
-#undef TC
-    default:
-      set_error("temporal attention: T=%d unsupported (<= 16)", T);
-      return JZ_EINVAL;
+  const int D = H * HD;
+  const int threads = 32 * H;
+  if (!bwd) {
+    const size_t smem = (size_t)16 * (3 * D + 8) * 2;
+    JZ_CUDA_TRY(cudaFuncSetAttribute(temporal_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    temporal_fwd_kernel<<<(unsigned)BS, threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), T, S, H,
+                                                             reinterpret_cast<__nv_bfloat16*>(out), lse, scale);
+  } else {
+    const size_t smem = (size_t)16 * (3 * D + 8) * 2 + (size_t)2 * 16 * (D + 8) * 2 + (size_t)H * 2 * 16 * LDP * 2;
+    JZ_CUDA_TRY(cudaFuncSetAttribute(temporal_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    temporal_bwd_kernel<<<(unsigned)BS, threads, smem, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(o),
+        reinterpret_cast<const __nv_bfloat16*>(dout), lse, T, S, H, reinterpret_cast<__nv_bfloat16*>(out), scale);
   }
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
 }
 
 }  // namespace jz

@@ -115,12 +115,24 @@ __global__ void dyn_embed_bwd_pos_kernel(const float* __restrict__ dx, const uin
     float4 acc_s = make_float4(0, 0, 0, 0), acc_m = make_float4(0, 0, 0, 0);
     for (int t = 0; t < T; ++t) {
       float4 acc_t = make_float4(0, 0, 0, 0);
-      for (int64_t b = 0; b < B; ++b) {
-        const int64_t row = (b * T + t) * S + s;
-        float4 g = *reinterpret_cast<const float4*>(dx + row * D + d);
-        acc_t.x += g.x; acc_t.y += g.y; acc_t.z += g.z; acc_t.w += g.w;
-        if (n >= 0 && mask && mask[(b * T + t) * N + n]) {
-          acc_m.x += g.x; acc_m.y += g.y; acc_m.z += g.z; acc_m.w += g.w;
+      for (int64_t b0 = 0; b0 < B; b0 += 4) {
+        float4 g[4];
+        bool mk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t b = b0 + q;
+          g[q] = make_float4(0, 0, 0, 0);
+          mk[q] = false;
+          if (b < B) {
+            const int64_t row = (b * T + t) * S + s;
+            g[q] = *reinterpret_cast<const float4*>(dx + row * D + d);
+            mk[q] = n >= 0 && mask && mask[(b * T + t) * N + n];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc_t.x += g[q].x; acc_t.y += g[q].y; acc_t.z += g[q].z; acc_t.w += g[q].w;
+          if (mk[q]) { acc_m.x += g[q].x; acc_m.y += g[q].y; acc_m.z += g[q].z; acc_m.w += g[q].w; }
         }
       }
       *reinterpret_cast<float4*>(part_pt + ((int64_t)s * T + t) * D + d) = acc_t;
@@ -213,24 +225,28 @@ __global__ void dyn_dact_additive_kernel(const float* __restrict__ dx, int64_t B
   }
 }
 
+// partial[chunk][i][d] (i < dl) and partial_b[chunk][d] over bt in [chunk*per, (chunk+1)*per)
 __global__ void dyn_action_w_kernel(const float* __restrict__ dact, int64_t dact_stride, int64_t B, int T,
                                     const float* __restrict__ latents, const float* __restrict__ null_action,
-                                    int dl, int D, float* __restrict__ dWa, float* __restrict__ dba) {
+                                    int dl, int D, int64_t per, float* __restrict__ part_w, float* __restrict__ part_b) {
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
   if (d >= D) return;
   float acc[64];
   for (int i = 0; i < dl; ++i) acc[i] = 0.f;
   float sb = 0.f;
-  for (int64_t b = 0; b < B; ++b)
-    for (int t = 0; t < T; ++t) {
-      const int64_t bt = b * T + t;
-      const float g = dact[bt * dact_stride + d];
-      const float* cond = t == 0 ? null_action : latents + (b * (T - 1) + (t - 1)) * dl;
-      for (int i = 0; i < dl; ++i) acc[i] += cond[i] * g;
-      sb += g;
-    }
-  for (int i = 0; i < dl; ++i) dWa[(int64_t)i * D + d] = acc[i];
-  dba[d] = sb;
+  const int64_t BT = B * T;
+  const int64_t bt0 = chunk * per, bt1 = min(BT, bt0 + per);
+  for (int64_t bt = bt0; bt < bt1; ++bt) {
+    const int64_t b = bt / T;
+    const int t = (int)(bt - b * T);
+    const float g = dact[bt * dact_stride + d];
+    const float* cond = t == 0 ? null_action : latents + (b * (T - 1) + (t - 1)) * dl;
+    for (int i = 0; i < dl; ++i) acc[i] += cond[i] * g;
+    sb += g;
+  }
+  for (int i = 0; i < dl; ++i) part_w[((int64_t)chunk * dl + i) * D + d] = acc[i];
+  part_b[(int64_t)chunk * D + d] = sb;
 }
 
 __global__ void dyn_action_cond_kernel(const float* __restrict__ dact, int64_t dact_stride, int64_t BT,
@@ -310,7 +326,7 @@ extern "C" int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, cons
 // Workspace floats needed by jz_dyn_embed_bwd.
 extern "C" int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend) {
   const int S = N + (prepend ? 1 : 0);
-  return (int64_t)S * T * D + (int64_t)S * D + (prepend ? 0 : B * T * D) + B * T * dl;
+  return (int64_t)S * T * D + (int64_t)S * D + (prepend ? 0 : B * T * D) + B * T * dl + 64ll * (dl + 1) * D;
 }
 
 extern "C" int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_t* mask,
@@ -358,9 +374,19 @@ extern "C" int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const ui
     dact = dact_buf;
     dact_stride = D;
   }
-  dyn_action_w_kernel<<<(D + 127) / 128, 128, 0, st>>>(dact, dact_stride, B, T, latents, null_action, dl, D,
-                                                        d_action_w, d_action_b);
-  JZ_LAUNCH_CHECK();
+  {
+    const int chunks = 64;
+    const int64_t per = (B * T + chunks - 1) / chunks;
+    float* part_w = dcond + B * T * dl;
+    float* part_b = part_w + (int64_t)chunks * dl * D;
+    dyn_action_w_kernel<<<dim3((D + 127) / 128, chunks), 128, 0, st>>>(dact, dact_stride, B, T, latents, null_action,
+                                                                        dl, D, per, part_w, part_b);
+    JZ_LAUNCH_CHECK();
+    rc = jz_reduce_partials(part_w, chunks, (int64_t)dl * D, d_action_w, 0, s);
+    if (rc) return rc;
+    rc = jz_reduce_partials(part_b, chunks, D, d_action_b, 0, s);
+    if (rc) return rc;
+  }
   dyn_action_cond_kernel<<<(unsigned)((B * T + 7) / 8), 256, 0, st>>>(dact, dact_stride, B * T, action_w, dl, D,
                                                                        dcond);
   JZ_LAUNCH_CHECK();

@@ -193,13 +193,31 @@ __global__ void __launch_bounds__(kRowThreads) colsum_bf16_kernel(const __nv_bfl
   }
 }
 
-__global__ void reduce_partials_kernel(const float* __restrict__ part, int nparts, int64_t D,
-                                       float* __restrict__ out, int accumulate) {
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < D;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * D + c];
-    out[c] = accumulate ? out[c] + s : s;
+// out[c] = sum_p part[p][c]: 8 fixed part-groups x 32 columns per CTA, groups combined in order.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ part, int nparts, int64_t D,
+                                                             float* __restrict__ out, int accumulate) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < D; c0 += (int64_t)gridDim.x * 32) {
+    const int64_t c = c0 + lane;
+    float s0 = 0.f, s1 = 0.f;
+    if (c < D) {
+      int p = grp;
+      for (; p + 8 < nparts; p += 16) {
+        s0 += part[(int64_t)p * D + c];
+        s1 += part[(int64_t)(p + 8) * D + c];
+      }
+      if (p < nparts) s0 += part[(int64_t)p * D + c];
+    }
+    sm[grp][lane] = s0 + s1;
+    __syncthreads();
+    if (grp == 0 && c < D) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += sm[k][lane];
+      out[c] = accumulate ? out[c] + t : t;
+    }
+    __syncthreads();
   }
 }
 
@@ -271,22 +289,21 @@ __global__ void __launch_bounds__(kRowThreads) ce_kernel(const float* __restrict
   }
 }
 
-// loss = sum(row_loss) / count  (single CTA, fixed order)
+// loss = sum(row_loss) / count  (single CTA, fixed order, f64 accumulation)
 __global__ void ce_finalize_kernel(const float* __restrict__ row_loss, int64_t rows,
                                    const int* __restrict__ count, float* __restrict__ loss) {
-  __shared__ float sm[1024];
-  float s = 0.f;
-  // each thread sums a contiguous chunk -> fixed order
+  __shared__ double sm[1024];
+  double s = 0.0;
   const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
   const int64_t a = threadIdx.x * per, b = min(rows, a + per);
-  for (int64_t i = a; i < b; ++i) s += row_loss[i];
+  for (int64_t i = a; i < b; ++i) s += (double)row_loss[i];
   sm[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float t = 0.f;
+    double t = 0.0;
     for (int i = 0; i < (int)blockDim.x; ++i) t += sm[i];
     const int c = *count;
-    *loss = c > 0 ? t / (float)c : 0.0f;
+    *loss = c > 0 ? (float)(t / (double)c) : 0.0f;
   }
 }
 
@@ -362,7 +379,7 @@ extern "C" int jz_layernorm_fwd(const float* x, int64_t rows, int D, const float
 
 extern "C" int jz_row_partials(int64_t rows) {
   // number of per-CTA partial rows used by the column reductions for `rows` input rows
-  int64_t p = (int64_t)num_sms() * 4;
+  int64_t p = (int64_t)num_sms() * 2;
   if (rows < p) p = rows > 0 ? rows : 1;
   return (int)p;
 }
@@ -422,7 +439,9 @@ extern "C" int jz_colsum_bf16(const void* x, int64_t rows, int cols, int64_t ld,
 extern "C" int jz_reduce_partials(const float* part, int nparts, int64_t D, float* out, int accumulate,
                                   jz_stream_t s) {
   if (D == 0) return JZ_OK;
-  reduce_partials_kernel<<<grid_for(D, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(part, nparts, D, out,
+  int64_t blocks = (D + 31) / 32;
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(part, nparts, D, out,
                                                                                           accumulate);
   JZ_LAUNCH_CHECK();
   return JZ_OK;

@@ -1,0 +1,275 @@
+"""Thin torch-facing wrappers over the libjz C ABI (include/jz.h).
+
+Every function here takes device torch tensors, validates shapes/dtypes on the
+host, and issues exactly one C-ABI call (or a fixed small sequence) on the
+current CUDA stream.  torch is used only for device memory and streams; all
+arithmetic happens in libjz's sm_100a kernels.  There is no fallback path.
+"""
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from . import _lib as L
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+
+def _s() -> int:
+    return L.stream_ptr()
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+# --------------------------------------------------------------------------
+# scratch buffers (stream-ordered reuse; one set per device)
+# --------------------------------------------------------------------------
+class _Scratch(threading.local):
+    def __init__(self):
+        self.bufs: dict = {}
+
+
+_scratch = _Scratch()
+
+
+def scratch(name: str, numel: int, dtype=F32, device=None) -> torch.Tensor:
+    """A reusable device buffer of at least `numel` elements (contents undefined)."""
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (name, dtype, dev)
+    buf = _scratch.bufs.get(key)
+    if buf is None or buf.numel() < numel:
+        buf = torch.empty(max(numel, 1), dtype=dtype, device=dev)
+        _scratch.bufs[key] = buf
+    return buf[:numel]
+
+
+def num_sms() -> int:
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+# --------------------------------------------------------------------------
+# K1 GEMM
+# --------------------------------------------------------------------------
+def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: bool, b_kmajor: bool,
+         out: torch.Tensor, epilogue: int, bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
+         out2: torch.Tensor | None = None, split_k: int = 1, lda: int | None = None, ldb: int | None = None,
+         ldd: int | None = None, ldaux: int | None = None, ldd2: int | None = None) -> torch.Tensor:
+    """out = epilogue(A . B); see include/jz.h for operand layouts."""
+    assert A.dtype == BF16 and B.dtype == BF16, "GEMM operands must be bf16"
+    lda = lda if lda is not None else A.stride(0)
+    ldb = ldb if ldb is not None else B.stride(0)
+    ldd = ldd if ldd is not None else out.stride(0)
+    ws = None
+    if split_k > 1:
+        nbytes = L.load().jz_gemm_workspace_bytes(M, N, split_k)
+        ws = scratch("gemm_splitk", nbytes // 4 + 1)
+    L.call("jz_gemm_bf16", A.data_ptr(), lda, int(a_kmajor), B.data_ptr(), ldb, int(b_kmajor), out.data_ptr(),
+           ldd, M, N, K, epilogue, _p(bias), _p(aux), ldaux if ldaux is not None else (aux.stride(0) if aux is not None else 0),
+           _p(out2), ldd2 if ldd2 is not None else (out2.stride(0) if out2 is not None else 0), split_k, _p(ws), _s())
+    return out
+
+
+def splitk_for(m_out: int, n_out: int, k: int) -> int:
+    bn = 256 if n_out > 128 else (128 if n_out > 64 else 64)
+    tiles = -(-m_out // 128) * -(-n_out // bn)
+    kb = -(-k // 64)
+    return max(1, min(kb, round(num_sms() / tiles)))
+
+
+def linear_fwd(x_bf16: torch.Tensor, w_bf16: torch.Tensor, bias: torch.Tensor | None, *, epilogue=L.EPI_BF16,
+               out=None, aux=None, out2=None) -> torch.Tensor:
+    """y = x @ W (+b), W stored (din, dout) as the reference (nn.py:43-47)."""
+    M, K = x_bf16.shape
+    N = w_bf16.shape[1]
+    if out is None:
+        dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU, L.EPI_GELU_BWD) else F32
+        out = torch.empty(M, N, dtype=dt, device=x_bf16.device)
+    return gemm(x_bf16, w_bf16, M=M, N=N, K=K, a_kmajor=True, b_kmajor=False, out=out, epilogue=epilogue,
+                bias=bias, aux=aux, out2=out2)
+
+
+def linear_dx(dy_bf16: torch.Tensor, w_bf16: torch.Tensor, *, epilogue=L.EPI_F32, out=None, aux=None,
+              out2=None) -> torch.Tensor:
+    """dx = dy @ W^T  (W (din, dout) row-major is K-major for this product)."""
+    M, N = dy_bf16.shape
+    K_in = w_bf16.shape[0]
+    if out is None:
+        dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU_BWD) else F32
+        out = torch.empty(M, K_in, dtype=dt, device=dy_bf16.device)
+    return gemm(dy_bf16, w_bf16, M=M, N=K_in, K=N, a_kmajor=True, b_kmajor=True, out=out, epilogue=epilogue,
+                aux=aux, out2=out2, ldb=w_bf16.stride(0))
+
+
+def linear_dw(x_bf16: torch.Tensor, dy_bf16: torch.Tensor, out_f32: torch.Tensor, *, accumulate=False,
+              n_cols: int | None = None) -> torch.Tensor:
+    """dW = x^T @ dy  -> out_f32 (din, dout); dy may be a column slice (n_cols, row pitch = stride)."""
+    Mtok, K_in = x_bf16.shape
+    N = n_cols if n_cols is not None else dy_bf16.shape[1]
+    split = splitk_for(K_in, N, Mtok)
+    return gemm(x_bf16, dy_bf16, M=K_in, N=N, K=Mtok, a_kmajor=False, b_kmajor=False, out=out_f32,
+                epilogue=L.EPI_F32_ACC if accumulate else L.EPI_F32, split_k=split, lda=x_bf16.stride(0),
+                ldb=dy_bf16.stride(0), ldd=out_f32.stride(0))
+
+
+# --------------------------------------------------------------------------
+# reductions / casts
+# --------------------------------------------------------------------------
+def row_partials(rows: int) -> int:
+    return L.load().jz_row_partials(rows)
+
+
+def colsum_bf16(x: torch.Tensor, out: torch.Tensor, *, cols: int | None = None, accumulate=False) -> torch.Tensor:
+    rows = x.shape[0]
+    cols = cols if cols is not None else x.shape[1]
+    npart = row_partials(rows)
+    part = scratch("colsum_part", npart * cols)
+    L.call("jz_colsum_bf16", x.data_ptr(), rows, cols, x.stride(0), part.data_ptr(), npart, _s())
+    L.call("jz_reduce_partials", part.data_ptr(), npart, cols, out.data_ptr(), int(accumulate), _s())
+    return out
+
+
+def reduce_partials(part: torch.Tensor, nparts: int, D: int, out: torch.Tensor, accumulate=False) -> None:
+    L.call("jz_reduce_partials", part.data_ptr(), nparts, D, out.data_ptr(), int(accumulate), _s())
+
+
+def cast_bf16(src: torch.Tensor, dst: torch.Tensor | None = None) -> torch.Tensor:
+    """2-D (or 1-D) fp32 -> bf16; dst may be a column slice of a wider matrix."""
+    if src.dim() == 1:
+        src2 = src.view(1, -1)
+    else:
+        src2 = src
+    rows, cols = src2.shape
+    if dst is None:
+        dst = torch.empty(rows, cols, dtype=BF16, device=src.device)
+    dst2 = dst.view(1, -1) if dst.dim() == 1 else dst
+    L.call("jz_cast_f32_bf16_2d", src2.data_ptr(), src2.stride(0), dst2.data_ptr(), dst2.stride(0), rows, cols, _s())
+    return dst
+
+
+# --------------------------------------------------------------------------
+# K2 LayerNorm
+# --------------------------------------------------------------------------
+def layernorm_fwd(x: torch.Tensor, g: torch.Tensor, b: torch.Tensor, *, skip_period: int = 0, eps: float = 1e-5):
+    rows, D = x.shape
+    out_rows = rows - (rows // skip_period if skip_period else 0)
+    y = torch.empty(out_rows, D, dtype=BF16, device=x.device)
+    mean = torch.empty(rows, dtype=F32, device=x.device)
+    rstd = torch.empty(rows, dtype=F32, device=x.device)
+    L.call("jz_layernorm_fwd", x.data_ptr(), rows, D, g.data_ptr(), b.data_ptr(), eps, y.data_ptr(),
+           mean.data_ptr(), rstd.data_ptr(), skip_period, _s())
+    return y, mean, rstd
+
+
+def layernorm_bwd(x, mean, rstd, g, dy, dres, *, accumulate: bool, dres_bf16=None, dgamma=None, dbeta=None,
+                  dbias=None, skip_period: int = 0, acc_params: bool = False):
+    """dres = (accumulate ? dres : 0) + LN'(dy); reduces dgamma/dbeta/dbias(=colsum dres) into the given outs."""
+    rows, D = x.shape
+    npart = row_partials(rows)
+    part = scratch("ln_part", 3 * npart * D)
+    pg = part[: npart * D] if dgamma is not None else None
+    pb = part[npart * D: 2 * npart * D] if dbeta is not None else None
+    pz = part[2 * npart * D:] if dbias is not None else None
+    L.call("jz_layernorm_bwd", x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), g.data_ptr(), dy.data_ptr(),
+           dres.data_ptr(), int(accumulate), _p(dres_bf16), _p(pg), _p(pb), _p(pz), npart, rows, D, skip_period,
+           _s())
+    if dgamma is not None:
+        reduce_partials(pg, npart, D, dgamma, acc_params)
+    if dbeta is not None:
+        reduce_partials(pb, npart, D, dbeta, acc_params)
+    if dbias is not None:
+        reduce_partials(pz, npart, D, dbias, acc_params)
+
+
+# --------------------------------------------------------------------------
+# attention
+# --------------------------------------------------------------------------
+def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: bool = True):
+    """-> (out bf16, out fp32 or None, lse)."""
+    D = H * 64
+    out = torch.empty(frames * S, D, dtype=BF16, device=qkv.device)
+    out32 = torch.empty(frames * S, D, dtype=F32, device=qkv.device) if keep_f32 else None
+    lse = torch.empty(frames, H, S, dtype=F32, device=qkv.device)
+    L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), _p(out32), lse.data_ptr(), _s())
+    return out, out32, lse
+
+
+def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=None):
+    if dqkv is None:
+        dqkv = torch.empty_like(qkv)
+    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
+           64, dqkv.data_ptr(), _s())
+    return dqkv
+
+
+def attn_temporal_fwd(qkv: torch.Tensor, B: int, T: int, S: int, H: int):
+    D = H * 64
+    out = torch.empty(B * T * S, D, dtype=BF16, device=qkv.device)
+    lse = torch.empty(B * S, H, T, dtype=F32, device=qkv.device)
+    L.call("jz_attn_temporal_fwd", qkv.data_ptr(), B, T, S, H, 64, out.data_ptr(), lse.data_ptr(), _s())
+    return out, lse
+
+
+def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=None):
+    if dqkv is None:
+        dqkv = torch.empty_like(qkv)
+    L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, T, S, H, 64,
+           dqkv.data_ptr(), _s())
+    return dqkv
+
+
+# --------------------------------------------------------------------------
+# dynamics input side, masks, CE, AdamW
+# --------------------------------------------------------------------------
+def philox_mask(state, B_global: int, b0: int, B_local: int, T: int, N: int, mask_limit: float,
+                mask_out: torch.Tensor, count_out: torch.Tensor) -> None:
+    """state: rng.PhiloxState (host).  count_out must be zeroed (int32 device scalar)."""
+    import ctypes as C
+    ctr = (C.c_uint64 * 4)(*state.counter)
+    key = (C.c_uint64 * 2)(*state.key)
+    buf = (C.c_uint64 * 4)(*state.buffer)
+    L.call("jz_philox_mask", C.addressof(ctr), C.addressof(key), C.addressof(buf), state.buffer_pos, B_global, b0,
+           B_local, T, N, float(mask_limit), mask_out.data_ptr(), count_out.data_ptr(), _s())
+
+
+def dyn_embed_fwd(tokens, mask, latents, P: dict, *, B, T, N, D, dl, K, prepend, err):
+    S = N + (1 if prepend else 0)
+    x = torch.empty(B * T * S, D, dtype=F32, device=tokens.device)
+    L.call("jz_dyn_embed_fwd", tokens.data_ptr(), _p(mask), _p(latents), P["token_embed"].data_ptr(),
+           P["mask_token"].data_ptr(), P["null_action"].data_ptr(), P["action_proj.w"].data_ptr(),
+           P["action_proj.b"].data_ptr(), P["pos_spatial"].data_ptr(), P["pos_temporal"].data_ptr(), B, T, N, D,
+           dl, K, int(prepend), x.data_ptr(), err.data_ptr(), _s())
+    return x
+
+
+def dyn_embed_bwd(dx, tokens, mask, latents, P: dict, G: dict, *, B, T, N, D, dl, K, prepend, d_latents=None):
+    nws = L.load().jz_dyn_embed_bwd_workspace(B, T, N, D, dl, int(prepend))
+    ws = scratch("embed_ws", nws)
+    L.call("jz_dyn_embed_bwd", dx.data_ptr(), tokens.data_ptr(), _p(mask), _p(latents),
+           P["null_action"].data_ptr(), P["action_proj.w"].data_ptr(), B, T, N, D, dl, K, int(prepend),
+           G["token_embed"].data_ptr(), G["mask_token"].data_ptr(), G["null_action"].data_ptr(),
+           G["action_proj.w"].data_ptr(), G["action_proj.b"].data_ptr(), G["pos_spatial"].data_ptr(),
+           G["pos_temporal"].data_ptr(), _p(d_latents), ws.data_ptr(), _s())
+
+
+def ce_fwd_bwd(logits: torch.Tensor, targets: torch.Tensor, mask: torch.Tensor | None, count: torch.Tensor,
+               grad_scale: float = 1.0):
+    rows, K = logits.shape
+    dlogits = torch.empty(rows, K, dtype=BF16, device=logits.device)
+    row_loss = scratch("ce_rowloss", rows)
+    loss = torch.empty((), dtype=F32, device=logits.device)
+    L.call("jz_ce_fwd_bwd", logits.data_ptr(), rows, K, targets.data_ptr(), _p(mask), count.data_ptr(),
+           float(grad_scale), dlogits.data_ptr(), row_loss.data_ptr(), loss.data_ptr(), _s())
+    return loss, dlogits
+
+
+def finite_check(g: torch.Tensor, flag: torch.Tensor) -> None:
+    L.call("jz_finite_check", g.data_ptr(), g.numel(), flag.data_ptr(), _s())
+
+
+def adamw(p, g, m, v, *, lr, b1, b2, omb1, omb2, bc1, bc2, eps, lrwd, flag=None) -> None:
+    L.call("jz_adamw_step", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(), lr, b1, b2, omb1,
+           omb2, bc1, bc2, eps, lrwd, _p(flag), _s())

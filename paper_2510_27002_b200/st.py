@@ -1,0 +1,221 @@
+"""Spatio-temporal transformer backbone on B200 (mirror of deskworld/st.py).
+
+`st_forward` / `st_backward` run one ST stack (st.py:69-85) as a fixed schedule
+of libjz kernels on rows ordered (b, t, s):
+
+  per block:  LN -> QKV GEMM(+bias) -> tcgen05 spatial attention -> O GEMM(+bias+residual)
+              LN -> QKV GEMM(+bias) -> causal temporal attention  -> O GEMM(+bias+residual)
+              LN -> up GEMM(+bias, GELU fused) -> down GEMM(+bias+residual)
+  final LN (optionally dropping the s=0 action-token rows, dynamics.py:135-136)
+
+The (B, T, S, D) -> (B, S, T, D) transpose of the reference's temporal sub-layer
+(st.py:74-76) never materialises: the temporal kernel gathers rows with stride S.
+The residual stream stays fp32; GEMM operands are bf16 with fp32 TMEM accumulation.
+The backward is the exact reverse schedule with deterministic reductions.
+"""
+from __future__ import annotations
+
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import kernels as K
+from .tensor import Tensor, param_count  # noqa: F401  (re-export, st.py:97-98)
+
+
+@dataclass(frozen=True)
+class StConfig:
+    """st.py:20-31 (same fields, defaults and validation)."""
+    model_dim: int = 512
+    heads: int = 8
+    ffn_dim: int = 2048
+    blocks: int = 4
+
+    def __post_init__(self):
+        if self.model_dim % self.heads != 0:
+            raise ValueError("model_dim must divide by heads")
+        if self.ffn_dim % self.model_dim != 0 or self.ffn_dim // self.model_dim not in (1, 4):
+            raise ValueError("ffn expansion factor must be 1 or 4")
+
+
+def init_st_stack_arrays(rng, cfg: StConfig, prefix: str = "st", dtype=np.float32) -> "OrderedDict[str, np.ndarray]":
+    """Host init in the reference's exact draw order (st.py:34-57)."""
+    p: "OrderedDict[str, np.ndarray]" = OrderedDict()
+    d, f = cfg.model_dim, cfg.ffn_dim
+
+    def lin(name, din, dout):
+        p[f"{name}.w"] = rng.normal(0.0, 0.02, size=(din, dout)).astype(dtype)
+        p[f"{name}.b"] = np.zeros(dout, dtype=dtype)
+
+    def ln(name, dim):
+        p[f"{name}.g"] = np.ones(dim, dtype=dtype)
+        p[f"{name}.b"] = np.zeros(dim, dtype=dtype)
+
+    for i in range(cfg.blocks):
+        base = f"{prefix}.block{i}"
+        for sub in ("spatial", "temporal"):
+            ln(f"{base}.{sub}.ln", d)
+            for proj in ("q", "k", "v", "o"):
+                lin(f"{base}.{sub}.{proj}", d, d)
+        ln(f"{base}.ffn.ln", d)
+        lin(f"{base}.ffn.up", d, f)
+        lin(f"{base}.ffn.down", f, d)
+    ln(f"{prefix}.final_ln", d)
+    return p
+
+
+def init_st_stack(rng, cfg: StConfig, prefix: str = "st", dtype=np.float32) -> dict:
+    """st.py:44-57: returns device parameters."""
+    return {k: Tensor(v, requires_grad=True) for k, v in init_st_stack_arrays(rng, cfg, prefix, dtype).items()}
+
+
+def st_stack_param_count(cfg: StConfig) -> int:
+    """st.py:88-94."""
+    d, f = cfg.model_dim, cfg.ffn_dim
+    per_attn = 4 * (d * d + d) + 2 * d
+    per_ffn = d * f + f + f * d + d + 2 * d
+    return cfg.blocks * (2 * per_attn + per_ffn) + 2 * d
+
+
+def check_supported(cfg: StConfig, S: int, T: int) -> None:
+    """The device path's shape envelope (raises ValueError outside it; no CPU fallback)."""
+    if cfg.model_dim // cfg.heads != 64:
+        raise ValueError(f"device ST stack needs head_dim 64 (got {cfg.model_dim // cfg.heads})")
+    if cfg.model_dim % 128 or cfg.model_dim > 1024:
+        raise ValueError(f"device ST stack needs model_dim % 128 == 0 and <= 1024 (got {cfg.model_dim})")
+    if S not in (256, 257):
+        raise ValueError(f"device spatial attention supports S in (256, 257), got {S}")
+    if T > 16:
+        raise ValueError(f"device temporal attention supports T <= 16, got {T}")
+
+
+# --------------------------------------------------------------------------
+# weight shadows (re-derived every call: callers may swap `params` wholesale)
+# --------------------------------------------------------------------------
+def _shadows(P: dict, cfg: StConfig, prefix: str) -> list:
+    d, f = cfg.model_dim, cfg.ffn_dim
+    dev = P[f"{prefix}.final_ln.g"].data.device
+    out = []
+    for i in range(cfg.blocks):
+        base = f"{prefix}.block{i}"
+        blk = {}
+        for sub in ("spatial", "temporal"):
+            w = torch.empty(d, 3 * d, dtype=K.BF16, device=dev)
+            for j, proj in enumerate("qkv"):
+                K.cast_bf16(P[f"{base}.{sub}.{proj}.w"].data, w[:, j * d:(j + 1) * d])
+            blk[f"{sub}.wqkv"] = w
+            blk[f"{sub}.bqkv"] = torch.cat([P[f"{base}.{sub}.{p}.b"].data for p in "qkv"])
+            blk[f"{sub}.wo"] = K.cast_bf16(P[f"{base}.{sub}.o.w"].data)
+        blk["ffn.wup"] = K.cast_bf16(P[f"{base}.ffn.up.w"].data)
+        blk["ffn.wdown"] = K.cast_bf16(P[f"{base}.ffn.down.w"].data)
+        out.append(blk)
+    return out
+
+
+def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, T: int, S: int,
+               final_skip: bool = False, save: bool = True):
+    """x f32 [B*T*S, D] (consumed as the residual stream).
+
+    Returns (y bf16 [rows, D], ctx); y drops the s=0 rows when final_skip.
+    """
+    check_supported(cfg, S, T)
+    H = cfg.heads
+    frames = B * T
+    sh = _shadows(P, cfg, prefix)
+    blocks_ctx = []
+    for i in range(cfg.blocks):
+        base = f"{prefix}.block{i}"
+        w = sh[i]
+        c = {"x_in": x}
+        # spatial sub-layer (st.py:73)
+        xn, m1, r1 = K.layernorm_fwd(x, P[f"{base}.spatial.ln.g"].data, P[f"{base}.spatial.ln.b"].data)
+        qkv = K.linear_fwd(xn, w["spatial.wqkv"], w["spatial.bqkv"])
+        ao, ao32, lse_s = K.attn_spatial_fwd(qkv, frames, S, H, keep_f32=save)
+        x1 = K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=L.EPI_RESID, aux=x)
+        # temporal sub-layer (st.py:74-76)
+        xn2, m2, r2 = K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
+        qkv2 = K.linear_fwd(xn2, w["temporal.wqkv"], w["temporal.bqkv"])
+        ao2, lse_t = K.attn_temporal_fwd(qkv2, B, T, S, H)
+        x2 = K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=L.EPI_RESID, aux=x1)
+        # FFN (st.py:77-79)
+        xn3, m3, r3 = K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
+        hpre = torch.empty(xn3.shape[0], cfg.ffn_dim, dtype=K.BF16, device=x.device)
+        h = K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=L.EPI_GELU, out2=hpre)
+        x3 = K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=L.EPI_RESID, aux=x2)
+        if save:
+            c.update(xn=xn, m1=m1, r1=r1, qkv=qkv, ao=ao, ao32=ao32, lse_s=lse_s, x1=x1, xn2=xn2, m2=m2, r2=r2, qkv2=qkv2,
+                     ao2=ao2, lse_t=lse_t, x2=x2, xn3=xn3, m3=m3, r3=r3, h=h, hpre=hpre)
+            blocks_ctx.append(c)
+        x = x3
+    y, mf, rf = K.layernorm_fwd(x, P[f"{prefix}.final_ln.g"].data, P[f"{prefix}.final_ln.b"].data,
+                                skip_period=S if final_skip else 0)
+    ctx = None
+    if save:
+        ctx = dict(blocks=blocks_ctx, shadows=sh, x_final=x, mf=mf, rf=rf, B=B, T=T, S=S,
+                   final_skip=final_skip)
+    return y, ctx
+
+
+def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, prefix: str) -> torch.Tensor:
+    """dy: f32 gradient of the final-LN output (compacted like y).  Writes G[...]; returns dx f32 [rows, D]."""
+    B, T, S = ctx["B"], ctx["T"], ctx["S"]
+    H = cfg.heads
+    frames = B * T
+    d = cfg.model_dim
+    x_final = ctx["x_final"]
+    rows = x_final.shape[0]
+    dev = x_final.device
+    dres = torch.empty(rows, d, dtype=K.F32, device=dev)
+    dres_b = torch.empty(rows, d, dtype=K.BF16, device=dev)
+    nb = cfg.blocks
+    # final LN; its dbias partial is the last block's down-projection bias gradient
+    K.layernorm_bwd(x_final, ctx["mf"], ctx["rf"], P[f"{prefix}.final_ln.g"].data, dy, dres, accumulate=False,
+                    dres_bf16=dres_b, dgamma=G[f"{prefix}.final_ln.g"], dbeta=G[f"{prefix}.final_ln.b"],
+                    dbias=G[f"{prefix}.block{nb - 1}.ffn.down.b"], skip_period=S if ctx["final_skip"] else 0)
+    dtmp = torch.empty(rows, d, dtype=K.F32, device=dev)
+    dh = torch.empty(rows, cfg.ffn_dim, dtype=K.BF16, device=dev)
+    dao = torch.empty(rows, d, dtype=K.BF16, device=dev)
+    for i in reversed(range(nb)):
+        base = f"{prefix}.block{i}"
+        c = ctx["blocks"][i]
+        w = ctx["shadows"][i]
+        # ---- FFN: x3 = x2 + gelu(LN(x2) Wup + bup) Wdown + bdown
+        K.linear_dw(c["h"], dres_b, G[f"{base}.ffn.down.w"])
+        K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_GELU_BWD, out=dh, aux=c["hpre"])
+        K.colsum_bf16(dh, G[f"{base}.ffn.up.b"])
+        K.linear_dw(c["xn3"], dh, G[f"{base}.ffn.up.w"])
+        K.linear_dx(dh, w["ffn.wup"], epilogue=L.EPI_F32, out=dtmp)
+        K.layernorm_bwd(c["x2"], c["m3"], c["r3"], P[f"{base}.ffn.ln.g"].data, dtmp, dres, accumulate=True,
+                        dres_bf16=dres_b, dgamma=G[f"{base}.ffn.ln.g"], dbeta=G[f"{base}.ffn.ln.b"],
+                        dbias=G[f"{base}.temporal.o.b"])
+        # ---- temporal: x2 = x1 + attn_t(LN(x1)) Wo + bo
+        K.linear_dw(c["ao2"], dres_b, G[f"{base}.temporal.o.w"])
+        K.linear_dx(dres_b, w["temporal.wo"], epilogue=L.EPI_BF16, out=dao)
+        dqkv = K.attn_temporal_bwd(c["qkv2"], c["ao2"], dao, c["lse_t"], B, T, S, H)
+        _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d)
+        K.linear_dx(dqkv, w["temporal.wqkv"], epilogue=L.EPI_F32, out=dtmp)
+        K.layernorm_bwd(c["x1"], c["m2"], c["r2"], P[f"{base}.temporal.ln.g"].data, dtmp, dres, accumulate=True,
+                        dres_bf16=dres_b, dgamma=G[f"{base}.temporal.ln.g"], dbeta=G[f"{base}.temporal.ln.b"],
+                        dbias=G[f"{base}.spatial.o.b"])
+        # ---- spatial: x1 = x + attn_s(LN(x)) Wo + bo
+        K.linear_dw(c["ao"], dres_b, G[f"{base}.spatial.o.w"])
+        K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao)
+        dqkv = K.attn_spatial_bwd(c["qkv"], c["ao32"], dao, c["lse_s"], frames, S, H, dqkv=dqkv)
+        _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d)
+        K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_F32, out=dtmp)
+        prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
+        K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
+                        dres_bf16=dres_b if i > 0 else None, dgamma=G[f"{base}.spatial.ln.g"],
+                        dbeta=G[f"{base}.spatial.ln.b"], dbias=prev_bias)
+    return dres
+
+
+def _qkv_param_grads(dqkv: torch.Tensor, xn: torch.Tensor, G: dict, base: str, d: int) -> None:
+    bq = torch.empty(3 * d, dtype=K.F32, device=dqkv.device)
+    K.colsum_bf16(dqkv, bq)
+    for j, proj in enumerate("qkv"):
+        G[f"{base}.{proj}.b"].copy_(bq[j * d:(j + 1) * d])
+        K.linear_dw(xn, dqkv[:, j * d:(j + 1) * d], G[f"{base}.{proj}.w"], n_cols=d)
