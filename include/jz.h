@@ -50,6 +50,9 @@ JZ_API int jz_device_check(int device);
 /* Library build identification (compile-time arch list). */
 JZ_API const char* jz_build_info(void);
 
+/* Number of kernels libjz has launched in this process (all threads). */
+JZ_API unsigned long long jz_launch_count(void);
+
 /* ------------------------------------------------------------------------
  * K1  GEMM  D[M,N] = epilogue( A[M,K] . B[K,N] )   bf16 x bf16 -> fp32 (TMEM)
  * Replaces nn.linear (nn.py:43-47) and the matmul forward/backward of

@@ -83,12 +83,18 @@ def load() -> C.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = []
             fn.restype = C.c_char_p
+        lib.jz_launch_count.argtypes = []
+        lib.jz_launch_count.restype = C.c_ulonglong
         _lib = lib
         return lib
 
 
 def exported_symbols() -> list[str]:
-    return sorted(PROTOTYPES) + ["jz_last_error", "jz_build_info"]
+    return sorted(PROTOTYPES) + ["jz_last_error", "jz_build_info", "jz_launch_count"]
+
+
+def launch_count() -> int:
+    return int(load().jz_launch_count())
 
 
 def last_error() -> str:

@@ -3,6 +3,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "common.h"
@@ -13,6 +14,9 @@
 namespace jz {
 
 static thread_local char g_err[1024] = {0};
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -93,3 +97,5 @@ extern "C" int jz_device_check(int device) {
 extern "C" const char* jz_build_info(void) {
   return "libjz sm_100a (tcgen05/TMEM/TMA), CUDA " JZ_XSTR(__CUDACC_VER_MAJOR__) "." JZ_XSTR(__CUDACC_VER_MINOR__);
 }
+
+extern "C" unsigned long long jz_launch_count(void) { return jz::g_launches.load(std::memory_order_relaxed); }

@@ -11,6 +11,7 @@
 namespace jz {
 
 void set_error(const char* fmt, ...);
+void count_launch();
 
 #define JZ_CHECK_ARG(cond, ...)        \
   do {                                 \
@@ -31,6 +32,7 @@ void set_error(const char* fmt, ...);
 
 #define JZ_LAUNCH_CHECK()                                                                      \
   do {                                                                                         \
+    ::jz::count_launch();                                                                      \
     cudaError_t _e = cudaGetLastError();                                                       \
     if (_e != cudaSuccess) {                                                                   \
       ::jz::set_error("%s:%d kernel launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \

@@ -209,8 +209,14 @@ class DynamicsModel:
         f = self._forward(tokens, lat, mask_d, save=False)
         return Tensor(f["logits"].view(f["B"], f["T"], f["N"], self.cfg.token_codes))
 
-    def loss(self, tokens, actions, rng: np.random.Generator, source_codebook=None, mask=None):
-        """dynamics.py:139-153: (loss Tensor with .backward(), stats)."""
+    def loss(self, tokens, actions, rng: np.random.Generator, source_codebook=None, mask=None, *,
+             _count=None, _on_grads_done=None):
+        """dynamics.py:139-153: (loss Tensor with .backward(), stats).
+
+        Internal keywords (data parallel, dp.py): `_count` overrides the masked-position count
+        used for normalisation (the GLOBAL count); `_on_grads_done(name)` is called as each
+        gradient bucket ("head", "block{i}", "embed") becomes final during backward.
+        """
         cfg = self.cfg
         b, t, n = tuple(np.shape(tokens)) if not isinstance(tokens, torch.Tensor) else tuple(tokens.shape)
         latents = self.action_latents_for(actions, source_codebook)
@@ -222,6 +228,8 @@ class DynamicsModel:
             else:
                 mask_d = as_device(np.asarray(mask, dtype=np.uint8))
             count = mask_d.sum(dtype=torch.int32)
+        if _count is not None:
+            count = _count
         stats = _LazyStats(mask_d, count)
         f = self._forward(tokens, latents, mask_d, save=True)
         loss, dlogits = K.ce_fwd_bwd(f["logits"], f["tok"].view(-1), mask_d.view(-1), count)
@@ -234,11 +242,17 @@ class DynamicsModel:
             K.colsum_bf16(dlogits, G["to_logits.b"])
             K.linear_dw(f["y"], dlogits, G["to_logits.w"])
             dy = K.linear_dx(dlogits, f["wl"], epilogue=L.EPI_F32)
-            dx = st_backward(f["ctx"], dy, P, G, cfg.st, "dyn")
+            hook = None
+            if _on_grads_done is not None:
+                def hook(name):
+                    _on_grads_done("head" if name == "head_ln" else name)
+            dx = st_backward(f["ctx"], dy, P, G, cfg.st, "dyn", on_done=hook)
             d_lat = torch.empty_like(f["lat"]) if need_lat_grad else None
             K.dyn_embed_bwd(dx, f["tok"], mask_d, f["lat"], {k: v.data for k, v in P.items()}, G,
                             B=f["B"], T=f["T"], N=f["N"], D=cfg.model_dim, dl=cfg.action_latent_dim,
                             K=cfg.token_codes, prepend=self._prepend, d_latents=d_lat)
+            if _on_grads_done is not None:
+                _on_grads_done("embed")
             if need_lat_grad:
                 latents.grad = d_lat.view_as(latents.data)
                 if latents._backward is not None:

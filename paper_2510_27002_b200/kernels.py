@@ -54,6 +54,22 @@ def num_sms() -> int:
 # --------------------------------------------------------------------------
 # K1 GEMM
 # --------------------------------------------------------------------------
+class KernelTimer:
+    """CUDA-event timing of every GEMM launch while active (roofline evidence for bench.py)."""
+
+    def __init__(self):
+        self.active = False
+        self.events: list = []
+        self.flops = 0
+        self.launches = 0
+
+    def ms(self) -> float:
+        return sum(a.elapsed_time(b) for a, b in self.events)
+
+
+TIMER: KernelTimer | None = None
+
+
 def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: bool, b_kmajor: bool,
          out: torch.Tensor, epilogue: int, bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
          out2: torch.Tensor | None = None, split_k: int = 1, lda: int | None = None, ldb: int | None = None,
@@ -67,9 +83,19 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: 
     if split_k > 1:
         nbytes = L.load().jz_gemm_workspace_bytes(M, N, split_k)
         ws = scratch("gemm_splitk", nbytes // 4 + 1)
+    timed = TIMER is not None and TIMER.active
+    if timed:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
     L.call("jz_gemm_bf16", A.data_ptr(), lda, int(a_kmajor), B.data_ptr(), ldb, int(b_kmajor), out.data_ptr(),
            ldd, M, N, K, epilogue, _p(bias), _p(aux), ldaux if ldaux is not None else (aux.stride(0) if aux is not None else 0),
            _p(out2), ldd2 if ldd2 is not None else (out2.stride(0) if out2 is not None else 0), split_k, _p(ws), _s())
+    if timed:
+        e1.record()
+        TIMER.events.append((e0, e1))
+        TIMER.flops += 2 * M * N * K
+        TIMER.launches += 1
     return out
 
 

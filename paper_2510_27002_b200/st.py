@@ -159,8 +159,13 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
     return y, ctx
 
 
-def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, prefix: str) -> torch.Tensor:
-    """dy: f32 gradient of the final-LN output (compacted like y).  Writes G[...]; returns dx f32 [rows, D]."""
+def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, prefix: str,
+                on_done=None) -> torch.Tensor:
+    """dy: f32 gradient of the final-LN output (compacted like y).  Writes G[...]; returns dx f32 [rows, D].
+
+    on_done(name) is called (stream-ordered) as soon as a parameter group's gradients are final:
+    "head_ln" after the final LN, then "block{i}" for i = n-1 .. 0 (data-parallel bucket hooks).
+    """
     B, T, S = ctx["B"], ctx["T"], ctx["S"]
     H = cfg.heads
     frames = B * T
@@ -175,6 +180,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
     K.layernorm_bwd(x_final, ctx["mf"], ctx["rf"], P[f"{prefix}.final_ln.g"].data, dy, dres, accumulate=False,
                     dres_bf16=dres_b, dgamma=G[f"{prefix}.final_ln.g"], dbeta=G[f"{prefix}.final_ln.b"],
                     dbias=G[f"{prefix}.block{nb - 1}.ffn.down.b"], skip_period=S if ctx["final_skip"] else 0)
+    if on_done is not None:
+        on_done("head_ln")
     dtmp = torch.empty(rows, d, dtype=K.F32, device=dev)
     dh = torch.empty(rows, cfg.ffn_dim, dtype=K.BF16, device=dev)
     dao = torch.empty(rows, d, dtype=K.BF16, device=dev)
@@ -210,6 +217,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
                         dres_bf16=dres_b if i > 0 else None, dgamma=G[f"{base}.spatial.ln.g"],
                         dbeta=G[f"{base}.spatial.ln.b"], dbias=prev_bias)
+        if on_done is not None:
+            on_done(f"block{i}")
     return dres
 
 

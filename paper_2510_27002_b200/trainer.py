@@ -1,0 +1,66 @@
+"""Device training step for the dynamics stage (mirror of trainer.run_stage's step body).
+
+run_stage (trainer.py:165-191) per step:
+    rng = stream(seed, stage, "step", step)
+    loss = loss_fn(frames, actions, rng); backward
+    adamw_step(params, grads, adam, wsd_lr(schedule, step + 1)); grads reset
+
+DynamicsTrainStep does the same for the dynamics model on device-resident tokens
+and action latents (the frozen tokenizer/LAM labels), optionally data-parallel:
+rank r draws its shard of the global Philox mask, normalises by the global mask
+count and all-reduces gradient buckets (dp.py) overlapped with the backward.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import kernels as K
+from .dp import GradAllReduce, block_buckets, shard
+from .dynamics import DynamicsModel
+from .optim import WsdSchedule, adamw_init, adamw_step, wsd_lr
+from .rng import consume, stream
+from .tensor import Tensor
+
+
+class DynamicsTrainStep:
+    def __init__(self, model: DynamicsModel, schedule: WsdSchedule, *, seed: int = 0, stage: str = "dynamics",
+                 rank: int = 0, world: int = 1, group=None):
+        self.model = model
+        self.schedule = schedule
+        self.seed = seed
+        self.stage = stage
+        self.rank, self.world = rank, world
+        self.opt = adamw_init(model.params)
+        self.reducer = None
+        if world > 1:
+            store = model._store
+            store.grads()  # allocate the flat gradient buffer
+            buckets = block_buckets(store.offsets, "dyn", model.cfg.blocks, store.flat.numel())
+            self.reducer = GradAllReduce(store.grad_flat, buckets, group=group)
+
+    def step(self, step: int, tokens: torch.Tensor, latents: Tensor, global_batch: int | None = None):
+        """One training step on this rank's slice; returns the (rank-local share of the) loss tensor."""
+        m = self.model
+        cfg = m.cfg
+        B, T, N = tokens.shape
+        gb = global_batch if global_batch is not None else B * self.world
+        rng = stream(self.seed, self.stage, "step", step)
+        st = consume(rng, gb + gb * T * N)
+        dev = tokens.device
+        b0, bl = shard(gb, self.rank, self.world)
+        mask = torch.empty(bl, T, N, dtype=torch.uint8, device=dev)
+        count_local = torch.zeros((), dtype=torch.int32, device=dev)
+        K.philox_mask(st, gb, b0, bl, T, N, cfg.mask_limit, mask, count_local)
+        count = count_local
+        if self.world > 1:
+            full = K.scratch("dp_full_mask", gb * T * N, dtype=torch.uint8).view(gb, T, N)
+            count = torch.zeros((), dtype=torch.int32, device=dev)
+            K.philox_mask(st, gb, 0, gb, T, N, cfg.mask_limit, full, count)
+        hook = self.reducer.ready if self.reducer is not None else None
+        loss, _ = m.loss(tokens, latents, None, mask=mask, _count=count, _on_grads_done=hook)
+        loss.backward()
+        if self.reducer is not None:
+            self.reducer.finish()
+        adamw_step(m.params, {n: p.grad for n, p in m.params.items()}, self.opt, wsd_lr(self.schedule, step + 1),
+                   check="deferred")
+        return loss
