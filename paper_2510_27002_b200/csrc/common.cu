@@ -40,27 +40,32 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return g_encode;
 }
 
-int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                      uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+int make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
+                 uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
   auto enc = encoder();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return JZ_ECUDA;
   }
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint64_t strides[1] = {pitch_elems * (uint64_t)elem_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu pitch=%llu box=%ux%u", (int)r,
-              (unsigned long long)inner, (unsigned long long)outer,
-              (unsigned long long)pitch_elems, box_inner, box_outer);
+              (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)pitch_elems, box_inner,
+              box_outer);
     return JZ_ECUDA;
   }
   return JZ_OK;
+}
+
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                      uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(map, base, 2, inner, outer, pitch_elems, box_inner, box_outer);
 }
 
 int num_sms() {

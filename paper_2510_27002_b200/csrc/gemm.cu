@@ -8,12 +8,15 @@
 // operand "major-ness" carried in the UMMA instruction descriptor, so no operand is
 // ever transposed in HBM.
 //
-// Roles (192 threads, one CTA per SM, persistent over output tiles):
+// Roles (320 threads, one CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer: A/B tiles -> smem ring (128B swizzle), mbarrier tx
 //   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=BN, K=16)
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+//   warps 2..9  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue -> HBM
+//               (two warps per TMEM lane quarter, each owning half of the columns)
 // TMEM holds two BN-column fp32 accumulators so the epilogue of tile i overlaps the
 // main loop of tile i+1.
+#include <string.h>
+
 #include <mutex>
 
 #include "common.h"
@@ -21,7 +24,8 @@
 
 namespace jz {
 
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;                     // 2 warps per TMEM lane quarter
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // + TMA warp + MMA warp
 constexpr int BM = 128;
 constexpr int BK = 64;
 
@@ -36,6 +40,11 @@ struct GemmParams {
   int64_t ldaux;
   void* D2;
   int64_t ldd2;
+  int tma_epi;  // 1: staged TMA-store epilogue (maps valid), 0: direct per-thread stores
+};
+
+struct EpiMaps {
+  CUtensorMap d, d2, aux;
 };
 
 template <int BN>
@@ -46,7 +55,8 @@ struct GemmShape {
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STG_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B, 128B-swizzled
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + kEpiWarps * STG_BYTES + 1024 + 256 + BN * 4;
 };
 
 JZ_DEV float fast_tanh(float x) {
@@ -72,18 +82,6 @@ JZ_DEV float gelu_grad_fast(float x) {
 JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], float* ws_out) {
   const int N = p.N;
   const bool full = (n + 32 <= N);
-  if (p.bias != nullptr && ws_out == nullptr) {
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 b = *reinterpret_cast<const float4*>(p.bias + n + j);
-        v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
-      }
-    } else {
-      for (int j = 0; j < 32; ++j)
-        if (n + j < N) v[j] += p.bias[n + j];
-    }
-  }
   if (ws_out != nullptr) {  // split-K partial: plain fp32 [M][N]
     float* dst = ws_out + (int64_t)m * N + n;
     if (full && (N % 4 == 0)) {
@@ -210,16 +208,19 @@ JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], fl
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     GemmParams p, float* ws) {
+                     const __grid_constant__ EpiMaps em, GemmParams p, float* ws) {
   using S = GemmShape<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
+  uint8_t* stg_base = smem + S::STAGES * S::STAGE_BYTES;  // kEpiWarps x 4 KB (1024-aligned)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * S::STG_BYTES);
   uint64_t* empty_bar = full_bar + S::STAGES;
   uint64_t* tfull_bar = empty_bar + S::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
+  float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + 256);  // [BN]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -227,6 +228,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (p.tma_epi) {
+      tma_prefetch_desc(&em.d);
+      if (p.epi == JZ_EPI_GELU) tma_prefetch_desc(&em.d2);
+      if (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD) tma_prefetch_desc(&em.aux);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < S::STAGES; ++i) {
@@ -235,8 +241,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 128);
+      mbar_init(&tempty_bar[i], 32 * kEpiWarps);
     }
+    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<S::TMEM_COLS>(tmem_slot);
@@ -314,34 +321,150 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
     const uint32_t quarter = warp & 3;
+    const int ew = warp - 2;
+    const int chalf = ew >> 2;
+    constexpr int HALF = BN / 2;
+    const int etid = threadIdx.x - 64;  // 0 .. 32*kEpiWarps-1
+    uint8_t* stg = stg_base + ew * S::STG_BYTES;
+    uint32_t apar = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int tile = u / p.splits, split = u % p.splits;
       const int m0 = (tile / p.n_tiles) * BM, n0 = (tile % p.n_tiles) * BN;
+      const bool has_bias = p.bias != nullptr && p.splits == 1;
+      if (has_bias) {  // stage this tile's bias (previous tile fully consumed by all warps first)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        for (int c = etid; c < BN; c += 32 * kEpiWarps) sbias[c] = (n0 + c < p.N) ? p.bias[n0 + c] : 0.f;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int m = m0 + quarter * 32 + lane;
-      float* ws_out = (p.splits > 1) ? ws + (int64_t)split * p.M * p.N : nullptr;
+      const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * BN + chalf * HALF;
+      const int row0 = m0 + quarter * 32;
+      if (p.tma_epi) {
+        // ---------- staged TMA epilogue ----------
+        const bool f32out = p.splits > 1 || p.epi == JZ_EPI_F32 || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_RESID;
+        const bool need_aux = p.splits == 1 &&
+                              (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD);
+        const int CW = f32out ? 32 : 64;
+        const CUtensorMap* dmap = &em.d;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((quarter * 32) << 16) + acc * BN + c * 32, r);
-        tmem_ld_wait();
-        const int n = n0 + c * 32;
-        if (m < p.M && n < p.N) {
-          float v[32];
+        for (int cc = 0; cc < HALF / CW; ++cc) {
+          const int col = chalf * HALF + cc * CW;
+          const int n = n0 + col;
+          if (n >= p.N) break;  // warp-uniform
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          if (need_aux && lane == 0) {
+            mbar_arrive_expect_tx(&aux_bar[ew], S::STG_BYTES);
+            tma_load_2d(stg, &em.aux, &aux_bar[ew], n, row0);
+          }
+          float v[64];
+          {
+            uint32_t r0[32];
+            tmem_ld_32x32b_x32(tbase + cc * CW, r0);
+            tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          epilogue_chunk(p, m, n, v, ws_out);
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
+            if (!f32out) {
+              tmem_ld_32x32b_x32(tbase + cc * CW + 32, r0);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r0[j]);
+            }
+          }
+          if (has_bias) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (j < CW) v[j] += sbias[col + j];
+          }
+          if (need_aux) {
+            mbar_wait(&aux_bar[ew], apar);
+            apar ^= 1;
+            if (p.epi == JZ_EPI_GELU_BWD) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 w = *reinterpret_cast<const uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4));
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = unpack_bf16(ww[e]);
+                  v[8 * c + 2 * e] *= gelu_grad_fast(f.x);
+                  v[8 * c + 2 * e + 1] *= gelu_grad_fast(f.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const float4 w = *reinterpret_cast<const float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4));
+                v[4 * c] += w.x; v[4 * c + 1] += w.y; v[4 * c + 2] += w.z; v[4 * c + 3] += w.w;
+              }
+            }
+            __syncwarp();
+          }
+          if (f32out) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          } else {
+            if (p.epi == JZ_EPI_GELU) {  // pre-activation copy first (D2), then GELU into D
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                    make_uint4(pack_bf16(v[8 * c], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                               pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&em.d2, stg, n, row0);
+                bulk_commit();
+                bulk_wait_read0();
+              }
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_uint4(pack_bf16(v[8 * c], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                             pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(dmap, stg, n, row0 + (p.splits > 1 ? split * p.M : 0));
+            bulk_commit();
+          }
+        }
+      } else {
+        // ---------- direct epilogue (unaligned shapes) ----------
+        const int m = row0 + lane;
+        float* ws_out = (p.splits > 1) ? ws + (int64_t)split * p.M * p.N : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < HALF / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + 32 * c, r);
+          tmem_ld_wait();
+          const int col = chalf * HALF + c * 32;
+          const int n = n0 + col;
+          if (m < p.M && n < p.N && p.epi != 7) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (has_bias ? sbias[col + j] : 0.f);
+            epilogue_chunk(p, m, n, v, ws_out);
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait0();
   }
   __syncthreads();
   if (warp == 2) {
@@ -367,8 +490,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
 }
 
 template <int BN, bool A_MN, bool B_MN>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, float* ws,
-                       cudaStream_t stream) {
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmParams& p,
+                       float* ws, cudaStream_t stream) {
   using S = GemmShape<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -379,18 +502,18 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   JZ_CUDA_TRY(attr_err);
   const int units = p.m_tiles * p.n_tiles * p.splits;
   const int grid = units < num_sms() ? units : num_sms();
-  gemm_bf16_kernel<BN, A_MN, B_MN><<<grid, kGemmThreads, S::SMEM_BYTES, stream>>>(ta, tb, p, ws);
+  gemm_bf16_kernel<BN, A_MN, B_MN><<<grid, kGemmThreads, S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
 
 template <int BN>
-static int dispatch_major(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb,
+static int dispatch_major(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em,
                           const GemmParams& p, float* ws, cudaStream_t s) {
-  if (!a_mn && !b_mn) return launch_gemm<BN, false, false>(ta, tb, p, ws, s);
-  if (!a_mn && b_mn) return launch_gemm<BN, false, true>(ta, tb, p, ws, s);
-  if (a_mn && !b_mn) return launch_gemm<BN, true, false>(ta, tb, p, ws, s);
-  return launch_gemm<BN, true, true>(ta, tb, p, ws, s);
+  if (!a_mn && !b_mn) return launch_gemm<BN, false, false>(ta, tb, em, p, ws, s);
+  if (!a_mn && b_mn) return launch_gemm<BN, false, true>(ta, tb, em, p, ws, s);
+  if (a_mn && !b_mn) return launch_gemm<BN, true, false>(ta, tb, em, p, ws, s);
+  return launch_gemm<BN, true, true>(ta, tb, em, p, ws, s);
 }
 
 }  // namespace jz
@@ -413,7 +536,7 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
   JZ_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "gemm: lda/ldb must be multiples of 8 (got %lld, %lld)",
                (long long)lda, (long long)ldb);
   JZ_CHECK_ARG(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0, "gemm: A/B must be 16B aligned");
-  JZ_CHECK_ARG(epilogue >= JZ_EPI_F32 && epilogue <= JZ_EPI_BF16_F32, "gemm: bad epilogue %d", epilogue);
+  JZ_CHECK_ARG(epilogue >= JZ_EPI_F32 && epilogue <= 7, "gemm: bad epilogue %d", epilogue);
   JZ_CHECK_ARG(D != nullptr, "gemm: null output");
   if (epilogue == JZ_EPI_RESID || epilogue == JZ_EPI_GELU_BWD)
     JZ_CHECK_ARG(aux != nullptr, "gemm: epilogue %d needs aux", epilogue);
@@ -453,9 +576,32 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
   p.D2 = D2; p.ldd2 = ldd2;
 
   float* ws = p.splits > 1 ? reinterpret_cast<float*>(workspace) : nullptr;
-  if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, p, ws, stream);
-  else if (BN == 128) rc = dispatch_major<128>(a_mn, b_mn, ta, tb, p, ws, stream);
-  else rc = dispatch_major<64>(a_mn, b_mn, ta, tb, p, ws, stream);
+  // staged TMA epilogue when every global operand of the epilogue is TMA-legal
+  EpiMaps em;
+  memset(&em, 0, sizeof(em));
+  p.tma_epi = 0;
+  if (epilogue != 7) {
+    const bool f32out = p.splits > 1 || epilogue == JZ_EPI_F32 || epilogue == JZ_EPI_F32_ACC || epilogue == JZ_EPI_RESID;
+    const bool bf16out = epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD;
+    // split-K partials keep the direct path (long-K GEMMs: the epilogue is negligible there);
+    // 32-column bf16 chunks (BN = 64) do not fill a 128-byte swizzle row either.
+    bool ok = (f32out || bf16out) && p.splits == 1 && !(bf16out && BN == 64);
+    auto al = [](const void* q) { return ((uintptr_t)q % 16) == 0; };
+    if (ok && f32out) ok = al(D) && ldd % 4 == 0 && make_tmap_2d(&em.d, D, 4, N, M, ldd, 32, 32) == JZ_OK;
+    else if (ok) ok = al(D) && ldd % 8 == 0 && make_tmap_2d(&em.d, D, 2, N, M, ldd, 64, 32) == JZ_OK;
+    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU)
+      ok = al(D2) && ldd2 % 8 == 0 && make_tmap_2d(&em.d2, D2, 2, N, M, ldd2, 64, 32) == JZ_OK;
+    if (ok && p.splits == 1 && epilogue == JZ_EPI_RESID)
+      ok = al(aux) && ldaux % 4 == 0 && make_tmap_2d(&em.aux, aux, 4, N, M, ldaux, 32, 32) == JZ_OK;
+    if (ok && p.splits == 1 && epilogue == JZ_EPI_F32_ACC)
+      ok = make_tmap_2d(&em.aux, D, 4, N, M, ldd, 32, 32) == JZ_OK;
+    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU_BWD)
+      ok = al(aux) && ldaux % 8 == 0 && make_tmap_2d(&em.aux, aux, 2, N, M, ldaux, 64, 32) == JZ_OK;
+    p.tma_epi = ok ? 1 : 0;
+  }
+  if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, em, p, ws, stream);
+  else if (BN == 128) rc = dispatch_major<128>(a_mn, b_mn, ta, tb, em, p, ws, stream);
+  else rc = dispatch_major<64>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   if (rc) return rc;
   if (p.splits > 1) {
     const int64_t MN = M * N;

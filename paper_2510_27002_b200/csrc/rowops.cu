@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const float* __rest
 // combined in warp order through shared memory.
 // ---------------------------------------------------------------------------
 template <int V4>
-__global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
+__global__ void __launch_bounds__(kRowThreads, 2) ln_bwd_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ dy, float* dres, int accumulate,
     __nv_bfloat16* __restrict__ dres_bf16, float* __restrict__ part_dg, float* __restrict__ part_db,
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
   for (int64_t r = r0 + warp; r < r1; r += kRowThreads / 32) {
     const float mu = mean[r], rs = rstd[r];
     const float* xr = x + r * D;
-    float4 xv[V4], dyv[V4];
+    float4 xv[V4], dyv[V4], pv[V4];
     bool has_dy = true;
     int64_t irow = r;
     if (skip_period > 0) {
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
       const int c = 4 * lane + 128 * i;
       xv[i] = *reinterpret_cast<const float4*>(xr + c);
       dyv[i] = has_dy ? *reinterpret_cast<const float4*>(dy + irow * D + c) : make_float4(0, 0, 0, 0);
+      pv[i] = accumulate ? *reinterpret_cast<const float4*>(dres + r * D + c) : make_float4(0, 0, 0, 0);
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -139,10 +140,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_bwd_kernel(
       float4 o = make_float4(rs * (dyv[i].x - m1 - xv[i].x * m2), rs * (dyv[i].y - m1 - xv[i].y * m2),
                              rs * (dyv[i].z - m1 - xv[i].z * m2), rs * (dyv[i].w - m1 - xv[i].w * m2));
       float* dr = dres + r * D + c;
-      if (accumulate) {
-        float4 p = *reinterpret_cast<const float4*>(dr);
-        o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
-      }
+      o.x += pv[i].x; o.y += pv[i].y; o.z += pv[i].z; o.w += pv[i].w;
       *reinterpret_cast<float4*>(dr) = o;
       if (dres_bf16) {
         uint2 w = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
@@ -181,7 +179,19 @@ __global__ void __launch_bounds__(kRowThreads) colsum_bf16_kernel(const __nv_bfl
   const int64_t r1 = min(rows, r0 + rows_per_block);
   for (int c8 = threadIdx.x * 8; c8 < cols; c8 += kRowThreads * 8) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int64_t r = r0; r < r1; ++r) {
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4) {  // 4 independent 16-byte loads in flight, summed in row order
+      uint4 w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(x + (r + q) * ld + c8);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float2 a = unpack_bf16(w[q].x), b = unpack_bf16(w[q].y), c = unpack_bf16(w[q].z), d = unpack_bf16(w[q].w);
+        acc[0] += a.x; acc[1] += a.y; acc[2] += b.x; acc[3] += b.y;
+        acc[4] += c.x; acc[5] += c.y; acc[6] += d.x; acc[7] += d.y;
+      }
+    }
+    for (; r < r1; ++r) {
       uint4 w = *reinterpret_cast<const uint4*>(x + r * ld + c8);
       float2 a = unpack_bf16(w.x), b = unpack_bf16(w.y), c = unpack_bf16(w.z), d = unpack_bf16(w.w);
       acc[0] += a.x; acc[1] += a.y; acc[2] += b.x; acc[3] += b.y;
