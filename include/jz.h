@@ -100,13 +100,14 @@ JZ_API int jz_cast_f32_bf16_2d(const float* src, int64_t lds, void* dst, int64_t
 
 /* ------------------------------------------------------------------------
  * K2  LayerNorm, eps inside the sqrt, biased variance, two-pass (nn.py:35-40).
- * x f32 [rows, D] -> y bf16; mean/rstd f32 [rows] saved for the backward.
+ * x f32 [rows, D] -> y bf16 and/or y_f32 (either may be NULL); mean/rstd f32 [rows]
+ * saved for the backward.
  * skip_period > 0: rows r with r % skip_period == 0 are not written and the
  * output is compacted (drops the prepended action token before to_logits,
  * dynamics.py:135-136).  D multiple of 128, <= 1024.
  * ---------------------------------------------------------------------- */
 JZ_API int jz_layernorm_fwd(const float* x, int64_t rows, int D, const float* gamma, const float* beta,
-                            float eps, void* y_bf16, float* mean, float* rstd, int64_t skip_period,
+                            float eps, void* y_bf16, float* y_f32, float* mean, float* rstd, int64_t skip_period,
                             jz_stream_t stream);
 /* dres[r] = (accumulate ? dres[r] : 0) + LN_bwd(dy[r]); optional bf16 copy of dres;
  * per-CTA partials of dgamma = sum dy*xhat, dbeta = sum dy, dbias = sum dres_out
@@ -199,6 +200,62 @@ JZ_API int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, int H,
                                 float* lse, jz_stream_t stream);
 JZ_API int jz_attn_temporal_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                                 int64_t B, int T, int S, int H, int head_dim, void* dqkv, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K9  frames -> patches and back (tokenizer.py:49-55, nn.py:113-131).
+ * frames: uint8 (is_u8=1, unit = x/127.5 - 1) or fp32 unit-range, [BT, H, W, C];
+ * patches [BT*N, P*P*C] in (gh, gw) row-major order, inner (ph, pw, c): bf16
+ * (GEMM operand) and/or fp32 (recon target).  unpatchify writes fp32 unit frames
+ * and/or uint8 frames = rint(clip((u+1)*127.5, 0, 255)) (round half-even).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_patchify(const void* frames, int is_u8, int64_t BT, int H, int W, int C, int P, void* out_bf16,
+                       float* out_f32, jz_stream_t stream);
+JZ_API int jz_unpatchify(const float* patches, int64_t BT, int H, int W, int C, int P, float* unit,
+                         uint8_t* frames_u8, jz_stream_t stream);
+
+/* Token assembly: x[b,t,s] = (e + pos_spatial[s]) + pos_temporal[t] where e is the
+ * patch embedding emb[b,t,s-prepend] or, when prepend and s == 0, act[b,t]
+ * (tokenizer.py:113-119, lam.py:86-90, lam.py:108-113).  Backward splits dx into a
+ * compact bf16 d_emb, an fp32 d_act and deterministic position gradients. */
+JZ_API int jz_assemble_fwd(const float* emb, const float* act, const float* pos_spatial, const float* pos_temporal,
+                           int64_t B, int T, int N, int D, int prepend, float* x, jz_stream_t stream);
+JZ_API int64_t jz_assemble_bwd_workspace(int64_t B, int T, int N, int D, int prepend);
+JZ_API int jz_assemble_bwd(const float* dx, int64_t B, int T, int N, int D, int prepend, void* d_emb_bf16,
+                           float* d_act, float* d_pos_spatial, float* d_pos_temporal, float* workspace,
+                           jz_stream_t stream);
+
+/* K10 mean over the N patch rows of each frame (lam.py:92) and its backward. */
+JZ_API int jz_mean_pool(const float* x, int64_t BT, int N, int D, float* out, jz_stream_t stream);
+JZ_API int jz_mean_pool_bwd(const float* dpool, int64_t BT, int N, int D, float* dx, jz_stream_t stream);
+
+/* K15 loss = mean((pred - target)^2) (nn.py:50-53); grad = grad_scale * 2 (pred - target) / n
+ * into grad32 and/or grad16 (either may be NULL).  workspace: 2*num_SMs doubles. */
+JZ_API int jz_mse(const float* pred, const float* target, int64_t n, float grad_scale, float* loss, float* grad32,
+                  void* grad16, double* workspace, jz_stream_t stream);
+
+/* out = scale * sum(x) (fp64 accumulation, fixed order).  workspace: 2*num_SMs doubles. */
+JZ_API int jz_sum(const float* x, int64_t n, double scale, float* out, double* workspace, jz_stream_t stream);
+
+/* fp32 CUDA-core linear for the 32-wide latent projections (lam.py:94, lam.py:109):
+ * y = x W + b (W (K, N) as stored by the reference); backward dx = dy W^T,
+ * dW = x^T dy, db = sum dy (any output may be NULL; fixed summation order). */
+JZ_API int jz_linear_f32(const float* x, int64_t R, int K, const float* W, int N, const float* b, float* y,
+                         int accumulate, jz_stream_t stream);
+JZ_API int jz_linear_f32_bwd(const float* x, const float* dy, int64_t R, int K, int N, const float* W, float* dx,
+                             float* dW, float* db, int accumulate, jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K8  vector quantizer (tokenizer.vq_quantize, tokenizer.py:58-79), fp32:
+ * d2 = (|z|^2 - (2z).c) + |c|^2, idx = argmin (lowest index on ties),
+ * zq_st = z + (c_idx - z), row_sq[r] = sum (c_idx - z)^2 (losses = mean).
+ * Backward: dz = g_zq_st + commit_coef (z - c_idx);
+ *           dcodebook[k] = cb_coef * sum_{idx=k} (c_k - z)  (deterministic).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_vq_fwd(const float* z, int64_t rows, int dz, const float* codebook, int K, int64_t* idx,
+                     float* zq_st, float* row_sq, jz_stream_t stream);
+JZ_API int jz_vq_bwd(const float* z, const float* codebook, const int64_t* idx, const float* g_zq_st, int64_t rows,
+                     int dz, int K, float commit_coef, float cb_coef, float* dz_out, float* dcodebook,
+                     jz_stream_t stream);
 
 #ifdef __cplusplus
 }

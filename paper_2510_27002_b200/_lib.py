@@ -32,7 +32,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_colsum_bf16": [_P, _I64, _I32, _I64, _P, _I32, _P],
     "jz_reduce_partials": [_P, _I32, _I64, _P, _I32, _P],
     "jz_cast_f32_bf16_2d": [_P, _I64, _P, _I64, _I64, _I64, _P],
-    "jz_layernorm_fwd": [_P, _I64, _I32, _P, _P, _F32, _P, _P, _P, _I64, _P],
+    "jz_layernorm_fwd": [_P, _I64, _I32, _P, _P, _F32, _P, _P, _P, _P, _I64, _P],
     "jz_layernorm_bwd": [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I64, _I32, _I64, _P],
     "jz_ce_fwd_bwd": [_P, _I64, _I32, _P, _P, _P, _F32, _P, _P, _P, _P],
     "jz_finite_check": [_P, _I64, _P, _P],
@@ -47,8 +47,21 @@ PROTOTYPES: dict[str, list] = {
     "jz_attn_spatial_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P],
     "jz_attn_temporal_fwd": [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
     "jz_attn_temporal_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P],
+    "jz_patchify": [_P, _I32, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "jz_unpatchify": [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "jz_assemble_fwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P],
+    "jz_assemble_bwd_workspace": [_I64, _I32, _I32, _I32, _I32],
+    "jz_assemble_bwd": [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P],
+    "jz_mean_pool": [_P, _I64, _I32, _I32, _P, _P],
+    "jz_mean_pool_bwd": [_P, _I64, _I32, _I32, _P, _P],
+    "jz_mse": [_P, _P, _I64, _F32, _P, _P, _P, _P, _P],
+    "jz_sum": [_P, _I64, _F64, _P, _P, _P],
+    "jz_linear_f32": [_P, _I64, _I32, _P, _I32, _P, _P, _I32, _P],
+    "jz_linear_f32_bwd": [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _I32, _P],
+    "jz_vq_fwd": [_P, _I64, _I32, _P, _I32, _P, _P, _P, _P],
+    "jz_vq_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _F32, _F32, _P, _P, _P],
 }
-_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
+_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_assemble_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
             "jz_build_info": C.c_char_p}
 
 

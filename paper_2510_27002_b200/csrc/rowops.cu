@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const float* __rest
                                                              const float* __restrict__ g,
                                                              const float* __restrict__ b, float eps,
                                                              __nv_bfloat16* __restrict__ y,
+                                                             float* __restrict__ y32,
                                                              float* __restrict__ mean_out,
                                                              float* __restrict__ rstd_out,
                                                              int64_t skip_period) {
@@ -57,7 +58,6 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const float* __rest
       if (r % skip_period == 0) continue;
       orow = r - r / skip_period - 1;
     }
-    __nv_bfloat16* yr = y + orow * D;
 #pragma unroll
     for (int i = 0; i < V4; ++i) {
       const int c = 4 * lane + 128 * i;
@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const float* __rest
       float o1 = (v[i].y - mu) * rs * gg.y + bb.y;
       float o2 = (v[i].z - mu) * rs * gg.z + bb.z;
       float o3 = (v[i].w - mu) * rs * gg.w + bb.w;
-      uint2 w = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
-      *reinterpret_cast<uint2*>(yr + c) = w;
+      if (y) *reinterpret_cast<uint2*>(y + orow * D + c) = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+      if (y32) *reinterpret_cast<float4*>(y32 + orow * D + c) = make_float4(o0, o1, o2, o3);
     }
   }
 }
@@ -366,7 +366,7 @@ static int grid_for(int64_t n, int threads, int max_per_sm = 8) {
 using namespace jz;
 
 extern "C" int jz_layernorm_fwd(const float* x, int64_t rows, int D, const float* gamma, const float* beta,
-                                float eps, void* y_bf16, float* mean, float* rstd, int64_t skip_period,
+                                float eps, void* y_bf16, float* y_f32, float* mean, float* rstd, int64_t skip_period,
                                 jz_stream_t s) {
   JZ_CHECK_ARG(rows >= 0 && D % 128 == 0 && D >= 128 && D <= 1024,
                "layernorm: model dim %d unsupported on device (multiple of 128, <= 1024)", D);
@@ -375,12 +375,12 @@ extern "C" int jz_layernorm_fwd(const float* x, int64_t rows, int D, const float
   auto st = reinterpret_cast<cudaStream_t>(s);
   auto y = reinterpret_cast<__nv_bfloat16*>(y_bf16);
   switch (D / 128) {
-    case 1: ln_fwd_kernel<1><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, mean, rstd, skip_period); break;
-    case 2: ln_fwd_kernel<2><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, mean, rstd, skip_period); break;
-    case 3: ln_fwd_kernel<3><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, mean, rstd, skip_period); break;
-    case 4: ln_fwd_kernel<4><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, mean, rstd, skip_period); break;
-    case 6: ln_fwd_kernel<6><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, mean, rstd, skip_period); break;
-    case 8: ln_fwd_kernel<8><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, mean, rstd, skip_period); break;
+    case 1: ln_fwd_kernel<1><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, y_f32, mean, rstd, skip_period); break;
+    case 2: ln_fwd_kernel<2><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, y_f32, mean, rstd, skip_period); break;
+    case 3: ln_fwd_kernel<3><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, y_f32, mean, rstd, skip_period); break;
+    case 4: ln_fwd_kernel<4><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, y_f32, mean, rstd, skip_period); break;
+    case 6: ln_fwd_kernel<6><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, y_f32, mean, rstd, skip_period); break;
+    case 8: ln_fwd_kernel<8><<<grid, kRowThreads, 0, st>>>(x, rows, gamma, beta, eps, y, y_f32, mean, rstd, skip_period); break;
     default: set_error("layernorm: D=%d unsupported", D); return JZ_EINVAL;
   }
   JZ_LAUNCH_CHECK();

@@ -1,0 +1,375 @@
+// Pixel/latent-side kernels of the tokenizer and latent action model (all HBM-bound):
+//   K9  frames_to_unit + patchify        (tokenizer.py:49-51, nn.py:113-121)
+//       unpatchify + unit_to_frames     (nn.py:124-131, tokenizer.py:54-55; round half-even)
+//   token assembly: (+ prepended action token) + spatial + temporal positions, fwd/bwd
+//       (tokenizer.py:113-119, lam.py:86-90, lam.py:108-113)
+//   K10 mean-pool over patches           (lam.py:92-93)
+//   K15 recon MSE fwd/bwd                (nn.py:50-53, tokenizer.py:139, lam.py:125)
+//   small fp32 linear (CUDA cores) for the 32-wide latent projections whose outputs feed
+//       argmins (lam.py:94, lam.py:109) — too small for tensor-core tiles
+#include "common.h"
+#include "ptx.cuh"
+
+namespace jz {
+
+static int grid_of(int64_t n, int threads, int per_sm = 8) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * per_sm;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+// out[(bt*N + n)][(ph*P + pw)*C + c] = unit(frames[bt][gh*P+ph][gw*P+pw][c]),  n = gh*GW + gw
+__global__ void patchify_kernel(const void* __restrict__ frames, int is_u8, int64_t BT, int H, int W, int C, int P,
+                                __nv_bfloat16* __restrict__ out, float* __restrict__ out32) {
+  const int GW = W / P, N = (H / P) * GW, PD = P * P * C;
+  const int64_t total = BT * N * PD;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / PD;
+    const int col = (int)(e - row * PD);
+    const int64_t bt = row / N;
+    const int n = (int)(row - bt * N);
+    const int gh = n / GW, gw = n - gh * GW;
+    const int ph = col / (P * C), rem = col - ph * P * C, pw = rem / C, c = rem - pw * C;
+    const int64_t src = ((bt * H + gh * P + ph) * W + gw * P + pw) * C + c;
+    float v;
+    if (is_u8)
+      v = (float)reinterpret_cast<const uint8_t*>(frames)[src] / 127.5f - 1.0f;
+    else
+      v = reinterpret_cast<const float*>(frames)[src];
+    if (out) out[e] = __float2bfloat16_rn(v);
+    if (out32) out32[e] = v;
+  }
+}
+
+__global__ void unpatchify_kernel(const float* __restrict__ patches, int64_t BT, int H, int W, int C, int P,
+                                  float* __restrict__ unit, uint8_t* __restrict__ u8) {
+  const int GW = W / P, N = (H / P) * GW, PD = P * P * C;
+  const int64_t total = BT * H * W * C;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bt = e / ((int64_t)H * W * C);
+    int64_t r = e - bt * H * W * C;
+    const int y = (int)(r / (W * C));
+    r -= (int64_t)y * W * C;
+    const int x = (int)(r / C), c = (int)(r - x * C);
+    const int n = (y / P) * GW + x / P;
+    const int col = ((y % P) * P + (x % P)) * C + c;
+    const float v = patches[(bt * N + n) * PD + col];
+    if (unit) unit[e] = v;
+    if (u8) {
+      float f = (v + 1.0f) * 127.5f;
+      f = fminf(fmaxf(f, 0.0f), 255.0f);
+      u8[e] = (uint8_t)rintf(f);
+    }
+  }
+}
+
+// x[(b,t,s)] = ((e + ps[s]) + pt[t]);  prepend: s = 0 takes act[b,t], s >= 1 takes emb[b,t,s-1]
+__global__ void assemble_fwd_kernel(const float* __restrict__ emb, const float* __restrict__ act,
+                                    const float* __restrict__ ps, const float* __restrict__ pt, int T, int N, int D,
+                                    int prepend, float* __restrict__ x) {
+  const int S = N + prepend;
+  const int64_t row = blockIdx.x;
+  const int s = (int)(row % S);
+  const int64_t bt = row / S;
+  const int t = (int)(bt % T);
+  const float* src = (prepend && s == 0) ? act + bt * D : emb + (bt * N + (s - prepend)) * D;
+  for (int d = threadIdx.x * 4; d < D; d += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(src + d);
+    const float4 a = *reinterpret_cast<const float4*>(ps + (int64_t)s * D + d);
+    const float4 b = *reinterpret_cast<const float4*>(pt + (int64_t)t * D + d);
+    v.x = (v.x + a.x) + b.x; v.y = (v.y + a.y) + b.y; v.z = (v.z + a.z) + b.z; v.w = (v.w + a.w) + b.w;
+    *reinterpret_cast<float4*>(x + row * D + d) = v;
+  }
+}
+
+// d_emb (bf16, compact rows s >= prepend) and d_act (f32, rows s == 0) from dx
+__global__ void assemble_split_kernel(const float* __restrict__ dx, int N, int D, int prepend,
+                                      __nv_bfloat16* __restrict__ demb, float* __restrict__ dact) {
+  const int S = N + prepend;
+  const int64_t row = blockIdx.x;
+  const int s = (int)(row % S);
+  const int64_t bt = row / S;
+  for (int d = threadIdx.x * 4; d < D; d += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(dx + row * D + d);
+    if (prepend && s == 0) {
+      if (dact) *reinterpret_cast<float4*>(dact + bt * D + d) = v;
+    } else if (demb) {
+      *reinterpret_cast<uint2*>(demb + (bt * N + (s - prepend)) * D + d) =
+          make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    }
+  }
+}
+
+// positions: dps[s] = sum_{t,b} dx[b,t,s];  part_pt[s][t] = sum_b dx[b,t,s]
+__global__ void pos_bwd_kernel(const float* __restrict__ dx, int64_t B, int T, int S, int D, float* __restrict__ dps,
+                               float* __restrict__ part_pt) {
+  const int s = blockIdx.x;
+  for (int d = threadIdx.x * 4; d < D; d += blockDim.x * 4) {
+    float4 acc_s = make_float4(0, 0, 0, 0);
+    for (int t = 0; t < T; ++t) {
+      float4 acc_t = make_float4(0, 0, 0, 0);
+      for (int64_t b0 = 0; b0 < B; b0 += 4) {
+        float4 g[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          g[q] = (b0 + q < B) ? *reinterpret_cast<const float4*>(dx + (((b0 + q) * T + t) * S + s) * D + d)
+                              : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc_t.x += g[q].x; acc_t.y += g[q].y; acc_t.z += g[q].z; acc_t.w += g[q].w;
+        }
+      }
+      *reinterpret_cast<float4*>(part_pt + ((int64_t)s * T + t) * D + d) = acc_t;
+      acc_s.x += acc_t.x; acc_s.y += acc_t.y; acc_s.z += acc_t.z; acc_s.w += acc_t.w;
+    }
+    if (dps) *reinterpret_cast<float4*>(dps + (int64_t)s * D + d) = acc_s;
+  }
+}
+
+// pooled[bt] = mean_n x[bt*N + n]  (fixed order, 4-way ILP with ordered sums)
+__global__ void mean_pool_kernel(const float* __restrict__ x, int N, int D, float* __restrict__ out) {
+  const int64_t bt = blockIdx.x;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float s = 0.f;
+    const float* p = x + bt * N * D + d;
+    int n = 0;
+    for (; n + 4 <= N; n += 4) {
+      const float a = p[(int64_t)n * D], b = p[(int64_t)(n + 1) * D], c = p[(int64_t)(n + 2) * D],
+                  e = p[(int64_t)(n + 3) * D];
+      s += a; s += b; s += c; s += e;
+    }
+    for (; n < N; ++n) s += p[(int64_t)n * D];
+    out[bt * D + d] = s / (float)N;
+  }
+}
+
+// dx[bt*N + n] = dpool[bt] / N  (fp32, optional accumulate)
+__global__ void mean_pool_bwd_kernel(const float* __restrict__ dpool, int64_t rows, int N, int D,
+                                     float* __restrict__ dx) {
+  const int64_t total = rows * D;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / D;
+    const int d = (int)(e - r * D);
+    dx[e] = dpool[(r / N) * D + d] / (float)N;
+  }
+}
+
+// MSE: per-CTA partial sums of (pred - target)^2 (f64), grad = scale * 2 (pred - target) / n
+__global__ void mse_kernel(const float* __restrict__ pred, const float* __restrict__ target, int64_t n,
+                           double* __restrict__ part, float gscale, float* __restrict__ grad32,
+                           __nv_bfloat16* __restrict__ grad16) {
+  double acc = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t a = blockIdx.x * per, b = min(n, a + per);
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+    const float d = pred[i] - target[i];
+    acc += (double)(d * d);
+    const float g = gscale * (2.0f * d);
+    if (grad32) grad32[i] = g;
+    if (grad16) grad16[i] = __float2bfloat16_rn(g);
+  }
+  __shared__ double sm[256];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) t += sm[i];
+    part[blockIdx.x] = t;
+  }
+}
+
+// per-CTA f64 partial sums of x (fixed chunking)
+__global__ void sum_kernel(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+  double acc = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t a = blockIdx.x * per, b = min(n, a + per);
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) acc += (double)x[i];
+  __shared__ double sm[256];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) t += sm[i];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int nparts, double scale, float* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < nparts; ++i) t += part[i];
+    *out = (float)(t * scale);
+  }
+}
+
+// y[r][j] = sum_k x[r][k] W[k][j] + b[j]   (fp32, one thread per output, sequential k)
+__global__ void linear_f32_kernel(const float* __restrict__ x, int64_t R, int K, const float* __restrict__ W, int N,
+                                  const float* __restrict__ b, float* __restrict__ y, int accumulate) {
+  const int64_t total = R * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / N;
+    const int j = (int)(e - r * N);
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += x[r * K + k] * W[(int64_t)k * N + j];
+    if (b) s += b[j];
+    y[e] = accumulate ? y[e] + s : s;
+  }
+}
+
+// dx[r][k] = sum_j dy[r][j] W[k][j]
+__global__ void linear_f32_dx_kernel(const float* __restrict__ dy, int64_t R, int N, const float* __restrict__ W,
+                                     int K, float* __restrict__ dx, int accumulate) {
+  const int64_t total = R * K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / K;
+    const int k = (int)(e - r * K);
+    float s = 0.f;
+    for (int j = 0; j < N; ++j) s += dy[r * N + j] * W[(int64_t)k * N + j];
+    dx[e] = accumulate ? dx[e] + s : s;
+  }
+}
+
+// dW[k][j] = sum_r x[r][k] dy[r][j];  db[j] = sum_r dy[r][j]   (one thread per output, fixed order)
+__global__ void linear_f32_dw_kernel(const float* __restrict__ x, const float* __restrict__ dy, int64_t R, int K, int N,
+                                     float* __restrict__ dW, float* __restrict__ db, int accumulate) {
+  const int64_t total = (int64_t)K * N + (db ? N : 0);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < (int64_t)K * N) {
+      const int k = (int)(e / N), j = (int)(e - (int64_t)k * N);
+      float s = 0.f;
+      for (int64_t r = 0; r < R; ++r) s += x[r * K + k] * dy[r * N + j];
+      dW[e] = accumulate ? dW[e] + s : s;
+    } else {
+      const int j = (int)(e - (int64_t)K * N);
+      float s = 0.f;
+      for (int64_t r = 0; r < R; ++r) s += dy[r * N + j];
+      db[j] = accumulate ? db[j] + s : s;
+    }
+  }
+}
+
+}  // namespace jz
+
+using namespace jz;
+
+extern "C" int jz_patchify(const void* frames, int is_u8, int64_t BT, int H, int W, int C, int P, void* out_bf16,
+                           float* out_f32, jz_stream_t s) {
+  JZ_CHECK_ARG(P > 0 && H % P == 0 && W % P == 0, "geometry %dx%d not divisible by patch %d", H, W, P);
+  const int64_t total = BT * H * W * C;
+  if (total == 0) return JZ_OK;
+  patchify_kernel<<<grid_of(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      frames, is_u8, BT, H, W, C, P, reinterpret_cast<__nv_bfloat16*>(out_bf16), out_f32);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_unpatchify(const float* patches, int64_t BT, int H, int W, int C, int P, float* unit,
+                             uint8_t* frames_u8, jz_stream_t s) {
+  JZ_CHECK_ARG(P > 0 && H % P == 0 && W % P == 0, "patch grid does not match target geometry");
+  const int64_t total = BT * H * W * C;
+  if (total == 0) return JZ_OK;
+  unpatchify_kernel<<<grid_of(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(patches, BT, H, W, C, P,
+                                                                                         unit, frames_u8);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_assemble_fwd(const float* emb, const float* act, const float* pos_spatial, const float* pos_temporal,
+                               int64_t B, int T, int N, int D, int prepend, float* x, jz_stream_t s) {
+  JZ_CHECK_ARG(D % 4 == 0, "assemble: D %% 4");
+  const int64_t rows = B * T * (N + prepend);
+  if (rows == 0) return JZ_OK;
+  assemble_fwd_kernel<<<(unsigned)rows, 128, 0, reinterpret_cast<cudaStream_t>(s)>>>(emb, act, pos_spatial,
+                                                                                     pos_temporal, T, N, D, prepend, x);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int64_t jz_assemble_bwd_workspace(int64_t B, int T, int N, int D, int prepend) {
+  return (int64_t)(N + prepend) * T * D;
+}
+
+extern "C" int jz_assemble_bwd(const float* dx, int64_t B, int T, int N, int D, int prepend, void* d_emb_bf16,
+                               float* d_act, float* d_pos_spatial, float* d_pos_temporal, float* workspace,
+                               jz_stream_t s) {
+  JZ_CHECK_ARG(D % 4 == 0, "assemble_bwd: D %% 4");
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  const int S = N + prepend;
+  const int64_t rows = B * T * S;
+  if (rows == 0) return JZ_OK;
+  if (d_emb_bf16 || d_act) {
+    assemble_split_kernel<<<(unsigned)rows, 128, 0, st>>>(dx, N, D, prepend,
+                                                          reinterpret_cast<__nv_bfloat16*>(d_emb_bf16), d_act);
+    JZ_LAUNCH_CHECK();
+  }
+  if (d_pos_spatial || d_pos_temporal) {
+    pos_bwd_kernel<<<S, 128, 0, st>>>(dx, B, T, S, D, d_pos_spatial, workspace);
+    JZ_LAUNCH_CHECK();
+    if (d_pos_temporal) {
+      int rc = jz_reduce_partials(workspace, S, (int64_t)T * D, d_pos_temporal, 0, s);
+      if (rc) return rc;
+    }
+  }
+  return JZ_OK;
+}
+
+extern "C" int jz_mean_pool(const float* x, int64_t BT, int N, int D, float* out, jz_stream_t s) {
+  if (BT == 0) return JZ_OK;
+  mean_pool_kernel<<<(unsigned)BT, 128, 0, reinterpret_cast<cudaStream_t>(s)>>>(x, N, D, out);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_mean_pool_bwd(const float* dpool, int64_t BT, int N, int D, float* dx, jz_stream_t s) {
+  const int64_t n = BT * N * D;
+  if (n == 0) return JZ_OK;
+  mean_pool_bwd_kernel<<<grid_of(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(dpool, BT * N, N, D, dx);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_mse(const float* pred, const float* target, int64_t n, float grad_scale, float* loss, float* grad32,
+                      void* grad16, double* workspace, jz_stream_t s) {
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  const int parts = num_sms() * 2;
+  mse_kernel<<<parts, 256, 0, st>>>(pred, target, n, workspace, n > 0 ? grad_scale / (float)n : 0.f, grad32,
+                                    reinterpret_cast<__nv_bfloat16*>(grad16));
+  JZ_LAUNCH_CHECK();
+  sum_parts_kernel<<<1, 32, 0, st>>>(workspace, parts, n > 0 ? 1.0 / (double)n : 0.0, loss);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_sum(const float* x, int64_t n, double scale, float* out, double* workspace, jz_stream_t s) {
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  const int parts = num_sms() * 2;
+  sum_kernel<<<parts, 256, 0, st>>>(x, n, workspace);
+  JZ_LAUNCH_CHECK();
+  sum_parts_kernel<<<1, 32, 0, st>>>(workspace, parts, scale, out);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_linear_f32(const float* x, int64_t R, int K, const float* W, int N, const float* b, float* y,
+                             int accumulate, jz_stream_t s) {
+  const int64_t n = R * N;
+  if (n == 0) return JZ_OK;
+  linear_f32_kernel<<<grid_of(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, N, b, y, accumulate);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_linear_f32_bwd(const float* x, const float* dy, int64_t R, int K, int N, const float* W, float* dx,
+                                 float* dW, float* db, int accumulate, jz_stream_t s) {
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  if (dx && R * K > 0) {
+    linear_f32_dx_kernel<<<grid_of(R * K, 256), 256, 0, st>>>(dy, R, N, W, K, dx, 0);
+    JZ_LAUNCH_CHECK();
+  }
+  if (dW) {
+    const int64_t n = (int64_t)K * N + (db ? N : 0);
+    linear_f32_dw_kernel<<<grid_of(n, 128), 128, 0, st>>>(x, dy, R, K, N, dW, db, accumulate);
+    JZ_LAUNCH_CHECK();
+  }
+  return JZ_OK;
+}

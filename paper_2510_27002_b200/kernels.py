@@ -179,14 +179,19 @@ def cast_bf16(src: torch.Tensor, dst: torch.Tensor | None = None) -> torch.Tenso
 # --------------------------------------------------------------------------
 # K2 LayerNorm
 # --------------------------------------------------------------------------
-def layernorm_fwd(x: torch.Tensor, g: torch.Tensor, b: torch.Tensor, *, skip_period: int = 0, eps: float = 1e-5):
+def layernorm_fwd(x: torch.Tensor, g: torch.Tensor, b: torch.Tensor, *, skip_period: int = 0, eps: float = 1e-5,
+                  out_f32: bool = False, out_bf16: bool = True):
+    """-> (y_bf16 or None, mean, rstd) or (y_bf16, y_f32, mean, rstd) when out_f32."""
     rows, D = x.shape
     out_rows = rows - (rows // skip_period if skip_period else 0)
-    y = torch.empty(out_rows, D, dtype=BF16, device=x.device)
+    y = torch.empty(out_rows, D, dtype=BF16, device=x.device) if out_bf16 else None
+    y32 = torch.empty(out_rows, D, dtype=F32, device=x.device) if out_f32 else None
     mean = torch.empty(rows, dtype=F32, device=x.device)
     rstd = torch.empty(rows, dtype=F32, device=x.device)
-    L.call("jz_layernorm_fwd", x.data_ptr(), rows, D, g.data_ptr(), b.data_ptr(), eps, y.data_ptr(),
+    L.call("jz_layernorm_fwd", x.data_ptr(), rows, D, g.data_ptr(), b.data_ptr(), eps, _p(y), _p(y32),
            mean.data_ptr(), rstd.data_ptr(), skip_period, _s())
+    if out_f32:
+        return y, y32, mean, rstd
     return y, mean, rstd
 
 
@@ -299,3 +304,102 @@ def finite_check(g: torch.Tensor, flag: torch.Tensor) -> None:
 def adamw(p, g, m, v, *, lr, b1, b2, omb1, omb2, bc1, bc2, eps, lrwd, flag=None) -> None:
     L.call("jz_adamw_step", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(), lr, b1, b2, omb1,
            omb2, bc1, bc2, eps, lrwd, _p(flag), _s())
+
+
+# --------------------------------------------------------------------------
+# tokenizer / LAM side
+# --------------------------------------------------------------------------
+def patchify(frames: torch.Tensor, P: int, *, bf16=True, f32=False):
+    """frames uint8 or fp32 (BT, H, W, C) -> (patches bf16 [BT*N, P*P*C] or None, fp32 or None)."""
+    BT, H, W, C = frames.shape
+    N, PD = (H // P) * (W // P), P * P * C
+    o16 = torch.empty(BT * N, PD, dtype=BF16, device=frames.device) if bf16 else None
+    o32 = torch.empty(BT * N, PD, dtype=F32, device=frames.device) if f32 else None
+    L.call("jz_patchify", frames.data_ptr(), int(frames.dtype == torch.uint8), BT, H, W, C, P, _p(o16), _p(o32), _s())
+    return o16, o32
+
+
+def unpatchify(patches: torch.Tensor, BT: int, H: int, W: int, C: int, P: int, *, unit=True, u8=False):
+    un = torch.empty(BT, H, W, C, dtype=F32, device=patches.device) if unit else None
+    fr = torch.empty(BT, H, W, C, dtype=torch.uint8, device=patches.device) if u8 else None
+    L.call("jz_unpatchify", patches.data_ptr(), BT, H, W, C, P, _p(un), _p(fr), _s())
+    return un, fr
+
+
+def assemble_fwd(emb, act, ps, pt, *, B, T, N, D, prepend):
+    S = N + (1 if prepend else 0)
+    x = torch.empty(B * T * S, D, dtype=F32, device=ps.device)
+    L.call("jz_assemble_fwd", emb.data_ptr(), _p(act), ps.data_ptr(), pt.data_ptr(), B, T, N, D, int(prepend),
+           x.data_ptr(), _s())
+    return x
+
+
+def assemble_bwd(dx, *, B, T, N, D, prepend, d_emb=None, d_act=None, d_ps=None, d_pt=None):
+    nws = L.load().jz_assemble_bwd_workspace(B, T, N, D, int(prepend))
+    ws = scratch("assemble_ws", nws)
+    L.call("jz_assemble_bwd", dx.data_ptr(), B, T, N, D, int(prepend), _p(d_emb), _p(d_act), _p(d_ps), _p(d_pt),
+           ws.data_ptr(), _s())
+
+
+def mean_pool(x, BT, N, D):
+    out = torch.empty(BT, D, dtype=F32, device=x.device)
+    L.call("jz_mean_pool", x.data_ptr(), BT, N, D, out.data_ptr(), _s())
+    return out
+
+
+def mean_pool_bwd(dpool, BT, N, D):
+    dx = torch.empty(BT * N, D, dtype=F32, device=dpool.device)
+    L.call("jz_mean_pool_bwd", dpool.data_ptr(), BT, N, D, dx.data_ptr(), _s())
+    return dx
+
+
+def mse(pred, target, *, grad_scale=1.0, grad32=False, grad16=False):
+    n = pred.numel()
+    loss = torch.empty((), dtype=F32, device=pred.device)
+    g32 = torch.empty_like(pred) if grad32 else None
+    g16 = torch.empty(pred.shape, dtype=BF16, device=pred.device) if grad16 else None
+    ws = scratch("mse_ws", 4 * num_sms(), dtype=torch.float64)
+    L.call("jz_mse", pred.data_ptr(), target.data_ptr(), n, float(grad_scale), loss.data_ptr(), _p(g32), _p(g16),
+           ws.data_ptr(), _s())
+    return loss, g32, g16
+
+
+def linear_f32(x, W, b=None, out=None, accumulate=False):
+    R, Kd = x.shape
+    N = W.shape[1]
+    if out is None:
+        out = torch.empty(R, N, dtype=F32, device=x.device)
+    L.call("jz_linear_f32", x.data_ptr(), R, Kd, W.data_ptr(), N, _p(b), out.data_ptr(), int(accumulate), _s())
+    return out
+
+
+def linear_f32_bwd(x, dy, W, *, dx=None, dW=None, db=None, accumulate=False):
+    R, Kd = x.shape
+    N = W.shape[1]
+    L.call("jz_linear_f32_bwd", x.data_ptr(), dy.data_ptr(), R, Kd, N, W.data_ptr(), _p(dx), _p(dW), _p(db),
+           int(accumulate), _s())
+
+
+def vq_fwd(z: torch.Tensor, codebook: torch.Tensor):
+    """z f32 [rows, dz] -> (idx int64 [rows], zq_st f32 [rows, dz], row_sq f32 [rows])."""
+    rows, dz = z.shape
+    idx = torch.empty(rows, dtype=torch.int64, device=z.device)
+    zq = torch.empty_like(z)
+    sq = torch.empty(rows, dtype=F32, device=z.device)
+    L.call("jz_vq_fwd", z.data_ptr(), rows, dz, codebook.data_ptr(), codebook.shape[0], idx.data_ptr(),
+           zq.data_ptr(), sq.data_ptr(), _s())
+    return idx, zq, sq
+
+
+def vq_bwd(z, codebook, idx, g_zq_st, *, commit_coef, cb_coef, dz_out=None, dcodebook=None):
+    rows, dz = z.shape
+    L.call("jz_vq_bwd", z.data_ptr(), codebook.data_ptr(), idx.data_ptr(), _p(g_zq_st), rows, dz, codebook.shape[0],
+           float(commit_coef), float(cb_coef), _p(dz_out), _p(dcodebook), _s())
+
+
+def sum_scaled(x: torch.Tensor, scale: float) -> torch.Tensor:
+    """Deterministic fp64-accumulated scale * sum(x) of a device fp32 tensor -> fp32 device scalar."""
+    out = torch.empty((), dtype=F32, device=x.device)
+    ws = scratch("sum_ws", 4 * num_sms(), dtype=torch.float64)
+    L.call("jz_sum", x.data_ptr(), x.numel(), float(scale), out.data_ptr(), ws.data_ptr(), _s())
+    return out

@@ -116,10 +116,11 @@ def _shadows(P: dict, cfg: StConfig, prefix: str) -> list:
 
 
 def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, T: int, S: int,
-               final_skip: bool = False, save: bool = True):
+               final_skip: bool = False, save: bool = True, final_f32: bool = False, final_bf16: bool = True):
     """x f32 [B*T*S, D] (consumed as the residual stream).
 
-    Returns (y bf16 [rows, D], ctx); y drops the s=0 rows when final_skip.
+    Returns (y, ctx): y is the final-LN output, bf16 [rows, D] (or (bf16|None, f32) when
+    final_f32); rows drop the s=0 action-token rows when final_skip.
     """
     check_supported(cfg, S, T)
     H = cfg.heads
@@ -150,8 +151,13 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
                      ao2=ao2, lse_t=lse_t, x2=x2, xn3=xn3, m3=m3, r3=r3, h=h, hpre=hpre)
             blocks_ctx.append(c)
         x = x3
-    y, mf, rf = K.layernorm_fwd(x, P[f"{prefix}.final_ln.g"].data, P[f"{prefix}.final_ln.b"].data,
-                                skip_period=S if final_skip else 0)
+    if final_f32:
+        y16, y32, mf, rf = K.layernorm_fwd(x, P[f"{prefix}.final_ln.g"].data, P[f"{prefix}.final_ln.b"].data,
+                                           skip_period=S if final_skip else 0, out_f32=True, out_bf16=final_bf16)
+        y = (y16, y32)
+    else:
+        y, mf, rf = K.layernorm_fwd(x, P[f"{prefix}.final_ln.g"].data, P[f"{prefix}.final_ln.b"].data,
+                                    skip_period=S if final_skip else 0)
     ctx = None
     if save:
         ctx = dict(blocks=blocks_ctx, shadows=sh, x_final=x, mf=mf, rf=rf, B=B, T=T, S=S,
@@ -160,7 +166,7 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
 
 
 def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, prefix: str,
-                on_done=None) -> torch.Tensor:
+                on_done=None, want_dx_bf16: bool = False):
     """dy: f32 gradient of the final-LN output (compacted like y).  Writes G[...]; returns dx f32 [rows, D].
 
     on_done(name) is called (stream-ordered) as soon as a parameter group's gradients are final:
@@ -215,10 +221,12 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_F32, out=dtmp)
         prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
         K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
-                        dres_bf16=dres_b if i > 0 else None, dgamma=G[f"{base}.spatial.ln.g"],
+                        dres_bf16=dres_b if (i > 0 or want_dx_bf16) else None, dgamma=G[f"{base}.spatial.ln.g"],
                         dbeta=G[f"{base}.spatial.ln.b"], dbias=prev_bias)
         if on_done is not None:
             on_done(f"block{i}")
+    if want_dx_bf16:
+        return dres, dres_b
     return dres
 
 
