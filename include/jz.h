@@ -257,6 +257,37 @@ JZ_API int jz_vq_bwd(const float* z, const float* codebook, const int64_t* idx, 
                      int dz, int K, float commit_coef, float cb_coef, float* dz_out, float* dcodebook,
                      jz_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * K12 KV-cached MaskGIT decoding (dynamics.py:156-194 computes the full clip's
+ * logits every step; by temporal causality only the last frame changes).
+ * jz_dyn_embed_frame: one frame's tokens (B, N) -> x [B*(N+1), D] with the
+ *   action token from cond [B, dl]; known[b,n] == 0 selects the mask token
+ *   (known == NULL: all known); pos_temporal_row = pos_temporal + t*D.
+ * jz_attn_temporal_decode: temporal attention of the frame (qkv [B*S, 3D]) over
+ *   cache [B, Tmax, S, 2D] (k|v, bf16) frames 0..t-1 plus itself; append writes
+ *   its k, v into cache[:, t].
+ * jz_kv_fill: cache[:, t0 .. t0+T) = k|v of qkv rows (b, tau, s).
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_dyn_embed_frame(const int64_t* tokens, const uint8_t* known, const float* cond,
+                              const float* token_embed, const float* mask_token, const float* action_w,
+                              const float* action_b, const float* pos_spatial, const float* pos_temporal_row,
+                              int64_t B, int N, int D, int dl, int K, float* x, jz_stream_t stream);
+JZ_API int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, int t, int Tmax, int S, int H,
+                                   int append, void* out, jz_stream_t stream);
+JZ_API int jz_kv_fill(const void* qkv, void* cache, int64_t B, int T, int t0, int Tmax, int S, int D,
+                      jz_stream_t stream);
+
+/* K11 one MaskGIT refinement step (dynamics.py:177-192 with _sample_with_confidence,
+ * dynamics.py:198-217): for each (b, n): softmax(logits/T), u = draw (draw_base +
+ * b*N + n) of the numpy Philox state (counter/key/buffer/pos as in jz_philox_mask),
+ * sampled = #(u > cdf) clamped to K-1 (argmax when T < 1e-6, no draw), conf =
+ * p[sampled]; cur = known ? cur : sampled; conf = known ? +inf : conf; then the
+ * n_keep best (conf desc, position asc) of each row become known. */
+JZ_API int jz_maskgit_step(const float* logits, int64_t B, int N, int K, float temperature,
+                           const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4,
+                           int buffer_pos, uint64_t draw_base, int n_keep, int64_t* cur, uint8_t* known,
+                           float* conf, jz_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

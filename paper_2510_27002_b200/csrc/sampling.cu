@@ -1,0 +1,299 @@
+// Autoregressive MaskGIT sampling on device (dynamics.py:156-260):
+//   K12 KV-cached last-frame forward: single-frame embedding with per-sample
+//       conditioning, temporal attention of the new frame over cached per-layer K/V
+//       (exact: spatial attention is intra-frame and temporal attention is causal, so
+//       frames < t never change while frame t is refined), cache fill/append
+//   K11 MaskGIT sampler step (_sample_with_confidence, dynamics.py:198-217, and the
+//       known/confidence update + stable top-n_keep of dynamics.py:185-192):
+//       temperature softmax over K codes, inverse-CDF draw with the caller's numpy
+//       Philox stream continued on device, confidence of the sampled code, then
+//       known positions get +inf and the n_keep best (conf desc, position asc) become known.
+#include "common.h"
+#include "philox.cuh"
+#include "ptx.cuh"
+
+namespace jz {
+
+// ---------------------------------------------------------------------------
+// single-frame embedding: x[b, s] for frame index t (pos_temporal row pt_row)
+//   s = 0 -> (cond[b] Wa + ba) + ps[0] + pt;  s >= 1 -> (known ? E[tok] : mt) + ps[s] + pt
+//   (known == NULL: every token known)
+// ---------------------------------------------------------------------------
+__global__ void embed_frame_kernel(const int64_t* __restrict__ tokens, const uint8_t* __restrict__ known,
+                                   const float* __restrict__ cond, const float* __restrict__ E,
+                                   const float* __restrict__ mt, const float* __restrict__ Wa,
+                                   const float* __restrict__ ba, const float* __restrict__ ps,
+                                   const float* __restrict__ pt_row, int N, int D, int dl, int K,
+                                   float* __restrict__ x) {
+  const int S = N + 1;
+  const int64_t row = blockIdx.x;
+  const int s = (int)(row % S);
+  const int64_t b = row / S;
+  const int d = threadIdx.x * 4;
+  if (d >= D) return;
+  float4 v;
+  if (s == 0) {
+    float4 acc = make_float4(0, 0, 0, 0);
+    for (int i = 0; i < dl; ++i) {
+      const float c = cond[b * dl + i];
+      const float4 w = *reinterpret_cast<const float4*>(Wa + (int64_t)i * D + d);
+      acc.x += c * w.x; acc.y += c * w.y; acc.z += c * w.z; acc.w += c * w.w;
+    }
+    const float4 bb = *reinterpret_cast<const float4*>(ba + d);
+    v = make_float4(acc.x + bb.x, acc.y + bb.y, acc.z + bb.z, acc.w + bb.w);
+  } else {
+    const int64_t pos = b * N + (s - 1);
+    if (known && !known[pos]) {
+      v = *reinterpret_cast<const float4*>(mt + d);
+    } else {
+      int64_t tok = tokens[pos];
+      tok = tok < 0 ? 0 : (tok >= K ? K - 1 : tok);
+      v = *reinterpret_cast<const float4*>(E + tok * D + d);
+    }
+  }
+  const float4 p1 = *reinterpret_cast<const float4*>(ps + (int64_t)s * D + d);
+  const float4 p2 = *reinterpret_cast<const float4*>(pt_row + d);
+  v.x = (v.x + p1.x) + p2.x; v.y = (v.y + p1.y) + p2.y;
+  v.z = (v.z + p1.z) + p2.z; v.w = (v.w + p1.w) + p2.w;
+  *reinterpret_cast<float4*>(x + row * D + d) = v;
+}
+
+// ---------------------------------------------------------------------------
+// temporal attention of frame t over cache[:, 0..t-1] + itself.  One warp per (b, s, h),
+// lane holds head dims 2*lane, 2*lane+1.  cache [B, Tmax, S, 2D] bf16 (k | v).
+// append: also write the current k, v into cache[:, t].
+// ---------------------------------------------------------------------------
+__global__ void temporal_decode_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ cache,
+                                       int64_t B, int t, int Tmax, int S, int H, int append,
+                                       __nv_bfloat16* __restrict__ out) {
+  const int D = H * 64;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gw >= B * S * H) return;
+  const int h = (int)(gw % H);
+  const int64_t bs = gw / H;
+  const int s = (int)(bs % S);
+  const int64_t b = bs / S;
+  const __nv_bfloat16* row = qkv + bs * 3 * D;
+  const float2 q = unpack_bf16(*reinterpret_cast<const uint32_t*>(row + h * 64 + 2 * lane));
+  const uint32_t kc = *reinterpret_cast<const uint32_t*>(row + D + h * 64 + 2 * lane);
+  const uint32_t vc = *reinterpret_cast<const uint32_t*>(row + 2 * D + h * 64 + 2 * lane);
+  float sc[17];
+  float mx = -INFINITY;
+  for (int tau = 0; tau <= t; ++tau) {
+    float2 k;
+    if (tau < t) {
+      const __nv_bfloat16* cr = cache + (((b * Tmax + tau) * S + s) * 2 * D);
+      k = unpack_bf16(*reinterpret_cast<const uint32_t*>(cr + h * 64 + 2 * lane));
+    } else {
+      k = unpack_bf16(kc);
+    }
+    const float a = warp_sum(q.x * k.x + q.y * k.y) * 0.125f;
+    sc[tau] = a;
+    mx = fmaxf(mx, a);
+  }
+  float l = 0.f, o0 = 0.f, o1 = 0.f;
+  for (int tau = 0; tau <= t; ++tau) {
+    const float p = __expf(sc[tau] - mx);
+    l += p;
+    float2 v;
+    if (tau < t) {
+      const __nv_bfloat16* cr = cache + (((b * Tmax + tau) * S + s) * 2 * D);
+      v = unpack_bf16(*reinterpret_cast<const uint32_t*>(cr + D + h * 64 + 2 * lane));
+    } else {
+      v = unpack_bf16(vc);
+    }
+    o0 += p * v.x;
+    o1 += p * v.y;
+  }
+  *reinterpret_cast<uint32_t*>(out + bs * D + h * 64 + 2 * lane) = pack_bf16(o0 / l, o1 / l);
+  if (append) {
+    __nv_bfloat16* cw = cache + (((b * Tmax + t) * S + s) * 2 * D);
+    *reinterpret_cast<uint32_t*>(cw + h * 64 + 2 * lane) = kc;
+    *reinterpret_cast<uint32_t*>(cw + D + h * 64 + 2 * lane) = vc;
+  }
+}
+
+// cache[b, t0 + tau, s, :] = (k | v) of qkv rows (b, tau, s) for tau < T
+__global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ cache, int64_t B,
+                               int T, int t0, int Tmax, int S, int D) {
+  const int64_t rows = B * T * S;
+  const int c8 = 2 * D / 8;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * c8;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / c8;
+    const int c = (int)(e - r * c8);
+    const int s = (int)(r % S);
+    const int64_t bt = r / S;
+    const int tau = (int)(bt % T);
+    const int64_t b = bt / T;
+    const uint4 w = reinterpret_cast<const uint4*>(qkv + r * 3 * D + D)[c];
+    reinterpret_cast<uint4*>(cache + (((b * Tmax + t0 + tau) * S + s) * 2 * D))[c] = w;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K11a: per (b, n) row of K logits: temperature softmax, inverse-CDF sample with
+// u = draw (draw_base + b*N + n) of the Philox state, confidence; then the
+// known/cur/conf update.  One warp per row; lane owns K/32 consecutive codes.
+// ---------------------------------------------------------------------------
+template <int PER>  // codes per lane
+__global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t rows, int K, float inv_temp,
+                                      int greedy, PhiloxState st, uint64_t draw_base, int64_t* __restrict__ cur,
+                                      const uint8_t* __restrict__ known, float* __restrict__ conf) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* lr = logits + r * K + lane * PER;
+  float v[PER];
+  float mx = -INFINITY, amax_v = -INFINITY;
+  int amax_i = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const float raw = lr[i];
+    v[i] = __fmul_rn(raw, inv_temp);
+    mx = fmaxf(mx, v[i]);
+    if (raw > amax_v) { amax_v = raw; amax_i = lane * PER + i; }
+  }
+  mx = warp_max(mx);
+  float local = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = __expf(v[i] - mx);
+    local += v[i];
+  }
+  const float total = warp_sum(local);
+  const float inv = 1.0f / total;
+  int sampled;
+  if (greedy) {
+    // argmax with first-index ties across lanes
+    float bv = amax_v;
+    int bi = amax_i;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    sampled = bi;
+  } else {
+    const double u = u64_to_double(philox_word(st, draw_base + (uint64_t)r));
+    // exclusive prefix of lane sums (probabilities), then the count of cdf < u inside the lane
+    float lsum = local * inv;
+    float pre = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    float cdf = pre - lsum;
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      cdf += v[i] * inv;
+      cnt += ((double)cdf < u) ? 1 : 0;
+    }
+    cnt = (int)warp_sum((float)cnt);
+    sampled = cnt < K - 1 ? cnt : K - 1;
+  }
+  // confidence = probs[sampled] from the very exponentials the CDF used (no recomputation)
+  float mine = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (lane * PER + i == sampled) mine = v[i];
+  const float p = __shfl_sync(0xffffffffu, mine, sampled / PER) * inv;
+  if (lane == 0) {
+    const bool kn = known[r] != 0;
+    if (!kn) cur[r] = sampled;
+    conf[r] = kn ? INFINITY : p;
+  }
+}
+
+// K11b: per batch row, the n_keep highest-confidence positions (ties by position) become known.
+__global__ void maskgit_select_kernel(const float* __restrict__ conf, int N, int n_keep, uint8_t* __restrict__ known) {
+  extern __shared__ float sconf[];
+  const int64_t b = blockIdx.x;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) sconf[i] = conf[b * N + i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const float ci = sconf[i];
+    int rank = 0;
+    for (int j = 0; j < N; ++j) {
+      const float cj = sconf[j];
+      rank += (cj > ci || (cj == ci && j < i)) ? 1 : 0;
+    }
+    known[b * N + i] = rank < n_keep ? 1 : 0;
+  }
+}
+
+}  // namespace jz
+
+using namespace jz;
+
+extern "C" int jz_dyn_embed_frame(const int64_t* tokens, const uint8_t* known, const float* cond,
+                                  const float* token_embed, const float* mask_token, const float* action_w,
+                                  const float* action_b, const float* pos_spatial, const float* pos_temporal_row,
+                                  int64_t B, int N, int D, int dl, int K, float* x, jz_stream_t s) {
+  JZ_CHECK_ARG(D % 4 == 0 && D / 4 <= 1024, "embed_frame: D=%d", D);
+  if (B == 0) return JZ_OK;
+  embed_frame_kernel<<<(unsigned)(B * (N + 1)), D / 4, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      tokens, known, cond, token_embed, mask_token, action_w, action_b, pos_spatial, pos_temporal_row, N, D, dl, K, x);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, int t, int Tmax, int S, int H,
+                                       int append, void* out, jz_stream_t s) {
+  JZ_CHECK_ARG(t >= 0 && t < Tmax && t <= 16, "temporal decode: frame index %d out of range", t);
+  const int64_t warps = B * S * H;
+  if (warps == 0) return JZ_OK;
+  temporal_decode_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(cache), B, t, Tmax, S, H, append,
+      reinterpret_cast<__nv_bfloat16*>(out));
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_kv_fill(const void* qkv, void* cache, int64_t B, int T, int t0, int Tmax, int S, int D,
+                          jz_stream_t s) {
+  JZ_CHECK_ARG(t0 + T <= Tmax, "kv_fill: %d + %d frames exceed cache %d", t0, T, Tmax);
+  const int64_t n = B * T * S * (2 * D / 8);
+  if (n == 0) return JZ_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  kv_fill_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(cache), B, T, t0, Tmax, S, D);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, float temperature,
+                               const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4, int buffer_pos,
+                               uint64_t draw_base, int n_keep, int64_t* cur, uint8_t* known, float* conf,
+                               jz_stream_t s) {
+  JZ_CHECK_ARG(K % 32 == 0 && K / 32 <= 64, "maskgit: vocabulary %d unsupported (multiple of 32, <= 2048)", K);
+  JZ_CHECK_ARG(n_keep >= 0 && n_keep <= N, "maskgit: n_keep %d", n_keep);
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  PhiloxState ps;
+  for (int i = 0; i < 4; ++i) {
+    ps.ctr[i] = counter4 ? counter4[i] : 0;
+    ps.buf[i] = buffer4 ? buffer4[i] : 0;
+  }
+  ps.key[0] = key2 ? key2[0] : 0;
+  ps.key[1] = key2 ? key2[1] : 0;
+  ps.pos = buffer_pos;
+  const int greedy = temperature < 1e-6f;
+  const float inv_temp = 1.0f / fmaxf(temperature, 1e-8f);
+  const int64_t rows = B * N;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  switch (K / 32) {
+#define MS(P) case P: maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, cur, known, conf); break;
+    MS(1) MS(2) MS(4) MS(8) MS(16) MS(32) MS(64)
+#undef MS
+    default: set_error("maskgit: vocabulary %d unsupported", K); return JZ_EINVAL;
+  }
+  JZ_LAUNCH_CHECK();
+  maskgit_select_kernel<<<(unsigned)B, 256, N * sizeof(float), st>>>(conf, N, n_keep, known);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}

@@ -43,6 +43,9 @@ def _sample_with_confidence(logits: np.ndarray, temperature: float, rng: np.rand
 
 def decode_frame(model, prev_tokens, action_latents, steps: int = 25, temperature: float = 1.0,
                  rng: np.random.Generator | None = None) -> np.ndarray:
+    from .dynamics import DynamicsModel
+    if isinstance(model, DynamicsModel) and model.cfg.mode.value != "additive":
+        return decode_frame_device(model, prev_tokens, action_latents, steps, temperature, rng).cpu().numpy()
     if steps < 1:
         raise ValueError("steps must be >= 1")
     if rng is None:
@@ -75,7 +78,12 @@ def decode_frame(model, prev_tokens, action_latents, steps: int = 25, temperatur
 
 def rollout(tokenizer, dynamics, conditioning_frames, actions, horizon: int, steps: int = 25,
             temperature: float = 1.0, rng=None, source_codebook=None, prefix_action_latents=None):
-    from .tokenizer import unit_to_frames
+    from .dynamics import DynamicsModel
+    from .tokenizer import VideoTokenizer, unit_to_frames
+    if isinstance(dynamics, DynamicsModel) and isinstance(tokenizer, VideoTokenizer) \
+            and dynamics.cfg.mode.value != "additive":
+        return rollout_device(tokenizer, dynamics, conditioning_frames, actions, horizon, steps, temperature, rng,
+                              source_codebook, prefix_action_latents).cpu().numpy()
     if len(actions) < horizon:
         raise ValueError(f"need {horizon} actions, got {len(actions)}")
     n_cond = conditioning_frames.shape[1]
@@ -103,3 +111,194 @@ def rollout(tokenizer, dynamics, conditioning_frames, actions, horizon: int, ste
         tokens = np.concatenate([tokens, np.asarray(nxt)[:, None, :]], axis=1)
     unit = tokenizer.decode(tokens)
     return unit_to_frames(unit)
+
+
+# ==========================================================================
+# Device path: KV-cached MaskGIT decoding (K11 + K12)
+# ==========================================================================
+import ctypes as _C
+
+from . import _lib as _L
+from . import kernels as _K
+from .rng import PhiloxState as _PS
+from .rng import consume as _consume
+from .st import _shadows, check_supported
+
+
+def keep_counts(n: int, steps: int) -> list[int]:
+    """n_keep per step (dynamics.py:177-179), floor-maxed with the previous count (known grows)."""
+    out, prev = [], 0
+    for s in range(1, steps + 1):
+        frac = np.cos(np.pi / 2 * s / steps)
+        k = n if s == steps else min(n, int(np.ceil(n * (1.0 - frac))))
+        k = max(k, prev)
+        out.append(k)
+        prev = k
+    return out
+
+
+class FrameDecoder:
+    """Per-layer temporal K/V cache + single-frame forward of a DynamicsModel (prepend mode)."""
+
+    def __init__(self, model, B: int, t_max: int | None = None):
+        cfg = model.cfg
+        if cfg.mode.value == "additive":
+            raise ValueError("device MaskGIT decoding supports the prepended action token (prepend / ground-truth modes)")
+        self.model, self.cfg, self.B = model, cfg, B
+        self.N, self.D, self.H = cfg.patches_per_frame, cfg.model_dim, cfg.heads
+        self.S = self.N + 1
+        self.t_max = t_max or cfg.max_frames
+        check_supported(cfg.st, self.S, self.t_max)
+        dev = model.params["token_embed"].data.device
+        self.cache = [torch.empty(B, self.t_max, self.S, 2 * self.D, dtype=torch.bfloat16, device=dev)
+                      for _ in range(cfg.blocks)]
+        P = model.params
+        self.P = P
+        self.sh = _shadows(P, cfg.st, "dyn")
+        self.wl = _K.cast_bf16(P["to_logits.w"].data)
+        self.t = 0  # frames cached
+
+    def prefill(self, tokens: torch.Tensor, latents: torch.Tensor) -> None:
+        """Cache frames 0..t0-1 (tokens (B,t0,N) int64, latents (B,t0-1,dl)) — the full-clip forward of those frames."""
+        cfg, P = self.cfg, self.P
+        B, t0, N = tokens.shape
+        err = torch.zeros((), dtype=torch.int32, device=tokens.device)
+        x = _K.dyn_embed_fwd(tokens, None, latents.contiguous(), {k: v.data for k, v in P.items()}, B=B, T=t0, N=N,
+                             D=self.D, dl=cfg.action_latent_dim, K=cfg.token_codes, prepend=True, err=err)
+        for i in range(cfg.blocks):
+            x = self._block(i, x, B=B, T=t0, temporal=("full", None))
+        self.t = t0
+
+    def _block(self, i, x, *, B, T, temporal):
+        P, w, base = self.P, self.sh[i], f"dyn.block{i}"
+        H, S = self.H, self.S
+        xn, _, _ = _K.layernorm_fwd(x, P[f"{base}.spatial.ln.g"].data, P[f"{base}.spatial.ln.b"].data)
+        qkv = _K.linear_fwd(xn, w["spatial.wqkv"], w["spatial.bqkv"])
+        ao, _, _ = _K.attn_spatial_fwd(qkv, B * T, S, H, keep_f32=False)
+        x1 = _K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=_L.EPI_RESID, aux=x)
+        xn2, _, _ = _K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
+        qkv2 = _K.linear_fwd(xn2, w["temporal.wqkv"], w["temporal.bqkv"])
+        mode, arg = temporal
+        if mode == "full":
+            ao2, _ = _K.attn_temporal_fwd(qkv2, B, T, S, H)
+            _L.call("jz_kv_fill", qkv2.data_ptr(), self.cache[i].data_ptr(), B, T, 0, self.t_max, S, self.D,
+                    _L.stream_ptr())
+        else:
+            t, append = arg
+            ao2 = torch.empty(B * S, self.D, dtype=torch.bfloat16, device=x.device)
+            _L.call("jz_attn_temporal_decode", qkv2.data_ptr(), self.cache[i].data_ptr(), B, t, self.t_max, S, H,
+                    int(append), ao2.data_ptr(), _L.stream_ptr())
+        x2 = _K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=_L.EPI_RESID, aux=x1)
+        xn3, _, _ = _K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
+        hpre = torch.empty(xn3.shape[0], self.cfg.ffn_dim, dtype=torch.bfloat16, device=x.device)
+        h = _K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=_L.EPI_GELU, out2=hpre)
+        return _K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=_L.EPI_RESID, aux=x2)
+
+    def frame(self, tokens: torch.Tensor, known: torch.Tensor | None, cond: torch.Tensor, *, append: bool,
+              logits: bool = True):
+        """Forward frame index self.t ((B,N) tokens; known (B,N) u8 or None=all known) over the cache."""
+        cfg, P = self.cfg, self.P
+        B, N, D, t = self.B, self.N, self.D, self.t
+        x = torch.empty(B * self.S, D, dtype=torch.float32, device=tokens.device)
+        pt_row = P["pos_temporal"].data[t]
+        _L.call("jz_dyn_embed_frame", tokens.data_ptr(), None if known is None else known.data_ptr(),
+                cond.data_ptr(), P["token_embed"].data.data_ptr(), P["mask_token"].data.data_ptr(),
+                P["action_proj.w"].data.data_ptr(), P["action_proj.b"].data.data_ptr(),
+                P["pos_spatial"].data.data_ptr(), pt_row.data_ptr(), B, N, D, cfg.action_latent_dim,
+                cfg.token_codes, x.data_ptr(), _L.stream_ptr())
+        for i in range(cfg.blocks):
+            x = self._block(i, x, B=B, T=1, temporal=("decode", (t, append)))
+        if append:
+            self.t = t + 1
+        if not logits:
+            return None
+        y, _, _ = _K.layernorm_fwd(x, P["dyn.final_ln.g"].data, P["dyn.final_ln.b"].data, skip_period=self.S)
+        return _K.linear_fwd(y, self.wl, P["to_logits.b"].data, epilogue=_L.EPI_F32)
+
+    def decode(self, cond: torch.Tensor, steps: int, temperature: float, rng: np.random.Generator) -> torch.Tensor:
+        """MaskGIT-decode frame self.t; returns cur (B, N) int64 in HBM and appends it to the cache."""
+        cfg = self.cfg
+        B, N, K = self.B, self.N, cfg.token_codes
+        dev = cond.device
+        cur = torch.zeros(B, N, dtype=torch.int64, device=dev)
+        known = torch.zeros(B, N, dtype=torch.uint8, device=dev)
+        conf = torch.empty(B, N, dtype=torch.float32, device=dev)
+        greedy = temperature < 1e-6
+        st = _consume(rng, steps * B * N) if not greedy else _PS([0, 0, 0, 0], (0, 0), [0, 0, 0, 0], 4)
+        ctr = (_C.c_uint64 * 4)(*st.counter)
+        key = (_C.c_uint64 * 2)(*st.key)
+        buf = (_C.c_uint64 * 4)(*st.buffer)
+        for s, n_keep in enumerate(keep_counts(N, steps)):
+            logits = self.frame(cur, known, cond, append=False)
+            _L.call("jz_maskgit_step", logits.data_ptr(), B, N, K, float(temperature), _C.addressof(ctr),
+                    _C.addressof(key), _C.addressof(buf), st.buffer_pos, s * B * N, n_keep, cur.data_ptr(),
+                    known.data_ptr(), conf.data_ptr(), _L.stream_ptr())
+        self.frame(cur, None, cond, append=True, logits=False)
+        return cur
+
+
+def _dev_latents(model, action_latents) -> torch.Tensor:
+    lat = action_latents.data if isinstance(action_latents, Tensor) else action_latents
+    if not isinstance(lat, torch.Tensor):
+        lat = torch.as_tensor(np.asarray(lat, dtype=np.float32))
+    return lat.to(model.params["token_embed"].data.device, torch.float32).contiguous()
+
+
+def decode_frame_device(model, prev_tokens, action_latents, steps: int = 25, temperature: float = 1.0,
+                        rng: np.random.Generator | None = None) -> torch.Tensor:
+    """dynamics.py:156-194 on device: prefill frames 0..t-1, then 'steps' KV-cached refinements."""
+    if steps < 1:
+        raise ValueError("steps must be >= 1")
+    if rng is None:
+        rng = stream(0, "maskgit-decode")
+    tok = prev_tokens if isinstance(prev_tokens, torch.Tensor) else torch.as_tensor(np.asarray(prev_tokens))
+    dev = model.params["token_embed"].data.device
+    tok = tok.to(dev, torch.int64).contiguous()
+    b, t_prev, n = tok.shape
+    lat = _dev_latents(model, action_latents)
+    if lat.shape[1] != t_prev:
+        raise ValueError(f"need {t_prev} action latents, got {lat.shape[1]}")
+    dec = FrameDecoder(model, b, max(model.cfg.max_frames, t_prev + 1))
+    dec.prefill(tok, lat[:, : t_prev - 1])
+    return dec.decode(lat[:, t_prev - 1].contiguous(), steps, temperature, rng)
+
+
+def rollout_device(tokenizer, dynamics, conditioning_frames, actions, horizon: int, steps: int = 25,
+                   temperature: float = 1.0, rng=None, source_codebook=None, prefix_action_latents=None,
+                   return_tokens: bool = False):
+    """dynamics.py:220-260 fully on device; returns uint8 frames (B, n_cond+horizon, H, W, C) in HBM."""
+    if len(actions) < horizon:
+        raise ValueError(f"need {horizon} actions, got {len(actions)}")
+    n_cond = conditioning_frames.shape[1]
+    if n_cond + horizon > dynamics.cfg.max_frames:
+        raise ValueError("horizon exceeds the model's maximum clip length")
+    if rng is None:
+        rng = stream(0, "rollout")
+    tokens = tokenizer.encode_device(conditioning_frames)
+    b = tokens.shape[0]
+    dlat = dynamics.cfg.action_latent_dim
+    dev = tokens.device
+    if prefix_action_latents is not None:
+        history = _dev_latents(dynamics, prefix_action_latents)
+    else:
+        null = dynamics.params["null_action"].data.reshape(1, 1, dlat)
+        history = torch.zeros((b, n_cond - 1, dlat), dtype=torch.float32, device=dev) + null
+    dec = FrameDecoder(dynamics, b, dynamics.cfg.max_frames)
+    dec.prefill(tokens, history)
+    frames_tok = [tokens]
+    for step in range(horizon):
+        action = actions[step]
+        if isinstance(action, Tensor):
+            lat = action.data.reshape(b, dlat).float()
+        else:
+            lat = dynamics.action_latents_for(np.asarray(action).reshape(b, 1), source_codebook).data.reshape(b, dlat)
+        nxt = dec.decode(lat.contiguous(), steps, temperature, rng)
+        frames_tok.append(nxt[:, None, :])
+    all_tok = torch.cat(frames_tok, dim=1)
+    unit = tokenizer.decode_device(all_tok)
+    cfg = tokenizer.cfg
+    B, T = all_tok.shape[0], all_tok.shape[1]
+    _, p32 = _K.patchify(unit.view(B * T, cfg.height, cfg.width, cfg.channels), cfg.patch, bf16=False, f32=True)
+    _, u8 = _K.unpatchify(p32, B * T, cfg.height, cfg.width, cfg.channels, cfg.patch, unit=False, u8=True)
+    out = u8.view(B, T, cfg.height, cfg.width, cfg.channels)
+    return (out, all_tok) if return_tokens else out
