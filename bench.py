@@ -110,6 +110,71 @@ def cpu_baseline(steps: int = 2) -> dict:
                       f"B=1 (16 frames), {steps} timed steps after 1 warm-up, {r['seconds_per_step']:.2f} s/step"}
 
 
+def _events_ms(fn, reps: int = 1) -> float:
+    import torch
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def secondary_configs(dev) -> dict:
+    """BASELINE configs other than the headline: C5 sampling (generated frames/s), C2 LAM train
+    step and C1 tokenizer forward (frames/s), jasmine-base dims at patch 4, synthetic data."""
+    import numpy as np
+    import torch
+
+    from paper_2510_27002_b200.dynamics import DynamicsConfig, DynamicsModel
+    from paper_2510_27002_b200.lam import LamConfig, LatentActionModel
+    from paper_2510_27002_b200.rng import stream
+    from paper_2510_27002_b200.sampling import rollout_device
+    from paper_2510_27002_b200.tokenizer import TokenizerConfig, VideoTokenizer
+
+    out = {}
+    tok = VideoTokenizer(TokenizerConfig(patch=4, codes=1024, latent_dim=32), seed=0)
+    dyn = DynamicsModel(DynamicsConfig(patches_per_frame=PATCHES, max_frames=FRAMES_T), seed=0)
+    lam_cb = torch.as_tensor(stream(2, "bench-lam-codebook").uniform(-1 / 6, 1 / 6, size=(6, DLAT)).astype(np.float32),
+                             device=dev)
+    # C5: batch 64, 4 conditioning frames -> 12 generated, 25 MaskGIT steps, temperature 1
+    B5 = 64
+    cond = torch.as_tensor(stream(5, "cond-frames").integers(0, 256, size=(B5, 4, 64, 64, 3)).astype(np.uint8),
+                           device=dev)
+    acts = [stream(5, "acts", i).integers(0, 6, size=(B5,)) for i in range(12)]
+    rollout_device(tok, dyn, cond, acts, horizon=1, steps=2, rng=stream(0, "roll-warm"), source_codebook=lam_cb)
+    ms = _events_ms(lambda: rollout_device(tok, dyn, cond, acts, horizon=12, steps=25, rng=stream(0, "roll"),
+                                           source_codebook=lam_cb))
+    gen = B5 * 12
+    out["sample"] = {"metric": "sample frames/sec (generated)", "value": round(gen / (ms / 1e3), 1),
+                     "unit": "frames/s", "ms_per_rollout": round(ms, 1),
+                     "config": "C5: batch 64, 4 cond -> 12 generated frames, 25 MaskGIT steps, T=1, KV-cached "
+                               "last-frame forward, tokenizer encode+decode included",
+                     "algorithmic_tflops": round(351.2e9 * gen / (ms / 1e3) / 1e12, 1)}
+    # C2: LAM train step, B=8, T=16
+    lam = LatentActionModel(LamConfig(patch=4, codes=6, latent_dim=32), seed=0)
+    fr8 = torch.as_tensor(stream(0, "bench-frames").integers(0, 256, size=(8, FRAMES_T, 64, 64, 3)).astype(np.uint8),
+                          device=dev)
+
+    def lam_step():
+        _, _, losses = lam.forward(fr8)
+        losses["total"].backward()
+
+    lam_step()
+    ms2 = _events_ms(lam_step, reps=3)
+    out["lam_train"] = {"metric": "LAM train frames/sec", "value": round(8 * FRAMES_T / (ms2 / 1e3), 1),
+                        "unit": "frames/s", "ms_per_step": round(ms2, 2), "config": "C2: B=8, T=16, 6 codes"}
+    # C1: tokenizer forward (encode + VQ + decode), B=2
+    fr2 = fr8[:2]
+    tok.forward(fr2)
+    ms1 = _events_ms(lambda: tok.forward(fr2), reps=5)
+    out["tokenizer_fwd"] = {"metric": "tokenizer fwd+quantize frames/sec", "value": round(2 * FRAMES_T / (ms1 / 1e3), 1),
+                            "unit": "frames/s", "ms_per_step": round(ms1, 2), "config": "C1: B=2, T=16, 1024 codes"}
+    return out
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -138,6 +203,7 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=36, help="per-GPU batch (clips of 16 frames)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C1/C2/C5 secondary measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -237,6 +303,14 @@ def main() -> None:
     e2e_value = frames_per_step / (ms_e2e / 1e3)
     h2d = tokens_h.numel() * tokens_h.element_size() + lat_h.numel() * lat_h.element_size()
 
+    # ---- secondary BASELINE configs (rank 0, N=1): C5 sampling, C2 LAM step, C1 tokenizer fwd ----
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        try:
+            extra = secondary_configs(dev)
+        except Exception as exc:  # never sink the headline line
+            extra = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+
     peaks = _peaks()
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = None
@@ -274,7 +348,7 @@ def main() -> None:
                 "roofline": roofline,
                 "model_tflops": round(step_flops / (ms / 1e3) / 1e12, 1),
                 "model_flops_frac": round(step_flops / (ms / 1e3) / 1e12 / peaks["bf16_sustained"], 4),
-                "cpu_baseline": cpu, "clocks": clk, "loss": round(loss_val, 5)}
+                "cpu_baseline": cpu, "clocks": clk, "loss": round(loss_val, 5), **extra}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

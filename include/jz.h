@@ -262,18 +262,20 @@ JZ_API int jz_vq_bwd(const float* z, const float* codebook, const int64_t* idx, 
  * logits every step; by temporal causality only the last frame changes).
  * jz_dyn_embed_frame: one frame's tokens (B, N) -> x [B*(N+1), D] with the
  *   action token from cond [B, dl]; known[b,n] == 0 selects the mask token
- *   (known == NULL: all known); pos_temporal_row = pos_temporal + t*D.
+ *   (known == NULL: all known); pos_temporal_row = pos_temporal + t*D, or, when
+ *   dev_t != NULL, pos_temporal + (*dev_t)*D (frame index read on device).
  * jz_attn_temporal_decode: temporal attention of the frame (qkv [B*S, 3D]) over
  *   cache [B, Tmax, S, 2D] (k|v, bf16) frames 0..t-1 plus itself; append writes
- *   its k, v into cache[:, t].
+ *   its k, v into cache[:, t]; dev_t != NULL overrides t from device memory.
  * jz_kv_fill: cache[:, t0 .. t0+T) = k|v of qkv rows (b, tau, s).
  * ---------------------------------------------------------------------- */
 JZ_API int jz_dyn_embed_frame(const int64_t* tokens, const uint8_t* known, const float* cond,
                               const float* token_embed, const float* mask_token, const float* action_w,
                               const float* action_b, const float* pos_spatial, const float* pos_temporal_row,
-                              int64_t B, int N, int D, int dl, int K, float* x, jz_stream_t stream);
-JZ_API int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, int t, int Tmax, int S, int H,
-                                   int append, void* out, jz_stream_t stream);
+                              const int* dev_t, int64_t B, int N, int D, int dl, int K, float* x,
+                              jz_stream_t stream);
+JZ_API int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, int t, const int* dev_t, int Tmax,
+                                   int S, int H, int append, void* out, jz_stream_t stream);
 JZ_API int jz_kv_fill(const void* qkv, void* cache, int64_t B, int T, int t0, int Tmax, int S, int D,
                       jz_stream_t stream);
 
@@ -282,11 +284,14 @@ JZ_API int jz_kv_fill(const void* qkv, void* cache, int64_t B, int T, int t0, in
  * b*N + n) of the numpy Philox state (counter/key/buffer/pos as in jz_philox_mask),
  * sampled = #(u > cdf) clamped to K-1 (argmax when T < 1e-6, no draw), conf =
  * p[sampled]; cur = known ? cur : sampled; conf = known ? +inf : conf; then the
- * n_keep best (conf desc, position asc) of each row become known. */
+ * n_keep best (conf desc, position asc) of each row become known.  dev_params (may be
+ * NULL): device int64[13] {draw_base, n_keep, counter[4], key[2], buffer[4], buffer_pos}
+ * read by the kernels instead of the host values (buffer_pos < 0: keep the host Philox
+ * state), so one captured CUDA graph serves every refinement step of every frame. */
 JZ_API int jz_maskgit_step(const float* logits, int64_t B, int N, int K, float temperature,
                            const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4,
-                           int buffer_pos, uint64_t draw_base, int n_keep, int64_t* cur, uint8_t* known,
-                           float* conf, jz_stream_t stream);
+                           int buffer_pos, uint64_t draw_base, int n_keep, const int64_t* dev_params,
+                           int64_t* cur, uint8_t* known, float* conf, jz_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -23,9 +23,10 @@ __global__ void embed_frame_kernel(const int64_t* __restrict__ tokens, const uin
                                    const float* __restrict__ cond, const float* __restrict__ E,
                                    const float* __restrict__ mt, const float* __restrict__ Wa,
                                    const float* __restrict__ ba, const float* __restrict__ ps,
-                                   const float* __restrict__ pt_row, int N, int D, int dl, int K,
-                                   float* __restrict__ x) {
+                                   const float* __restrict__ pt_row, const int* __restrict__ dev_t, int N, int D,
+                                   int dl, int K, float* __restrict__ x) {
   const int S = N + 1;
+  if (dev_t) pt_row += (int64_t)(*dev_t) * D;
   const int64_t row = blockIdx.x;
   const int s = (int)(row % S);
   const int64_t b = row / S;
@@ -59,58 +60,88 @@ __global__ void embed_frame_kernel(const int64_t* __restrict__ tokens, const uin
 }
 
 // ---------------------------------------------------------------------------
-// temporal attention of frame t over cache[:, 0..t-1] + itself.  One warp per (b, s, h),
-// lane holds head dims 2*lane, 2*lane+1.  cache [B, Tmax, S, 2D] bf16 (k | v).
-// append: also write the current k, v into cache[:, t].
+// temporal attention of frame t over cache[:, 0..t-1] + itself.  One warp per (b, s)
+// covering every head: lane l owns dims [16l, 16l+16) (head l/4), so a head's score is a
+// 16-wide partial dot reduced over 4 lanes.  cache [B, Tmax, S, 2D] bf16 (k | v).
+// append: also write the current k, v into cache[:, t].  Requires D == 512 (8 heads x 64).
 // ---------------------------------------------------------------------------
+template <int DPL>
+JZ_DEV void loadv(const __nv_bfloat16* p, float (&f)[DPL]) {
+#pragma unroll
+  for (int c = 0; c < DPL / 4; ++c) {
+    const uint2 a = reinterpret_cast<const uint2*>(p)[c];
+    const float2 x = unpack_bf16(a.x), y = unpack_bf16(a.y);
+    f[4 * c] = x.x; f[4 * c + 1] = x.y; f[4 * c + 2] = y.x; f[4 * c + 3] = y.y;
+  }
+}
+
+template <int DPL>
+JZ_DEV void storev(__nv_bfloat16* p, const float (&f)[DPL], float scale) {
+#pragma unroll
+  for (int c = 0; c < DPL / 4; ++c)
+    reinterpret_cast<uint2*>(p)[c] = make_uint2(pack_bf16(f[4 * c] * scale, f[4 * c + 1] * scale),
+                                                pack_bf16(f[4 * c + 2] * scale, f[4 * c + 3] * scale));
+}
+
+template <int DPL>
+JZ_DEV void copyv(__nv_bfloat16* dst, const __nv_bfloat16* src) {
+#pragma unroll
+  for (int c = 0; c < DPL / 4; ++c) reinterpret_cast<uint2*>(dst)[c] = reinterpret_cast<const uint2*>(src)[c];
+}
+
+// DPL = head dims per lane: D = 32*DPL, a head (64 dims) spans 64/DPL lanes
+template <int DPL>
 __global__ void temporal_decode_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ cache,
-                                       int64_t B, int t, int Tmax, int S, int H, int append,
+                                       int64_t B, int t, const int* __restrict__ dev_t, int Tmax, int S, int append,
                                        __nv_bfloat16* __restrict__ out) {
-  const int D = H * 64;
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  constexpr int D = 32 * DPL;
+  if (dev_t) t = *dev_t;
+  const int64_t bs = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (gw >= B * S * H) return;
-  const int h = (int)(gw % H);
-  const int64_t bs = gw / H;
+  if (bs >= B * S) return;
   const int s = (int)(bs % S);
   const int64_t b = bs / S;
   const __nv_bfloat16* row = qkv + bs * 3 * D;
-  const float2 q = unpack_bf16(*reinterpret_cast<const uint32_t*>(row + h * 64 + 2 * lane));
-  const uint32_t kc = *reinterpret_cast<const uint32_t*>(row + D + h * 64 + 2 * lane);
-  const uint32_t vc = *reinterpret_cast<const uint32_t*>(row + 2 * D + h * 64 + 2 * lane);
+  const int d0 = DPL * lane;
+  float q[DPL], kc[DPL], vc[DPL];
+  loadv<DPL>(row + d0, q);
+  loadv<DPL>(row + D + d0, kc);
+  loadv<DPL>(row + 2 * D + d0, vc);
+  const __nv_bfloat16* base = cache + ((b * Tmax) * S + s) * 2 * D + d0;
+  const int64_t tstride = (int64_t)S * 2 * D;
   float sc[17];
   float mx = -INFINITY;
+#pragma unroll 4
   for (int tau = 0; tau <= t; ++tau) {
-    float2 k;
-    if (tau < t) {
-      const __nv_bfloat16* cr = cache + (((b * Tmax + tau) * S + s) * 2 * D);
-      k = unpack_bf16(*reinterpret_cast<const uint32_t*>(cr + h * 64 + 2 * lane));
-    } else {
-      k = unpack_bf16(kc);
-    }
-    const float a = warp_sum(q.x * k.x + q.y * k.y) * 0.125f;
+    float k[DPL];
+    if (tau < t) loadv<DPL>(base + tau * tstride, k);
+    float a = 0.f;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) a += q[i] * (tau < t ? k[i] : kc[i]);
+#pragma unroll
+    for (int o = 1; o < 64 / DPL; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    a *= 0.125f;
     sc[tau] = a;
     mx = fmaxf(mx, a);
   }
-  float l = 0.f, o0 = 0.f, o1 = 0.f;
+  float o[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) o[i] = 0.f;
+  float l = 0.f;
+#pragma unroll 4
   for (int tau = 0; tau <= t; ++tau) {
     const float p = __expf(sc[tau] - mx);
     l += p;
-    float2 v;
-    if (tau < t) {
-      const __nv_bfloat16* cr = cache + (((b * Tmax + tau) * S + s) * 2 * D);
-      v = unpack_bf16(*reinterpret_cast<const uint32_t*>(cr + D + h * 64 + 2 * lane));
-    } else {
-      v = unpack_bf16(vc);
-    }
-    o0 += p * v.x;
-    o1 += p * v.y;
+    float v[DPL];
+    if (tau < t) loadv<DPL>(base + tau * tstride + D, v);
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) o[i] += p * (tau < t ? v[i] : vc[i]);
   }
-  *reinterpret_cast<uint32_t*>(out + bs * D + h * 64 + 2 * lane) = pack_bf16(o0 / l, o1 / l);
+  storev<DPL>(out + bs * D + d0, o, 1.0f / l);
   if (append) {
-    __nv_bfloat16* cw = cache + (((b * Tmax + t) * S + s) * 2 * D);
-    *reinterpret_cast<uint32_t*>(cw + h * 64 + 2 * lane) = kc;
-    *reinterpret_cast<uint32_t*>(cw + D + h * 64 + 2 * lane) = vc;
+    __nv_bfloat16* cw = cache + ((b * Tmax + t) * S + s) * 2 * D + d0;
+    copyv<DPL>(cw, row + D + d0);
+    copyv<DPL>(cw + D, row + 2 * D + d0);
   }
 }
 
@@ -139,8 +170,21 @@ __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloa
 // ---------------------------------------------------------------------------
 template <int PER>  // codes per lane
 __global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t rows, int K, float inv_temp,
-                                      int greedy, PhiloxState st, uint64_t draw_base, int64_t* __restrict__ cur,
+                                      int greedy, PhiloxState st, uint64_t draw_base,
+                                      const int64_t* __restrict__ dev_params, int64_t* __restrict__ cur,
                                       const uint8_t* __restrict__ known, float* __restrict__ conf) {
+  if (dev_params) {
+    draw_base = (uint64_t)dev_params[0];
+    if (dev_params[12] >= 0) {  // Philox state from device memory
+      for (int i = 0; i < 4; ++i) {
+        st.ctr[i] = (uint64_t)dev_params[2 + i];
+        st.buf[i] = (uint64_t)dev_params[8 + i];
+      }
+      st.key[0] = (uint64_t)dev_params[6];
+      st.key[1] = (uint64_t)dev_params[7];
+      st.pos = (int)dev_params[12];
+    }
+  }
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -210,8 +254,10 @@ __global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t 
 }
 
 // K11b: per batch row, the n_keep highest-confidence positions (ties by position) become known.
-__global__ void maskgit_select_kernel(const float* __restrict__ conf, int N, int n_keep, uint8_t* __restrict__ known) {
+__global__ void maskgit_select_kernel(const float* __restrict__ conf, int N, int n_keep,
+                                      const int64_t* __restrict__ dev_params, uint8_t* __restrict__ known) {
   extern __shared__ float sconf[];
+  if (dev_params) n_keep = (int)dev_params[1];
   const int64_t b = blockIdx.x;
   for (int i = threadIdx.x; i < N; i += blockDim.x) sconf[i] = conf[b * N + i];
   __syncthreads();
@@ -233,23 +279,35 @@ using namespace jz;
 extern "C" int jz_dyn_embed_frame(const int64_t* tokens, const uint8_t* known, const float* cond,
                                   const float* token_embed, const float* mask_token, const float* action_w,
                                   const float* action_b, const float* pos_spatial, const float* pos_temporal_row,
-                                  int64_t B, int N, int D, int dl, int K, float* x, jz_stream_t s) {
+                                  const int* dev_t, int64_t B, int N, int D, int dl, int K, float* x,
+                                  jz_stream_t s) {
   JZ_CHECK_ARG(D % 4 == 0 && D / 4 <= 1024, "embed_frame: D=%d", D);
   if (B == 0) return JZ_OK;
   embed_frame_kernel<<<(unsigned)(B * (N + 1)), D / 4, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      tokens, known, cond, token_embed, mask_token, action_w, action_b, pos_spatial, pos_temporal_row, N, D, dl, K, x);
+      tokens, known, cond, token_embed, mask_token, action_w, action_b, pos_spatial, pos_temporal_row, dev_t, N, D, dl,
+      K, x);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
 
-extern "C" int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, int t, int Tmax, int S, int H,
-                                       int append, void* out, jz_stream_t s) {
+extern "C" int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, int t, const int* dev_t, int Tmax,
+                                       int S, int H, int append, void* out, jz_stream_t s) {
   JZ_CHECK_ARG(t >= 0 && t < Tmax && t <= 16, "temporal decode: frame index %d out of range", t);
-  const int64_t warps = B * S * H;
+  const int D = H * 64;
+  JZ_CHECK_ARG(D == 128 || D == 256 || D == 512 || D == 1024, "temporal decode: model dim %d unsupported", D);
+  const int64_t warps = B * S;
   if (warps == 0) return JZ_OK;
-  temporal_decode_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(cache), B, t, Tmax, S, H, append,
-      reinterpret_cast<__nv_bfloat16*>(out));
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  auto q = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  auto c = reinterpret_cast<__nv_bfloat16*>(cache);
+  auto o = reinterpret_cast<__nv_bfloat16*>(out);
+  switch (D) {
+    case 128: temporal_decode_kernel<4><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 256: temporal_decode_kernel<8><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 512: temporal_decode_kernel<16><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    default: temporal_decode_kernel<32><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+  }
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
@@ -269,8 +327,8 @@ extern "C" int jz_kv_fill(const void* qkv, void* cache, int64_t B, int T, int t0
 
 extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, float temperature,
                                const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4, int buffer_pos,
-                               uint64_t draw_base, int n_keep, int64_t* cur, uint8_t* known, float* conf,
-                               jz_stream_t s) {
+                               uint64_t draw_base, int n_keep, const int64_t* dev_params, int64_t* cur,
+                               uint8_t* known, float* conf, jz_stream_t s) {
   JZ_CHECK_ARG(K % 32 == 0 && K / 32 <= 64, "maskgit: vocabulary %d unsupported (multiple of 32, <= 2048)", K);
   JZ_CHECK_ARG(n_keep >= 0 && n_keep <= N, "maskgit: n_keep %d", n_keep);
   auto st = reinterpret_cast<cudaStream_t>(s);
@@ -287,13 +345,13 @@ extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, flo
   const int64_t rows = B * N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
   switch (K / 32) {
-#define MS(P) case P: maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, cur, known, conf); break;
+#define MS(P) case P: maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf); break;
     MS(1) MS(2) MS(4) MS(8) MS(16) MS(32) MS(64)
 #undef MS
     default: set_error("maskgit: vocabulary %d unsupported", K); return JZ_EINVAL;
   }
   JZ_LAUNCH_CHECK();
-  maskgit_select_kernel<<<(unsigned)B, 256, N * sizeof(float), st>>>(conf, N, n_keep, known);
+  maskgit_select_kernel<<<(unsigned)B, 256, N * sizeof(float), st>>>(conf, N, n_keep, dev_params, known);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

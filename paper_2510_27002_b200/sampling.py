@@ -161,6 +161,7 @@ class FrameDecoder:
     def prefill(self, tokens: torch.Tensor, latents: torch.Tensor) -> None:
         """Cache frames 0..t0-1 (tokens (B,t0,N) int64, latents (B,t0-1,dl)) — the full-clip forward of those frames."""
         cfg, P = self.cfg, self.P
+        self._refresh_weights()
         B, t0, N = tokens.shape
         err = torch.zeros((), dtype=torch.int32, device=tokens.device)
         x = _K.dyn_embed_fwd(tokens, None, latents.contiguous(), {k: v.data for k, v in P.items()}, B=B, T=t0, N=N,
@@ -168,6 +169,14 @@ class FrameDecoder:
         for i in range(cfg.blocks):
             x = self._block(i, x, B=B, T=t0, temporal=("full", None))
         self.t = t0
+
+    def _refresh_weights(self):
+        """Re-cast the bf16 weight shadows IN PLACE (graph-captured kernels hold their addresses)."""
+        fresh = _shadows(self.P, self.cfg.st, "dyn")
+        for old, new in zip(self.sh, fresh):
+            for k in old:
+                old[k].copy_(new[k])
+        _K.cast_bf16(self.P["to_logits.w"].data, self.wl)
 
     def _block(self, i, x, *, B, T, temporal):
         P, w, base = self.P, self.sh[i], f"dyn.block{i}"
@@ -184,10 +193,11 @@ class FrameDecoder:
             _L.call("jz_kv_fill", qkv2.data_ptr(), self.cache[i].data_ptr(), B, T, 0, self.t_max, S, self.D,
                     _L.stream_ptr())
         else:
-            t, append = arg
+            t, append, dev_t = arg
             ao2 = torch.empty(B * S, self.D, dtype=torch.bfloat16, device=x.device)
-            _L.call("jz_attn_temporal_decode", qkv2.data_ptr(), self.cache[i].data_ptr(), B, t, self.t_max, S, H,
-                    int(append), ao2.data_ptr(), _L.stream_ptr())
+            _L.call("jz_attn_temporal_decode", qkv2.data_ptr(), self.cache[i].data_ptr(), B, t,
+                    None if dev_t is None else dev_t.data_ptr(), self.t_max, S, H, int(append), ao2.data_ptr(),
+                    _L.stream_ptr())
         x2 = _K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=_L.EPI_RESID, aux=x1)
         xn3, _, _ = _K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
         hpre = torch.empty(xn3.shape[0], self.cfg.ffn_dim, dtype=torch.bfloat16, device=x.device)
@@ -195,46 +205,122 @@ class FrameDecoder:
         return _K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=_L.EPI_RESID, aux=x2)
 
     def frame(self, tokens: torch.Tensor, known: torch.Tensor | None, cond: torch.Tensor, *, append: bool,
-              logits: bool = True):
-        """Forward frame index self.t ((B,N) tokens; known (B,N) u8 or None=all known) over the cache."""
+              logits: bool = True, dev_t: torch.Tensor | None = None):
+        """Forward one frame ((B,N) tokens; known (B,N) u8 or None=all known) over the cache.
+
+        The frame index is self.t, or the device scalar dev_t (graph-captured path)."""
         cfg, P = self.cfg, self.P
         B, N, D, t = self.B, self.N, self.D, self.t
         x = torch.empty(B * self.S, D, dtype=torch.float32, device=tokens.device)
-        pt_row = P["pos_temporal"].data[t]
+        pt = P["pos_temporal"].data
+        pt_row = pt if dev_t is not None else pt[t]
         _L.call("jz_dyn_embed_frame", tokens.data_ptr(), None if known is None else known.data_ptr(),
                 cond.data_ptr(), P["token_embed"].data.data_ptr(), P["mask_token"].data.data_ptr(),
                 P["action_proj.w"].data.data_ptr(), P["action_proj.b"].data.data_ptr(),
-                P["pos_spatial"].data.data_ptr(), pt_row.data_ptr(), B, N, D, cfg.action_latent_dim,
-                cfg.token_codes, x.data_ptr(), _L.stream_ptr())
+                P["pos_spatial"].data.data_ptr(), pt_row.data_ptr(), None if dev_t is None else dev_t.data_ptr(),
+                B, N, D, cfg.action_latent_dim, cfg.token_codes, x.data_ptr(), _L.stream_ptr())
         for i in range(cfg.blocks):
-            x = self._block(i, x, B=B, T=1, temporal=("decode", (t, append)))
-        if append:
+            x = self._block(i, x, B=B, T=1, temporal=("decode", (t, append, dev_t)))
+        if append and dev_t is None:
             self.t = t + 1
         if not logits:
             return None
         y, _, _ = _K.layernorm_fwd(x, P["dyn.final_ln.g"].data, P["dyn.final_ln.b"].data, skip_period=self.S)
         return _K.linear_fwd(y, self.wl, P["to_logits.b"].data, epilogue=_L.EPI_F32)
 
-    def decode(self, cond: torch.Tensor, steps: int, temperature: float, rng: np.random.Generator) -> torch.Tensor:
-        """MaskGIT-decode frame self.t; returns cur (B, N) int64 in HBM and appends it to the cache."""
-        cfg = self.cfg
-        B, N, K = self.B, self.N, cfg.token_codes
+    # -- graph-captured decoding ------------------------------------------------
+    def _static(self, dev):
+        if getattr(self, "_cur", None) is None:
+            B, N = self.B, self.N
+            self._cur = torch.zeros(B, N, dtype=torch.int64, device=dev)
+            self._known = torch.zeros(B, N, dtype=torch.uint8, device=dev)
+            self._conf = torch.empty(B, N, dtype=torch.float32, device=dev)
+            self._cond = torch.empty(B, self.cfg.action_latent_dim, dtype=torch.float32, device=dev)
+            self._dev_t = torch.zeros((), dtype=torch.int32, device=dev)
+            self._params = torch.zeros(13, dtype=torch.int64, device=dev)
+            self._graphs: dict = {}
+
+    def _step(self, temperature: float):
+        logits = self.frame(self._cur, self._known, self._cond, append=False, dev_t=self._dev_t)
+        z = (_C.c_uint64 * 4)()
+        _L.call("jz_maskgit_step", logits.data_ptr(), self.B, self.N, self.cfg.token_codes, float(temperature),
+                _C.addressof(z), _C.addressof(z), _C.addressof(z), 4, 0, 0, self._params.data_ptr(),
+                self._cur.data_ptr(), self._known.data_ptr(), self._conf.data_ptr(), _L.stream_ptr())
+
+    def _append(self):
+        self.frame(self._cur, None, self._cond, append=True, logits=False, dev_t=self._dev_t)
+
+    def decode(self, cond: torch.Tensor, steps: int, temperature: float, rng: np.random.Generator,
+               graph: bool = True) -> torch.Tensor:
+        """MaskGIT-decode frame self.t; returns cur (B, N) int64 in HBM and appends it to the cache.
+
+        The refinement step (single-frame forward over the cache + sampler) and the cache
+        append are each captured ONCE per decoder in a CUDA graph; the frame index, the
+        step's draw offset / n_keep and the Philox state live in device memory and are
+        refreshed by one small H2D copy before each replay.
+        """
         dev = cond.device
-        cur = torch.zeros(B, N, dtype=torch.int64, device=dev)
-        known = torch.zeros(B, N, dtype=torch.uint8, device=dev)
-        conf = torch.empty(B, N, dtype=torch.float32, device=dev)
+        self._static(dev)
+        B, N = self.B, self.N
         greedy = temperature < 1e-6
-        st = _consume(rng, steps * B * N) if not greedy else _PS([0, 0, 0, 0], (0, 0), [0, 0, 0, 0], 4)
-        ctr = (_C.c_uint64 * 4)(*st.counter)
-        key = (_C.c_uint64 * 2)(*st.key)
-        buf = (_C.c_uint64 * 4)(*st.buffer)
-        for s, n_keep in enumerate(keep_counts(N, steps)):
-            logits = self.frame(cur, known, cond, append=False)
-            _L.call("jz_maskgit_step", logits.data_ptr(), B, N, K, float(temperature), _C.addressof(ctr),
-                    _C.addressof(key), _C.addressof(buf), st.buffer_pos, s * B * N, n_keep, cur.data_ptr(),
-                    known.data_ptr(), conf.data_ptr(), _L.stream_ptr())
-        self.frame(cur, None, cond, append=True, logits=False)
-        return cur
+        st = _consume(rng, steps * B * N) if not greedy else None
+        rows = []
+        for s, k in enumerate(keep_counts(N, steps)):
+            if st is None:
+                rows.append([0, k] + [0] * 10 + [-1])
+            else:
+                rows.append([s * B * N, k] + st.counter + list(st.key) + st.buffer + [st.buffer_pos])
+        mask64 = (1 << 64) - 1
+        host = torch.tensor(np.array([[v & mask64 for v in r] for r in rows], dtype=np.uint64).view(np.int64),
+                            dtype=torch.int64).pin_memory()
+        host_t = torch.tensor(self.t, dtype=torch.int32).pin_memory()
+        self._cond.copy_(cond)
+        self._cur.zero_()
+        self._known.zero_()
+        self._dev_t.copy_(host_t, non_blocking=True)
+        key = ("step", float(temperature))
+        g = self._graphs.get(key) if graph else None
+        s0 = 0
+        if graph and g is None:
+            self._params.copy_(host[0], non_blocking=True)
+            self._step(temperature)  # eager first step: loads every kernel before capture
+            s0 = 1
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._step(temperature)
+            self._graphs[key] = g
+        for s in range(s0, steps):
+            self._params.copy_(host[s], non_blocking=True)
+            if g is not None:
+                g.replay()
+            else:
+                self._step(temperature)
+        ga = self._graphs.get("append") if graph else None
+        if graph and ga is None:
+            ga = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga):
+                self._append()
+            self._graphs["append"] = ga
+        if ga is not None:
+            ga.replay()
+        else:
+            self._append()
+        self.t += 1
+        return self._cur.clone()
+
+
+def decoder_for(model, B: int, t_max: int) -> "FrameDecoder":
+    """A FrameDecoder (KV cache + captured graphs) reused across calls for the same model/batch.
+
+    The weight shadows are re-derived on every prefill (callers may update or swap params)."""
+    cache = model.__dict__.setdefault("_frame_decoders", {})
+    key = (B, t_max, id(model.params))
+    dec = cache.get(key)
+    if dec is None:
+        cache.clear()  # keep one decoder (its KV cache is large)
+        dec = FrameDecoder(model, B, t_max)
+        cache[key] = dec
+    return dec
 
 
 def _dev_latents(model, action_latents) -> torch.Tensor:
@@ -258,7 +344,7 @@ def decode_frame_device(model, prev_tokens, action_latents, steps: int = 25, tem
     lat = _dev_latents(model, action_latents)
     if lat.shape[1] != t_prev:
         raise ValueError(f"need {t_prev} action latents, got {lat.shape[1]}")
-    dec = FrameDecoder(model, b, max(model.cfg.max_frames, t_prev + 1))
+    dec = decoder_for(model, b, max(model.cfg.max_frames, t_prev + 1))
     dec.prefill(tok, lat[:, : t_prev - 1])
     return dec.decode(lat[:, t_prev - 1].contiguous(), steps, temperature, rng)
 
@@ -283,7 +369,7 @@ def rollout_device(tokenizer, dynamics, conditioning_frames, actions, horizon: i
     else:
         null = dynamics.params["null_action"].data.reshape(1, 1, dlat)
         history = torch.zeros((b, n_cond - 1, dlat), dtype=torch.float32, device=dev) + null
-    dec = FrameDecoder(dynamics, b, dynamics.cfg.max_frames)
+    dec = decoder_for(dynamics, b, dynamics.cfg.max_frames)
     dec.prefill(tokens, history)
     frames_tok = [tokens]
     for step in range(horizon):

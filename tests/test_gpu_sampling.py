@@ -54,7 +54,7 @@ def test_sampler_kernel_vs_oracle():
         ctr, key, buf = (C.c_uint64 * 4)(*st.counter), (C.c_uint64 * 2)(*st.key), (C.c_uint64 * 4)(*st.buffer)
         lg = torch.tensor(logits).cuda()
         L.call("jz_maskgit_step", lg.data_ptr(), 3, 256, 1024, float(temp), C.addressof(ctr), C.addressof(key),
-               C.addressof(buf), st.buffer_pos, 0, 0, cur.data_ptr(), known.data_ptr(), conf.data_ptr(),
+               C.addressof(buf), st.buffer_pos, 0, 0, None, cur.data_ptr(), known.data_ptr(), conf.data_ptr(),
                L.stream_ptr())
         s = cur.cpu().numpy()
         assert (s == ref_s).mean() >= 0.998, temp  # only cdf-boundary coincidences may differ
@@ -75,7 +75,7 @@ def test_selection_is_stable_topk():
     conf = torch.empty(B, N, device="cuda")
     z = (C.c_uint64 * 4)()
     L.call("jz_maskgit_step", logits.data_ptr(), B, N, K, 0.0, C.addressof(z), C.addressof(z), C.addressof(z), 4, 0,
-           100, cur.data_ptr(), known.data_ptr(), conf.data_ptr(), L.stream_ptr())
+           100, None, cur.data_ptr(), known.data_ptr(), conf.data_ptr(), L.stream_ptr())
     k = known.cpu().numpy()
     assert k[0, :100].all() and not k[0, 100:].any()
     assert k[1, 200:].all() and k[1, :44].all() and not k[1, 44:200].any()
