@@ -1,3 +1,4 @@
+import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))  # noqa: E402
 """Scratch GPU check of the tcgen05 GEMM against torch fp32 (all majors/epilogues)."""
 import sys
 import time

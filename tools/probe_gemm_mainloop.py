@@ -1,3 +1,4 @@
+import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))  # noqa: E402
 import torch
 from paper_2510_27002_b200 import _lib as L
 L.ensure_device()

@@ -1,3 +1,4 @@
+import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))  # noqa: E402
 """Run a few dynamics train steps at B=36 (target for ncu captures; no timing printed)."""
 import sys
 from pathlib import Path

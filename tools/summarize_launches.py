@@ -1,3 +1,4 @@
+import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))  # noqa: E402
 """Summarise an ncu --metrics gpu__time_duration.sum CSV launch list: time share per kernel."""
 import csv
 import re

@@ -1,3 +1,4 @@
+import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))  # noqa: E402
 """Scratch: time one dynamics train step at B=36 (jasmine-base dims, patch 4)."""
 import sys
 import time
