@@ -305,7 +305,15 @@ def main() -> None:
 
     # ---- secondary BASELINE configs (rank 0, N=1): C5 sampling, C2 LAM step, C1 tokenizer fwd ----
     extra = {}
+    peak_gb = torch.cuda.max_memory_allocated(dev) / 2**30
     if rank == 0 and world == 1 and not args.no_extra:
+        # independent workloads: release the training state (weights, AdamW moments, activation
+        # scratch) so they run on a clean allocator, as they would in their own process
+        del trainer, model, loss, tokens_d, lat_d
+        import gc
+        gc.collect()
+        K.release_scratch()
+        torch.cuda.empty_cache()
         try:
             extra = secondary_configs(dev)
         except Exception as exc:  # never sink the headline line
@@ -348,7 +356,8 @@ def main() -> None:
                 "roofline": roofline,
                 "model_tflops": round(step_flops / (ms / 1e3) / 1e12, 1),
                 "model_flops_frac": round(step_flops / (ms / 1e3) / 1e12 / peaks["bf16_sustained"], 4),
-                "cpu_baseline": cpu, "clocks": clk, "loss": round(loss_val, 5), **extra}
+                "cpu_baseline": cpu, "clocks": clk, "loss": round(loss_val, 5),
+            "hbm_peak_gb": round(peak_gb, 1), **extra}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

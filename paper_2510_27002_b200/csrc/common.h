@@ -46,7 +46,7 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64
                       uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer);
 // generic: elem_bytes 2 (bf16) or 4 (f32), 128-byte swizzle
 int make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
-                 uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer);
+                 uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool swizzle128 = true);
 
 int num_sms();
 

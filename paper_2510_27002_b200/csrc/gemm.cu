@@ -15,12 +15,40 @@
 //               (two warps per TMEM lane quarter, each owning half of the columns)
 // TMEM holds two BN-column fp32 accumulators so the epilogue of tile i overlaps the
 // main loop of tile i+1.
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
 
 #include "common.h"
 #include "ptx.cuh"
+
+#ifdef JZ_GEMM_PROF
+__device__ unsigned long long g_gemm_prof[64 * 8];
+__device__ int g_gemm_dbg;
+__device__ long long g_gemm_ph[64 * 4];
+#define PH_T(v) long long v = clock64()
+#define PH_ADD(i, t0)                                                                     \
+  do {                                                                                    \
+    if (blockIdx.x == 0 && warp == 2 && lane == 0 && ti < 64) g_gemm_ph[ti * 4 + (i)] += clock64() - (t0); \
+  } while (0)
+#define GPROF(slot)                                                                     \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && ti < 64) g_gemm_prof[ti * 8 + (slot)] = clock64();          \
+  } while (0)
+#define GDBG (dbg_)
+#else
+#define GDBG 0
+#define PH_T(v) \
+  do {          \
+  } while (0)
+#define PH_ADD(i, t0) \
+  do {                \
+  } while (0)
+#define GPROF(slot) \
+  do {              \
+  } while (0)
+#endif
 
 namespace jz {
 
@@ -40,19 +68,38 @@ struct GemmParams {
   int64_t ldaux;
   void* D2;
   int64_t ldd2;
-  int tma_epi;  // 1: staged TMA-store epilogue (maps valid), 0: direct per-thread stores
+  int tma_epi;    // 1: smem-staged epilogue, 0: direct per-thread stores (unaligned shapes)
+  int store_tma;  // staged epilogue writes with TMA bulk stores (1) or coalesced st.global (0)
 };
 
 struct EpiMaps {
   CUtensorMap d, d2, aux;
 };
 
-template <int BN>
+// Coalesced write-out of one warp's 32x128-byte staging tile (rows swizzled in 16-byte chunks):
+// each instruction covers 4 rows x 128 contiguous bytes. The LSU path keeps the per-SM TMA unit
+// free for operand loads (TMA stores measurably delayed them on epilogue-heavy shapes).
+__device__ __forceinline__ void stg_write_rows(const uint8_t* stg, uint8_t* gbase, int64_t ld_bytes, int rows_ok,
+                                               int cols_bytes, int lane) {
+  const int c = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + (lane >> 3);
+    if (r < rows_ok && c * 16 < cols_bytes)
+      *reinterpret_cast<uint4*>(gbase + r * ld_bytes + c * 16) =
+          *reinterpret_cast<const uint4*>(stg + r * 128 + ((c ^ (r & 7)) << 4));
+  }
+}
+
+// PAIR: a cluster of two CTAs runs one cta_group::2 MMA of M = 256; each CTA stages its own 128
+// rows of A and half of the BN columns of B, so operand bytes per MAC drop by a third.
+template <int BN, bool PAIR = false>
 struct GemmShape {
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = ((PAIR ? 192 : 200) * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int STG_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B, 128B-swizzled
@@ -205,11 +252,15 @@ JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], fl
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ EpiMaps em, GemmParams p, float* ws) {
-  using S = GemmShape<BN>;
+  using S = GemmShape<BN, PAIR>;
+  constexpr int TM = PAIR ? 2 * BM : BM;  // rows per (pair) tile
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int unit_stride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -224,13 +275,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+#ifdef JZ_GEMM_PROF
+  const int dbg_ = g_gemm_dbg;
+#endif
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (p.tma_epi) {
-      tma_prefetch_desc(&em.d);
-      if (p.epi == JZ_EPI_GELU) tma_prefetch_desc(&em.d2);
+      if (p.store_tma) tma_prefetch_desc(&em.d);
+      if (p.store_tma && p.epi == JZ_EPI_GELU) tma_prefetch_desc(&em.d2);
       if (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD) tma_prefetch_desc(&em.aux);
     }
   }
@@ -241,13 +295,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 32 * kEpiWarps);
+      mbar_init(&tempty_bar[i], (PAIR ? 2 : 1) * kEpiWarps);  // one arrival per epilogue warp of the pair
     }
     for (int i = 0; i < kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair<S::TMEM_COLS>(tmem_slot);
+    else tmem_alloc<S::TMEM_COLS>(tmem_slot);
+  }
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -257,51 +315,68 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      // pair: every load signals the leader's full barrier, which expects both CTAs' bytes
+      const uint32_t full0 = PAIR ? mapa_shared(smem_u32(&full_bar[0]), 0) : 0;
+      for (int u = first_unit; u < units; u += unit_stride) {
         const int tile = u / p.splits, split = u % p.splits;
-        const int m0 = (tile / p.n_tiles) * BM, n0 = (tile % p.n_tiles) * BN;
+        const int m0 = (tile / p.n_tiles) * TM + (int)rank * BM;
+        const int nb0 = (tile % p.n_tiles) * BN + (int)rank * S::B_ROWS;
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], S::STAGE_BYTES);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], (PAIR ? 2 : 1) * S::STAGE_BYTES);
           uint8_t* a_dst = smem + stage * S::STAGE_BYTES;
           uint8_t* b_dst = a_dst + S::A_BYTES;
           const int k = kb * BK;
+          auto load = [&](uint8_t* dst, const CUtensorMap* map, int c0, int c1) {
+            if constexpr (PAIR) tma_load_2d_pair(dst, map, full0 + stage * 8, c0, c1);
+            else tma_load_2d(dst, map, &full_bar[stage], c0, c1);
+          };
           if (!A_MN) {
-            tma_load_2d(a_dst, &tmA, &full_bar[stage], k, m0);
+            load(a_dst, &tmA, k, m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(a_dst + j * (64 * BK * 2), &tmA, &full_bar[stage], m0 + 64 * j, k);
+            for (int j = 0; j < BM / 64; ++j) load(a_dst + j * (64 * BK * 2), &tmA, m0 + 64 * j, k);
           }
           if (!B_MN) {
-            tma_load_2d(b_dst, &tmB, &full_bar[stage], k, n0);
+            load(b_dst, &tmB, k, nb0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(b_dst + j * (64 * BK * 2), &tmB, &full_bar[stage], n0 + 64 * j, k);
+            for (int j = 0; j < S::B_ROWS / 64; ++j) load(b_dst + j * (64 * BK * 2), &tmB, nb0 + 64 * j, k);
           }
           if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(TM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int ti = 0;
+      for (int u = first_unit; u < units; u += unit_stride, ++ti) {
         const int split = u % p.splits;
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+        GPROF(0);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        GPROF(1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+#ifdef JZ_GEMM_PROF
+        long long fw = 0;
+#endif
         for (int kb = kb0; kb < kb1; ++kb) {
+#ifdef JZ_GEMM_PROF
+          long long t0 = clock64();
+#endif
           mbar_wait(&full_bar[stage], phase);
+#ifdef JZ_GEMM_PROF
+          fw += clock64() - t0;
+#endif
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * S::STAGE_BYTES);
           const uint32_t b_addr = a_addr + S::A_BYTES;
@@ -311,12 +386,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                         : sdesc_sw128(a_addr + kk * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_addr + kk * 2048, 64 * BK * 2, 1024)
                                         : sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            umma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            if constexpr (PAIR) umma_bf16_ss_pair(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            else umma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          if constexpr (PAIR) umma_commit_pair(&empty_bar[stage], 0x3);
+          else umma_commit(&empty_bar[stage]);
           if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (PAIR) umma_commit_pair(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
+        GPROF(2);
+#ifdef JZ_GEMM_PROF
+        if (blockIdx.x == 0 && ti < 64) g_gemm_prof[ti * 8 + 6] = fw;
+#endif
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -331,16 +413,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t apar = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const bool has_bias = p.bias != nullptr && p.splits == 1;
+    // staged epilogue: bias comes straight from global (all lanes read the same address -> one
+    // L1 broadcast per vector), so the epilogue warps never synchronise with each other
+    const bool bias_vec = has_bias && (reinterpret_cast<uintptr_t>(p.bias) % 16 == 0) && (p.N % 4 == 0);
+    int ti = 0;
+    for (int u = first_unit; u < units; u += unit_stride, ++ti) {
       const int tile = u / p.splits, split = u % p.splits;
-      const int m0 = (tile / p.n_tiles) * BM, n0 = (tile % p.n_tiles) * BN;
-      const bool has_bias = p.bias != nullptr && p.splits == 1;
-      if (has_bias) {  // stage this tile's bias (previous tile fully consumed by all warps first)
+      const int m0 = (tile / p.n_tiles) * TM + (int)rank * BM, n0 = (tile % p.n_tiles) * BN;
+      if (has_bias && !p.tma_epi) {  // direct path: stage this tile's bias in smem
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         for (int c = etid; c < BN; c += 32 * kEpiWarps) sbias[c] = (n0 + c < p.N) ? p.bias[n0 + c] : 0.f;
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
+      if (warp == 2 && lane == 0) GPROF(3);
       mbar_wait(&tfull_bar[acc], acc_phase);
+      if (warp == 2 && lane == 0) GPROF(4);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * BN + chalf * HALF;
       const int row0 = m0 + quarter * 32;
@@ -350,19 +438,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const bool need_aux = p.splits == 1 &&
                               (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD);
         const int CW = f32out ? 32 : 64;
-        const CUtensorMap* dmap = &em.d;
+        const int esz = f32out ? 4 : 2;
+        // split-K partials: slab `split` of the fp32 workspace, row pitch N
+        uint8_t* dbase = p.splits > 1 ? reinterpret_cast<uint8_t*>(ws + (int64_t)split * p.M * p.N)
+                                      : reinterpret_cast<uint8_t*>(p.D);
+        const int64_t dld = (p.splits > 1 ? (int64_t)p.N : p.ldd) * esz;
+        const int rows_ok = p.M - row0;
 #pragma unroll 1
         for (int cc = 0; cc < HALF / CW; ++cc) {
           const int col = chalf * HALF + cc * CW;
           const int n = n0 + col;
           if (n >= p.N) break;  // warp-uniform
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
+          const int cols_bytes = min(CW, p.N - n) * esz;
+          PH_T(t_a);
+          if (p.store_tma) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+          PH_ADD(0, t_a);
           if (need_aux && lane == 0) {
+            fence_proxy_async();  // generic reads of the previous chunk before the async-proxy write
             mbar_arrive_expect_tx(&aux_bar[ew], S::STG_BYTES);
             tma_load_2d(stg, &em.aux, &aux_bar[ew], n, row0);
           }
           float v[64];
+          PH_T(t_b);
           {
             uint32_t r0[32];
             tmem_ld_32x32b_x32(tbase + cc * CW, r0);
@@ -376,10 +476,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r0[j]);
             }
           }
-          if (has_bias) {
+          PH_ADD(1, t_b);
+          PH_T(t_c);
+          if (bias_vec) {
+            const float4* b4p = reinterpret_cast<const float4*>(p.bias + n);
+            const int nv = min(CW, p.N - n) >> 2;
+#pragma unroll
+            for (int j = 0; j < 64; j += 4) {
+              if (j < CW && (j >> 2) < nv) {
+                const float4 b4 = __ldg(b4p + (j >> 2));
+                v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+              }
+            }
+          } else if (has_bias) {
 #pragma unroll
             for (int j = 0; j < 64; ++j)
-              if (j < CW) v[j] += sbias[col + j];
+              if (j < CW && n + j < p.N) v[j] += __ldg(p.bias + n + j);
           }
           if (need_aux) {
             mbar_wait(&aux_bar[ew], apar);
@@ -417,29 +529,54 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
                     make_uint4(pack_bf16(v[8 * c], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
                                pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
-              fence_proxy_async();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_2d(&em.d2, stg, n, row0);
-                bulk_commit();
-                bulk_wait_read0();
+              if (p.store_tma) {
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&em.d2, stg, n, row0);
+                  bulk_commit();
+                }
+#pragma unroll
+                for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);  // overlaps the store's smem read
+                if (lane == 0) bulk_wait_read0();
+              } else {
+                __syncwarp();
+                stg_write_rows(stg, reinterpret_cast<uint8_t*>(p.D2) + ((int64_t)row0 * p.ldd2 + n) * 2,
+                               (int64_t)p.ldd2 * 2, rows_ok, cols_bytes, lane);
+#pragma unroll
+                for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);
               }
               __syncwarp();
-#pragma unroll
-              for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);
             }
+            if (GDBG == 3) {
+              uint32_t x = 0;
+#pragma unroll
+              for (int c = 0; c < 32; ++c) x ^= pack_bf16(v[2 * c], v[2 * c + 1]);
+              if (x == 0x12345679u) *reinterpret_cast<uint32_t*>(stg) = x;
+            } else if (GDBG != 2) {
 #pragma unroll
             for (int c = 0; c < 8; ++c)
               *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
                   make_uint4(pack_bf16(v[8 * c], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
                              pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+            }
           }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(dmap, stg, n, row0 + (p.splits > 1 ? split * p.M : 0));
-            bulk_commit();
+          PH_ADD(2, t_c);
+          PH_T(t_d);
+          if (p.store_tma) {
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && GDBG != 1 && GDBG != 3) {
+              tma_store_2d(&em.d, stg, n, row0);
+              bulk_commit();
+            }
+          } else {
+            __syncwarp();
+            if (GDBG != 1 && GDBG != 3)
+              stg_write_rows(stg, dbase + (int64_t)row0 * dld + (int64_t)n * esz, dld, rows_ok, cols_bytes, lane);
+            __syncwarp();
           }
+          PH_ADD(3, t_d);
         }
       } else {
         // ---------- direct epilogue (unaligned shapes) ----------
@@ -461,15 +598,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if (warp == 2 && lane == 0) GPROF(5);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait0();
   }
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's MMAs/arrivals target this CTA until here
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<S::TMEM_COLS>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc_pair<S::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<S::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -489,36 +633,72 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool PAIR>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmParams& p,
                        float* ws, cudaStream_t stream) {
-  using S = GemmShape<BN>;
+  using S = GemmShape<BN, PAIR>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN>,
+    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN, PAIR>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
   });
   JZ_CUDA_TRY(attr_err);
   const int units = p.m_tiles * p.n_tiles * p.splits;
-  const int grid = units < num_sms() ? units : num_sms();
-  gemm_bf16_kernel<BN, A_MN, B_MN><<<grid, kGemmThreads, S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
-  JZ_LAUNCH_CHECK();
+  if constexpr (PAIR) {
+    const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(kGemmThreads, 1, 1);
+    cfg.dynamicSmemBytes = S::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    JZ_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, A_MN, B_MN, PAIR>, ta, tb, em, p, ws));
+    count_launch();
+  } else {
+    const int grid = units < num_sms() ? units : num_sms();
+    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR><<<grid, kGemmThreads, S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
+    JZ_LAUNCH_CHECK();
+  }
   return JZ_OK;
 }
 
-template <int BN>
+template <int BN, bool PAIR = false>
 static int dispatch_major(bool a_mn, bool b_mn, const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em,
                           const GemmParams& p, float* ws, cudaStream_t s) {
-  if (!a_mn && !b_mn) return launch_gemm<BN, false, false>(ta, tb, em, p, ws, s);
-  if (!a_mn && b_mn) return launch_gemm<BN, false, true>(ta, tb, em, p, ws, s);
-  if (a_mn && !b_mn) return launch_gemm<BN, true, false>(ta, tb, em, p, ws, s);
-  return launch_gemm<BN, true, true>(ta, tb, em, p, ws, s);
+  if (!a_mn && !b_mn) return launch_gemm<BN, false, false, PAIR>(ta, tb, em, p, ws, s);
+  if (!a_mn && b_mn) return launch_gemm<BN, false, true, PAIR>(ta, tb, em, p, ws, s);
+  if (a_mn && !b_mn) return launch_gemm<BN, true, false, PAIR>(ta, tb, em, p, ws, s);
+  return launch_gemm<BN, true, true, PAIR>(ta, tb, em, p, ws, s);
 }
 
 }  // namespace jz
 
 using namespace jz;
+
+// Tuning switches (read once): JZ_GEMM_PAIR=0 disables CTA pairs, JZ_GEMM_STORE=lsu replaces
+// the staged epilogue's TMA bulk stores by coalesced st.global.
+static bool pair_mode_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("JZ_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool store_tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("JZ_GEMM_STORE");
+    return !(e && e[0] == 'l');
+  }();
+  return on;
+}
 
 extern "C" int64_t jz_gemm_workspace_bytes(int64_t M, int64_t N, int split_k) {
   return split_k <= 1 ? 0 : (int64_t)split_k * M * N * (int64_t)sizeof(float);
@@ -551,19 +731,22 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
 
   const bool a_mn = !a_kmajor, b_mn = !b_kmajor;
   const int BN = N > 128 ? 256 : (N > 64 ? 128 : 64);
+  // CTA pairs for the wide shapes: 256x256 tiles across two SMs (see GemmShape)
+  const bool pair = BN == 256 && M > BM && pair_mode_enabled();
+  const int TM = pair ? 2 * BM : BM;
 
   CUtensorMap ta, tb;
   int rc;
   if (!a_mn) rc = make_tmap_2d_bf16(&ta, A, K, M, lda, 64, 128);
   else rc = make_tmap_2d_bf16(&ta, A, M, K, lda, 64, 64);
   if (rc) return rc;
-  if (!b_mn) rc = make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, BN);
+  if (!b_mn) rc = make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, pair ? BN / 2 : BN);
   else rc = make_tmap_2d_bf16(&tb, B, N, K, ldb, 64, 64);
   if (rc) return rc;
 
   GemmParams p;
   p.M = (int)M; p.N = (int)N; p.K = (int)K;
-  p.m_tiles = (int)((M + BM - 1) / BM);
+  p.m_tiles = (int)((M + TM - 1) / TM);
   p.n_tiles = (int)((N + BN - 1) / BN);
   p.kb_total = (int)((K + BK - 1) / BK);
   if (split_k > p.kb_total) split_k = p.kb_total;
@@ -580,17 +763,17 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
   EpiMaps em;
   memset(&em, 0, sizeof(em));
   p.tma_epi = 0;
+  p.store_tma = 0;
   if (epilogue != 7) {
     const bool f32out = p.splits > 1 || epilogue == JZ_EPI_F32 || epilogue == JZ_EPI_F32_ACC || epilogue == JZ_EPI_RESID;
     const bool bf16out = epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD;
-    // split-K partials keep the direct path (long-K GEMMs: the epilogue is negligible there);
-    // 32-column bf16 chunks (BN = 64) do not fill a 128-byte swizzle row either.
-    bool ok = (f32out || bf16out) && p.splits == 1 && !(bf16out && BN == 64);
+    // 32-column bf16 chunks (BN = 64) do not fill a 128-byte staging row.
+    bool ok = (f32out || bf16out) && !(bf16out && BN == 64);
     auto al = [](const void* q) { return ((uintptr_t)q % 16) == 0; };
-    if (ok && f32out) ok = al(D) && ldd % 4 == 0 && make_tmap_2d(&em.d, D, 4, N, M, ldd, 32, 32) == JZ_OK;
-    else if (ok) ok = al(D) && ldd % 8 == 0 && make_tmap_2d(&em.d, D, 2, N, M, ldd, 64, 32) == JZ_OK;
-    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU)
-      ok = al(D2) && ldd2 % 8 == 0 && make_tmap_2d(&em.d2, D2, 2, N, M, ldd2, 64, 32) == JZ_OK;
+    if (ok && p.splits > 1) ok = al(ws) && N % 4 == 0;
+    else if (ok && f32out) ok = al(D) && ldd % 4 == 0 && N % 4 == 0;
+    else if (ok) ok = al(D) && ldd % 8 == 0 && N % 8 == 0;
+    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU) ok = al(D2) && ldd2 % 8 == 0;
     if (ok && p.splits == 1 && epilogue == JZ_EPI_RESID)
       ok = al(aux) && ldaux % 4 == 0 && make_tmap_2d(&em.aux, aux, 4, N, M, ldaux, 32, 32) == JZ_OK;
     if (ok && p.splits == 1 && epilogue == JZ_EPI_F32_ACC)
@@ -598,8 +781,17 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
     if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU_BWD)
       ok = al(aux) && ldaux % 8 == 0 && make_tmap_2d(&em.aux, aux, 2, N, M, ldaux, 64, 32) == JZ_OK;
     p.tma_epi = ok ? 1 : 0;
+    // TMA bulk stores from the staging tiles (clip at M and N for free); split-K partial slabs
+    // use st.global so a partial last tile cannot spill into the next slab
+    if (ok && p.splits == 1 && store_tma_enabled()) {
+      const bool ok2 = f32out ? make_tmap_2d(&em.d, D, 4, N, M, ldd, 32, 32) == JZ_OK
+                              : make_tmap_2d(&em.d, D, 2, N, M, ldd, 64, 32) == JZ_OK;
+      const bool ok3 = epilogue != JZ_EPI_GELU || make_tmap_2d(&em.d2, D2, 2, N, M, ldd2, 64, 32) == JZ_OK;
+      p.store_tma = ok2 && ok3 ? 1 : 0;
+    }
   }
-  if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, em, p, ws, stream);
+  if (BN == 256 && pair) rc = dispatch_major<256, true>(a_mn, b_mn, ta, tb, em, p, ws, stream);
+  else if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else if (BN == 128) rc = dispatch_major<128>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else rc = dispatch_major<64>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   if (rc) return rc;
@@ -614,3 +806,18 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
   }
   return JZ_OK;
 }
+
+#ifdef JZ_GEMM_PROF
+extern "C" int jz_gemm_prof_ph(long long* host) {
+  int rc = cudaMemcpyFromSymbol(host, g_gemm_ph, sizeof(long long) * 64 * 4) == cudaSuccess ? 0 : -3;
+  static long long zeros[64 * 4];
+  cudaMemcpyToSymbol(g_gemm_ph, zeros, sizeof(zeros));
+  return rc;
+}
+extern "C" int jz_gemm_prof_dbg(int v) {
+  return cudaMemcpyToSymbol(g_gemm_dbg, &v, sizeof(int)) == cudaSuccess ? 0 : -3;
+}
+extern "C" int jz_gemm_prof_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_gemm_prof, sizeof(unsigned long long) * 64 * 8) == cudaSuccess ? 0 : -3;
+}
+#endif

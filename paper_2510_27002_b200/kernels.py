@@ -47,6 +47,11 @@ def scratch(name: str, numel: int, dtype=F32, device=None) -> torch.Tensor:
     return buf[:numel]
 
 
+def release_scratch() -> None:
+    """Drop every cached scratch buffer of this thread (they are re-created on demand)."""
+    _scratch.bufs.clear()
+
+
 def num_sms() -> int:
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 

@@ -1,0 +1,189 @@
+"""Kernel-level parity of the hand-written sm_100a kernels against plain torch fp32 references.
+
+These are the floating-point kernels of the dynamics step: the tcgen05 GEMM with
+every epilogue the model uses, LayerNorm fwd/bwd, spatial (S = 256/257, bidirectional) and temporal
+(causal) attention fwd/bwd.  Tolerances are relative Frobenius errors; bf16 operands with fp32
+accumulation put GEMM fp32 outputs at ~1e-6 of the fp32 product of the SAME bf16 operands, so the
+GEMM bounds are tight, while attention goes through bf16 P/dS tiles (2e-2, as fidelity_threshold.json).
+"""
+import math
+
+import pytest
+import torch
+
+from paper_2510_27002_b200 import _lib as L
+from paper_2510_27002_b200 import kernels as Kn
+
+pytestmark = pytest.mark.gpu
+dev = "cuda"
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+def _operands(M, N, K, a_kmajor, b_kmajor, seed):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    X = torch.randn(M, K, device=dev, generator=g).bfloat16()
+    W = torch.randn(K, N, device=dev, generator=g).bfloat16()
+    A = X.contiguous() if a_kmajor else X.t().contiguous()
+    B = W.t().contiguous() if b_kmajor else W.contiguous()
+    return X, W, A, B
+
+
+@pytest.mark.parametrize("a_kmajor", [1, 0])
+@pytest.mark.parametrize("b_kmajor", [0, 1])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (296, 200, 192), (128, 64, 64), (1000, 1536, 512), (333, 48, 512)])
+def test_gemm_majors_f32(M, N, K, a_kmajor, b_kmajor):
+    if (not b_kmajor and N % 8) or (not a_kmajor and M % 8):
+        pytest.skip("MN-major operand pitch must be a multiple of 8 elements")
+    X, W, A, B = _operands(M, N, K, a_kmajor, b_kmajor, M + N + K)
+    bias = torch.randn(N, device=dev)
+    ref = X.float() @ W.float() + bias
+    D = torch.full((M, N), float("nan"), device=dev)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=a_kmajor, b_kmajor=b_kmajor, out=D, epilogue=L.EPI_F32, bias=bias,
+            lda=K if a_kmajor else M, ldb=K if b_kmajor else N)
+    assert rel(D, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K,split", [(512, 512, 4096, 4), (504, 296, 2048, 3), (1000, 1536, 2048, 2),
+                                         (512, 1536, 20000, 6)])
+@pytest.mark.parametrize("acc", [False, True])
+def test_gemm_splitk_dw(M, N, K, split, acc):
+    """dW = x^T dy form (both operands MN-major), split-K partials + reduction, optional accumulate."""
+    X, W, A, B = _operands(M, N, K, 0, 0, K)
+    prev = torch.randn(M, N, device=dev)
+    D = prev.clone()
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=False, b_kmajor=False, out=D,
+            epilogue=L.EPI_F32_ACC if acc else L.EPI_F32, split_k=split, lda=M, ldb=N)
+    ref = X.float() @ W.float() + (prev if acc else 0)
+    assert rel(D, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M", [1000, 4096 + 77])
+def test_gemm_epilogues(M):
+    N, K = 512, 256
+    X, W, A, B = _operands(M, N, K, 1, 0, M)
+    acc = X.float() @ W.float()
+    bias = torch.randn(N, device=dev)
+    aux = torch.randn(M, N, device=dev)
+    # BF16: y = acc + b, rounded once
+    y = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=y, epilogue=L.EPI_BF16, bias=bias)
+    assert rel(y, acc + bias) < 4e-3
+    # RESID: out = aux + acc + b (fp32 residual stream)
+    r = torch.empty(M, N, device=dev)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=r, epilogue=L.EPI_RESID, bias=bias, aux=aux)
+    assert rel(r, aux + acc + bias) < 1e-5
+    # F32_ACC: out += acc
+    r2 = aux.clone()
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=r2, epilogue=L.EPI_F32_ACC)
+    assert rel(r2, aux + acc) < 1e-5
+    # GELU: D = gelu(acc + b) bf16, D2 = pre-activation bf16 (tanh form, as nn.gelu)
+    g = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    pre = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=g, epilogue=L.EPI_GELU, bias=bias, out2=pre)
+    assert rel(pre, acc + bias) < 4e-3
+    assert rel(g, torch.nn.functional.gelu(acc + bias, approximate="tanh")) < 5e-3
+    # GELU_BWD: D = acc * gelu'(aux_pre) bf16
+    pre_aux = (torch.randn(M, N, device=dev) * 2).bfloat16()
+    gb = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=gb, epilogue=L.EPI_GELU_BWD, aux=pre_aux)
+    xp = pre_aux.float().requires_grad_(True)
+    torch.nn.functional.gelu(xp, approximate="tanh").backward(acc)
+    assert rel(gb, xp.grad) < 5e-3
+
+
+def test_gemm_rejects_bad_shapes():
+    A = torch.zeros(64, 64, device=dev, dtype=torch.bfloat16)
+    D = torch.zeros(64, 64, device=dev)
+    with pytest.raises(ValueError):
+        Kn.gemm(A, A, M=64, N=64, K=0, a_kmajor=1, b_kmajor=0, out=D, epilogue=L.EPI_F32)
+
+
+@pytest.mark.parametrize("rows,D,skip", [(4096, 512, 0), (257 * 6, 512, 257), (1000, 256, 0)])
+def test_layernorm_fwd_bwd(rows, D, skip):
+    g = torch.Generator(device=dev).manual_seed(rows)
+    x = torch.randn(rows, D, device=dev, generator=g) * 3 + 1
+    gamma = torch.randn(D, device=dev, generator=g)
+    beta = torch.randn(D, device=dev, generator=g)
+    y, y32, mean, rstd = Kn.layernorm_fwd(x, gamma, beta, skip_period=skip, out_f32=True)
+    keep = torch.ones(rows, dtype=torch.bool, device=dev)
+    if skip:
+        keep[::skip] = False  # skip_period drops row 0 of every period from the outputs
+    xr = x.clone().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xr, (D,), gamma, beta, eps=1e-5)
+    assert rel(y32, ref[keep]) < 1e-5
+    assert rel(y, ref[keep]) < 4e-3
+    dy = torch.randn(int(keep.sum()), D, device=dev, generator=g)
+    full_dy = torch.zeros(rows, D, device=dev)
+    full_dy[keep] = dy
+    ref.backward(full_dy)
+    dres = torch.randn(rows, D, device=dev, generator=g)
+    dres0 = dres.clone()
+    dg, db = torch.zeros(D, device=dev), torch.zeros(D, device=dev)
+    Kn.layernorm_bwd(x, mean, rstd, gamma, dy, dres, accumulate=True, dgamma=dg, dbeta=db, skip_period=skip)
+    assert rel(dres - dres0, xr.grad) < 1e-5
+    gp = torch.nn.functional.layer_norm(x, (D,), eps=1e-5)
+    assert rel(dg, (full_dy * gp).sum(0)) < 1e-5
+    assert rel(db, full_dy.sum(0)) < 1e-5
+
+
+def _ref_attn(qkv, lead, L_, H, causal):
+    x = qkv.float().reshape(*lead, L_, 3, H, 64)
+    q, k, v = (x[..., i, :, :].transpose(-3, -2) for i in range(3))
+    s = q @ k.transpose(-1, -2) / math.sqrt(64)
+    if causal:
+        s = s.masked_fill(torch.triu(torch.ones(L_, L_, dtype=torch.bool, device=dev), 1), float("-inf"))
+    o = (torch.softmax(s, -1) @ v).transpose(-3, -2).reshape(*lead, L_, H * 64)
+    return o, torch.logsumexp(s, -1)
+
+
+@pytest.mark.parametrize("S", [257, 256])
+def test_attn_spatial_fwd_bwd(S):
+    frames, H = 13, 8
+    D = H * 64
+    g = torch.Generator(device=dev).manual_seed(S)
+    qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
+    out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+    qf = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = _ref_attn(qf.reshape(frames, S, 3 * D), (frames,), S, H, False)
+    assert rel(out.reshape(frames, S, D), o_ref) < 1e-2
+    assert rel(out32.reshape(frames, S, D), o_ref) < 1e-2
+    assert rel(out.reshape(frames, S, D)[:, -1], o_ref[:, -1]) < 1e-2  # the CUDA-core 257th row
+    assert rel(lse, lse_ref) < 1e-4
+    go = torch.randn(o_ref.shape, device=dev, generator=g)
+    o_ref.backward(go)
+    dqkv = torch.full_like(qkv, float("nan"))
+    Kn.attn_spatial_bwd(qkv, out32, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv)
+    assert torch.isfinite(dqkv.float()).all()
+    for i in range(3):
+        got, ref = dqkv[:, i * D:(i + 1) * D], qf.grad[:, i * D:(i + 1) * D]
+        assert rel(got, ref) < 2e-2, "qkv"[i]
+        assert rel(got.reshape(frames, S, D)[:, -1], ref.reshape(frames, S, D)[:, -1]) < 2e-2, "qkv"[i]
+
+
+@pytest.mark.parametrize("T", [16, 5, 1])
+def test_attn_temporal_fwd_bwd(T):
+    B, S, H = 2, 257, 8
+    D = H * 64
+    g = torch.Generator(device=dev).manual_seed(T)
+    qkv = (torch.randn(B * T * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
+    out, lse = Kn.attn_temporal_fwd(qkv, B, T, S, H)
+    qf = qkv.float().requires_grad_(True)
+    x = qf.reshape(B, T, S, 3 * D).transpose(1, 2)
+    o_ref, lse_ref = _ref_attn(x, (B, S), T, H, True)
+    assert rel(out.reshape(B, T, S, D).transpose(1, 2), o_ref) < 1e-2
+    assert rel(lse.reshape(B, S, H, T), lse_ref) < 1e-4
+    go = torch.randn(o_ref.shape, device=dev, generator=g)
+    o_ref.backward(go)
+    dout = go.transpose(1, 2).reshape(B * T * S, D).bfloat16().contiguous()
+    dqkv = Kn.attn_temporal_bwd(qkv, out, dout, lse, B, T, S, H)
+    scale = float(qf.grad[:, 2 * D:].norm())
+    for i in range(3):
+        got, ref = dqkv[:, i * D:(i + 1) * D].float(), qf.grad[:, i * D:(i + 1) * D]
+        if T == 1 and i < 2:  # one key: softmax has no gradient, dq = dk = 0 exactly
+            assert float(got.norm()) < 1e-3 * scale, "qkv"[i]
+        else:
+            assert rel(got, ref) < 2e-2, "qkv"[i]

@@ -46,12 +46,14 @@ for akm in (1, 0):
         run(128, 64, 64, akm, bkm)
         run(1000, 1536, 512, akm, bkm, epi=L.EPI_BF16)
 run(512, 512, 4096, 0, 0, split=4)
+run(500, 300, 2048, 0, 0, split=3)
+run(1000, 1536, 2048, 0, 0, split=2)
 run(333, 48, 512, 1, 0)
 run(333, 512, 48, 1, 0)
 run(333, 32, 512, 1, 0)
 
 # timing of the big forward shapes
-def bench(M, N, K, akm=1, bkm=0, epi=L.EPI_BF16, split=1):
+def bench(M, N, K, akm=1, bkm=0, epi=L.EPI_BF16, split=1, aux=False):
     A = torch.randn(M, K, device=dev).bfloat16() if akm else torch.randn(K, M, device=dev).bfloat16()
     B = torch.randn(K, N, device=dev).bfloat16() if not bkm else torch.randn(N, K, device=dev).bfloat16()
     D = torch.empty(M, N, device=dev, dtype=torch.bfloat16 if epi == L.EPI_BF16 else torch.float32)
@@ -60,7 +62,13 @@ def bench(M, N, K, akm=1, bkm=0, epi=L.EPI_BF16, split=1):
     ws = None
     if split > 1:
         ws = torch.empty(L.load().jz_gemm_workspace_bytes(M, N, split) // 4 + 1, device=dev)
-    args = (A.data_ptr(), lda, akm, B.data_ptr(), ldb, bkm, D.data_ptr(), N, M, N, K, epi, None, None, 0, None, 0, split, L.ptr(ws), L.stream_ptr())
+    bias = torch.randn(N, device=dev) if split == 1 else None
+    AUX = torch.randn(M, N, device=dev) if epi == L.EPI_RESID else None
+    D2 = torch.empty(M, N, device=dev, dtype=torch.bfloat16) if epi == L.EPI_GELU else None
+    if epi == L.EPI_GELU:
+        D = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    args = (A.data_ptr(), lda, akm, B.data_ptr(), ldb, bkm, D.data_ptr(), N, M, N, K, epi, L.ptr(bias), L.ptr(AUX), N,
+            L.ptr(D2), N, split, L.ptr(ws), L.stream_ptr())
     for _ in range(3):
         L.call("jz_gemm_bf16", *args)
     torch.cuda.synchronize()
@@ -74,14 +82,14 @@ def bench(M, N, K, akm=1, bkm=0, epi=L.EPI_BF16, split=1):
     ms = e0.elapsed_time(e1) / n
     tf = 2 * M * N * K / ms / 1e9
     Ab = A.float() if False else None
-    print(f"bench M={M} N={N} K={K} akm={akm} bkm={bkm} split={split}: {ms*1e3:.1f} us  {tf:.0f} TFLOP/s", flush=True)
+    print(f"bench M={M} N={N} K={K} akm={akm} bkm={bkm} epi={epi} split={split}: {ms*1e3:.1f} us  {tf:.0f} TFLOP/s", flush=True)
 
 
 M = 148032
 bench(M, 1536, 512)
-bench(M, 512, 512, epi=L.EPI_F32)
-bench(M, 2048, 512)
-bench(M, 512, 2048, epi=L.EPI_F32)
+bench(M, 512, 512, epi=L.EPI_RESID)
+bench(M, 2048, 512, epi=L.EPI_GELU)
+bench(M, 512, 2048, epi=L.EPI_RESID)
 bench(M, 512, 1536, akm=1, bkm=1, epi=L.EPI_F32)
 bench(512, 1536, M, akm=0, bkm=0, epi=L.EPI_F32, split=6)
 bench(2048, 512, M, akm=0, bkm=0, epi=L.EPI_F32, split=4)

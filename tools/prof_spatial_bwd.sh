@@ -1,0 +1,40 @@
+#!/bin/bash
+# Build a profiling variant of libjz (clock64 marks in the spatial backward) into /tmp and run it.
+set -e
+cd "$(dirname "$0")/.."
+mkdir -p /tmp/jzprof
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DJZ_ATTN_PROF -Iinclude -c paper_2510_27002_b200/csrc/attn_spatial.cu -o /tmp/jzprof/attn_spatial.o
+objs=""
+for f in paper_2510_27002_b200/lib/obj/*.o; do b=$(basename $f); [ "$b" = attn_spatial.o ] || objs="$objs $f"; done
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o /tmp/jzprof/libjz.so /tmp/jzprof/attn_spatial.o $objs -Xcompiler -fPIC -lpthread -ldl -lrt
+python - <<'PY'
+import ctypes as C, torch, numpy as np
+import paper_2510_27002_b200._lib as L
+L.LIB_PATH = __import__("pathlib").Path("/tmp/jzprof/libjz.so")
+L.ensure_device()
+lib = L.load()
+frames, S, H = 576, 257, 8
+D = H * 64
+qkv = torch.randn(frames * S, 3 * D, device="cuda").bfloat16()
+out = torch.empty(frames * S, D, device="cuda", dtype=torch.bfloat16)
+o32 = torch.empty(frames * S, D, device="cuda")
+lse = torch.empty(frames, H, S, device="cuda")
+dq = torch.empty_like(qkv)
+L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
+for _ in range(3):
+    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), L.stream_ptr())
+torch.cuda.synchronize()
+buf = np.zeros(64 * 32, dtype=np.uint64)
+lib.jz_attn_prof_read.argtypes = [C.c_void_p]
+assert lib.jz_attn_prof_read(buf.ctypes.data) == 0
+t = buf.reshape(64, 32).astype(np.int64)
+names = {0: "start", 22: "bar1 passed", 23: "P1 loads done", 24: "bar2 passed", 25: "P2 main done", 1: "prologue done", 18: "dq_full", 19: "dq done", 20: "tail ready", 21: "tail inputs free"}
+for g in range(4):
+    names[2 + 4 * g] = f"sdp_full[{g}]"; names[3 + 4 * g] = f"pds_free ok[{g}]"; names[4 + 4 * g] = f"pds written[{g}]"; names[5 + 4 * g] = f"dkdv done[{g}]"
+for u in (2, 3, 10):
+    base = t[u, 0]
+    print(f"unit {u}: total {t[u + 1, 0] - base} cycles")
+    for k in sorted(names):
+        if t[u, k]:
+            print(f"   {names[k]:18s} {t[u, k] - base:8d}")
+PY
