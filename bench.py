@@ -321,11 +321,14 @@ def main() -> None:
 
     peaks = _peaks()
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-    traffic = None
+    traffic, traffic_note = None, None
     tf = ROOT / "profiles" / "roofline_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("gemm_dram_bytes_per_launch")
+            tj = json.loads(tf.read_text())
+            traffic = tj.get("gemm_dram_bytes_per_launch")
+            traffic_note = {"kernel": tj.get("kernel"), "algorithmic_bytes": tj.get("algorithmic_bytes"),
+                            "source": tj.get("source")}
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": "jz::gemm_bf16_kernel (all K1 GEMM launches of the step)",
@@ -333,7 +336,7 @@ def main() -> None:
                 "frac": round(achieved / peaks["bf16_sustained"], 4), "traffic": traffic,
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained",
                 "gemm_share_of_step": round(gemm_ms / args.steps / ms, 4), "gemm_launches_per_step": gemm_launches // args.steps,
-                "algorithmic_flops_per_step": gemm_flops // args.steps}
+                "algorithmic_flops_per_step": gemm_flops // args.steps, "traffic_launch": traffic_note}
     step_flops = 42.13e9 * frames_per_step / world  # SURVEY §8d algorithmic FLOPs per GPU-step
     if rank == 0:
         cpu = None

@@ -52,8 +52,12 @@ __device__ long long g_gemm_ph[64 * 4];
 
 namespace jz {
 
-constexpr int kEpiWarps = 8;                     // 2 warps per TMEM lane quarter
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // + TMA warp + MMA warp
+// epilogue warps: 2 per TMEM lane quarter (16 measured slower: register cap 96 + spills and one
+// fewer pipeline stage)
+template <bool PAIR>
+constexpr int epi_warps() { return 8; }
+template <bool PAIR>
+constexpr int gemm_threads() { return 64 + 32 * epi_warps<PAIR>(); }
 constexpr int BM = 128;
 constexpr int BK = 64;
 
@@ -103,7 +107,9 @@ struct GemmShape {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int STG_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B, 128B-swizzled
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + kEpiWarps * STG_BYTES + 1024 + 256 + BN * 4;
+  static constexpr int EW = epi_warps<PAIR>();
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EW * STG_BYTES + 1024 + BAR_BYTES + BN * 4;
 };
 
 JZ_DEV float fast_tanh(float x) {
@@ -253,7 +259,7 @@ JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], fl
 }
 
 template <int BN, bool A_MN, bool B_MN, bool PAIR>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ EpiMaps em, GemmParams p, float* ws) {
   using S = GemmShape<BN, PAIR>;
@@ -264,6 +270,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  constexpr int kEpiWarps = S::EW;
   uint8_t* stg_base = smem + S::STAGES * S::STAGE_BYTES;  // kEpiWarps x 4 KB (1024-aligned)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * S::STG_BYTES);
   uint64_t* empty_bar = full_bar + S::STAGES;
@@ -271,7 +278,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
-  float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + 256);  // [BN]
+  float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + S::BAR_BYTES);  // [BN]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -406,8 +413,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
     const uint32_t quarter = warp & 3;
     const int ew = warp - 2;
-    const int chalf = ew >> 2;
-    constexpr int HALF = BN / 2;
+    const int chalf = ew >> 2;                 // column slot of this warp
+    constexpr int HALF = BN / (kEpiWarps / 4);  // columns per warp
     const int etid = threadIdx.x - 64;  // 0 .. 32*kEpiWarps-1
     uint8_t* stg = stg_base + ew * S::STG_BYTES;
     uint32_t apar = 0;
@@ -464,17 +471,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           float v[64];
           PH_T(t_b);
           {
-            uint32_t r0[32];
-            tmem_ld_32x32b_x32(tbase + cc * CW, r0);
+            uint32_t* r = reinterpret_cast<uint32_t*>(v);
+            tmem_ld_32x32b_x32(tbase + cc * CW, *reinterpret_cast<uint32_t(*)[32]>(r));
+            if (!f32out) tmem_ld_32x32b_x32(tbase + cc * CW + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
             tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
-            if (!f32out) {
-              tmem_ld_32x32b_x32(tbase + cc * CW + 32, r0);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r0[j]);
-            }
           }
           PH_ADD(1, t_b);
           PH_T(t_c);
@@ -532,12 +532,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if (p.store_tma) {
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0) {
+                if (lane == 0 && GDBG != 4) {
                   tma_store_2d(&em.d2, stg, n, row0);
                   bulk_commit();
                 }
+                if (GDBG != 5) {
 #pragma unroll
-                for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);  // overlaps the store's smem read
+                  for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);  // overlaps the store's smem read
+                }
                 if (lane == 0) bulk_wait_read0();
               } else {
                 __syncwarp();
@@ -649,7 +651,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
     const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs, 1, 1);
-    cfg.blockDim = dim3(kGemmThreads, 1, 1);
+    cfg.blockDim = dim3(gemm_threads<PAIR>(), 1, 1);
     cfg.dynamicSmemBytes = S::SMEM_BYTES;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -663,7 +665,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
     count_launch();
   } else {
     const int grid = units < num_sms() ? units : num_sms();
-    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR><<<grid, kGemmThreads, S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
+    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR><<<grid, gemm_threads<PAIR>(), S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
     JZ_LAUNCH_CHECK();
   }
   return JZ_OK;

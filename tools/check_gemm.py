@@ -62,8 +62,11 @@ def bench(M, N, K, akm=1, bkm=0, epi=L.EPI_BF16, split=1, aux=False):
     ws = None
     if split > 1:
         ws = torch.empty(L.load().jz_gemm_workspace_bytes(M, N, split) // 4 + 1, device=dev)
-    bias = torch.randn(N, device=dev) if split == 1 else None
+    bias = torch.randn(N, device=dev) if split == 1 and epi != L.EPI_GELU_BWD else None
     AUX = torch.randn(M, N, device=dev) if epi == L.EPI_RESID else None
+    if epi == L.EPI_GELU_BWD:
+        AUX = torch.randn(M, N, device=dev).bfloat16()
+        D = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
     D2 = torch.empty(M, N, device=dev, dtype=torch.bfloat16) if epi == L.EPI_GELU else None
     if epi == L.EPI_GELU:
         D = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
@@ -91,6 +94,7 @@ bench(M, 512, 512, epi=L.EPI_RESID)
 bench(M, 2048, 512, epi=L.EPI_GELU)
 bench(M, 512, 2048, epi=L.EPI_RESID)
 bench(M, 512, 1536, akm=1, bkm=1, epi=L.EPI_F32)
+bench(M, 2048, 512, akm=1, bkm=1, epi=L.EPI_GELU_BWD)
 bench(512, 1536, M, akm=0, bkm=0, epi=L.EPI_F32, split=6)
 bench(2048, 512, M, akm=0, bkm=0, epi=L.EPI_F32, split=4)
 print("ALL OK" if ok else "SOME FAILED")
