@@ -186,10 +186,13 @@ JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_
 JZ_API int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
                                float* out_f32, float* lse, jz_stream_t stream);
 /* dqkv bf16 [frames*S, 3*H*64] (fully overwritten).  out_f32 is the forward's fp32
- * output: D_i = dO_i . O_i is formed from it so dP - D does not cancel against the
- * bf16 rounding of O. */
+ * output: Delta_i = dO_i . O_i is formed from it (first launch, into `workspace`) so
+ * dP - Delta does not cancel against the bf16 rounding of O.  workspace: caller-owned,
+ * jz_attn_spatial_bwd_workspace_bytes(frames, S, H) bytes, 16-byte aligned. */
+JZ_API int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H);
 JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
-                               int64_t frames, int S, int H, int head_dim, void* dqkv, jz_stream_t stream);
+                               int64_t frames, int S, int H, int head_dim, void* dqkv, void* workspace,
+                               jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K4  causal temporal (inter-frame) attention (st.py:74-76, nn.py:103-105):

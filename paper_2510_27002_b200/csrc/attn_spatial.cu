@@ -11,6 +11,8 @@
 // on CUDA cores — exactly, no padding waste.
 //
 // qkv bf16 [M, 3D] (row = frame*S + s), out bf16 [M, D], lse f32 [frame][H][S].
+#include <mutex>
+
 #include "common.h"
 #include "ptx.cuh"
 
@@ -18,9 +20,7 @@ namespace jz {
 
 namespace sp {
 
-constexpr int kThreads = 256;   // backward: w0 TMA, w1 MMA, w2-5 P/dS + epilogues, w6-7 tail row
 constexpr int kFwdThreads = 384;  // forward: w0 TMA, w1 MMA, w2-5 tile 0, w6-9 tile 1, w10-11 tail row
-constexpr int kBwdThreads = 384;  // backward: w0 TMA, w1 MMA, w2-9 two P/dS warpgroups, w10-11 tail
 constexpr int TILE = 16384;    // 128 rows x 128 B
 // forward smem map (bytes, from a 1024-aligned base)
 constexpr int F_Q = 0;                 // 2 tiles
@@ -157,7 +157,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t par = i & 1;
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
-      const int64_t grow = row0 + 128 * t + r;
       // previous unit's TMA stores must have finished reading this tile's P buffer
       if (wtid == 0) bulk_wait_read0();
       named_bar(1 + t, 128);
@@ -405,19 +404,25 @@ extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H
 }
 
 // ============================================================================
-// Backward.  Per (frame, head), in the transposed ("S^T") formulation: for each
-// key half j (128 keys) and query tile t (128 queries)
-//   S^T  = K_j Q_t^T,  dP^T = V_j dO_t^T                         (TMEM, 2 x 128 cols)
-//   P^T  = exp(S^T*scale - lse),  dS^T = P^T (dP^T - Dq)            (CUDA cores -> smem bf16)
-//   dV_j += P^T dO_t,  dK_j += dS^T Q_t,  dQ_t += dS K_j           (TMEM accumulators)
-// The dS tile written K-major over queries for dK is read MN-major as the A operand
-// of dQ, so one smem copy serves both products.  Query/key 256 terms on CUDA cores.
+// Backward.  Per (frame, head) unit, in the transposed ("S^T") formulation, over
+// 8 blocks x = (key half j in 0..1) x (64-query block c in 0..3):
+//   S^T  = K_j Q_c^T,  dP^T = V_j dO_c^T          (TMEM, double-buffered 2 x 128 cols)
+//   P^T  = exp2(S^T*c2 - lse2),  dS^T = P^T (dP^T - D)      (8 "P/dS" warps)
+//        P^T goes back into TMEM over its own S^T columns (bf16 pairs), dS^T to smem slot c
+//   dV_j += P^T dO_c  (A from TMEM),  dK_j += dS^T Q_c,   and per query tile t = c/2:
+//   dQ_t += dS K_j    (A = slots 2t, 2t+1 read MN-major)    (TMEM accumulators, 256 cols)
+// The MMA warp issues S/dP of block x+1 before the gradient MMAs of block x, so the
+// tensor core overlaps the elementwise stage. Delta = rowsum(dO o O_f32) comes from a
+// separate coalesced pass (spatial_delta_kernel). The P/dS warps also form the row-256 /
+// key-256 dot products of each key half; a 4-warp helper group reduces the row-256
+// gradients, runs the three epilogues (TMEM -> swizzled smem -> coalesced stores, TMEM
+// released before the stores), and prefetches the next unit's lse / Delta / tail vectors.
 // ============================================================================
 #ifdef JZ_ATTN_PROF
 __device__ unsigned long long g_attn_prof[64 * 32];
 #define PROF_MARK(slot)                                                                   \
   do {                                                                                    \
-    if (blockIdx.x == 0 && i < 32) g_attn_prof[i * 32 + (slot)] = clock64();             \
+    if (blockIdx.x == 0 && i < 32) g_attn_prof[i * 64 + (slot)] = clock64();             \
   } while (0)
 #else
 #define PROF_MARK(slot) \
@@ -426,33 +431,74 @@ __device__ unsigned long long g_attn_prof[64 * 32];
 #endif
 namespace jz {
 namespace sp {
+constexpr int kBwdWarps = 14;  // w0 TMA, w1 MMA, w2-9 P/dS, w10-13 helper (tail + epilogues + prep)
+constexpr int kBwdThreads2 = 32 * kBwdWarps;
 constexpr int B_Q = 0;
 constexpr int B_K = B_Q + 2 * TILE;
 constexpr int B_V = B_K + 2 * TILE;
 constexpr int B_DO = B_V + 2 * TILE;
-constexpr int B_PT = B_DO + 2 * TILE;   // [2 query atoms][128 key rows][128 B]
-constexpr int B_DST = B_PT + 2 * TILE;
-constexpr int B_END = B_DST + 2 * TILE;  // 196608
+constexpr int B_DS = B_DO + 2 * TILE;    // 4 slots [128 keys][64 queries] bf16, slot = query block
+constexpr int B_ST = B_DS + 4 * TILE;    // epilogue staging tile [128 rows][64] bf16 (TMA store)
+constexpr int B_END = B_ST + TILE;       // 212992
 
 struct BwdSmallSmem {
-  uint64_t load_full, inputs_free, sdp_full, pds_full, pds_free, dkdv_full, dkdv_free, dq_full, dq_free,
-      tail_ready;
+  uint64_t load_full, inputs_free, dkdv_full, dkdv_free, dq_full, dq_free;
+  uint64_t sdp_full[2], pds_full[2], ds_free[2], prep_ready[2], tail_ready[2];
+
   uint32_t tmem_base;
-  float lse2[260];
-  float Dv[260];
-  float p_col[260], ds_col[260];  // key 256 column over queries 0..256
-  float p_row[260], ds_row[260];  // query 256 row over keys 0..256
-  float q256[64], do256[64], k256[64], v256[64];
-  float tail_red[3][64][2];
+  // per-unit vectors, double-buffered: written by the helper one unit ahead
+  alignas(16) float lse2[2][260];
+  alignas(16) float Dv[2][260];
+  float p_col[2][260], ds_col[2][260];  // key 256 column over queries 0..256
+  alignas(16) float q256[2][64];
+  alignas(16) float do256[2][64];
+  alignas(16) float k256[2][64];
+  alignas(16) float v256[2][64];
+  float p_row[260], ds_row[260];        // query 256 row over keys 0..256 (current unit)
+  float tail_red[3][4][64];
 };
 constexpr int B_SMEM = B_END + 1024 + (int)sizeof(BwdSmallSmem) + 64;
+static_assert(B_SMEM <= 232448, "spatial bwd smem budget");
 }  // namespace sp
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+// One warp writes its 32 rows (64 bf16 each) coalesced: stage row-per-lane in its own 4 KB
+// (128B-swizzled), then read back 4 rows x 128 B per instruction.
+// TMEM row (64 fp32 columns at taddr) -> sc * (acc + coef * vec) -> bf16 straight into the staging row.
+JZ_DEV void bwd_stage_acc(uint8_t* wstage, uint32_t taddr, float coef, const float* vec, float sc, int lane) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t vv[16];
+    tmem_ld_32x32b_x16(taddr + 16 * q, vv);
+    tmem_ld_wait();
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 16; e += 2)
+      w[e / 2] = pack_bf16(sc * (__uint_as_float(vv[e]) + coef * vec[16 * q + e]),
+                           sc * (__uint_as_float(vv[e + 1]) + coef * vec[16 * q + e + 1]));
+    *reinterpret_cast<uint4*>(wstage + lane * 128 + (((2 * q) ^ (lane & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(wstage + lane * 128 + (((2 * q + 1) ^ (lane & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  __syncwarp();
+}
+
+JZ_DEV void bwd_flush_rows(const uint8_t* wstage, __nv_bfloat16* dqkv, int64_t row_first, int64_t ld3, int64_t col,
+                           int lane) {
+  const int cch = lane & 7;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int rr = 4 * k + (lane >> 3);
+    const uint4 w = *reinterpret_cast<const uint4*>(wstage + rr * 128 + ((cch ^ (rr & 7)) << 4));
+    *reinterpret_cast<uint4*>(dqkv + (row_first + rr) * ld3 + col + 8 * cch) = w;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     spatial_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ out,
+                       const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ delta,
                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
                        __nv_bfloat16* __restrict__ dqkv, int frames, int S, int H) {
+  using namespace sp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   BwdSmallSmem& sm = *reinterpret_cast<BwdSmallSmem*>(smem + B_END);
@@ -462,7 +508,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const bool has_tail = S > 256;
   const float scale = 0.125f;
   const float c2 = 0.125f * 1.4426950408889634f;
-  constexpr uint32_t C_ST = 0, C_DPT = 128, C_DV = 256, C_DK = 320, C_DQ = 384;
+  const int64_t ld3 = 3 * (int64_t)D;
+  constexpr uint32_t C_DV = 256, C_DK = 320, C_DQ = 384;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
@@ -470,15 +517,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.load_full, 1);
-    mbar_init(&sm.inputs_free, has_tail ? 65 : 1);
-    mbar_init(&sm.sdp_full, 1);
-    mbar_init(&sm.pds_full, 256);
-    mbar_init(&sm.pds_free, 1);
+    mbar_init(&sm.inputs_free, 1 + 4);  // MMA commit + 4 helper warps (row-256 reductions read the tiles)
     mbar_init(&sm.dkdv_full, 1);
-    mbar_init(&sm.dkdv_free, 256);
+    mbar_init(&sm.dkdv_free, 4);
     mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_free, 256);
-    mbar_init(&sm.tail_ready, 64);
+    mbar_init(&sm.dq_free, 4);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.sdp_full[b], 1);
+      mbar_init(&sm.pds_full[b], 8);
+      mbar_init(&sm.ds_free[b], 1);
+      mbar_init(&sm.prep_ready[b], 4);
+      mbar_init(&sm.tail_ready[b], 8);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -487,334 +537,359 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       int i = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         const int f = u / H, h = u % H;
         const int row0 = f * S;
         mbar_wait(&sm.inputs_free, (i & 1) ^ 1);
+        PROF_MARK(53);
         mbar_arrive_expect_tx(&sm.load_full, 8 * TILE);
         for (int t = 0; t < 2; ++t) {
-          tma_load_2d(smem + B_Q + t * TILE, &tm_qkv, &sm.load_full, h * 64, row0 + 128 * t);
           tma_load_2d(smem + B_K + t * TILE, &tm_qkv, &sm.load_full, D + h * 64, row0 + 128 * t);
+          tma_load_2d(smem + B_Q + t * TILE, &tm_qkv, &sm.load_full, h * 64, row0 + 128 * t);
           tma_load_2d(smem + B_V + t * TILE, &tm_qkv, &sm.load_full, 2 * D + h * 64, row0 + 128 * t);
           tma_load_2d(smem + B_DO + t * TILE, &tm_do, &sm.load_full, h * 64, row0 + 128 * t);
         }
       }
     }
   } else if (warp == 1) {
+    // ------------------------------ MMA issuer ------------------------------
     if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16_f32(128, 128, false, false);
-      constexpr uint32_t id_kv = idesc_bf16_f32(128, 64, false, true);
-      constexpr uint32_t id_q = idesc_bf16_f32(128, 64, true, true);
+      constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);   // K_j Q_c^T, V_j dO_c^T
+      constexpr uint32_t id_kv = idesc_bf16_f32(128, 64, false, true);   // P^T dO_c, dS^T Q_c
+      constexpr uint32_t id_q = idesc_bf16_f32(128, 64, true, true);     // dS K_j
       const uint32_t aq = smem_u32(smem + B_Q), ak = smem_u32(smem + B_K), av = smem_u32(smem + B_V),
-                     ado = smem_u32(smem + B_DO), apt = smem_u32(smem + B_PT), adst = smem_u32(smem + B_DST);
-      int i = 0;
-      uint32_t g = 0;  // running (j,t) iteration counter
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-        mbar_wait(&sm.load_full, i & 1);
-        for (int j = 0; j < 2; ++j) {
-          for (int t = 0; t < 2; ++t, ++g) {
-            if (t == 0) {
-              // C_DV/C_DK (and at j == 0 also C_DQ) are overwritten: wait for their readers
-              if (2 * i + j > 0) mbar_wait(&sm.dkdv_free, (2 * i + j - 1) & 1);
-              if (j == 0 && i > 0) mbar_wait(&sm.dq_free, (i - 1) & 1);
-              tc_fence_after();
-            }
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              umma_bf16_ss(tmem + C_ST, sdesc_sw128(ak + j * TILE + kk * 32, 16, 1024),
-                           sdesc_sw128(aq + t * TILE + kk * 32, 16, 1024), id_s, kk > 0);
-              umma_bf16_ss(tmem + C_DPT, sdesc_sw128(av + j * TILE + kk * 32, 16, 1024),
-                           sdesc_sw128(ado + t * TILE + kk * 32, 16, 1024), id_s, kk > 0);
-            }
-            umma_commit(&sm.sdp_full);
-            mbar_wait(&sm.pds_full, g & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-              const uint32_t aoff = (ks >> 2) * TILE + (ks & 3) * 32;
-              umma_bf16_ss(tmem + C_DV, sdesc_sw128(apt + aoff, 16, 1024),
-                           sdesc_sw128(ado + t * TILE + ks * 2048, 8192, 1024), id_kv, (t > 0 || ks > 0));
-              umma_bf16_ss(tmem + C_DK, sdesc_sw128(adst + aoff, 16, 1024),
-                           sdesc_sw128(aq + t * TILE + ks * 2048, 8192, 1024), id_kv, (t > 0 || ks > 0));
-              umma_bf16_ss(tmem + C_DQ + 64 * t, sdesc_sw128(adst + ks * 2048, 16384, 1024),
-                           sdesc_sw128(ak + j * TILE + ks * 2048, 8192, 1024), id_q, (j > 0 || ks > 0));
-            }
-            umma_commit(&sm.pds_free);
-            if (t == 1) umma_commit(&sm.dkdv_full);
-          }
+                     ado = smem_u32(smem + B_DO), ads = smem_u32(smem + B_DS);
+      // gradient MMAs of block y of unit i (its P^T / dS^T are ready once pds_full fires)
+      auto grad_mmas = [&](int i, int y) {
+        const uint32_t gy = 8u * i + y, by = gy & 1;
+        const int jy = y >> 2, cy = y & 3;
+        mbar_wait(&sm.pds_full[by], (gy >> 1) & 1);
+        PROF_MARK(10 + y);
+        tc_fence_after();
+        if (cy == 0 && 2 * i + jy > 0) {  // dV_j / dK_j are re-initialised: the epilogue must be done
+          mbar_wait(&sm.dkdv_free, (2 * i + jy - 1) & 1);
+          tc_fence_after();
         }
+        if (cy == 1 && jy == 0 && i > 0) {  // dQ re-initialised: previous unit's dQ epilogue done
+          mbar_wait(&sm.dq_free, (i - 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t qoff = (cy >> 1) * TILE + (cy & 1) * 8192;  // rows 64c.. of Q / dO
+        const uint32_t pcol = tmem + 128 * by;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t pa = pcol + (ks < 2 ? 8 * ks : 32 + 8 * (ks - 2));
+          umma_bf16_ts(tmem + C_DV, pa, sdesc_sw128(ado + qoff + ks * 2048, 8192, 1024), id_kv, (cy > 0 || ks > 0));
+          umma_bf16_ss(tmem + C_DK, sdesc_sw128(ads + cy * TILE + ks * 32, 16, 1024),
+                       sdesc_sw128(aq + qoff + ks * 2048, 8192, 1024), id_kv, (cy > 0 || ks > 0));
+        }
+        if (cy & 1) {
+          const int t = cy >> 1;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            umma_bf16_ss(tmem + C_DQ + 64 * t, sdesc_sw128(ads + 2 * t * TILE + ks * 2048, TILE, 1024),
+                         sdesc_sw128(ak + jy * TILE + ks * 2048, 8192, 1024), id_q, (jy > 0 || ks > 0));
+          umma_commit(&sm.ds_free[t]);
+        }
+        if (cy == 3) umma_commit(&sm.dkdv_full);
+        PROF_MARK(18 + y);
+      };
+      int i = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        PROF_MARK(0);
+        mbar_wait(&sm.load_full, i & 1);
+        PROF_MARK(1);
+        tc_fence_after();
+        for (int x = 0; x < 8; ++x) {
+          const uint32_t gx = 8u * i + x, b = gx & 1;
+          const int j = x >> 2, c = x & 3;
+          const uint32_t qoff = (c >> 1) * TILE + (c & 1) * 8192;
+          // TMEM buffer b was last read by the dV MMA of block gx-2, issued earlier by this thread
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            umma_bf16_ss(tmem + 128 * b, sdesc_sw128(ak + j * TILE + kk * 32, 16, 1024),
+                         sdesc_sw128(aq + qoff + kk * 32, 16, 1024), id_s, kk > 0);
+            umma_bf16_ss(tmem + 128 * b + 64, sdesc_sw128(av + j * TILE + kk * 32, 16, 1024),
+                         sdesc_sw128(ado + qoff + kk * 32, 16, 1024), id_s, kk > 0);
+          }
+          umma_commit(&sm.sdp_full[b]);
+          PROF_MARK(2 + x);
+          if (x > 0) grad_mmas(i, x - 1);
+        }
+        grad_mmas(i, 7);
         umma_commit(&sm.dq_full);
         umma_commit(&sm.inputs_free);
       }
     }
-  } else {
-    const bool main_role = warp < 10;
-    const int g = (warp - 2) >> 2;      // main: warpgroup 0/1
+  } else if (warp < 10) {
+    // ------------------------------ P / dS warps ------------------------------
     const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // main: TMEM lane / row within a 128 tile
-    const int wtid = threadIdx.x - 64;  // main: 0..255
-    const int tid = threadIdx.x - 320;  // tail: 0..63
+    const int half = (warp - 2) >> 2;      // query columns [32 half, 32 half + 32) of a block
+    const int r = quarter * 32 + lane;     // key row within the key half (TMEM lane)
+    const uint32_t base = tmem + ((quarter * 32) << 16);
     int i = 0;
-    uint32_t gi = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      const int pb = i & 1;
+      mbar_wait(&sm.prep_ready[pb], (i >> 1) & 1);
+      if (threadIdx.x == 64) PROF_MARK(26);
+      const float* lse2 = sm.lse2[pb];
+      const float* Dv = sm.Dv[pb];
+      for (int x = 0; x < 8; ++x) {
+        const uint32_t gx = 8u * i + x, b = gx & 1;
+        const int j = x >> 2, c = x & 3;
+        if ((c & 1) == 0 && 2 * i + j > 0) mbar_wait(&sm.ds_free[c >> 1], (2 * i + j - 1) & 1);
+        mbar_wait(&sm.sdp_full[b], (gx >> 1) & 1);
+        if (threadIdx.x == 64) PROF_MARK(27 + x);
+        tc_fence_after();
+        uint32_t vs[32], vd[32];
+        tmem_ld_32x32b_x32(base + 128 * b + 32 * half, vs);
+        tmem_ld_32x32b_x32(base + 128 * b + 64 + 32 * half, vd);
+        tmem_ld_wait();
+        const int q0 = 64 * c + 32 * half;
+        uint32_t pp[16], pd[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(lse2 + q0 + e);
+          const float4 d4 = *reinterpret_cast<const float4*>(Dv + q0 + e);
+          const float p0 = ex2(__uint_as_float(vs[e]) * c2 - l4.x);
+          const float p1 = ex2(__uint_as_float(vs[e + 1]) * c2 - l4.y);
+          const float p2 = ex2(__uint_as_float(vs[e + 2]) * c2 - l4.z);
+          const float p3 = ex2(__uint_as_float(vs[e + 3]) * c2 - l4.w);
+          pp[e / 2] = pack_bf16(p0, p1);
+          pp[e / 2 + 1] = pack_bf16(p2, p3);
+          pd[e / 2] = pack_bf16(p0 * (__uint_as_float(vd[e]) - d4.x), p1 * (__uint_as_float(vd[e + 1]) - d4.y));
+          pd[e / 2 + 1] = pack_bf16(p2 * (__uint_as_float(vd[e + 2]) - d4.z), p3 * (__uint_as_float(vd[e + 3]) - d4.w));
+        }
+        // P^T (bf16 pairs) over this warp's own S^T columns; dS^T into smem slot c
+        tmem_st_32x32b_x16(base + 128 * b + 32 * half, pp);
+        uint8_t* slot = smem + B_DS + c * TILE;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<uint4*>(slot + sw128(r, 4 * half + k)) =
+              make_uint4(pd[4 * k], pd[4 * k + 1], pd[4 * k + 2], pd[4 * k + 3]);
+        tmem_st_wait();
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pds_full[b]);
+        if (threadIdx.x == 64) PROF_MARK(35 + x);
+        if (c == 0 && has_tail) {
+          // CUDA-core tail terms of this key half, off the tensor-core path:
+          //   half 0: query 256 against key 128j + r   -> p_row, ds_row
+          //   half 1: key 256 against query 128j + r   -> p_col, ds_col
+          const int idx = 128 * j + r;
+          const uint8_t* at = smem + (half == 0 ? B_K : B_Q) + j * TILE;
+          const uint8_t* bt = smem + (half == 0 ? B_V : B_DO) + j * TILE;
+          const float* va = half == 0 ? sm.q256[pb] : sm.k256[pb];
+          const float* vb = half == 0 ? sm.do256[pb] : sm.v256[pb];
+          float a = 0.f, dp = 0.f;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint4 wa = *reinterpret_cast<const uint4*>(at + sw128(r, cc));
+            const uint4 wb = *reinterpret_cast<const uint4*>(bt + sw128(r, cc));
+            const float4 a0 = *reinterpret_cast<const float4*>(va + 8 * cc);
+            const float4 a1 = *reinterpret_cast<const float4*>(va + 8 * cc + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(vb + 8 * cc);
+            const float4 b1 = *reinterpret_cast<const float4*>(vb + 8 * cc + 4);
+            const float2 x0 = unpack_bf16(wa.x), x1 = unpack_bf16(wa.y), x2 = unpack_bf16(wa.z), x3 = unpack_bf16(wa.w);
+            const float2 y0 = unpack_bf16(wb.x), y1 = unpack_bf16(wb.y), y2 = unpack_bf16(wb.z), y3 = unpack_bf16(wb.w);
+            a += x0.x * a0.x + x0.y * a0.y + x1.x * a0.z + x1.y * a0.w + x2.x * a1.x + x2.y * a1.y + x3.x * a1.z + x3.y * a1.w;
+            dp += y0.x * b0.x + y0.y * b0.y + y1.x * b0.z + y1.y * b0.w + y2.x * b1.x + y2.y * b1.y + y3.x * b1.z + y3.y * b1.w;
+          }
+          if (half == 0) {
+            const float p = ex2(a * c2 - lse2[256]);
+            sm.p_row[idx] = p;
+            sm.ds_row[idx] = p * (dp - Dv[256]);
+          } else {
+            const float p = ex2(a * c2 - lse2[idx]);
+            sm.p_col[pb][idx] = p;
+            sm.ds_col[pb][idx] = p * (dp - Dv[idx]);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.tail_ready[j]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------ helper warpgroup ------------------------------
+    const int quarter = warp & 3;
+    const int ht = threadIdx.x - 320;     // 0..127
+    const int hw = warp - 10;             // helper warp 0..3
+    const int r = quarter * 32 + lane;    // TMEM lane for the epilogues
+    const uint32_t base = tmem + ((quarter * 32) << 16);
+    // prepare(u -> buffer pb): lse2, D (precomputed delta) and the row-256 vectors of unit u,
+    // one unit ahead; all loads are independent and issued together
+    auto prepare = [&](int u, int pb) {
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
-      const int64_t ld3 = 3 * (int64_t)D;
-      // ---- prologue P1: vectors of row 256 + lse ----
-      if (threadIdx.x == 64) PROF_MARK(0);
-      named_bar(1, 320);
-      if (threadIdx.x == 64) PROF_MARK(22);
-      if (main_role) {
-        if (wtid < 64) {
-          const int d = wtid;
-          const int64_t rr = row0 + 256;
-          sm.q256[d] = has_tail ? __bfloat162float(qkv[rr * ld3 + h * 64 + d]) : 0.f;
-          sm.k256[d] = has_tail ? __bfloat162float(qkv[rr * ld3 + D + h * 64 + d]) : 0.f;
-          sm.v256[d] = has_tail ? __bfloat162float(qkv[rr * ld3 + 2 * D + h * 64 + d]) : 0.f;
-          sm.do256[d] = has_tail ? __bfloat162float(dout[rr * D + h * 64 + d]) : 0.f;
-        }
-      } else {
-        for (int q = tid; q < S; q += 64) sm.lse2[q] = lse[((int64_t)f * H + h) * S + q] * 1.4426950408889634f;
+      const int64_t vb = ((int64_t)f * H + h) * S;
+      float l[3], dl[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int q = ht + 128 * k;
+        l[k] = q < S ? lse[vb + q] : 0.f;
+        dl[k] = q < S ? delta[vb + q] : 0.f;
       }
-      if (threadIdx.x == 64) PROF_MARK(23);
-      named_bar(1, 320);
-      if (threadIdx.x == 64) PROF_MARK(24);
-      // ---- prologue P2: D_q = dO_q . O_q, key-256 column ----
-      if (main_role) {
-        const int q = 128 * g + r;
-        const int64_t rr = row0 + q;
-        // fp32 O row from HBM (all 16 loads in flight), dO and Q rows from the staged smem tiles
-        const float4* op = reinterpret_cast<const float4*>(out + rr * D + h * 64);
-        float4 ov[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) ov[c] = __ldg(op + c);
-        mbar_wait(&sm.load_full, i & 1);
-        const uint8_t* gt = smem + B_DO + g * TILE;
-        const uint8_t* qt = smem + B_Q + g * TILE;
-        float dd = 0.f, sk = 0.f, dpv = 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 wg = *reinterpret_cast<const uint4*>(gt + sw128(r, c));
-          const uint4 wq = *reinterpret_cast<const uint4*>(qt + sw128(r, c));
-          const uint32_t ag[4] = {wg.x, wg.y, wg.z, wg.w}, aqv[4] = {wq.x, wq.y, wq.z, wq.w};
-          const float of[8] = {ov[2 * c].x, ov[2 * c].y, ov[2 * c].z, ov[2 * c].w,
-                               ov[2 * c + 1].x, ov[2 * c + 1].y, ov[2 * c + 1].z, ov[2 * c + 1].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 fg = unpack_bf16(ag[e]), fq = unpack_bf16(aqv[e]);
-            const int d = 8 * c + 2 * e;
-            dd += of[2 * e] * fg.x + of[2 * e + 1] * fg.y;
-            sk += fq.x * sm.k256[d] + fq.y * sm.k256[d + 1];
-            dpv += fg.x * sm.v256[d] + fg.y * sm.v256[d + 1];
-          }
-        }
-        sm.Dv[q] = dd;
-        if (threadIdx.x == 64) PROF_MARK(25);
-        if (has_tail) {
-          const float p = ex2(sk * c2 - sm.lse2[q]);
-          sm.p_col[q] = p;
-          sm.ds_col[q] = p * (dpv - dd);
-        }
-      } else if (has_tail) {
-        // row 256: the 64 tail threads each take one head dim, reduce over both warps
+      float v4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (ht < 64 && has_tail) {
         const int64_t rr = row0 + 256;
-        const int d = tid;
-        float dd = out[rr * D + h * 64 + d] * sm.do256[d];
-        float sk = sm.q256[d] * sm.k256[d];
-        float dpv = sm.do256[d] * sm.v256[d];
-        dd = warp_sum(dd);
+        v4[0] = __bfloat162float(qkv[rr * ld3 + h * 64 + ht]);
+        v4[1] = __bfloat162float(qkv[rr * ld3 + D + h * 64 + ht]);
+        v4[2] = __bfloat162float(qkv[rr * ld3 + 2 * D + h * 64 + ht]);
+        v4[3] = __bfloat162float(dout[rr * D + h * 64 + ht]);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int q = ht + 128 * k;
+        if (q < S) {
+          sm.lse2[pb][q] = l[k] * 1.4426950408889634f;
+          sm.Dv[pb][q] = dl[k];
+        }
+      }
+      if (ht < 64) {
+        sm.q256[pb][ht] = v4[0];
+        sm.k256[pb][ht] = v4[1];
+        sm.v256[pb][ht] = v4[2];
+        sm.do256[pb][ht] = v4[3];
+      }
+      named_bar(3, 128);
+      if (has_tail && hw == 0) {  // key-256 entry of query row 256
+        const int d = 2 * lane;
+        float sk = sm.q256[pb][d] * sm.k256[pb][d] + sm.q256[pb][d + 1] * sm.k256[pb][d + 1];
+        float dpv = sm.do256[pb][d] * sm.v256[pb][d] + sm.do256[pb][d + 1] * sm.v256[pb][d + 1];
         sk = warp_sum(sk);
         dpv = warp_sum(dpv);
         if (lane == 0) {
-          sm.tail_red[0][warp - 10][0] = dd;
-          sm.tail_red[1][warp - 10][0] = sk;
-          sm.tail_red[2][warp - 10][0] = dpv;
-        }
-        named_bar(2, 64);
-        if (tid == 0) {
-          const float ddt = sm.tail_red[0][0][0] + sm.tail_red[0][1][0];
-          const float skt = sm.tail_red[1][0][0] + sm.tail_red[1][1][0];
-          const float dpt = sm.tail_red[2][0][0] + sm.tail_red[2][1][0];
-          sm.Dv[256] = ddt;
-          const float p = ex2(skt * c2 - sm.lse2[256]);
-          sm.p_col[256] = p;
-          sm.ds_col[256] = p * (dpt - ddt);
+          const float p = ex2(sk * c2 - sm.lse2[pb][256]);
+          sm.p_col[pb][256] = p;
+          sm.ds_col[pb][256] = p * (dpv - sm.Dv[pb][256]);
         }
       }
-      named_bar(1, 320);
-      if (threadIdx.x == 64) PROF_MARK(1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.prep_ready[pb]);
+    };
+    // one warp writes its 32 rows (64 bf16 each) coalesced: stage row-per-lane in its own 4 KB
+    // of the staging tile (128B-swizzled), read back 4 rows x 128 B per instruction
+    uint8_t* wstage = smem + B_ST + quarter * 4096;
+#define stage_acc(col, coef, vec, sc) bwd_stage_acc(wstage, base + (col), (coef), (vec), (sc), lane)
+#define flush_rows(row_first, col) bwd_flush_rows(wstage, dqkv, (row_first), ld3, (col), lane)
 
-      if (main_role) {
-        const uint32_t base = tmem + ((quarter * 32) << 16);
-        for (int j = 0; j < 2; ++j) {
-          for (int t = 0; t < 2; ++t, ++gi) {
-            mbar_wait(&sm.sdp_full, gi & 1);
-            if (threadIdx.x == 64) PROF_MARK(2 + 4 * (2 * j + t));
-            tc_fence_after();
-            if (gi > 0) mbar_wait(&sm.pds_free, (gi - 1) & 1);
-            if (threadIdx.x == 64) PROF_MARK(3 + 4 * (2 * j + t));
-            // warpgroup g computes query columns [64g, 64g + 64) of this (j, t) tile -> atom g
-            uint8_t* at_p = smem + B_PT + g * TILE;
-            uint8_t* at_d = smem + B_DST + g * TILE;
-#pragma unroll 1
-            for (int cc = 0; cc < 4; ++cc) {
-              const int col = 64 * g + 16 * cc;
-              uint32_t vs[16], vd[16];
-              tmem_ld_32x32b_x16(base + C_ST + col, vs);
-              tmem_ld_32x32b_x16(base + C_DPT + col, vd);
-              tmem_ld_wait();
-              uint32_t pp[8], pd[8];
-#pragma unroll
-              for (int e = 0; e < 16; e += 2) {
-                const int q = 128 * t + col + e;
-                const float p0 = ex2(__uint_as_float(vs[e]) * c2 - sm.lse2[q]);
-                const float p1 = ex2(__uint_as_float(vs[e + 1]) * c2 - sm.lse2[q + 1]);
-                pp[e / 2] = pack_bf16(p0, p1);
-                pd[e / 2] = pack_bf16(p0 * (__uint_as_float(vd[e]) - sm.Dv[q]),
-                                      p1 * (__uint_as_float(vd[e + 1]) - sm.Dv[q + 1]));
-              }
-#pragma unroll
-              for (int qq = 0; qq < 2; ++qq) {
-                const uint32_t off = sw128(r, 2 * cc + qq);
-                *reinterpret_cast<uint4*>(at_p + off) = make_uint4(pp[4 * qq], pp[4 * qq + 1], pp[4 * qq + 2], pp[4 * qq + 3]);
-                *reinterpret_cast<uint4*>(at_d + off) = make_uint4(pd[4 * qq], pd[4 * qq + 1], pd[4 * qq + 2], pd[4 * qq + 3]);
-              }
-            }
-            fence_proxy_async();
-            tc_fence_before();
-            mbar_arrive(&sm.pds_full);
-            if (threadIdx.x == 64) PROF_MARK(4 + 4 * (2 * j + t));
-            if (t == 1) {
-              if (j == 0 && has_tail) mbar_wait(&sm.tail_ready, i & 1);
-              mbar_wait(&sm.dkdv_full, (2 * i + j) & 1);
-              tc_fence_after();
-              // warpgroup 0 writes dV, warpgroup 1 writes dK (key rows 128j + r)
-              const int key = 128 * j + r;
-              const int64_t rr = row0 + key;
-              const float coef = has_tail ? (g == 0 ? sm.p_row[key] : sm.ds_row[key]) : 0.f;
-              const float* vec = g == 0 ? sm.do256 : sm.q256;
-              const float sc = g == 0 ? 1.0f : scale;
-              uint4* dst = reinterpret_cast<uint4*>(dqkv + rr * ld3 + (g == 0 ? 2 * D : D) + h * 64);
-#pragma unroll 1
-              for (int c = 0; c < 2; ++c) {
-                uint32_t vv[32];
-                tmem_ld_32x32b_x32(base + (g == 0 ? C_DV : C_DK) + 32 * c, vv);
-                tmem_ld_wait();
-                float ov[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) ov[e] = sc * (__uint_as_float(vv[e]) + coef * vec[32 * c + e]);
-#pragma unroll
-                for (int qq = 0; qq < 4; ++qq)
-                  dst[4 * c + qq] = make_uint4(pack_bf16(ov[8 * qq], ov[8 * qq + 1]), pack_bf16(ov[8 * qq + 2], ov[8 * qq + 3]),
-                                               pack_bf16(ov[8 * qq + 4], ov[8 * qq + 5]), pack_bf16(ov[8 * qq + 6], ov[8 * qq + 7]));
-              }
-              tc_fence_before();
-              mbar_arrive(&sm.dkdv_free);
-              if (threadIdx.x == 64) PROF_MARK(5 + 4 * (2 * j + t));
-            }
-          }
-        }
-        // dQ epilogue: warpgroup g -> query tile g
-        mbar_wait(&sm.dq_full, i & 1);
-        if (threadIdx.x == 64) PROF_MARK(18);
-        tc_fence_after();
-        {
-          const int q = 128 * g + r;
-          const int64_t rr = row0 + q;
-          const float dsc = has_tail ? sm.ds_col[q] : 0.f;
-          uint4* dq_dst = reinterpret_cast<uint4*>(dqkv + rr * ld3 + h * 64);
-#pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
-            uint32_t vq[32];
-            tmem_ld_32x32b_x32(base + C_DQ + 64 * g + 32 * c, vq);
-            tmem_ld_wait();
-            float oq[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) oq[e] = scale * (__uint_as_float(vq[e]) + dsc * sm.k256[32 * c + e]);
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq)
-              dq_dst[4 * c + qq] = make_uint4(pack_bf16(oq[8 * qq], oq[8 * qq + 1]), pack_bf16(oq[8 * qq + 2], oq[8 * qq + 3]),
-                                              pack_bf16(oq[8 * qq + 4], oq[8 * qq + 5]), pack_bf16(oq[8 * qq + 6], oq[8 * qq + 7]));
-          }
-        }
+    int i = 0;
+    if (blockIdx.x < units) prepare(blockIdx.x, 0);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      const int f = u / H, h = u % H;
+      const int64_t row0 = (int64_t)f * S;
+      const int pb = i & 1;
+      mbar_wait(&sm.prep_ready[pb], (i >> 1) & 1);
+      mbar_wait(&sm.load_full, i & 1);
+      if (ht == 0) PROF_MARK(43);
+      const int64_t qrow0 = row0 + quarter * 32;  // first of this warp's 32 rows in a 128-row tile
+      // ---- (e) dV_0 / dK_0 ----
+      mbar_wait(&sm.dkdv_full, (2 * i) & 1);
+      if (has_tail) mbar_wait(&sm.tail_ready[0], i & 1);
+      if (ht == 0) PROF_MARK(46);
+      tc_fence_after();
+      {
+        const float cp = has_tail ? sm.p_row[r] : 0.f, cd = has_tail ? sm.ds_row[r] : 0.f;
+        stage_acc(C_DV, cp, sm.do256[pb], 1.0f);
+        flush_rows(qrow0, 2 * D + h * 64);
+        stage_acc(C_DK, cd, sm.q256[pb], scale);
         tc_fence_before();
-        mbar_arrive(&sm.dq_free);
-        if (threadIdx.x == 64) PROF_MARK(19);
-      } else if (has_tail) {
-        // ---- tail: query 256 row and key 256 column ----
-        mbar_wait(&sm.load_full, i & 1);
-        for (int k = tid; k < 256; k += 64) {
-          const uint8_t* kt = smem + B_K + (k >> 7) * TILE;
-          const uint8_t* vt = smem + B_V + (k >> 7) * TILE;
-          float a = 0.f, dp = 0.f;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint4 wk = *reinterpret_cast<const uint4*>(kt + sw128(k & 127, c));
-            const uint4 wv = *reinterpret_cast<const uint4*>(vt + sw128(k & 127, c));
-            const uint32_t ak[4] = {wk.x, wk.y, wk.z, wk.w}, av[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 fk = unpack_bf16(ak[e]), fv = unpack_bf16(av[e]);
-              const int d = 8 * c + 2 * e;
-              a += sm.q256[d] * fk.x + sm.q256[d + 1] * fk.y;
-              dp += sm.do256[d] * fv.x + sm.do256[d + 1] * fv.y;
-            }
-          }
-          const float p = ex2(a * c2 - sm.lse2[256]);
-          sm.p_row[k] = p;
-          sm.ds_row[k] = p * (dp - sm.Dv[256]);
-        }
-        if (tid == 0) {
-          sm.p_row[256] = sm.p_col[256];
-          sm.ds_row[256] = sm.ds_col[256];
-        }
-        mbar_arrive(&sm.tail_ready);
-        if (tid == 0) PROF_MARK(20);
-        named_bar(2, 64);
-        const int dpair = tid & 31, half = tid >> 5;
-        const uint32_t chunk = dpair >> 2, within = (dpair & 3) * 4;
-        float aq0 = 0.f, aq1 = 0.f, ak0 = 0.f, ak1 = 0.f, av0 = 0.f, av1 = 0.f;
-        const uint8_t* kt = smem + B_K + half * TILE;
-        const uint8_t* qt = smem + B_Q + half * TILE;
-        const uint8_t* gt = smem + B_DO + half * TILE;
-#pragma unroll 4
-        for (int rr = 0; rr < 128; ++rr) {
-          const uint32_t off = sw128(rr, chunk) + within;
-          const int idx = half * 128 + rr;
-          const float2 fk = unpack_bf16(*reinterpret_cast<const uint32_t*>(kt + off));
-          const float2 fq = unpack_bf16(*reinterpret_cast<const uint32_t*>(qt + off));
-          const float2 fg = unpack_bf16(*reinterpret_cast<const uint32_t*>(gt + off));
-          const float dsr = sm.ds_row[idx], dsc = sm.ds_col[idx], pc = sm.p_col[idx];
-          aq0 += dsr * fk.x; aq1 += dsr * fk.y;   // dQ_256 over keys
-          ak0 += dsc * fq.x; ak1 += dsc * fq.y;   // dK_256 over queries
-          av0 += pc * fg.x; av1 += pc * fg.y;     // dV_256 over queries
-        }
-        mbar_arrive(&sm.inputs_free);
-        if (tid == 0) PROF_MARK(21);
-        if (half == 1) {
-          const int d = 2 * dpair;
-          aq0 += sm.ds_row[256] * sm.k256[d]; aq1 += sm.ds_row[256] * sm.k256[d + 1];
-          ak0 += sm.ds_col[256] * sm.q256[d]; ak1 += sm.ds_col[256] * sm.q256[d + 1];
-          av0 += sm.p_col[256] * sm.do256[d]; av1 += sm.p_col[256] * sm.do256[d + 1];
-          sm.tail_red[0][dpair][0] = aq0; sm.tail_red[0][dpair][1] = aq1;
-          sm.tail_red[1][dpair][0] = ak0; sm.tail_red[1][dpair][1] = ak1;
-          sm.tail_red[2][dpair][0] = av0; sm.tail_red[2][dpair][1] = av1;
-        }
-        named_bar(2, 64);
-        if (half == 0) {
-          const int64_t rr = row0 + 256;
-          const int d = 2 * dpair;
-          aq0 += sm.tail_red[0][dpair][0]; aq1 += sm.tail_red[0][dpair][1];
-          ak0 += sm.tail_red[1][dpair][0]; ak1 += sm.tail_red[1][dpair][1];
-          av0 += sm.tail_red[2][dpair][0]; av1 += sm.tail_red[2][dpair][1];
-          *reinterpret_cast<uint32_t*>(dqkv + rr * ld3 + h * 64 + d) = pack_bf16(scale * aq0, scale * aq1);
-          *reinterpret_cast<uint32_t*>(dqkv + rr * ld3 + D + h * 64 + d) = pack_bf16(scale * ak0, scale * ak1);
-          *reinterpret_cast<uint32_t*>(dqkv + rr * ld3 + 2 * D + h * 64 + d) = pack_bf16(av0, av1);
-        }
-        named_bar(2, 64);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.dkdv_free);
+        flush_rows(qrow0, D + h * 64);
       }
+      if (ht == 0) PROF_MARK(47);
+      // ---- (b) row 256: dQ_256 = sum_k ds_row K_k, dK_256 = sum_q ds_col Q_q, dV_256 = sum_q p_col dO_q ----
+      if (has_tail) {
+        mbar_wait(&sm.tail_ready[1], i & 1);
+        mbar_wait(&sm.load_full, i & 1);
+        {
+          const int dpair = ht & 31, part = ht >> 5;  // 2 dims, 64 rows per part
+          const uint32_t chunk = dpair >> 2, within = (dpair & 3) * 4;
+          float aq0 = 0.f, aq1 = 0.f, ak0 = 0.f, ak1 = 0.f, av0 = 0.f, av1 = 0.f;
+          const uint8_t* kt = smem + B_K + (part >> 1) * TILE;
+          const uint8_t* qt = smem + B_Q + (part >> 1) * TILE;
+          const uint8_t* gt = smem + B_DO + (part >> 1) * TILE;
+          const float* pc = sm.p_col[pb];
+          const float* dc = sm.ds_col[pb];
+#pragma unroll 4
+          for (int k = 0; k < 64; ++k) {
+            const int rr = (part & 1) * 64 + k;
+            const uint32_t off = sw128(rr, chunk) + within;
+            const int idx = (part >> 1) * 128 + rr;
+            const float2 fk = unpack_bf16(*reinterpret_cast<const uint32_t*>(kt + off));
+            const float2 fq = unpack_bf16(*reinterpret_cast<const uint32_t*>(qt + off));
+            const float2 fg = unpack_bf16(*reinterpret_cast<const uint32_t*>(gt + off));
+            const float dsr = sm.ds_row[idx], dsc = dc[idx], pcc = pc[idx];
+            aq0 += dsr * fk.x; aq1 += dsr * fk.y;
+            ak0 += dsc * fq.x; ak1 += dsc * fq.y;
+            av0 += pcc * fg.x; av1 += pcc * fg.y;
+          }
+          sm.tail_red[0][part][2 * dpair] = aq0; sm.tail_red[0][part][2 * dpair + 1] = aq1;
+          sm.tail_red[1][part][2 * dpair] = ak0; sm.tail_red[1][part][2 * dpair + 1] = ak1;
+          sm.tail_red[2][part][2 * dpair] = av0; sm.tail_red[2][part][2 * dpair + 1] = av1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.inputs_free);  // this warp is done with the staged tiles
+        named_bar(3, 128);
+        if (ht == 0) PROF_MARK(45);
+        if (ht < 64) {
+          const int d = ht;
+          const int64_t rr = row0 + 256;
+          float sq = sm.ds_col[pb][256] * sm.k256[pb][d], skk = sm.ds_col[pb][256] * sm.q256[pb][d],
+                sv = sm.p_col[pb][256] * sm.do256[pb][d];
+#pragma unroll
+          for (int pt = 0; pt < 4; ++pt) {
+            sq += sm.tail_red[0][pt][d];
+            skk += sm.tail_red[1][pt][d];
+            sv += sm.tail_red[2][pt][d];
+          }
+          dqkv[rr * ld3 + h * 64 + d] = __float2bfloat16_rn(scale * sq);
+          dqkv[rr * ld3 + D + h * 64 + d] = __float2bfloat16_rn(scale * skk);
+          dqkv[rr * ld3 + 2 * D + h * 64 + d] = __float2bfloat16_rn(sv);
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.inputs_free);
+      }
+      // ---- next unit's vectors (the P/dS warps of this unit are past j = 0 already) ----
+      if (u + (int)gridDim.x < units) prepare(u + gridDim.x, pb ^ 1);
+      if (ht == 0) PROF_MARK(48);
+      // ---- (f) dV_1 / dK_1 ----
+      mbar_wait(&sm.dkdv_full, (2 * i + 1) & 1);
+      if (ht == 0) PROF_MARK(49);
+      tc_fence_after();
+      {
+        const int key = 128 + r;
+        const float cp = has_tail ? sm.p_row[key] : 0.f, cd = has_tail ? sm.ds_row[key] : 0.f;
+        stage_acc(C_DV, cp, sm.do256[pb], 1.0f);
+        flush_rows(qrow0 + 128, 2 * D + h * 64);
+        stage_acc(C_DK, cd, sm.q256[pb], scale);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.dkdv_free);
+        flush_rows(qrow0 + 128, D + h * 64);
+      }
+      if (ht == 0) PROF_MARK(50);
+      // ---- (g) dQ for query tiles 0, 1 (+ key-256 column term) ----
+      mbar_wait(&sm.dq_full, i & 1);
+      if (ht == 0) PROF_MARK(51);
+      tc_fence_after();
+      {
+        stage_acc(C_DQ, has_tail ? sm.ds_col[pb][r] : 0.f, sm.k256[pb], scale);
+        flush_rows(qrow0, h * 64);
+        stage_acc(C_DQ + 64, has_tail ? sm.ds_col[pb][128 + r] : 0.f, sm.k256[pb], scale);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.dq_free);
+        flush_rows(qrow0 + 128, h * 64);
+      }
+      if (ht == 0) PROF_MARK(52);
+      (void)hw;
     }
   }
   __syncthreads();
@@ -823,11 +898,46 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tmem_dealloc<512>(tmem);
   }
 }
+#undef stage_acc
+#undef flush_rows
 
 }  // namespace jz
 
+// Delta_i = rowsum(dO_i o O_i) per (frame, head, row), same layout as lse: one warp per token row,
+// coalesced over the H*64 columns. dO is the bf16 tensor the MMAs consume, O the forward's fp32 copy.
+__global__ void spatial_delta_kernel(const float* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
+                                     int64_t rows, int S, int H, float* __restrict__ delta) {
+  const int lane = threadIdx.x & 31;
+  const int D = H * 64;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = w0; row < rows; row += nw) {
+    const float* o = out + row * D;
+    const __nv_bfloat16* g = dout + row * D;
+    const int64_t f = row / S, sidx = row - f * S;
+    for (int c = 0; c < D / 128; ++c) {
+      const int col = 128 * c + 4 * lane;
+      const float4 ov = __ldg(reinterpret_cast<const float4*>(o + col));
+      const uint2 gv = __ldg(reinterpret_cast<const uint2*>(g + col));
+      const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
+      float acc = ov.x * g0.x + ov.y * g0.y + ov.z * g1.x + ov.w * g1.y;
+#pragma unroll
+      for (int m = 8; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);  // 16 lanes = one head
+      if ((lane & 15) == 0) {
+        const int h = col >> 6;
+        delta[((int64_t)f * H + h) * S + sidx] = acc;
+      }
+    }
+  }
+}
+
+extern "C" int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H) {
+  return frames * (int64_t)S * H * (int64_t)sizeof(float);
+}
+
 extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
-                                   int64_t frames, int S, int H, int head_dim, void* dqkv, jz_stream_t s) {
+                                   int64_t frames, int S, int H, int head_dim, void* dqkv, void* workspace,
+                                   jz_stream_t s) {
   using namespace jz;
   JZ_CHECK_ARG(head_dim == 64, "spatial attention bwd: head_dim %d unsupported (64)", head_dim);
   JZ_CHECK_ARG(S == 256 || S == 257, "spatial attention bwd: sequence length %d unsupported", S);
@@ -837,15 +947,26 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
   if (rc) return rc;
   rc = make_tmap_2d_bf16(&td, dout, D, frames * S, D, 64, 128);
   if (rc) return rc;
-  static bool attr_done = false;
-  if (!attr_done) {
-    JZ_CUDA_TRY(cudaFuncSetAttribute(spatial_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp::B_SMEM));
-    attr_done = true;
+  JZ_CHECK_ARG(workspace != nullptr, "spatial attention bwd: workspace (frames*S*H floats) required");
+  float* delta = reinterpret_cast<float*>(workspace);
+  {
+    const int64_t rows = frames * S;
+    int blocks = (int)((rows * 32 + 255) / 256);
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    spatial_delta_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+        out_f32, reinterpret_cast<const __nv_bfloat16*>(dout), rows, S, H, delta);
+    JZ_LAUNCH_CHECK();
   }
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(spatial_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sp::B_SMEM);
+  });
+  JZ_CUDA_TRY(attr_err);
   const int64_t units = frames * H;
   const int grid = (int)(units < num_sms() ? units : num_sms());
-  spatial_bwd_kernel<<<grid, sp::kBwdThreads, sp::B_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
-      tq, td, reinterpret_cast<const __nv_bfloat16*>(qkv), out_f32,
+  spatial_bwd_kernel<<<grid, sp::kBwdThreads2, sp::B_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
+      tq, td, reinterpret_cast<const __nv_bfloat16*>(qkv), delta,
       reinterpret_cast<const __nv_bfloat16*>(dout), lse, reinterpret_cast<__nv_bfloat16*>(dqkv), (int)frames, S, H);
   JZ_LAUNCH_CHECK();
   return JZ_OK;

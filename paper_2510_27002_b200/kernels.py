@@ -236,8 +236,9 @@ def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: b
 def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=None):
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
+    ws = scratch("attn_delta", frames * S * H)
     L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
-           64, dqkv.data_ptr(), _s())
+           64, dqkv.data_ptr(), ws.data_ptr(), _s())
     return dqkv
 
 

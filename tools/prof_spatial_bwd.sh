@@ -20,21 +20,25 @@ out = torch.empty(frames * S, D, device="cuda", dtype=torch.bfloat16)
 o32 = torch.empty(frames * S, D, device="cuda")
 lse = torch.empty(frames, H, S, device="cuda")
 dq = torch.empty_like(qkv)
+WS = torch.empty(frames * S * H, device='cuda')
 L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
 for _ in range(3):
-    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), L.stream_ptr())
+    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), L.stream_ptr())
 torch.cuda.synchronize()
 buf = np.zeros(64 * 32, dtype=np.uint64)
 lib.jz_attn_prof_read.argtypes = [C.c_void_p]
 assert lib.jz_attn_prof_read(buf.ctypes.data) == 0
-t = buf.reshape(64, 32).astype(np.int64)
-names = {0: "start", 22: "bar1 passed", 23: "P1 loads done", 24: "bar2 passed", 25: "P2 main done", 1: "prologue done", 18: "dq_full", 19: "dq done", 20: "tail ready", 21: "tail inputs free"}
-for g in range(4):
-    names[2 + 4 * g] = f"sdp_full[{g}]"; names[3 + 4 * g] = f"pds_free ok[{g}]"; names[4 + 4 * g] = f"pds written[{g}]"; names[5 + 4 * g] = f"dkdv done[{g}]"
+t = buf.reshape(32, 64).astype(np.int64)
+names = {0: "MMA start", 1: "MMA load_full", 26: "EW prep_ready", 43: "HLP prep+load", 45: "HLP tail done", 46: "HLP dkdv_full0",
+         47: "HLP epi0 done", 48: "HLP prepare done", 49: "HLP dkdv_full1", 50: "HLP epi1 done", 51: "HLP dq_full", 52: "HLP dq done",
+         53: "TMA issue"}
+for x in range(8):
+    names[2 + x] = f"MMA sdp issued {x}"; names[10 + x] = f"MMA pds_full {x}"; names[18 + x] = f"MMA grad issued {x}"
+    names[27 + x] = f"EW sdp_full {x}"; names[35 + x] = f"EW pds done {x}"
 for u in (2, 3, 10):
     base = t[u, 0]
     print(f"unit {u}: total {t[u + 1, 0] - base} cycles")
-    for k in sorted(names):
+    for k in sorted(names, key=lambda k: t[u, k]):
         if t[u, k]:
-            print(f"   {names[k]:18s} {t[u, k] - base:8d}")
+            print(f"   {names[k]:20s} {t[u, k] - base:8d}")
 PY
