@@ -49,9 +49,16 @@ def shard(global_batch: int, rank: int, world: int) -> tuple[int, int]:
 
 def block_buckets(offsets: dict, prefix: str, blocks: int, total: int) -> list[tuple[str, int, int]]:
     """Contiguous gradient ranges in backward-completion order:
-    head (params after the last block), block[n-1] .. block[0], embeddings (params before block 0)."""
+    head (params after the last block), block[n-1] .. block[0], embeddings (params before block 0).
+
+    `offsets`: name -> (offset, shape) of contiguous params, or a ParamStore's `extents`
+    (name -> (first, end) storage range, which also covers grouped strided views)."""
+    def span(v):
+        a, b = v
+        return (a, b) if isinstance(b, int) else (a, a + max(1, _numel(b)))
+
     def rng_of(pred):
-        idx = [(o, o + max(1, _numel(shp))) for n, (o, shp) in offsets.items() if pred(n)]
+        idx = [span(v) for n, v in offsets.items() if pred(n)]
         return (min(a for a, _ in idx), max(b for _, b in idx)) if idx else None
 
     out = []

@@ -24,7 +24,7 @@ import torch
 from . import _lib as L
 from . import kernels as K
 from .rng import PhiloxState, consume, stream
-from .st import StConfig, init_st_stack_arrays, st_backward, st_forward
+from .st import StConfig, init_st_stack_arrays, st_backward, st_forward, st_param_groups
 from .tensor import ParamStore, Tensor, as_device, grad_buffers
 
 
@@ -137,7 +137,7 @@ class DynamicsModel:
         p.update(init_st_stack_arrays(rng, cfg.st, prefix="dyn", dtype=dtype))
         p["to_logits.w"] = rng.normal(0, 0.02, (d, cfg.token_codes)).astype(dtype)
         p["to_logits.b"] = np.zeros(cfg.token_codes, dtype=dtype)
-        self._store = ParamStore(p)
+        self._store = ParamStore(p, groups=st_param_groups(cfg.st, "dyn"))
         self.params = self._store.params
 
     # -- conditioning (dynamics.py:90-99) -----------------------------------

@@ -56,10 +56,9 @@ def adamw_init(params: dict, weight_decay: float = 0.0, beta1: float = 0.9, beta
         st.store = store
         st.m_flat = torch.zeros_like(store.flat)
         st.v_flat = torch.zeros_like(store.flat)
-        for name, (o, shp) in store.offsets.items():
-            n = int(np.prod(shp)) if shp else 1
-            st.m[name] = st.m_flat[o:o + n].view(shp)
-            st.v[name] = st.v_flat[o:o + n].view(shp)
+        for name in store.layout:
+            st.m[name] = store.view_of(st.m_flat, name)
+            st.v[name] = store.view_of(st.v_flat, name)
     else:
         for name, p in params.items():
             st.m[name] = torch.zeros_like(p.data)

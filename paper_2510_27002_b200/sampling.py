@@ -154,7 +154,9 @@ class FrameDecoder:
                       for _ in range(cfg.blocks)]
         P = model.params
         self.P = P
-        self.sh = _shadows(P, cfg.st, "dyn")
+        # private copies: the captured graph holds these addresses, and the store's shared shadow
+        # is recast by every forward of the model
+        self.sh = [{k: v.clone() for k, v in blk.items()} for blk in _shadows(P, cfg.st, "dyn")]
         self.wl = _K.cast_bf16(P["to_logits.w"].data)
         self.t = 0  # frames cached
 
@@ -271,9 +273,18 @@ class FrameDecoder:
             else:
                 rows.append([s * B * N, k] + st.counter + list(st.key) + st.buffer + [st.buffer_pos])
         mask64 = (1 << 64) - 1
-        host = torch.tensor(np.array([[v & mask64 for v in r] for r in rows], dtype=np.uint64).view(np.int64),
-                            dtype=torch.int64).pin_memory()
-        host_t = torch.tensor(self.t, dtype=torch.int32).pin_memory()
+        vals = torch.from_numpy(np.array([[v & mask64 for v in r] for r in rows], dtype=np.uint64).view(np.int64))
+        # persistent pinned staging (freeing pinned blocks records CUDA events, which must never
+        # happen while a graph is being captured)
+        if getattr(self, "_host_rows", None) is None or self._host_rows.shape[0] < steps:
+            torch.cuda.synchronize()
+            self._host_rows = torch.empty((max(steps, 32), 13), dtype=torch.int64).pin_memory()
+            self._host_t = torch.empty((), dtype=torch.int32).pin_memory()
+        torch.cuda.current_stream().synchronize()  # previous H2D copies out of the staging are done
+        host = self._host_rows
+        host[:steps].copy_(vals)
+        host_t = self._host_t
+        host_t.fill_(self.t)
         self._cond.copy_(cond)
         self._cur.zero_()
         self._known.zero_()
@@ -286,7 +297,7 @@ class FrameDecoder:
             self._step(temperature)  # eager first step: loads every kernel before capture
             s0 = 1
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with _no_gc(), torch.cuda.graph(g):
                 self._step(temperature)
             self._graphs[key] = g
         for s in range(s0, steps):
@@ -298,7 +309,7 @@ class FrameDecoder:
         ga = self._graphs.get("append") if graph else None
         if graph and ga is None:
             ga = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(ga):
+            with _no_gc(), torch.cuda.graph(ga):
                 self._append()
             self._graphs["append"] = ga
         if ga is not None:
@@ -307,6 +318,23 @@ class FrameDecoder:
             self._append()
         self.t += 1
         return self._cur.clone()
+
+
+class _no_gc:
+    """No Python garbage collection while a CUDA graph is captured: collecting an unrelated
+    pinned tensor frees a host block and records a CUDA event, invalidating the capture."""
+
+    def __enter__(self):
+        import gc
+        gc.collect()
+        self._was = gc.isenabled()
+        gc.disable()
+
+    def __exit__(self, *exc):
+        import gc
+        if self._was:
+            gc.enable()
+        return False
 
 
 def decoder_for(model, B: int, t_max: int) -> "FrameDecoder":

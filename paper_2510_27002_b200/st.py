@@ -23,7 +23,7 @@ import torch
 
 from . import _lib as L
 from . import kernels as K
-from .tensor import Tensor, param_count  # noqa: F401  (re-export, st.py:97-98)
+from .tensor import Tensor, param_count, store_for  # noqa: F401  (re-export, st.py:97-98)
 
 
 @dataclass(frozen=True)
@@ -67,6 +67,18 @@ def init_st_stack_arrays(rng, cfg: StConfig, prefix: str = "st", dtype=np.float3
     return p
 
 
+def st_param_groups(cfg: StConfig, prefix: str) -> list:
+    """ParamStore groups: each attention sub-layer's q/k/v weights (and biases) side by side,
+    so the fused QKV projection reads one (d, 3d) bf16 view and writes one (d, 3d) gradient."""
+    out = []
+    for i in range(cfg.blocks):
+        for sub in ("spatial", "temporal"):
+            base = f"{prefix}.block{i}.{sub}"
+            out.append(tuple(f"{base}.{p}.w" for p in "qkv"))
+            out.append(tuple(f"{base}.{p}.b" for p in "qkv"))
+    return out
+
+
 def init_st_stack(rng, cfg: StConfig, prefix: str = "st", dtype=np.float32) -> dict:
     """st.py:44-57: returns device parameters."""
     return {k: Tensor(v, requires_grad=True) for k, v in init_st_stack_arrays(rng, cfg, prefix, dtype).items()}
@@ -96,6 +108,25 @@ def check_supported(cfg: StConfig, S: int, T: int) -> None:
 # weight shadows (re-derived every call: callers may swap `params` wholesale)
 # --------------------------------------------------------------------------
 def _shadows(P: dict, cfg: StConfig, prefix: str) -> list:
+    """bf16 GEMM operands of every block. With the model's grouped ParamStore this is ONE flat
+    cast of all parameters (views into the shadow; qkv weights/biases are already fused blocks);
+    otherwise (caller-assembled params) per-tensor casts."""
+    st = store_for(P)
+    if st is not None and st.block_of(st.flat, f"{prefix}.block0.spatial.q.w") is not None:
+        sh = st.shadow()
+        K.cast_bf16(st.flat, sh)
+        out = []
+        for i in range(cfg.blocks):
+            base = f"{prefix}.block{i}"
+            blk = {}
+            for sub in ("spatial", "temporal"):
+                blk[f"{sub}.wqkv"] = st.block_of(sh, f"{base}.{sub}.q.w")
+                blk[f"{sub}.bqkv"] = st.block_of(st.flat, f"{base}.{sub}.q.b")
+                blk[f"{sub}.wo"] = st.view_of(sh, f"{base}.{sub}.o.w")
+            blk["ffn.wup"] = st.view_of(sh, f"{base}.ffn.up.w")
+            blk["ffn.wdown"] = st.view_of(sh, f"{base}.ffn.down.w")
+            out.append(blk)
+        return out
     d, f = cfg.model_dim, cfg.ffn_dim
     dev = P[f"{prefix}.final_ln.g"].data.device
     out = []
@@ -178,6 +209,9 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
     d = cfg.model_dim
     x_final = ctx["x_final"]
     rows = x_final.shape[0]
+    st = store_for(P)  # grouped-store gradients: the fused qkv blocks are written in place
+    gst = st if (st is not None and st.grad_flat is not None and st.grads_are_views(G)
+                 and st.block_of(st.grad_flat, f"{prefix}.block0.spatial.q.w") is not None) else None
     dev = x_final.device
     dres = torch.empty(rows, d, dtype=K.F32, device=dev)
     dres_b = torch.empty(rows, d, dtype=K.BF16, device=dev)
@@ -208,7 +242,7 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.linear_dw(c["ao2"], dres_b, G[f"{base}.temporal.o.w"])
         K.linear_dx(dres_b, w["temporal.wo"], epilogue=L.EPI_BF16, out=dao)
         dqkv = K.attn_temporal_bwd(c["qkv2"], c["ao2"], dao, c["lse_t"], B, T, S, H)
-        _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d)
+        _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d, gst)
         K.linear_dx(dqkv, w["temporal.wqkv"], epilogue=L.EPI_F32, out=dtmp)
         K.layernorm_bwd(c["x1"], c["m2"], c["r2"], P[f"{base}.temporal.ln.g"].data, dtmp, dres, accumulate=True,
                         dres_bf16=dres_b, dgamma=G[f"{base}.temporal.ln.g"], dbeta=G[f"{base}.temporal.ln.b"],
@@ -217,7 +251,7 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.linear_dw(c["ao"], dres_b, G[f"{base}.spatial.o.w"])
         K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao)
         dqkv = K.attn_spatial_bwd(c["qkv"], c["ao32"], dao, c["lse_s"], frames, S, H, dqkv=dqkv)
-        _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d)
+        _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst)
         K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_F32, out=dtmp)
         prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
         K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
@@ -230,7 +264,14 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
     return dres
 
 
-def _qkv_param_grads(dqkv: torch.Tensor, xn: torch.Tensor, G: dict, base: str, d: int) -> None:
+def _qkv_param_grads(dqkv: torch.Tensor, xn: torch.Tensor, G: dict, base: str, d: int, st=None) -> None:
+    if st is not None:
+        gw = st.block_of(st.grad_flat, f"{base}.q.w")
+        gb = st.block_of(st.grad_flat, f"{base}.q.b")
+        if gw is not None and gb is not None:  # one (d, 3d) dW GEMM, bias sums straight into place
+            K.colsum_bf16(dqkv, gb)
+            K.linear_dw(xn, dqkv, gw)
+            return
     bq = torch.empty(3 * d, dtype=K.F32, device=dqkv.device)
     K.colsum_bf16(dqkv, bq)
     for j, proj in enumerate("qkv"):

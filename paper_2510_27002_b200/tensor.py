@@ -83,52 +83,120 @@ class ParamStore:
     """Flat fp32 storage for a model's parameters (+ lazily a flat gradient buffer).
 
     `params` is an OrderedDict name -> Tensor whose `.data` are views into `flat`.
+    `groups` lists tuples of names laid out side by side as the column blocks of one matrix
+    (2-D members with equal rows) or one vector (1-D members): an attention sub-layer's
+    q/k/v weights become one (d, 3d) block, so its bf16 shadow and its weight gradient are
+    plain contiguous views (one GEMM operand, one dW GEMM). Members are strided views.
     """
 
-    def __init__(self, arrays: "OrderedDict[str, np.ndarray]"):
+    def __init__(self, arrays: "OrderedDict[str, np.ndarray]", groups=()):
         dev = device()
         total = sum(int(a.size) for a in arrays.values())
         host = np.empty(total, dtype=np.float32)
-        self.offsets: dict[str, tuple[int, tuple]] = {}
+        group_of = {}
+        for g in groups:
+            for n in g:
+                group_of[n] = tuple(g)
+        # name -> (storage offset, shape, strides); extents -> (first, last+1) storage element
+        self.layout: dict[str, tuple[int, tuple, tuple]] = {}
+        self.extents: dict[str, tuple[int, int]] = {}
+        self.blocks: dict[tuple, tuple[int, tuple]] = {}  # group -> (offset, block shape)
         off = 0
         for name, a in arrays.items():
-            n = int(a.size)
-            host[off:off + n] = a.reshape(-1).astype(np.float32)
-            self.offsets[name] = (off, tuple(a.shape))
-            off += n
+            if name in self.layout:
+                continue
+            g = group_of.get(name)
+            if g is None:
+                n = int(a.size)
+                host[off:off + n] = a.reshape(-1).astype(np.float32)
+                shp = tuple(a.shape)
+                self.layout[name] = (off, shp, _contig_strides(shp))
+                self.extents[name] = (off, off + max(n, 1))
+                off += n
+                continue
+            mem = [arrays[m] for m in g]
+            if any(x.ndim != mem[0].ndim for x in mem) or mem[0].ndim not in (1, 2):
+                raise ValueError(f"parameter group {g}: members must all be 1-D or all 2-D")
+            if mem[0].ndim == 2:
+                rows = mem[0].shape[0]
+                if any(x.shape[0] != rows for x in mem):
+                    raise ValueError(f"parameter group {g}: 2-D members need equal row counts")
+                cols = sum(x.shape[1] for x in mem)
+                block = np.concatenate([x.astype(np.float32) for x in mem], axis=1)
+                bshape = (rows, cols)
+                c0 = 0
+                for m, x in zip(g, mem):
+                    self.layout[m] = (off + c0, tuple(x.shape), (cols, 1))
+                    self.extents[m] = (off + c0, off + (rows - 1) * cols + c0 + x.shape[1])
+                    c0 += x.shape[1]
+            else:
+                block = np.concatenate([x.astype(np.float32) for x in mem])
+                bshape = (block.size,)
+                c0 = 0
+                for m, x in zip(g, mem):
+                    self.layout[m] = (off + c0, tuple(x.shape), (1,))
+                    self.extents[m] = (off + c0, off + c0 + x.size)
+                    c0 += x.size
+            host[off:off + block.size] = block.reshape(-1)
+            self.blocks[tuple(g)] = (off, bshape)
+            off += block.size
+        # offsets (name -> (offset, shape)) kept for callers that only need the first element
+        self.offsets = {n: (o, shp) for n, (o, shp, _) in self.layout.items()}
         self.flat = torch.from_numpy(host).to(dev)
         self.grad_flat: torch.Tensor | None = None
         self.params: "OrderedDict[str, Tensor]" = OrderedDict()
-        for name, (o, shp) in self.offsets.items():
-            n = int(np.prod(shp)) if shp else 1
-            self.params[name] = Tensor(self.flat[o:o + n].view(shp), requires_grad=True)
+        for name in arrays:
+            self.params[name] = Tensor(self.view_of(self.flat, name), requires_grad=True)
         _STORES[id(self.params)] = self
+
+    def view_of(self, buf: torch.Tensor, name: str) -> torch.Tensor:
+        """`name`'s view into a flat buffer laid out like `flat` (params, grads, moments, shadows)."""
+        o, shp, st = self.layout[name]
+        return buf.as_strided(shp, st, buf.storage_offset() + o)
+
+    def block_of(self, buf: torch.Tensor, first: str) -> torch.Tensor | None:
+        """The whole group block starting with member `first` as a contiguous view, or None."""
+        for g, (o, bshape) in self.blocks.items():
+            if g[0] == first:
+                n = int(np.prod(bshape))
+                return buf[o:o + n].view(bshape)
+        return None
 
     def grads_are_views(self, grads: dict) -> bool:
         if self.grad_flat is None:
             return False
-        base = self.grad_flat.data_ptr()
-        for name, (o, _) in self.offsets.items():
+        for name, (o, shp, st) in self.layout.items():
             g = grads.get(name)
-            if g is None or g.data_ptr() != base + 4 * o:
+            if (g is None or g.data_ptr() != self.grad_flat.data_ptr() + 4 * o or tuple(g.shape) != shp
+                    or (g.numel() > 1 and tuple(g.stride()) != st)):
                 return False
         return True
 
     def grads(self) -> dict:
-        """Gradient views (allocated on first use) keyed by name; also sets p.grad."""
+        """Gradient views (allocated on first use) keyed by name."""
         if self.grad_flat is None:
             self.grad_flat = torch.zeros_like(self.flat)
-        out = {}
-        for name, (o, shp) in self.offsets.items():
-            n = int(np.prod(shp)) if shp else 1
-            out[name] = self.grad_flat[o:o + n].view(shp)
-        return out
+        return {name: self.view_of(self.grad_flat, name) for name in self.layout}
+
+    def shadow(self) -> torch.Tensor:
+        """bf16 copy of `flat` (same layout), refreshed by the caller with one cast per use."""
+        if getattr(self, "_shadow", None) is None:
+            self._shadow = torch.empty(self.flat.numel(), dtype=torch.bfloat16, device=self.flat.device)
+        return self._shadow
 
     def owns(self, params: dict) -> bool:
         """True when `params` are still exactly this store's views (not swapped by a caller)."""
         if params.keys() != self.params.keys():
             return False
         return all(params[k] is self.params[k] for k in params)
+
+
+def _contig_strides(shp: tuple) -> tuple:
+    st, acc = [], 1
+    for s in reversed(shp):
+        st.append(acc)
+        acc *= s
+    return tuple(reversed(st))
 
 
 _STORES: "weakref.WeakValueDictionary[int, ParamStore]" = weakref.WeakValueDictionary()

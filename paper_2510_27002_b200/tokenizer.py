@@ -20,7 +20,7 @@ import torch
 from . import _lib as L
 from . import kernels as K
 from .rng import stream
-from .st import StConfig, init_st_stack_arrays, st_forward
+from .st import StConfig, init_st_stack_arrays, st_forward, st_param_groups
 from .tensor import ParamStore, Tensor, as_device
 
 
@@ -142,7 +142,7 @@ class VideoTokenizer:
         p.update(init_st_stack_arrays(rng, cfg.st, prefix="dec", dtype=dtype))
         p["to_pixels.w"] = rng.normal(0, 0.02, (d, cfg.patch_dim)).astype(dtype)
         p["to_pixels.b"] = np.zeros(cfg.patch_dim, dtype=dtype)
-        self._store = ParamStore(p)
+        self._store = ParamStore(p, groups=st_param_groups(cfg.st, "enc") + st_param_groups(cfg.st, "dec"))
         self.params = self._store.params
 
     # -- device building blocks ---------------------------------------------

@@ -35,7 +35,7 @@ class DynamicsTrainStep:
         if world > 1:
             store = model._store
             store.grads()  # allocate the flat gradient buffer
-            buckets = block_buckets(store.offsets, "dyn", model.cfg.blocks, store.flat.numel())
+            buckets = block_buckets(store.extents, "dyn", model.cfg.blocks, store.flat.numel())
             self.reducer = GradAllReduce(store.grad_flat, buckets, group=group)
 
     def step(self, step: int, tokens: torch.Tensor, latents: Tensor, global_batch: int | None = None):
