@@ -121,12 +121,63 @@ class LatentActionModel:
         return Tensor(e["z_e"].view(e["B"], e["T"] - 1, self.cfg.latent_dim))
 
     def encoder_only(self, frames):
-        """(indices (B, T-1), z_q_st Tensor, codebook_loss, commitment_loss)."""
-        z_e = self._encode_pre_vq(frames)
-        idx, zq, sq = _vq(z_e.data.view(-1, self.cfg.latent_dim), self.params["codebook"].data)
-        loss = K.sum_scaled(sq, 1.0 / z_e.data.numel())
-        lead = tuple(z_e.shape[:-1])
-        return idx.view(lead).cpu().numpy(), Tensor(zq.view(z_e.shape)), Tensor(loss), Tensor(loss.clone())
+        """lam.py:96-101: (indices (B, T-1), z_q_st Tensor, codebook_loss, commitment_loss).
+
+        The three tensors share one encoder graph (cotrain, trainer.py:306-309): the dynamics
+        backward hands d(z_q_st) to z_q_st.backward(), the losses contribute their coefficients
+        (codebook -> codebook rows, beta * commitment -> z_e), and the encoder backward runs once
+        into p.grad (encoder parameters and codebook; decoder gradients are zero)."""
+        cfg, P = self.cfg, self.params
+        fr = self._frames_device(frames)
+        self._check(fr)
+        e = self._encoder(fr, save=True)
+        B, T = e["B"], e["T"]
+        Tm, D, N, dl = T - 1, cfg.model_dim, cfg.patches_per_frame, cfg.latent_dim
+        z_e = e["z_e"]
+        idx, zq, sq = _vq(z_e, P["codebook"].data)
+        numel_z = z_e.numel()
+        loss = K.sum_scaled(sq, 1.0 / numel_z)
+        store = self._store
+        graph = {"cb": 0.0, "commit": 0.0, "done": False}
+        zq_t = Tensor(zq.view(B, Tm, dl), requires_grad=True)
+
+        def run(d_zq):
+            if graph["done"]:
+                return
+            graph["done"] = True
+            G = grad_buffers(P, store)
+            if store is not None and store.grad_flat is not None and store.grads_are_views(G):
+                store.grad_flat.zero_()  # decoder parameters take no part in this graph
+            else:
+                for g in G.values():
+                    g.zero_()
+            dz = d_zq.reshape(B * Tm, dl).float().contiguous() if d_zq is not None else torch.zeros_like(z_e)
+            d_ze = torch.empty_like(z_e)
+            K.vq_bwd(z_e, P["codebook"].data, idx, dz, commit_coef=graph["commit"] * 2.0 / numel_z,
+                     cb_coef=graph["cb"] * 2.0 / numel_z, dz_out=d_ze, dcodebook=G["codebook"])
+            d_trans = torch.empty(B * Tm, D, dtype=K.F32, device=z_e.device)
+            K.linear_f32_bwd(e["trans"], d_ze, P["to_latent.w"].data, dx=d_trans, dW=G["to_latent.w"],
+                             db=G["to_latent.b"])
+            d_pool = torch.zeros(B, T, D, dtype=K.F32, device=z_e.device)
+            d_pool[:, 1:] = d_trans.view(B, Tm, D)
+            d_y = K.mean_pool_bwd(d_pool.view(B * T, D), B * T, N, D)
+            dx_e = st_backward(e["ctx"], d_y, P, G, cfg.st, "enc")
+            d_emb = torch.empty(B * T * N, D, dtype=K.BF16, device=z_e.device)
+            K.assemble_bwd(dx_e, B=B, T=T, N=N, D=D, prepend=False, d_emb=d_emb, d_ps=G["pos_spatial"],
+                           d_pt=G["pos_temporal"][:T])
+            K.colsum_bf16(d_emb, G["patch_embed.b"])
+            K.linear_dw(e["p16"], d_emb, G["patch_embed.w"])
+
+        zq_t._backward = lambda: run(zq_t.grad)
+
+        def hook(role):
+            def add(c):
+                graph[role] += c
+            return add
+
+        cb_t = Tensor(loss, _backward=lambda: run(None), _coef_hook=hook("cb"))
+        commit_t = Tensor(loss.clone(), _backward=lambda: run(None), _coef_hook=hook("commit"))
+        return idx.view(B, Tm).cpu().numpy(), zq_t, cb_t, commit_t
 
     def infer_actions_device(self, frames) -> torch.Tensor:
         z_e = self._encode_pre_vq(frames)

@@ -25,9 +25,13 @@ def device() -> torch.device:
 
 
 class Tensor:
-    __slots__ = ("data", "grad", "requires_grad", "_backward", "__weakref__")
+    """A device array with the reference's Tensor surface (autodiff.py:22-103), narrowed to what
+    the hot path needs: a loss carries its hand-scheduled backward, and scalar losses combine
+    linearly (`ce + cb + beta * commit`, trainer.py:306-309) with the coefficients routed to
+    each leaf's backward."""
+    __slots__ = ("data", "grad", "requires_grad", "_backward", "_terms", "_coef_hook", "__weakref__")
 
-    def __init__(self, data, requires_grad: bool = False, _backward=None):
+    def __init__(self, data, requires_grad: bool = False, _backward=None, _terms=None, _coef_hook=None):
         if not isinstance(data, torch.Tensor):
             arr = np.asarray(data)
             if arr.dtype == np.float64:
@@ -37,6 +41,8 @@ class Tensor:
         self.grad = None
         self.requires_grad = requires_grad
         self._backward = _backward
+        self._terms = _terms          # linear combination of leaf losses: [(leaf, coef)]
+        self._coef_hook = _coef_hook  # leaf whose backward needs its total coefficient up front
 
     # -- array-like ---------------------------------------------------------
     @property
@@ -63,12 +69,72 @@ class Tensor:
     def detach(self) -> "Tensor":
         return Tensor(self.data)
 
+    # -- linear combinations of scalar losses ----------------------------------
+    def _leaf_terms(self, c: float):
+        if self._terms is None:
+            return [(self, c)]
+        return [(t, cc * c) for t, cc in self._terms]
+
+    def _combine(self, other, ca: float, cb: float) -> "Tensor":
+        if isinstance(other, Tensor):
+            return Tensor(self.data * ca + other.data * cb, _terms=self._leaf_terms(ca) + other._leaf_terms(cb))
+        if isinstance(other, (int, float, np.floating, np.integer)):
+            return Tensor(self.data * ca + float(other) * cb, _terms=self._leaf_terms(ca))
+        return NotImplemented
+
+    def __add__(self, other):
+        return self._combine(other, 1.0, 1.0)
+
+    def __radd__(self, other):
+        return self._combine(other, 1.0, 1.0)
+
+    def __sub__(self, other):
+        return self._combine(other, 1.0, -1.0)
+
+    def __rsub__(self, other):
+        return self._combine(other, -1.0, 1.0)
+
+    def __mul__(self, k):
+        if isinstance(k, (int, float, np.floating, np.integer)):
+            return Tensor(self.data * float(k), _terms=self._leaf_terms(float(k)))
+        return NotImplemented
+
+    __rmul__ = __mul__
+
+    def __neg__(self):
+        return self * -1.0
+
     def backward(self) -> None:
-        """Run the hand-scheduled backward of the op that produced this scalar."""
-        if self._backward is None:
+        """Run the hand-scheduled backward of the op(s) that produced this scalar.
+
+        Leaves with a coefficient hook (VQ losses of an encoder graph) learn their total
+        coefficient first, then ordinary leaves run (only with coefficient 1: their backward
+        kernels are normalised for the loss itself), then hook leaves finish their graphs."""
+        if self._terms is None and self._coef_hook is None:
+            if self._backward is None:
+                raise RuntimeError("backward() on a tensor that does not require grad")
+            fn, self._backward = self._backward, None
+            fn()
+            return
+        acc: dict = {}
+        for t, c in self._leaf_terms(1.0):
+            acc.setdefault(id(t), [t, 0.0])[1] += c
+        leaves = list(acc.values())
+        if all(t._backward is None and t._coef_hook is None for t, _ in leaves):
             raise RuntimeError("backward() on a tensor that does not require grad")
-        fn, self._backward = self._backward, None
-        fn()
+        for t, c in leaves:
+            if t._coef_hook is not None:
+                t._coef_hook(c)
+        for t, c in leaves:
+            if t._coef_hook is None and t._backward is not None:
+                if abs(c - 1.0) > 1e-12:
+                    raise NotImplementedError(f"scaled backward (coefficient {c}) of a fused loss")
+                fn, t._backward = t._backward, None
+                fn()
+        for t, _ in leaves:
+            if t._coef_hook is not None and t._backward is not None:
+                fn, t._backward = t._backward, None
+                fn()
 
 
 def parameter(data) -> Tensor:

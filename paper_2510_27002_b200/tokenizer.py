@@ -20,8 +20,8 @@ import torch
 from . import _lib as L
 from . import kernels as K
 from .rng import stream
-from .st import StConfig, init_st_stack_arrays, st_forward, st_param_groups
-from .tensor import ParamStore, Tensor, as_device
+from .st import StConfig, init_st_stack_arrays, st_backward, st_forward, st_param_groups
+from .tensor import ParamStore, Tensor, as_device, grad_buffers
 
 
 @dataclass(frozen=True)
@@ -178,19 +178,68 @@ class VideoTokenizer:
         return Tensor(unit.view(B, T, cfg.height, cfg.width, cfg.channels))
 
     def forward(self, frames):
-        """tokenizer.py:134-143: (recon, indices, {"recon","codebook","commitment","total"}) — forward only."""
+        """tokenizer.py:134-143: (recon, indices, {"recon","codebook","commitment","total"}).
+
+        losses["total"].backward() runs the full training backward (trainer.py:211-223): recon MSE
+        through to_pixels and the decoder stack, from_latent, the VQ straight-through estimator
+        plus the commitment (beta) and codebook terms, to_latent, the encoder stack and the
+        patch / positional embeddings; gradients land in p.grad.
+        """
+        cfg, P = self.cfg, self.params
         fr = self._frames_device(frames)
-        z_e = self.encode_latent(fr)
-        idx, z_q, cb, commit = vq_quantize(z_e, self.params["codebook"])
-        recon = self.decode_latent(z_q)
-        unit = fr.float() if fr.dtype != torch.uint8 else \
-            K.unpatchify(K.patchify(fr.reshape(-1, *fr.shape[2:]), self.cfg.patch, bf16=False, f32=True)[1],
-                         fr.shape[0] * fr.shape[1], self.cfg.height, self.cfg.width, self.cfg.channels,
-                         self.cfg.patch)[0].view(fr.shape)
-        rec, _, _ = K.mse(recon.data.contiguous(), unit.contiguous())
-        total = rec + cb.data + self.cfg.commitment_beta * commit.data
-        losses = {"recon": Tensor(rec), "codebook": cb, "commitment": commit, "total": Tensor(total)}
-        return recon, idx, losses
+        _check_geometry(cfg, tuple(fr.shape))
+        B, T = fr.shape[0], fr.shape[1]
+        N, D, dl = cfg.patches_per_frame, cfg.model_dim, cfg.latent_dim
+        # encoder (tokenizer.py:113-126)
+        p16, p32 = K.patchify(fr.reshape(B * T, cfg.height, cfg.width, cfg.channels), cfg.patch, f32=True)
+        w_pe = K.cast_bf16(P["patch_embed.w"].data)
+        emb = K.linear_fwd(p16, w_pe, P["patch_embed.b"].data, epilogue=L.EPI_F32)
+        x = K.assemble_fwd(emb, None, P["pos_spatial"].data, P["pos_temporal"].data, B=B, T=T, N=N, D=D,
+                           prepend=False)
+        (_, y32), ectx = st_forward(x, P, cfg.st, "enc", B=B, T=T, S=N, save=True, final_f32=True, final_bf16=False)
+        z_e = K.linear_f32(y32, P["to_latent.w"].data, P["to_latent.b"].data)
+        # VQ (tokenizer.py:58-79)
+        idx, zq_st, sq = _vq(z_e, P["codebook"].data)
+        numel_z = z_e.numel()
+        vq_loss = K.sum_scaled(sq, 1.0 / numel_z)
+        # decoder (tokenizer.py:128-132, no positional embeddings)
+        xd = K.linear_f32(zq_st, P["from_latent.w"].data, P["from_latent.b"].data)
+        yd, dctx = st_forward(xd, P, cfg.st, "dec", B=B, T=T, S=N, save=True)
+        w_tp = K.cast_bf16(P["to_pixels.w"].data)
+        rp = K.linear_fwd(yd, w_tp, P["to_pixels.b"].data, epilogue=L.EPI_F32)
+        rec_loss, _, g16 = K.mse(rp, p32, grad16=True)
+        total = rec_loss + vq_loss + cfg.commitment_beta * vq_loss
+        recon, _ = K.unpatchify(rp, B * T, cfg.height, cfg.width, cfg.channels, cfg.patch)
+        store = self._store
+
+        def backward():
+            G = grad_buffers(P, store)
+            K.colsum_bf16(g16, G["to_pixels.b"])
+            K.linear_dw(yd, g16, G["to_pixels.w"])
+            dy = K.linear_dx(g16, w_tp, epilogue=L.EPI_F32)
+            dxd = st_backward(dctx, dy, P, G, cfg.st, "dec")
+            d_zq = torch.empty(B * T * N, dl, dtype=K.F32, device=dxd.device)
+            K.linear_f32_bwd(zq_st, dxd, P["from_latent.w"].data, dx=d_zq, dW=G["from_latent.w"],
+                             db=G["from_latent.b"])
+            # straight-through to z_e, + beta * d commitment; codebook term into the codebook
+            d_ze = torch.empty_like(z_e)
+            K.vq_bwd(z_e, P["codebook"].data, idx, d_zq, commit_coef=cfg.commitment_beta * 2.0 / numel_z,
+                     cb_coef=2.0 / numel_z, dz_out=d_ze, dcodebook=G["codebook"])
+            d_y = torch.empty(B * T * N, D, dtype=K.F32, device=dxd.device)
+            K.linear_f32_bwd(y32, d_ze, P["to_latent.w"].data, dx=d_y, dW=G["to_latent.w"], db=G["to_latent.b"])
+            dxe = st_backward(ectx, d_y, P, G, cfg.st, "enc")
+            d_emb = torch.empty(B * T * N, D, dtype=K.BF16, device=dxd.device)
+            K.assemble_bwd(dxe, B=B, T=T, N=N, D=D, prepend=False, d_emb=d_emb, d_ps=G["pos_spatial"],
+                           d_pt=G["pos_temporal"][:T])
+            if T < cfg.max_frames:
+                G["pos_temporal"][T:].zero_()
+            K.colsum_bf16(d_emb, G["patch_embed.b"])
+            K.linear_dw(p16, d_emb, G["patch_embed.w"])
+
+        losses = {"recon": Tensor(rec_loss), "codebook": Tensor(vq_loss), "commitment": Tensor(vq_loss.clone()),
+                  "total": Tensor(total, _backward=backward)}
+        return (Tensor(recon.view(B, T, cfg.height, cfg.width, cfg.channels)), idx.view(B, T, N).cpu().numpy(),
+                losses)
 
     def encode_device(self, frames) -> torch.Tensor:
         """(B, T, N) int64 token grid in HBM."""

@@ -126,6 +126,39 @@ class TestTokenizer:
         for k in ("recon", "codebook", "commitment", "total"):
             assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
 
+    def test_forward_backward_vs_oracle(self, frames):
+        """Tokenizer training step (trainer.py:211-223): losses and every parameter gradient."""
+        from paper_2510_27002_b200.tokenizer import TokenizerConfig, VideoTokenizer
+        tok = VideoTokenizer(TokenizerConfig(**TOKKW), seed=3)
+        ocfg = OM.TokCfg(**TOKKW)
+        P = OM.params_to_torch(OM.init_tokenizer(ocfg, seed=3))
+        unit = OM.frames_to_unit(frames)
+        recon, idx, losses = tok.forward(unit)
+        _, i2, _ = OM.tok_forward(P, ocfg, torch.tensor(unit))
+        assert (idx == np.asarray(i2)).mean() > 0.99  # bf16 encoder: only near-tie codes may flip
+        # oracle step on OUR code indices (a flipped code moves a whole patch): tokenizer.py:58-79, 134-143
+        u = torch.tensor(unit)
+        z_e = OM.tok_encode_latent(P, ocfg, u)
+        z_q = P["codebook"][torch.as_tensor(idx)]
+        cb, commit = OM.mse(z_q, z_e.detach()), OM.mse(z_e, z_q.detach())
+        r2 = OM.tok_decode_latent(P, ocfg, z_e + (z_q - z_e).detach())
+        rec = OM.mse(r2, u)
+        l2 = {"recon": rec, "codebook": cb, "commitment": commit, "total": rec + cb + ocfg.commitment_beta * commit}
+        assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
+        for k in ("recon", "codebook", "commitment", "total"):
+            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
+        losses["total"].backward()
+        l2["total"].backward()
+        bad = []
+        for k, p in tok.params.items():
+            ref = P[k].grad.numpy()
+            got = p.grad.cpu().numpy()
+            if k.endswith(".k.b") or np.linalg.norm(ref) < 1e-9:
+                continue  # .k.b: exactly zero in exact arithmetic (softmax shift invariance)
+            if _cos(got, ref) < 0.995:
+                bad.append((k, _cos(got, ref), _rel(got, ref)))
+        assert not bad, bad
+
     def test_geometry_errors(self):
         from paper_2510_27002_b200.tokenizer import TokenizerConfig, VideoTokenizer
         tok = VideoTokenizer(TokenizerConfig(**TOKKW), seed=3)
@@ -179,3 +212,48 @@ class TestLam:
         np.testing.assert_array_equal(lat.numpy(), P["codebook"].numpy()[idx])
         with pytest.raises(ValueError):
             lam.infer_actions(frames[:, :1])
+
+
+class TestCotrain:
+    def test_cotrain_loss_and_grads_vs_oracle(self, frames):
+        """trainer.py:306-309 cotrain: ce(dynamics | z_q_st of the LAM encoder) + cb + beta * commit.
+
+        Gradients reach the dynamics model, and through the straight-through estimator, the LAM
+        encoder (to_latent, stack, embeddings) and codebook; the LAM decoder takes no gradient."""
+        from paper_2510_27002_b200.dynamics import DynamicsConfig, DynamicsModel
+        from paper_2510_27002_b200.lam import LamConfig, LatentActionModel
+        lam = LatentActionModel(LamConfig(**LAMKW), seed=5)
+        dkw = dict(model_dim=128, heads=2, ffn_dim=512, blocks=1, token_codes=256, action_latent_dim=32,
+                   patches_per_frame=256, max_frames=4)
+        dyn = DynamicsModel(DynamicsConfig(**dkw), seed=9)
+        Pl = OM.params_to_torch(OM.init_lam(OM.LamCfg(**LAMKW), seed=5))
+        Pd = OM.params_to_torch(OM.init_dynamics(OM.DynCfg(**dkw), seed=9))
+        unit = OM.frames_to_unit(frames)
+        B, T = unit.shape[0], unit.shape[1]
+        tokens = OR.stream(41, "cotrain-tokens").integers(0, 256, size=(B, T, 256))
+        mask = OR.sample_masks(OR.PhiloxState.fresh(OR.fold_key(3, "cotrain")), B, T, 256)
+        beta = lam.cfg.commitment_beta
+        idx, zq, cb, commit = lam.encoder_only(unit)
+        ce, _ = dyn.loss(tokens, zq, None, mask=mask)
+        total = ce + cb + beta * commit
+        i2, zq2, cb2, commit2 = OM.lam_encoder_only(Pl, OM.LamCfg(**LAMKW), torch.tensor(unit))
+        ce2, _ = OM.dyn_loss(Pd, OM.DynCfg(**dkw), tokens, zq2, mask)
+        total2 = ce2 + cb2 + beta * commit2
+        np.testing.assert_array_equal(idx, np.asarray(i2))
+        assert abs(float(total.data) - float(total2)) < max(TOL["bf16_loss_abs"], 1e-2 * float(total2))
+        total.backward()
+        total2.backward()
+        bad = []
+        for model, P in ((dyn, Pd), (lam, Pl)):
+            for k, p in model.params.items():
+                got = p.grad.cpu().numpy() if p.grad is not None else np.zeros(p.shape)
+                ref = P[k].grad.numpy() if P[k].grad is not None else np.zeros(p.shape)
+                if k.endswith(".k.b") or np.linalg.norm(ref) < 1e-9:
+                    if k.startswith("dec") and model is lam:
+                        assert np.linalg.norm(got) == 0, k  # decoder is not in the cotrain graph
+                    continue
+                if _cos(got, ref) < 0.99:
+                    bad.append((k, _cos(got, ref), _rel(got, ref)))
+        assert not bad, bad
+        with pytest.raises(NotImplementedError):
+            (2.0 * dyn.loss(tokens, zq.detach(), None, mask=mask)[0]).backward()
