@@ -68,7 +68,7 @@ enum {
   JZ_EPI_F32 = 0,       /* D f32  = acc (+ bias)                                  */
   JZ_EPI_BF16 = 1,      /* D bf16 = acc (+ bias)                                  */
   JZ_EPI_RESID = 2,     /* D f32  = aux_f32 + acc (+ bias)   (aux may alias D)    */
-  JZ_EPI_GELU = 3,      /* D bf16 = gelu(acc + bias); D2 bf16 = acc + bias        */
+  JZ_EPI_GELU = 3,      /* D bf16 = gelu(acc + bias); D2 bf16 = acc + bias (D2 may be NULL) */
   JZ_EPI_GELU_BWD = 4,  /* D bf16 = acc * gelu'(aux_bf16)                          */
   JZ_EPI_F32_ACC = 5,   /* D f32 += acc                                           */
   JZ_EPI_BF16_F32 = 6   /* D f32 = acc (+bias); D2 bf16 copy                       */

@@ -23,6 +23,8 @@
 #include "common.h"
 #include "ptx.cuh"
 
+#include <cuda_fp16.h>
+
 #ifdef JZ_GEMM_PROF
 __device__ unsigned long long g_gemm_prof[64 * 8];
 __device__ int g_gemm_dbg;
@@ -124,6 +126,25 @@ JZ_DEV float gelu_fast(float x) {
   return 0.5f * (x * (1.0f + fast_tanh(inner)));
 }
 
+// gelu'(x) for two packed pre-activations in f16x2 arithmetic (one MUFU op per pair). Inputs are
+// clamped to +-10 where gelu' is 0 / 1 to f16 precision; the error (~2^-11 absolute on tanh) matches
+// the fp32 tanh.approx path it replaces, well inside the bf16 output rounding.
+JZ_DEV float2 gelu_grad_pair(uint32_t pre_bf16x2) {
+  const float2 f = unpack_bf16(pre_bf16x2);
+  __half2 x = __floats2half2_rn(f.x, f.y);
+  x = __hmax2(__hmin2(x, __float2half2_rn(10.0f)), __float2half2_rn(-10.0f));
+  const __half2 one = __float2half2_rn(1.0f), half = __float2half2_rn(0.5f);
+  const __half2 c = __float2half2_rn(0.7978845608028654f);
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 inner = __hmul2(__hfma2(__hmul2(__float2half2_rn(0.044715f), x2), x, x), c);
+  __half2 t;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(*reinterpret_cast<uint32_t*>(&t)) : "r"(*reinterpret_cast<const uint32_t*>(&inner)));
+  const __half2 a = __hmul2(half, __hadd2(one, t));
+  const __half2 b = __hmul2(__hmul2(__hmul2(half, x), __hfma2(__hneg2(t), t, one)),
+                            __hmul2(c, __hfma2(__float2half2_rn(0.134145f), x2, one)));
+  return __half22float2(__hadd2(a, b));
+}
+
 JZ_DEV float gelu_grad_fast(float x) {
   const float c = 0.7978845608028654f;
   float x2 = x * x;
@@ -134,6 +155,7 @@ JZ_DEV float gelu_grad_fast(float x) {
 // Epilogue for one thread: row m, 32 consecutive columns starting at n.
 JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], float* ws_out) {
   const int N = p.N;
+  float gbuf_[32];
   const bool full = (n + 32 <= N);
   if (ws_out != nullptr) {  // split-K partial: plain fp32 [M][N]
     float* dst = ws_out + (int64_t)m * N + n;
@@ -205,21 +227,27 @@ JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], fl
     case JZ_EPI_BF16:
     case JZ_EPI_GELU:
     case JZ_EPI_GELU_BWD: {
-      if (p.epi == JZ_EPI_GELU) {
+      if (p.epi == JZ_EPI_GELU && p.D2 == nullptr) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+      } else if (p.epi == JZ_EPI_GELU) {
         __nv_bfloat16* d2 = reinterpret_cast<__nv_bfloat16*>(p.D2) + (int64_t)m * p.ldd2 + n;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {  // D2 = pre-activation, v <- gelu(v)
+          gbuf_[j] = v[j];
+          v[j] = gelu_fast(v[j]);
+        }
         if (full && (p.ldd2 % 8 == 0)) {
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
-            uint4 w = make_uint4(pack_bf16(v[j], v[j + 1]), pack_bf16(v[j + 2], v[j + 3]),
-                                 pack_bf16(v[j + 4], v[j + 5]), pack_bf16(v[j + 6], v[j + 7]));
+            uint4 w = make_uint4(pack_bf16(gbuf_[j], gbuf_[j + 1]), pack_bf16(gbuf_[j + 2], gbuf_[j + 3]),
+                                 pack_bf16(gbuf_[j + 4], gbuf_[j + 5]), pack_bf16(gbuf_[j + 6], gbuf_[j + 7]));
             *reinterpret_cast<uint4*>(d2 + j) = w;
           }
         } else {
           for (int j = 0; j < 32; ++j)
-            if (n + j < N) d2[j] = __float2bfloat16_rn(v[j]);
+            if (n + j < N) d2[j] = __float2bfloat16_rn(gbuf_[j]);
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
       } else if (p.epi == JZ_EPI_GELU_BWD) {
         const __nv_bfloat16* pre =
             reinterpret_cast<const __nv_bfloat16*>(p.aux) + (int64_t)m * p.ldaux + n;
@@ -291,7 +319,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
     tma_prefetch_desc(&tmB);
     if (p.tma_epi) {
       if (p.store_tma) tma_prefetch_desc(&em.d);
-      if (p.store_tma && p.epi == JZ_EPI_GELU) tma_prefetch_desc(&em.d2);
+      if (p.store_tma && p.epi == JZ_EPI_GELU && p.D2 != nullptr) tma_prefetch_desc(&em.d2);
       if (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD) tma_prefetch_desc(&em.aux);
     }
   }
@@ -503,9 +531,9 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
                 const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float2 f = unpack_bf16(ww[e]);
-                  v[8 * c + 2 * e] *= gelu_grad_fast(f.x);
-                  v[8 * c + 2 * e + 1] *= gelu_grad_fast(f.y);
+                  const float2 g = gelu_grad_pair(ww[e]);  // pre-activation stored by the forward
+                  v[8 * c + 2 * e] *= g.x;
+                  v[8 * c + 2 * e + 1] *= g.y;
                 }
               }
             } else {
@@ -523,7 +551,10 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
               *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
                   make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
           } else {
-            if (p.epi == JZ_EPI_GELU) {  // pre-activation copy first (D2), then GELU into D
+            if (p.epi == JZ_EPI_GELU && p.D2 == nullptr) {  // inference: gelu only
+#pragma unroll
+              for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);
+            } else if (p.epi == JZ_EPI_GELU) {  // pre-activation copy first (D2), then GELU into D
 #pragma unroll
               for (int c = 0; c < 8; ++c)
                 *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
@@ -536,10 +567,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
                   tma_store_2d(&em.d2, stg, n, row0);
                   bulk_commit();
                 }
-                if (GDBG != 5) {
 #pragma unroll
-                  for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);  // overlaps the store's smem read
-                }
+                for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);  // overlaps the store's smem read
                 if (lane == 0) bulk_wait_read0();
               } else {
                 __syncwarp();
@@ -722,8 +751,7 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
   JZ_CHECK_ARG(D != nullptr, "gemm: null output");
   if (epilogue == JZ_EPI_RESID || epilogue == JZ_EPI_GELU_BWD)
     JZ_CHECK_ARG(aux != nullptr, "gemm: epilogue %d needs aux", epilogue);
-  if (epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_BF16_F32)
-    JZ_CHECK_ARG(D2 != nullptr, "gemm: epilogue %d needs D2", epilogue);
+  if (epilogue == JZ_EPI_BF16_F32) JZ_CHECK_ARG(D2 != nullptr, "gemm: epilogue %d needs D2", epilogue);
   if (split_k < 1) split_k = 1;
   if (split_k > 1) {
     JZ_CHECK_ARG(epilogue == JZ_EPI_F32 || epilogue == JZ_EPI_F32_ACC,
@@ -775,7 +803,7 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
     if (ok && p.splits > 1) ok = al(ws) && N % 4 == 0;
     else if (ok && f32out) ok = al(D) && ldd % 4 == 0 && N % 4 == 0;
     else if (ok) ok = al(D) && ldd % 8 == 0 && N % 8 == 0;
-    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU) ok = al(D2) && ldd2 % 8 == 0;
+    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU && D2 != nullptr) ok = al(D2) && ldd2 % 8 == 0;
     if (ok && p.splits == 1 && epilogue == JZ_EPI_RESID)
       ok = al(aux) && ldaux % 4 == 0 && make_tmap_2d(&em.aux, aux, 4, N, M, ldaux, 32, 32) == JZ_OK;
     if (ok && p.splits == 1 && epilogue == JZ_EPI_F32_ACC)
@@ -788,7 +816,8 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
     if (ok && p.splits == 1 && store_tma_enabled()) {
       const bool ok2 = f32out ? make_tmap_2d(&em.d, D, 4, N, M, ldd, 32, 32) == JZ_OK
                               : make_tmap_2d(&em.d, D, 2, N, M, ldd, 64, 32) == JZ_OK;
-      const bool ok3 = epilogue != JZ_EPI_GELU || make_tmap_2d(&em.d2, D2, 2, N, M, ldd2, 64, 32) == JZ_OK;
+      const bool ok3 = epilogue != JZ_EPI_GELU || D2 == nullptr ||
+                       make_tmap_2d(&em.d2, D2, 2, N, M, ldd2, 64, 32) == JZ_OK;
       p.store_tma = ok2 && ok3 ? 1 : 0;
     }
   }

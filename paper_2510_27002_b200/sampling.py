@@ -202,8 +202,7 @@ class FrameDecoder:
                     _L.stream_ptr())
         x2 = _K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=_L.EPI_RESID, aux=x1)
         xn3, _, _ = _K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
-        hpre = torch.empty(xn3.shape[0], self.cfg.ffn_dim, dtype=torch.bfloat16, device=x.device)
-        h = _K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=_L.EPI_GELU, out2=hpre)
+        h = _K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=_L.EPI_GELU)
         return _K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=_L.EPI_RESID, aux=x2)
 
     def frame(self, tokens: torch.Tensor, known: torch.Tensor | None, cond: torch.Tensor, *, append: bool,

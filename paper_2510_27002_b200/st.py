@@ -174,7 +174,8 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
         x2 = K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=L.EPI_RESID, aux=x1)
         # FFN (st.py:77-79)
         xn3, m3, r3 = K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
-        hpre = torch.empty(xn3.shape[0], cfg.ffn_dim, dtype=K.BF16, device=x.device)
+        # the pre-activation is kept (bf16) for gelu' in the backward epilogue; inference skips it
+        hpre = torch.empty(xn3.shape[0], cfg.ffn_dim, dtype=K.BF16, device=x.device) if save else None
         h = K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=L.EPI_GELU, out2=hpre)
         x3 = K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=L.EPI_RESID, aux=x2)
         if save:

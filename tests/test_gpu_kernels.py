@@ -80,12 +80,15 @@ def test_gemm_epilogues(M):
     r2 = aux.clone()
     Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=r2, epilogue=L.EPI_F32_ACC)
     assert rel(r2, aux + acc) < 1e-5
-    # GELU: D = gelu(acc + b) bf16, D2 = pre-activation bf16 (tanh form, as nn.gelu)
+    # GELU: D = gelu(acc + b) bf16, D2 = pre-activation bf16 (tanh form, as nn.gelu); D2 optional
     g = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
     pre = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
     Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=g, epilogue=L.EPI_GELU, bias=bias, out2=pre)
     assert rel(pre, acc + bias) < 4e-3
     assert rel(g, torch.nn.functional.gelu(acc + bias, approximate="tanh")) < 5e-3
+    g2 = torch.empty_like(g)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=g2, epilogue=L.EPI_GELU, bias=bias)
+    assert torch.equal(g2, g)
     # GELU_BWD: D = acc * gelu'(aux_pre) bf16
     pre_aux = (torch.randn(M, N, device=dev) * 2).bfloat16()
     gb = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
