@@ -82,6 +82,16 @@ JZ_API int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void* B,
                  int epilogue, const float* bias, const void* aux, int64_t ldaux, void* D2,
                  int64_t ldd2, int split_k, void* workspace, jz_stream_t stream);
 
+/* Same GEMM (split_k = 1, bf16-output epilogues) that also writes the column sums of its bf16
+ * output per 32-row block: colsum_part f32 [jz_gemm_colsum_parts(M)][N].  jz_reduce_partials
+ * over those rows gives the bias gradient of the layer that consumes D (autodiff.py:22-32
+ * _unbroadcast) without re-reading D.  Needs N % 8 == 0 and N > 64. */
+JZ_API int64_t jz_gemm_colsum_parts(int64_t M);
+JZ_API int jz_gemm_bf16_colsum(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb,
+                               int b_kmajor, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K,
+                               int epilogue, const float* bias, const void* aux, int64_t ldaux, void* D2,
+                               int64_t ldd2, float* colsum_part, jz_stream_t stream);
+
 
 /* ------------------------------------------------------------------------
  * Column reductions (bias / LayerNorm-affine gradients; replaces the

@@ -28,6 +28,9 @@ PROTOTYPES: dict[str, list] = {
     "jz_gemm_workspace_bytes": [_I64, _I64, _I32],
     "jz_gemm_bf16": [_P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I64, _I64, _I64,
                      _I32, _P, _P, _I64, _P, _I64, _I32, _P, _P],
+    "jz_gemm_bf16_colsum": [_P, _I64, _I32, _P, _I64, _I32, _P, _I64, _I64, _I64, _I64,
+                            _I32, _P, _P, _I64, _P, _I64, _P, _P],
+    "jz_gemm_colsum_parts": [_I64],
     "jz_row_partials": [_I64],
     "jz_colsum_bf16": [_P, _I64, _I32, _I64, _P, _I32, _P],
     "jz_reduce_partials": [_P, _I32, _I64, _P, _I32, _P],
@@ -66,7 +69,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_kv_fill": [_P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P],
     "jz_maskgit_step": [_P, _I64, _I32, _I32, _F32, _P, _P, _P, _I32, _U64, _I32, _P, _P, _P, _P, _P],
 }
-_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_attn_spatial_bwd_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_assemble_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
+_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_gemm_colsum_parts": _I64, "jz_attn_spatial_bwd_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_assemble_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
             "jz_build_info": C.c_char_p}
 
 

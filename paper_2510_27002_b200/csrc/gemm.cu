@@ -74,6 +74,7 @@ struct GemmParams {
   int64_t ldaux;
   void* D2;
   int64_t ldd2;
+  float* colsum;  // optional per-32-row-block column sums of the bf16 output [ceil(M/32)][N]
   int tma_epi;    // 1: smem-staged epilogue, 0: direct per-thread stores (unaligned shapes)
   int store_tma;  // staged epilogue writes with TMA bulk stores (1) or coalesced st.global (0)
 };
@@ -605,8 +606,24 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
             __syncwarp();
             if (GDBG != 1 && GDBG != 3)
               stg_write_rows(stg, dbase + (int64_t)row0 * dld + (int64_t)n * esz, dld, rows_ok, cols_bytes, lane);
-            __syncwarp();
           }
+          if (p.colsum != nullptr && !f32out) {
+            // bias gradient of the next layer: column sums of this warp's 32 staged bf16 rows
+            // (lane -> columns 2 lane, 2 lane + 1), one fp32 partial row per 32-row block
+            const int ch = lane >> 2, wd = lane & 3;
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+              if (r < rows_ok) {
+                const float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(stg + r * 128 + ((ch ^ (r & 7)) << 4) + wd * 4));
+                s0 += f.x;
+                s1 += f.y;
+              }
+            }
+            if (rows_ok > 0 && 2 * lane < p.N - n)
+              *reinterpret_cast<float2*>(p.colsum + (int64_t)(row0 >> 5) * p.N + n + 2 * lane) = make_float2(s0, s1);
+          }
+          __syncwarp();
           PH_ADD(3, t_d);
         }
       } else {
@@ -735,11 +752,37 @@ extern "C" int64_t jz_gemm_workspace_bytes(int64_t M, int64_t N, int split_k) {
   return split_k <= 1 ? 0 : (int64_t)split_k * M * N * (int64_t)sizeof(float);
 }
 
+static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor, void* D,
+                     int64_t ldd, int64_t M, int64_t N, int64_t K, int epilogue, const float* bias, const void* aux,
+                     int64_t ldaux, void* D2, int64_t ldd2, int split_k, void* workspace, float* colsum,
+                     jz_stream_t stream_);
+
 extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb,
                             int b_kmajor, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K,
                             int epilogue, const float* bias, const void* aux, int64_t ldaux,
                             void* D2, int64_t ldd2, int split_k, void* workspace,
                             jz_stream_t stream_) {
+  return gemm_impl(A, lda, a_kmajor, B, ldb, b_kmajor, D, ldd, M, N, K, epilogue, bias, aux, ldaux, D2, ldd2,
+                   split_k, workspace, nullptr, stream_);
+}
+
+extern "C" int64_t jz_gemm_colsum_parts(int64_t M) { return (M + 31) / 32; }
+
+extern "C" int jz_gemm_bf16_colsum(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb,
+                                   int b_kmajor, void* D, int64_t ldd, int64_t M, int64_t N, int64_t K,
+                                   int epilogue, const float* bias, const void* aux, int64_t ldaux,
+                                   void* D2, int64_t ldd2, float* colsum_part, jz_stream_t stream_) {
+  JZ_CHECK_ARG(colsum_part != nullptr, "gemm colsum: null partial buffer");
+  JZ_CHECK_ARG(epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD,
+               "gemm colsum: bf16-output epilogues only (got %d)", epilogue);
+  return gemm_impl(A, lda, a_kmajor, B, ldb, b_kmajor, D, ldd, M, N, K, epilogue, bias, aux, ldaux, D2, ldd2,
+                   1, nullptr, colsum_part, stream_);
+}
+
+static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor, void* D,
+                     int64_t ldd, int64_t M, int64_t N, int64_t K, int epilogue, const float* bias, const void* aux,
+                     int64_t ldaux, void* D2, int64_t ldd2, int split_k, void* workspace, float* colsum,
+                     jz_stream_t stream_) {
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   JZ_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty problem M=%lld N=%lld K=%lld", (long long)M,
                (long long)N, (long long)K);
@@ -787,6 +830,7 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
   p.bias = bias;
   p.aux = aux; p.ldaux = ldaux;
   p.D2 = D2; p.ldd2 = ldd2;
+  p.colsum = colsum;
 
   float* ws = p.splits > 1 ? reinterpret_cast<float*>(workspace) : nullptr;
   // staged TMA epilogue when every global operand of the epilogue is TMA-legal
@@ -821,6 +865,9 @@ extern "C" int jz_gemm_bf16(const void* A, int64_t lda, int a_kmajor, const void
       p.store_tma = ok2 && ok3 ? 1 : 0;
     }
   }
+  if (colsum != nullptr)
+    JZ_CHECK_ARG(p.tma_epi == 1 && (reinterpret_cast<uintptr_t>(colsum) % 8) == 0,
+                 "gemm colsum: needs the staged epilogue (N %% 8 == 0, N > 64, aligned output) and an 8-byte aligned buffer");
   if (BN == 256 && pair) rc = dispatch_major<256, true>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else if (BN == 128) rc = dispatch_major<128>(a_mn, b_mn, ta, tb, em, p, ws, stream);

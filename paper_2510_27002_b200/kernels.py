@@ -78,8 +78,12 @@ TIMER: KernelTimer | None = None
 def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: bool, b_kmajor: bool,
          out: torch.Tensor, epilogue: int, bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
          out2: torch.Tensor | None = None, split_k: int = 1, lda: int | None = None, ldb: int | None = None,
-         ldd: int | None = None, ldaux: int | None = None, ldd2: int | None = None) -> torch.Tensor:
-    """out = epilogue(A . B); see include/jz.h for operand layouts."""
+         ldd: int | None = None, ldaux: int | None = None, ldd2: int | None = None,
+         colsum: torch.Tensor | None = None, colsum_accumulate: bool = False) -> torch.Tensor:
+    """out = epilogue(A . B); see include/jz.h for operand layouts.
+
+    colsum (fp32 [N]): also the column sums of the bf16 output (bias gradient of its consumer),
+    reduced from per-32-row partials the epilogue writes (jz_gemm_bf16_colsum)."""
     assert A.dtype == BF16 and B.dtype == BF16, "GEMM operands must be bf16"
     lda = lda if lda is not None else A.stride(0)
     ldb = ldb if ldb is not None else B.stride(0)
@@ -93,14 +97,23 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: 
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-    L.call("jz_gemm_bf16", A.data_ptr(), lda, int(a_kmajor), B.data_ptr(), ldb, int(b_kmajor), out.data_ptr(),
-           ldd, M, N, K, epilogue, _p(bias), _p(aux), ldaux if ldaux is not None else (aux.stride(0) if aux is not None else 0),
-           _p(out2), ldd2 if ldd2 is not None else (out2.stride(0) if out2 is not None else 0), split_k, _p(ws), _s())
+    la = ldaux if ldaux is not None else (aux.stride(0) if aux is not None else 0)
+    l2 = ldd2 if ldd2 is not None else (out2.stride(0) if out2 is not None else 0)
+    if colsum is not None:
+        nparts = L.load().jz_gemm_colsum_parts(M)
+        part = scratch("gemm_colsum", nparts * N)
+        L.call("jz_gemm_bf16_colsum", A.data_ptr(), lda, int(a_kmajor), B.data_ptr(), ldb, int(b_kmajor),
+               out.data_ptr(), ldd, M, N, K, epilogue, _p(bias), _p(aux), la, _p(out2), l2, part.data_ptr(), _s())
+    else:
+        L.call("jz_gemm_bf16", A.data_ptr(), lda, int(a_kmajor), B.data_ptr(), ldb, int(b_kmajor), out.data_ptr(),
+               ldd, M, N, K, epilogue, _p(bias), _p(aux), la, _p(out2), l2, split_k, _p(ws), _s())
     if timed:
         e1.record()
         TIMER.events.append((e0, e1))
         TIMER.flops += 2 * M * N * K
         TIMER.launches += 1
+    if colsum is not None:
+        reduce_partials(part, nparts, N, colsum, colsum_accumulate)
     return out
 
 
@@ -124,7 +137,7 @@ def linear_fwd(x_bf16: torch.Tensor, w_bf16: torch.Tensor, bias: torch.Tensor | 
 
 
 def linear_dx(dy_bf16: torch.Tensor, w_bf16: torch.Tensor, *, epilogue=L.EPI_F32, out=None, aux=None,
-              out2=None) -> torch.Tensor:
+              out2=None, colsum=None) -> torch.Tensor:
     """dx = dy @ W^T  (W (din, dout) row-major is K-major for this product)."""
     M, N = dy_bf16.shape
     K_in = w_bf16.shape[0]
@@ -132,7 +145,7 @@ def linear_dx(dy_bf16: torch.Tensor, w_bf16: torch.Tensor, *, epilogue=L.EPI_F32
         dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU_BWD) else F32
         out = torch.empty(M, K_in, dtype=dt, device=dy_bf16.device)
     return gemm(dy_bf16, w_bf16, M=M, N=K_in, K=N, a_kmajor=True, b_kmajor=True, out=out, epilogue=epilogue,
-                aux=aux, out2=out2, ldb=w_bf16.stride(0))
+                aux=aux, out2=out2, ldb=w_bf16.stride(0), colsum=colsum)
 
 
 def linear_dw(x_bf16: torch.Tensor, dy_bf16: torch.Tensor, out_f32: torch.Tensor, *, accumulate=False,

@@ -232,8 +232,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         w = ctx["shadows"][i]
         # ---- FFN: x3 = x2 + gelu(LN(x2) Wup + bup) Wdown + bdown
         K.linear_dw(c["h"], dres_b, G[f"{base}.ffn.down.w"])
-        K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_GELU_BWD, out=dh, aux=c["hpre"])
-        K.colsum_bf16(dh, G[f"{base}.ffn.up.b"])
+        K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_GELU_BWD, out=dh, aux=c["hpre"],
+                    colsum=G[f"{base}.ffn.up.b"])  # up-bias gradient from the epilogue's column sums
         K.linear_dw(c["xn3"], dh, G[f"{base}.ffn.up.w"])
         K.linear_dx(dh, w["ffn.wup"], epilogue=L.EPI_F32, out=dtmp)
         K.layernorm_bwd(c["x2"], c["m3"], c["r3"], P[f"{base}.ffn.ln.g"].data, dtmp, dres, accumulate=True,

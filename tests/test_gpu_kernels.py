@@ -98,6 +98,23 @@ def test_gemm_epilogues(M):
     assert rel(gb, xp.grad) < 5e-3
 
 
+@pytest.mark.parametrize("M,N", [(4096 + 77, 2048), (1000, 512), (96, 1536)])
+def test_gemm_colsum_epilogue(M, N):
+    """Column sums of the bf16 output (bias gradient of the consumer) from the epilogue partials."""
+    K = 256
+    X, W, A, B = _operands(M, N, K, 1, 1, M + N)
+    pre = (torch.randn(M, N, device=dev) * 2).bfloat16()
+    out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    cs = torch.full((N,), float("nan"), device=dev)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=1, out=out, epilogue=L.EPI_GELU_BWD, aux=pre, colsum=cs)
+    ref = torch.empty_like(cs)
+    Kn.colsum_bf16(out, ref)
+    assert rel(cs, ref) < 1e-6
+    out2 = torch.empty_like(out)
+    Kn.gemm(A, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=1, out=out2, epilogue=L.EPI_GELU_BWD, aux=pre)
+    assert torch.equal(out, out2)
+
+
 def test_gemm_rejects_bad_shapes():
     A = torch.zeros(64, 64, device=dev, dtype=torch.bfloat16)
     D = torch.zeros(64, 64, device=dev)
