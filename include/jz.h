@@ -102,6 +102,8 @@ JZ_API int jz_gemm_bf16_colsum(const void* A, int64_t lda, int a_kmajor, const v
 JZ_API int jz_row_partials(int64_t rows);
 JZ_API int jz_colsum_bf16(const void* x, int64_t rows, int cols, int64_t ld, float* part, int nparts,
                           jz_stream_t stream);
+/* out[c] (+)= sum_p part[p][c] in a fixed order.  With nparts > 512 the reduction runs in two stages
+ * and uses `part` as scratch (rows 0, 256, 512, ... are overwritten). */
 JZ_API int jz_reduce_partials(const float* part, int nparts, int64_t D, float* out, int accumulate,
                               jz_stream_t stream);
 /* dst_bf16[r*ldd + c] = bf16(src[r*lds + c])  (weight shadows) */
@@ -200,9 +202,12 @@ JZ_API int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, in
  * dP - Delta does not cancel against the bf16 rounding of O.  workspace: caller-owned,
  * jz_attn_spatial_bwd_workspace_bytes(frames, S, H) bytes, 16-byte aligned. */
 JZ_API int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H);
+/* colsum_part (nullable): fp32 [jz_attn_spatial_colsum_parts(frames)][3*H*64] partial column sums
+ * of dqkv (the QKV bias gradient after jz_reduce_partials), written instead of re-reading dqkv. */
+JZ_API int64_t jz_attn_spatial_colsum_parts(int64_t frames);
 JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
                                int64_t frames, int S, int H, int head_dim, void* dqkv, void* workspace,
-                               jz_stream_t stream);
+                               float* colsum_part, jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K4  causal temporal (inter-frame) attention (st.py:74-76, nn.py:103-105):
@@ -211,8 +216,11 @@ JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void
  * ---------------------------------------------------------------------- */
 JZ_API int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, int H, int head_dim, void* out,
                                 float* lse, jz_stream_t stream);
+/* colsum_part (nullable): fp32 [jz_attn_temporal_colsum_parts(B, S)][3*H*64], as the spatial one. */
+JZ_API int64_t jz_attn_temporal_colsum_parts(int64_t B, int S);
 JZ_API int jz_attn_temporal_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
-                                int64_t B, int T, int S, int H, int head_dim, void* dqkv, jz_stream_t stream);
+                                int64_t B, int T, int S, int H, int head_dim, void* dqkv, float* colsum_part,
+                                jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K9  frames -> patches and back (tokenizer.py:49-55, nn.py:113-131).

@@ -481,14 +481,38 @@ JZ_DEV void bwd_stage_acc(uint8_t* wstage, uint32_t taddr, float coef, const flo
   __syncwarp();
 }
 
+// ... and, when `part` is set, the warp's column sums over its 32 rows (8 columns per lane of the
+// first 8 lanes) into one partial row: part[col .. col + 63] (bias gradients of the QKV layer).
 JZ_DEV void bwd_flush_rows(const uint8_t* wstage, __nv_bfloat16* dqkv, int64_t row_first, int64_t ld3, int64_t col,
-                           int lane) {
+                           int lane, float* part) {
   const int cch = lane & 7;
+  float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int rr = 4 * k + (lane >> 3);
     const uint4 w = *reinterpret_cast<const uint4*>(wstage + rr * 128 + ((cch ^ (rr & 7)) << 4));
     *reinterpret_cast<uint4*>(dqkv + (row_first + rr) * ld3 + col + 8 * cch) = w;
+    if (part != nullptr) {
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = unpack_bf16(ww[e]);
+        cs[2 * e] += f.x;
+        cs[2 * e + 1] += f.y;
+      }
+    }
+  }
+  if (part != nullptr) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 8);
+      cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 16);
+    }
+    if (lane < 8) {
+      float4* dst = reinterpret_cast<float4*>(part + col + 8 * cch);
+      dst[0] = make_float4(cs[0], cs[1], cs[2], cs[3]);
+      dst[1] = make_float4(cs[4], cs[5], cs[6], cs[7]);
+    }
   }
   __syncwarp();
 }
@@ -497,7 +521,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     spatial_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                        const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ delta,
                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
-                       __nv_bfloat16* __restrict__ dqkv, int frames, int S, int H) {
+                       __nv_bfloat16* __restrict__ dqkv, float* __restrict__ colsum, int frames, int S, int H) {
   using namespace sp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -775,7 +799,10 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     // of the staging tile (128B-swizzled), read back 4 rows x 128 B per instruction
     uint8_t* wstage = smem + B_ST + quarter * 4096;
 #define stage_acc(col, coef, vec, sc) bwd_stage_acc(wstage, base + (col), (coef), (vec), (sc), lane)
-#define flush_rows(row_first, col) bwd_flush_rows(wstage, dqkv, (row_first), ld3, (col), lane)
+// colsum partial rows: [frame][9][3D], row block = 4 * (row tile) + quarter, block 8 = token 256
+#define flush_rows(row_first, col)                                                                        \
+  bwd_flush_rows(wstage, dqkv, (row_first), ld3, (col), lane,                                             \
+                 colsum ? colsum + ((int64_t)f * 9 + (((row_first) - row0) >> 5)) * ld3 : nullptr)
 
     int i = 0;
     if (blockIdx.x < units) prepare(blockIdx.x, 0);
@@ -848,13 +875,27 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
             skk += sm.tail_red[1][pt][d];
             sv += sm.tail_red[2][pt][d];
           }
-          dqkv[rr * ld3 + h * 64 + d] = __float2bfloat16_rn(scale * sq);
-          dqkv[rr * ld3 + D + h * 64 + d] = __float2bfloat16_rn(scale * skk);
-          dqkv[rr * ld3 + 2 * D + h * 64 + d] = __float2bfloat16_rn(sv);
+          const __nv_bfloat16 bq = __float2bfloat16_rn(scale * sq), bk = __float2bfloat16_rn(scale * skk),
+                              bv = __float2bfloat16_rn(sv);
+          dqkv[rr * ld3 + h * 64 + d] = bq;
+          dqkv[rr * ld3 + D + h * 64 + d] = bk;
+          dqkv[rr * ld3 + 2 * D + h * 64 + d] = bv;
+          if (colsum) {
+            float* pr = colsum + ((int64_t)f * 9 + 8) * ld3 + h * 64 + d;
+            pr[0] = __bfloat162float(bq);
+            pr[D] = __bfloat162float(bk);
+            pr[2 * D] = __bfloat162float(bv);
+          }
         }
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.inputs_free);
+        if (colsum && ht < 64) {  // S = 256: no token 256, its partial row is zero
+          float* pr = colsum + ((int64_t)f * 9 + 8) * ld3 + h * 64 + ht;
+          pr[0] = 0.f;
+          pr[D] = 0.f;
+          pr[2 * D] = 0.f;
+        }
       }
       // ---- next unit's vectors (the P/dS warps of this unit are past j = 0 already) ----
       if (u + (int)gridDim.x < units) prepare(u + gridDim.x, pb ^ 1);
@@ -935,9 +976,11 @@ extern "C" int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, in
   return frames * (int64_t)S * H * (int64_t)sizeof(float);
 }
 
+extern "C" int64_t jz_attn_spatial_colsum_parts(int64_t frames) { return frames * 9; }
+
 extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
                                    int64_t frames, int S, int H, int head_dim, void* dqkv, void* workspace,
-                                   jz_stream_t s) {
+                                   float* colsum_part, jz_stream_t s) {
   using namespace jz;
   JZ_CHECK_ARG(head_dim == 64, "spatial attention bwd: head_dim %d unsupported (64)", head_dim);
   JZ_CHECK_ARG(S == 256 || S == 257, "spatial attention bwd: sequence length %d unsupported", S);
@@ -967,7 +1010,8 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
   const int grid = (int)(units < num_sms() ? units : num_sms());
   spatial_bwd_kernel<<<grid, sp::kBwdThreads2, sp::B_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
       tq, td, reinterpret_cast<const __nv_bfloat16*>(qkv), delta,
-      reinterpret_cast<const __nv_bfloat16*>(dout), lse, reinterpret_cast<__nv_bfloat16*>(dqkv), (int)frames, S, H);
+      reinterpret_cast<const __nv_bfloat16*>(dout), lse, reinterpret_cast<__nv_bfloat16*>(dqkv), colsum_part,
+      (int)frames, S, H);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

@@ -126,8 +126,10 @@ JZ_DEV void c_to_smem(__nv_bfloat16* dst, const float (&c)[2][4]) {
 
 // out[16 rows][64] = A(16x16) . B where B rows (k) are stored [k][n] pitch ld; writes rows < T of
 // global `dst` (row index (b*T + r)*S + s, pitch dld, column offset col0) scaled by mul (per row)
+// `part` (optional): column sums over the T stored rows of the bf16 values, one fp32 partial
+// row for this (b, s) at columns col0 .. col0 + 63 (QKV bias gradients, no re-read of dqkv).
 JZ_DEV void av_store(const uint32_t (&a)[4], const __nv_bfloat16* bsm, int ld, __nv_bfloat16* dst, int64_t dld,
-                     int col0, int64_t b, int T, int S, int64_t s, float mul0, float mul1) {
+                     int col0, int64_t b, int T, int S, int64_t s, float mul0, float mul1, float* part = nullptr) {
   const int L = lane_id();
   const int r0 = L >> 2, cq = 2 * (L & 3);
 #pragma unroll
@@ -138,15 +140,36 @@ JZ_DEV void av_store(const uint32_t (&a)[4], const __nv_bfloat16* bsm, int ld, _
     mma16816(o0, a, bb[0], bb[1]);
     mma16816(o1, a, bb[2], bb[3]);
     const int dcol = col0 + 16 * np + cq;
+    const uint32_t w00 = pack_bf16(o0[0] * mul0, o0[1] * mul0), w01 = pack_bf16(o1[0] * mul0, o1[1] * mul0);
+    const uint32_t w10 = pack_bf16(o0[2] * mul1, o0[3] * mul1), w11 = pack_bf16(o1[2] * mul1, o1[3] * mul1);
     if (r0 < T) {
       __nv_bfloat16* row = dst + ((b * T + r0) * S + s) * dld + dcol;
-      *reinterpret_cast<uint32_t*>(row) = pack_bf16(o0[0] * mul0, o0[1] * mul0);
-      *reinterpret_cast<uint32_t*>(row + 8) = pack_bf16(o1[0] * mul0, o1[1] * mul0);
+      *reinterpret_cast<uint32_t*>(row) = w00;
+      *reinterpret_cast<uint32_t*>(row + 8) = w01;
     }
     if (r0 + 8 < T) {
       __nv_bfloat16* row = dst + ((b * T + r0 + 8) * S + s) * dld + dcol;
-      *reinterpret_cast<uint32_t*>(row) = pack_bf16(o0[2] * mul1, o0[3] * mul1);
-      *reinterpret_cast<uint32_t*>(row + 8) = pack_bf16(o1[2] * mul1, o1[3] * mul1);
+      *reinterpret_cast<uint32_t*>(row) = w10;
+      *reinterpret_cast<uint32_t*>(row + 8) = w11;
+    }
+    if (part != nullptr) {
+      float2 c0 = r0 < T ? unpack_bf16(w00) : make_float2(0.f, 0.f);
+      float2 c1 = r0 < T ? unpack_bf16(w01) : make_float2(0.f, 0.f);
+      if (r0 + 8 < T) {
+        const float2 e0 = unpack_bf16(w10), e1 = unpack_bf16(w11);
+        c0.x += e0.x; c0.y += e0.y; c1.x += e1.x; c1.y += e1.y;
+      }
+#pragma unroll
+      for (int m = 4; m <= 16; m <<= 1) {  // sum over the 8 row groups (lanes with equal L & 3)
+        c0.x += __shfl_xor_sync(0xffffffffu, c0.x, m);
+        c0.y += __shfl_xor_sync(0xffffffffu, c0.y, m);
+        c1.x += __shfl_xor_sync(0xffffffffu, c1.x, m);
+        c1.y += __shfl_xor_sync(0xffffffffu, c1.y, m);
+      }
+      if (r0 == 0) {
+        *reinterpret_cast<float2*>(part + dcol) = c0;
+        *reinterpret_cast<float2*>(part + dcol + 8) = c1;
+      }
     }
   }
 }
@@ -209,7 +232,8 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
                                                            const __nv_bfloat16* __restrict__ o,
                                                            const __nv_bfloat16* __restrict__ dout,
                                                            const float* __restrict__ lse, int T, int S, int H,
-                                                           __nv_bfloat16* __restrict__ dqkv, float scale) {
+                                                           __nv_bfloat16* __restrict__ dqkv, float scale,
+                                                           float* __restrict__ colsum) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int D = H * HD;
   const int ldq = 3 * D + 8, ldo = D + 8;
@@ -266,18 +290,19 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
   __syncwarp();
   // dQ = scale * dS K      (A = dS from registers, B = K stored [j][d])
   uint32_t a[4];
+  float* part = colsum ? colsum + bs * (3 * D) : nullptr;  // one partial row per (b, s)
   c_to_a(a, dS);
-  av_store(a, k, ldq, dqkv, 3 * D, h * HD, b, T, S, s, scale, scale);
+  av_store(a, k, ldq, dqkv, 3 * D, h * HD, b, T, S, s, scale, scale, part);
   // dK = scale * dS^T Q    (A = dS^T from smem, B = Q stored [t][d])
   load_a_trans(a, sdS, LDP);
-  av_store(a, q, ldq, dqkv, 3 * D, D + h * HD, b, T, S, s, scale, scale);
+  av_store(a, q, ldq, dqkv, 3 * D, D + h * HD, b, T, S, s, scale, scale, part);
   // dV = P^T dO
   load_a_trans(a, sP, LDP);
-  av_store(a, dog, ldo, dqkv, 3 * D, 2 * D + h * HD, b, T, S, s, 1.0f, 1.0f);
+  av_store(a, dog, ldo, dqkv, 3 * D, 2 * D + h * HD, b, T, S, s, 1.0f, 1.0f, part);
 }
 
 static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B,
-                             int T, int S, int H, void* out, cudaStream_t st) {
+                             int T, int S, int H, void* out, cudaStream_t st, float* colsum = nullptr) {
   JZ_CHECK_ARG(H >= 1 && H <= 16, "temporal attention: heads %d unsupported (<= 16)", H);
   JZ_CHECK_ARG(T >= 1 && T <= 16, "temporal attention: T=%d unsupported (<= 16)", T);
   const float scale = 0.125f;  // 1/sqrt(64)
@@ -295,7 +320,8 @@ static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const voi
     JZ_CUDA_TRY(cudaFuncSetAttribute(temporal_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     temporal_bwd_kernel<<<(unsigned)BS, threads, smem, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(o),
-        reinterpret_cast<const __nv_bfloat16*>(dout), lse, T, S, H, reinterpret_cast<__nv_bfloat16*>(out), scale);
+        reinterpret_cast<const __nv_bfloat16*>(dout), lse, T, S, H, reinterpret_cast<__nv_bfloat16*>(out), scale,
+        colsum);
   }
   JZ_LAUNCH_CHECK();
   return JZ_OK;
@@ -311,9 +337,12 @@ extern "C" int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, in
   return dispatch_temporal(false, qkv, nullptr, nullptr, lse, B, T, S, H, out, reinterpret_cast<cudaStream_t>(s));
 }
 
+extern "C" int64_t jz_attn_temporal_colsum_parts(int64_t B, int S) { return B * S; }
+
 extern "C" int jz_attn_temporal_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
-                                    int64_t B, int T, int S, int H, int head_dim, void* dqkv, jz_stream_t s) {
+                                    int64_t B, int T, int S, int H, int head_dim, void* dqkv, float* colsum_part,
+                                    jz_stream_t s) {
   JZ_CHECK_ARG(head_dim == 64, "temporal attention: head_dim %d unsupported (64)", head_dim);
   return dispatch_temporal(true, qkv, out, dout, const_cast<float*>(lse), B, T, S, H, dqkv,
-                           reinterpret_cast<cudaStream_t>(s));
+                           reinterpret_cast<cudaStream_t>(s), colsum_part);
 }

@@ -203,9 +203,10 @@ __global__ void __launch_bounds__(kRowThreads) colsum_bf16_kernel(const __nv_bfl
   }
 }
 
-// out[c] = sum_p part[p][c]: 8 fixed part-groups x 32 columns per CTA, groups combined in order.
+// out[c] = sum_p part[p * stride][c]: 8 fixed part-groups x 32 columns per CTA, groups combined in order.
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ part, int nparts, int64_t D,
-                                                             float* __restrict__ out, int accumulate) {
+                                                             float* __restrict__ out, int accumulate,
+                                                             int stride = 1) {
   __shared__ float sm[8][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < D; c0 += (int64_t)gridDim.x * 32) {
@@ -214,10 +215,10 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
     if (c < D) {
       int p = grp;
       for (; p + 8 < nparts; p += 16) {
-        s0 += part[(int64_t)p * D + c];
-        s1 += part[(int64_t)(p + 8) * D + c];
+        s0 += part[(int64_t)p * stride * D + c];
+        s1 += part[(int64_t)(p + 8) * stride * D + c];
       }
-      if (p < nparts) s0 += part[(int64_t)p * D + c];
+      if (p < nparts) s0 += part[(int64_t)p * stride * D + c];
     }
     sm[grp][lane] = s0 + s1;
     __syncthreads();
@@ -228,6 +229,35 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
       out[c] = accumulate ? out[c] + t : t;
     }
     __syncthreads();
+  }
+}
+
+// Stage 1 for many partial rows: CTA (column block x, chunk y) sums rows [256 y, 256 y + 256) of its
+// 32 columns in a fixed order and writes the result into row 256 y (a row only it reads).
+constexpr int kChunkRows = 256;
+__global__ void __launch_bounds__(256) reduce_chunks_kernel(float* __restrict__ part, int nparts, int64_t D) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const int p0 = blockIdx.y * kChunkRows, p1 = min(nparts, p0 + kChunkRows);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (c < D) {
+    int p = p0 + grp;
+    for (; p + 24 < p1; p += 32) {
+      s0 += part[(int64_t)p * D + c];
+      s1 += part[(int64_t)(p + 8) * D + c];
+      s2 += part[(int64_t)(p + 16) * D + c];
+      s3 += part[(int64_t)(p + 24) * D + c];
+    }
+    for (; p < p1; p += 8) s0 += part[(int64_t)p * D + c];
+  }
+  sm[grp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (grp == 0 && c < D) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][lane];
+    part[(int64_t)p0 * D + c] = t;
   }
 }
 
@@ -449,10 +479,20 @@ extern "C" int jz_colsum_bf16(const void* x, int64_t rows, int cols, int64_t ld,
 extern "C" int jz_reduce_partials(const float* part, int nparts, int64_t D, float* out, int accumulate,
                                   jz_stream_t s) {
   if (D == 0) return JZ_OK;
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  int stride = 1;
+  if (nparts > 2 * kChunkRows) {
+    // two deterministic stages; the partial buffer is scratch (its chunk-leading rows are overwritten)
+    const int chunks = (nparts + kChunkRows - 1) / kChunkRows;
+    reduce_chunks_kernel<<<dim3((unsigned)((D + 31) / 32), (unsigned)chunks), 256, 0, st>>>(
+        const_cast<float*>(part), nparts, D);
+    JZ_LAUNCH_CHECK();
+    nparts = chunks;
+    stride = kChunkRows;
+  }
   int64_t blocks = (D + 31) / 32;
   if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
-  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(part, nparts, D, out,
-                                                                                          accumulate);
+  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, nparts, D, out, accumulate, stride);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

@@ -246,12 +246,19 @@ def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: b
     return out, out32, lse
 
 
-def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=None):
+def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=None, colsum=None):
+    """colsum (fp32 [3*H*64], optional): also the column sums of dqkv (QKV bias gradient)."""
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
     ws = scratch("attn_delta", frames * S * H)
+    part, nparts = None, 0
+    if colsum is not None:
+        nparts = L.load().jz_attn_spatial_colsum_parts(frames)
+        part = scratch("attn_colsum", nparts * 3 * H * 64)
     L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
-           64, dqkv.data_ptr(), ws.data_ptr(), _s())
+           64, dqkv.data_ptr(), ws.data_ptr(), _p(part), _s())
+    if colsum is not None:
+        reduce_partials(part, nparts, 3 * H * 64, colsum)
     return dqkv
 
 
@@ -263,11 +270,18 @@ def attn_temporal_fwd(qkv: torch.Tensor, B: int, T: int, S: int, H: int):
     return out, lse
 
 
-def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=None):
+def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=None, colsum=None):
+    """colsum (fp32 [3*H*64], optional): also the column sums of dqkv (QKV bias gradient)."""
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
+    part, nparts = None, 0
+    if colsum is not None:
+        nparts = L.load().jz_attn_temporal_colsum_parts(B, S)
+        part = scratch("attn_colsum", nparts * 3 * H * 64)
     L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, T, S, H, 64,
-           dqkv.data_ptr(), _s())
+           dqkv.data_ptr(), _p(part), _s())
+    if colsum is not None:
+        reduce_partials(part, nparts, 3 * H * 64, colsum)
     return dqkv
 
 

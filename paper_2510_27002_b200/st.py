@@ -242,8 +242,9 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         # ---- temporal: x2 = x1 + attn_t(LN(x1)) Wo + bo
         K.linear_dw(c["ao2"], dres_b, G[f"{base}.temporal.o.w"])
         K.linear_dx(dres_b, w["temporal.wo"], epilogue=L.EPI_BF16, out=dao)
-        dqkv = K.attn_temporal_bwd(c["qkv2"], c["ao2"], dao, c["lse_t"], B, T, S, H)
-        _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d, gst)
+        gbt = gst.block_of(gst.grad_flat, f"{base}.temporal.q.b") if gst is not None else None
+        dqkv = K.attn_temporal_bwd(c["qkv2"], c["ao2"], dao, c["lse_t"], B, T, S, H, colsum=gbt)
+        _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d, gst, bias_done=gbt is not None)
         K.linear_dx(dqkv, w["temporal.wqkv"], epilogue=L.EPI_F32, out=dtmp)
         K.layernorm_bwd(c["x1"], c["m2"], c["r2"], P[f"{base}.temporal.ln.g"].data, dtmp, dres, accumulate=True,
                         dres_bf16=dres_b, dgamma=G[f"{base}.temporal.ln.g"], dbeta=G[f"{base}.temporal.ln.b"],
@@ -251,6 +252,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         # ---- spatial: x1 = x + attn_s(LN(x)) Wo + bo
         K.linear_dw(c["ao"], dres_b, G[f"{base}.spatial.o.w"])
         K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao)
+        # (the spatial kernel can emit the bias column sums too, but its helper warps are its critical
+        # path: a separate pass over dqkv measured faster)
         dqkv = K.attn_spatial_bwd(c["qkv"], c["ao32"], dao, c["lse_s"], frames, S, H, dqkv=dqkv)
         _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst)
         K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_F32, out=dtmp)
@@ -265,12 +268,15 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
     return dres
 
 
-def _qkv_param_grads(dqkv: torch.Tensor, xn: torch.Tensor, G: dict, base: str, d: int, st=None) -> None:
+def _qkv_param_grads(dqkv: torch.Tensor, xn: torch.Tensor, G: dict, base: str, d: int, st=None,
+                     bias_done: bool = False) -> None:
+    """bias_done: the attention backward already wrote the fused bias gradient (its colsum partials)."""
     if st is not None:
         gw = st.block_of(st.grad_flat, f"{base}.q.w")
         gb = st.block_of(st.grad_flat, f"{base}.q.b")
         if gw is not None and gb is not None:  # one (d, 3d) dW GEMM, bias sums straight into place
-            K.colsum_bf16(dqkv, gb)
+            if not bias_done:
+                K.colsum_bf16(dqkv, gb)
             K.linear_dw(xn, dqkv, gw)
             return
     bq = torch.empty(3 * d, dtype=K.F32, device=dqkv.device)

@@ -176,8 +176,13 @@ def test_attn_spatial_fwd_bwd(S):
     go = torch.randn(o_ref.shape, device=dev, generator=g)
     o_ref.backward(go)
     dqkv = torch.full_like(qkv, float("nan"))
-    Kn.attn_spatial_bwd(qkv, out32, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv)
+    cs = torch.full((3 * D,), float("nan"), device=dev)
+    Kn.attn_spatial_bwd(qkv, out32, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
+                        colsum=cs)
     assert torch.isfinite(dqkv.float()).all()
+    cs_ref = torch.empty_like(cs)
+    Kn.colsum_bf16(dqkv, cs_ref)  # fused bias-gradient column sums == a pass over the written dqkv
+    assert rel(cs, cs_ref) < 1e-5
     for i in range(3):
         got, ref = dqkv[:, i * D:(i + 1) * D], qf.grad[:, i * D:(i + 1) * D]
         assert rel(got, ref) < 2e-2, "qkv"[i]
@@ -199,7 +204,11 @@ def test_attn_temporal_fwd_bwd(T):
     go = torch.randn(o_ref.shape, device=dev, generator=g)
     o_ref.backward(go)
     dout = go.transpose(1, 2).reshape(B * T * S, D).bfloat16().contiguous()
-    dqkv = Kn.attn_temporal_bwd(qkv, out, dout, lse, B, T, S, H)
+    cs = torch.full((3 * D,), float("nan"), device=dev)
+    dqkv = Kn.attn_temporal_bwd(qkv, out, dout, lse, B, T, S, H, colsum=cs)
+    cs_ref = torch.empty_like(cs)
+    Kn.colsum_bf16(dqkv, cs_ref)
+    assert rel(cs, cs_ref) < 1e-5
     scale = float(qf.grad[:, 2 * D:].norm())
     for i in range(3):
         got, ref = dqkv[:, i * D:(i + 1) * D].float(), qf.grad[:, i * D:(i + 1) * D]

@@ -32,7 +32,7 @@ for S in (256, 257):
     WS = torch.empty(frames * S * H, device='cuda')
     f = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
     f2 = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), None, lse.data_ptr(), L.stream_ptr())
-    bw = lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), L.stream_ptr())
+    bw = lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
     fl = 4 * frames * H * S * S * 64
     for name, fn, mult in (("fwd+f32", f, 1), ("fwd", f2, 1), ("bwd", bw, 2.5)):
         us = timeit(fn)

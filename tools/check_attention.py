@@ -73,7 +73,7 @@ dref = qkv_f.grad.reshape(B * T * S, 3 * D)
 dout = go.transpose(1, 2).reshape(B * T * S, D).bfloat16().contiguous()
 dqkv = torch.empty_like(qkv)
 L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, T, S, H, 64,
-       dqkv.data_ptr(), L.stream_ptr())
+       dqkv.data_ptr(), None, L.stream_ptr())
 torch.cuda.synchronize()
 for i, nm in enumerate("qkv"):
     check(f"temporal bwd d{nm}", dqkv[:, i * D:(i + 1) * D], dref[:, i * D:(i + 1) * D], 2e-2)
@@ -95,7 +95,7 @@ if "spatial_bwd" in sys.argv:
         dout = go.reshape(frames * S, D).bfloat16().contiguous()
         dqkv = torch.full_like(qkv, float("nan"))
         L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
-               64, dqkv.data_ptr(), torch.empty(frames * S * H, device=dev).data_ptr(), L.stream_ptr())
+               64, dqkv.data_ptr(), torch.empty(frames * S * H, device=dev).data_ptr(), None, L.stream_ptr())
         torch.cuda.synchronize()
         for i, nm in enumerate("qkv"):
             check(f"spatial bwd S={S} d{nm}", dqkv[:, i * D:(i + 1) * D], dref[:, i * D:(i + 1) * D], 2e-2)
@@ -130,10 +130,10 @@ us = timeit(lambda: L.call("jz_attn_temporal_fwd", qkv.data_ptr(), 36, 16, S, H,
 print(f"temporal fwd B36: {us:.1f} us  {(qkv.numel() * 2 + out.numel() * 2) / us / 1e3:.0f} GB/s", flush=True)
 dq = torch.empty_like(qkv)
 WS = torch.empty(frames * S * H, device='cuda')
-us = timeit(lambda: L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), out.data_ptr(), lse_t.data_ptr(), 36, 16, S, H, 64, dq.data_ptr(), L.stream_ptr()))
+us = timeit(lambda: L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), out.data_ptr(), lse_t.data_ptr(), 36, 16, S, H, 64, dq.data_ptr(), None, L.stream_ptr()))
 print(f"temporal bwd B36: {us:.1f} us  {(qkv.numel() * 4 + out.numel() * 4) / us / 1e3:.0f} GB/s", flush=True)
 if "spatial_bwd" in sys.argv:
-    us = timeit(lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), L.stream_ptr()))
+    us = timeit(lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr()))
     print(f"spatial bwd B36: {us:.1f} us  {2.5 * fl / us / 1e6:.0f} TFLOP/s", flush=True)
 print("ALL OK" if ok else "SOME FAILED")
 sys.exit(0 if ok else 1)

@@ -23,7 +23,7 @@ dq = torch.empty_like(qkv)
 WS = torch.empty(frames * S * H, device='cuda')
 L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
 for _ in range(3):
-    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), L.stream_ptr())
+    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
 torch.cuda.synchronize()
 buf = np.zeros(64 * 32, dtype=np.uint64)
 lib.jz_attn_prof_read.argtypes = [C.c_void_p]
