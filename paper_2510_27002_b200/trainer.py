@@ -64,3 +64,34 @@ class DynamicsTrainStep:
         adamw_step(m.params, {n: p.grad for n, p in m.params.items()}, self.opt, wsd_lr(self.schedule, step + 1),
                    check="deferred")
         return loss
+
+    # -- checkpoint / resume (trainer.py:91-115, 442-473) ------------------------------
+    def pack(self, step: int, config: dict | None = None, loader_state=None):
+        """JASCKPT1 bundle of this stage (params + AdamW moments + loader state), deskworld layout."""
+        from .checkpoint import pack_stage
+        from .records import LoaderState
+        ls = loader_state if loader_state is not None else LoaderState(seed=self.seed)
+        return pack_stage(self.stage, config or {}, self.model.params, self.opt, ls, step, self.seed)
+
+    def restore(self, bundle) -> tuple:
+        """Load a bundle into the live device tensors; returns (loader_state dict, step)."""
+        from .checkpoint import restore_stage
+        _, ls, step = restore_stage(bundle, self.model.params, self.opt)
+        return ls, step
+
+
+class PretrainLamStep:
+    """The pretrain_lam dynamics-stage step from raw frames (trainer.py:297-305): frozen tokenizer
+    tokens + frozen LAM action latents (codebook rows of the inferred actions) -> dynamics step.
+
+    frames: device uint8 (B, T, H, W, C), e.g. straight from records.DeviceBatchLoader."""
+
+    def __init__(self, tokenizer, lam, dynamics: DynamicsModel, schedule: WsdSchedule, **kw):
+        self.tokenizer, self.lam = tokenizer, lam
+        self.inner = DynamicsTrainStep(dynamics, schedule, **kw)
+
+    def step(self, step: int, frames: torch.Tensor):
+        tokens = self.tokenizer.encode_device(frames)
+        idx = self.lam.infer_actions_device(frames)
+        latents = Tensor(self.lam.params["codebook"].data[idx])
+        return self.inner.step(step, tokens, latents)

@@ -205,9 +205,54 @@ def gen_jasmine_summary():
     print(f"jasmine summary in {time.time() - t0:.1f}s")
 
 
+def gen_checkpoint():
+    """A JASCKPT1 bundle written by the reference's save_checkpoint (checkpoint.py:40-66)."""
+    from deskworld.checkpoint import CheckpointBundle, save_checkpoint
+    g = R.stream(7, "ckpt-golden")
+    arrays = {"param.w": g.normal(size=(3, 5)).astype(np.float32),
+              "param.b": g.normal(size=(5,)).astype(np.float32),
+              "adam.m.w": np.zeros((3, 5), np.float32),
+              "counts": np.arange(6, dtype=np.int64).reshape(2, 3),
+              "scalar": np.array(2.5, dtype=np.float64)}
+    bundle = CheckpointBundle(step=42, config={"preset": "tiny", "lr": 3e-5, "dims": [4, 8]}, arrays=arrays,
+                              loader_state={"seed": 3, "epoch": 1, "cursor": 8, "prefetch_depth": 2},
+                              rng_state={"seed": 3, "stage": "dynamics"},
+                              meta={"stage": "dynamics", "seed": 3,
+                                    "adam": {"t": 5, "beta1": 0.9, "beta2": 0.999, "eps": 1e-8, "weight_decay": 0.0}})
+    save_checkpoint(bundle, OUT / "ckpt_ref.jasckpt")
+    print("wrote ckpt_ref.jasckpt")
+
+
+def gen_records():
+    """A tiny JASREC dataset (records.py:120-169) and the reference loader's first batches."""
+    import shutil
+
+    from deskworld.env import Episode
+    from deskworld.records import Chunking, LoaderState, shuffled_batches, write_dataset
+    root = OUT / "jasrec_ref"
+    shutil.rmtree(root, ignore_errors=True)
+    g = R.stream(8, "jasrec-golden")
+    eps = []
+    for s in range(7):
+        n = int(g.integers(10, 30))
+        eps.append(Episode(seed=100 + s, frames=g.integers(0, 256, size=(n, 8, 8, 3), dtype=np.uint8),
+                           actions=g.integers(0, 6, size=(n,)).astype(np.uint8)))
+    index = write_dataset(iter(eps), Chunking(frames_per_record=8, records_per_file=4), root)
+    it = shuffled_batches(index, LoaderState(seed=11), batch_size=3, seq_len=5)
+    out = {}
+    for k in range(5):
+        fr, ac, st = next(it)
+        out[f"frames{k}"] = fr
+        out[f"actions{k}"] = ac
+        out[f"state{k}"] = np.array([st.seed, st.epoch, st.cursor, st.prefetch_depth], dtype=np.int64)
+    save("records", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "vq", "dynamics", "toklam", "sampling", "adamw", "jasmine"]
+    which = sys.argv[1:] or ["rng", "vq", "dynamics", "toklam", "sampling", "adamw", "jasmine", "checkpoint",
+                             "records"]
     fns = {"rng": gen_rng, "vq": gen_vq, "dynamics": gen_dynamics, "toklam": gen_tokenizer_lam,
-           "sampling": gen_sampling, "adamw": gen_adamw, "jasmine": gen_jasmine_summary}
+           "sampling": gen_sampling, "adamw": gen_adamw, "jasmine": gen_jasmine_summary,
+           "checkpoint": gen_checkpoint, "records": gen_records}
     for w in which:
         fns[w]()
