@@ -184,7 +184,50 @@ def secondary_configs(dev) -> dict:
     out["tokenizer_train"] = {"metric": "tokenizer train frames/sec", "value": round(8 * FRAMES_T / (ms3 / 1e3), 1),
                               "unit": "frames/s", "ms_per_step": round(ms3, 2),
                               "config": "B=8, T=16, 1024 codes, recon + VQ losses, full backward"}
+    out["pretrain_lam_stage"] = _pretrain_lam_stage(tok, lam, dev)
     return out
+
+
+def _pretrain_lam_stage(tok, lam, dev) -> dict:
+    """SURVEY §8d 'C3 full pretrain_lam stage step' from disk: JASREC records (synthetic frames
+    written to a temp dir) -> DeviceBatchLoader (pinned ring, H2D u8) -> frozen tokenizer encode +
+    LAM action inference -> dynamics train step, B=36, jasmine-base dims."""
+    import tempfile
+
+    import numpy as np
+
+    from paper_2510_27002_b200.dynamics import DynamicsConfig, DynamicsModel
+    from paper_2510_27002_b200.optim import WsdSchedule
+    from paper_2510_27002_b200.records import Chunking, DeviceBatchLoader, LoaderState, write_dataset
+    from paper_2510_27002_b200.rng import stream
+    from paper_2510_27002_b200.trainer import PretrainLamStep
+
+    B = 36
+
+    class _Ep:
+        def __init__(self, seed, frames, actions):
+            self.seed, self.frames, self.actions = seed, frames, actions
+
+    g = stream(9, "bench-records")
+    with tempfile.TemporaryDirectory() as root:
+        eps = (_Ep(i, g.integers(0, 256, size=(32, 64, 64, 3), dtype=np.uint8), np.zeros(32, np.uint8))
+               for i in range(2 * B))
+        index = write_dataset(eps, Chunking(frames_per_record=32, records_per_file=16), root)
+        dyn = DynamicsModel(DynamicsConfig(patches_per_frame=PATCHES, max_frames=FRAMES_T), seed=0)
+        step = PretrainLamStep(tok, lam, dyn, WsdSchedule(peak_lr=3e-5, total_steps=200_000), seed=0)
+        loader = DeviceBatchLoader(index, LoaderState(seed=1), batch_size=B, seq_len=FRAMES_T, depth=2)
+        try:
+            for k in range(2):
+                frames, _, _ = next(loader)
+                step.step(k, frames)
+            n = 4
+            ms = _events_ms(lambda: step.step(2, next(loader)[0]), reps=n)
+        finally:
+            loader.close()
+    return {"metric": "pretrain_lam stage frames/sec", "value": round(B * FRAMES_T / (ms / 1e3), 1), "unit": "frames/s",
+            "ms_per_step": round(ms, 2),
+            "config": "B=36, T=16 from JASREC on local disk via the device loader; tokenizer encode + LAM infer + "
+                      "dynamics step (SURVEY §8d: ~60.5 GFLOP/frame)"}
 
 
 def run_reference(args) -> None:
