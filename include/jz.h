@@ -128,6 +128,11 @@ JZ_API int jz_layernorm_bwd(const float* x, const float* mean, const float* rstd
                             const float* dy, float* dres, int accumulate, void* dres_bf16,
                             float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
                             int64_t rows, int D, int64_t skip_period, jz_stream_t stream);
+/* Same with dy bf16 (the producing dX GEMM writes bf16: half the bytes of this HBM-bound pass). */
+JZ_API int jz_layernorm_bwd_bf16dy(const float* x, const float* mean, const float* rstd, const float* gamma,
+                                   const void* dy, float* dres, int accumulate, void* dres_bf16,
+                                   float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
+                                   int64_t rows, int D, int64_t skip_period, jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K7  masked softmax cross-entropy (nn.py:56-77 with weights = mask,

@@ -37,6 +37,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_cast_f32_bf16_2d": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "jz_layernorm_fwd": [_P, _I64, _I32, _P, _P, _F32, _P, _P, _P, _P, _I64, _P],
     "jz_layernorm_bwd": [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I64, _I32, _I64, _P],
+    "jz_layernorm_bwd_bf16dy": [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I64, _I32, _I64, _P],
     "jz_ce_fwd_bwd": [_P, _I64, _I32, _P, _P, _P, _F32, _P, _P, _P, _P],
     "jz_finite_check": [_P, _I64, _P, _P],
     "jz_adamw_step": [_P, _P, _P, _P, _I64, _F32, _F32, _F32, _F32, _F32, _F32, _F32, _F32, _F32, _P, _P],

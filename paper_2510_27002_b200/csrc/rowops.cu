@@ -82,10 +82,18 @@ __global__ void __launch_bounds__(kRowThreads) ln_fwd_kernel(const float* __rest
 // One CTA owns rows [blk*rpb, (blk+1)*rpb); warps stride by 8 inside; warp partials are
 // combined in warp order through shared memory.
 // ---------------------------------------------------------------------------
-template <int V4>
+// dy row loader: fp32 or bf16 (the dX GEMM's bf16 output halves the bytes of this HBM-bound pass)
+JZ_DEV float4 load4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+JZ_DEV float4 load4(const __nv_bfloat16* p) {
+  const uint2 w = *reinterpret_cast<const uint2*>(p);
+  const float2 a = unpack_bf16(w.x), b = unpack_bf16(w.y);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <int V4, typename DyT>
 __global__ void __launch_bounds__(kRowThreads, 2) ln_bwd_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
-    const float* __restrict__ g, const float* __restrict__ dy, float* dres, int accumulate,
+    const float* __restrict__ g, const DyT* __restrict__ dy, float* dres, int accumulate,
     __nv_bfloat16* __restrict__ dres_bf16, float* __restrict__ part_dg, float* __restrict__ part_db,
     float* __restrict__ part_dbias, int64_t rows, int64_t rows_per_block, int64_t skip_period) {
   constexpr int D = 128 * V4;
@@ -113,7 +121,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) ln_bwd_kernel(
     for (int i = 0; i < V4; ++i) {
       const int c = 4 * lane + 128 * i;
       xv[i] = *reinterpret_cast<const float4*>(xr + c);
-      dyv[i] = has_dy ? *reinterpret_cast<const float4*>(dy + irow * D + c) : make_float4(0, 0, 0, 0);
+      dyv[i] = has_dy ? load4(dy + irow * D + c) : make_float4(0, 0, 0, 0);
       pv[i] = accumulate ? *reinterpret_cast<const float4*>(dres + r * D + c) : make_float4(0, 0, 0, 0);
     }
     float s1 = 0.f, s2 = 0.f;
@@ -424,10 +432,11 @@ extern "C" int jz_row_partials(int64_t rows) {
   return (int)p;
 }
 
-extern "C" int jz_layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* gamma,
-                                const float* dy, float* dres, int accumulate, void* dres_bf16,
-                                float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
-                                int64_t rows, int D, int64_t skip_period, jz_stream_t s) {
+template <typename DyT>
+static int layernorm_bwd_impl(const float* x, const float* mean, const float* rstd, const float* gamma,
+                              const DyT* dy, float* dres, int accumulate, void* dres_bf16,
+                              float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
+                              int64_t rows, int D, int64_t skip_period, jz_stream_t s) {
   JZ_CHECK_ARG(D % 128 == 0 && D >= 128 && D <= 1024, "layernorm_bwd: D=%d unsupported", D);
   JZ_CHECK_ARG(nparts >= 1, "layernorm_bwd: nparts");
   if (rows == 0) return JZ_OK;
@@ -436,7 +445,7 @@ extern "C" int jz_layernorm_bwd(const float* x, const float* mean, const float* 
   auto st = reinterpret_cast<cudaStream_t>(s);
   auto yb = reinterpret_cast<__nv_bfloat16*>(dres_bf16);
 #define LNB(V)                                                                                         \
-  ln_bwd_kernel<V><<<grid, kRowThreads, 0, st>>>(x, mean, rstd, gamma, dy, dres, accumulate, yb,       \
+  ln_bwd_kernel<V, DyT><<<grid, kRowThreads, 0, st>>>(x, mean, rstd, gamma, dy, dres, accumulate, yb,  \
                                                  part_dgamma, part_dbeta, part_dbias, rows, rpb, skip_period)
   switch (D / 128) {
     case 1: LNB(1); break;
@@ -455,6 +464,22 @@ extern "C" int jz_layernorm_bwd(const float* x, const float* mean, const float* 
     if (part_dbias) JZ_CUDA_TRY(cudaMemsetAsync(part_dbias + (int64_t)grid * D, 0, bytes, st));
   }
   return JZ_OK;
+}
+
+extern "C" int jz_layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* gamma,
+                                const float* dy, float* dres, int accumulate, void* dres_bf16,
+                                float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
+                                int64_t rows, int D, int64_t skip_period, jz_stream_t s) {
+  return layernorm_bwd_impl(x, mean, rstd, gamma, dy, dres, accumulate, dres_bf16, part_dgamma, part_dbeta,
+                            part_dbias, nparts, rows, D, skip_period, s);
+}
+
+extern "C" int jz_layernorm_bwd_bf16dy(const float* x, const float* mean, const float* rstd, const float* gamma,
+                                       const void* dy, float* dres, int accumulate, void* dres_bf16,
+                                       float* part_dgamma, float* part_dbeta, float* part_dbias, int nparts,
+                                       int64_t rows, int D, int64_t skip_period, jz_stream_t s) {
+  return layernorm_bwd_impl(x, mean, rstd, gamma, reinterpret_cast<const __nv_bfloat16*>(dy), dres, accumulate,
+                            dres_bf16, part_dgamma, part_dbeta, part_dbias, nparts, rows, D, skip_period, s);
 }
 
 extern "C" int jz_colsum_bf16(const void* x, int64_t rows, int cols, int64_t ld, float* part, int nparts,

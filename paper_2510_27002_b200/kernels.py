@@ -222,7 +222,8 @@ def layernorm_bwd(x, mean, rstd, g, dy, dres, *, accumulate: bool, dres_bf16=Non
     pg = part[: npart * D] if dgamma is not None else None
     pb = part[npart * D: 2 * npart * D] if dbeta is not None else None
     pz = part[2 * npart * D:] if dbias is not None else None
-    L.call("jz_layernorm_bwd", x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), g.data_ptr(), dy.data_ptr(),
+    L.call("jz_layernorm_bwd_bf16dy" if dy.dtype == BF16 else "jz_layernorm_bwd", x.data_ptr(), mean.data_ptr(),
+           rstd.data_ptr(), g.data_ptr(), dy.data_ptr(),
            dres.data_ptr(), int(accumulate), _p(dres_bf16), _p(pg), _p(pb), _p(pz), npart, rows, D, skip_period,
            _s())
     if dgamma is not None:

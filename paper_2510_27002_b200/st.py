@@ -223,7 +223,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
                     dbias=G[f"{prefix}.block{nb - 1}.ffn.down.b"], skip_period=S if ctx["final_skip"] else 0)
     if on_done is not None:
         on_done("head_ln")
-    dtmp = torch.empty(rows, d, dtype=K.F32, device=dev)
+    # LN-backward inputs in bf16: the dX GEMMs write half the bytes and the HBM-bound LN pass reads half
+    dtmp = torch.empty(rows, d, dtype=K.BF16, device=dev)
     dh = torch.empty(rows, cfg.ffn_dim, dtype=K.BF16, device=dev)
     dao = torch.empty(rows, d, dtype=K.BF16, device=dev)
     for i in reversed(range(nb)):
@@ -235,7 +236,7 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_GELU_BWD, out=dh, aux=c["hpre"],
                     colsum=G[f"{base}.ffn.up.b"])  # up-bias gradient from the epilogue's column sums
         K.linear_dw(c["xn3"], dh, G[f"{base}.ffn.up.w"])
-        K.linear_dx(dh, w["ffn.wup"], epilogue=L.EPI_F32, out=dtmp)
+        K.linear_dx(dh, w["ffn.wup"], epilogue=L.EPI_BF16, out=dtmp)
         K.layernorm_bwd(c["x2"], c["m3"], c["r3"], P[f"{base}.ffn.ln.g"].data, dtmp, dres, accumulate=True,
                         dres_bf16=dres_b, dgamma=G[f"{base}.ffn.ln.g"], dbeta=G[f"{base}.ffn.ln.b"],
                         dbias=G[f"{base}.temporal.o.b"])
@@ -245,7 +246,7 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         gbt = gst.block_of(gst.grad_flat, f"{base}.temporal.q.b") if gst is not None else None
         dqkv = K.attn_temporal_bwd(c["qkv2"], c["ao2"], dao, c["lse_t"], B, T, S, H, colsum=gbt)
         _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d, gst, bias_done=gbt is not None)
-        K.linear_dx(dqkv, w["temporal.wqkv"], epilogue=L.EPI_F32, out=dtmp)
+        K.linear_dx(dqkv, w["temporal.wqkv"], epilogue=L.EPI_BF16, out=dtmp)
         K.layernorm_bwd(c["x1"], c["m2"], c["r2"], P[f"{base}.temporal.ln.g"].data, dtmp, dres, accumulate=True,
                         dres_bf16=dres_b, dgamma=G[f"{base}.temporal.ln.g"], dbeta=G[f"{base}.temporal.ln.b"],
                         dbias=G[f"{base}.spatial.o.b"])
@@ -256,7 +257,7 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         # path: a separate pass over dqkv measured faster)
         dqkv = K.attn_spatial_bwd(c["qkv"], c["ao32"], dao, c["lse_s"], frames, S, H, dqkv=dqkv)
         _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst)
-        K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_F32, out=dtmp)
+        K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_BF16, out=dtmp)
         prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
         K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
                         dres_bf16=dres_b if (i > 0 or want_dx_bf16) else None, dgamma=G[f"{base}.spatial.ln.g"],
