@@ -118,10 +118,28 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: 
 
 
 def splitk_for(m_out: int, n_out: int, k: int) -> int:
+    """Split-K for long-K GEMMs (dW): the smallest split whose work units fill the persistent grid's
+    waves to >= 85% (fewer splits = fewer fp32 partials and longer pipelined K runs; measured: one
+    86%-full wave beats two 97%-full ones).  Mirrors the kernel's tiling: CTA pairs with 256 x 256 tiles when N > 128 and
+    M > 128 (num_sms / 2 workers), otherwise single CTAs with 128-row tiles."""
     bn = 256 if n_out > 128 else (128 if n_out > 64 else 64)
-    tiles = -(-m_out // 128) * -(-n_out // bn)
+    pair = bn == 256 and m_out > 128
+    tm = 256 if pair else 128
+    workers = num_sms() // 2 if pair else num_sms()
+    tiles = -(-m_out // tm) * -(-n_out // bn)
     kb = -(-k // 64)
-    return max(1, min(kb, round(num_sms() / tiles)))
+    best, best_eff = 1, 0.0
+    for sp in range(1, min(kb, 64) + 1):
+        units = tiles * sp
+        waves = -(-units // workers)
+        eff = units / (waves * workers)
+        if kb // sp < 8:  # keep >= 8 k-blocks per unit (pipeline fill)
+            break
+        if eff >= 0.85:
+            return sp
+        if eff > best_eff + 1e-9:
+            best, best_eff = sp, eff
+    return best
 
 
 def linear_fwd(x_bf16: torch.Tensor, w_bf16: torch.Tensor, bias: torch.Tensor | None, *, epilogue=L.EPI_BF16,

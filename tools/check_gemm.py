@@ -97,5 +97,8 @@ bench(M, 512, 1536, akm=1, bkm=1, epi=L.EPI_F32)
 bench(M, 2048, 512, akm=1, bkm=1, epi=L.EPI_GELU_BWD)
 bench(512, 1536, M, akm=0, bkm=0, epi=L.EPI_F32, split=6)
 bench(2048, 512, M, akm=0, bkm=0, epi=L.EPI_F32, split=4)
+from paper_2510_27002_b200.kernels import splitk_for
+for (mm, nn) in ((512, 2048), (2048, 512), (512, 1536), (512, 512)):
+    bench(mm, nn, M, akm=0, bkm=0, epi=L.EPI_F32, split=splitk_for(mm, nn, M))
 print("ALL OK" if ok else "SOME FAILED")
 sys.exit(0 if ok else 1)
