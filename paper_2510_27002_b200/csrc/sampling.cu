@@ -75,6 +75,17 @@ JZ_DEV void loadv(const __nv_bfloat16* p, float (&f)[DPL]) {
   }
 }
 
+// raw bf16 pairs (converted at use: half the registers of an fp32 copy)
+template <int DPL>
+JZ_DEV void loadraw(const __nv_bfloat16* p, uint32_t (&w)[DPL / 2]) {
+#pragma unroll
+  for (int c = 0; c < DPL / 4; ++c) {
+    const uint2 a = reinterpret_cast<const uint2*>(p)[c];
+    w[2 * c] = a.x;
+    w[2 * c + 1] = a.y;
+  }
+}
+
 template <int DPL>
 JZ_DEV void storev(__nv_bfloat16* p, const float (&f)[DPL], float scale) {
 #pragma unroll
@@ -89,12 +100,17 @@ JZ_DEV void copyv(__nv_bfloat16* dst, const __nv_bfloat16* src) {
   for (int c = 0; c < DPL / 4; ++c) reinterpret_cast<uint2*>(dst)[c] = reinterpret_cast<const uint2*>(src)[c];
 }
 
-// DPL = head dims per lane: D = 32*DPL, a head (64 dims) spans 64/DPL lanes
+// DPL = head dims per lane: D = 32*DPL, a head (64 dims) spans 64/DPL lanes.
+// One warp per (b, s) over all heads; keys/values tau < t come from the cache, tau = t is the
+// current frame's own k/v.  Single pass with an online softmax over chunks of 4 time steps: each
+// chunk issues its 8 K/V row loads (clamped to a valid row, masked afterwards) before any use,
+// and every loop is fully unrolled (t <= 15) so scores and accumulators stay in registers.
 template <int DPL>
 __global__ void temporal_decode_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ cache,
                                        int64_t B, int t, const int* __restrict__ dev_t, int Tmax, int S, int append,
                                        __nv_bfloat16* __restrict__ out) {
   constexpr int D = 32 * DPL;
+  constexpr int HL = 64 / DPL;  // lanes per head
   if (dev_t) t = *dev_t;
   const int64_t bs = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -109,33 +125,55 @@ __global__ void temporal_decode_kernel(const __nv_bfloat16* __restrict__ qkv, __
   loadv<DPL>(row + 2 * D + d0, vc);
   const __nv_bfloat16* base = cache + ((b * Tmax) * S + s) * 2 * D + d0;
   const int64_t tstride = (int64_t)S * 2 * D;
-  float sc[17];
-  float mx = -INFINITY;
-#pragma unroll 4
-  for (int tau = 0; tau <= t; ++tau) {
-    float k[DPL];
-    if (tau < t) loadv<DPL>(base + tau * tstride, k);
-    float a = 0.f;
-#pragma unroll
-    for (int i = 0; i < DPL; ++i) a += q[i] * (tau < t ? k[i] : kc[i]);
-#pragma unroll
-    for (int o = 1; o < 64 / DPL; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    a *= 0.125f;
-    sc[tau] = a;
-    mx = fmaxf(mx, a);
-  }
-  float o[DPL];
+  float m = -INFINITY, l = 0.f, o[DPL];
 #pragma unroll
   for (int i = 0; i < DPL; ++i) o[i] = 0.f;
-  float l = 0.f;
-#pragma unroll 4
-  for (int tau = 0; tau <= t; ++tau) {
-    const float p = __expf(sc[tau] - mx);
-    l += p;
-    float v[DPL];
-    if (tau < t) loadv<DPL>(base + tau * tstride + D, v);
 #pragma unroll
-    for (int i = 0; i < DPL; ++i) o[i] += p * (tau < t ? v[i] : vc[i]);
+  for (int c0 = 0; c0 < 16; c0 += 4) {
+    if (c0 > t) break;  // warp-uniform
+    uint32_t kk[4][DPL / 2], vv[4][DPL / 2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int tau = c0 + j;
+      const int tt = tau < t ? tau : 0;  // row 0 always exists when t > 0; unused otherwise
+      if (t > 0) {
+        loadraw<DPL>(base + tt * tstride, kk[j]);
+        loadraw<DPL>(base + tt * tstride + D, vv[j]);
+      }
+    }
+    float sc[4];
+    float cm = m;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int tau = c0 + j;
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < DPL / 2; ++i) {
+        const float2 kf = unpack_bf16(kk[j][i]);
+        a += q[2 * i] * (tau < t ? kf.x : kc[2 * i]) + q[2 * i + 1] * (tau < t ? kf.y : kc[2 * i + 1]);
+      }
+#pragma unroll
+      for (int off = 1; off < HL; off <<= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      sc[j] = tau <= t ? a * 0.125f : -INFINITY;
+      cm = fmaxf(cm, sc[j]);
+    }
+    const float corr = __expf(m - cm);  // 0 on the first chunk (m = -inf)
+    l *= corr;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) o[i] *= corr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int tau = c0 + j;
+      const float p = __expf(sc[j] - cm);
+      l += p;
+#pragma unroll
+      for (int i = 0; i < DPL / 2; ++i) {
+        const float2 vf = unpack_bf16(vv[j][i]);
+        o[2 * i] += p * (tau < t ? vf.x : vc[2 * i]);
+        o[2 * i + 1] += p * (tau < t ? vf.y : vc[2 * i + 1]);
+      }
+    }
+    m = cm;
   }
   storev<DPL>(out + bs * D + d0, o, 1.0f / l);
   if (append) {
@@ -298,15 +336,15 @@ extern "C" int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, 
   const int64_t warps = B * S;
   if (warps == 0) return JZ_OK;
   auto st = reinterpret_cast<cudaStream_t>(s);
-  const unsigned grid = (unsigned)((warps + 7) / 8);
+  const unsigned grid = (unsigned)((warps + 3) / 4);
   auto q = reinterpret_cast<const __nv_bfloat16*>(qkv);
   auto c = reinterpret_cast<__nv_bfloat16*>(cache);
   auto o = reinterpret_cast<__nv_bfloat16*>(out);
   switch (D) {
-    case 128: temporal_decode_kernel<4><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
-    case 256: temporal_decode_kernel<8><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
-    case 512: temporal_decode_kernel<16><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
-    default: temporal_decode_kernel<32><<<grid, 256, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 128: temporal_decode_kernel<4><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 256: temporal_decode_kernel<8><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 512: temporal_decode_kernel<16><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    default: temporal_decode_kernel<32><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
   }
   JZ_LAUNCH_CHECK();
   return JZ_OK;
