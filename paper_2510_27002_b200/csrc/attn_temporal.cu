@@ -174,6 +174,39 @@ JZ_DEV void av_store(const uint32_t (&a)[4], const __nv_bfloat16* bsm, int ld, _
   }
 }
 
+// out[16][64] = A . B (as av_store) kept in registers: o[np][0..3] = n-tile 2np, o[np][4..7] = 2np + 1
+JZ_DEV void av_frag(const uint32_t (&a)[4], const __nv_bfloat16* bsm, int ld, float (&o)[HD / 16][8]) {
+#pragma unroll
+  for (int np = 0; np < HD / 16; ++np) {
+    uint32_t bb[4];
+    load_b_kn(bb, bsm, ld, 16 * np);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[np][e] = 0.f;
+    float o0[4] = {0, 0, 0, 0}, o1[4] = {0, 0, 0, 0};
+    mma16816(o0, a, bb[0], bb[1]);
+    mma16816(o1, a, bb[2], bb[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      o[np][e] = o0[e];
+      o[np][4 + e] = o1[e];
+    }
+  }
+}
+
+// fragment -> bf16 smem tile [16][ld] at columns col0..col0+63 (rows r0: * mul0, r0 + 8: * mul1)
+JZ_DEV void frag_to_smem(const float (&o)[HD / 16][8], __nv_bfloat16* dst, int ld, int col0, float mul0, float mul1) {
+  const int L = lane_id();
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+#pragma unroll
+  for (int np = 0; np < HD / 16; ++np) {
+    const int c = col0 + 16 * np + cq;
+    *reinterpret_cast<uint32_t*>(dst + r0 * ld + c) = pack_bf16(o[np][0] * mul0, o[np][1] * mul0);
+    *reinterpret_cast<uint32_t*>(dst + r0 * ld + c + 8) = pack_bf16(o[np][4] * mul0, o[np][5] * mul0);
+    *reinterpret_cast<uint32_t*>(dst + (r0 + 8) * ld + c) = pack_bf16(o[np][2] * mul1, o[np][3] * mul1);
+    *reinterpret_cast<uint32_t*>(dst + (r0 + 8) * ld + c + 8) = pack_bf16(o[np][6] * mul1, o[np][7] * mul1);
+  }
+}
+
 }  // namespace tp
 
 using namespace tp;
@@ -191,7 +224,6 @@ __global__ void __launch_bounds__(512) temporal_fwd_kernel(const __nv_bfloat16* 
   cp_async_wait_all();
   __syncthreads();
   const int h = warp_id(), L = lane_id();
-  if (h >= H) return;
   float sc[2][4];
   xyT(sc, sq + h * HD, ld, sq + D + h * HD, ld);
   const int r0 = L >> 2, cq = 2 * (L & 3);
@@ -220,11 +252,20 @@ __global__ void __launch_bounds__(512) temporal_fwd_kernel(const __nv_bfloat16* 
   l1 = quad_sum(l1);
   uint32_t pa[4];
   c_to_a(pa, sc);
-  av_store(pa, sq + 2 * D + h * HD, ld, out, D, h * HD, b, T, S, s, 1.0f / l0, 1.0f / l1);
+  float o[HD / 16][8];
+  av_frag(pa, sq + 2 * D + h * HD, ld, o);
+  __syncwarp();  // this head's q columns are consumed: O overwrites them in place
+  frag_to_smem(o, sq, ld, h * HD, 1.0f / l0, 1.0f / l1);
   if ((L & 3) == 0) {
     float* lp = lse + (bs * H + h) * T;
     if (r0 < T) lp[r0] = m0 + logf(l0);
     if (r0 + 8 < T) lp[r0 + 8] = m1 + logf(l1);
+  }
+  __syncthreads();
+  const int c16 = D / 8;  // coalesced write-out of the T token rows
+  for (int i = threadIdx.x; i < T * c16; i += blockDim.x) {
+    const int t = i / c16, c = i - t * c16;
+    *reinterpret_cast<uint4*>(out + ((b * T + t) * S + s) * D + 8 * c) = *reinterpret_cast<const uint4*>(sq + t * ld + 8 * c);
   }
 }
 
@@ -249,7 +290,6 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
   cp_async_wait_all();
   __syncthreads();
   const int h = warp_id(), L = lane_id();
-  if (h >= H) return;
   __nv_bfloat16* sP = sp_all + h * 2 * 16 * LDP;
   __nv_bfloat16* sdS = sP + 16 * LDP;
   const __nv_bfloat16* q = sq + h * HD;
@@ -290,15 +330,37 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
   __syncwarp();
   // dQ = scale * dS K      (A = dS from registers, B = K stored [j][d])
   uint32_t a[4];
-  float* part = colsum ? colsum + bs * (3 * D) : nullptr;  // one partial row per (b, s)
+  float oq[HD / 16][8], ok[HD / 16][8], ov[HD / 16][8];
   c_to_a(a, dS);
-  av_store(a, k, ldq, dqkv, 3 * D, h * HD, b, T, S, s, scale, scale, part);
-  // dK = scale * dS^T Q    (A = dS^T from smem, B = Q stored [t][d])
+  av_frag(a, k, ldq, oq);          // dQ = scale * dS K
   load_a_trans(a, sdS, LDP);
-  av_store(a, q, ldq, dqkv, 3 * D, D + h * HD, b, T, S, s, scale, scale, part);
-  // dV = P^T dO
+  av_frag(a, q, ldq, ok);          // dK = scale * dS^T Q
   load_a_trans(a, sP, LDP);
-  av_store(a, dog, ldo, dqkv, 3 * D, 2 * D + h * HD, b, T, S, s, 1.0f, 1.0f, part);
+  av_frag(a, dog, ldo, ov);        // dV = P^T dO
+  __syncwarp();  // this warp's q/k/v columns are consumed: its gradients overwrite them in place
+  frag_to_smem(oq, sq, ldq, h * HD, scale, scale);
+  frag_to_smem(ok, sq, ldq, D + h * HD, scale, scale);
+  frag_to_smem(ov, sq, ldq, 2 * D + h * HD, 1.0f, 1.0f);
+  __syncthreads();
+  // coalesced write-out of the T token rows (3 KB contiguous each)
+  const int c16 = 3 * D / 8;
+  for (int i = threadIdx.x; i < T * c16; i += blockDim.x) {
+    const int t = i / c16, c = i - t * c16;
+    *reinterpret_cast<uint4*>(dqkv + ((b * T + t) * S + s) * (3 * D) + 8 * c) =
+        *reinterpret_cast<const uint4*>(sq + t * ldq + 8 * c);
+  }
+  if (colsum) {  // QKV bias-gradient partial row of this (b, s): column sums over its T rows
+    float* part = colsum + bs * (3 * D);
+    for (int c2 = threadIdx.x; c2 < 3 * D / 2; c2 += blockDim.x) {
+      float s0 = 0.f, s1 = 0.f;
+      for (int t = 0; t < T; ++t) {
+        const float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(sq + t * ldq + 2 * c2));
+        s0 += f.x;
+        s1 += f.y;
+      }
+      *reinterpret_cast<float2*>(part + 2 * c2) = make_float2(s0, s1);
+    }
+  }
 }
 
 static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B,
