@@ -811,6 +811,9 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
       const int64_t row0 = (int64_t)f * S;
       const int pb = i & 1;
       mbar_wait(&sm.prep_ready[pb], (i >> 1) & 1);
+      // next unit's vectors first: only global loads, and buffer pb ^ 1 was last read in unit i - 1,
+      // which every warp has finished (this warp's own unit i - 1 dQ epilogue came after its MMAs)
+      if (u + (int)gridDim.x < units) prepare(u + gridDim.x, pb ^ 1);
       mbar_wait(&sm.load_full, i & 1);
       if (ht == 0) PROF_MARK(43);
       const int64_t qrow0 = row0 + quarter * 32;  // first of this warp's 32 rows in a 128-row tile
@@ -897,8 +900,6 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
           pr[2 * D] = 0.f;
         }
       }
-      // ---- next unit's vectors (the P/dS warps of this unit are past j = 0 already) ----
-      if (u + (int)gridDim.x < units) prepare(u + gridDim.x, pb ^ 1);
       if (ht == 0) PROF_MARK(48);
       // ---- (f) dV_1 / dK_1 ----
       mbar_wait(&sm.dkdv_full, (2 * i + 1) & 1);
