@@ -649,8 +649,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
       if (warp == 2 && lane == 0) GPROF(5);
       __syncwarp();
       if (lane == 0) {
-        if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
-        else mbar_arrive(&tempty_bar[acc]);
+        if constexpr (PAIR) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+        else mbar_arrive_relaxed(&tempty_bar[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }

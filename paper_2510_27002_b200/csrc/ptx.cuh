@@ -179,6 +179,17 @@ JZ_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Relaxed arrivals for "TMEM drained" barriers: the arriving thread's tcgen05.ld already completed
+// (tcgen05.wait::ld) and no generic memory has to be published, so no release fence is needed.
+// (A release arrive waits on every outstanding memory op of the thread: the epilogue's lane 0 also
+// issued the tile's bulk stores, and that wait was a quarter of the GEMM's stall samples.)
+JZ_DEV void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+JZ_DEV void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 JZ_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
