@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       lse[((int64_t)f * H + h) * S + 128 * t + r] = mx * 0.125f + logf(sum);
       tc_fence_before();
-      mbar_arrive(&sm.tmem_free[t]);
+      mbar_arrive_relaxed(&sm.tmem_free[t]);  // only TMEM reads precede (tcgen05.wait::ld done)
     }
   } else if (has_tail) {
     // tail warps: query row 256 on CUDA cores, reading K/V from the staged smem tiles
@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
         stage_acc(C_DK, cd, sm.q256[pb], scale);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.dkdv_free);
+        if (lane == 0) mbar_arrive_relaxed(&sm.dkdv_free);
         flush_rows(qrow0, D + h * 64);
       }
       if (ht == 0) PROF_MARK(47);
@@ -913,7 +913,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
         stage_acc(C_DK, cd, sm.q256[pb], scale);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.dkdv_free);
+        if (lane == 0) mbar_arrive_relaxed(&sm.dkdv_free);
         flush_rows(qrow0 + 128, D + h * 64);
       }
       if (ht == 0) PROF_MARK(50);
@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
         stage_acc(C_DQ + 64, has_tail ? sm.ds_col[pb][128 + r] : 0.f, sm.k256[pb], scale);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.dq_free);
+        if (lane == 0) mbar_arrive_relaxed(&sm.dq_free);
         flush_rows(qrow0 + 128, h * 64);
       }
       if (ht == 0) PROF_MARK(52);
