@@ -252,11 +252,17 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
                         dbias=G[f"{base}.spatial.o.b"])
         # ---- spatial: x1 = x + attn_s(LN(x)) Wo + bo
         K.linear_dw(c["ao"], dres_b, G[f"{base}.spatial.o.w"])
-        K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao)
-        # (the spatial kernel can emit the bias column sums too, but its helper warps are its critical
-        # path: a separate pass over dqkv measured faster)
+        gbs = gst.block_of(gst.grad_flat, f"{base}.spatial.q.b") if gst is not None else None
+        # Softmax rows sum to 1 (the key-256 column included), so the QKV bias gradient needs no pass
+        # over all of dqkv: d b_v = sum_k dV_k = sum_q dO_q (column sums of dO from this GEMM's
+        # epilogue), d b_k = sum_k dK_k = 0 exactly (shift invariance), only d b_q reads dq.
+        K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao,
+                    colsum=gbs[2 * d:] if gbs is not None else None)
         dqkv = K.attn_spatial_bwd(c["qkv"], c["ao32"], dao, c["lse_s"], frames, S, H, dqkv=dqkv)
-        _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst)
+        if gbs is not None:
+            gbs[d:2 * d].zero_()
+            K.colsum_bf16(dqkv, gbs[:d], cols=d)
+        _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst, bias_done=gbs is not None)
         K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_BF16, out=dtmp)
         prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
         K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
