@@ -105,41 +105,63 @@ __global__ void dyn_embed_fwd_kernel(const int64_t* __restrict__ tokens, const u
 //   part_pt[s][t]   = sum_b dx[b,t,s]                 (-> dpt[t] = sum_s part_pt[s][t])
 //   part_mt[s]      = sum_{b,t: mask[b,t,n(s)]} dx[b,t,s]   (-> dmask_token)
 // ---------------------------------------------------------------------------
-__global__ void dyn_embed_bwd_pos_kernel(const float* __restrict__ dx, const uint8_t* __restrict__ mask,
-                                         int64_t B, int T, int N, int D, int prepend, float* __restrict__ dps,
-                                         float* __restrict__ part_pt, float* __restrict__ part_mt) {
+// One CTA per spatial slot s: 4 thread groups split the T frames (each group 128 threads x 4 dims
+// over D = 512), 8 row loads in flight per thread; the groups' spatial / mask-token sums are then
+// combined in group order through shared memory (deterministic).
+constexpr int kPosGroups = 4;
+__global__ void __launch_bounds__(128 * kPosGroups) dyn_embed_bwd_pos_kernel(
+    const float* __restrict__ dx, const uint8_t* __restrict__ mask, int64_t B, int T, int N, int D, int prepend,
+    float* __restrict__ dps, float* __restrict__ part_pt, float* __restrict__ part_mt) {
+  __shared__ float4 red_s[kPosGroups - 1][128], red_m[kPosGroups - 1][128];
   const int S = N + (prepend ? 1 : 0);
   const int s = blockIdx.x;
   const int n = prepend ? s - 1 : s;
-  for (int d = threadIdx.x * 4; d < D; d += blockDim.x * 4) {
+  const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;
+  for (int d0 = 0; d0 < D; d0 += 512) {
+    const int d = d0 + 4 * tid;
+    const bool live = d < D;
     float4 acc_s = make_float4(0, 0, 0, 0), acc_m = make_float4(0, 0, 0, 0);
-    for (int t = 0; t < T; ++t) {
+    for (int t = grp; t < T; t += kPosGroups) {
       float4 acc_t = make_float4(0, 0, 0, 0);
-      for (int64_t b0 = 0; b0 < B; b0 += 4) {
-        float4 g[4];
-        bool mk[4];
+      for (int64_t b0 = 0; b0 < B; b0 += 8) {
+        float4 g[8];
+        bool mk[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
           const int64_t b = b0 + q;
           g[q] = make_float4(0, 0, 0, 0);
           mk[q] = false;
-          if (b < B) {
+          if (live && b < B) {
             const int64_t row = (b * T + t) * S + s;
-            g[q] = *reinterpret_cast<const float4*>(dx + row * D + d);
+            g[q] = __ldg(reinterpret_cast<const float4*>(dx + row * D + d));
             mk[q] = n >= 0 && mask && mask[(b * T + t) * N + n];
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
           acc_t.x += g[q].x; acc_t.y += g[q].y; acc_t.z += g[q].z; acc_t.w += g[q].w;
           if (mk[q]) { acc_m.x += g[q].x; acc_m.y += g[q].y; acc_m.z += g[q].z; acc_m.w += g[q].w; }
         }
       }
-      *reinterpret_cast<float4*>(part_pt + ((int64_t)s * T + t) * D + d) = acc_t;
+      if (live) *reinterpret_cast<float4*>(part_pt + ((int64_t)s * T + t) * D + d) = acc_t;
       acc_s.x += acc_t.x; acc_s.y += acc_t.y; acc_s.z += acc_t.z; acc_s.w += acc_t.w;
     }
-    *reinterpret_cast<float4*>(dps + (int64_t)s * D + d) = acc_s;
-    *reinterpret_cast<float4*>(part_mt + (int64_t)s * D + d) = acc_m;
+    if (grp > 0) {
+      red_s[grp - 1][tid] = acc_s;
+      red_m[grp - 1][tid] = acc_m;
+    }
+    __syncthreads();
+    if (grp == 0 && live) {
+#pragma unroll
+      for (int g2 = 0; g2 < kPosGroups - 1; ++g2) {
+        const float4 a = red_s[g2][tid], m = red_m[g2][tid];
+        acc_s.x += a.x; acc_s.y += a.y; acc_s.z += a.z; acc_s.w += a.w;
+        acc_m.x += m.x; acc_m.y += m.y; acc_m.z += m.z; acc_m.w += m.w;
+      }
+      *reinterpret_cast<float4*>(dps + (int64_t)s * D + d) = acc_s;
+      *reinterpret_cast<float4*>(part_mt + (int64_t)s * D + d) = acc_m;
+    }
+    __syncthreads();
   }
 }
 
@@ -344,7 +366,8 @@ extern "C" int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const ui
   float* dact_buf = part_mt + (int64_t)S * D;
   float* dcond = dact_buf + (prepend ? 0 : B * T * D);
   // positions + mask token
-  dyn_embed_bwd_pos_kernel<<<S, 128, 0, st>>>(dx, mask, B, T, N, D, prepend, d_pos_spatial, part_pt, part_mt);
+  dyn_embed_bwd_pos_kernel<<<S, 128 * kPosGroups, 0, st>>>(dx, mask, B, T, N, D, prepend, d_pos_spatial, part_pt,
+                                                           part_mt);
   JZ_LAUNCH_CHECK();
   int rc = jz_reduce_partials(part_pt, S, (int64_t)T * D, d_pos_temporal, 0, s);
   if (rc) return rc;
