@@ -183,7 +183,8 @@ JZ_API int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, const fl
                             const float* action_w, const float* action_b, const float* pos_spatial,
                             const float* pos_temporal, int64_t B, int T, int N, int D, int dl, int K,
                             int prepend, float* x, int* err, jz_stream_t stream);
-JZ_API int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend);
+/* Workspace (floats) for jz_dyn_embed_bwd; K = vocabulary (token-table sort buffers). */
+JZ_API int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend, int K);
 /* Deterministic backward of jz_dyn_embed_fwd (no float atomics).  d_latents may be NULL. */
 JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_t* mask,
                             const float* latents, const float* null_action, const float* action_w,

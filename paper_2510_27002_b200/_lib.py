@@ -44,7 +44,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_philox_mask": [_P, _P, _P, _I32, _I64, _I64, _I64, _I32, _I32, _F64, _P, _P, _P],
     "jz_dyn_embed_fwd": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32,
                          _I32, _P, _P, _P],
-    "jz_dyn_embed_bwd_workspace": [_I64, _I32, _I32, _I32, _I32, _I32],
+    "jz_dyn_embed_bwd_workspace": [_I64, _I32, _I32, _I32, _I32, _I32, _I32],
     "jz_dyn_embed_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32,
                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "jz_attn_spatial_fwd": [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],

@@ -165,71 +165,149 @@ __global__ void __launch_bounds__(128 * kPosGroups) dyn_embed_bwd_pos_kernel(
   }
 }
 
-// ---------------------------------------------------------------------------
-// K5 backward, token table (deterministic scatter-add, "owner computes"):
-// CTA c owns token ids k = c, c+G, c+2G, ... (at most kOwn).  Warp w scans the fixed
-// position range [w*P/8, (w+1)*P/8) in order and accumulates unmasked rows into its
-// own registers; warps are then summed in warp order.
-// ---------------------------------------------------------------------------
-constexpr int kOwn = 8;
 
-template <int V4>  // D = 128 * V4
-__global__ void __launch_bounds__(256) dyn_embed_bwd_tok_kernel(const float* __restrict__ dx,
-                                                                const int64_t* __restrict__ tokens,
-                                                                const uint8_t* __restrict__ mask, int64_t P,
-                                                                int N, int S, int prepend, int K,
-                                                                float* __restrict__ dE) {
-  constexpr int D = 128 * V4;
-  const int G = gridDim.x;
-  const int c = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n_own = (K - c + G - 1) / G;  // ids c + j*G < K
-  float4 acc[kOwn][V4];
+// Token-table backward as a deterministic stable counting sort of positions by token id, then one
+// warp per token summing its dx rows in position order:
+//   tok_hist:    per position block, counts of unmasked tokens (integer: order-independent)
+//   tok_scan:    per-token starts + per-(block, token) offsets, in fixed order
+//   tok_scatter: stable placement (one warp per block, 32 positions at a time, __match_any_sync rank)
+//   tok_accum:   warp k sums the rows of token k (4 rows in flight), writes dE[k]
+constexpr int kTokChunk = 512;  // positions per histogram / scatter block
+
+__global__ void __launch_bounds__(256) tok_hist_kernel(const int64_t* __restrict__ tokens,
+                                                       const uint8_t* __restrict__ mask, int64_t P, int K,
+                                                       int* __restrict__ hist) {
+  extern __shared__ int sh[];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
+  __syncthreads();
+  const int64_t p0 = (int64_t)blockIdx.x * kTokChunk, p1 = min(P, p0 + kTokChunk);
+  for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    if (mask && mask[p]) continue;
+    const int64_t t = tokens[p];
+    if (t >= 0 && t < K) atomicAdd(&sh[t], 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) hist[(int64_t)blockIdx.x * K + k] = sh[k];
+}
+
+// per token k (one thread each): hist[b][k] <- sum_{b' < b} hist[b'][k]; total[k] = sum_b hist[b][k]
+__global__ void __launch_bounds__(256) tok_colscan_kernel(int* __restrict__ hist, int nb, int K, int* __restrict__ total) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  int r = 0;
+  int b0 = 0;
+  for (; b0 + 8 <= nb; b0 += 8) {  // 8 independent loads in flight, prefix in registers
+    int c[8];
 #pragma unroll
-  for (int j = 0; j < kOwn; ++j)
+    for (int q = 0; q < 8; ++q) c[q] = hist[(int64_t)(b0 + q) * K + k];
 #pragma unroll
-    for (int i = 0; i < V4; ++i) acc[j][i] = make_float4(0, 0, 0, 0);
-  const int64_t per = (P + 7) / 8;
-  const int64_t p0 = warp * per, p1 = min(P, p0 + per);
+    for (int q = 0; q < 8; ++q) {
+      hist[(int64_t)(b0 + q) * K + k] = r;
+      r += c[q];
+    }
+  }
+  for (; b0 < nb; ++b0) {
+    const int c = hist[(int64_t)b0 * K + k];
+    hist[(int64_t)b0 * K + k] = r;
+    r += c;
+  }
+  total[k] = r;
+}
+
+// one block of 1024 threads: tok_start[k] = sum_{k' < k} total[k'] (K <= 8192), tok_start[K] = total
+__global__ void __launch_bounds__(1024) tok_scan_kernel(const int* __restrict__ total, int K, int* __restrict__ tok_start) {
+  __shared__ int wsum[32];
+  constexpr int kPer = 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int v[kPer];
+  int run = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int k = tid * kPer + q;
+    v[q] = k < K ? total[k] : 0;
+    run += v[q];
+  }
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int start = incl - run;
+  for (int w = 0; w < warp; ++w) start += wsum[w];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int k = tid * kPer + q;
+    if (k < K) tok_start[k] = start;
+    start += v[q];
+  }
+  if (tid == 1023) tok_start[K] = start;
+}
+
+__global__ void __launch_bounds__(32) tok_scatter_kernel(const int64_t* __restrict__ tokens,
+                                                         const uint8_t* __restrict__ mask, int64_t P, int K,
+                                                         const int* __restrict__ offsets,
+                                                         const int* __restrict__ tok_start,
+                                                         int32_t* __restrict__ sorted) {
+  extern __shared__ int cur[];
+  const int lane = threadIdx.x;
+  for (int k = lane; k < K; k += 32) cur[k] = tok_start[k] + offsets[(int64_t)blockIdx.x * K + k];
+  __syncwarp();
+  const int64_t p0 = (int64_t)blockIdx.x * kTokChunk, p1 = min(P, p0 + kTokChunk);
+  const unsigned lt = (1u << lane) - 1u;
   for (int64_t base = p0; base < p1; base += 32) {
     const int64_t p = base + lane;
-    int64_t tok = -1;
-    if (p < p1 && !(mask && mask[p])) tok = tokens[p];
-    const bool mine = tok >= 0 && tok < K && (tok % G) == c;
-    unsigned bal = __ballot_sync(0xffffffffu, mine);
-    while (bal) {
-      const int src = __ffs(bal) - 1;
-      bal &= bal - 1;
-      const int64_t tk = __shfl_sync(0xffffffffu, tok, src);
-      const int64_t pp = base + src;
-      const int j = (int)(tk / G);
-      const int64_t row = prepend ? (pp / N) * S + (pp % N) + 1 : pp;
-      const float* g = dx + row * D;
+    int t = -1;
+    if (p < p1 && !(mask && mask[p])) {
+      const int64_t tt = tokens[p];
+      if (tt >= 0 && tt < K) t = (int)tt;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, t);
+    const int rank = __popc(peers & lt);
+    if (t >= 0) sorted[cur[t] + rank] = (int32_t)p;
+    __syncwarp();
+    if (t >= 0 && rank == 0) cur[t] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+template <int V4>  // D = 128 * V4; one warp per token
+__global__ void __launch_bounds__(256) tok_accum_kernel(const float* __restrict__ dx, const int32_t* __restrict__ sorted,
+                                                        const int* __restrict__ tok_start, int K, int N, int S,
+                                                        int prepend, float* __restrict__ dE) {
+  constexpr int D = 128 * V4;
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (k >= K) return;
+  const int e0 = tok_start[k], e1 = tok_start[k + 1];
+  float4 acc[V4];
 #pragma unroll
-      for (int jj = 0; jj < kOwn; ++jj) {
-        if (jj == j) {
+  for (int i = 0; i < V4; ++i) acc[i] = make_float4(0, 0, 0, 0);
+  for (int e = e0; e < e1; e += 4) {
+    float4 v[4][V4];
 #pragma unroll
-          for (int i = 0; i < V4; ++i) {
-            float4 v = *reinterpret_cast<const float4*>(g + 4 * lane + 128 * i);
-            acc[jj][i].x += v.x; acc[jj][i].y += v.y; acc[jj][i].z += v.z; acc[jj][i].w += v.w;
-          }
-        }
+    for (int q = 0; q < 4; ++q) {
+      if (e + q < e1) {
+        const int pp = sorted[e + q];
+        const int64_t row = prepend ? ((int64_t)pp / N) * S + (pp % N) + 1 : pp;
+        const float* g = dx + row * D;
+#pragma unroll
+        for (int i = 0; i < V4; ++i) v[q][i] = __ldg(reinterpret_cast<const float4*>(g + 4 * lane + 128 * i));
       }
     }
-  }
-  __shared__ float sm[8][D];
-  for (int j = 0; j < n_own && j < kOwn; ++j) {
 #pragma unroll
-    for (int i = 0; i < V4; ++i) *reinterpret_cast<float4*>(&sm[warp][4 * lane + 128 * i]) = acc[j][i];
-    __syncthreads();
-    for (int d = threadIdx.x; d < D; d += 256) {
-      float s = 0.f;
+    for (int q = 0; q < 4; ++q)
+      if (e + q < e1) {
 #pragma unroll
-      for (int w = 0; w < 8; ++w) s += sm[w][d];
-      dE[(int64_t)(c + j * G) * D + d] = s;
-    }
-    __syncthreads();
+        for (int i = 0; i < V4; ++i) {
+          acc[i].x += v[q][i].x; acc[i].y += v[q][i].y; acc[i].z += v[q][i].z; acc[i].w += v[q][i].w;
+        }
+      }
   }
+#pragma unroll
+  for (int i = 0; i < V4; ++i) *reinterpret_cast<float4*>(dE + (int64_t)k * D + 4 * lane + 128 * i) = acc[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -346,9 +424,12 @@ extern "C" int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, cons
 }
 
 // Workspace floats needed by jz_dyn_embed_bwd.
-extern "C" int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend) {
+extern "C" int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend, int K) {
   const int S = N + (prepend ? 1 : 0);
-  return (int64_t)S * T * D + (int64_t)S * D + (prepend ? 0 : B * T * D) + B * T * dl + 64ll * (dl + 1) * D;
+  const int64_t P = B * T * N;
+  const int64_t nb = (P + kTokChunk - 1) / kTokChunk;
+  return (int64_t)S * T * D + (int64_t)S * D + (prepend ? 0 : B * T * D) + B * T * dl + 64ll * (dl + 1) * D +
+         nb * K + 2 * K + 1 + P;  // token sort: histograms/offsets, starts, totals, sorted positions (int32)
 }
 
 extern "C" int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_t* mask,
@@ -373,20 +454,38 @@ extern "C" int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const ui
   if (rc) return rc;
   rc = jz_reduce_partials(part_mt, S, D, d_mask_token, 0, s);
   if (rc) return rc;
-  // token table
-  const int G = (K + kOwn - 1) / kOwn < num_sms() ? num_sms() : (K + kOwn - 1) / kOwn;
-  JZ_CHECK_ARG((K + G - 1) / G <= kOwn, "embed_bwd: vocabulary %d too large", K);
-  const int64_t P = B * T * N;
-  switch (D / 128) {
-    case 1: dyn_embed_bwd_tok_kernel<1><<<G, 256, 0, st>>>(dx, tokens, mask, P, N, S, prepend, K, d_token_embed); break;
-    case 2: dyn_embed_bwd_tok_kernel<2><<<G, 256, 0, st>>>(dx, tokens, mask, P, N, S, prepend, K, d_token_embed); break;
-    case 4: dyn_embed_bwd_tok_kernel<4><<<G, 256, 0, st>>>(dx, tokens, mask, P, N, S, prepend, K, d_token_embed); break;
-    case 8: dyn_embed_bwd_tok_kernel<8><<<G, 256, 0, st>>>(dx, tokens, mask, P, N, S, prepend, K, d_token_embed); break;
-    default: set_error("embed_bwd: D=%d unsupported", D); return JZ_EINVAL;
-  }
-  JZ_LAUNCH_CHECK();
-  if (G < K) {
-    // ids >= G*? all covered: ids c + j*G for j < n_own cover [0, K)
+  // token table: stable counting sort of positions by token, then one warp per token
+  {
+    JZ_CHECK_ARG(K >= 1 && K <= 8192, "embed_bwd: vocabulary %d unsupported (<= 8192)", K);
+    const int64_t P = B * T * N;
+    const int nb = (int)((P + kTokChunk - 1) / kTokChunk);
+    int* hist = reinterpret_cast<int*>(dcond + B * T * dl + 64ll * (dl + 1) * D);
+    int* tok_start = hist + (int64_t)nb * K;
+    int* total = tok_start + K + 1;
+    int32_t* sorted = total + K;
+    if (P > 0) {
+      tok_hist_kernel<<<nb, 256, K * sizeof(int), st>>>(tokens, mask, P, K, hist);
+      JZ_LAUNCH_CHECK();
+      tok_colscan_kernel<<<(K + 63) / 64, 64, 0, st>>>(hist, nb, K, total);
+      JZ_LAUNCH_CHECK();
+    } else {
+      JZ_CUDA_TRY(cudaMemsetAsync(total, 0, K * sizeof(int), st));
+    }
+    tok_scan_kernel<<<1, 1024, 0, st>>>(total, K, tok_start);
+    JZ_LAUNCH_CHECK();
+    if (P > 0) {
+      tok_scatter_kernel<<<nb, 32, K * sizeof(int), st>>>(tokens, mask, P, K, hist, tok_start, sorted);
+      JZ_LAUNCH_CHECK();
+    }
+    const unsigned gk = (unsigned)((K + 7) / 8);
+    switch (D / 128) {
+      case 1: tok_accum_kernel<1><<<gk, 256, 0, st>>>(dx, sorted, tok_start, K, N, S, prepend, d_token_embed); break;
+      case 2: tok_accum_kernel<2><<<gk, 256, 0, st>>>(dx, sorted, tok_start, K, N, S, prepend, d_token_embed); break;
+      case 4: tok_accum_kernel<4><<<gk, 256, 0, st>>>(dx, sorted, tok_start, K, N, S, prepend, d_token_embed); break;
+      case 8: tok_accum_kernel<8><<<gk, 256, 0, st>>>(dx, sorted, tok_start, K, N, S, prepend, d_token_embed); break;
+      default: set_error("embed_bwd: D=%d unsupported", D); return JZ_EINVAL;
+    }
+    JZ_LAUNCH_CHECK();
   }
   // action conditioning
   const float* dact = dx;

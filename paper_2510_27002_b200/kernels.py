@@ -329,7 +329,7 @@ def dyn_embed_fwd(tokens, mask, latents, P: dict, *, B, T, N, D, dl, K, prepend,
 
 
 def dyn_embed_bwd(dx, tokens, mask, latents, P: dict, G: dict, *, B, T, N, D, dl, K, prepend, d_latents=None):
-    nws = L.load().jz_dyn_embed_bwd_workspace(B, T, N, D, dl, int(prepend))
+    nws = L.load().jz_dyn_embed_bwd_workspace(B, T, N, D, dl, int(prepend), K)
     ws = scratch("embed_ws", nws)
     L.call("jz_dyn_embed_bwd", dx.data_ptr(), tokens.data_ptr(), _p(mask), _p(latents),
            P["null_action"].data_ptr(), P["action_proj.w"].data_ptr(), B, T, N, D, dl, K, int(prepend),
