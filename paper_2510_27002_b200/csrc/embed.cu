@@ -33,70 +33,90 @@ __global__ void philox_mask_kernel(PhiloxState st, int64_t B_global, int64_t b0,
 }
 
 // ---------------------------------------------------------------------------
-// K5 forward.  One CTA (D/4 threads) per output row (b, t, s).
+// K5 forward.  One warp per output row (b, t, s).
 //   prepend : s = 0 -> act(b,t) + ps[0] + pt[t];  s >= 1 -> sel(b,t,s-1) + ps[s] + pt[t]
 //   additive: s = n -> (sel(b,t,n) + act(b,t)) + ps[n] + pt[t]
 //   sel = mask ? mask_token : E[token];  act = cond @ Wa + ba, cond = t ? lat[b,t-1] : null
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float4 act_proj4(const float* cond, int dl, const float* __restrict__ Wa,
-                                            const float* __restrict__ ba, int D, int d) {
-  float4 acc = make_float4(0, 0, 0, 0);
-  for (int i = 0; i < dl; ++i) {
-    const float c = cond[i];
-    float4 w = *reinterpret_cast<const float4*>(Wa + (int64_t)i * D + d);
-    acc.x += c * w.x; acc.y += c * w.y; acc.z += c * w.z; acc.w += c * w.w;
-  }
-  float4 b = *reinterpret_cast<const float4*>(ba + d);
-  return make_float4(acc.x + b.x, acc.y + b.y, acc.z + b.z, acc.w + b.w);
-}
-
-__global__ void dyn_embed_fwd_kernel(const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask,
-                                     const float* __restrict__ latents, const float* __restrict__ E,
-                                     const float* __restrict__ mask_token, const float* __restrict__ null_action,
-                                     const float* __restrict__ Wa, const float* __restrict__ ba,
-                                     const float* __restrict__ ps, const float* __restrict__ pt, int T, int N,
-                                     int D, int dl, int K, int prepend, float* __restrict__ x, int* err) {
-  const int S = N + (prepend ? 1 : 0);
-  const int64_t row = blockIdx.x;  // (b*T + t)*S + s
-  const int s = (int)(row % S);
-  const int64_t bt = row / S;
-  const int t = (int)(bt % T);
-  const int64_t b = bt / T;
-  const int d = threadIdx.x * 4;
-  if (d >= D) return;
-  __shared__ float cond[64];
-  const bool need_act = prepend ? (s == 0) : true;
-  if (need_act) {
-    for (int i = threadIdx.x; i < dl; i += blockDim.x)
-      cond[i] = t == 0 ? null_action[i] : latents[(b * (T - 1) + (t - 1)) * dl + i];
-    __syncthreads();
-  }
-  float4 v;
-  if (prepend && s == 0) {
-    v = act_proj4(cond, dl, Wa, ba, D, d);
-  } else {
-    const int n = prepend ? s - 1 : s;
-    const int64_t pos = bt * N + n;
-    if (mask && mask[pos]) {
-      v = *reinterpret_cast<const float4*>(mask_token + d);
-    } else {
-      int64_t tok = tokens[pos];
-      if (tok < 0 || tok >= K) {
-        if (threadIdx.x == 0) atomicExch(err, 1);
-        tok = 0;
+// One warp per output row (grid-stride), lane l covering dims 4l + 128i; row -> (b, t, s) index math in
+// 32 bits when the row count allows (IDX = uint32_t: the int64 div/mod chain dominated the issue slots).
+// The action projection keeps the sequential i-order of cond @ Wa (cond broadcast from lanes by shuffle).
+// NC = D/128 chunks per lane when known at compile time (row loads issue before the stores), 0 = generic.
+template <int NC, typename IDX>
+__global__ void __launch_bounds__(256) dyn_embed_fwd_kernel(
+    const int64_t* __restrict__ tokens, const uint8_t* __restrict__ mask, const float* __restrict__ latents,
+    const float* __restrict__ E, const float* __restrict__ mask_token, const float* __restrict__ null_action,
+    const float* __restrict__ Wa, const float* __restrict__ ba, const float* __restrict__ ps,
+    const float* __restrict__ pt, int64_t rows, int T, int N, int D, int dl, int K, int prepend,
+    float* __restrict__ x, int* err) {
+  const IDX S = (IDX)(N + (prepend ? 1 : 0));
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = w0; row < rows; row += nw) {
+    const IDX bt = (IDX)row / S;
+    const int s = (int)((IDX)row - bt * S);
+    const IDX bq = bt / (IDX)T;
+    const int t = (int)(bt - bq * (IDX)T);
+    const bool need_act = prepend ? (s == 0) : true;
+    float c0 = 0.f, c1 = 0.f;  // cond[lane], cond[32 + lane]
+    if (need_act) {
+      const float* cp = t == 0 ? null_action : latents + ((int64_t)bq * (T - 1) + (t - 1)) * dl;
+      if (lane < dl) c0 = cp[lane];
+      if (32 + lane < dl) c1 = cp[32 + lane];
+    }
+    const float* src = nullptr;  // token / mask-token row (nullptr for the prepended action slot)
+    if (!(prepend && s == 0)) {
+      const int64_t pos = (int64_t)bt * N + (prepend ? s - 1 : s);
+      if (mask && mask[pos]) {
+        src = mask_token;
+      } else {
+        int64_t tok = tokens[pos];
+        if (tok < 0 || tok >= K) {
+          if (lane == 0) atomicExch(err, 1);
+          tok = 0;
+        }
+        src = E + tok * D;
       }
-      v = *reinterpret_cast<const float4*>(E + tok * D + d);
     }
-    if (!prepend) {
-      float4 a = act_proj4(cond, dl, Wa, ba, D, d);
-      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+    const float* psr = ps + (int64_t)s * D;
+    const float* ptr_ = pt + (int64_t)t * D;
+    float* xr = x + row * D;
+    auto chunk = [&](int d, float4 v) {
+      if (need_act) {
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int i = 0; i < dl; ++i) {
+          const float c = __shfl_sync(0xffffffffu, i < 32 ? c0 : c1, i & 31);
+          const float4 w = __ldg(reinterpret_cast<const float4*>(Wa + (int64_t)i * D + d));
+          acc.x += c * w.x; acc.y += c * w.y; acc.z += c * w.z; acc.w += c * w.w;
+        }
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(ba + d));
+        const float4 a = make_float4(acc.x + bb.x, acc.y + bb.y, acc.z + bb.z, acc.w + bb.w);
+        if (prepend) {
+          v = a;
+        } else {
+          v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+        }
+      }
+      const float4 p1 = __ldg(reinterpret_cast<const float4*>(psr + d));
+      const float4 p2 = __ldg(reinterpret_cast<const float4*>(ptr_ + d));
+      float4 o;
+      o.x = (v.x + p1.x) + p2.x; o.y = (v.y + p1.y) + p2.y;
+      o.z = (v.z + p1.z) + p2.z; o.w = (v.w + p1.w) + p2.w;
+      *reinterpret_cast<float4*>(xr + d) = o;
+    };
+    if constexpr (NC > 0) {
+      float4 v[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i)
+        v[i] = src ? __ldg(reinterpret_cast<const float4*>(src + 4 * lane + 128 * i)) : make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < NC; ++i) chunk(4 * lane + 128 * i, v[i]);
+    } else {
+      for (int d = 4 * lane; d < D; d += 128)
+        chunk(d, src ? __ldg(reinterpret_cast<const float4*>(src + d)) : make_float4(0, 0, 0, 0));
     }
   }
-  float4 p1 = *reinterpret_cast<const float4*>(ps + (int64_t)s * D + d);
-  float4 p2 = *reinterpret_cast<const float4*>(pt + (int64_t)t * D + d);
-  v.x = (v.x + p1.x) + p2.x; v.y = (v.y + p1.y) + p2.y;
-  v.z = (v.z + p1.z) + p2.z; v.w = (v.w + p1.w) + p2.w;
-  *reinterpret_cast<float4*>(x + row * D + d) = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -105,63 +125,59 @@ __global__ void dyn_embed_fwd_kernel(const int64_t* __restrict__ tokens, const u
 //   part_pt[s][t]   = sum_b dx[b,t,s]                 (-> dpt[t] = sum_s part_pt[s][t])
 //   part_mt[s]      = sum_{b,t: mask[b,t,n(s)]} dx[b,t,s]   (-> dmask_token)
 // ---------------------------------------------------------------------------
-// One CTA per spatial slot s: 4 thread groups split the T frames (each group 128 threads x 4 dims
-// over D = 512), 8 row loads in flight per thread; the groups' spatial / mask-token sums are then
-// combined in group order through shared memory (deterministic).
+// CTA per (spatial slot s, 128-dim slice): 4 warps split the T frames (warp g takes t = g mod 4, each lane
+// 4 dims), 8 row loads in flight per thread; the warps' spatial / mask-token sums are then combined in
+// warp order through shared memory (deterministic).  ~S * D/128 small CTAs keep every SM streaming.
 constexpr int kPosGroups = 4;
-__global__ void __launch_bounds__(128 * kPosGroups) dyn_embed_bwd_pos_kernel(
+__global__ void __launch_bounds__(32 * kPosGroups, 8) dyn_embed_bwd_pos_kernel(
     const float* __restrict__ dx, const uint8_t* __restrict__ mask, int64_t B, int T, int N, int D, int prepend,
     float* __restrict__ dps, float* __restrict__ part_pt, float* __restrict__ part_mt) {
-  __shared__ float4 red_s[kPosGroups - 1][128], red_m[kPosGroups - 1][128];
+  __shared__ float4 red_s[kPosGroups - 1][32], red_m[kPosGroups - 1][32];
   const int S = N + (prepend ? 1 : 0);
   const int s = blockIdx.x;
   const int n = prepend ? s - 1 : s;
-  const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;
-  for (int d0 = 0; d0 < D; d0 += 512) {
-    const int d = d0 + 4 * tid;
-    const bool live = d < D;
-    float4 acc_s = make_float4(0, 0, 0, 0), acc_m = make_float4(0, 0, 0, 0);
-    for (int t = grp; t < T; t += kPosGroups) {
-      float4 acc_t = make_float4(0, 0, 0, 0);
-      for (int64_t b0 = 0; b0 < B; b0 += 8) {
-        float4 g[8];
-        bool mk[8];
+  const int grp = threadIdx.x >> 5, tid = threadIdx.x & 31;
+  const int d = blockIdx.y * 128 + 4 * tid;
+  float4 acc_s = make_float4(0, 0, 0, 0), acc_m = make_float4(0, 0, 0, 0);
+  for (int t = grp; t < T; t += kPosGroups) {
+    float4 acc_t = make_float4(0, 0, 0, 0);
+    for (int64_t b0 = 0; b0 < B; b0 += 8) {
+      float4 g[8];
+      bool mk[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int64_t b = b0 + q;
-          g[q] = make_float4(0, 0, 0, 0);
-          mk[q] = false;
-          if (live && b < B) {
-            const int64_t row = (b * T + t) * S + s;
-            g[q] = __ldg(reinterpret_cast<const float4*>(dx + row * D + d));
-            mk[q] = n >= 0 && mask && mask[(b * T + t) * N + n];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          acc_t.x += g[q].x; acc_t.y += g[q].y; acc_t.z += g[q].z; acc_t.w += g[q].w;
-          if (mk[q]) { acc_m.x += g[q].x; acc_m.y += g[q].y; acc_m.z += g[q].z; acc_m.w += g[q].w; }
+      for (int q = 0; q < 8; ++q) {
+        const int64_t b = b0 + q;
+        g[q] = make_float4(0, 0, 0, 0);
+        mk[q] = false;
+        if (b < B) {
+          const int64_t row = (b * T + t) * S + s;
+          g[q] = __ldg(reinterpret_cast<const float4*>(dx + row * D + d));
+          mk[q] = n >= 0 && mask && mask[(b * T + t) * N + n];
         }
       }
-      if (live) *reinterpret_cast<float4*>(part_pt + ((int64_t)s * T + t) * D + d) = acc_t;
-      acc_s.x += acc_t.x; acc_s.y += acc_t.y; acc_s.z += acc_t.z; acc_s.w += acc_t.w;
-    }
-    if (grp > 0) {
-      red_s[grp - 1][tid] = acc_s;
-      red_m[grp - 1][tid] = acc_m;
-    }
-    __syncthreads();
-    if (grp == 0 && live) {
 #pragma unroll
-      for (int g2 = 0; g2 < kPosGroups - 1; ++g2) {
-        const float4 a = red_s[g2][tid], m = red_m[g2][tid];
-        acc_s.x += a.x; acc_s.y += a.y; acc_s.z += a.z; acc_s.w += a.w;
-        acc_m.x += m.x; acc_m.y += m.y; acc_m.z += m.z; acc_m.w += m.w;
+      for (int q = 0; q < 8; ++q) {
+        acc_t.x += g[q].x; acc_t.y += g[q].y; acc_t.z += g[q].z; acc_t.w += g[q].w;
+        if (mk[q]) { acc_m.x += g[q].x; acc_m.y += g[q].y; acc_m.z += g[q].z; acc_m.w += g[q].w; }
       }
-      *reinterpret_cast<float4*>(dps + (int64_t)s * D + d) = acc_s;
-      *reinterpret_cast<float4*>(part_mt + (int64_t)s * D + d) = acc_m;
     }
-    __syncthreads();
+    *reinterpret_cast<float4*>(part_pt + ((int64_t)s * T + t) * D + d) = acc_t;
+    acc_s.x += acc_t.x; acc_s.y += acc_t.y; acc_s.z += acc_t.z; acc_s.w += acc_t.w;
+  }
+  if (grp > 0) {
+    red_s[grp - 1][tid] = acc_s;
+    red_m[grp - 1][tid] = acc_m;
+  }
+  __syncthreads();
+  if (grp == 0) {
+#pragma unroll
+    for (int g2 = 0; g2 < kPosGroups - 1; ++g2) {
+      const float4 a = red_s[g2][tid], m = red_m[g2][tid];
+      acc_s.x += a.x; acc_s.y += a.y; acc_s.z += a.z; acc_s.w += a.w;
+      acc_m.x += m.x; acc_m.y += m.y; acc_m.z += m.z; acc_m.w += m.w;
+    }
+    *reinterpret_cast<float4*>(dps + (int64_t)s * D + d) = acc_s;
+    *reinterpret_cast<float4*>(part_mt + (int64_t)s * D + d) = acc_m;
   }
 }
 
@@ -416,10 +432,22 @@ extern "C" int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, cons
   const int S = N + (prepend ? 1 : 0);
   const int64_t rows = B * T * S;
   if (rows == 0) return JZ_OK;
-  dyn_embed_fwd_kernel<<<(unsigned)rows, D / 4, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      tokens, mask, latents, token_embed, mask_token, null_action, action_w, action_b, pos_spatial,
-      pos_temporal, T, N, D, dl, K, prepend, x, err);
-  JZ_LAUNCH_CHECK();
+  {
+    int64_t blocks = (rows + 7) / 8;  // 8 warps, one row each per pass
+    if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+    auto st = reinterpret_cast<cudaStream_t>(s);
+    auto launch = [&](auto kern) {
+      kern<<<(unsigned)blocks, 256, 0, st>>>(tokens, mask, latents, token_embed, mask_token, null_action, action_w,
+                                             action_b, pos_spatial, pos_temporal, rows, T, N, D, dl, K, prepend, x,
+                                             err);
+    };
+    const bool small = rows < (1ll << 31);  // 32-bit row -> (b, t, s) math
+#define EMB_FWD(NC)                                                                                  \
+  (small ? launch(dyn_embed_fwd_kernel<NC, uint32_t>) : launch(dyn_embed_fwd_kernel<NC, uint64_t>))
+    EMB_FWD(0);  // the runtime chunk loop measured faster than the unrolled NC variants at D = 512
+#undef EMB_FWD
+    JZ_LAUNCH_CHECK();
+  }
   return JZ_OK;
 }
 
@@ -447,7 +475,7 @@ extern "C" int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const ui
   float* dact_buf = part_mt + (int64_t)S * D;
   float* dcond = dact_buf + (prepend ? 0 : B * T * D);
   // positions + mask token
-  dyn_embed_bwd_pos_kernel<<<S, 128 * kPosGroups, 0, st>>>(dx, mask, B, T, N, D, prepend, d_pos_spatial, part_pt,
+  dyn_embed_bwd_pos_kernel<<<dim3(S, D / 128), 32 * kPosGroups, 0, st>>>(dx, mask, B, T, N, D, prepend, d_pos_spatial, part_pt,
                                                            part_mt);
   JZ_LAUNCH_CHECK();
   int rc = jz_reduce_partials(part_pt, S, (int64_t)T * D, d_pos_temporal, 0, s);
