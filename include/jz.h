@@ -204,7 +204,8 @@ JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_
 JZ_API int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
                                float* out_f32, float* lse, jz_stream_t stream);
 /* dqkv bf16 [frames*S, 3*H*64] (fully overwritten).  out_f32 is the forward's fp32
- * output: Delta_i = dO_i . O_i is formed from it (first launch, into `workspace`) so
+ * output: Delta_i = dO_i . O_i is formed from it (first launch, into per-(frame, head)
+ * vector blocks in `workspace`, with lse and the token-256 vectors) so
  * dP - Delta does not cancel against the bf16 rounding of O.  workspace: caller-owned,
  * jz_attn_spatial_bwd_workspace_bytes(frames, S, H) bytes, 16-byte aligned. */
 JZ_API int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H);

@@ -413,9 +413,9 @@ extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H
 //   dQ_t += dS K_j    (A = slots 2t, 2t+1 read MN-major)    (TMEM accumulators, 256 cols)
 // The MMA warp issues S/dP of block x+1 before the gradient MMAs of block x, so the
 // tensor core overlaps the elementwise stage. Delta = rowsum(dO o O_f32) comes from a
-// separate coalesced pass (spatial_delta_kernel). The P/dS warps also form the row-256 /
-// key-256 dot products of each key half; a 4-warp helper group reduces the row-256
-// gradients, runs the three epilogues (TMEM -> swizzled smem -> coalesced stores, TMEM
+// separate coalesced pass (spatial_delta_kernel). A 4-warp helper group forms the
+// row-256 / key-256 dot products on CUDA cores as soon as the tiles land (off the P/dS
+// critical path), reduces the row-256 gradients, runs the three epilogues (TMEM -> swizzled smem -> coalesced stores, TMEM
 // released before the stores), and prefetches the next unit's lse / Delta / tail vectors.
 // ============================================================================
 #ifdef JZ_ATTN_PROF
@@ -440,20 +440,25 @@ constexpr int B_DO = B_V + 2 * TILE;
 constexpr int B_DS = B_DO + 2 * TILE;    // 4 slots [128 keys][64 queries] bf16, slot = query block
 constexpr int B_ST = B_DS + 4 * TILE;    // epilogue staging tile [128 rows][64] bf16 (TMA store)
 constexpr int B_END = B_ST + TILE;       // 212992
+// per-unit vector block written by spatial_delta_kernel, one per (frame, head), floats:
+constexpr int U_LSE2 = 0;     // [0, 260)   lse * log2(e) per query row
+constexpr int U_DV = 260;     // [260, 520) Delta = rowsum(dO o O) per query row
+constexpr int U_Q = 520;      // q, k, v, dO of token 256 (fp32, 64 each)
+constexpr int U_K = 584;
+constexpr int U_V = 648;
+constexpr int U_DO = 712;
+constexpr int U_PC = 776;     // p and dS of (query 256, key 256)
+constexpr int U_DC = 777;
+constexpr int kUvbFloats = 780;  // 3120 bytes: 16-byte multiple for cp.async.bulk
 
 struct BwdSmallSmem {
   uint64_t load_full, inputs_free, dkdv_full, dkdv_free, dq_full, dq_free;
-  uint64_t sdp_full[2], pds_full[2], ds_free[2], prep_ready[2], tail_ready[2];
+  uint64_t sdp_full[2], pds_full[2], ds_free[2];
 
   uint32_t tmem_base;
-  // per-unit vectors, double-buffered: written by the helper one unit ahead
-  alignas(16) float lse2[2][260];
-  alignas(16) float Dv[2][260];
-  float p_col[2][260], ds_col[2][260];  // key 256 column over queries 0..256
-  alignas(16) float q256[2][64];
-  alignas(16) float do256[2][64];
-  alignas(16) float k256[2][64];
-  alignas(16) float v256[2][64];
+  // per-unit vector block (UVB), double-buffered, bulk-loaded by the TMA warp with the tiles
+  alignas(16) float uvb[2][kUvbFloats];
+  float p_col[2][260], ds_col[2][260];  // key 256 column over queries 0..255 (helper, per unit)
   float p_row[260], ds_row[260];        // query 256 row over keys 0..256 (current unit)
   float tail_red[3][4][64];
 };
@@ -519,9 +524,8 @@ JZ_DEV void bwd_flush_rows(const uint8_t* wstage, __nv_bfloat16* dqkv, int64_t r
 
 __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     spatial_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ delta,
-                       const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
-                       __nv_bfloat16* __restrict__ dqkv, float* __restrict__ colsum, int frames, int S, int H) {
+                       const float* __restrict__ uvb, __nv_bfloat16* __restrict__ dqkv, float* __restrict__ colsum,
+                       int frames, int S, int H) {
   using namespace sp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -550,8 +554,6 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
       mbar_init(&sm.sdp_full[b], 1);
       mbar_init(&sm.pds_full[b], 8);
       mbar_init(&sm.ds_free[b], 1);
-      mbar_init(&sm.prep_ready[b], 4);
-      mbar_init(&sm.tail_ready[b], 8);
     }
     fence_barrier_init();
   }
@@ -569,7 +571,8 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
         const int row0 = f * S;
         mbar_wait(&sm.inputs_free, (i & 1) ^ 1);
         PROF_MARK(53);
-        mbar_arrive_expect_tx(&sm.load_full, 8 * TILE);
+        mbar_arrive_expect_tx(&sm.load_full, 8 * TILE + kUvbFloats * 4);
+        bulk_load(sm.uvb[i & 1], uvb + (int64_t)u * kUvbFloats, kUvbFloats * 4, &sm.load_full);
         for (int t = 0; t < 2; ++t) {
           tma_load_2d(smem + B_K + t * TILE, &tm_qkv, &sm.load_full, D + h * 64, row0 + 128 * t);
           tma_load_2d(smem + B_Q + t * TILE, &tm_qkv, &sm.load_full, h * 64, row0 + 128 * t);
@@ -580,12 +583,19 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
-    if (lane == 0) {
+    // the whole warp runs the loop (convergent: uniform operands); one elected lane issues
+    {
       constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);   // K_j Q_c^T, V_j dO_c^T
       constexpr uint32_t id_kv = idesc_bf16_f32(128, 64, false, true);   // P^T dO_c, dS^T Q_c
       constexpr uint32_t id_q = idesc_bf16_f32(128, 64, true, true);     // dS K_j
-      const uint32_t aq = smem_u32(smem + B_Q), ak = smem_u32(smem + B_K), av = smem_u32(smem + B_V),
-                     ado = smem_u32(smem + B_DO), ads = smem_u32(smem + B_DS);
+      // SW128 descriptors share one high word (SBO = 1024, version, swizzle); the low word is
+      // (address >> 4) | (LBO >> 4) << 16, so each MMA's descriptor is one add on a shifted base
+      const uint32_t dhi = (uint32_t)(sdesc_sw128(0, 0, 1024) >> 32);
+      const uint32_t aq = smem_u32(smem + B_Q) >> 4, ak = smem_u32(smem + B_K) >> 4, av = smem_u32(smem + B_V) >> 4,
+                     ado = smem_u32(smem + B_DO) >> 4, ads = smem_u32(smem + B_DS) >> 4;
+      auto dsc = [dhi](uint32_t addr4, uint32_t off, uint32_t lbo) -> uint64_t {
+        return ((uint64_t)dhi << 32) | (addr4 + (off >> 4) + ((lbo >> 4) << 16));
+      };
       // gradient MMAs of block y of unit i (its P^T / dS^T are ready once pds_full fires)
       auto grad_mmas = [&](int i, int y) {
         const uint32_t gy = 8u * i + y, by = gy & 1;
@@ -606,19 +616,19 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint32_t pa = pcol + (ks < 2 ? 8 * ks : 32 + 8 * (ks - 2));
-          umma_bf16_ts(tmem + C_DV, pa, sdesc_sw128(ado + qoff + ks * 2048, 8192, 1024), id_kv, (cy > 0 || ks > 0));
-          umma_bf16_ss(tmem + C_DK, sdesc_sw128(ads + cy * TILE + ks * 32, 16, 1024),
-                       sdesc_sw128(aq + qoff + ks * 2048, 8192, 1024), id_kv, (cy > 0 || ks > 0));
+          umma_bf16_ts_w(tmem + C_DV, pa, dsc(ado, qoff + ks * 2048, 8192), id_kv, (cy > 0 || ks > 0));
+          umma_bf16_ss_w(tmem + C_DK, dsc(ads, cy * TILE + ks * 32, 16),
+                       dsc(aq, qoff + ks * 2048, 8192), id_kv, (cy > 0 || ks > 0));
         }
         if (cy & 1) {
           const int t = cy >> 1;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks)
-            umma_bf16_ss(tmem + C_DQ + 64 * t, sdesc_sw128(ads + 2 * t * TILE + ks * 2048, TILE, 1024),
-                         sdesc_sw128(ak + jy * TILE + ks * 2048, 8192, 1024), id_q, (jy > 0 || ks > 0));
-          umma_commit(&sm.ds_free[t]);
+            umma_bf16_ss_w(tmem + C_DQ + 64 * t, dsc(ads, 2 * t * TILE + ks * 2048, TILE),
+                         dsc(ak, jy * TILE + ks * 2048, 8192), id_q, (jy > 0 || ks > 0));
+          umma_commit_w(&sm.ds_free[t]);
         }
-        if (cy == 3) umma_commit(&sm.dkdv_full);
+        if (cy == 3) umma_commit_w(&sm.dkdv_full);
         PROF_MARK(18 + y);
       };
       int i = 0;
@@ -634,18 +644,18 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
           // TMEM buffer b was last read by the dV MMA of block gx-2, issued earlier by this thread
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            umma_bf16_ss(tmem + 128 * b, sdesc_sw128(ak + j * TILE + kk * 32, 16, 1024),
-                         sdesc_sw128(aq + qoff + kk * 32, 16, 1024), id_s, kk > 0);
-            umma_bf16_ss(tmem + 128 * b + 64, sdesc_sw128(av + j * TILE + kk * 32, 16, 1024),
-                         sdesc_sw128(ado + qoff + kk * 32, 16, 1024), id_s, kk > 0);
+            umma_bf16_ss_w(tmem + 128 * b, dsc(ak, j * TILE + kk * 32, 16),
+                         dsc(aq, qoff + kk * 32, 16), id_s, kk > 0);
+            umma_bf16_ss_w(tmem + 128 * b + 64, dsc(av, j * TILE + kk * 32, 16),
+                         dsc(ado, qoff + kk * 32, 16), id_s, kk > 0);
           }
-          umma_commit(&sm.sdp_full[b]);
+          umma_commit_w(&sm.sdp_full[b]);
           PROF_MARK(2 + x);
           if (x > 0) grad_mmas(i, x - 1);
         }
         grad_mmas(i, 7);
-        umma_commit(&sm.dq_full);
-        umma_commit(&sm.inputs_free);
+        umma_commit_w(&sm.dq_full);
+        umma_commit_w(&sm.inputs_free);
       }
     }
   } else if (warp < 10) {
@@ -657,10 +667,10 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const int pb = i & 1;
-      mbar_wait(&sm.prep_ready[pb], (i >> 1) & 1);
+      mbar_wait(&sm.load_full, i & 1);  // tiles + this unit's vector block
       if (threadIdx.x == 64) PROF_MARK(26);
-      const float* lse2 = sm.lse2[pb];
-      const float* Dv = sm.Dv[pb];
+      const float* lse2 = sm.uvb[pb] + U_LSE2;
+      const float* Dv = sm.uvb[pb] + U_DV;
       for (int x = 0; x < 8; ++x) {
         const uint32_t gx = 8u * i + x, b = gx & 1;
         const int j = x >> 2, c = x & 3;
@@ -700,41 +710,6 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pds_full[b]);
         if (threadIdx.x == 64) PROF_MARK(35 + x);
-        if (c == 0 && has_tail) {
-          // CUDA-core tail terms of this key half, off the tensor-core path:
-          //   half 0: query 256 against key 128j + r   -> p_row, ds_row
-          //   half 1: key 256 against query 128j + r   -> p_col, ds_col
-          const int idx = 128 * j + r;
-          const uint8_t* at = smem + (half == 0 ? B_K : B_Q) + j * TILE;
-          const uint8_t* bt = smem + (half == 0 ? B_V : B_DO) + j * TILE;
-          const float* va = half == 0 ? sm.q256[pb] : sm.k256[pb];
-          const float* vb = half == 0 ? sm.do256[pb] : sm.v256[pb];
-          float a = 0.f, dp = 0.f;
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const uint4 wa = *reinterpret_cast<const uint4*>(at + sw128(r, cc));
-            const uint4 wb = *reinterpret_cast<const uint4*>(bt + sw128(r, cc));
-            const float4 a0 = *reinterpret_cast<const float4*>(va + 8 * cc);
-            const float4 a1 = *reinterpret_cast<const float4*>(va + 8 * cc + 4);
-            const float4 b0 = *reinterpret_cast<const float4*>(vb + 8 * cc);
-            const float4 b1 = *reinterpret_cast<const float4*>(vb + 8 * cc + 4);
-            const float2 x0 = unpack_bf16(wa.x), x1 = unpack_bf16(wa.y), x2 = unpack_bf16(wa.z), x3 = unpack_bf16(wa.w);
-            const float2 y0 = unpack_bf16(wb.x), y1 = unpack_bf16(wb.y), y2 = unpack_bf16(wb.z), y3 = unpack_bf16(wb.w);
-            a += x0.x * a0.x + x0.y * a0.y + x1.x * a0.z + x1.y * a0.w + x2.x * a1.x + x2.y * a1.y + x3.x * a1.z + x3.y * a1.w;
-            dp += y0.x * b0.x + y0.y * b0.y + y1.x * b0.z + y1.y * b0.w + y2.x * b1.x + y2.y * b1.y + y3.x * b1.z + y3.y * b1.w;
-          }
-          if (half == 0) {
-            const float p = ex2(a * c2 - lse2[256]);
-            sm.p_row[idx] = p;
-            sm.ds_row[idx] = p * (dp - Dv[256]);
-          } else {
-            const float p = ex2(a * c2 - lse2[idx]);
-            sm.p_col[pb][idx] = p;
-            sm.ds_col[pb][idx] = p * (dp - Dv[idx]);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.tail_ready[j]);
-        }
       }
     }
   } else {
@@ -744,57 +719,6 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
     const int hw = warp - 10;             // helper warp 0..3
     const int r = quarter * 32 + lane;    // TMEM lane for the epilogues
     const uint32_t base = tmem + ((quarter * 32) << 16);
-    // prepare(u -> buffer pb): lse2, D (precomputed delta) and the row-256 vectors of unit u,
-    // one unit ahead; all loads are independent and issued together
-    auto prepare = [&](int u, int pb) {
-      const int f = u / H, h = u % H;
-      const int64_t row0 = (int64_t)f * S;
-      const int64_t vb = ((int64_t)f * H + h) * S;
-      float l[3], dl[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int q = ht + 128 * k;
-        l[k] = q < S ? lse[vb + q] : 0.f;
-        dl[k] = q < S ? delta[vb + q] : 0.f;
-      }
-      float v4[4] = {0.f, 0.f, 0.f, 0.f};
-      if (ht < 64 && has_tail) {
-        const int64_t rr = row0 + 256;
-        v4[0] = __bfloat162float(qkv[rr * ld3 + h * 64 + ht]);
-        v4[1] = __bfloat162float(qkv[rr * ld3 + D + h * 64 + ht]);
-        v4[2] = __bfloat162float(qkv[rr * ld3 + 2 * D + h * 64 + ht]);
-        v4[3] = __bfloat162float(dout[rr * D + h * 64 + ht]);
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int q = ht + 128 * k;
-        if (q < S) {
-          sm.lse2[pb][q] = l[k] * 1.4426950408889634f;
-          sm.Dv[pb][q] = dl[k];
-        }
-      }
-      if (ht < 64) {
-        sm.q256[pb][ht] = v4[0];
-        sm.k256[pb][ht] = v4[1];
-        sm.v256[pb][ht] = v4[2];
-        sm.do256[pb][ht] = v4[3];
-      }
-      named_bar(3, 128);
-      if (has_tail && hw == 0) {  // key-256 entry of query row 256
-        const int d = 2 * lane;
-        float sk = sm.q256[pb][d] * sm.k256[pb][d] + sm.q256[pb][d + 1] * sm.k256[pb][d + 1];
-        float dpv = sm.do256[pb][d] * sm.v256[pb][d] + sm.do256[pb][d + 1] * sm.v256[pb][d + 1];
-        sk = warp_sum(sk);
-        dpv = warp_sum(dpv);
-        if (lane == 0) {
-          const float p = ex2(sk * c2 - sm.lse2[pb][256]);
-          sm.p_col[pb][256] = p;
-          sm.ds_col[pb][256] = p * (dpv - sm.Dv[pb][256]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.prep_ready[pb]);
-    };
     // one warp writes its 32 rows (64 bf16 each) coalesced: stage row-per-lane in its own 4 KB
     // of the staging tile (128B-swizzled), read back 4 rows x 128 B per instruction
     uint8_t* wstage = smem + B_ST + quarter * 4096;
@@ -805,28 +729,66 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
                  colsum ? colsum + ((int64_t)f * 9 + (((row_first) - row0) >> 5)) * ld3 : nullptr)
 
     int i = 0;
-    if (blockIdx.x < units) prepare(blockIdx.x, 0);
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
       const int pb = i & 1;
-      mbar_wait(&sm.prep_ready[pb], (i >> 1) & 1);
-      // next unit's vectors first: only global loads, and buffer pb ^ 1 was last read in unit i - 1,
-      // which every warp has finished (this warp's own unit i - 1 dQ epilogue came after its MMAs)
-      if (u + (int)gridDim.x < units) prepare(u + gridDim.x, pb ^ 1);
-      mbar_wait(&sm.load_full, i & 1);
+      const float* uv = sm.uvb[pb];
+      const float *q256 = uv + U_Q, *k256 = uv + U_K, *v256 = uv + U_V, *do256 = uv + U_DO;
+      mbar_wait(&sm.load_full, i & 1);  // tiles + vector block (uvb[pb] is reloaded only after this
+                                        // unit's inputs_free, which this group arrives on below)
       if (ht == 0) PROF_MARK(43);
+      if (has_tail) {
+        // CUDA-core tail terms (no tensor-core input needed, so they run while the helper would idle):
+        //   query 256 against key idx  -> p_row, ds_row;   key 256 against query idx -> p_col, ds_col
+        const float* lse2 = uv + U_LSE2;
+        const float* Dv = uv + U_DV;
+        named_bar(3, 128);  // p_row / ds_row are single-buffered: every helper warp is past unit i-1's (f)
+#pragma unroll 1
+        for (int jj = 0; jj < 2; ++jj) {
+          const int idx = 128 * jj + ht;
+          float a[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
+#pragma unroll 1
+          for (int side = 0; side < 2; ++side) {  // 0: K.q256 / V.do256   1: Q.k256 / dO.v256
+            const uint8_t* at = smem + (side == 0 ? B_K : B_Q) + jj * TILE;
+            const uint8_t* bt = smem + (side == 0 ? B_V : B_DO) + jj * TILE;
+            const float* va = side == 0 ? q256 : k256;
+            const float* vb = side == 0 ? do256 : v256;
+            float sa = 0.f, sb = 0.f;
+#pragma unroll 4
+            for (int cc = 0; cc < 8; ++cc) {
+              const uint4 wa = *reinterpret_cast<const uint4*>(at + sw128(ht, cc));
+              const uint4 wb = *reinterpret_cast<const uint4*>(bt + sw128(ht, cc));
+              const float4 a0 = *reinterpret_cast<const float4*>(va + 8 * cc);
+              const float4 a1 = *reinterpret_cast<const float4*>(va + 8 * cc + 4);
+              const float4 b0 = *reinterpret_cast<const float4*>(vb + 8 * cc);
+              const float4 b1 = *reinterpret_cast<const float4*>(vb + 8 * cc + 4);
+              const float2 x0 = unpack_bf16(wa.x), x1 = unpack_bf16(wa.y), x2 = unpack_bf16(wa.z), x3 = unpack_bf16(wa.w);
+              const float2 y0 = unpack_bf16(wb.x), y1 = unpack_bf16(wb.y), y2 = unpack_bf16(wb.z), y3 = unpack_bf16(wb.w);
+              sa += x0.x * a0.x + x0.y * a0.y + x1.x * a0.z + x1.y * a0.w + x2.x * a1.x + x2.y * a1.y + x3.x * a1.z + x3.y * a1.w;
+              sb += y0.x * b0.x + y0.y * b0.y + y1.x * b0.z + y1.y * b0.w + y2.x * b1.x + y2.y * b1.y + y3.x * b1.z + y3.y * b1.w;
+            }
+            if (side == 0) { a[0] = sa; dp[0] = sb; } else { a[1] = sa; dp[1] = sb; }
+          }
+          const float p = ex2(a[0] * c2 - lse2[256]);
+          sm.p_row[idx] = p;
+          sm.ds_row[idx] = p * (dp[0] - Dv[256]);
+          const float pc = ex2(a[1] * c2 - lse2[idx]);
+          sm.p_col[pb][idx] = pc;
+          sm.ds_col[pb][idx] = pc * (dp[1] - Dv[idx]);
+        }
+        named_bar(3, 128);
+      }
       const int64_t qrow0 = row0 + quarter * 32;  // first of this warp's 32 rows in a 128-row tile
       // ---- (e) dV_0 / dK_0 ----
       mbar_wait(&sm.dkdv_full, (2 * i) & 1);
-      if (has_tail) mbar_wait(&sm.tail_ready[0], i & 1);
       if (ht == 0) PROF_MARK(46);
       tc_fence_after();
       {
         const float cp = has_tail ? sm.p_row[r] : 0.f, cd = has_tail ? sm.ds_row[r] : 0.f;
-        stage_acc(C_DV, cp, sm.do256[pb], 1.0f);
+        stage_acc(C_DV, cp, do256, 1.0f);
         flush_rows(qrow0, 2 * D + h * 64);
-        stage_acc(C_DK, cd, sm.q256[pb], scale);
+        stage_acc(C_DK, cd, q256, scale);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_relaxed(&sm.dkdv_free);
@@ -835,8 +797,6 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
       if (ht == 0) PROF_MARK(47);
       // ---- (b) row 256: dQ_256 = sum_k ds_row K_k, dK_256 = sum_q ds_col Q_q, dV_256 = sum_q p_col dO_q ----
       if (has_tail) {
-        mbar_wait(&sm.tail_ready[1], i & 1);
-        mbar_wait(&sm.load_full, i & 1);
         {
           const int dpair = ht & 31, part = ht >> 5;  // 2 dims, 64 rows per part
           const uint32_t chunk = dpair >> 2, within = (dpair & 3) * 4;
@@ -870,8 +830,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
         if (ht < 64) {
           const int d = ht;
           const int64_t rr = row0 + 256;
-          float sq = sm.ds_col[pb][256] * sm.k256[pb][d], skk = sm.ds_col[pb][256] * sm.q256[pb][d],
-                sv = sm.p_col[pb][256] * sm.do256[pb][d];
+          float sq = uv[U_DC] * k256[d], skk = uv[U_DC] * q256[d], sv = uv[U_PC] * do256[d];
 #pragma unroll
           for (int pt = 0; pt < 4; ++pt) {
             sq += sm.tail_red[0][pt][d];
@@ -908,9 +867,9 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
       {
         const int key = 128 + r;
         const float cp = has_tail ? sm.p_row[key] : 0.f, cd = has_tail ? sm.ds_row[key] : 0.f;
-        stage_acc(C_DV, cp, sm.do256[pb], 1.0f);
+        stage_acc(C_DV, cp, do256, 1.0f);
         flush_rows(qrow0 + 128, 2 * D + h * 64);
-        stage_acc(C_DK, cd, sm.q256[pb], scale);
+        stage_acc(C_DK, cd, q256, scale);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_relaxed(&sm.dkdv_free);
@@ -922,9 +881,9 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
       if (ht == 0) PROF_MARK(51);
       tc_fence_after();
       {
-        stage_acc(C_DQ, has_tail ? sm.ds_col[pb][r] : 0.f, sm.k256[pb], scale);
+        stage_acc(C_DQ, has_tail ? sm.ds_col[pb][r] : 0.f, k256, scale);
         flush_rows(qrow0, h * 64);
-        stage_acc(C_DQ + 64, has_tail ? sm.ds_col[pb][128 + r] : 0.f, sm.k256[pb], scale);
+        stage_acc(C_DQ + 64, has_tail ? sm.ds_col[pb][128 + r] : 0.f, k256, scale);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_relaxed(&sm.dq_free);
@@ -945,36 +904,82 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
 
 }  // namespace jz
 
-// Delta_i = rowsum(dO_i o O_i) per (frame, head, row), same layout as lse: one warp per token row,
-// coalesced over the H*64 columns. dO is the bf16 tensor the MMAs consume, O the forward's fp32 copy.
-__global__ void spatial_delta_kernel(const float* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
-                                     int64_t rows, int S, int H, float* __restrict__ delta) {
-  const int lane = threadIdx.x & 31;
+// Per-unit vector blocks for the backward (layout sp::U_*), one CTA per frame: its warps take the
+// token rows (coalesced over the H*64 columns) and form Delta_i = rowsum(dO_i o O_i) per head into
+// shared memory (dO the bf16 tensor the MMAs consume, O the forward's fp32 copy); then each head's
+// block is written contiguously: lse_i * log2(e) and Delta_i for every row, and for token 256 its
+// q, k, v, dO vectors (fp32) and the (256, 256) entry p = exp(q.k / 8 - lse), dS = p (dO.v - Delta).
+constexpr int kUvbMaxH = 16;
+__global__ void __launch_bounds__(256) spatial_uvb_kernel(const float* __restrict__ out,
+                                                          const __nv_bfloat16* __restrict__ dout,
+                                                          const __nv_bfloat16* __restrict__ qkv,
+                                                          const float* __restrict__ lse, int64_t frames, int S,
+                                                          int H, float* __restrict__ uvb) {
+  using namespace jz::sp;
+  __shared__ float dv_s[kUvbMaxH][260];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int D = H * 64;
-  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t row = w0; row < rows; row += nw) {
-    const float* o = out + row * D;
-    const __nv_bfloat16* g = dout + row * D;
-    const int64_t f = row / S, sidx = row - f * S;
-    for (int c = 0; c < D / 128; ++c) {
-      const int col = 128 * c + 4 * lane;
-      const float4 ov = __ldg(reinterpret_cast<const float4*>(o + col));
-      const uint2 gv = __ldg(reinterpret_cast<const uint2*>(g + col));
-      const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
-      float acc = ov.x * g0.x + ov.y * g0.y + ov.z * g1.x + ov.w * g1.y;
-#pragma unroll
-      for (int m = 8; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);  // 16 lanes = one head
-      if ((lane & 15) == 0) {
+  const float c2 = 0.125f * 1.4426950408889634f;
+  for (int64_t f = blockIdx.x; f < frames; f += gridDim.x) {
+    for (int sidx = warp; sidx < S; sidx += nwarps) {
+      const int64_t row = f * S + sidx;
+      const float* o = out + row * D;
+      const __nv_bfloat16* g = dout + row * D;
+#pragma unroll 4
+      for (int c = 0; c < D / 128; ++c) {
+        const int col = 128 * c + 4 * lane;
         const int h = col >> 6;
-        delta[((int64_t)f * H + h) * S + sidx] = acc;
+        const float4 ov = __ldg(reinterpret_cast<const float4*>(o + col));
+        const uint2 gv = __ldg(reinterpret_cast<const uint2*>(g + col));
+        const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
+        float acc = ov.x * g0.x + ov.y * g0.y + ov.z * g1.x + ov.w * g1.y;
+#pragma unroll
+        for (int m = 8; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);  // 16 lanes = one head
+        if ((lane & 15) == 0) dv_s[h][sidx] = acc;
+        if (sidx == 256) {
+          float* ub = uvb + (f * H + h) * kUvbFloats;
+          const __nv_bfloat16* qr = qkv + row * 3 * (int64_t)D;
+          const uint2 qv = __ldg(reinterpret_cast<const uint2*>(qr + col));
+          const uint2 kv = __ldg(reinterpret_cast<const uint2*>(qr + D + col));
+          const uint2 vv = __ldg(reinterpret_cast<const uint2*>(qr + 2 * D + col));
+          const float2 q0 = unpack_bf16(qv.x), q1 = unpack_bf16(qv.y), k0 = unpack_bf16(kv.x), k1 = unpack_bf16(kv.y);
+          const float2 v0 = unpack_bf16(vv.x), v1 = unpack_bf16(vv.y);
+          const int d = col & 63;
+          *reinterpret_cast<float4*>(ub + U_Q + d) = make_float4(q0.x, q0.y, q1.x, q1.y);
+          *reinterpret_cast<float4*>(ub + U_K + d) = make_float4(k0.x, k0.y, k1.x, k1.y);
+          *reinterpret_cast<float4*>(ub + U_V + d) = make_float4(v0.x, v0.y, v1.x, v1.y);
+          *reinterpret_cast<float4*>(ub + U_DO + d) = make_float4(g0.x, g0.y, g1.x, g1.y);
+          float sk = q0.x * k0.x + q0.y * k0.y + q1.x * k1.x + q1.y * k1.y;
+          float dpv = g0.x * v0.x + g0.y * v0.y + g1.x * v1.x + g1.y * v1.y;
+#pragma unroll
+          for (int m = 8; m >= 1; m >>= 1) {
+            sk += __shfl_xor_sync(0xffffffffu, sk, m);
+            dpv += __shfl_xor_sync(0xffffffffu, dpv, m);
+          }
+          if ((lane & 15) == 0) {
+            const float p = exp2f(sk * c2 - __ldg(lse + (f * H + h) * S + 256) * 1.4426950408889634f);
+            ub[U_PC] = p;
+            ub[U_DC] = p * (dpv - acc);
+          }
+        }
       }
     }
+    __syncthreads();
+    for (int h = 0; h < H; ++h) {
+      float* ub = uvb + (f * H + h) * kUvbFloats;
+      const float* lr = lse + (f * H + h) * S;
+      for (int q = threadIdx.x; q < S; q += blockDim.x) {
+        ub[U_LSE2 + q] = __ldg(lr + q) * 1.4426950408889634f;
+        ub[U_DV + q] = dv_s[h][q];
+      }
+    }
+    __syncthreads();
   }
 }
 
 extern "C" int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H) {
-  return frames * (int64_t)S * H * (int64_t)sizeof(float);
+  (void)S;
+  return frames * (int64_t)H * jz::sp::kUvbFloats * (int64_t)sizeof(float);
 }
 
 extern "C" int64_t jz_attn_spatial_colsum_parts(int64_t frames) { return frames * 9; }
@@ -991,14 +996,15 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
   if (rc) return rc;
   rc = make_tmap_2d_bf16(&td, dout, D, frames * S, D, 64, 128);
   if (rc) return rc;
-  JZ_CHECK_ARG(workspace != nullptr, "spatial attention bwd: workspace (frames*S*H floats) required");
-  float* delta = reinterpret_cast<float*>(workspace);
+  JZ_CHECK_ARG(workspace != nullptr, "spatial attention bwd: workspace (jz_attn_spatial_bwd_workspace_bytes) required");
+  JZ_CHECK_ARG(reinterpret_cast<uintptr_t>(workspace) % 16 == 0, "spatial attention bwd: workspace must be 16-byte aligned");
+  float* uvb = reinterpret_cast<float*>(workspace);
   {
-    const int64_t rows = frames * S;
-    int blocks = (int)((rows * 32 + 255) / 256);
-    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
-    spatial_delta_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-        out_f32, reinterpret_cast<const __nv_bfloat16*>(dout), rows, S, H, delta);
+    JZ_CHECK_ARG(H <= kUvbMaxH, "spatial attention bwd: %d heads unsupported (<= 16)", H);
+    int blocks = (int)(frames < num_sms() * 8 ? frames : num_sms() * 8);
+    spatial_uvb_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+        out_f32, reinterpret_cast<const __nv_bfloat16*>(dout), reinterpret_cast<const __nv_bfloat16*>(qkv), lse,
+        frames, S, H, uvb);
     JZ_LAUNCH_CHECK();
   }
   static std::once_flag once;
@@ -1010,9 +1016,7 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
   const int64_t units = frames * H;
   const int grid = (int)(units < num_sms() ? units : num_sms());
   spatial_bwd_kernel<<<grid, sp::kBwdThreads2, sp::B_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
-      tq, td, reinterpret_cast<const __nv_bfloat16*>(qkv), delta,
-      reinterpret_cast<const __nv_bfloat16*>(dout), lse, reinterpret_cast<__nv_bfloat16*>(dqkv), colsum_part,
-      (int)frames, S, H);
+      tq, td, uvb, reinterpret_cast<__nv_bfloat16*>(dqkv), colsum_part, (int)frames, S, H);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

@@ -269,7 +269,7 @@ def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=
     """colsum (fp32 [3*H*64], optional): also the column sums of dqkv (QKV bias gradient)."""
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
-    ws = scratch("attn_delta", frames * S * H)
+    ws = scratch("attn_uvb", L.load().jz_attn_spatial_bwd_workspace_bytes(frames, S, H) // 4)
     part, nparts = None, 0
     if colsum is not None:
         nparts = L.load().jz_attn_spatial_colsum_parts(frames)

@@ -29,7 +29,7 @@ for S in (256, 257):
     o32 = torch.empty(frames * S, D, device=dev)
     lse = torch.empty(frames, H, S, device=dev)
     dq = torch.empty_like(qkv)
-    WS = torch.empty(frames * S * H, device='cuda')
+    WS = torch.empty(frames * H * 780, device='cuda')
     f = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
     f2 = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), None, lse.data_ptr(), L.stream_ptr())
     bw = lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())

@@ -95,7 +95,7 @@ if "spatial_bwd" in sys.argv:
         dout = go.reshape(frames * S, D).bfloat16().contiguous()
         dqkv = torch.full_like(qkv, float("nan"))
         L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
-               64, dqkv.data_ptr(), torch.empty(frames * S * H, device=dev).data_ptr(), None, L.stream_ptr())
+               64, dqkv.data_ptr(), torch.empty(frames * H * 780, device=dev).data_ptr(), None, L.stream_ptr())
         torch.cuda.synchronize()
         for i, nm in enumerate("qkv"):
             check(f"spatial bwd S={S} d{nm}", dqkv[:, i * D:(i + 1) * D], dref[:, i * D:(i + 1) * D], 2e-2)
@@ -129,7 +129,7 @@ lse_t = torch.empty(36 * S, H, 16, device=dev)
 us = timeit(lambda: L.call("jz_attn_temporal_fwd", qkv.data_ptr(), 36, 16, S, H, 64, out.data_ptr(), lse_t.data_ptr(), L.stream_ptr()))
 print(f"temporal fwd B36: {us:.1f} us  {(qkv.numel() * 2 + out.numel() * 2) / us / 1e3:.0f} GB/s", flush=True)
 dq = torch.empty_like(qkv)
-WS = torch.empty(frames * S * H, device='cuda')
+WS = torch.empty(frames * H * 780, device='cuda')
 us = timeit(lambda: L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), out.data_ptr(), lse_t.data_ptr(), 36, 16, S, H, 64, dq.data_ptr(), None, L.stream_ptr()))
 print(f"temporal bwd B36: {us:.1f} us  {(qkv.numel() * 4 + out.numel() * 4) / us / 1e3:.0f} GB/s", flush=True)
 if "spatial_bwd" in sys.argv:

@@ -20,7 +20,7 @@ out = torch.empty(frames * S, D, device="cuda", dtype=torch.bfloat16)
 o32 = torch.empty(frames * S, D, device="cuda")
 lse = torch.empty(frames, H, S, device="cuda")
 dq = torch.empty_like(qkv)
-WS = torch.empty(frames * S * H, device='cuda')
+WS = torch.empty(frames * H * 780, device='cuda')
 L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
 for _ in range(3):
     L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
