@@ -114,10 +114,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // the whole warp runs the loop (convergent: uniform operands); one elected lane issues
+    {
       constexpr uint32_t idesc_s = idesc_bf16_f32(128, 256, false, false);
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, 64, false, true);
-      const uint32_t q_addr = smem_u32(smem + F_Q), k_addr = smem_u32(smem + F_K), v_addr = smem_u32(smem + F_V);
+      // SW128 descriptors share one high word; low word = (address >> 4) | (LBO >> 4) << 16
+      const uint32_t dhi = (uint32_t)(sdesc_sw128(0, 0, 1024) >> 32);
+      auto dsc = [dhi](uint32_t addr4, uint32_t off, uint32_t lbo) -> uint64_t {
+        return ((uint64_t)dhi << 32) | (addr4 + (off >> 4) + ((lbo >> 4) << 16));
+      };
+      const uint32_t q4 = smem_u32(smem + F_Q) >> 4, k4 = smem_u32(smem + F_K) >> 4, v4 = smem_u32(smem + F_V) >> 4;
+      const uint32_t p4[2] = {smem_u32(smem + F_P0) >> 4, smem_u32(smem + F_P1) >> 4};
       int i = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         const uint32_t par = i & 1;
@@ -127,23 +134,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_bf16_ss(tmem + 256 * t, sdesc_sw128(q_addr + t * TILE + kk * 32, 16, 1024),
-                         sdesc_sw128(k_addr + kk * 32, 16, 1024), idesc_s, kk > 0);
-          umma_commit(&sm.s_full[t]);
+            umma_bf16_ss_w(tmem + 256 * t, dsc(q4, t * TILE + kk * 32, 16), dsc(k4, kk * 32, 16), idesc_s, kk > 0);
+          umma_commit_w(&sm.s_full[t]);
         }
-        umma_commit(&sm.qk_free);
+        umma_commit_w(&sm.qk_free);
         mbar_wait(&sm.v_full, par);
         for (int t = 0; t < 2; ++t) {
           mbar_wait(&sm.p_full[t], par);
           tc_fence_after();
-          const uint32_t p_addr = smem_u32(smem + (t ? F_P1 : F_P0));
 #pragma unroll
           for (int ks = 0; ks < 16; ++ks)
-            umma_bf16_ss(tmem + 256 * t, sdesc_sw128(p_addr + (ks >> 2) * TILE + (ks & 3) * 32, 16, 1024),
-                         sdesc_sw128(v_addr + ks * 2048, 8192, 1024), idesc_o, ks > 0);
-          umma_commit(&sm.o_full[t]);
+            umma_bf16_ss_w(tmem + 256 * t, dsc(p4[t], (ks >> 2) * TILE + (ks & 3) * 32, 16),
+                           dsc(v4, ks * 2048, 8192), idesc_o, ks > 0);
+          umma_commit_w(&sm.o_full[t]);
         }
-        umma_commit(&sm.v_free);
+        umma_commit_w(&sm.v_free);
       }
     }
   } else if (warp < 10) {

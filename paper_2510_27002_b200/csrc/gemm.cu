@@ -386,8 +386,12 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    // the whole warp runs the issue loop (convergent: operands stay warp-uniform, no per-MMA
+    // elect/R2UR waterfall); one elected lane issues each tcgen05 instruction
+    if (rank == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(TM, BN, A_MN, B_MN);
+      const uint32_t dhi = (uint32_t)(sdesc_sw128(0, 0, 1024) >> 32);
+      const uint32_t smem_base4 = smem_u32(smem) >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -414,23 +418,24 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
           fw += clock64() - t0;
 #endif
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * S::STAGE_BYTES);
-          const uint32_t b_addr = a_addr + S::A_BYTES;
+          // SW128 descriptors: one shared high word, low word = (address >> 4) | (LBO >> 4) << 16
+          const uint32_t a4 = (smem_base4 + stage * (S::STAGE_BYTES >> 4));
+          const uint32_t b4 = a4 + (S::A_BYTES >> 4);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t adesc = A_MN ? sdesc_sw128(a_addr + kk * 2048, 64 * BK * 2, 1024)
-                                        : sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? sdesc_sw128(b_addr + kk * 2048, 64 * BK * 2, 1024)
-                                        : sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            if constexpr (PAIR) umma_bf16_ss_pair(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-            else umma_bf16_ss(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            const uint32_t alo = A_MN ? a4 + kk * 128 + (((64 * BK * 2) >> 4) << 16) : a4 + kk * 2 + (1u << 16);
+            const uint32_t blo = B_MN ? b4 + kk * 128 + (((64 * BK * 2) >> 4) << 16) : b4 + kk * 2 + (1u << 16);
+            const uint64_t adesc = ((uint64_t)dhi << 32) | alo;
+            const uint64_t bdesc = ((uint64_t)dhi << 32) | blo;
+            if constexpr (PAIR) umma_bf16_ss_pair_w(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            else umma_bf16_ss_w(d_tmem, adesc, bdesc, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
-          if constexpr (PAIR) umma_commit_pair(&empty_bar[stage], 0x3);
-          else umma_commit(&empty_bar[stage]);
+          if constexpr (PAIR) umma_commit_pair_w(&empty_bar[stage], 0x3);
+          else umma_commit_w(&empty_bar[stage]);
           if (++stage == S::STAGES) { stage = 0; phase ^= 1; }
         }
-        if constexpr (PAIR) umma_commit_pair(&tfull_bar[acc], 0x3);
-        else umma_commit(&tfull_bar[acc]);
+        if constexpr (PAIR) umma_commit_pair_w(&tfull_bar[acc], 0x3);
+        else umma_commit_w(&tfull_bar[acc]);
         GPROF(2);
 #ifdef JZ_GEMM_PROF
         if (blockIdx.x == 0 && ti < 64) g_gemm_prof[ti * 8 + 6] = fw;

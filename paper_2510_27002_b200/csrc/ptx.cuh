@@ -266,6 +266,29 @@ JZ_DEV void umma_bf16_ss_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// warp-wide (elect-one) variants of the pair MMA / commit, see umma_bf16_ss_w
+JZ_DEV void umma_bf16_ss_pair_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+JZ_DEV void umma_commit_pair_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // Commit the pair's MMAs to the mbarrier at the same offset in every CTA of `mask`.
 JZ_DEV void umma_commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile(
