@@ -179,35 +179,62 @@ __global__ void __launch_bounds__(kRowThreads, 2) ln_bwd_kernel(
 // ---------------------------------------------------------------------------
 // Column sums of a bf16 matrix (bias gradients), per-CTA partials.
 // ---------------------------------------------------------------------------
+// Threads form `groups` row-groups of cpt = cols/8 threads (8 columns each); group g takes rows
+// r0 + g, r0 + g + groups, ... with 16 independent 16-byte loads in flight, and the groups' sums are
+// combined in group order through shared memory (deterministic).  cols/8 > kRowThreads: one group,
+// looping over column blocks.
 __global__ void __launch_bounds__(kRowThreads) colsum_bf16_kernel(const __nv_bfloat16* __restrict__ x,
                                                                   int64_t rows, int cols, int64_t ld,
                                                                   int64_t rows_per_block,
                                                                   float* __restrict__ part) {
+  __shared__ float4 red[kRowThreads][2];
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = min(rows, r0 + rows_per_block);
-  for (int c8 = threadIdx.x * 8; c8 < cols; c8 += kRowThreads * 8) {
+  const int cpt = cols / 8;
+  const int groups = cpt >= kRowThreads ? 1 : kRowThreads / cpt;
+  const int g = cpt >= kRowThreads ? 0 : threadIdx.x / cpt;
+  const int tcol = cpt >= kRowThreads ? threadIdx.x : threadIdx.x - g * cpt;
+  const bool live = g < groups;
+  for (int c8 = tcol * 8; c8 < cols; c8 += kRowThreads * 8) {
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int64_t r = r0;
-    for (; r + 4 <= r1; r += 4) {  // 4 independent 16-byte loads in flight, summed in row order
-      uint4 w[4];
+    if (live) {
+      int64_t r = r0 + g;
+      for (; r + 15 * groups < r1; r += 16 * groups) {
+        uint4 w[16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = *reinterpret_cast<const uint4*>(x + (r + q) * ld + c8);
+        for (int q = 0; q < 16; ++q) w[q] = __ldg(reinterpret_cast<const uint4*>(x + (r + q * groups) * ld + c8));
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float2 a = unpack_bf16(w[q].x), b = unpack_bf16(w[q].y), c = unpack_bf16(w[q].z), d = unpack_bf16(w[q].w);
+        for (int q = 0; q < 16; ++q) {
+          float2 a = unpack_bf16(w[q].x), b = unpack_bf16(w[q].y), c = unpack_bf16(w[q].z), d = unpack_bf16(w[q].w);
+          acc[0] += a.x; acc[1] += a.y; acc[2] += b.x; acc[3] += b.y;
+          acc[4] += c.x; acc[5] += c.y; acc[6] += d.x; acc[7] += d.y;
+        }
+      }
+      for (; r < r1; r += groups) {
+        uint4 w = __ldg(reinterpret_cast<const uint4*>(x + r * ld + c8));
+        float2 a = unpack_bf16(w.x), b = unpack_bf16(w.y), c = unpack_bf16(w.z), d = unpack_bf16(w.w);
         acc[0] += a.x; acc[1] += a.y; acc[2] += b.x; acc[3] += b.y;
         acc[4] += c.x; acc[5] += c.y; acc[6] += d.x; acc[7] += d.y;
       }
     }
-    for (; r < r1; ++r) {
-      uint4 w = *reinterpret_cast<const uint4*>(x + r * ld + c8);
-      float2 a = unpack_bf16(w.x), b = unpack_bf16(w.y), c = unpack_bf16(w.z), d = unpack_bf16(w.w);
-      acc[0] += a.x; acc[1] += a.y; acc[2] += b.x; acc[3] += b.y;
-      acc[4] += c.x; acc[5] += c.y; acc[6] += d.x; acc[7] += d.y;
+    if (groups > 1) {
+      red[threadIdx.x][0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      red[threadIdx.x][1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      __syncthreads();
+      if (g == 0) {
+        for (int g2 = 1; g2 < groups; ++g2) {
+          const float4 u = red[g2 * cpt + tcol][0], v = red[g2 * cpt + tcol][1];
+          acc[0] += u.x; acc[1] += u.y; acc[2] += u.z; acc[3] += u.w;
+          acc[4] += v.x; acc[5] += v.y; acc[6] += v.z; acc[7] += v.w;
+        }
+      }
     }
-    float* out = part + (int64_t)blockIdx.x * cols + c8;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) out[j] = acc[j];
+    if (g == 0) {
+      float4* out = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * cols + c8);
+      out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+    if (groups > 1) break;  // cpt < kRowThreads: every column is covered by the first pass
   }
 }
 
