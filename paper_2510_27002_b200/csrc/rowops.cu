@@ -246,16 +246,16 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < D; c0 += (int64_t)gridDim.x * 32) {
     const int64_t c = c0 + lane;
-    float s0 = 0.f, s1 = 0.f;
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 loads in flight, fixed order
     if (c < D) {
       int p = grp;
-      for (; p + 8 < nparts; p += 16) {
-        s0 += part[(int64_t)p * stride * D + c];
-        s1 += part[(int64_t)(p + 8) * stride * D + c];
+      for (; p + 56 < nparts; p += 64) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] += __ldg(part + (int64_t)(p + 8 * q) * stride * D + c);
       }
-      if (p < nparts) s0 += part[(int64_t)p * stride * D + c];
+      for (int q = 0; p < nparts; p += 8, ++q) s[q] += __ldg(part + (int64_t)p * stride * D + c);
     }
-    sm[grp][lane] = s0 + s1;
+    sm[grp][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     __syncthreads();
     if (grp == 0 && c < D) {
       float t = 0.f;
@@ -275,18 +275,16 @@ __global__ void __launch_bounds__(256) reduce_chunks_kernel(float* __restrict__ 
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   const int p0 = blockIdx.y * kChunkRows, p1 = min(nparts, p0 + kChunkRows);
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 loads in flight, fixed order
   if (c < D) {
     int p = p0 + grp;
-    for (; p + 24 < p1; p += 32) {
-      s0 += part[(int64_t)p * D + c];
-      s1 += part[(int64_t)(p + 8) * D + c];
-      s2 += part[(int64_t)(p + 16) * D + c];
-      s3 += part[(int64_t)(p + 24) * D + c];
+    for (; p + 56 < p1; p += 64) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[q] += part[(int64_t)(p + 8 * q) * D + c];
     }
-    for (; p < p1; p += 8) s0 += part[(int64_t)p * D + c];
+    for (int q = 0; p < p1; p += 8, ++q) s[q] += part[(int64_t)p * D + c];
   }
-  sm[grp][lane] = (s0 + s1) + (s2 + s3);
+  sm[grp][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
   __syncthreads();
   if (grp == 0 && c < D) {
     float t = 0.f;
