@@ -216,3 +216,84 @@ def test_attn_temporal_fwd_bwd(T):
             assert float(got.norm()) < 1e-3 * scale, "qkv"[i]
         else:
             assert rel(got, ref) < 2e-2, "qkv"[i]
+
+
+# ---------------------------------------------------------------------------------------------
+# column sums / partial-row reductions (bias and LayerNorm parameter gradients): every thread
+# layout the kernels pick (row groups for cols/8 < 256, a column loop above), ragged row counts,
+# padded leading dimensions, the two-stage path above 512 partials; deterministic run to run.
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("rows,cols,ld", [(1, 8, 8), (5, 64, 72), (296 * 3 + 7, 512, 1536), (5000, 1536, 1536),
+                                          (777, 2056, 2064), (40000, 512, 3 * 512)])
+def test_colsum_bf16_layouts(rows, cols, ld):
+    g = torch.Generator(device=dev).manual_seed(rows + cols)
+    x = torch.randn(rows, ld, device=dev, generator=g).bfloat16()
+    out = torch.full((cols,), float("nan"), device=dev)
+    Kn.colsum_bf16(x, out, cols=cols)
+    ref = x[:, :cols].double().sum(0)
+    assert float((out.double() - ref).abs().max()) <= 1e-5 * max(1.0, float(ref.abs().max())) + 1e-4
+    again = torch.empty_like(out)
+    Kn.colsum_bf16(x, again, cols=cols)
+    assert torch.equal(out, again)
+
+
+@pytest.mark.parametrize("nparts", [1, 7, 63, 64, 65, 296, 513, 1100, 9252])
+@pytest.mark.parametrize("D", [1, 33, 512])
+def test_reduce_partials(nparts, D):
+    g = torch.Generator(device=dev).manual_seed(nparts * 7 + D)
+    part = torch.randn(nparts, D, device=dev, generator=g)
+    ref = part.double().sum(0)
+    base = torch.randn(D, device=dev, generator=g)
+    for acc in (False, True):
+        out = base.clone()
+        Kn.reduce_partials(part.clone(), nparts, D, out, accumulate=acc)  # two-stage path overwrites its input
+        want = ref + (base.double() if acc else 0.0)
+        assert float((out.double() - want).abs().max()) < 1e-5 * math.sqrt(nparts) + 1e-6
+        again = base.clone()
+        Kn.reduce_partials(part.clone(), nparts, D, again, accumulate=acc)
+        assert torch.equal(out, again)
+
+
+# ---------------------------------------------------------------------------------------------
+# dynamics input embedding (K5 forward): both conditioning modes, masked positions, latent widths
+# above one warp (dl > 32 takes the second shuffle register), and the bad-token error flag.
+# ---------------------------------------------------------------------------------------------
+def _embed_ref(tokens, mask, lat, P, B, T, N, D, dl, prepend):
+    E, mt = P["token_embed"].double(), P["mask_token"].double()
+    sel = E[tokens.long()]
+    if mask is not None:
+        sel = torch.where(mask.bool()[..., None], mt.expand_as(sel), sel)
+    cond = torch.cat([P["null_action"].double().expand(B, 1, dl), lat.double()], 1)  # (B, T, dl)
+    act = cond @ P["action_proj.w"].double() + P["action_proj.b"].double()        # (B, T, D)
+    if prepend:
+        x = torch.cat([act[:, :, None], sel], 2)
+    else:
+        x = sel + act[:, :, None]
+    S = x.shape[2]
+    return x + P["pos_spatial"].double()[:S] + P["pos_temporal"].double()[:T, None]
+
+
+@pytest.mark.parametrize("prepend", [True, False])
+@pytest.mark.parametrize("D,dl", [(512, 32), (256, 48), (96, 7)])
+def test_dyn_embed_fwd_modes(prepend, D, dl):
+    B, T, N, K = 3, 5, 19, 37
+    g = torch.Generator(device=dev).manual_seed(D + dl + prepend)
+    P = {"token_embed": torch.randn(K, D, device=dev, generator=g),
+         "mask_token": torch.randn(D, device=dev, generator=g),
+         "null_action": torch.randn(dl, device=dev, generator=g),
+         "action_proj.w": torch.randn(dl, D, device=dev, generator=g),
+         "action_proj.b": torch.randn(D, device=dev, generator=g),
+         "pos_spatial": torch.randn(N + 1, D, device=dev, generator=g),
+         "pos_temporal": torch.randn(T, D, device=dev, generator=g)}
+    tokens = torch.randint(0, K, (B, T, N), device=dev, generator=g)
+    mask = (torch.rand(B, T, N, device=dev, generator=g) < 0.3).to(torch.uint8)
+    lat = torch.randn(B, T - 1, dl, device=dev, generator=g)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    x = Kn.dyn_embed_fwd(tokens, mask, lat, P, B=B, T=T, N=N, D=D, dl=dl, K=K, prepend=prepend, err=err)
+    S = N + (1 if prepend else 0)
+    ref = _embed_ref(tokens, mask, lat, P, B, T, N, D, dl, prepend).reshape(B * T * S, D)
+    assert float((x.double() - ref).abs().max()) < 1e-4 * max(1.0, math.sqrt(dl))
+    assert int(err.item()) == 0
+    tokens[1, 2, 3] = K  # out of range: flagged (and read as token 0), never an out-of-bounds read
+    Kn.dyn_embed_fwd(tokens, None, lat, P, B=B, T=T, N=N, D=D, dl=dl, K=K, prepend=prepend, err=err)
+    assert int(err.item()) == 1
