@@ -71,7 +71,11 @@ enum {
   JZ_EPI_GELU = 3,      /* D bf16 = gelu(acc + bias); D2 bf16 = acc + bias (D2 may be NULL) */
   JZ_EPI_GELU_BWD = 4,  /* D bf16 = acc * gelu'(aux_bf16)                          */
   JZ_EPI_F32_ACC = 5,   /* D f32 += acc                                           */
-  JZ_EPI_BF16_F32 = 6   /* D f32 = acc (+bias); D2 bf16 copy                       */
+  JZ_EPI_BF16_F32 = 6,  /* D f32 = acc (+bias); D2 bf16 copy                       */
+  /* value 7 is reserved (no-store timing probe) */
+  JZ_EPI_GELU_DG = 8,   /* D bf16 = gelu(acc + bias); D2 f16 = gelu'(acc + bias) (D2 required):
+                           the training forward saves the GELU derivative, not the pre-activation */
+  JZ_EPI_MUL_F16 = 9    /* D bf16 = acc * aux_f16 (the backward of JZ_EPI_GELU_DG: aux = its D2) */
 };
 
 /* Workspace bytes needed for a split-K GEMM (0 when split_k <= 1). */

@@ -19,6 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libjz.so"
 JZ_OK, JZ_EINVAL, JZ_EINDEX, JZ_ECUDA, JZ_EUNSUPPORTED, JZ_ENONFINITE = 0, -1, -2, -3, -4, -5
 
 EPI_F32, EPI_BF16, EPI_RESID, EPI_GELU, EPI_GELU_BWD, EPI_F32_ACC, EPI_BF16_F32 = range(7)
+EPI_GELU_DG, EPI_MUL_F16 = 8, 9
 
 _P, _I64, _I32, _F32, _F64, _U64 = C.c_void_p, C.c_int64, C.c_int, C.c_float, C.c_double, C.c_uint64
 

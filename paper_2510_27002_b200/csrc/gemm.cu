@@ -146,6 +146,30 @@ JZ_DEV float2 gelu_grad_pair(uint32_t pre_bf16x2) {
   return __half22float2(__hadd2(a, b));
 }
 
+// gelu(x) (fp32, written as bf16) and gelu'(x) (f16x2, saved for the backward) of two packed
+// values from one f16x2 tanh: the backward epilogue then only multiplies (JZ_EPI_MUL_F16).
+// tanh.approx.f16x2 has ~2^-11 absolute error, the accuracy of the fp32 tanh.approx it shares.
+JZ_DEV uint32_t gelu_and_grad_pair(float& x0, float& x1) {
+  __half2 x = __floats2half2_rn(x0, x1);
+  x = __hmax2(__hmin2(x, __float2half2_rn(10.0f)), __float2half2_rn(-10.0f));
+  const float c = 0.7978845608028654f;
+  const __half2 x2 = __hmul2(x, x);
+  const __half2 inner = __hmul2(x, __hfma2(x2, __float2half2_rn(c * 0.044715f), __float2half2_rn(c)));
+  __half2 t;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(*reinterpret_cast<uint32_t*>(&t)) : "r"(*reinterpret_cast<const uint32_t*>(&inner)));
+  const __half2 half = __float2half2_rn(0.5f);
+  const __half2 a = __hfma2(t, half, half);                                   // 0.5 (1 + t)
+  const __half2 omt = __hfma2(__hneg2(t), t, __float2half2_rn(1.0f));         // 1 - t^2
+  const __half2 poly = __hfma2(x2, __float2half2_rn(0.5f * c * 0.134145f), __float2half2_rn(0.5f * c));
+  const __half2 g = __hfma2(__hmul2(x, poly), omt, a);                        // gelu'(x)
+  const float2 af = __half22float2(a);
+  x0 *= af.x;  // gelu = x * 0.5 (1 + t), on the unclamped fp32 value
+  x1 *= af.y;
+  return *reinterpret_cast<const uint32_t*>(&g);
+}
+
+JZ_DEV float2 unpack_f16(uint32_t w) { return __half22float2(*reinterpret_cast<const __half2*>(&w)); }
+
 JZ_DEV float gelu_grad_fast(float x) {
   const float c = 0.7978845608028654f;
   float x2 = x * x;
@@ -227,8 +251,22 @@ JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], fl
     }
     case JZ_EPI_BF16:
     case JZ_EPI_GELU:
-    case JZ_EPI_GELU_BWD: {
-      if (p.epi == JZ_EPI_GELU && p.D2 == nullptr) {
+    case JZ_EPI_GELU_BWD:
+    case JZ_EPI_GELU_DG:
+    case JZ_EPI_MUL_F16: {
+      if (p.epi == JZ_EPI_GELU_DG) {
+        __half* d2 = reinterpret_cast<__half*>(p.D2) + (int64_t)m * p.ldd2 + n;
+        for (int j = 0; j < 32; j += 2) {
+          const uint32_t g = gelu_and_grad_pair(v[j], v[j + 1]);
+          const float2 gf = unpack_f16(g);
+          if (n + j < N) d2[j] = __float2half_rn(gf.x);
+          if (n + j + 1 < N) d2[j + 1] = __float2half_rn(gf.y);
+        }
+      } else if (p.epi == JZ_EPI_MUL_F16) {
+        const __half* g = reinterpret_cast<const __half*>(p.aux) + (int64_t)m * p.ldaux + n;
+        for (int j = 0; j < 32; ++j)
+          if (n + j < N) v[j] *= __half2float(g[j]);
+      } else if (p.epi == JZ_EPI_GELU && p.D2 == nullptr) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
       } else if (p.epi == JZ_EPI_GELU) {
@@ -321,7 +359,9 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
     if (p.tma_epi) {
       if (p.store_tma) tma_prefetch_desc(&em.d);
       if (p.store_tma && p.epi == JZ_EPI_GELU && p.D2 != nullptr) tma_prefetch_desc(&em.d2);
-      if (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD) tma_prefetch_desc(&em.aux);
+      if (p.epi == JZ_EPI_GELU_DG && p.store_tma) tma_prefetch_desc(&em.d2);
+      if (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD || p.epi == JZ_EPI_MUL_F16)
+        tma_prefetch_desc(&em.aux);
     }
   }
   if (warp == 1 && lane == 0) {
@@ -477,7 +517,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
         // ---------- staged TMA epilogue ----------
         const bool f32out = p.splits > 1 || p.epi == JZ_EPI_F32 || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_RESID;
         const bool need_aux = p.splits == 1 &&
-                              (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD);
+                              (p.epi == JZ_EPI_RESID || p.epi == JZ_EPI_F32_ACC || p.epi == JZ_EPI_GELU_BWD ||
+                               p.epi == JZ_EPI_MUL_F16);
         const int CW = f32out ? 32 : 64;
         const int esz = f32out ? 4 : 2;
         // split-K partials: slab `split` of the fp32 workspace, row pitch N
@@ -530,7 +571,19 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
           if (need_aux) {
             mbar_wait(&aux_bar[ew], apar);
             apar ^= 1;
-            if (p.epi == JZ_EPI_GELU_BWD) {
+            if (p.epi == JZ_EPI_MUL_F16) {
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const uint4 w = *reinterpret_cast<const uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4));
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 gg = unpack_f16(ww[e]);  // gelu' saved by the forward (JZ_EPI_GELU_DG)
+                  v[8 * c + 2 * e] *= gg.x;
+                  v[8 * c + 2 * e + 1] *= gg.y;
+                }
+              }
+            } else if (p.epi == JZ_EPI_GELU_BWD) {
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
                 const uint4 w = *reinterpret_cast<const uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4));
@@ -560,6 +613,28 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
             if (p.epi == JZ_EPI_GELU && p.D2 == nullptr) {  // inference: gelu only
 #pragma unroll
               for (int j = 0; j < 64; ++j) v[j] = gelu_fast(v[j]);
+            } else if (p.epi == JZ_EPI_GELU_DG) {  // gelu' (f16) staged and stored first, gelu into D
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                uint32_t gw[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) gw[e] = gelu_and_grad_pair(v[8 * c + 2 * e], v[8 * c + 2 * e + 1]);
+                *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = make_uint4(gw[0], gw[1], gw[2], gw[3]);
+              }
+              if (p.store_tma) {
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&em.d2, stg, n, row0);
+                  bulk_commit();
+                  bulk_wait_read0();
+                }
+              } else {
+                __syncwarp();
+                stg_write_rows(stg, reinterpret_cast<uint8_t*>(p.D2) + ((int64_t)row0 * p.ldd2 + n) * 2,
+                               (int64_t)p.ldd2 * 2, rows_ok, cols_bytes, lane);
+              }
+              __syncwarp();
             } else if (p.epi == JZ_EPI_GELU) {  // pre-activation copy first (D2), then GELU into D
 #pragma unroll
               for (int c = 0; c < 8; ++c)
@@ -778,7 +853,8 @@ extern "C" int jz_gemm_bf16_colsum(const void* A, int64_t lda, int a_kmajor, con
                                    int epilogue, const float* bias, const void* aux, int64_t ldaux,
                                    void* D2, int64_t ldd2, float* colsum_part, jz_stream_t stream_) {
   JZ_CHECK_ARG(colsum_part != nullptr, "gemm colsum: null partial buffer");
-  JZ_CHECK_ARG(epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD,
+  JZ_CHECK_ARG(epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD ||
+                   epilogue == JZ_EPI_GELU_DG || epilogue == JZ_EPI_MUL_F16,
                "gemm colsum: bf16-output epilogues only (got %d)", epilogue);
   return gemm_impl(A, lda, a_kmajor, B, ldb, b_kmajor, D, ldd, M, N, K, epilogue, bias, aux, ldaux, D2, ldd2,
                    1, nullptr, colsum_part, stream_);
@@ -795,9 +871,10 @@ static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, in
   JZ_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "gemm: lda/ldb must be multiples of 8 (got %lld, %lld)",
                (long long)lda, (long long)ldb);
   JZ_CHECK_ARG(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0, "gemm: A/B must be 16B aligned");
-  JZ_CHECK_ARG(epilogue >= JZ_EPI_F32 && epilogue <= 7, "gemm: bad epilogue %d", epilogue);
+  JZ_CHECK_ARG(epilogue >= JZ_EPI_F32 && epilogue <= JZ_EPI_MUL_F16, "gemm: bad epilogue %d", epilogue);
   JZ_CHECK_ARG(D != nullptr, "gemm: null output");
-  if (epilogue == JZ_EPI_RESID || epilogue == JZ_EPI_GELU_BWD)
+  if (epilogue == JZ_EPI_GELU_DG) JZ_CHECK_ARG(D2 != nullptr, "gemm: epilogue %d needs D2", epilogue);
+  if (epilogue == JZ_EPI_RESID || epilogue == JZ_EPI_GELU_BWD || epilogue == JZ_EPI_MUL_F16)
     JZ_CHECK_ARG(aux != nullptr, "gemm: epilogue %d needs aux", epilogue);
   if (epilogue == JZ_EPI_BF16_F32) JZ_CHECK_ARG(D2 != nullptr, "gemm: epilogue %d needs D2", epilogue);
   if (split_k < 1) split_k = 1;
@@ -845,19 +922,21 @@ static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, in
   p.store_tma = 0;
   if (epilogue != 7) {
     const bool f32out = p.splits > 1 || epilogue == JZ_EPI_F32 || epilogue == JZ_EPI_F32_ACC || epilogue == JZ_EPI_RESID;
-    const bool bf16out = epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD;
+    const bool bf16out = epilogue == JZ_EPI_BF16 || epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_BWD ||
+                         epilogue == JZ_EPI_GELU_DG || epilogue == JZ_EPI_MUL_F16;
     // 32-column bf16 chunks (BN = 64) do not fill a 128-byte staging row.
     bool ok = (f32out || bf16out) && !(bf16out && BN == 64);
     auto al = [](const void* q) { return ((uintptr_t)q % 16) == 0; };
     if (ok && p.splits > 1) ok = al(ws) && N % 4 == 0;
     else if (ok && f32out) ok = al(D) && ldd % 4 == 0 && N % 4 == 0;
     else if (ok) ok = al(D) && ldd % 8 == 0 && N % 8 == 0;
-    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU && D2 != nullptr) ok = al(D2) && ldd2 % 8 == 0;
+    if (ok && p.splits == 1 && (epilogue == JZ_EPI_GELU || epilogue == JZ_EPI_GELU_DG) && D2 != nullptr)
+      ok = al(D2) && ldd2 % 8 == 0;
     if (ok && p.splits == 1 && epilogue == JZ_EPI_RESID)
       ok = al(aux) && ldaux % 4 == 0 && make_tmap_2d(&em.aux, aux, 4, N, M, ldaux, 32, 32) == JZ_OK;
     if (ok && p.splits == 1 && epilogue == JZ_EPI_F32_ACC)
       ok = make_tmap_2d(&em.aux, D, 4, N, M, ldd, 32, 32) == JZ_OK;
-    if (ok && p.splits == 1 && epilogue == JZ_EPI_GELU_BWD)
+    if (ok && p.splits == 1 && (epilogue == JZ_EPI_GELU_BWD || epilogue == JZ_EPI_MUL_F16))
       ok = al(aux) && ldaux % 8 == 0 && make_tmap_2d(&em.aux, aux, 2, N, M, ldaux, 64, 32) == JZ_OK;
     p.tma_epi = ok ? 1 : 0;
     // TMA bulk stores from the staging tiles (clip at M and N for free); split-K partial slabs
@@ -865,7 +944,7 @@ static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, in
     if (ok && p.splits == 1 && store_tma_enabled()) {
       const bool ok2 = f32out ? make_tmap_2d(&em.d, D, 4, N, M, ldd, 32, 32) == JZ_OK
                               : make_tmap_2d(&em.d, D, 2, N, M, ldd, 64, 32) == JZ_OK;
-      const bool ok3 = epilogue != JZ_EPI_GELU || D2 == nullptr ||
+      const bool ok3 = (epilogue != JZ_EPI_GELU && epilogue != JZ_EPI_GELU_DG) || D2 == nullptr ||
                        make_tmap_2d(&em.d2, D2, 2, N, M, ldd2, 64, 32) == JZ_OK;
       p.store_tma = ok2 && ok3 ? 1 : 0;
     }

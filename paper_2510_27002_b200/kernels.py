@@ -148,7 +148,7 @@ def linear_fwd(x_bf16: torch.Tensor, w_bf16: torch.Tensor, bias: torch.Tensor | 
     M, K = x_bf16.shape
     N = w_bf16.shape[1]
     if out is None:
-        dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU, L.EPI_GELU_BWD) else F32
+        dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU, L.EPI_GELU_BWD, L.EPI_GELU_DG, L.EPI_MUL_F16) else F32
         out = torch.empty(M, N, dtype=dt, device=x_bf16.device)
     return gemm(x_bf16, w_bf16, M=M, N=N, K=K, a_kmajor=True, b_kmajor=False, out=out, epilogue=epilogue,
                 bias=bias, aux=aux, out2=out2)
@@ -160,7 +160,7 @@ def linear_dx(dy_bf16: torch.Tensor, w_bf16: torch.Tensor, *, epilogue=L.EPI_F32
     M, N = dy_bf16.shape
     K_in = w_bf16.shape[0]
     if out is None:
-        dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU_BWD) else F32
+        dt = BF16 if epilogue in (L.EPI_BF16, L.EPI_GELU_BWD, L.EPI_MUL_F16) else F32
         out = torch.empty(M, K_in, dtype=dt, device=dy_bf16.device)
     return gemm(dy_bf16, w_bf16, M=M, N=K_in, K=N, a_kmajor=True, b_kmajor=True, out=out, epilogue=epilogue,
                 aux=aux, out2=out2, ldb=w_bf16.stride(0), colsum=colsum)

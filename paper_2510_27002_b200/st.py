@@ -174,9 +174,11 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
         x2 = K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=L.EPI_RESID, aux=x1)
         # FFN (st.py:77-79)
         xn3, m3, r3 = K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
-        # the pre-activation is kept (bf16) for gelu' in the backward epilogue; inference skips it
-        hpre = torch.empty(xn3.shape[0], cfg.ffn_dim, dtype=K.BF16, device=x.device) if save else None
-        h = K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=L.EPI_GELU, out2=hpre)
+        # training saves gelu'(pre-activation) (f16) from the same tanh, so the backward epilogue
+        # only multiplies; inference skips it
+        hpre = torch.empty(xn3.shape[0], cfg.ffn_dim, dtype=torch.float16, device=x.device) if save else None
+        h = K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data,
+                         epilogue=L.EPI_GELU_DG if save else L.EPI_GELU, out2=hpre)
         x3 = K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=L.EPI_RESID, aux=x2)
         if save:
             c.update(xn=xn, m1=m1, r1=r1, qkv=qkv, ao=ao, ao32=ao32, lse_s=lse_s, x1=x1, xn2=xn2, m2=m2, r2=r2, qkv2=qkv2,
@@ -233,7 +235,7 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         w = ctx["shadows"][i]
         # ---- FFN: x3 = x2 + gelu(LN(x2) Wup + bup) Wdown + bdown
         K.linear_dw(c["h"], dres_b, G[f"{base}.ffn.down.w"])
-        K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_GELU_BWD, out=dh, aux=c["hpre"],
+        K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_MUL_F16, out=dh, aux=c["hpre"],
                     colsum=G[f"{base}.ffn.up.b"])  # up-bias gradient from the epilogue's column sums
         K.linear_dw(c["xn3"], dh, G[f"{base}.ffn.up.w"])
         K.linear_dx(dh, w["ffn.wup"], epilogue=L.EPI_BF16, out=dtmp)

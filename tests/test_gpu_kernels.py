@@ -98,6 +98,33 @@ def test_gemm_epilogues(M):
     assert rel(gb, xp.grad) < 5e-3
 
 
+@pytest.mark.parametrize("M,N", [(1000, 512), (4096 + 77, 2048), (300, 48)])
+def test_gemm_gelu_dg_and_mul_epilogues(M, N):
+    """GELU_DG: D = gelu(acc + b) bf16 and D2 = gelu'(acc + b) f16 (the training forward);
+    MUL_F16: D = acc * aux_f16 (its backward). N = 48 runs the direct (unstaged) epilogue."""
+    K = 256
+    X, W, A, B = _operands(M, N, K, 1, 0, 7 * M + N)
+    # pre-activation 0.25 acc + b (std ~4 plus a +-12 ramp: both clamp sides and the centre)
+    A4 = (A.float() * 0.25).bfloat16()  # exact: power-of-two scale
+    bias = torch.linspace(-12, 12, N, device=dev)
+    pre = (X.float() * 0.25) @ W.float() + bias
+    g = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    dg = torch.empty(M, N, device=dev, dtype=torch.float16)
+    Kn.gemm(A4, B, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=g, epilogue=L.EPI_GELU_DG, bias=bias, out2=dg)
+    xp = pre.clone().requires_grad_(True)
+    y = torch.nn.functional.gelu(xp, approximate="tanh")
+    y.backward(torch.ones_like(y))
+    assert rel(g, y.detach()) < 5e-3
+    assert rel(dg, xp.grad) < 4e-3  # f16 tanh.approx: ~2^-11 absolute
+    assert (dg.float() - xp.grad).abs().max() < 1.5e-2  # 1 - t^2 from a tanh.approx t near +-1
+    # MUL_F16 with the saved derivative: D = acc2 * gelu'
+    X2, W2, A2, B2 = _operands(M, N, K, 1, 0, 11 * M + N)
+    acc2 = X2.float() @ W2.float()
+    gb = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    Kn.gemm(A2, B2, M=M, N=N, K=K, a_kmajor=1, b_kmajor=0, out=gb, epilogue=L.EPI_MUL_F16, aux=dg)
+    assert rel(gb, acc2 * dg.float()) < 4e-3
+
+
 @pytest.mark.parametrize("M,N", [(4096 + 77, 2048), (1000, 512), (96, 1536)])
 def test_gemm_colsum_epilogue(M, N):
     """Column sums of the bf16 output (bias gradient of the consumer) from the epilogue partials."""
