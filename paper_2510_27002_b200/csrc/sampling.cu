@@ -183,6 +183,124 @@ __global__ void temporal_decode_kernel(const __nv_bfloat16* __restrict__ qkv, __
   }
 }
 
+// Same attention with 16-byte coalesced row accesses (D = 256 NV): lane l owns the 8-dim vectors
+// at dims [256 v + 8 l, +8) for v < NV, i.e. one 64-dim head slice per vector (head 4 v + l / 8),
+// reduced over 8 lanes.  Every warp-wide load instruction reads 512 contiguous bytes of a K or V row
+// (the DPL kernel's 8-byte lane accesses at a 32-byte stride touched each sector 4 times).
+template <int NV>
+__global__ void __launch_bounds__(128, 4) temporal_decode_v_kernel(
+    const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ cache, int64_t B, int t,
+    const int* __restrict__ dev_t, int Tmax, int S, int append, __nv_bfloat16* __restrict__ out) {
+  constexpr int D = 256 * NV;
+  constexpr int RV = D / 8;  // 16-byte vectors per D-wide row
+  if (dev_t) t = *dev_t;
+  const int64_t bs = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (bs >= B * S) return;
+  const int s = (int)(bs % S);
+  const int64_t b = bs / S;
+  const uint4* row = reinterpret_cast<const uint4*>(qkv + bs * 3 * D) + lane;
+  float q[NV][8];
+  uint4 kc[NV], vc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const uint4 w = row[v * 32];
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = unpack_bf16(ww[e]);
+      q[v][2 * e] = f.x;
+      q[v][2 * e + 1] = f.y;
+    }
+    kc[v] = row[RV + v * 32];
+    vc[v] = row[2 * RV + v * 32];
+  }
+  const uint4* base = reinterpret_cast<const uint4*>(cache + ((b * Tmax) * S + s) * 2 * D) + lane;
+  const int64_t tstride = (int64_t)S * 2 * RV;  // uint4 per cached frame
+  float m[NV], l[NV], o[NV][8];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    m[v] = -INFINITY;
+    l[v] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[v][i] = 0.f;
+  }
+#pragma unroll
+  for (int c0 = 0; c0 < 16; c0 += 4) {
+    if (c0 > t) break;  // warp-uniform
+    uint4 kk[4][NV], vv[4][NV];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int tau = c0 + j;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (tau < t) {
+          kk[j][v] = base[tau * tstride + v * 32];
+          vv[j][v] = base[tau * tstride + RV + v * 32];
+        } else if (tau == t) {
+          kk[j][v] = kc[v];
+          vv[j][v] = vc[v];
+        } else {
+          kk[j][v] = make_uint4(0, 0, 0, 0);
+          vv[j][v] = make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float sc[4];
+      float cm = m[v];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t ww[4] = {kk[j][v].x, kk[j][v].y, kk[j][v].z, kk[j][v].w};
+        float a = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 kf = unpack_bf16(ww[e]);
+          a += q[v][2 * e] * kf.x + q[v][2 * e + 1] * kf.y;
+        }
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 4);
+        sc[j] = (c0 + j) <= t ? a * 0.125f : -INFINITY;
+        cm = fmaxf(cm, sc[j]);
+      }
+      const float corr = __expf(m[v] - cm);  // 0 on the first chunk (m = -inf)
+      l[v] *= corr;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[v][i] *= corr;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float pj = __expf(sc[j] - cm);
+        l[v] += pj;
+        const uint32_t ww[4] = {vv[j][v].x, vv[j][v].y, vv[j][v].z, vv[j][v].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 vf = unpack_bf16(ww[e]);
+          o[v][2 * e] += pj * vf.x;
+          o[v][2 * e + 1] += pj * vf.y;
+        }
+      }
+      m[v] = cm;
+    }
+  }
+  uint4* orow = reinterpret_cast<uint4*>(out + bs * D) + lane;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const float r = 1.0f / l[v];
+    orow[v * 32] = make_uint4(pack_bf16(o[v][0] * r, o[v][1] * r), pack_bf16(o[v][2] * r, o[v][3] * r),
+                              pack_bf16(o[v][4] * r, o[v][5] * r), pack_bf16(o[v][6] * r, o[v][7] * r));
+  }
+  if (append) {
+    uint4* cw = reinterpret_cast<uint4*>(cache + ((b * Tmax + t) * S + s) * 2 * D) + lane;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      cw[v * 32] = kc[v];
+      cw[RV + v * 32] = vc[v];
+    }
+  }
+}
+
 // cache[b, t0 + tau, s, :] = (k | v) of qkv rows (b, tau, s) for tau < T
 __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ cache, int64_t B,
                                int T, int t0, int Tmax, int S, int D) {
@@ -206,33 +324,16 @@ __global__ void kv_fill_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloa
 // u = draw (draw_base + b*N + n) of the Philox state, confidence; then the
 // known/cur/conf update.  One warp per row; lane owns K/32 consecutive codes.
 // ---------------------------------------------------------------------------
-template <int PER>  // codes per lane
-__global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t rows, int K, float inv_temp,
-                                      int greedy, PhiloxState st, uint64_t draw_base,
-                                      const int64_t* __restrict__ dev_params, int64_t* __restrict__ cur,
-                                      const uint8_t* __restrict__ known, float* __restrict__ conf) {
-  if (dev_params) {
-    draw_base = (uint64_t)dev_params[0];
-    if (dev_params[12] >= 0) {  // Philox state from device memory
-      for (int i = 0; i < 4; ++i) {
-        st.ctr[i] = (uint64_t)dev_params[2 + i];
-        st.buf[i] = (uint64_t)dev_params[8 + i];
-      }
-      st.key[0] = (uint64_t)dev_params[6];
-      st.key[1] = (uint64_t)dev_params[7];
-      st.pos = (int)dev_params[12];
-    }
-  }
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float* lr = logits + r * K + lane * PER;
-  float v[PER];
+// Per-row sampler math on the lane's PER consecutive logits v (scaled in place).
+template <int PER>
+JZ_DEV void sample_row(float (&v)[PER], int64_t r, int lane, int K, float inv_temp, int greedy,
+                       const PhiloxState& st, uint64_t draw_base, int64_t* __restrict__ cur,
+                       const uint8_t* __restrict__ known, float* __restrict__ conf) {
   float mx = -INFINITY, amax_v = -INFINITY;
   int amax_i = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const float raw = lr[i];
+    const float raw = v[i];
     v[i] = __fmul_rn(raw, inv_temp);
     mx = fmaxf(mx, v[i]);
     if (raw > amax_v) { amax_v = raw; amax_i = lane * PER + i; }
@@ -291,6 +392,88 @@ __global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t 
   }
 }
 
+JZ_DEV void load_sampler_params(const int64_t* __restrict__ dev_params, PhiloxState& st, uint64_t& draw_base) {
+  if (dev_params) {
+    draw_base = (uint64_t)dev_params[0];
+    if (dev_params[12] >= 0) {  // Philox state from device memory
+      for (int i = 0; i < 4; ++i) {
+        st.ctr[i] = (uint64_t)dev_params[2 + i];
+        st.buf[i] = (uint64_t)dev_params[8 + i];
+      }
+      st.key[0] = (uint64_t)dev_params[6];
+      st.key[1] = (uint64_t)dev_params[7];
+      st.pos = (int)dev_params[12];
+    }
+  }
+}
+
+template <int PER>  // codes per lane
+__global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t rows, int K, float inv_temp,
+                                      int greedy, PhiloxState st, uint64_t draw_base,
+                                      const int64_t* __restrict__ dev_params, int64_t* __restrict__ cur,
+                                      const uint8_t* __restrict__ known, float* __restrict__ conf) {
+  load_sampler_params(dev_params, st, draw_base);
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* lr = logits + r * K + lane * PER;
+  float v[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) v[i] = lr[i];
+  sample_row<PER>(v, r, lane, K, inv_temp, greedy, st, draw_base, cur, known, conf);
+}
+
+// Pipelined variant (K = 32 PER, PER % 4 == 0): each warp walks rows r, r + nwarps, ... and
+// streams row r + nwarps into its second shared-memory buffer (cp.async, 512 contiguous bytes
+// per instruction) while it samples row r.  Buffers hold 16-byte units u at u ^ ((u >> 3) & 7),
+// so the lane-contiguous reads (lane l: units l PER/4 ..) are conflict-free.
+constexpr int kSampleWarps = 4;
+template <int PER>
+__global__ void __launch_bounds__(32 * kSampleWarps) maskgit_sample_pipe_kernel(
+    const float* __restrict__ logits, int64_t rows, int K, float inv_temp, int greedy, PhiloxState st,
+    uint64_t draw_base, const int64_t* __restrict__ dev_params, int64_t* __restrict__ cur,
+    const uint8_t* __restrict__ known, float* __restrict__ conf) {
+  constexpr int U = 8 * PER;  // 16-byte units per row
+  extern __shared__ uint4 sbuf[];
+  load_sampler_params(dev_params, st, draw_base);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint4* const buf = sbuf + w * 2 * U;
+  const int64_t nw = (int64_t)gridDim.x * kSampleWarps;
+  auto issue = [&](int64_t row, uint4* dst) {
+    const uint4* src = reinterpret_cast<const uint4*>(logits + row * K);
+#pragma unroll
+    for (int j = 0; j < PER / 4; ++j) {
+      const int u = j * 32 + lane;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + (u ^ ((u >> 3) & 7)))),
+                   "l"(src + u) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t r = (int64_t)blockIdx.x * kSampleWarps + w;
+  if (r < rows) issue(r, buf);
+  for (int b = 0; r < rows; r += nw, b ^= 1) {
+    const int64_t rn = r + nw;
+    if (rn < rows) {
+      issue(rn, buf + (b ^ 1) * U);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const uint4* cb = buf + b * U;
+    float v[PER];
+#pragma unroll
+    for (int i = 0; i < PER / 4; ++i) {
+      const int u = lane * (PER / 4) + i;
+      const float4 f = *reinterpret_cast<const float4*>(cb + (u ^ ((u >> 3) & 7)));
+      v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+    }
+    __syncwarp();  // the buffer is refilled by the next iteration's prefetch
+    sample_row<PER>(v, r, lane, K, inv_temp, greedy, st, draw_base, cur, known, conf);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K11b: per batch row, the n_keep highest-confidence positions (ties by position) become known.
 __global__ void maskgit_select_kernel(const float* __restrict__ conf, int N, int n_keep,
                                       const int64_t* __restrict__ dev_params, uint8_t* __restrict__ known) {
@@ -342,9 +525,9 @@ extern "C" int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, 
   auto o = reinterpret_cast<__nv_bfloat16*>(out);
   switch (D) {
     case 128: temporal_decode_kernel<4><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
-    case 256: temporal_decode_kernel<8><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
-    case 512: temporal_decode_kernel<16><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
-    default: temporal_decode_kernel<32><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 256: temporal_decode_v_kernel<1><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    case 512: temporal_decode_v_kernel<2><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    default: temporal_decode_v_kernel<4><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
   }
   JZ_LAUNCH_CHECK();
   return JZ_OK;
@@ -382,10 +565,18 @@ extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, flo
   const float inv_temp = 1.0f / fmaxf(temperature, 1e-8f);
   const int64_t rows = B * N;
   const unsigned grid = (unsigned)((rows + 7) / 8);
+  if (rows == 0) return JZ_OK;
+  // pipelined kernel: one resident wave (4 CTAs of 4 warps per SM at 128 registers), each warp
+  // walking several rows
+  int64_t pgrid = (rows + kSampleWarps - 1) / kSampleWarps;
+  if (pgrid > (int64_t)num_sms() * 4) pgrid = (int64_t)num_sms() * 4;
+  const size_t psmem = (size_t)kSampleWarps * 2 * K * sizeof(float);
   switch (K / 32) {
 #define MS(P) case P: maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf); break;
-    MS(1) MS(2) MS(4) MS(8) MS(16) MS(32) MS(64)
+#define MP(P) case P: maskgit_sample_pipe_kernel<P><<<(unsigned)pgrid, 32 * kSampleWarps, psmem, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf); break;
+    MS(1) MS(2) MP(4) MP(8) MP(16) MP(32) MS(64)
 #undef MS
+#undef MP
     default: set_error("maskgit: vocabulary %d unsupported", K); return JZ_EINVAL;
   }
   JZ_LAUNCH_CHECK();

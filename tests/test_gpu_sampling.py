@@ -138,3 +138,37 @@ def test_rollout_through_real_tokenizer():
     np.testing.assert_array_equal(out, again)
     with pytest.raises(ValueError):
         rollout(tok, dyn, frames, actions[:1], horizon=2)
+
+
+@pytest.mark.parametrize("D", [128, 256, 512, 1024])
+@pytest.mark.parametrize("t", [0, 1, 5, 15])
+def test_temporal_decode_kernel_vs_torch(D, t):
+    """jz_attn_temporal_decode (K12 cached temporal attention of frame t) against a torch fp32
+    softmax over cache[:, :t] + the frame's own k/v, per head; append writes k|v into cache[:, t]."""
+    from paper_2510_27002_b200 import _lib as L
+    B, S, Tmax, H = 3, 257, 16, D // 64
+    g = torch.Generator(device="cuda").manual_seed(D + t)
+    qkv = torch.randn(B * S, 3 * D, device="cuda", generator=g).bfloat16()
+    cache = torch.randn(B, Tmax, S, 2 * D, device="cuda", generator=g).bfloat16()
+    ref_cache = cache.clone()
+    out = torch.empty(B * S, D, device="cuda", dtype=torch.bfloat16)
+    dev_t = torch.tensor(t, dtype=torch.int32, device="cuda")
+    L.call("jz_attn_temporal_decode", qkv.data_ptr(), cache.data_ptr(), B, 0, dev_t.data_ptr(), Tmax, S, H, 1,
+           out.data_ptr(), L.stream_ptr())
+    q, k, v = qkv.float().view(B, S, 3, H, 64).unbind(2)
+    ck = ref_cache[:, :t, :, :D].float().view(B, t, S, H, 64).permute(0, 2, 1, 3, 4)  # (B,S,t,H,64)
+    cv = ref_cache[:, :t, :, D:].float().view(B, t, S, H, 64).permute(0, 2, 1, 3, 4)
+    keys = torch.cat([ck, k.unsqueeze(2)], 2)
+    vals = torch.cat([cv, v.unsqueeze(2)], 2)
+    sc = torch.einsum("bshd,bsthd->bsht", q, keys) / 8.0
+    ref = torch.einsum("bsht,bsthd->bshd", sc.softmax(-1), vals).reshape(B * S, D)
+    assert float((out.float() - ref).norm() / ref.norm()) < 8e-3
+    assert torch.equal(cache[:, t], qkv.view(B, S, 3 * D)[:, :, D:])
+    assert torch.equal(cache[:, :t], ref_cache[:, :t])
+    # host frame index, no append: same output
+    out2 = torch.empty_like(out)
+    cache2 = ref_cache.clone()
+    L.call("jz_attn_temporal_decode", qkv.data_ptr(), cache2.data_ptr(), B, t, None, Tmax, S, H, 0,
+           out2.data_ptr(), L.stream_ptr())
+    assert torch.equal(out2, out)
+    assert torch.equal(cache2, ref_cache)
