@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
             tma_load_2d(stg, &em.aux, &aux_bar[ew], n, row0);
           }
           float v[64];
+          bool gelu_dg_staged = false;
           PH_T(t_b);
           {
             uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -553,7 +554,25 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
           }
           PH_ADD(1, t_b);
           PH_T(t_c);
-          if (bias_vec) {
+          if (bias_vec && n + CW <= p.N) {
+            // full chunk: every bias vector load issued before the first add (no per-load predicate
+            // chain; the loads are L1 broadcasts)
+            const float4* b4p = reinterpret_cast<const float4*>(p.bias + n);
+#pragma unroll
+            for (int h = 0; h < 16; h += 8) {
+              float4 b4[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (4 * (h + j) < CW) b4[j] = __ldg(b4p + h + j);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (4 * (h + j) < CW) {
+                  float* vv = v + 4 * (h + j);
+                  vv[0] += b4[j].x; vv[1] += b4[j].y; vv[2] += b4[j].z; vv[3] += b4[j].w;
+                }
+              }
+            }
+          } else if (bias_vec) {
             const float4* b4p = reinterpret_cast<const float4*>(p.bias + n);
             const int nv = min(CW, p.N - n) >> 2;
 #pragma unroll
@@ -627,14 +646,24 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
                 if (lane == 0) {
                   tma_store_2d(&em.d2, stg, n, row0);
                   bulk_commit();
-                  bulk_wait_read0();
                 }
+                // pack GELU while the bulk store reads the staging tile
+                uint32_t pk[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(v[2 * c], v[2 * c + 1]);
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                  *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                      make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                gelu_dg_staged = true;
               } else {
                 __syncwarp();
                 stg_write_rows(stg, reinterpret_cast<uint8_t*>(p.D2) + ((int64_t)row0 * p.ldd2 + n) * 2,
                                (int64_t)p.ldd2 * 2, rows_ok, cols_bytes, lane);
+                __syncwarp();
               }
-              __syncwarp();
             } else if (p.epi == JZ_EPI_GELU) {  // pre-activation copy first (D2), then GELU into D
 #pragma unroll
               for (int c = 0; c < 8; ++c)
@@ -660,7 +689,9 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
               }
               __syncwarp();
             }
-            if (GDBG == 3) {
+            if (gelu_dg_staged) {
+              // already packed into the staging tile
+            } else if (GDBG == 3) {
               uint32_t x = 0;
 #pragma unroll
               for (int c = 0; c < 32; ++c) x ^= pack_bf16(v[2 * c], v[2 * c + 1]);

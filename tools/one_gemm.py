@@ -13,6 +13,7 @@ xn = torch.randn(M, d, device="cuda").bfloat16()
 res = torch.randn(M, d, device="cuda")
 hp = torch.randn(M, f, device="cuda").bfloat16()
 hh = torch.empty(M, f, device="cuda", dtype=torch.bfloat16)
+hd = torch.rand(M, f, device="cuda").half()
 w = (torch.randn(f, d, device="cuda") * 0.02).bfloat16()
 wup = (torch.randn(d, f, device="cuda") * 0.02).bfloat16()
 wo = (torch.randn(d, d, device="cuda") * 0.02).bfloat16()
@@ -22,6 +23,8 @@ xo = torch.empty(M, d, device="cuda")
 qkv = torch.empty(M, 3 * d, device="cuda", dtype=torch.bfloat16)
 fn = {
     "gelu_bwd": lambda: Kn.linear_dx(xn, w, epilogue=L.EPI_GELU_BWD, out=hh, aux=hp),
+    "gelu_dg": lambda: Kn.linear_fwd(xn, wup, bf_, epilogue=L.EPI_GELU_DG, out2=hd, out=hh),
+    "mul_f16": lambda: Kn.linear_dx(xn, w, epilogue=L.EPI_MUL_F16, out=hh, aux=hd),
     "gelu_d2": lambda: Kn.linear_fwd(xn, wup, bf_, epilogue=L.EPI_GELU, out2=hp, out=hh),
     "resid": lambda: Kn.linear_fwd(xn, wo, bd, epilogue=L.EPI_RESID, aux=res, out=xo),
     "qkv": lambda: Kn.linear_fwd(xn, wqkv, bq, out=qkv),
