@@ -19,44 +19,53 @@ namespace jz {
 //   s = 0 -> (cond[b] Wa + ba) + ps[0] + pt;  s >= 1 -> (known ? E[tok] : mt) + ps[s] + pt
 //   (known == NULL: every token known)
 // ---------------------------------------------------------------------------
-__global__ void embed_frame_kernel(const int64_t* __restrict__ tokens, const uint8_t* __restrict__ known,
-                                   const float* __restrict__ cond, const float* __restrict__ E,
-                                   const float* __restrict__ mt, const float* __restrict__ Wa,
-                                   const float* __restrict__ ba, const float* __restrict__ ps,
-                                   const float* __restrict__ pt_row, const int* __restrict__ dev_t, int N, int D,
-                                   int dl, int K, float* __restrict__ x) {
+// One warp per row (8 rows per 256-thread CTA, grid-stride): lane owns float4 columns
+// 4 lane + 128 i; the token id / known flag are read once per row by the whole warp.
+constexpr int kEmbedRowsPerCta = 8;
+__global__ void __launch_bounds__(32 * kEmbedRowsPerCta) embed_frame_kernel(
+    const int64_t* __restrict__ tokens, const uint8_t* __restrict__ known, const float* __restrict__ cond,
+    const float* __restrict__ E, const float* __restrict__ mt, const float* __restrict__ Wa,
+    const float* __restrict__ ba, const float* __restrict__ ps, const float* __restrict__ pt_row,
+    const int* __restrict__ dev_t, int64_t rows, int N, int D, int dl, int K, float* __restrict__ x) {
   const int S = N + 1;
   if (dev_t) pt_row += (int64_t)(*dev_t) * D;
-  const int64_t row = blockIdx.x;
-  const int s = (int)(row % S);
-  const int64_t b = row / S;
-  const int d = threadIdx.x * 4;
-  if (d >= D) return;
-  float4 v;
-  if (s == 0) {
-    float4 acc = make_float4(0, 0, 0, 0);
-    for (int i = 0; i < dl; ++i) {
-      const float c = cond[b * dl + i];
-      const float4 w = *reinterpret_cast<const float4*>(Wa + (int64_t)i * D + d);
-      acc.x += c * w.x; acc.y += c * w.y; acc.z += c * w.z; acc.w += c * w.w;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * kEmbedRowsPerCta;
+  for (int64_t row = (int64_t)blockIdx.x * kEmbedRowsPerCta + (threadIdx.x >> 5); row < rows; row += nw) {
+    const int s = (int)(row % S);
+    const int64_t b = row / S;
+    const float* src = nullptr;
+    if (s > 0) {
+      const int64_t pos = b * N + (s - 1);
+      if (known && !known[pos]) {
+        src = mt;
+      } else {
+        int64_t tok = tokens[pos];
+        tok = tok < 0 ? 0 : (tok >= K ? K - 1 : tok);
+        src = E + tok * D;
+      }
     }
-    const float4 bb = *reinterpret_cast<const float4*>(ba + d);
-    v = make_float4(acc.x + bb.x, acc.y + bb.y, acc.z + bb.z, acc.w + bb.w);
-  } else {
-    const int64_t pos = b * N + (s - 1);
-    if (known && !known[pos]) {
-      v = *reinterpret_cast<const float4*>(mt + d);
-    } else {
-      int64_t tok = tokens[pos];
-      tok = tok < 0 ? 0 : (tok >= K ? K - 1 : tok);
-      v = *reinterpret_cast<const float4*>(E + tok * D + d);
+    for (int d = 4 * lane; d < D; d += 128) {
+      float4 v;
+      if (s == 0) {
+        float4 acc = make_float4(0, 0, 0, 0);
+        for (int i = 0; i < dl; ++i) {
+          const float c = cond[b * dl + i];
+          const float4 w = *reinterpret_cast<const float4*>(Wa + (int64_t)i * D + d);
+          acc.x += c * w.x; acc.y += c * w.y; acc.z += c * w.z; acc.w += c * w.w;
+        }
+        const float4 bb = *reinterpret_cast<const float4*>(ba + d);
+        v = make_float4(acc.x + bb.x, acc.y + bb.y, acc.z + bb.z, acc.w + bb.w);
+      } else {
+        v = *reinterpret_cast<const float4*>(src + d);
+      }
+      const float4 p1 = *reinterpret_cast<const float4*>(ps + (int64_t)s * D + d);
+      const float4 p2 = *reinterpret_cast<const float4*>(pt_row + d);
+      v.x = (v.x + p1.x) + p2.x; v.y = (v.y + p1.y) + p2.y;
+      v.z = (v.z + p1.z) + p2.z; v.w = (v.w + p1.w) + p2.w;
+      *reinterpret_cast<float4*>(x + row * D + d) = v;
     }
   }
-  const float4 p1 = *reinterpret_cast<const float4*>(ps + (int64_t)s * D + d);
-  const float4 p2 = *reinterpret_cast<const float4*>(pt_row + d);
-  v.x = (v.x + p1.x) + p2.x; v.y = (v.y + p1.y) + p2.y;
-  v.z = (v.z + p1.z) + p2.z; v.w = (v.w + p1.w) + p2.w;
-  *reinterpret_cast<float4*>(x + row * D + d) = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -504,9 +513,12 @@ extern "C" int jz_dyn_embed_frame(const int64_t* tokens, const uint8_t* known, c
                                   jz_stream_t s) {
   JZ_CHECK_ARG(D % 4 == 0 && D / 4 <= 1024, "embed_frame: D=%d", D);
   if (B == 0) return JZ_OK;
-  embed_frame_kernel<<<(unsigned)(B * (N + 1)), D / 4, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      tokens, known, cond, token_embed, mask_token, action_w, action_b, pos_spatial, pos_temporal_row, dev_t, N, D, dl,
-      K, x);
+  const int64_t rows = B * (N + 1);
+  int64_t grid = (rows + kEmbedRowsPerCta - 1) / kEmbedRowsPerCta;
+  if (grid > (int64_t)num_sms() * 8) grid = (int64_t)num_sms() * 8;
+  embed_frame_kernel<<<(unsigned)grid, 32 * kEmbedRowsPerCta, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      tokens, known, cond, token_embed, mask_token, action_w, action_b, pos_spatial, pos_temporal_row, dev_t, rows, N,
+      D, dl, K, x);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
