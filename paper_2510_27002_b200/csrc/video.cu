@@ -7,6 +7,8 @@
 //   K15 recon MSE fwd/bwd                (nn.py:50-53, tokenizer.py:139, lam.py:125)
 //   small fp32 linear (CUDA cores) for the 32-wide latent projections whose outputs feed
 //       argmins (lam.py:94, lam.py:109) — too small for tensor-core tiles
+#include <mutex>
+
 #include "common.h"
 #include "ptx.cuh"
 
@@ -216,6 +218,56 @@ __global__ void linear_f32_kernel(const float* __restrict__ x, int64_t R, int K,
   }
 }
 
+// N = 32 (the latent projections, K up to 512): W lives in shared memory, lane j owns output
+// column j, a warp computes 4 rows at a time from broadcast float4 reads of x.  Per output the sum
+// runs over k in order, bit-identical to linear_f32_kernel.
+constexpr int kLinN32Rows = 4;
+__global__ void __launch_bounds__(256) linear_f32_n32_kernel(const float* __restrict__ x, int64_t R, int K,
+                                                             const float* __restrict__ W, const float* __restrict__ b,
+                                                             float* __restrict__ y, int accumulate) {
+  extern __shared__ float sW[];  // [K][32]
+  for (int e = threadIdx.x * 4; e < K * 32; e += blockDim.x * 4)
+    *reinterpret_cast<float4*>(sW + e) = *reinterpret_cast<const float4*>(W + e);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const float bias = b ? b[lane] : 0.f;
+  const int64_t groups = (R + kLinN32Rows - 1) / kLinN32Rows;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t gidx = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gidx < groups; gidx += nw) {
+    const int64_t r0 = gidx * kLinN32Rows;
+    const float* xr[kLinN32Rows];
+#pragma unroll
+    for (int j = 0; j < kLinN32Rows; ++j) xr[j] = x + min(r0 + j, R - 1) * K;
+    float acc[kLinN32Rows];
+#pragma unroll
+    for (int j = 0; j < kLinN32Rows; ++j) acc[j] = 0.f;
+#pragma unroll 2
+    for (int k = 0; k < K; k += 4) {
+      float4 xv[kLinN32Rows];
+#pragma unroll
+      for (int j = 0; j < kLinN32Rows; ++j) xv[j] = __ldg(reinterpret_cast<const float4*>(xr[j] + k));
+      const float w0 = sW[(k + 0) * 32 + lane], w1 = sW[(k + 1) * 32 + lane];
+      const float w2 = sW[(k + 2) * 32 + lane], w3 = sW[(k + 3) * 32 + lane];
+#pragma unroll
+      for (int j = 0; j < kLinN32Rows; ++j) {
+        acc[j] = fmaf(xv[j].x, w0, acc[j]);
+        acc[j] = fmaf(xv[j].y, w1, acc[j]);
+        acc[j] = fmaf(xv[j].z, w2, acc[j]);
+        acc[j] = fmaf(xv[j].w, w3, acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kLinN32Rows; ++j) {
+      const int64_t r = r0 + j;
+      if (r < R) {
+        float* dst = y + r * 32 + lane;
+        const float v = acc[j] + bias;
+        *dst = accumulate ? *dst + v : v;
+      }
+    }
+  }
+}
+
 // dx[r][k] = sum_j dy[r][j] W[k][j]
 __global__ void linear_f32_dx_kernel(const float* __restrict__ dy, int64_t R, int N, const float* __restrict__ W,
                                      int K, float* __restrict__ dx, int accumulate) {
@@ -354,7 +406,20 @@ extern "C" int jz_linear_f32(const float* x, int64_t R, int K, const float* W, i
                              int accumulate, jz_stream_t s) {
   const int64_t n = R * N;
   if (n == 0) return JZ_OK;
-  linear_f32_kernel<<<grid_of(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, N, b, y, accumulate);
+  if (N == 32 && K % 4 == 0 && K <= 1024 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)W % 16) == 0) {
+    const size_t smem = (size_t)K * 32 * sizeof(float);
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+      attr_err = cudaFuncSetAttribute(linear_f32_n32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 32 * 4);
+    });
+    JZ_CUDA_TRY(attr_err);
+    int64_t grid = (R + 8 * kLinN32Rows - 1) / (8 * kLinN32Rows);
+    if (grid > (int64_t)num_sms() * 2) grid = (int64_t)num_sms() * 2;
+    linear_f32_n32_kernel<<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, b, y, accumulate);
+  } else {
+    linear_f32_kernel<<<grid_of(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, N, b, y, accumulate);
+  }
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

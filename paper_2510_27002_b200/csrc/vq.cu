@@ -69,6 +69,82 @@ __global__ void __launch_bounds__(256) vq_fwd_kernel(const float* __restrict__ z
   if (row_sq) row_sq[r] = se;
 }
 
+// DZ % 4 == 0: codes staged unpadded (every lane reads the same code -> broadcast float4 reads) and
+// two codes per step as independent FMA chains; each distance keeps the sequential i order of
+// vq_fwd_kernel and codes are compared in index order, so the result is bit-identical.
+template <int DZ>
+__global__ void __launch_bounds__(256) vq_fwd4_kernel(const float* __restrict__ z, int64_t rows,
+                                                      const float* __restrict__ cb, int K, int64_t* __restrict__ idx,
+                                                      float* __restrict__ zq_st, float* __restrict__ row_sq) {
+  constexpr int kChunk = DZ >= 64 ? 128 : 256;
+  constexpr int V = DZ / 4;
+  __shared__ float4 sc[kChunk * V];
+  __shared__ float scc[kChunk];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = r < rows;
+  float zr[DZ], z2[DZ];
+  float zz = 0.f;
+#pragma unroll
+  for (int i = 0; i < DZ; ++i) {
+    zr[i] = valid ? z[r * DZ + i] : 0.f;
+    zz += zr[i] * zr[i];
+    z2[i] = 2.0f * zr[i];
+  }
+  float best = INFINITY;
+  int bi = 0;
+  for (int k0 = 0; k0 < K; k0 += kChunk) {
+    const int kn = min(kChunk, K - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kn * V; e += blockDim.x)
+      sc[e] = *reinterpret_cast<const float4*>(cb + (int64_t)k0 * DZ + 4 * e);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kn; k += blockDim.x) {
+      float cc = 0.f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 c4 = sc[k * V + v];
+        cc += c4.x * c4.x; cc += c4.y * c4.y; cc += c4.z * c4.z; cc += c4.w * c4.w;
+      }
+      scc[k] = cc;
+    }
+    __syncthreads();
+    int k = 0;
+    for (; k + 1 < kn; k += 2) {
+      float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 a = sc[k * V + v], c = sc[(k + 1) * V + v];
+        d0 += z2[4 * v] * a.x; d0 += z2[4 * v + 1] * a.y; d0 += z2[4 * v + 2] * a.z; d0 += z2[4 * v + 3] * a.w;
+        d1 += z2[4 * v] * c.x; d1 += z2[4 * v + 1] * c.y; d1 += z2[4 * v + 2] * c.z; d1 += z2[4 * v + 3] * c.w;
+      }
+      const float e0 = (zz - d0) + scc[k], e1 = (zz - d1) + scc[k + 1];
+      if (e0 < best) { best = e0; bi = k0 + k; }
+      if (e1 < best) { best = e1; bi = k0 + k + 1; }
+    }
+    if (k < kn) {
+      float d0 = 0.f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 a = sc[k * V + v];
+        d0 += z2[4 * v] * a.x; d0 += z2[4 * v + 1] * a.y; d0 += z2[4 * v + 2] * a.z; d0 += z2[4 * v + 3] * a.w;
+      }
+      const float e0 = (zz - d0) + scc[k];
+      if (e0 < best) { best = e0; bi = k0 + k; }
+    }
+  }
+  if (!valid) return;
+  idx[r] = bi;
+  float se = 0.f;
+#pragma unroll
+  for (int i = 0; i < DZ; ++i) {
+    const float q = cb[(int64_t)bi * DZ + i];
+    const float diff = q - zr[i];
+    se += diff * diff;
+    if (zq_st) zq_st[r * DZ + i] = zr[i] + diff;
+  }
+  if (row_sq) row_sq[r] = se;
+}
+
 // dz = g + commit_coef * (z - c_idx)
 __global__ void vq_bwd_z_kernel(const float* __restrict__ z, const float* __restrict__ cb,
                                 const int64_t* __restrict__ idx, const float* __restrict__ g, int64_t rows, int dz,
@@ -156,7 +232,10 @@ extern "C" int jz_vq_fwd(const float* z, int64_t rows, int dz, const float* code
   switch (dz) {
     case 8: vq_fwd_kernel<8><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;
     case 16: vq_fwd_kernel<16><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;
-    case 32: vq_fwd_kernel<32><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;
+    case 32:
+      if (((uintptr_t)codebook % 16) == 0) vq_fwd4_kernel<32><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq);
+      else vq_fwd_kernel<32><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq);
+      break;
     default: vq_fwd_kernel<64><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;
   }
   JZ_LAUNCH_CHECK();
