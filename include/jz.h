@@ -110,6 +110,10 @@ JZ_API int jz_colsum_bf16(const void* x, int64_t rows, int cols, int64_t ld, flo
  * and uses `part` as scratch (rows 0, 256, 512, ... are overwritten). */
 JZ_API int jz_reduce_partials(const float* part, int nparts, int64_t D, float* out, int accumulate,
                               jz_stream_t stream);
+/* Three independent reductions of the same shape in one launch (NULL outputs are skipped); the
+ * partial rows of each may live anywhere.  Used for the LayerNorm backward's gamma / beta / bias. */
+JZ_API int jz_reduce_partials3(const float* part0, const float* part1, const float* part2, int nparts, int64_t D,
+                               float* out0, float* out1, float* out2, int accumulate, jz_stream_t stream);
 /* dst_bf16[r*ldd + c] = bf16(src[r*lds + c])  (weight shadows) */
 JZ_API int jz_cast_f32_bf16_2d(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
                                int64_t cols, jz_stream_t stream);

@@ -35,6 +35,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_row_partials": [_I64],
     "jz_colsum_bf16": [_P, _I64, _I32, _I64, _P, _I32, _P],
     "jz_reduce_partials": [_P, _I32, _I64, _P, _I32, _P],
+    "jz_reduce_partials3": [_P, _P, _P, _I32, _I64, _P, _P, _P, _I32, _P],
     "jz_cast_f32_bf16_2d": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "jz_layernorm_fwd": [_P, _I64, _I32, _P, _P, _F32, _P, _P, _P, _P, _I64, _P],
     "jz_layernorm_bwd": [_P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _I32, _I64, _I32, _I64, _P],

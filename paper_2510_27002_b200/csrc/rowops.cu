@@ -267,6 +267,42 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
   }
 }
 
+// Up to three independent single-stage reductions in one launch (blockIdx.y = which): the
+// LayerNorm backward's gamma / beta / residual-bias partials are reduced concurrently instead of by
+// three latency-bound launches.  Same per-column summation order as reduce_partials_kernel.
+struct Reduce3 {
+  const float* part[3];
+  float* out[3];
+};
+__global__ void __launch_bounds__(256) reduce_partials3_kernel(Reduce3 r, int nparts, int64_t D, int accumulate) {
+  const float* part = r.part[blockIdx.y];
+  float* out = r.out[blockIdx.y];
+  if (out == nullptr) return;
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  for (int64_t c0 = (int64_t)blockIdx.x * 32; c0 < D; c0 += (int64_t)gridDim.x * 32) {
+    const int64_t c = c0 + lane;
+    float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c < D) {
+      int p = grp;
+      for (; p + 56 < nparts; p += 64) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] += __ldg(part + (int64_t)(p + 8 * q) * D + c);
+      }
+      for (int q = 0; p < nparts; p += 8, ++q) s[q] += __ldg(part + (int64_t)p * D + c);
+    }
+    sm[grp][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    __syncthreads();
+    if (grp == 0 && c < D) {
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += sm[k][lane];
+      out[c] = accumulate ? out[c] + t : t;
+    }
+    __syncthreads();
+  }
+}
+
 // Stage 1 for many partial rows: CTA (column block x, chunk y) sums rows [256 y, 256 y + 256) of its
 // 32 columns in a fixed order and writes the result into row 256 y (a row only it reads).
 constexpr int kChunkRows = 256;
@@ -543,6 +579,30 @@ extern "C" int jz_reduce_partials(const float* part, int nparts, int64_t D, floa
   int64_t blocks = (D + 31) / 32;
   if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
   reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, nparts, D, out, accumulate, stride);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_reduce_partials3(const float* part0, const float* part1, const float* part2, int nparts, int64_t D,
+                                   float* out0, float* out1, float* out2, int accumulate, jz_stream_t s) {
+  if (D == 0 || (!out0 && !out1 && !out2)) return JZ_OK;
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  if (nparts > 2 * kChunkRows) {  // large partial counts: the two-stage path, one output at a time
+    const float* ps[3] = {part0, part1, part2};
+    float* os[3] = {out0, out1, out2};
+    for (int i = 0; i < 3; ++i)
+      if (os[i]) {
+        const int rc = jz_reduce_partials(ps[i], nparts, D, os[i], accumulate, s);
+        if (rc) return rc;
+      }
+    return JZ_OK;
+  }
+  Reduce3 r;
+  r.part[0] = part0; r.part[1] = part1; r.part[2] = part2;
+  r.out[0] = out0; r.out[1] = out1; r.out[2] = out2;
+  int64_t blocks = (D + 31) / 32;
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  reduce_partials3_kernel<<<dim3((unsigned)blocks, 3), 256, 0, st>>>(r, nparts, D, accumulate);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

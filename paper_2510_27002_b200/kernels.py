@@ -244,12 +244,9 @@ def layernorm_bwd(x, mean, rstd, g, dy, dres, *, accumulate: bool, dres_bf16=Non
            rstd.data_ptr(), g.data_ptr(), dy.data_ptr(),
            dres.data_ptr(), int(accumulate), _p(dres_bf16), _p(pg), _p(pb), _p(pz), npart, rows, D, skip_period,
            _s())
-    if dgamma is not None:
-        reduce_partials(pg, npart, D, dgamma, acc_params)
-    if dbeta is not None:
-        reduce_partials(pb, npart, D, dbeta, acc_params)
-    if dbias is not None:
-        reduce_partials(pz, npart, D, dbias, acc_params)
+    if dgamma is not None or dbeta is not None or dbias is not None:  # one launch for the three reductions
+        L.call("jz_reduce_partials3", _p(pg), _p(pb), _p(pz), npart, D, _p(dgamma), _p(dbeta), _p(dbias),
+               int(acc_params), _s())
 
 
 # --------------------------------------------------------------------------
