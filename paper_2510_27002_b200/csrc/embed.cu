@@ -367,13 +367,17 @@ __global__ void dyn_action_w_kernel(const float* __restrict__ dact, int64_t dact
 
 __global__ void dyn_action_cond_kernel(const float* __restrict__ dact, int64_t dact_stride, int64_t BT,
                                        const float* __restrict__ Wa, int dl, int D, float* __restrict__ dcond) {
+  // one warp per (b, t) row; lanes stride over d (coalesced dact and Wa rows), one warp sum per output
   const int64_t bt = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (bt >= BT) return;
-  for (int i = lane; i < dl; i += 32) {
+  const float* a = dact + bt * dact_stride;
+  for (int i = 0; i < dl; ++i) {
+    const float* w = Wa + (int64_t)i * D;
     float s = 0.f;
-    for (int d = 0; d < D; ++d) s += dact[bt * dact_stride + d] * Wa[(int64_t)i * D + d];
-    dcond[bt * dl + i] = s;
+    for (int d = lane; d < D; d += 32) s += a[d] * w[d];
+    s = warp_sum(s);
+    if (lane == 0) dcond[bt * dl + i] = s;
   }
 }
 

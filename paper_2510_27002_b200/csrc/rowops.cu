@@ -402,11 +402,16 @@ __global__ void __launch_bounds__(kRowThreads) ce_kernel(const float* __restrict
 __global__ void ce_finalize_kernel(const float* __restrict__ row_loss, int64_t rows,
                                    const int* __restrict__ count, float* __restrict__ loss) {
   __shared__ double sm[1024];
-  double s = 0.0;
-  const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
-  const int64_t a = threadIdx.x * per, b = min(rows, a + per);
-  for (int64_t i = a; i < b; ++i) s += (double)row_loss[i];
-  sm[threadIdx.x] = s;
+  // thread t sums rows t, t + blockDim, ... (coalesced, 4 loads in flight), fixed order
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t nb = blockDim.x;
+  int64_t i = threadIdx.x;
+  for (; i + 3 * nb < rows; i += 4 * nb) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] += (double)row_loss[i + q * nb];
+  }
+  for (int q = 0; i < rows; i += nb, ++q) s[q] += (double)row_loss[i];
+  sm[threadIdx.x] = (s[0] + s[1]) + (s[2] + s[3]);
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
