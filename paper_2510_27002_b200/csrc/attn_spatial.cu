@@ -20,7 +20,9 @@ namespace jz {
 
 namespace sp {
 
-constexpr int kFwdThreads = 384;  // forward: w0 TMA, w1 MMA, w2-5 tile 0, w6-9 tile 1, w10-11 tail row
+constexpr int kFwdTailWarps = 4;  // query row 256 (S = 257) on CUDA cores, keys split 4 ways
+constexpr int kFwdTailThreads = 32 * kFwdTailWarps;
+constexpr int kFwdThreads = 320 + kFwdTailThreads;  // w0 TMA, w1 MMA, w2-5 tile 0, w6-9 tile 1, w10.. tail row
 constexpr int TILE = 16384;    // 128 rows x 128 B
 // forward smem map (bytes, from a 1024-aligned base)
 constexpr int F_Q = 0;                 // 2 tiles
@@ -38,8 +40,7 @@ struct FwdSmallSmem {
   alignas(128) uint8_t krow[128];  // key 256 of the unit (TMA, arrives with Q/K)
   alignas(128) uint8_t vrow[128];  // value 256 of the unit (TMA, arrives with V)
   float tail_s[260];
-  float tail_o[64];
-  float tail_red[4];
+  float tail_red[2 * kFwdTailWarps];
 };
 static_assert(sizeof(FwdSmallSmem) <= 2048, "forward small smem budget");
 
@@ -81,7 +82,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.qk_full, 1); mbar_init(&sm.v_full, 1);
     // Q/K and V smem (+ rows 256) are released by the MMA commit, both softmax warpgroups and the tail
-    mbar_init(&sm.qk_free, 1 + 256 + (has_tail ? 64 : 0)); mbar_init(&sm.v_free, 1 + 256 + (has_tail ? 64 : 0));
+    mbar_init(&sm.qk_free, 1 + 256 + (has_tail ? kFwdTailThreads : 0));
+    mbar_init(&sm.v_free, 1 + 256 + (has_tail ? kFwdTailThreads : 0));
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sm.s_full[t], 1); mbar_init(&sm.p_full[t], 128);
       mbar_init(&sm.o_full[t], 1); mbar_init(&sm.tmem_free[t], 128);
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (has_tail) {
     // tail warps: query row 256 on CUDA cores, reading K/V from the staged smem tiles
-    const int tid = threadIdx.x - 320;  // 0..63
+    const int tid = threadIdx.x - 320;  // 0 .. kFwdTailThreads - 1
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const uint32_t par = i & 1;
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         sm.tail_s[256] = a;
         mx = a;
       }
-      for (int k = tid; k < 256; k += 64) {
+      for (int k = tid; k < 256; k += kFwdTailThreads) {
         const uint8_t* kt = smem + F_K + (k >> 7) * TILE;
         float a = 0.f;
 #pragma unroll
@@ -324,49 +326,63 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_arrive(&sm.qk_free);
       mx = warp_max(mx);
       if (lane == 0) sm.tail_red[warp - 10] = mx;
-      named_bar(3, 64);
-      mx = fmaxf(sm.tail_red[0], sm.tail_red[1]);
+      named_bar(3, kFwdTailThreads);
+      mx = sm.tail_red[0];
+#pragma unroll
+      for (int w = 1; w < kFwdTailWarps; ++w) mx = fmaxf(mx, sm.tail_red[w]);
       const float mb = mx * c2;
       float sum = 0.f;
-      for (int k = tid; k < S; k += 64) {
+      for (int k = tid; k < S; k += kFwdTailThreads) {
         const float p = ex2(sm.tail_s[k] * c2 - mb);
         sm.tail_s[k] = p;
         sum += p;
       }
       sum = warp_sum(sum);
-      if (lane == 0) sm.tail_red[2 + warp - 10] = sum;
-      named_bar(3, 64);
-      sum = sm.tail_red[2] + sm.tail_red[3];
-      // o[d] for d = 2*(tid&31) .. +1, keys split in two halves by warp
-      const int dpair = tid & 31, half = tid >> 5;
+      if (lane == 0) sm.tail_red[kFwdTailWarps + warp - 10] = sum;
+      named_bar(3, kFwdTailThreads);
+      sum = 0.f;
+#pragma unroll
+      for (int w = 0; w < kFwdTailWarps; ++w) sum += sm.tail_red[kFwdTailWarps + w];
+      // o[d] for d = 2*(tid&31) .. +1, keys split into kFwdTailWarps parts by warp
+      constexpr int KP = 256 / kFwdTailWarps;
+      const int dpair = tid & 31, part = tid >> 5;
       float o0 = 0.f, o1 = 0.f;
       mbar_wait(&sm.v_full, par);
       const uint32_t chunk = dpair >> 2, within = (dpair & 3) * 4;
 #pragma unroll 8
-      for (int k = half * 128; k < half * 128 + 128; ++k) {
+      for (int k = part * KP; k < part * KP + KP; ++k) {
         const uint8_t* vt = smem + F_V + (k >> 7) * TILE;
         const float2 v = unpack_bf16(*reinterpret_cast<const uint32_t*>(vt + sw128(k & 127, chunk) + within));
         const float p = sm.tail_s[k];
         o0 += p * v.x;
         o1 += p * v.y;
       }
-      mbar_arrive(&sm.v_free);
-      if (half == 1) {
+      if (part == kFwdTailWarps - 1) {  // value row 256, read before this thread releases V
         const float2 vl = unpack_bf16(*reinterpret_cast<const uint32_t*>(sm.vrow + 4 * dpair));
-        o0 += sm.tail_s[256] * vl.x;
-        o1 += sm.tail_s[256] * vl.y;
-        sm.tail_o[2 * dpair] = o0;
-        sm.tail_o[2 * dpair + 1] = o1;
+        const float p256 = sm.tail_s[256];
+        o0 += p256 * vl.x;
+        o1 += p256 * vl.y;
       }
-      named_bar(3, 64);
-      if (half == 0) {
-        o0 = (o0 + sm.tail_o[2 * dpair]) / sum;
-        o1 = (o1 + sm.tail_o[2 * dpair + 1]) / sum;
+      mbar_arrive(&sm.v_free);
+      named_bar(3, kFwdTailThreads);  // every part is done reading the probabilities in tail_s
+      if (part > 0) {                 // partial outputs of parts 1.. into tail_s
+        sm.tail_s[(part - 1) * 64 + 2 * dpair] = o0;
+        sm.tail_s[(part - 1) * 64 + 2 * dpair + 1] = o1;
+      }
+      named_bar(3, kFwdTailThreads);
+      if (part == 0) {
+#pragma unroll
+        for (int w = 0; w < kFwdTailWarps - 1; ++w) {
+          o0 += sm.tail_s[w * 64 + 2 * dpair];
+          o1 += sm.tail_s[w * 64 + 2 * dpair + 1];
+        }
+        o0 /= sum;
+        o1 /= sum;
         *reinterpret_cast<uint32_t*>(out + (row0 + 256) * D + h * 64 + 2 * dpair) = pack_bf16(o0, o1);
         if (out_f32) *reinterpret_cast<float2*>(out_f32 + (row0 + 256) * D + h * 64 + 2 * dpair) = make_float2(o0, o1);
         if (tid == 0) lse[((int64_t)f * H + h) * S + 256] = mx * 0.125f + logf(sum);
       }
-      named_bar(3, 64);
+      named_bar(3, kFwdTailThreads);
     }
   }
   if (warp >= 2 && warp < 10 && lane == 0) bulk_wait0();
