@@ -13,7 +13,8 @@ import paper_2510_27002_b200._lib as L
 L.LIB_PATH = __import__("pathlib").Path("/tmp/jzprof/libjz.so")
 L.ensure_device()
 lib = L.load()
-frames, S, H = 576, 257, 8
+import os
+frames, S, H = 576, int(os.environ.get("S", "257")), 8
 D = H * 64
 qkv = torch.randn(frames * S, 3 * D, device="cuda").bfloat16()
 out = torch.empty(frames * S, D, device="cuda", dtype=torch.bfloat16)
