@@ -1,0 +1,82 @@
+"""Full-size (BASELINE C3: jasmine-base dims, B=36, T=16, 256 patches, 1024 codes) properties of
+the device training step, where the CPU oracle is too slow to run the same batch:
+
+- the masked cross-entropy at random init sits just above ln(1024), the value the reference's own
+  known-answer test pins for uniform logits (test_nn.py:46-50): with to_logits ~ N(0, 0.02^2) on a
+  unit-variance LN output the logits have variance s^2 = 0.02^2 * 512 and E[CE] ~ ln K + s^2 / 2;
+  every gradient is finite;
+- the step is run-to-run deterministic: loss and every parameter gradient are bitwise identical
+  on a second identical step (no float atomics anywhere);
+- two trainers built from the same seed stay bitwise identical through AdamW (WSD schedule,
+  the mask stream of run_stage, trainer.py:132-198).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+B, T, N, K = 36, 16, 256, 1024
+
+
+def _inputs():
+    from paper_2510_27002_b200.rng import stream
+    from paper_2510_27002_b200.tensor import Tensor
+    tokens = torch.as_tensor(stream(1, "bench-tokens").integers(0, K, size=(B, T, N)), device="cuda")
+    cb = stream(2, "bench-lam-codebook").uniform(-1 / 6, 1 / 6, size=(6, 32)).astype(np.float32)
+    lat = cb[stream(2, "bench-actions").integers(0, 6, size=(B, T - 1))]
+    return tokens, Tensor(torch.as_tensor(lat, device="cuda"))
+
+
+def _model():
+    from paper_2510_27002_b200.dynamics import DynamicsConfig, DynamicsModel
+    return DynamicsModel(DynamicsConfig(patches_per_frame=N, max_frames=T, token_codes=K), seed=0)
+
+
+def _loss_and_grads(model, tokens, lat, step):
+    from paper_2510_27002_b200.rng import stream
+    store = model._store
+    if store.grad_flat is not None:
+        store.grad_flat.zero_()
+    loss, _ = model.loss(tokens, lat, stream(0, "dynamics", "step", step))
+    loss.backward()
+    torch.cuda.synchronize()
+    return float(loss.data), store.grad_flat.clone()
+
+
+def test_full_size_loss_is_log_k_and_deterministic():
+    model = _model()
+    tokens, lat = _inputs()
+    l1, g1 = _loss_and_grads(model, tokens, lat, 0)
+    l2, g2 = _loss_and_grads(model, tokens, lat, 0)
+    s2 = 0.02 ** 2 * 512
+    assert abs(l1 - (math.log(K) + s2 / 2)) < 0.03, l1
+    assert bool(torch.isfinite(g1).all())
+    assert float(g1.abs().max()) > 0
+    assert l1 == l2
+    assert torch.equal(g1, g2)
+    # a different mask draw changes the loss (the masks come from the step's stream)
+    l3, _ = _loss_and_grads(model, tokens, lat, 1)
+    assert l3 != l1
+
+
+def test_full_size_training_is_bitwise_reproducible():
+    from paper_2510_27002_b200.optim import WsdSchedule
+    from paper_2510_27002_b200.trainer import DynamicsTrainStep
+    tokens, lat = _inputs()
+    finals, losses = [], []
+    for _ in range(2):
+        model = _model()
+        tr = DynamicsTrainStep(model, WsdSchedule(peak_lr=3e-4, total_steps=100, warmup_steps=2, decay_fraction=0.1))
+        ls = [float(tr.step(k, tokens, lat).data) for k in range(3)]
+        tr.opt.raise_if_nonfinite()
+        torch.cuda.synchronize()
+        finals.append(model._store.flat.clone())
+        losses.append(ls)
+        del tr, model
+        torch.cuda.empty_cache()
+    assert losses[0] == losses[1]
+    assert torch.equal(finals[0], finals[1])
+    assert losses[0][2] < losses[0][0]  # three AdamW steps at lr 3e-4 already lower the loss
