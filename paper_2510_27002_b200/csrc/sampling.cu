@@ -535,6 +535,19 @@ extern "C" int jz_attn_temporal_decode(const void* qkv, void* cache, int64_t B, 
   auto q = reinterpret_cast<const __nv_bfloat16*>(qkv);
   auto c = reinterpret_cast<__nv_bfloat16*>(cache);
   auto o = reinterpret_cast<__nv_bfloat16*>(out);
+  const bool al16 = ((uintptr_t)qkv % 16) == 0 && ((uintptr_t)cache % 16) == 0 && ((uintptr_t)out % 16) == 0;
+  JZ_CHECK_ARG(((uintptr_t)qkv % 8) == 0 && ((uintptr_t)cache % 8) == 0 && ((uintptr_t)out % 8) == 0,
+               "temporal decode: qkv / cache / out must be 8-byte aligned");
+  if (!al16) {  // 16-byte vector kernel needs 16-byte aligned rows; the 8-byte lane kernel does not
+    switch (D) {
+      case 128: temporal_decode_kernel<4><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+      case 256: temporal_decode_kernel<8><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+      case 512: temporal_decode_kernel<16><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+      default: temporal_decode_kernel<32><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
+    }
+    JZ_LAUNCH_CHECK();
+    return JZ_OK;
+  }
   switch (D) {
     case 128: temporal_decode_kernel<4><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
     case 256: temporal_decode_v_kernel<1><<<grid, 128, 0, st>>>(q, c, B, t, dev_t, Tmax, S, append, o); break;
@@ -584,10 +597,12 @@ extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, flo
   if (pgrid > (int64_t)num_sms() * 4) pgrid = (int64_t)num_sms() * 4;
   const size_t psmem = (size_t)kSampleWarps * 2 * K * sizeof(float);
   switch (K / 32) {
-#define MS(P) case P: maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf); break;
-#define MP(P) case P: maskgit_sample_pipe_kernel<P><<<(unsigned)pgrid, 32 * kSampleWarps, psmem, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf); break;
+#define MS_(P) maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf);
+#define MS(P) case P: MS_(P) break;
+#define MP(P) case P: if (((uintptr_t)logits % 16) != 0) { MS_(P) } else maskgit_sample_pipe_kernel<P><<<(unsigned)pgrid, 32 * kSampleWarps, psmem, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf); break;
     MS(1) MS(2) MP(4) MP(8) MP(16) MP(32) MS(64)
 #undef MS
+#undef MS_
 #undef MP
     default: set_error("maskgit: vocabulary %d unsupported", K); return JZ_EINVAL;
   }

@@ -172,3 +172,28 @@ def test_temporal_decode_kernel_vs_torch(D, t):
            out2.data_ptr(), L.stream_ptr())
     assert torch.equal(out2, out)
     assert torch.equal(cache2, ref_cache)
+
+
+def test_sampler_misaligned_logits_take_the_unpipelined_path():
+    """jz_maskgit_step on a logits view that is not 16-byte aligned (pipelined kernel refused,
+    per-row kernel used) gives the same draws and confidences as on an aligned copy."""
+    import ctypes as C
+    from paper_2510_27002_b200 import _lib as L
+    B, N, K = 3, 256, 1024
+    g = torch.Generator(device="cuda").manual_seed(5)
+    base = torch.randn(B * N * K + 1, device="cuda", generator=g) * 3
+    mis = base[1:].view(B * N, K)            # 4-byte offset
+    ali = mis.clone()
+    outs = []
+    for lg in (ali, mis):
+        cur = torch.zeros(B, N, dtype=torch.int64, device="cuda")
+        known = torch.zeros(B, N, dtype=torch.uint8, device="cuda")
+        conf = torch.empty(B, N, device="cuda")
+        z = (C.c_uint64 * 4)(1, 2, 3, 4)
+        k = (C.c_uint64 * 4)(5, 6)
+        L.call("jz_maskgit_step", lg.data_ptr(), B, N, K, 1.0, C.addressof(z), C.addressof(k), C.addressof(z), 4, 0, 7,
+               None, cur.data_ptr(), known.data_ptr(), conf.data_ptr(), L.stream_ptr())
+        outs.append((cur, known, conf))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(outs[0][2], outs[1][2])
