@@ -330,6 +330,16 @@ __global__ void __launch_bounds__(256) reduce_chunks_kernel(float* __restrict__ 
   }
 }
 
+// contiguous fp32 -> bf16 (the per-step flat weight shadow): 8 elements per thread per iteration
+__global__ void cast_flat8_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(src)[2 * i];
+    const float4 b = reinterpret_cast<const float4*>(src)[2 * i + 1];
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y),
+                                                  pack_bf16(b.z, b.w));
+  }
+}
+
 __global__ void cast2d_kernel(const float* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
                               int64_t ldd, int64_t rows, int64_t cols) {
   const int64_t n = rows * cols;
@@ -615,6 +625,15 @@ extern "C" int jz_reduce_partials3(const float* part0, const float* part1, const
 extern "C" int jz_cast_f32_bf16_2d(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
                                    int64_t cols, jz_stream_t s) {
   if (rows * cols == 0) return JZ_OK;
+  const int64_t n = rows * cols;
+  const bool flat = (rows == 1 || (lds == cols && ldd == cols)) && n % 8 == 0 && ((uintptr_t)src % 16) == 0 &&
+                    ((uintptr_t)dst % 16) == 0;
+  if (flat) {
+    cast_flat8_kernel<<<grid_for(n / 8, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+        src, reinterpret_cast<__nv_bfloat16*>(dst), n / 8);
+    JZ_LAUNCH_CHECK();
+    return JZ_OK;
+  }
   cast2d_kernel<<<grid_for(rows * cols, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
       src, lds, reinterpret_cast<__nv_bfloat16*>(dst), ldd, rows, cols);
   JZ_LAUNCH_CHECK();
