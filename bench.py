@@ -185,7 +185,42 @@ def secondary_configs(dev) -> dict:
                               "unit": "frames/s", "ms_per_step": round(ms3, 2),
                               "config": "B=8, T=16, 1024 codes, recon + VQ losses, full backward"}
     out["pretrain_lam_stage"] = _pretrain_lam_stage(tok, lam, dev)
+    out["play_act"] = _play_act(tok, lam, dev)
     return out
+
+
+def _play_act(tok, lam, dev) -> dict:
+    """one interactive play session (B=1, jasmine-base dims, 25 MaskGIT steps) on
+    the device sampler; latency of an 'act' (next frame decoded over the session's KV cache,
+    tokenizer-decoded, PNG-encoded), including the window slide once the clip reaches 16 frames."""
+    import time
+
+    import numpy as np
+    import torch
+
+    from paper_2510_27002_b200.dynamics import DynamicsConfig, DynamicsModel
+    from paper_2510_27002_b200.play import PlayService
+    from paper_2510_27002_b200.rng import stream
+
+    dyn = DynamicsModel(DynamicsConfig(patches_per_frame=PATCHES, max_frames=FRAMES_T), seed=0)
+    svc = PlayService(tok, dyn, lam=lam,
+                      episode_fn=lambda seed, n: stream(4, "play-episode", seed).integers(0, 256, size=(n, 64, 64, 3))
+                      .astype(np.uint8))
+    sid = svc.handle({"type": "reset", "seed": 1})["session"]
+    for a in range(3):  # graph capture and first-use costs
+        svc.handle({"type": "act", "session": sid, "action": a % 6})
+    torch.cuda.synchronize()
+    lat = []
+    for a in range(20):  # crosses the 16-frame window (slides re-prefill the cache)
+        t0 = time.perf_counter()
+        r = svc.handle({"type": "act", "session": sid, "action": a % 6})
+        lat.append((time.perf_counter() - t0) * 1e3)
+        assert r["type"] == "frames"
+    lat.sort()
+    return {"metric": "play act latency (ms, median)", "value": round(lat[len(lat) // 2], 2), "unit": "ms",
+            "higher_is_better": False, "p90_ms": round(lat[int(0.9 * (len(lat) - 1))], 2),
+            "config": "PlayService session, B=1, jasmine-base dynamics + tokenizer, 25 MaskGIT steps, KV-cached "
+                      "decode, PNG frame out; 20 acts after 3 warm-up, host wall clock per act"}
 
 
 def _pretrain_lam_stage(tok, lam, dev) -> dict:
