@@ -95,3 +95,52 @@ class PretrainLamStep:
         idx = self.lam.infer_actions_device(frames)
         latents = Tensor(self.lam.params["codebook"].data[idx])
         return self.inner.step(step, tokens, latents)
+
+
+class StageTrainStep:
+    """run_stage's per-step body (trainer.py:165-182) for any model stage on device:
+    rng = stream(seed, stage, "step", step); loss = loss_fn(frames, actions, rng); backward;
+    AdamW at wsd_lr(schedule, step + 1); gradients start from zero every step (the reference
+    resets p.grad to None, trainer.py:181-183).  The finiteness check is deferred to the
+    optimizer's device flag (`opt.raise_if_nonfinite()`), not a per-step host sync."""
+
+    def __init__(self, params: dict, loss_fn, schedule: WsdSchedule, *, seed: int = 0, stage: str = "stage"):
+        from .tensor import store_for
+        self.params = params
+        self.loss_fn = loss_fn
+        self.schedule = schedule
+        self.seed = seed
+        self.stage = stage
+        self.opt = adamw_init(params)
+        self._store = store_for(params)
+
+    def _zero_grads(self) -> None:
+        st = self._store
+        if st is not None and st.grad_flat is not None:
+            st.grad_flat.zero_()
+            return
+        for p in self.params.values():
+            if p.grad is not None:
+                p.grad.zero_()
+
+    def step(self, step: int, frames, actions=None):
+        self._zero_grads()
+        rng = stream(self.seed, self.stage, "step", step)
+        loss = self.loss_fn(frames, actions, rng)
+        loss.backward()
+        adamw_step(self.params, {n: p.grad for n, p in self.params.items()}, self.opt,
+                   wsd_lr(self.schedule, step + 1), check="deferred")
+        return loss
+
+
+def tokenizer_stage(tokenizer, schedule: WsdSchedule, *, seed: int = 0) -> StageTrainStep:
+    """train_tokenizer's loss_fn (trainer.py:220-223): the tokenizer forward's total loss
+    (reconstruction MSE + codebook + 0.25 commitment) on uint8 frames."""
+    return StageTrainStep(tokenizer.params, lambda frames, actions, rng: tokenizer.forward(frames)[2]["total"],
+                          schedule, seed=seed, stage="tokenizer")
+
+
+def lam_stage(lam, schedule: WsdSchedule, *, seed: int = 0) -> StageTrainStep:
+    """train_lam's loss_fn (trainer.py:254-257): the LAM forward's total loss."""
+    return StageTrainStep(lam.params, lambda frames, actions, rng: lam.forward(frames)[2]["total"],
+                          schedule, seed=seed, stage="lam")

@@ -1,0 +1,68 @@
+"""Tokenizer and LAM training stages on device (trainer.StageTrainStep: run_stage's step body,
+trainer.py:165-182, with train_tokenizer / train_lam loss functions, trainer.py:220-223, 254-257)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import rng as OR
+
+pytestmark = pytest.mark.gpu
+
+TK = dict(model_dim=128, heads=2, ffn_dim=512, blocks=1, codes=64, latent_dim=32, patch=4, max_frames=8)
+
+
+def _frames(b=2, t=4, seed=0):
+    return torch.as_tensor(OR.stream(41, "stage-frames", seed).integers(0, 256, size=(b, t, 64, 64, 3))
+                           .astype(np.uint8), device="cuda")
+
+
+def _models(kind):
+    if kind == "tokenizer":
+        from paper_2510_27002_b200.tokenizer import TokenizerConfig, VideoTokenizer
+        return VideoTokenizer(TokenizerConfig(**TK), seed=3)
+    from paper_2510_27002_b200.lam import LamConfig, LatentActionModel
+    return LatentActionModel(LamConfig(model_dim=128, heads=2, ffn_dim=512, blocks=1, codes=6, latent_dim=32,
+                                       patch=4, max_frames=8), seed=3)
+
+
+@pytest.mark.parametrize("kind", ["tokenizer", "lam"])
+def test_stage_step_is_backward_plus_adamw(kind):
+    """One stage step == a fresh backward of the same loss followed by adamw_step(wsd_lr(step + 1))."""
+    from paper_2510_27002_b200.optim import WsdSchedule, adamw_init, adamw_step, wsd_lr
+    from paper_2510_27002_b200.trainer import lam_stage, tokenizer_stage
+    sched = WsdSchedule(peak_lr=1e-3, total_steps=10, warmup_steps=2)
+    frames = _frames()
+    m1, m2 = _models(kind), _models(kind)
+    st = (tokenizer_stage if kind == "tokenizer" else lam_stage)(m1, sched, seed=5)
+    st.step(0, frames)  # grads of a previous step must not leak into the next
+    st.step(1, frames)
+    st.opt.raise_if_nonfinite()
+    # manual: two steps of forward/backward + adamw on the twin model
+    opt = adamw_init(m2.params)
+    for k in range(2):
+        for p in m2.params.values():
+            if p.grad is not None:
+                p.grad.zero_()
+        loss = m2.forward(frames)[2]["total"]
+        loss.backward()
+        adamw_step(m2.params, {n: p.grad for n, p in m2.params.items()}, opt, wsd_lr(sched, k + 1))
+    torch.cuda.synchronize()
+    for n in m1.params:
+        assert torch.equal(m1.params[n].data, m2.params[n].data), n
+
+
+@pytest.mark.parametrize("kind", ["tokenizer", "lam"])
+def test_stage_training_reduces_loss_deterministically(kind):
+    from paper_2510_27002_b200.optim import WsdSchedule
+    from paper_2510_27002_b200.trainer import lam_stage, tokenizer_stage
+    frames = _frames(seed=1)
+    runs = []
+    for _ in range(2):
+        m = _models(kind)
+        st = (tokenizer_stage if kind == "tokenizer" else lam_stage)(m, WsdSchedule(peak_lr=1e-3, total_steps=50,
+                                                                                      warmup_steps=1))
+        losses = [float(st.step(k, frames).data) for k in range(15)]
+        runs.append(losses)
+    assert runs[0] == runs[1]
+    # VQ code reassignment makes the first steps non-monotone; 15 steps at 1e-3 fit this one batch
+    assert runs[0][-1] < 0.95 * runs[0][0], runs[0]
