@@ -370,6 +370,8 @@ def main() -> None:
     gemm_ms = K.TIMER.ms()
     gemm_flops = K.TIMER.flops
     gemm_launches = K.TIMER.launches
+    families = {name: (K.TIMER.family_ms(name), f["flops"], f["bytes"], len(f["events"]))
+                for name, f in K.TIMER.families.items()}
     K.TIMER = None
     trainer.opt.raise_if_nonfinite()
     frames_per_step = B * FRAMES_T * world
@@ -427,6 +429,22 @@ def main() -> None:
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained",
                 "gemm_share_of_step": round(gemm_ms / args.steps / ms, 4), "gemm_launches_per_step": gemm_launches // args.steps,
                 "algorithmic_flops_per_step": gemm_flops // args.steps, "traffic_launch": traffic_note}
+    # attention kernels (north_star: tensor-pipe utilisation against the bf16 peak): event-timed like
+    # the GEMMs, algorithmic FLOPs and bytes per launch from kernels.py; the binding bound is the
+    # roof the kernel's arithmetic intensity puts under it
+    attention = {}
+    for name, (fms, ffl, fby, fn) in sorted(families.items()):
+        if fms <= 0:
+            continue
+        tfl = ffl / (fms / 1e3) / 1e12
+        gbs = fby / (fms / 1e3) / 1e9
+        t_tensor = ffl / (peaks["bf16_sustained"] * 1e12)
+        t_hbm = fby / (peaks["hbm_gbs"] * 1e9)
+        attention[name] = {"us_per_launch": round(fms * 1e3 / fn, 1), "launches_per_step": fn // args.steps,
+                           "tflops": round(tfl, 1), "frac_bf16_peak": round(tfl / peaks["bf16_sustained"], 4),
+                           "gbs": round(gbs, 1), "frac_hbm_peak": round(gbs / peaks["hbm_gbs"], 4),
+                           "bound": "hbm" if t_hbm > t_tensor else "tensor",
+                           "frac_of_bound": round(max(t_tensor, t_hbm) / (fms / 1e3), 4)}
     step_flops = 42.13e9 * frames_per_step / world  # SURVEY §8d algorithmic FLOPs per GPU-step
     if rank == 0:
         cpu = None
@@ -450,7 +468,7 @@ def main() -> None:
                 "model_tflops": round(step_flops / (ms / 1e3) / 1e12, 1),
                 "model_flops_frac": round(step_flops / (ms / 1e3) / 1e12 / peaks["bf16_sustained"], 4),
                 "cpu_baseline": cpu, "clocks": clk, "loss": round(loss_val, 5),
-            "hbm_peak_gb": round(peak_gb, 1), **extra}
+            "hbm_peak_gb": round(peak_gb, 1), "attention": attention, **extra}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -60,19 +60,43 @@ def num_sms() -> int:
 # K1 GEMM
 # --------------------------------------------------------------------------
 class KernelTimer:
-    """CUDA-event timing of every GEMM launch while active (roofline evidence for bench.py)."""
+    """CUDA-event timing of every GEMM launch while active (roofline evidence for bench.py), plus
+    per-family event pairs with algorithmic FLOPs and bytes for the attention kernels."""
 
     def __init__(self):
         self.active = False
         self.events: list = []
         self.flops = 0
         self.launches = 0
+        self.families: dict = {}  # name -> {"events": [(e0, e1)], "flops": int, "bytes": int}
 
     def ms(self) -> float:
         return sum(a.elapsed_time(b) for a, b in self.events)
 
+    def family_ms(self, name: str) -> float:
+        return sum(a.elapsed_time(b) for a, b in self.families[name]["events"])
+
 
 TIMER: KernelTimer | None = None
+
+
+def _fam_begin():
+    if TIMER is None or not TIMER.active:
+        return None
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    return e0
+
+
+def _fam_end(e0, name: str, flops: int, nbytes: int) -> None:
+    if e0 is None:
+        return
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record()
+    f = TIMER.families.setdefault(name, {"events": [], "flops": 0, "bytes": 0})
+    f["events"].append((e0, e1))
+    f["flops"] += int(flops)
+    f["bytes"] += int(nbytes)
 
 
 def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, a_kmajor: bool, b_kmajor: bool,
@@ -258,7 +282,11 @@ def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: b
     out = torch.empty(frames * S, D, dtype=BF16, device=qkv.device)
     out32 = torch.empty(frames * S, D, dtype=F32, device=qkv.device) if keep_f32 else None
     lse = torch.empty(frames, H, S, dtype=F32, device=qkv.device)
+    e0 = _fam_begin()
     L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), _p(out32), lse.data_ptr(), _s())
+    # algorithmic work: QK^T and PV over S x S per (frame, head); qkv in, O bf16 (+ fp32) and lse out
+    _fam_end(e0, "spatial_fwd", 4 * frames * H * S * S * 64,
+             frames * S * (3 * D * 2 + D * 2 + (D * 4 if keep_f32 else 0) + H * 4))
     return out, out32, lse
 
 
@@ -271,8 +299,12 @@ def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=
     if colsum is not None:
         nparts = L.load().jz_attn_spatial_colsum_parts(frames)
         part = scratch("attn_colsum", nparts * 3 * H * 64)
+    e0 = _fam_begin()
     L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
            64, dqkv.data_ptr(), ws.data_ptr(), _p(part), _s())
+    # 2.5x the forward FLOPs (S, dP, dV, dK, dQ); bytes: qkv, dO (twice: Delta pass + MMAs), O fp32 in, dqkv out
+    D = H * 64
+    _fam_end(e0, "spatial_bwd", 10 * frames * H * S * S * 64, frames * S * (3 * D * 2 + 2 * D * 2 + D * 4 + 3 * D * 2))
     if colsum is not None:
         reduce_partials(part, nparts, 3 * H * 64, colsum)
     return dqkv
@@ -282,7 +314,10 @@ def attn_temporal_fwd(qkv: torch.Tensor, B: int, T: int, S: int, H: int):
     D = H * 64
     out = torch.empty(B * T * S, D, dtype=BF16, device=qkv.device)
     lse = torch.empty(B * S, H, T, dtype=F32, device=qkv.device)
+    e0 = _fam_begin()
     L.call("jz_attn_temporal_fwd", qkv.data_ptr(), B, T, S, H, 64, out.data_ptr(), lse.data_ptr(), _s())
+    # causal pairs only: QK^T and PV over T (T + 1) / 2 pairs per (b, s, head)
+    _fam_end(e0, "temporal_fwd", 2 * 2 * 64 * B * S * H * (T * (T + 1) // 2), B * T * S * (3 * D * 2 + D * 2 + H * 4))
     return out, lse
 
 
@@ -294,8 +329,12 @@ def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=
     if colsum is not None:
         nparts = L.load().jz_attn_temporal_colsum_parts(B, S)
         part = scratch("attn_colsum", nparts * 3 * H * 64)
+    e0 = _fam_begin()
     L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, T, S, H, 64,
            dqkv.data_ptr(), _p(part), _s())
+    D = H * 64
+    _fam_end(e0, "temporal_bwd", 10 * 64 * B * S * H * (T * (T + 1) // 2),
+             B * T * S * (3 * D * 2 + 2 * D * 2 + 3 * D * 2))
     if colsum is not None:
         reduce_partials(part, nparts, 3 * H * 64, colsum)
     return dqkv
