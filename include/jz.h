@@ -165,6 +165,10 @@ JZ_API int jz_finite_check(const float* g, int64_t n, int* flag, jz_stream_t str
 JZ_API int jz_adamw_step(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1,
                          float b2, float omb1, float omb2, float bc1, float bc2, float eps, float lrwd,
                          const int* flag, jz_stream_t stream);
+/* Same update with the step's scalars read from device memory (CUDA-graph replays):
+ * float dev_scalars[9] = lr, b1, b2, 1-b1, 1-b2, 1-b1^t, 1-b2^t, eps, lr*wd. */
+JZ_API int jz_adamw_step_dev(float* p, const float* g, float* m, float* v, int64_t n, const float* dev_scalars,
+                             const int* flag, jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K6  Bernoulli MaskGIT masks, bit-exact with dynamics.sample_masks
@@ -177,6 +181,10 @@ JZ_API int jz_adamw_step(float* p, const float* g, float* m, float* v, int64_t n
 JZ_API int jz_philox_mask(const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4,
                           int buffer_pos, int64_t B_global, int64_t b0, int64_t B_local, int T, int N,
                           double mask_limit, uint8_t* mask, int* count, jz_stream_t stream);
+/* Same mask with the stream state read from device memory (CUDA-graph replays of a training
+ * step): int64 dev_state[11] = counter[4], key[2], buffer[4], buffer_pos. */
+JZ_API int jz_philox_mask_dev(const int64_t* dev_state, int64_t B_global, int64_t b0, int64_t B_local, int T, int N,
+                              double mask_limit, uint8_t* mask, int* count, jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K5  dynamics input embedding (dynamics.py:101-133): token embed, mask-token

@@ -44,6 +44,8 @@ PROTOTYPES: dict[str, list] = {
     "jz_finite_check": [_P, _I64, _P, _P],
     "jz_adamw_step": [_P, _P, _P, _P, _I64, _F32, _F32, _F32, _F32, _F32, _F32, _F32, _F32, _F32, _P, _P],
     "jz_philox_mask": [_P, _P, _P, _I32, _I64, _I64, _I64, _I32, _I32, _F64, _P, _P, _P],
+    "jz_philox_mask_dev": [_P, _I64, _I64, _I64, _I32, _I32, _F64, _P, _P, _P],
+    "jz_adamw_step_dev": [_P, _P, _P, _P, _I64, _P, _P, _P],
     "jz_dyn_embed_fwd": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32,
                          _I32, _P, _P, _P],
     "jz_dyn_embed_bwd_workspace": [_I64, _I32, _I32, _I32, _I32, _I32, _I32],

@@ -3,6 +3,8 @@
 //   K5  token embed + mask-token select + latent-action conditioning (prepend / additive)
 //       + spatial/temporal positions, forward and deterministic backward
 //       (dynamics.py:101-133; autodiff.embedding/where/concat backward, autodiff.py:318-364)
+#include <string.h>
+
 #include "common.h"
 #include "philox.cuh"
 #include "ptx.cuh"
@@ -14,7 +16,17 @@ namespace jz {
 //     p_b = lim + (1 - lim) * u[b]
 // ---------------------------------------------------------------------------
 __global__ void philox_mask_kernel(PhiloxState st, int64_t B_global, int64_t b0, int64_t B_local, int T,
-                                   int N, double lim, uint8_t* __restrict__ mask, int* __restrict__ count) {
+                                   int N, double lim, uint8_t* __restrict__ mask, int* __restrict__ count,
+                                   const int64_t* __restrict__ dev_state) {
+  if (dev_state) {  // graph replays: the step's stream state lives in device memory (layout of jz_philox_mask_dev)
+    for (int i = 0; i < 4; ++i) {
+      st.ctr[i] = (uint64_t)dev_state[i];
+      st.buf[i] = (uint64_t)dev_state[6 + i];
+    }
+    st.key[0] = (uint64_t)dev_state[4];
+    st.key[1] = (uint64_t)dev_state[5];
+    st.pos = (int)dev_state[10];
+  }
   const int64_t total = B_local * T * N;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool m = false;
@@ -421,7 +433,23 @@ extern "C" int jz_philox_mask(const uint64_t* counter4, const uint64_t* key2, co
   const int threads = 256;
   philox_mask_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0,
                        reinterpret_cast<cudaStream_t>(s)>>>(st, B_global, b0, B_local, T, N, mask_limit,
-                                                            mask, count);
+                                                            mask, count, nullptr);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_philox_mask_dev(const int64_t* dev_state, int64_t B_global, int64_t b0, int64_t B_local, int T,
+                                  int N, double mask_limit, uint8_t* mask, int* count, jz_stream_t s) {
+  JZ_CHECK_ARG(dev_state != nullptr, "philox: null device state");
+  JZ_CHECK_ARG(b0 >= 0 && b0 + B_local <= B_global, "philox: shard out of range");
+  const int64_t total = B_local * T * N;
+  if (total == 0) return JZ_OK;
+  PhiloxState st;
+  memset(&st, 0, sizeof(st));
+  const int threads = 256;
+  philox_mask_kernel<<<(unsigned)((total + threads - 1) / threads), threads, 0,
+                       reinterpret_cast<cudaStream_t>(s)>>>(st, B_global, b0, B_local, T, N, mask_limit,
+                                                            mask, count, dev_state);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

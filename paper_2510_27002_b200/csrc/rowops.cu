@@ -447,8 +447,12 @@ __global__ void finite_check_kernel(const float* __restrict__ g, int64_t n, int*
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, int64_t n, float lr, float b1, float b2, float omb1,
                              float omb2, float bc1, float bc2, float eps, float lrwd,
-                             const int* __restrict__ flag) {
+                             const int* __restrict__ flag, const float* __restrict__ dev_sc) {
   if (flag && *flag) return;  // non-finite gradient somewhere: leave every param untouched
+  if (dev_sc) {  // graph replays: this step's scalars from device memory (layout of jz_adamw_step_dev)
+    lr = dev_sc[0]; b1 = dev_sc[1]; b2 = dev_sc[2]; omb1 = dev_sc[3]; omb2 = dev_sc[4];
+    bc1 = dev_sc[5]; bc2 = dev_sc[6]; eps = dev_sc[7]; lrwd = dev_sc[8];
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
@@ -676,7 +680,17 @@ extern "C" int jz_adamw_step(float* p, const float* g, float* m, float* v, int64
                              const int* flag, jz_stream_t s) {
   if (n == 0) return JZ_OK;
   adamw_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      p, g, m, v, n, lr, b1, b2, omb1, omb2, bc1, bc2, eps, lrwd, flag);
+      p, g, m, v, n, lr, b1, b2, omb1, omb2, bc1, bc2, eps, lrwd, flag, nullptr);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int jz_adamw_step_dev(float* p, const float* g, float* m, float* v, int64_t n, const float* dev_scalars,
+                                 const int* flag, jz_stream_t s) {
+  JZ_CHECK_ARG(dev_scalars != nullptr, "adamw: null device scalars");
+  if (n == 0) return JZ_OK;
+  adamw_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      p, g, m, v, n, 0.f, 0.f, 0.f, 0.f, 0.f, 1.f, 1.f, 0.f, 0.f, flag, dev_scalars);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }

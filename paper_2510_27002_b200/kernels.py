@@ -343,10 +343,20 @@ def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=
 # --------------------------------------------------------------------------
 # dynamics input side, masks, CE, AdamW
 # --------------------------------------------------------------------------
+# (philox state int64[11], AdamW scalars f32[9]) device buffers while a training step is being
+# captured into a CUDA graph: the mask and optimizer launches then read the step's values from
+# device memory, which the graph's owner refreshes before every replay (trainer.GraphedTrainStep)
+DEVSTATE: tuple | None = None
+
+
 def philox_mask(state, B_global: int, b0: int, B_local: int, T: int, N: int, mask_limit: float,
                 mask_out: torch.Tensor, count_out: torch.Tensor) -> None:
     """state: rng.PhiloxState (host).  count_out must be zeroed (int32 device scalar)."""
     import ctypes as C
+    if DEVSTATE is not None:
+        L.call("jz_philox_mask_dev", DEVSTATE[0].data_ptr(), B_global, b0, B_local, T, N, float(mask_limit),
+               mask_out.data_ptr(), count_out.data_ptr(), _s())
+        return
     ctr = (C.c_uint64 * 4)(*state.counter)
     key = (C.c_uint64 * 2)(*state.key)
     buf = (C.c_uint64 * 4)(*state.buffer)
@@ -390,6 +400,10 @@ def finite_check(g: torch.Tensor, flag: torch.Tensor) -> None:
 
 
 def adamw(p, g, m, v, *, lr, b1, b2, omb1, omb2, bc1, bc2, eps, lrwd, flag=None) -> None:
+    if DEVSTATE is not None:
+        L.call("jz_adamw_step_dev", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(),
+               DEVSTATE[1].data_ptr(), _p(flag), _s())
+        return
     L.call("jz_adamw_step", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(), lr, b1, b2, omb1,
            omb2, bc1, bc2, eps, lrwd, _p(flag), _s())
 

@@ -40,12 +40,18 @@ class DynamicsTrainStep:
 
     def step(self, step: int, tokens: torch.Tensor, latents: Tensor, global_batch: int | None = None):
         """One training step on this rank's slice; returns the (rank-local share of the) loss tensor."""
-        m = self.model
-        cfg = m.cfg
         B, T, N = tokens.shape
         gb = global_batch if global_batch is not None else B * self.world
         rng = stream(self.seed, self.stage, "step", step)
         st = consume(rng, gb + gb * T * N)
+        return self._device_step(tokens, latents, st, wsd_lr(self.schedule, step + 1), gb)
+
+    def _device_step(self, tokens: torch.Tensor, latents: Tensor, st, lr: float, gb: int):
+        """The step's device work for mask stream state `st` and learning rate `lr` (both ignored,
+        read from device memory instead, while a GraphedTrainStep captures it)."""
+        m = self.model
+        cfg = m.cfg
+        B, T, N = tokens.shape
         dev = tokens.device
         b0, bl = shard(gb, self.rank, self.world)
         mask = torch.empty(bl, T, N, dtype=torch.uint8, device=dev)
@@ -61,8 +67,7 @@ class DynamicsTrainStep:
         loss.backward()
         if self.reducer is not None:
             self.reducer.finish()
-        adamw_step(m.params, {n: p.grad for n, p in m.params.items()}, self.opt, wsd_lr(self.schedule, step + 1),
-                   check="deferred")
+        adamw_step(m.params, {n: p.grad for n, p in m.params.items()}, self.opt, lr, check="deferred")
         return loss
 
     # -- checkpoint / resume (trainer.py:91-115, 442-473) ------------------------------
@@ -144,3 +149,85 @@ def lam_stage(lam, schedule: WsdSchedule, *, seed: int = 0) -> StageTrainStep:
     """train_lam's loss_fn (trainer.py:254-257): the LAM forward's total loss."""
     return StageTrainStep(lam.params, lambda frames, actions, rng: lam.forward(frames)[2]["total"],
                           schedule, seed=seed, stage="lam")
+
+
+class GraphedTrainStep:
+    """A single-process DynamicsTrainStep replayed as ONE CUDA graph per step.
+
+    Everything that changes from step to step is refreshed in device memory before the replay by
+    two small pinned H2D copies:
+    - the step's Philox mask-stream state;
+    - the AdamW scalars (learning rate, bias corrections; `opt.t` advances on the host as in
+      adamw_step).
+
+    The step's tokens and latents are copied into the graph's static inputs. Kernels, launch order
+    and arithmetic are the eager step's, so replays are bit-identical to `trainer.step`
+    (tests/test_gpu_fullsize.py). The data-parallel step stays eager: its NCCL buckets are
+    launched from backward hooks on a side stream.
+    """
+
+    RING = 4  # pinned staging slots in flight (a slot is reused only after its copy has run)
+
+    def __init__(self, trainer: DynamicsTrainStep):
+        if trainer.world != 1:
+            raise ValueError("graph replay is single-process; the data-parallel step runs eagerly")
+        self.tr = trainer
+        self.graph = None
+        self.loss = None
+        dev = trainer.model.params["token_embed"].data.device
+        self.state_d = torch.zeros(11, dtype=torch.int64, device=dev)
+        self.sc_d = torch.zeros(9, dtype=torch.float32, device=dev)
+        self._state_h = [torch.zeros(11, dtype=torch.int64).pin_memory() for _ in range(self.RING)]
+        self._sc_h = [torch.zeros(9, dtype=torch.float32).pin_memory() for _ in range(self.RING)]
+        self._ev = [None] * self.RING
+        self._k = 0
+
+    def _capture(self, tokens: torch.Tensor, latents: Tensor) -> None:
+        from .sampling import _no_gc
+        tr = self.tr
+        self.tok_buf = tokens.clone()
+        self.lat_buf = latents.data.clone()
+        t_saved = tr.opt.t
+        K.DEVSTATE = (self.state_d, self.sc_d)
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            B, T, N = tokens.shape
+            with _no_gc(), torch.cuda.graph(g):
+                self.loss = tr._device_step(self.tok_buf, Tensor(self.lat_buf), None, 0.0, B)
+        finally:
+            K.DEVSTATE = None
+            tr.opt.t = t_saved  # the capture ran adamw_step's host bookkeeping once without a real step
+        self.graph = g
+
+    def step(self, step: int, tokens: torch.Tensor, latents: Tensor):
+        import numpy as np
+        from .optim import _scalars
+        tr = self.tr
+        B, T, N = tokens.shape
+        st = consume(stream(tr.seed, tr.stage, "step", step), B + B * T * N)
+        tr.opt.t += 1
+        sc = _scalars(tr.opt, wsd_lr(tr.schedule, step + 1))
+        slot = self._k % self.RING
+        self._k += 1
+        if self._ev[slot] is not None:
+            self._ev[slot].synchronize()
+        sh, hh = self._state_h[slot], self._sc_h[slot]
+        vals = list(st.counter) + list(st.key) + list(st.buffer) + [st.buffer_pos]
+        sh.numpy()[:] = np.array([v & ((1 << 64) - 1) for v in vals], dtype=np.uint64).view(np.int64)
+        hh.numpy()[:] = [sc["lr"], sc["b1"], sc["b2"], sc["omb1"], sc["omb2"], sc["bc1"], sc["bc2"], sc["eps"],
+                         sc["lrwd"]]
+        self.state_d.copy_(sh, non_blocking=True)
+        self.sc_d.copy_(hh, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ev[slot] = ev
+        if self.graph is None:
+            self._capture(tokens, latents)
+        if tokens.data_ptr() != self.tok_buf.data_ptr():
+            self.tok_buf.copy_(tokens, non_blocking=True)
+        lat = latents.data
+        if lat.data_ptr() != self.lat_buf.data_ptr():
+            self.lat_buf.copy_(lat, non_blocking=True)
+        self.graph.replay()
+        return self.loss

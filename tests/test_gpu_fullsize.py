@@ -80,3 +80,31 @@ def test_full_size_training_is_bitwise_reproducible():
     assert losses[0] == losses[1]
     assert torch.equal(finals[0], finals[1])
     assert losses[0][2] < losses[0][0]  # three AdamW steps at lr 3e-4 already lower the loss
+
+
+def test_graphed_step_is_bitwise_the_eager_step():
+    """trainer.GraphedTrainStep (one CUDA graph per step, mask state and AdamW scalars refreshed in
+    device memory) against the eager DynamicsTrainStep: same losses and parameters, bit for bit,
+    across steps with a changing learning rate (warmup) and fresh masks."""
+    from paper_2510_27002_b200.optim import WsdSchedule
+    from paper_2510_27002_b200.trainer import DynamicsTrainStep, GraphedTrainStep
+    tokens, lat = _inputs()
+    sched = WsdSchedule(peak_lr=3e-4, total_steps=100, warmup_steps=4, decay_fraction=0.1)
+    out = []
+    for graphed in (False, True):
+        model = _model()
+        tr = DynamicsTrainStep(model, sched)
+        tr.step(0, tokens, lat)  # eager warm-up step (first-use allocations and kernel attributes)
+        runner = GraphedTrainStep(tr) if graphed else tr
+        losses = []
+        for k in range(1, 6):
+            loss = runner.step(k, tokens, lat)
+            losses.append(float(loss.data))
+        tr.opt.raise_if_nonfinite()
+        torch.cuda.synchronize()
+        out.append((losses, model._store.flat.clone(), tr.opt.t))
+        del runner, tr, model
+        torch.cuda.empty_cache()
+    assert out[0][0] == out[1][0]
+    assert out[0][2] == out[1][2] == 6
+    assert torch.equal(out[0][1], out[1][1])
