@@ -154,19 +154,26 @@ def secondary_configs(dev) -> dict:
                      "config": "C5: batch 64, 4 cond -> 12 generated frames, 25 MaskGIT steps, T=1, KV-cached "
                                "last-frame forward, tokenizer encode+decode included",
                      "algorithmic_tflops": round(351.2e9 * gen / (ms / 1e3) / 1e12, 1)}
-    # C2: LAM train step, B=8, T=16
+    # C2: LAM train step (forward, backward and AdamW: run_stage's step body), B=8, T=16
+    from paper_2510_27002_b200.optim import WsdSchedule
+    from paper_2510_27002_b200.trainer import lam_stage, tokenizer_stage
     lam = LatentActionModel(LamConfig(patch=4, codes=6, latent_dim=32), seed=0)
     fr8 = torch.as_tensor(stream(0, "bench-frames").integers(0, 256, size=(8, FRAMES_T, 64, 64, 3)).astype(np.uint8),
                           device=dev)
+    lam_tr = lam_stage(lam, WsdSchedule(peak_lr=3e-5, total_steps=200_000), seed=0)
+    lam_k = [0]
 
     def lam_step():
-        _, _, losses = lam.forward(fr8)
-        losses["total"].backward()
+        lam_tr.step(lam_k[0], fr8)
+        lam_k[0] += 1
 
     lam_step()
     ms2 = _events_ms(lam_step, reps=3)
+    lam_tr.opt.raise_if_nonfinite()
     out["lam_train"] = {"metric": "LAM train frames/sec", "value": round(8 * FRAMES_T / (ms2 / 1e3), 1),
-                        "unit": "frames/s", "ms_per_step": round(ms2, 2), "config": "C2: B=8, T=16, 6 codes"}
+                        "unit": "frames/s", "ms_per_step": round(ms2, 2),
+                        "config": "C2: B=8, T=16, 6 codes; forward + backward + AdamW (trainer.lam_stage)",
+                        "model_tflops": round(53.37e9 * 8 * FRAMES_T / (ms2 / 1e3) / 1e12, 1)}
     # C1: tokenizer forward (encode + VQ + decode), B=2
     fr2 = fr8[:2]
     tok.forward(fr2)
@@ -174,16 +181,21 @@ def secondary_configs(dev) -> dict:
     out["tokenizer_fwd"] = {"metric": "tokenizer fwd+quantize frames/sec", "value": round(2 * FRAMES_T / (ms1 / 1e3), 1),
                             "unit": "frames/s", "ms_per_step": round(ms1, 2), "config": "C1: B=2, T=16, 1024 codes"}
 
-    # tokenizer training step: forward + full backward, B=8
+    # tokenizer training step: forward + full backward + AdamW, B=8
+    tok_tr = tokenizer_stage(tok, WsdSchedule(peak_lr=3e-5, total_steps=200_000), seed=0)
+    tok_k = [0]
+
     def tok_step():
-        _, _, losses = tok.forward(fr8)
-        losses["total"].backward()
+        tok_tr.step(tok_k[0], fr8)
+        tok_k[0] += 1
 
     tok_step()
     ms3 = _events_ms(tok_step, reps=3)
+    tok_tr.opt.raise_if_nonfinite()
     out["tokenizer_train"] = {"metric": "tokenizer train frames/sec", "value": round(8 * FRAMES_T / (ms3 / 1e3), 1),
                               "unit": "frames/s", "ms_per_step": round(ms3, 2),
-                              "config": "B=8, T=16, 1024 codes, recon + VQ losses, full backward"}
+                              "config": "B=8, T=16, 1024 codes, recon + VQ losses, full backward + AdamW "
+                                        "(trainer.tokenizer_stage)"}
     out["pretrain_lam_stage"] = _pretrain_lam_stage(tok, lam, dev)
     out["play_act"] = _play_act(tok, lam, dev)
     return out
