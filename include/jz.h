@@ -287,6 +287,14 @@ JZ_API int jz_linear_f32(const float* x, int64_t R, int K, const float* W, int N
                          int accumulate, jz_stream_t stream);
 JZ_API int jz_linear_f32_bwd(const float* x, const float* dy, int64_t R, int K, int N, const float* W, float* dx,
                              float* dW, float* db, int accumulate, jz_stream_t stream);
+/* Same gradients through parallel kernels when one side of W is 32 wide (the latent projections):
+ * dW from per-256-row partials folded in index order by jz_reduce_partials (deterministic), dx from
+ * W staged in shared memory.  workspace: jz_linear_f32_bwd_workspace(R, K, N) floats (0: the shape
+ * is not covered and the call runs jz_linear_f32_bwd). */
+JZ_API int64_t jz_linear_f32_bwd_workspace(int64_t R, int K, int N);
+JZ_API int jz_linear_f32_bwd_ws(const float* x, const float* dy, int64_t R, int K, int N, const float* W, float* dx,
+                                float* dW, float* db, int accumulate, float* workspace, int64_t workspace_floats,
+                                jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K8  vector quantizer (tokenizer.vq_quantize, tokenizer.py:58-79), fp32:

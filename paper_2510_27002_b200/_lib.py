@@ -69,6 +69,8 @@ PROTOTYPES: dict[str, list] = {
     "jz_sum": [_P, _I64, _F64, _P, _P, _P],
     "jz_linear_f32": [_P, _I64, _I32, _P, _I32, _P, _P, _I32, _P],
     "jz_linear_f32_bwd": [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _I32, _P],
+    "jz_linear_f32_bwd_workspace": [_I64, _I32, _I32],
+    "jz_linear_f32_bwd_ws": [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _I32, _P, _I64, _P],
     "jz_vq_fwd": [_P, _I64, _I32, _P, _I32, _P, _P, _P, _P],
     "jz_vq_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _F32, _F32, _P, _P, _P],
     "jz_dyn_embed_frame": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P],
@@ -76,7 +78,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_kv_fill": [_P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _P],
     "jz_maskgit_step": [_P, _I64, _I32, _I32, _F32, _P, _P, _P, _I32, _U64, _I32, _P, _P, _P, _P, _P],
 }
-_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_gemm_colsum_parts": _I64, "jz_attn_spatial_colsum_parts": _I64,
+_RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_linear_f32_bwd_workspace": _I64, "jz_gemm_colsum_parts": _I64, "jz_attn_spatial_colsum_parts": _I64,
             "jz_attn_temporal_colsum_parts": _I64, "jz_attn_spatial_bwd_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_assemble_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
             "jz_build_info": C.c_char_p}
 

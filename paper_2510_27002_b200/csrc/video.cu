@@ -222,12 +222,18 @@ __global__ void linear_f32_kernel(const float* __restrict__ x, int64_t R, int K,
 // column j, a warp computes 4 rows at a time from broadcast float4 reads of x.  Per output the sum
 // runs over k in order, bit-identical to linear_f32_kernel.
 constexpr int kLinN32Rows = 4;
+// TRANS: W is stored [32][K] (dx = dy W^T of a 32 -> K projection) and staged as its transpose.
+template <bool TRANS>
 __global__ void __launch_bounds__(256) linear_f32_n32_kernel(const float* __restrict__ x, int64_t R, int K,
                                                              const float* __restrict__ W, const float* __restrict__ b,
                                                              float* __restrict__ y, int accumulate) {
   extern __shared__ float sW[];  // [K][32]
-  for (int e = threadIdx.x * 4; e < K * 32; e += blockDim.x * 4)
-    *reinterpret_cast<float4*>(sW + e) = *reinterpret_cast<const float4*>(W + e);
+  if (TRANS) {
+    for (int e = threadIdx.x; e < K * 32; e += blockDim.x) sW[(e % K) * 32 + e / K] = W[e];
+  } else {
+    for (int e = threadIdx.x * 4; e < K * 32; e += blockDim.x * 4)
+      *reinterpret_cast<float4*>(sW + e) = *reinterpret_cast<const float4*>(W + e);
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const float bias = b ? b[lane] : 0.f;
@@ -264,6 +270,123 @@ __global__ void __launch_bounds__(256) linear_f32_n32_kernel(const float* __rest
         const float v = acc[j] + bias;
         *dst = accumulate ? *dst + v : v;
       }
+    }
+  }
+}
+
+// dx = dy W^T for a K -> 32 projection (W [K][32], the latent projections' input gradient): W staged
+// transposed in shared memory, one warp per row with lane j holding dy[r][j] (shuffle-broadcast),
+// lane l computing columns l + 32 q.  Per output the sum runs over j in order (as linear_f32_dx_kernel).
+__global__ void __launch_bounds__(256) linear_f32_dx_in32_kernel(const float* __restrict__ dy, int64_t R, int K,
+                                                                const float* __restrict__ W,
+                                                                float* __restrict__ dx, int accumulate) {
+  extern __shared__ float sWT[];  // [32][K]
+  for (int e = threadIdx.x; e < K * 32; e += blockDim.x) sWT[(e % 32) * K + e / 32] = W[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < R; r += nw) {
+    const float dv = dy[r * 32 + lane];
+    for (int q0 = 0; q0 < K; q0 += 32 * 8) {
+      float acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const float dj = __shfl_sync(0xffffffffu, dv, j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = q0 + 32 * u + lane;
+          if (k < K) acc[u] = fmaf(dj, sWT[j * K + k], acc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = q0 + 32 * u + lane;
+        if (k < K) {
+          float* dst = dx + r * K + k;
+          *dst = accumulate ? *dst + acc[u] : acc[u];
+        }
+      }
+    }
+  }
+}
+
+// dW partials of y = x W (+ b) when one side is 32 wide: CTA c sums the rows [c RC, (c + 1) RC) into
+// part[c] = x_c^T dy_c ([K][N]) and, when db is wanted, bpart[c] = column sums of dy_c ([N]).  Threads
+// own big-dim indices (t, t + 256, ...) and all 32 small-dim indices; rows are staged 16 at a time.
+// jz_reduce_partials then folds the chunks in index order (deterministic).
+constexpr int kDwRowsPerCta = 256;
+constexpr int kDwStage = 16;
+template <int BPT>
+__global__ void __launch_bounds__(256) linear_f32_dw_part_kernel(const float* __restrict__ x,
+                                                                const float* __restrict__ dy, int64_t R, int K,
+                                                                int N, int k_big, float* __restrict__ part,
+                                                                float* __restrict__ bpart) {
+  extern __shared__ float sm[];
+  const int Bg = k_big ? K : N;
+  float* sbig = sm;                     // [kDwStage][Bg]
+  float* ssm = sm + kDwStage * Bg;      // [kDwStage][32]
+  const float* big = k_big ? x : dy;
+  const float* small = k_big ? dy : x;
+  float acc[BPT][32];
+#pragma unroll
+  for (int i = 0; i < BPT; ++i)
+#pragma unroll
+    for (int s = 0; s < 32; ++s) acc[i][s] = 0.f;
+  float bsum[BPT];  // column sums of dy: columns t + 256 i
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) bsum[i] = 0.f;
+  const int64_t r0 = (int64_t)blockIdx.x * kDwRowsPerCta;
+  const int64_t r1 = min(R, r0 + kDwRowsPerCta);
+  for (int64_t rb = r0; rb < r1; rb += kDwStage) {
+    const int nr = (int)min((int64_t)kDwStage, r1 - rb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * Bg; e += blockDim.x) sbig[e] = big[rb * Bg + e];
+    for (int e = threadIdx.x; e < nr * 32; e += blockDim.x) ssm[e] = small[rb * 32 + e];
+    __syncthreads();
+    for (int rr = 0; rr < nr; ++rr) {
+      float sv[32];
+#pragma unroll
+      for (int s = 0; s < 32; s += 4) {
+        const float4 f = *reinterpret_cast<const float4*>(ssm + rr * 32 + s);
+        sv[s] = f.x; sv[s + 1] = f.y; sv[s + 2] = f.z; sv[s + 3] = f.w;
+      }
+#pragma unroll
+      for (int i = 0; i < BPT; ++i) {
+        const int b = threadIdx.x + 256 * i;
+        if (b < Bg) {
+          const float bv = sbig[rr * Bg + b];
+#pragma unroll
+          for (int s = 0; s < 32; ++s) acc[i][s] = fmaf(bv, sv[s], acc[i][s]);
+        }
+      }
+      if (bpart != nullptr) {
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+          const int j = threadIdx.x + 256 * i;
+          if (j < N) bsum[i] += k_big ? ssm[rr * 32 + j] : sbig[rr * Bg + j];
+        }
+      }
+    }
+  }
+  float* pc = part + (int64_t)blockIdx.x * K * N;
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    const int b = threadIdx.x + 256 * i;
+    if (b < Bg) {
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        if (k_big) pc[(int64_t)b * N + s] = acc[i][s];
+        else pc[(int64_t)s * N + b] = acc[i][s];
+      }
+    }
+  }
+  if (bpart != nullptr) {
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+      const int j = threadIdx.x + 256 * i;
+      if (j < N) bpart[(int64_t)blockIdx.x * N + j] = bsum[i];
     }
   }
 }
@@ -411,16 +534,81 @@ extern "C" int jz_linear_f32(const float* x, int64_t R, int K, const float* W, i
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(linear_f32_n32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 32 * 4);
+      attr_err = cudaFuncSetAttribute(linear_f32_n32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 32 * 4);
     });
     JZ_CUDA_TRY(attr_err);
     int64_t grid = (R + 8 * kLinN32Rows - 1) / (8 * kLinN32Rows);
     if (grid > (int64_t)num_sms() * 2) grid = (int64_t)num_sms() * 2;
-    linear_f32_n32_kernel<<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, b, y, accumulate);
+    linear_f32_n32_kernel<false><<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, b, y, accumulate);
   } else {
     linear_f32_kernel<<<grid_of(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(x, R, K, W, N, b, y, accumulate);
   }
   JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+extern "C" int64_t jz_linear_f32_bwd_workspace(int64_t R, int K, int N) {
+  if (!((K == 32 && N <= 1024) || (N == 32 && K <= 1024))) return 0;
+  const int64_t chunks = (R + kDwRowsPerCta - 1) / kDwRowsPerCta;
+  return chunks * ((int64_t)K * N + N);
+}
+
+extern "C" int jz_reduce_partials(const float* part, int nparts, int64_t D, float* out, int accumulate,
+                                  jz_stream_t s);
+
+extern "C" int jz_linear_f32_bwd_ws(const float* x, const float* dy, int64_t R, int K, int N, const float* W,
+                                    float* dx, float* dW, float* db, int accumulate, float* workspace,
+                                    int64_t workspace_floats, jz_stream_t s) {
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  const int64_t need = jz_linear_f32_bwd_workspace(R, K, N);
+  const bool a16 = ((uintptr_t)x % 16) == 0 && ((uintptr_t)dy % 16) == 0;
+  if (need == 0 || workspace == nullptr || workspace_floats < need || R == 0 || !a16)
+    return jz_linear_f32_bwd(x, dy, R, K, N, W, dx, dW, db, accumulate, s);
+  if (dx) {
+    int64_t grid = (R + 7) / 8;
+    if (grid > (int64_t)num_sms() * 4) grid = (int64_t)num_sms() * 4;
+    const size_t smem = (size_t)K * 32 * sizeof(float);
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+      attr_err = cudaFuncSetAttribute(linear_f32_dx_in32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      1024 * 32 * 4);
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(linear_f32_n32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        1024 * 32 * 4);
+    });
+    JZ_CUDA_TRY(attr_err);
+    if (N == 32) {  // dx [R][K] = dy [R][32] W^T
+      linear_f32_dx_in32_kernel<<<(unsigned)grid, 256, smem, st>>>(dy, R, K, W, dx, 0);
+    } else {        // K == 32: dx [R][32] = dy [R][N] W^T with W [32][N]
+      int64_t g2 = (R + 8 * kLinN32Rows - 1) / (8 * kLinN32Rows);
+      if (g2 > (int64_t)num_sms() * 2) g2 = (int64_t)num_sms() * 2;
+      linear_f32_n32_kernel<true><<<(unsigned)g2, 256, (size_t)N * 32 * sizeof(float), st>>>(dy, R, N, W, nullptr,
+                                                                                            dx, 0);
+    }
+    JZ_LAUNCH_CHECK();
+  }
+  if (dW) {
+    const int chunks = (int)((R + kDwRowsPerCta - 1) / kDwRowsPerCta);
+    const int Bg = N == 32 ? K : N;
+    const int k_big = N == 32 ? 1 : 0;
+    float* part = workspace;
+    float* bpart = db ? workspace + (int64_t)chunks * K * N : nullptr;
+    const size_t smem = (size_t)kDwStage * (Bg + 32) * sizeof(float);
+    if (Bg <= 256)
+      linear_f32_dw_part_kernel<1><<<chunks, 256, smem, st>>>(x, dy, R, K, N, k_big, part, bpart);
+    else if (Bg <= 512)
+      linear_f32_dw_part_kernel<2><<<chunks, 256, smem, st>>>(x, dy, R, K, N, k_big, part, bpart);
+    else
+      linear_f32_dw_part_kernel<4><<<chunks, 256, smem, st>>>(x, dy, R, K, N, k_big, part, bpart);
+    JZ_LAUNCH_CHECK();
+    int rc = jz_reduce_partials(part, chunks, (int64_t)K * N, dW, accumulate, s);
+    if (rc) return rc;
+    if (db) {
+      rc = jz_reduce_partials(bpart, chunks, N, db, accumulate, s);
+      if (rc) return rc;
+    }
+  }
   return JZ_OK;
 }
 

@@ -478,8 +478,10 @@ def linear_f32(x, W, b=None, out=None, accumulate=False):
 def linear_f32_bwd(x, dy, W, *, dx=None, dW=None, db=None, accumulate=False):
     R, Kd = x.shape
     N = W.shape[1]
-    L.call("jz_linear_f32_bwd", x.data_ptr(), dy.data_ptr(), R, Kd, N, W.data_ptr(), _p(dx), _p(dW), _p(db),
-           int(accumulate), _s())
+    need = L.load().jz_linear_f32_bwd_workspace(R, Kd, N)
+    ws = scratch("linear_f32_bwd", need) if need > 0 else None
+    L.call("jz_linear_f32_bwd_ws", x.data_ptr(), dy.data_ptr(), R, Kd, N, W.data_ptr(), _p(dx), _p(dW), _p(db),
+           int(accumulate), _p(ws), need, _s())
 
 
 def vq_fwd(z: torch.Tensor, codebook: torch.Tensor):

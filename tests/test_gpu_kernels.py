@@ -324,3 +324,33 @@ def test_dyn_embed_fwd_modes(prepend, D, dl):
     tokens[1, 2, 3] = K  # out of range: flagged (and read as token 0), never an out-of-bounds read
     Kn.dyn_embed_fwd(tokens, None, lat, P, B=B, T=T, N=N, D=D, dl=dl, K=K, prepend=prepend, err=err)
     assert int(err.item()) == 1
+
+
+@pytest.mark.parametrize("K,N", [(512, 32), (32, 512), (48, 32)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_linear_f32_bwd_parallel_vs_reference_kernel(K, N, accumulate):
+    """jz_linear_f32_bwd_ws (the latent projections' backward: parallel dW partials folded in order,
+    dx from W in shared memory) against the thread-per-output jz_linear_f32_bwd: dx bit-identical
+    (same summation order), dW / db within fp32 reassociation."""
+    R = 5000 + 77
+    g = torch.Generator(device=dev).manual_seed(K * N + accumulate)
+    x = torch.randn(R, K, device=dev, generator=g)
+    dy = torch.randn(R, N, device=dev, generator=g)
+    W = torch.randn(K, N, device=dev, generator=g)
+    outs = []
+    for fast in (False, True):
+        dx = torch.randn(R, K, device=dev, generator=torch.Generator(device=dev).manual_seed(1))
+        dW = torch.randn(K, N, device=dev, generator=torch.Generator(device=dev).manual_seed(2))
+        db = torch.randn(N, device=dev, generator=torch.Generator(device=dev).manual_seed(3))
+        if fast:
+            Kn.linear_f32_bwd(x, dy, W, dx=dx, dW=dW, db=db, accumulate=bool(accumulate))
+        else:
+            L.call("jz_linear_f32_bwd", x.data_ptr(), dy.data_ptr(), R, K, N, W.data_ptr(), dx.data_ptr(),
+                   dW.data_ptr(), db.data_ptr(), accumulate, L.stream_ptr())
+        outs.append((dx, dW, db))
+    (dx0, dW0, db0), (dx1, dW1, db1) = outs
+    assert torch.equal(dx0, dx1)
+    assert rel(dW1, dW0) < 1e-5 and rel(db1, db0) < 1e-5
+    ref = x.double().t() @ dy.double()
+    base = torch.randn(K, N, device=dev, generator=torch.Generator(device=dev).manual_seed(2)).double()
+    assert rel(dW1.double(), ref + (base if accumulate else 0)) < 1e-5
