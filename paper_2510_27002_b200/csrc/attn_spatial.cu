@@ -925,76 +925,104 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
 
 }  // namespace jz
 
-// Per-unit vector blocks for the backward (layout sp::U_*), one CTA per frame: its warps take the
-// token rows (coalesced over the H*64 columns) and form Delta_i = rowsum(dO_i o O_i) per head into
-// shared memory (dO the bf16 tensor the MMAs consume, O the forward's fp32 copy); then each head's
-// block is written contiguously: lse_i * log2(e) and Delta_i for every row, and for token 256 its
-// q, k, v, dO vectors (fp32) and the (256, 256) entry p = exp(q.k / 8 - lse), dS = p (dO.v - Delta).
+
+// Per-unit vector blocks for the backward (layout sp::U_*): Delta_i = rowsum(dO_i o O_i) per head (dO
+// the bf16 tensor the MMAs consume, O the forward's fp32 copy), lse_i * log2(e) for every row, and for
+// token 256 its q, k, v, dO vectors (fp32) and the (256, 256) entry p = exp(q.k / 8 - lse),
+// dS = p (dO.v - Delta).  CTA (frame f, chunk c) owns rows [64 c, 64 c + 64) of the frame, so a
+// launch has frames * ceil(S / 64) CTAs (one CTA per frame walking 257 rows was latency-bound at small
+// batch: 90 -> 32 us at B = 8); each warp takes 8 rows, two at a time with both rows' loads in flight.
 constexpr int kUvbMaxH = 16;
-__global__ void __launch_bounds__(256) spatial_uvb_kernel(const float* __restrict__ out,
-                                                          const __nv_bfloat16* __restrict__ dout,
-                                                          const __nv_bfloat16* __restrict__ qkv,
-                                                          const float* __restrict__ lse, int64_t frames, int S,
-                                                          int H, float* __restrict__ uvb) {
+constexpr int kUvbRows = 64;
+template <int NC>  // D / 128 column chunks per lane
+__global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const float* __restrict__ out,
+                                                               const __nv_bfloat16* __restrict__ dout,
+                                                               const __nv_bfloat16* __restrict__ qkv,
+                                                               const float* __restrict__ lse, int64_t frames, int S,
+                                                               int H, float* __restrict__ uvb) {
   using namespace jz::sp;
-  __shared__ float dv_s[kUvbMaxH][260];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int D = H * 64;
   const float c2 = 0.125f * 1.4426950408889634f;
-  for (int64_t f = blockIdx.x; f < frames; f += gridDim.x) {
-    for (int sidx = warp; sidx < S; sidx += nwarps) {
+  const int chunks = (S + kUvbRows - 1) / kUvbRows;
+  const int64_t f = blockIdx.x / chunks;
+  const int c0 = (int)(blockIdx.x % chunks) * kUvbRows;
+  // lse * log2(e) for this chunk's rows, every head
+  for (int e = threadIdx.x; e < H * kUvbRows; e += blockDim.x) {
+    const int h = e / kUvbRows, q = c0 + e % kUvbRows;
+    if (q < S) uvb[(f * H + h) * kUvbFloats + U_LSE2 + q] = __ldg(lse + (f * H + h) * S + q) * 1.4426950408889634f;
+  }
+  for (int k0 = 0; k0 < kUvbRows / 8; k0 += 2) {
+    float acc[2][NC];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int sidx = c0 + warp * (kUvbRows / 8) + k0 + k;
+      if (sidx >= S) continue;
       const int64_t row = f * S + sidx;
-      const float* o = out + row * D;
-      const __nv_bfloat16* g = dout + row * D;
-#pragma unroll 4
-      for (int c = 0; c < D / 128; ++c) {
-        const int col = 128 * c + 4 * lane;
-        const int h = col >> 6;
-        const float4 ov = __ldg(reinterpret_cast<const float4*>(o + col));
-        const uint2 gv = __ldg(reinterpret_cast<const uint2*>(g + col));
-        const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
-        float acc = ov.x * g0.x + ov.y * g0.y + ov.z * g1.x + ov.w * g1.y;
 #pragma unroll
-        for (int m = 8; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);  // 16 lanes = one head
-        if ((lane & 15) == 0) dv_s[h][sidx] = acc;
-        if (sidx == 256) {
-          float* ub = uvb + (f * H + h) * kUvbFloats;
-          const __nv_bfloat16* qr = qkv + row * 3 * (int64_t)D;
-          const uint2 qv = __ldg(reinterpret_cast<const uint2*>(qr + col));
-          const uint2 kv = __ldg(reinterpret_cast<const uint2*>(qr + D + col));
-          const uint2 vv = __ldg(reinterpret_cast<const uint2*>(qr + 2 * D + col));
-          const float2 q0 = unpack_bf16(qv.x), q1 = unpack_bf16(qv.y), k0 = unpack_bf16(kv.x), k1 = unpack_bf16(kv.y);
-          const float2 v0 = unpack_bf16(vv.x), v1 = unpack_bf16(vv.y);
-          const int d = col & 63;
-          *reinterpret_cast<float4*>(ub + U_Q + d) = make_float4(q0.x, q0.y, q1.x, q1.y);
-          *reinterpret_cast<float4*>(ub + U_K + d) = make_float4(k0.x, k0.y, k1.x, k1.y);
-          *reinterpret_cast<float4*>(ub + U_V + d) = make_float4(v0.x, v0.y, v1.x, v1.y);
-          *reinterpret_cast<float4*>(ub + U_DO + d) = make_float4(g0.x, g0.y, g1.x, g1.y);
-          float sk = q0.x * k0.x + q0.y * k0.y + q1.x * k1.x + q1.y * k1.y;
-          float dpv = g0.x * v0.x + g0.y * v0.y + g1.x * v1.x + g1.y * v1.y;
+      for (int c = 0; c < NC; ++c) {
+        {
+          const int col = 128 * c + 4 * lane;
+          const float4 ov = __ldg(reinterpret_cast<const float4*>(out + row * D + col));
+          const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dout + row * D + col));
+          const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
+          acc[k][c] = ov.x * g0.x + ov.y * g0.y + ov.z * g1.x + ov.w * g1.y;
+        }
+      }
+    }
 #pragma unroll
-          for (int m = 8; m >= 1; m >>= 1) {
-            sk += __shfl_xor_sync(0xffffffffu, sk, m);
-            dpv += __shfl_xor_sync(0xffffffffu, dpv, m);
-          }
-          if ((lane & 15) == 0) {
-            const float p = exp2f(sk * c2 - __ldg(lse + (f * H + h) * S + 256) * 1.4426950408889634f);
-            ub[U_PC] = p;
-            ub[U_DC] = p * (dpv - acc);
+    for (int k = 0; k < 2; ++k) {
+      const int sidx = c0 + warp * (kUvbRows / 8) + k0 + k;
+      if (sidx >= S) continue;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        {
+          float a = acc[k][c];
+#pragma unroll
+          for (int m = 8; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);  // 16 lanes = one head
+          const int h = (128 * c + 4 * lane) >> 6;
+          if ((lane & 15) == 0) uvb[(f * H + h) * kUvbFloats + U_DV + sidx] = a;
+          acc[k][c] = a;
+        }
+      }
+      if (sidx == 256) {  // token 256: its vectors and the (256, 256) entry, per head
+        const int64_t row = f * S + sidx;
+        const __nv_bfloat16* qr = qkv + row * 3 * (int64_t)D;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          {
+            const int col = 128 * c + 4 * lane;
+            const int h = col >> 6;
+            float* ub = uvb + (f * H + h) * kUvbFloats;
+            const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dout + row * D + col));
+            const uint2 qv = __ldg(reinterpret_cast<const uint2*>(qr + col));
+            const uint2 kv = __ldg(reinterpret_cast<const uint2*>(qr + D + col));
+            const uint2 vv = __ldg(reinterpret_cast<const uint2*>(qr + 2 * D + col));
+            const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
+            const float2 q0 = unpack_bf16(qv.x), q1 = unpack_bf16(qv.y), kk0 = unpack_bf16(kv.x),
+                         kk1 = unpack_bf16(kv.y);
+            const float2 v0 = unpack_bf16(vv.x), v1 = unpack_bf16(vv.y);
+            const int d = col & 63;
+            *reinterpret_cast<float4*>(ub + U_Q + d) = make_float4(q0.x, q0.y, q1.x, q1.y);
+            *reinterpret_cast<float4*>(ub + U_K + d) = make_float4(kk0.x, kk0.y, kk1.x, kk1.y);
+            *reinterpret_cast<float4*>(ub + U_V + d) = make_float4(v0.x, v0.y, v1.x, v1.y);
+            *reinterpret_cast<float4*>(ub + U_DO + d) = make_float4(g0.x, g0.y, g1.x, g1.y);
+            float sk = q0.x * kk0.x + q0.y * kk0.y + q1.x * kk1.x + q1.y * kk1.y;
+            float dpv = g0.x * v0.x + g0.y * v0.y + g1.x * v1.x + g1.y * v1.y;
+#pragma unroll
+            for (int m = 8; m >= 1; m >>= 1) {
+              sk += __shfl_xor_sync(0xffffffffu, sk, m);
+              dpv += __shfl_xor_sync(0xffffffffu, dpv, m);
+            }
+            if ((lane & 15) == 0) {
+              const float p = exp2f(sk * c2 - __ldg(lse + (f * H + h) * S + 256) * 1.4426950408889634f);
+              ub[U_PC] = p;
+              ub[U_DC] = p * (dpv - acc[k][c]);
+            }
           }
         }
       }
     }
-    __syncthreads();
-    for (int h = 0; h < H; ++h) {
-      float* ub = uvb + (f * H + h) * kUvbFloats;
-      const float* lr = lse + (f * H + h) * S;
-      for (int q = threadIdx.x; q < S; q += blockDim.x) {
-        ub[U_LSE2 + q] = __ldg(lr + q) * 1.4426950408889634f;
-        ub[U_DV + q] = dv_s[h][q];
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -1022,10 +1050,22 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
   float* uvb = reinterpret_cast<float*>(workspace);
   {
     JZ_CHECK_ARG(H <= kUvbMaxH, "spatial attention bwd: %d heads unsupported (<= 16)", H);
-    int blocks = (int)(frames < num_sms() * 8 ? frames : num_sms() * 8);
-    spatial_uvb_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-        out_f32, reinterpret_cast<const __nv_bfloat16*>(dout), reinterpret_cast<const __nv_bfloat16*>(qkv), lse,
-        frames, S, H, uvb);
+    const int64_t blocks = frames * ((S + kUvbRows - 1) / kUvbRows);
+    JZ_CHECK_ARG(blocks < (1ll << 31), "spatial attention bwd: too many frames");
+    JZ_CHECK_ARG(H % 2 == 0, "spatial attention bwd: an even head count is required (D multiple of 128)");
+    auto dd = reinterpret_cast<const __nv_bfloat16*>(dout);
+    auto qq = reinterpret_cast<const __nv_bfloat16*>(qkv);
+    auto st_ = reinterpret_cast<cudaStream_t>(s);
+    switch (D / 128) {
+      case 1: spatial_uvb_rows_kernel<1><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 2: spatial_uvb_rows_kernel<2><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 3: spatial_uvb_rows_kernel<3><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 4: spatial_uvb_rows_kernel<4><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 5: spatial_uvb_rows_kernel<5><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 6: spatial_uvb_rows_kernel<6><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 7: spatial_uvb_rows_kernel<7><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      default: spatial_uvb_rows_kernel<8><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+    }
     JZ_LAUNCH_CHECK();
   }
   static std::once_flag once;
