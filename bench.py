@@ -363,10 +363,17 @@ def main() -> None:
     # single process: the step is replayed as one CUDA graph (trainer.GraphedTrainStep, bit-identical
     # to the eager step); data parallel: eager, with the NCCL buckets launched from backward hooks
     runner = trainer
+    step_mode = "eager"
     if world == 1:
         from paper_2510_27002_b200.trainer import GraphedTrainStep
-        runner = GraphedTrainStep(trainer)
-        runner.step(step, tokens_d, lat_d)  # capture + first replay (untimed)
+        try:
+            g_runner = GraphedTrainStep(trainer)
+            g_runner.step(step, tokens_d, lat_d)  # capture + first replay (untimed)
+            torch.cuda.synchronize()
+            runner, step_mode = g_runner, "cuda_graph"
+        except Exception as exc:  # never sink the headline line: time the eager step instead
+            step_mode = f"eager (graph capture failed: {type(exc).__name__}: {str(exc)[:120]})"
+            torch.cuda.synchronize()
         step += 1
     # kernel-level evidence (GEMM roofline, attention families, launch count): an eager pass with
     # per-launch CUDA events, separate from the timed region
@@ -497,7 +504,7 @@ def main() -> None:
                 "model_tflops": round(step_flops / (ms / 1e3) / 1e12, 1),
                 "model_flops_frac": round(step_flops / (ms / 1e3) / 1e12 / peaks["bf16_sustained"], 4),
                 "cpu_baseline": cpu, "clocks": clk, "loss": round(loss_val, 5),
-            "hbm_peak_gb": round(peak_gb, 1), "attention": attention, **extra}
+            "hbm_peak_gb": round(peak_gb, 1), "step_mode": step_mode, "attention": attention, **extra}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
