@@ -200,8 +200,9 @@ class LatentActionModel:
         return Tensor(self.params["codebook"].data[as_device(arr.astype(np.int64))])
 
     # -- full forward + backward (lam.py:104-129) ---------------------------------
-    def forward(self, frames):
-        """(recon of frames 1..T-1, action indices (B, T-1), losses); losses["total"].backward() trains."""
+    def forward(self, frames, _indices_on_device: bool = False):
+        """(recon of frames 1..T-1, action indices (B, T-1), losses); losses["total"].backward() trains.
+        `_indices_on_device` (internal, training stages): indices stay on device (no host sync)."""
         cfg, P = self.cfg, self.params
         fr = self._frames_device(frames)
         self._check(fr)
@@ -270,4 +271,4 @@ class LatentActionModel:
         losses = {"recon": Tensor(rec_loss), "codebook": Tensor(vq_loss), "commitment": Tensor(vq_loss.clone()),
                   "total": Tensor(total, _backward=backward)}
         return (Tensor(recon.view(B, Tm, cfg.height, cfg.width, cfg.channels)),
-                idx.view(B, Tm).cpu().numpy(), losses)
+                (idx.view(B, Tm) if _indices_on_device else idx.view(B, Tm).cpu().numpy()), losses)

@@ -177,8 +177,11 @@ class VideoTokenizer:
         unit, _ = K.unpatchify(rp, B * T, cfg.height, cfg.width, cfg.channels, cfg.patch)
         return Tensor(unit.view(B, T, cfg.height, cfg.width, cfg.channels))
 
-    def forward(self, frames):
+    def forward(self, frames, _indices_on_device: bool = False):
         """tokenizer.py:134-143: (recon, indices, {"recon","codebook","commitment","total"}).
+
+        `_indices_on_device` (internal, training stages): indices stay a device tensor, so the step
+        has no host synchronisation (the reference API returns a numpy array).
 
         losses["total"].backward() runs the full training backward (trainer.py:211-223): recon MSE
         through to_pixels and the decoder stack, from_latent, the VQ straight-through estimator
@@ -238,7 +241,8 @@ class VideoTokenizer:
 
         losses = {"recon": Tensor(rec_loss), "codebook": Tensor(vq_loss), "commitment": Tensor(vq_loss.clone()),
                   "total": Tensor(total, _backward=backward)}
-        return (Tensor(recon.view(B, T, cfg.height, cfg.width, cfg.channels)), idx.view(B, T, N).cpu().numpy(),
+        idx_out = idx.view(B, T, N) if _indices_on_device else idx.view(B, T, N).cpu().numpy()
+        return (Tensor(recon.view(B, T, cfg.height, cfg.width, cfg.channels)), idx_out,
                 losses)
 
     def encode_device(self, frames) -> torch.Tensor:

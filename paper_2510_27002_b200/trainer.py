@@ -129,25 +129,28 @@ class StageTrainStep:
                 p.grad.zero_()
 
     def step(self, step: int, frames, actions=None):
-        self._zero_grads()
         rng = stream(self.seed, self.stage, "step", step)
+        return self._device_step(frames, actions, rng, wsd_lr(self.schedule, step + 1))
+
+    def _device_step(self, frames, actions, rng, lr: float):
+        """The step's device work (lr is read from device memory while a GraphedStageStep captures it)."""
+        self._zero_grads()
         loss = self.loss_fn(frames, actions, rng)
         loss.backward()
-        adamw_step(self.params, {n: p.grad for n, p in self.params.items()}, self.opt,
-                   wsd_lr(self.schedule, step + 1), check="deferred")
+        adamw_step(self.params, {n: p.grad for n, p in self.params.items()}, self.opt, lr, check="deferred")
         return loss
 
 
 def tokenizer_stage(tokenizer, schedule: WsdSchedule, *, seed: int = 0) -> StageTrainStep:
     """train_tokenizer's loss_fn (trainer.py:220-223): the tokenizer forward's total loss
     (reconstruction MSE + codebook + 0.25 commitment) on uint8 frames."""
-    return StageTrainStep(tokenizer.params, lambda frames, actions, rng: tokenizer.forward(frames)[2]["total"],
+    return StageTrainStep(tokenizer.params, lambda frames, actions, rng: tokenizer.forward(frames, _indices_on_device=True)[2]["total"],
                           schedule, seed=seed, stage="tokenizer")
 
 
 def lam_stage(lam, schedule: WsdSchedule, *, seed: int = 0) -> StageTrainStep:
     """train_lam's loss_fn (trainer.py:254-257): the LAM forward's total loss."""
-    return StageTrainStep(lam.params, lambda frames, actions, rng: lam.forward(frames)[2]["total"],
+    return StageTrainStep(lam.params, lambda frames, actions, rng: lam.forward(frames, _indices_on_device=True)[2]["total"],
                           schedule, seed=seed, stage="lam")
 
 
@@ -229,5 +232,61 @@ class GraphedTrainStep:
         lat = latents.data
         if lat.data_ptr() != self.lat_buf.data_ptr():
             self.lat_buf.copy_(lat, non_blocking=True)
+        self.graph.replay()
+        return self.loss
+
+
+class GraphedStageStep:
+    """A StageTrainStep (tokenizer / LAM) replayed as one CUDA graph per step. The per-step inputs
+    are the frames, copied into the graph's static buffer, and the AdamW scalars, refreshed in device
+    memory. The stage loss functions do not draw from the step generator (trainer.py:220-223,
+    254-257), so nothing else changes. Replays are bit-identical to `stage.step`
+    (tests/test_gpu_stages.py)."""
+
+    RING = 4
+
+    def __init__(self, stage: StageTrainStep):
+        self.tr = stage
+        self.graph = None
+        self.loss = None
+        dev = next(iter(stage.params.values())).data.device
+        self.sc_d = torch.zeros(9, dtype=torch.float32, device=dev)
+        self._unused_state = torch.zeros(11, dtype=torch.int64, device=dev)
+        self._sc_h = [torch.zeros(9, dtype=torch.float32).pin_memory() for _ in range(self.RING)]
+        self._ev = [None] * self.RING
+        self._k = 0
+
+    def step(self, step: int, frames, actions=None):
+        from .optim import _scalars
+        from .sampling import _no_gc
+        tr = self.tr
+        tr.opt.t += 1
+        sc = _scalars(tr.opt, wsd_lr(tr.schedule, step + 1))
+        slot = self._k % self.RING
+        self._k += 1
+        if self._ev[slot] is not None:
+            self._ev[slot].synchronize()
+        hh = self._sc_h[slot]
+        hh.numpy()[:] = [sc["lr"], sc["b1"], sc["b2"], sc["omb1"], sc["omb2"], sc["bc1"], sc["bc2"], sc["eps"],
+                         sc["lrwd"]]
+        self.sc_d.copy_(hh, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ev[slot] = ev
+        if self.graph is None:
+            self.frames_buf = frames.clone()
+            t_saved = tr.opt.t
+            K.DEVSTATE = (self._unused_state, self.sc_d)
+            try:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with _no_gc(), torch.cuda.graph(g):
+                    self.loss = tr._device_step(self.frames_buf, None, None, 0.0)
+            finally:
+                K.DEVSTATE = None
+                tr.opt.t = t_saved
+            self.graph = g
+        if frames.data_ptr() != self.frames_buf.data_ptr():
+            self.frames_buf.copy_(frames, non_blocking=True)
         self.graph.replay()
         return self.loss

@@ -66,3 +66,25 @@ def test_stage_training_reduces_loss_deterministically(kind):
     assert runs[0] == runs[1]
     # VQ code reassignment makes the first steps non-monotone; 15 steps at 1e-3 fit this one batch
     assert runs[0][-1] < 0.95 * runs[0][0], runs[0]
+
+
+@pytest.mark.parametrize("kind", ["tokenizer", "lam"])
+def test_graphed_stage_step_is_bitwise_the_eager_step(kind):
+    from paper_2510_27002_b200.optim import WsdSchedule
+    from paper_2510_27002_b200.trainer import GraphedStageStep, lam_stage, tokenizer_stage
+    frames = _frames(seed=2)
+    sched = WsdSchedule(peak_lr=1e-3, total_steps=50, warmup_steps=3)
+    out = []
+    for graphed in (False, True):
+        m = _models(kind)
+        st = (tokenizer_stage if kind == "tokenizer" else lam_stage)(m, sched)
+        st.step(0, frames)  # eager warm-up
+        runner = GraphedStageStep(st) if graphed else st
+        losses = [float(runner.step(k, frames).data) for k in range(1, 5)]
+        st.opt.raise_if_nonfinite()
+        torch.cuda.synchronize()
+        out.append((losses, {n: p.data.clone() for n, p in m.params.items()}, st.opt.t))
+    assert out[0][0] == out[1][0]
+    assert out[0][2] == out[1][2] == 5
+    for n in out[0][1]:
+        assert torch.equal(out[0][1][n], out[1][1][n]), n
