@@ -176,12 +176,29 @@ def secondary_configs(dev) -> dict:
                         "config": "C2: B=8, T=16, 6 codes; forward + backward + AdamW (trainer.lam_stage), "
                                   f"replayed as {'a CUDA graph' if lam_run is not lam_tr else 'eager steps'}",
                         "model_tflops": round(53.37e9 * 8 * FRAMES_T / (ms2 / 1e3) / 1e12, 1)}
-    # C1: tokenizer forward (encode + VQ + decode), B=2
-    fr2 = fr8[:2]
+    # C1: tokenizer forward (encode + VQ + decode + losses), B=2; static shapes, so the forward is
+    # captured once as a CUDA graph (indices stay on device) and replayed
+    fr2 = fr8[:2].clone()
     tok.forward(fr2)
-    ms1 = _events_ms(lambda: tok.forward(fr2), reps=5)
+    ms1_eager = _events_ms(lambda: tok.forward(fr2), reps=5)
+    ms1, c1_mode = ms1_eager, "eager (indices copied to the host, as the reference API returns them)"
+    try:
+        from paper_2510_27002_b200.sampling import _no_gc
+        tok.forward(fr2, _indices_on_device=True)
+        torch.cuda.synchronize()
+        g1 = torch.cuda.CUDAGraph()
+        with _no_gc(), torch.cuda.graph(g1):
+            tok.forward(fr2, _indices_on_device=True)
+        g1.replay()
+        ms1 = _events_ms(g1.replay, reps=10)
+        c1_mode = "CUDA graph replay (indices on device)"
+    except Exception as exc:
+        c1_mode += f"; graph capture failed: {type(exc).__name__}"
+        torch.cuda.synchronize()
     out["tokenizer_fwd"] = {"metric": "tokenizer fwd+quantize frames/sec", "value": round(2 * FRAMES_T / (ms1 / 1e3), 1),
-                            "unit": "frames/s", "ms_per_step": round(ms1, 2), "config": "C1: B=2, T=16, 1024 codes"}
+                            "unit": "frames/s", "ms_per_step": round(ms1, 2),
+                            "eager_ms_per_step": round(ms1_eager, 2),
+                            "config": f"C1: B=2, T=16, 1024 codes; {c1_mode}"}
 
     # tokenizer training step: forward + full backward + AdamW, B=8
     tok_tr = tokenizer_stage(tok, WsdSchedule(peak_lr=3e-5, total_steps=200_000), seed=0)
