@@ -235,15 +235,33 @@ JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void
 /* ------------------------------------------------------------------------
  * K4  causal temporal (inter-frame) attention (st.py:74-76, nn.py:103-105):
  * for every (b, s) the T rows (b, t, s) attend causally over t.  qkv/out as
- * above with rows ordered (b, t, s); lse f32 [B*S, H, T].  T <= 16, head_dim 64.
+ * above with rows ordered (b, t, s); lse f32 [B*S, H, T].  T <= 32, head_dim 64
+ * (T > 16: two 16-row register tiles, model_dim <= 512 for the backward's shared memory).
  * ---------------------------------------------------------------------- */
 JZ_API int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, int H, int head_dim, void* out,
                                 float* lse, jz_stream_t stream);
 /* colsum_part (nullable): fp32 [jz_attn_temporal_colsum_parts(B, S)][3*H*64], as the spatial one. */
 JZ_API int64_t jz_attn_temporal_colsum_parts(int64_t B, int S);
+/* out: the forward output; not read (Delta_t = sum_j P_tj dP_tj is formed from the kernel's fp32
+ * P and dP registers, which removes the O read and the dP - Delta cancellation against a bf16 O);
+ * kept for interface stability, may be NULL. */
 JZ_API int jz_attn_temporal_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                                 int64_t B, int T, int S, int H, int head_dim, void* dqkv, float* colsum_part,
                                 jz_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K3s spatial attention of small frames, S <= 32 (st.py:73, nn.py:80-110,
+ * causal=False): the reference's patch-16 presets (S = 16/17), the MAE
+ * tokenizer (S = 16) and the ST-DiT (S = N + 2, diffusion.py:164-180).
+ * Register-tile MMAs, one CTA per frame.  qkv/out/lse in the K3 layouts
+ * (lse f32 [frames, H, S]); the backward's `out` is not read (may be NULL), as K4's.
+ * colsum_part (nullable): fp32 [frames][3*H*64] partial column sums of dqkv.
+ * ---------------------------------------------------------------------- */
+JZ_API int jz_attn_spatial_small_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
+                                     float* lse, jz_stream_t stream);
+JZ_API int jz_attn_spatial_small_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                                     int64_t frames, int S, int H, int head_dim, void* dqkv, float* colsum_part,
+                                     jz_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K9  frames -> patches and back (tokenizer.py:49-55, nn.py:113-131).

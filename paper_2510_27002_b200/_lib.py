@@ -58,6 +58,8 @@ PROTOTYPES: dict[str, list] = {
     "jz_attn_spatial_bwd_workspace_bytes": [_I64, _I32, _I32],
     "jz_attn_temporal_fwd": [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
     "jz_attn_temporal_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "jz_attn_spatial_small_fwd": [_P, _I64, _I32, _I32, _I32, _P, _P, _P],
+    "jz_attn_spatial_small_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P],
     "jz_patchify": [_P, _I32, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
     "jz_unpatchify": [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
     "jz_assemble_fwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P],

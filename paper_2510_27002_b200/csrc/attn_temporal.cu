@@ -281,11 +281,9 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
   const int64_t bs = blockIdx.x;
   const int64_t b = bs / S, s = bs - b * S;
   __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
-  __nv_bfloat16* so = sq + 16 * ldq;
-  __nv_bfloat16* sdo = so + 16 * ldo;
+  __nv_bfloat16* sdo = sq + 16 * ldq;
   __nv_bfloat16* sp_all = sdo + 16 * ldo;
   stage_rows(sq, ldq, qkv, 3 * D, 3 * D, b, T, S, s);
-  stage_rows(so, ldo, o, D, D, b, T, S, s);
   stage_rows(sdo, ldo, dout, D, D, b, T, S, s);
   cp_async_wait_all();
   __syncthreads();
@@ -295,27 +293,16 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
   const __nv_bfloat16* q = sq + h * HD;
   const __nv_bfloat16* k = sq + D + h * HD;
   const __nv_bfloat16* v = sq + 2 * D + h * HD;
-  const __nv_bfloat16* og = so + h * HD;
   const __nv_bfloat16* dog = sdo + h * HD;
   const int r0 = L >> 2, cq = 2 * (L & 3);
-  // D_t = sum_d dO[t][d] O[t][d]: lane -> row L%16, half L/16
-  float Dp = 0.f;
-  {
-    const int t = L & 15, d0 = 32 * (L >> 4);
-#pragma unroll
-    for (int d = 0; d < 32; d += 2) {
-      const float2 a = unpack_bf16(*reinterpret_cast<const uint32_t*>(og + t * ldo + d0 + d));
-      const float2 g = unpack_bf16(*reinterpret_cast<const uint32_t*>(dog + t * ldo + d0 + d));
-      Dp += a.x * g.x + a.y * g.y;
-    }
-    Dp += __shfl_xor_sync(0xffffffffu, Dp, 16);
-  }
-  const float D0 = __shfl_sync(0xffffffffu, Dp, r0), D1 = __shfl_sync(0xffffffffu, Dp, r0 + 8);
   const float* lp = lse + (bs * H + h) * T;
   const float L0 = r0 < T ? lp[r0] : 0.f, L1 = r0 + 8 < T ? lp[r0 + 8] : 0.f;
   float P[2][4], dS[2][4];
   xyT(P, q, ldq, k, ldq);
   xyT(dS, dog, ldo, v, ldq);
+  // Delta_t = sum_j P_tj dP_tj from the fp32 registers (= dO_t . O_t in exact arithmetic): no O
+  // read, and dP - Delta does not cancel against the bf16 rounding of a stored O
+  float D0 = 0.f, D1 = 0.f;
 #pragma unroll
   for (int n = 0; n < 2; ++n)
 #pragma unroll
@@ -323,8 +310,14 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
       const int row = r0 + 8 * (e >> 1), col = 8 * n + cq + (e & 1);
       const float p = (col <= row && row < T) ? __expf(P[n][e] * scale - (e < 2 ? L0 : L1)) : 0.f;
       P[n][e] = p;
-      dS[n][e] = p * (dS[n][e] - (e < 2 ? D0 : D1));
+      if (e < 2) D0 += p * dS[n][e]; else D1 += p * dS[n][e];
     }
+  D0 = quad_sum(D0);
+  D1 = quad_sum(D1);
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dS[n][e] = P[n][e] * (dS[n][e] - (e < 2 ? D0 : D1));
   c_to_smem(sP, P);
   c_to_smem(sdS, dS);
   __syncwarp();
@@ -363,10 +356,307 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row-tile attention over L <= 16 * NT rows of one slot, causal or not (NT = 1, 2).
+//
+// The same (b, t, s) addressing serves two sub-layers:
+//  - spatial attention of small frames (st.py:73, causal=False), S_sp <= 32: the reference's
+//    patch-16 presets (S = 16 / 17), the MAE tokenizer (S = 16) and the ST-DiT (S = N + 2 = 18,
+//    diffusion.py:164-180). Launched with B := frames, T := S_sp, S := 1, so a slot's rows are
+//    the frame's contiguous tokens and lse lands as [frame][H][S_sp], the K3 layout;
+//  - causal temporal attention with 16 < T <= 32 (st.py:74-76).
+// Per warp (= head): query tile qt against all NT key tiles in registers (m16n8k16), P / dS
+// tiles staged per warp in shared memory for the transposed dK / dV products. The backward
+// forms Delta = sum_j P_ij dP_ij from its fp32 registers, as the T <= 16 kernel does (the forward
+// output is not read). Tiles wholly above the causal
+// diagonal are computed and masked (at most one per warp).
+// ---------------------------------------------------------------------------
+namespace tp {
+
+// stage rows t = 0..R-1 (zero rows >= T), as stage_rows
+JZ_DEV void stage_rows_n(__nv_bfloat16* dst, int ld, int R, const __nv_bfloat16* src, int64_t src_ld, int cols,
+                         int64_t b, int T, int S, int64_t s) {
+  const int c16 = cols / 8;
+  for (int i = threadIdx.x; i < R * c16; i += blockDim.x) {
+    const int t = i / c16, c = i - t * c16;
+    if (t < T)
+      cp_async16(dst + t * ld + 8 * c, src + ((b * T + t) * S + s) * src_ld + 8 * c);
+    else
+      *reinterpret_cast<uint4*>(dst + t * ld + 8 * c) = make_uint4(0, 0, 0, 0);
+  }
+}
+
+// o += A . B (B stored [k][n] pitch ld), o as av_frag
+JZ_DEV void av_acc(const uint32_t (&a)[4], const __nv_bfloat16* bsm, int ld, float (&o)[HD / 16][8]) {
+#pragma unroll
+  for (int np = 0; np < HD / 16; ++np) {
+    uint32_t bb[4];
+    load_b_kn(bb, bsm, ld, 16 * np);
+    float o0[4] = {o[np][0], o[np][1], o[np][2], o[np][3]}, o1[4] = {o[np][4], o[np][5], o[np][6], o[np][7]};
+    mma16816(o0, a, bb[0], bb[1]);
+    mma16816(o1, a, bb[2], bb[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      o[np][e] = o0[e];
+      o[np][4 + e] = o1[e];
+    }
+  }
+}
+
+JZ_DEV void zero_frag(float (&o)[HD / 16][8]) {
+#pragma unroll
+  for (int np = 0; np < HD / 16; ++np)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[np][e] = 0.f;
+}
+
+// C-layout 16x16 -> bf16 smem tile (pitch ld)
+JZ_DEV void c_to_smem_ld(__nv_bfloat16* dst, int ld, const float (&c)[2][4]) {
+  const int L = lane_id();
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+#pragma unroll
+  for (int n = 0; n < 2; ++n) {
+    *reinterpret_cast<uint32_t*>(dst + r0 * ld + 8 * n + cq) = pack_bf16(c[n][0], c[n][1]);
+    *reinterpret_cast<uint32_t*>(dst + (r0 + 8) * ld + 8 * n + cq) = pack_bf16(c[n][2], c[n][3]);
+  }
+}
+
+}  // namespace tp
+
+template <int NT>
+__global__ void __launch_bounds__(512) rowtile_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int S, int H,
+                                                          int causal, __nv_bfloat16* __restrict__ out,
+                                                          float* __restrict__ lse, float scale) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  constexpr int R = 16 * NT;
+  const int D = H * HD;
+  const int ld = 3 * D + 8;
+  const int64_t bs = blockIdx.x;
+  const int64_t b = bs / S, s = bs - b * S;
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  stage_rows_n(sq, ld, R, qkv, 3 * D, 3 * D, b, T, S, s);
+  cp_async_wait_all();
+  __syncthreads();
+  const int h = warp_id(), L = lane_id();
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+  float* lp = lse + (bs * H + h) * T;
+#pragma unroll
+  for (int qt = 0; qt < NT; ++qt) {
+    float sc[NT][2][4];
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt) xyT(sc[kt], sq + 16 * qt * ld + h * HD, ld, sq + 16 * kt * ld + D + h * HD, ld);
+    float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = 16 * qt + r0 + 8 * (e >> 1), col = 16 * kt + 8 * n + cq + (e & 1);
+          const bool ok = col < T && (!causal || col <= row);
+          const float x = ok ? sc[kt][n][e] * scale : -INFINITY;
+          sc[kt][n][e] = x;
+          if (e < 2) m0 = fmaxf(m0, x); else m1 = fmaxf(m1, x);
+        }
+    m0 = quad_max(m0);
+    m1 = quad_max(m1);
+    float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p = __expf(sc[kt][n][e] - (e < 2 ? m0 : m1));
+          sc[kt][n][e] = p;
+          if (e < 2) l0 += p; else l1 += p;
+        }
+    l0 = quad_sum(l0);
+    l1 = quad_sum(l1);
+    float o[HD / 16][8];
+    zero_frag(o);
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt) {
+      uint32_t pa[4];
+      c_to_a(pa, sc[kt]);
+      av_acc(pa, sq + 16 * kt * ld + 2 * D + h * HD, ld, o);
+    }
+    __syncwarp();  // this head's q rows of tile qt are consumed: O overwrites them in place
+    frag_to_smem(o, sq + 16 * qt * ld, ld, h * HD, 1.0f / l0, 1.0f / l1);
+    if ((L & 3) == 0) {
+      const int ra = 16 * qt + r0;
+      if (ra < T) lp[ra] = m0 + logf(l0);
+      if (ra + 8 < T) lp[ra + 8] = m1 + logf(l1);
+    }
+  }
+  __syncthreads();
+  const int c16 = D / 8;
+  for (int i = threadIdx.x; i < T * c16; i += blockDim.x) {
+    const int t = i / c16, c = i - t * c16;
+    *reinterpret_cast<uint4*>(out + ((b * T + t) * S + s) * D + 8 * c) = *reinterpret_cast<const uint4*>(sq + t * ld + 8 * c);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(512) rowtile_bwd_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                          const __nv_bfloat16* __restrict__ o,
+                                                          const __nv_bfloat16* __restrict__ dout,
+                                                          const float* __restrict__ lse, int T, int S, int H,
+                                                          int causal, __nv_bfloat16* __restrict__ dqkv, float scale,
+                                                          float* __restrict__ colsum) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  constexpr int R = 16 * NT, LDR = R + 8;
+  const int D = H * HD;
+  const int ldq = 3 * D + 8, ldo = D + 8;
+  const int64_t bs = blockIdx.x;
+  const int64_t b = bs / S, s = bs - b * S;
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* so = sq + R * ldq;  // dQ staging (each warp its own head's columns)
+  __nv_bfloat16* sdo = so + R * ldo;
+  __nv_bfloat16* sp_all = sdo + R * ldo;
+  stage_rows_n(sq, ldq, R, qkv, 3 * D, 3 * D, b, T, S, s);
+  stage_rows_n(sdo, ldo, R, dout, D, D, b, T, S, s);
+  cp_async_wait_all();
+  __syncthreads();
+  const int h = warp_id(), L = lane_id();
+  __nv_bfloat16* sP = sp_all + h * 2 * R * LDR;
+  __nv_bfloat16* sdS = sP + R * LDR;
+  const __nv_bfloat16* q = sq + h * HD;
+  const __nv_bfloat16* k = sq + D + h * HD;
+  const __nv_bfloat16* v = sq + 2 * D + h * HD;
+  const __nv_bfloat16* dog = sdo + h * HD;
+  const int r0 = L >> 2, cq = 2 * (L & 3);
+  const float* lp = lse + (bs * H + h) * T;
+#pragma unroll
+  for (int qt = 0; qt < NT; ++qt) {
+    const int ra = 16 * qt + r0;
+    const float L0 = ra < T ? lp[ra] : 0.f, L1 = ra + 8 < T ? lp[ra + 8] : 0.f;
+    float P[NT][2][4], dS[NT][2][4];
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt) {
+      xyT(P[kt], q + 16 * qt * ldq, ldq, k + 16 * kt * ldq, ldq);
+      xyT(dS[kt], dog + 16 * qt * ldo, ldo, v + 16 * kt * ldq, ldq);
+    }
+    float D0 = 0.f, D1 = 0.f;
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = ra + 8 * (e >> 1), col = 16 * kt + 8 * n + cq + (e & 1);
+          const bool ok = row < T && col < T && (!causal || col <= row);
+          const float p = ok ? __expf(P[kt][n][e] * scale - (e < 2 ? L0 : L1)) : 0.f;
+          P[kt][n][e] = p;
+          if (e < 2) D0 += p * dS[kt][n][e]; else D1 += p * dS[kt][n][e];
+        }
+    // Delta over the whole key row from the fp32 registers (no O read; no bf16-O cancellation)
+    D0 = quad_sum(D0);
+    D1 = quad_sum(D1);
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dS[kt][n][e] = P[kt][n][e] * (dS[kt][n][e] - (e < 2 ? D0 : D1));
+    float oq[HD / 16][8];
+    zero_frag(oq);
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt) {
+      c_to_smem_ld(sP + 16 * qt * LDR + 16 * kt, LDR, P[kt]);
+      c_to_smem_ld(sdS + 16 * qt * LDR + 16 * kt, LDR, dS[kt]);
+      uint32_t a[4];
+      c_to_a(a, dS[kt]);
+      av_acc(a, k + 16 * kt * ldq, ldq, oq);  // dQ_qt += dS_(qt,kt) K_kt
+    }
+    frag_to_smem(oq, so + 16 * qt * ldo, ldo, h * HD, scale, scale);
+  }
+  __syncwarp();
+  // dK_kt = scale * sum_qt dS_(qt,kt)^T Q_qt, dV_kt = sum_qt P_(qt,kt)^T dO_qt; K and V are consumed
+#pragma unroll
+  for (int kt = 0; kt < NT; ++kt) {
+    float gk[HD / 16][8], gv[HD / 16][8];
+    zero_frag(gk);
+    zero_frag(gv);
+#pragma unroll
+    for (int qt = 0; qt < NT; ++qt) {
+      uint32_t a[4];
+      load_a_trans(a, sdS + 16 * qt * LDR + 16 * kt, LDR);
+      av_acc(a, q + 16 * qt * ldq, ldq, gk);
+      load_a_trans(a, sP + 16 * qt * LDR + 16 * kt, LDR);
+      av_acc(a, dog + 16 * qt * ldo, ldo, gv);
+    }
+    frag_to_smem(gk, sq + 16 * kt * ldq, ldq, D + h * HD, scale, scale);
+    frag_to_smem(gv, sq + 16 * kt * ldq, ldq, 2 * D + h * HD, 1.0f, 1.0f);
+  }
+  __syncthreads();
+  // coalesced write-out of the T rows: dQ from the O buffer, dK | dV from the qkv buffer
+  const int c16 = 3 * D / 8, cq16 = D / 8;
+  for (int i = threadIdx.x; i < T * c16; i += blockDim.x) {
+    const int t = i / c16, c = i - t * c16;
+    const __nv_bfloat16* src = c < cq16 ? so + t * ldo + 8 * c : sq + t * ldq + 8 * c;
+    *reinterpret_cast<uint4*>(dqkv + ((b * T + t) * S + s) * (3 * D) + 8 * c) = *reinterpret_cast<const uint4*>(src);
+  }
+  if (colsum) {
+    float* part = colsum + bs * (3 * D);
+    for (int c2 = threadIdx.x; c2 < 3 * D / 2; c2 += blockDim.x) {
+      float s0 = 0.f, s1 = 0.f;
+      for (int t = 0; t < T; ++t) {
+        const __nv_bfloat16* src = 2 * c2 < D ? so + t * ldo + 2 * c2 : sq + t * ldq + 2 * c2;
+        const float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(src));
+        s0 += f.x;
+        s1 += f.y;
+      }
+      *reinterpret_cast<float2*>(part + 2 * c2) = make_float2(s0, s1);
+    }
+  }
+}
+
+constexpr size_t kRowTileSmemMax = 227 * 1024;
+
+template <int NT>
+static int launch_rowtile(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B, int T,
+                          int S, int H, int causal, void* out, cudaStream_t st, float* colsum) {
+  constexpr int R = 16 * NT;
+  const float scale = 0.125f;
+  const int64_t BS = B * S;
+  if (BS == 0) return JZ_OK;
+  const int D = H * HD;
+  const int threads = 32 * H;
+  if (!bwd) {
+    const size_t smem = (size_t)R * (3 * D + 8) * 2;
+    JZ_CHECK_ARG(smem <= kRowTileSmemMax, "row-tile attention: %d rows x %d heads exceed shared memory", T, H);
+    JZ_CUDA_TRY(cudaFuncSetAttribute(rowtile_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rowtile_fwd_kernel<NT><<<(unsigned)BS, threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), T, S, H,
+                                                                causal, reinterpret_cast<__nv_bfloat16*>(out), lse,
+                                                                scale);
+  } else {
+    const size_t smem = (size_t)R * (3 * D + 8) * 2 + (size_t)2 * R * (D + 8) * 2 + (size_t)H * 2 * R * (R + 8) * 2;
+    JZ_CHECK_ARG(smem <= kRowTileSmemMax, "row-tile attention backward: %d rows x %d heads exceed shared memory", T,
+                 H);
+    JZ_CUDA_TRY(cudaFuncSetAttribute(rowtile_bwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rowtile_bwd_kernel<NT><<<(unsigned)BS, threads, smem, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(o),
+        reinterpret_cast<const __nv_bfloat16*>(dout), lse, T, S, H, causal, reinterpret_cast<__nv_bfloat16*>(out),
+        scale, colsum);
+  }
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
+static int dispatch_rowtile(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B, int T,
+                            int S, int H, int causal, void* out, cudaStream_t st, float* colsum) {
+  JZ_CHECK_ARG(H >= 1 && H <= 16, "row-tile attention: heads %d unsupported (<= 16)", H);
+  JZ_CHECK_ARG(T >= 1 && T <= 32, "row-tile attention: %d rows unsupported (<= 32)", T);
+  if (T <= 16) return launch_rowtile<1>(bwd, qkv, o, dout, lse, B, T, S, H, causal, out, st, colsum);
+  return launch_rowtile<2>(bwd, qkv, o, dout, lse, B, T, S, H, causal, out, st, colsum);
+}
+
 static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B,
                              int T, int S, int H, void* out, cudaStream_t st, float* colsum = nullptr) {
   JZ_CHECK_ARG(H >= 1 && H <= 16, "temporal attention: heads %d unsupported (<= 16)", H);
-  JZ_CHECK_ARG(T >= 1 && T <= 16, "temporal attention: T=%d unsupported (<= 16)", T);
+  JZ_CHECK_ARG(T >= 1 && T <= 32, "temporal attention: T=%d unsupported (<= 32)", T);
+  if (T > 16) return dispatch_rowtile(bwd, qkv, o, dout, lse, B, T, S, H, 1, out, st, colsum);
   const float scale = 0.125f;  // 1/sqrt(64)
   const int64_t BS = B * S;
   if (BS == 0) return JZ_OK;
@@ -378,7 +668,7 @@ static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const voi
     temporal_fwd_kernel<<<(unsigned)BS, threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), T, S, H,
                                                              reinterpret_cast<__nv_bfloat16*>(out), lse, scale);
   } else {
-    const size_t smem = (size_t)16 * (3 * D + 8) * 2 + (size_t)2 * 16 * (D + 8) * 2 + (size_t)H * 2 * 16 * LDP * 2;
+    const size_t smem = (size_t)16 * (3 * D + 8) * 2 + (size_t)16 * (D + 8) * 2 + (size_t)H * 2 * 16 * LDP * 2;
     JZ_CUDA_TRY(cudaFuncSetAttribute(temporal_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     temporal_bwd_kernel<<<(unsigned)BS, threads, smem, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(o),
@@ -407,4 +697,19 @@ extern "C" int jz_attn_temporal_bwd(const void* qkv, const void* out, const void
   JZ_CHECK_ARG(head_dim == 64, "temporal attention: head_dim %d unsupported (64)", head_dim);
   return dispatch_temporal(true, qkv, out, dout, const_cast<float*>(lse), B, T, S, H, dqkv,
                            reinterpret_cast<cudaStream_t>(s), colsum_part);
+}
+
+extern "C" int jz_attn_spatial_small_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
+                                         float* lse, jz_stream_t s) {
+  JZ_CHECK_ARG(head_dim == 64, "small spatial attention: head_dim %d unsupported (64)", head_dim);
+  return dispatch_rowtile(false, qkv, nullptr, nullptr, lse, frames, S, 1, H, 0, out,
+                          reinterpret_cast<cudaStream_t>(s), nullptr);
+}
+
+extern "C" int jz_attn_spatial_small_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                                         int64_t frames, int S, int H, int head_dim, void* dqkv, float* colsum_part,
+                                         jz_stream_t s) {
+  JZ_CHECK_ARG(head_dim == 64, "small spatial attention: head_dim %d unsupported (64)", head_dim);
+  return dispatch_rowtile(true, qkv, out, dout, const_cast<float*>(lse), frames, S, 1, H, 0, dqkv,
+                          reinterpret_cast<cudaStream_t>(s), colsum_part);
 }

@@ -276,10 +276,20 @@ def layernorm_bwd(x, mean, rstd, g, dy, dres, *, accumulate: bool, dres_bf16=Non
 # --------------------------------------------------------------------------
 # attention
 # --------------------------------------------------------------------------
+SMALL_S = 32  # spatial sequence lengths served by the register-tile kernel (K3s)
+
+
 def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: bool = True):
-    """-> (out bf16, out fp32 or None, lse)."""
+    """-> (out bf16, out fp32 or None, lse).  S <= 32 runs the register-tile kernel (K3s), whose
+    backward takes the bf16 output: no fp32 copy is written then."""
     D = H * 64
     out = torch.empty(frames * S, D, dtype=BF16, device=qkv.device)
+    if S <= SMALL_S:
+        lse = torch.empty(frames, H, S, dtype=F32, device=qkv.device)
+        e0 = _fam_begin()
+        L.call("jz_attn_spatial_small_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), lse.data_ptr(), _s())
+        _fam_end(e0, "spatial_small_fwd", 4 * frames * H * S * S * 64, frames * S * (3 * D * 2 + D * 2 + H * 4))
+        return out, None, lse
     out32 = torch.empty(frames * S, D, dtype=F32, device=qkv.device) if keep_f32 else None
     lse = torch.empty(frames, H, S, dtype=F32, device=qkv.device)
     e0 = _fam_begin()
@@ -291,9 +301,25 @@ def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: b
 
 
 def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=None, colsum=None):
-    """colsum (fp32 [3*H*64], optional): also the column sums of dqkv (QKV bias gradient)."""
+    """colsum (fp32 [3*H*64], optional): also the column sums of dqkv (QKV bias gradient).
+    out_f32: the forward's fp32 output (S in {256, 257}) or its bf16 output (S <= 32)."""
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
+    if S <= SMALL_S:
+        if out_f32.dtype != BF16:
+            raise ValueError("small-frame spatial attention backward takes the bf16 forward output")
+        part, nparts = None, 0
+        if colsum is not None:
+            nparts = frames
+            part = scratch("attn_colsum", nparts * 3 * H * 64)
+        e0 = _fam_begin()
+        L.call("jz_attn_spatial_small_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames,
+               S, H, 64, dqkv.data_ptr(), _p(part), _s())
+        D = H * 64
+        _fam_end(e0, "spatial_small_bwd", 10 * frames * H * S * S * 64, frames * S * (3 * D * 2 + D * 2 + 3 * D * 2))
+        if colsum is not None:
+            reduce_partials(part, nparts, 3 * H * 64, colsum)
+        return dqkv
     ws = scratch("attn_uvb", L.load().jz_attn_spatial_bwd_workspace_bytes(frames, S, H) // 4)
     part, nparts = None, 0
     if colsum is not None:
@@ -333,8 +359,9 @@ def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=
     L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, T, S, H, 64,
            dqkv.data_ptr(), _p(part), _s())
     D = H * 64
+    # bytes: qkv and dO in, dqkv out (Delta comes from the in-register P and dP: O is not read)
     _fam_end(e0, "temporal_bwd", 10 * 64 * B * S * H * (T * (T + 1) // 2),
-             B * T * S * (3 * D * 2 + 2 * D * 2 + 3 * D * 2))
+             B * T * S * (3 * D * 2 + D * 2 + 3 * D * 2))
     if colsum is not None:
         reduce_partials(part, nparts, 3 * H * 64, colsum)
     return dqkv

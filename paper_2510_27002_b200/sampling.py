@@ -149,6 +149,8 @@ class FrameDecoder:
         self.S = self.N + 1
         self.t_max = t_max or cfg.max_frames
         check_supported(cfg.st, self.S, self.t_max)
+        if self.t_max > 16:
+            raise ValueError(f"KV-cached decoding supports up to 16 frames (got t_max={self.t_max})")
         dev = model.params["token_embed"].data.device
         self.cache = [torch.empty(B, self.t_max, self.S, 2 * self.D, dtype=torch.bfloat16, device=dev)
                       for _ in range(cfg.blocks)]

@@ -98,10 +98,13 @@ def check_supported(cfg: StConfig, S: int, T: int) -> None:
         raise ValueError(f"device ST stack needs head_dim 64 (got {cfg.model_dim // cfg.heads})")
     if cfg.model_dim % 128 or cfg.model_dim > 1024:
         raise ValueError(f"device ST stack needs model_dim % 128 == 0 and <= 1024 (got {cfg.model_dim})")
-    if S not in (256, 257):
-        raise ValueError(f"device spatial attention supports S in (256, 257), got {S}")
-    if T > 16:
-        raise ValueError(f"device temporal attention supports T <= 16, got {T}")
+    if S not in (256, 257) and not 1 <= S <= 32:
+        raise ValueError(f"device spatial attention supports S in (256, 257) or S <= 32, got {S}")
+    if T > 32:
+        raise ValueError(f"device temporal attention supports T <= 32, got {T}")
+    if (S > 16 and S <= 32) or T > 16:
+        if cfg.model_dim > 512:
+            raise ValueError(f"device attention over 17..32 rows needs model_dim <= 512 (got {cfg.model_dim})")
 
 
 # --------------------------------------------------------------------------
@@ -260,7 +263,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         # epilogue), d b_k = sum_k dK_k = 0 exactly (shift invariance), only d b_q reads dq.
         K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao,
                     colsum=gbs[2 * d:] if gbs is not None else None)
-        dqkv = K.attn_spatial_bwd(c["qkv"], c["ao32"], dao, c["lse_s"], frames, S, H, dqkv=dqkv)
+        o_saved = c["ao32"] if c["ao32"] is not None else c["ao"]  # bf16 O for S <= 32
+        dqkv = K.attn_spatial_bwd(c["qkv"], o_saved, dao, c["lse_s"], frames, S, H, dqkv=dqkv)
         if gbs is not None:
             gbs[d:2 * d].zero_()
             K.colsum_bf16(dqkv, gbs[:d], cols=d)

@@ -245,6 +245,67 @@ def test_attn_temporal_fwd_bwd(T):
             assert rel(got, ref) < 2e-2, "qkv"[i]
 
 
+@pytest.mark.parametrize("T", [17, 24, 32])
+def test_attn_temporal_long_clip(T):
+    """16 < T <= 32: two 16-row register tiles, the diagonal-crossing key tile masked."""
+    B, S, H = 2, 17, 8
+    D = H * 64
+    g = torch.Generator(device=dev).manual_seed(100 + T)
+    qkv = (torch.randn(B * T * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
+    out, lse = Kn.attn_temporal_fwd(qkv, B, T, S, H)
+    qf = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = _ref_attn(qf.reshape(B, T, S, 3 * D).transpose(1, 2), (B, S), T, H, True)
+    assert rel(out.reshape(B, T, S, D).transpose(1, 2), o_ref) < 1e-2
+    assert rel(lse.reshape(B, S, H, T), lse_ref) < 1e-4
+    go = torch.randn(o_ref.shape, device=dev, generator=g)
+    o_ref.backward(go)
+    dout = go.transpose(1, 2).reshape(B * T * S, D).bfloat16().contiguous()
+    cs = torch.full((3 * D,), float("nan"), device=dev)
+    dqkv = Kn.attn_temporal_bwd(qkv, out, dout, lse, B, T, S, H, colsum=cs)
+    cs_ref = torch.empty_like(cs)
+    Kn.colsum_bf16(dqkv, cs_ref)
+    assert rel(cs, cs_ref) < 1e-5
+    for i in range(3):
+        assert rel(dqkv[:, i * D:(i + 1) * D].float(), qf.grad[:, i * D:(i + 1) * D]) < 2e-2, "qkv"[i]
+
+
+@pytest.mark.parametrize("S,H", [(16, 8), (17, 8), (18, 8), (32, 8), (5, 2), (1, 4), (24, 16)])
+def test_attn_spatial_small_fwd_bwd(S, H):
+    """S <= 32 (patch-16 presets, MAE S = 16, ST-DiT S = 18): the register-tile kernel, non-causal."""
+    frames = 37
+    D = H * 64
+    g = torch.Generator(device=dev).manual_seed(S * 31 + H)
+    qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
+    if S > 16 and H > 8:  # the backward's shared memory bounds 17..32 rows to model_dim 512
+        with pytest.raises(ValueError, match="shared memory"):
+            out, _, lse = Kn.attn_spatial_fwd(qkv, frames, S, H)
+            Kn.attn_spatial_bwd(qkv, out, torch.zeros_like(out), lse, frames, S, H)
+        return
+    out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+    assert out32 is None  # the small kernel's backward reads the bf16 output
+    qf = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = _ref_attn(qf.reshape(frames, S, 3 * D), (frames,), S, H, False)
+    assert rel(out.reshape(frames, S, D), o_ref) < 1e-2
+    assert rel(lse, lse_ref) < 1e-4
+    go = torch.randn(o_ref.shape, device=dev, generator=g)
+    o_ref.backward(go)
+    dqkv = torch.full_like(qkv, float("nan"))
+    cs = torch.full((3 * D,), float("nan"), device=dev)
+    Kn.attn_spatial_bwd(qkv, out, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
+                        colsum=cs)
+    assert torch.isfinite(dqkv.float()).all()
+    cs_ref = torch.empty_like(cs)
+    Kn.colsum_bf16(dqkv, cs_ref)
+    assert rel(cs, cs_ref) < 1e-5
+    vscale = float(qf.grad[:, 2 * D:].norm())
+    for i in range(3):
+        got, ref = dqkv[:, i * D:(i + 1) * D].float(), qf.grad[:, i * D:(i + 1) * D]
+        if S == 1 and i < 2:
+            assert float(got.norm()) < 1e-3 * vscale, "qkv"[i]
+        else:
+            assert rel(got, ref) < 2e-2, "qkv"[i]
+
+
 # ---------------------------------------------------------------------------------------------
 # column sums / partial-row reductions (bias and LayerNorm parameter gradients): every thread
 # layout the kernels pick (row groups for cols/8 < 256, a column loop above), ragged row counts,
