@@ -591,3 +591,107 @@ def wsd_lr(peak_lr, total_steps, warmup_steps, decay_fraction, step) -> float:  
 
 def params_to_torch(np_params: dict, requires_grad=True) -> dict:
     return _as_params(np_params, requires_grad)
+
+
+# --------------------------------------------------------------------------
+# ST-DiT diffusion-forcing dynamics (diffusion.py:114-215): test oracle only
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DitCfg:  # diffusion.py:114-128
+    model_dim: int = 512
+    heads: int = 8
+    ffn_dim: int = 2048
+    blocks: int = 6
+    latent_dim: int = 32
+    action_latent_dim: int = 32
+    action_vocab: int = 7
+    patches_per_frame: int = 16
+    max_frames: int = 16
+
+    @property
+    def st(self) -> StCfg:
+        return StCfg(self.model_dim, self.heads, self.ffn_dim, self.blocks)
+
+
+def sinusoidal_embedding(values, dim: int) -> np.ndarray:  # nn.py:134-142 (float32 throughout)
+    half = dim // 2
+    freqs = np.exp(-math.log(10000.0) * np.arange(half, dtype=np.float32) / max(half - 1, 1))
+    angles = np.asarray(values, dtype=np.float32)[..., None] * freqs * 1000.0
+    emb = np.concatenate([np.sin(angles), np.cos(angles)], axis=-1)
+    if dim % 2:
+        emb = np.concatenate([emb, np.zeros(emb.shape[:-1] + (1,), dtype=np.float32)], axis=-1)
+    return emb
+
+
+def init_dit(cfg: DitCfg, seed=0, dtype=np.float32) -> dict:  # diffusion.py:134-154 (draw order)
+    g = orng.stream(seed, "dit-init")
+    d = cfg.model_dim
+    p = {}
+    p["latent_embed.w"] = g.normal(0, 0.02, (cfg.latent_dim, d)).astype(dtype)
+    p["latent_embed.b"] = np.zeros(d, dtype=dtype)
+    p["action_proj.w"] = g.normal(0, 0.02, (cfg.action_latent_dim, d)).astype(dtype)
+    p["action_proj.b"] = np.zeros(d, dtype=dtype)
+    p["null_action"] = g.normal(0, 0.02, (cfg.action_latent_dim,)).astype(dtype)
+    p["gt_action_embed"] = g.normal(0, 0.02, (cfg.action_vocab, cfg.action_latent_dim)).astype(dtype)
+    p["noise_proj.w"] = g.normal(0, 0.02, (d, d)).astype(dtype)
+    p["noise_proj.b"] = np.zeros(d, dtype=dtype)
+    p["pos_spatial"] = g.normal(0, 0.02, (cfg.patches_per_frame + 2, d)).astype(dtype)
+    p["pos_temporal"] = g.normal(0, 0.02, (cfg.max_frames, d)).astype(dtype)
+    p.update(init_st_stack(g, cfg.st, "dit", dtype))
+    p["to_latent.w"] = g.normal(0, 0.02, (d, cfg.latent_dim)).astype(dtype)
+    p["to_latent.b"] = np.zeros(cfg.latent_dim, dtype=dtype)
+    return p
+
+
+def forcing_corrupt(latents: np.ndarray, tau, gen: np.random.Generator) -> np.ndarray:  # diffusion.py:106-111
+    tau = np.asarray(tau, dtype=latents.dtype)[..., None, None]
+    eps = gen.standard_normal(latents.shape).astype(latents.dtype)
+    return (1.0 - tau) * latents + tau * eps
+
+
+def dit_predict_clean(P, cfg: DitCfg, noised: np.ndarray, tau, action_latents):  # diffusion.py:164-180
+    b, t, n, _ = noised.shape
+    d = cfg.model_dim
+    dtype = P["latent_embed.w"].dtype
+    if action_latents.shape[1] != t - 1:  # _conditioning, diffusion.py:156-162
+        raise ValueError(f"need {t - 1} actions for {t} frames")
+    x = linear(torch.as_tensor(noised).to(dtype), P["latent_embed.w"], P["latent_embed.b"])
+    null = P["null_action"].reshape(1, 1, -1) + torch.zeros(b, 1, cfg.action_latent_dim, dtype=dtype)
+    act = linear(torch.cat([null, action_latents], dim=1), P["action_proj.w"], P["action_proj.b"])
+    noise_emb = torch.as_tensor(sinusoidal_embedding(tau, d)).to(dtype)
+    noise_tok = linear(noise_emb, P["noise_proj.w"], P["noise_proj.b"])
+    x = torch.cat([act.reshape(b, t, 1, d), noise_tok.reshape(b, t, 1, d), x], dim=2)
+    x = x + P["pos_spatial"]
+    x = x + P["pos_temporal"][:t].reshape(1, t, 1, d)
+    x = st_stack(x, P, cfg.st, "dit")
+    return linear(x[:, :, 2:], P["to_latent.w"], P["to_latent.b"])
+
+
+def dit_loss(P, cfg: DitCfg, latents: np.ndarray, action_latents, gen: np.random.Generator):  # :182-192
+    b, t = latents.shape[:2]
+    tau = gen.uniform(0.0, 1.0, size=(b, t))
+    noised = forcing_corrupt(latents, tau, gen)
+    pred = dit_predict_clean(P, cfg, noised, tau, action_latents)
+    err = pred - torch.as_tensor(latents).to(pred.dtype)
+    per_frame = (err * err).mean(dim=(2, 3))
+    return (per_frame * torch.as_tensor(tau).to(pred.dtype)).mean()
+
+
+def dit_sample_frame(P, cfg: DitCfg, context: np.ndarray, action_latents, steps=25, context_noise=0.1,
+                     gen: np.random.Generator | None = None) -> np.ndarray:  # diffusion.py:194-215
+    if steps < 1:
+        raise ValueError("steps must be >= 1")
+    if gen is None:
+        gen = orng.stream(0, "diffusion-sample")
+    b, t_prev, n, dl = context.shape
+    z = gen.standard_normal((b, 1, n, dl)).astype(context.dtype)
+    with torch.no_grad():
+        for k in range(steps, 0, -1):
+            tau_k, tau_prev = k / steps, (k - 1) / steps
+            ctx = forcing_corrupt(context, np.full((b, t_prev), context_noise), gen)
+            full = np.concatenate([ctx, z], axis=1)
+            tau = np.concatenate([np.full((b, t_prev), context_noise), np.full((b, 1), tau_k)], axis=1)
+            pred = dit_predict_clean(P, cfg, full, tau, action_latents).numpy()[:, -1:]
+            z = z + (tau_k - tau_prev) * (pred - z) / tau_k
+    return z[:, 0]

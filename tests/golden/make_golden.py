@@ -248,11 +248,29 @@ def gen_records():
     save("records", **out)
 
 
+def gen_dit():
+    """ST-DiT (diffusion.py:131-215): init, predict_clean, ramp-weighted loss + grads, sample_frame."""
+    from deskworld.diffusion import DitConfig, DitDynamics
+    kw = dict(model_dim=32, heads=2, ffn_dim=128, blocks=1, latent_dim=8, action_latent_dim=8, action_vocab=7,
+              patches_per_frame=4, max_frames=4)
+    dit = DitDynamics(DitConfig(**kw), seed=3, dtype=np.float64)
+    g = R.stream(21, "dit-golden")
+    latents = g.uniform(-1, 1, size=(2, 3, 4, 8))
+    act = g.normal(size=(2, 2, 8)) * 0.1
+    tau = g.uniform(0, 1, size=(2, 3))
+    pred = dit.predict_clean(latents, tau, Tensor(act)).data
+    loss = dit.loss(latents, Tensor(act), R.stream(22, "dit-loss"))
+    grads = grads_of(dit.params, loss)
+    z = dit.sample_frame(latents[:, :2], Tensor(act), steps=3, rng=R.stream(23, "dit-sample"))
+    save("dit_golden", latents=latents, act=act, tau=tau, pred=pred, loss=np.asarray(loss.data), sample=z,
+         **{f"param.{k}": v.data for k, v in dit.params.items()}, **grads)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "vq", "dynamics", "toklam", "sampling", "adamw", "jasmine", "checkpoint",
                              "records"]
     fns = {"rng": gen_rng, "vq": gen_vq, "dynamics": gen_dynamics, "toklam": gen_tokenizer_lam,
            "sampling": gen_sampling, "adamw": gen_adamw, "jasmine": gen_jasmine_summary,
-           "checkpoint": gen_checkpoint, "records": gen_records}
+           "checkpoint": gen_checkpoint, "records": gen_records, "dit": gen_dit}
     for w in which:
         fns[w]()

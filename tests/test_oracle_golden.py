@@ -234,3 +234,24 @@ def test_jasmine_b1_fp32(golden):
         ref = float(g[f"gnorm.{k}"])
         got = float(p.grad.double().norm())
         assert got == pytest.approx(ref, rel=2e-4, abs=1e-9), k
+
+
+def test_dit_predict_loss_grads_sample(golden):
+    """ST-DiT oracle (diffusion.py:131-215) against the reference's f64 run: init draw order,
+    x-prediction, ramp-weighted forcing loss with every gradient, and the Euler sampler."""
+    g = golden("dit_golden")
+    cfg = M.DitCfg(model_dim=32, heads=2, ffn_dim=128, blocks=1, latent_dim=8, action_latent_dim=8, action_vocab=7,
+                   patches_per_frame=4, max_frames=4)
+    init = M.init_dit(cfg, seed=3, dtype=np.float64)
+    for k, v in init.items():
+        np.testing.assert_array_equal(v, g[f"param.{k}"], err_msg=k)
+    P = M.params_to_torch(init)
+    act = torch.tensor(g["act"])
+    pred = M.dit_predict_clean(P, cfg, g["latents"], g["tau"], act)
+    np.testing.assert_allclose(pred.detach().numpy(), g["pred"], rtol=1e-10, atol=1e-12)
+    loss = M.dit_loss(P, cfg, g["latents"], act, R.stream(22, "dit-loss"))
+    np.testing.assert_allclose(float(loss), float(g["loss"]), rtol=1e-11)
+    loss.backward()
+    _check_grads(P, g)
+    z = M.dit_sample_frame(P, cfg, g["latents"][:, :2], act, steps=3, gen=R.stream(23, "dit-sample"))
+    np.testing.assert_allclose(z, g["sample"], rtol=1e-10, atol=1e-12)
