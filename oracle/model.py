@@ -695,3 +695,81 @@ def dit_sample_frame(P, cfg: DitCfg, context: np.ndarray, action_latents, steps=
             pred = dit_predict_clean(P, cfg, full, tau, action_latents).numpy()[:, -1:]
             z = z + (tau_k - tau_prev) * (pred - z) / tau_k
     return z[:, 0]
+
+
+@dataclass(frozen=True)
+class MaeCfg:  # diffusion.py:23-47
+    model_dim: int = 512
+    heads: int = 8
+    ffn_dim: int = 2048
+    blocks: int = 4
+    latent_dim: int = 32
+    patch: int = 16
+    height: int = 64
+    width: int = 64
+    channels: int = 3
+    max_frames: int = 16
+    mask_prob_max: float = 0.9
+
+    @property
+    def patches_per_frame(self) -> int:
+        return (self.height // self.patch) * (self.width // self.patch)
+
+    @property
+    def patch_dim(self) -> int:
+        return self.patch * self.patch * self.channels
+
+    @property
+    def st(self) -> StCfg:
+        return StCfg(self.model_dim, self.heads, self.ffn_dim, self.blocks)
+
+
+def init_mae(cfg: MaeCfg, seed=0, dtype=np.float32) -> dict:  # diffusion.py:51-70 (draw order)
+    g = orng.stream(seed, "mae-init")
+    d = cfg.model_dim
+    p = {}
+    p["patch_embed.w"] = g.normal(0, 0.02, (cfg.patch_dim, d)).astype(dtype)
+    p["patch_embed.b"] = np.zeros(d, dtype=dtype)
+    p["mask_token"] = g.normal(0, 0.02, (d,)).astype(dtype)
+    p["pos_spatial"] = g.normal(0, 0.02, (cfg.patches_per_frame, d)).astype(dtype)
+    p["pos_temporal"] = g.normal(0, 0.02, (cfg.max_frames, d)).astype(dtype)
+    p.update(init_st_stack(g, cfg.st, "enc", dtype))
+    p["to_latent.w"] = g.normal(0, 0.02, (d, cfg.latent_dim)).astype(dtype)
+    p["to_latent.b"] = np.zeros(cfg.latent_dim, dtype=dtype)
+    p["from_latent.w"] = g.normal(0, 0.02, (cfg.latent_dim, d)).astype(dtype)
+    p["from_latent.b"] = np.zeros(d, dtype=dtype)
+    p.update(init_st_stack(g, cfg.st, "dec", dtype))
+    p["to_pixels.w"] = g.normal(0, 0.02, (d, cfg.patch_dim)).astype(dtype)
+    p["to_pixels.b"] = np.zeros(cfg.patch_dim, dtype=dtype)
+    return p
+
+
+def mae_encode(P, cfg: MaeCfg, unit, mask=None):  # diffusion.py:72-86
+    t, d = unit.shape[1], cfg.model_dim
+    x = linear(patchify(unit, cfg.patch), P["patch_embed.w"], P["patch_embed.b"])
+    if mask is not None:
+        m = torch.as_tensor(np.asarray(mask, dtype=bool))[..., None]
+        x = torch.where(m, P["mask_token"].expand_as(x), x)
+    x = x + P["pos_spatial"]
+    x = x + P["pos_temporal"][:t].reshape(1, t, 1, d)
+    x = st_stack(x, P, cfg.st, "enc")
+    return torch.tanh(linear(x, P["to_latent.w"], P["to_latent.b"]))
+
+
+def mae_decode(P, cfg: MaeCfg, latents):  # diffusion.py:88-92
+    x = linear(latents, P["from_latent.w"], P["from_latent.b"])
+    x = st_stack(x, P, cfg.st, "dec")
+    x = linear(x, P["to_pixels.w"], P["to_pixels.b"])
+    return unpatchify(x, cfg.patch, cfg.height, cfg.width, cfg.channels)
+
+
+def mae_mask(cfg: MaeCfg, b: int, t: int, gen: np.random.Generator) -> np.ndarray:  # diffusion.py:97-99
+    p = gen.uniform(0.0, cfg.mask_prob_max, size=(b, t))
+    return gen.random((b, t, cfg.patches_per_frame)) < p[:, :, None]
+
+
+def mae_forward(P, cfg: MaeCfg, unit, gen: np.random.Generator):  # diffusion.py:94-103
+    mask = mae_mask(cfg, unit.shape[0], unit.shape[1], gen)
+    latents = mae_encode(P, cfg, unit, mask)
+    recon = mae_decode(P, cfg, latents)
+    return recon, latents, mse(recon, unit.detach())

@@ -266,11 +266,23 @@ def gen_dit():
          **{f"param.{k}": v.data for k, v in dit.params.items()}, **grads)
 
 
+def gen_mae():
+    """MAE tokenizer (diffusion.py:50-103): init, masked forward (recon, latents, loss) + grads, decode."""
+    from deskworld.diffusion import MaeConfig, MaeTokenizer
+    kw = dict(model_dim=32, heads=2, ffn_dim=128, blocks=1, latent_dim=8, patch=4, height=8, width=8, max_frames=3)
+    mae = MaeTokenizer(MaeConfig(**kw), seed=5, dtype=np.float64)
+    unit = R.stream(24, "mae-golden").uniform(-1, 1, size=(2, 3, 8, 8, 3))
+    recon, latents, loss = mae.forward(Tensor(unit), R.stream(25, "mae-mask"))
+    grads = grads_of(mae.params, loss)
+    save("mae_golden", unit=unit, recon=recon.data, latents=latents.data, loss=np.asarray(loss.data),
+         **{f"param.{k}": v.data for k, v in mae.params.items()}, **grads)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "vq", "dynamics", "toklam", "sampling", "adamw", "jasmine", "checkpoint",
                              "records"]
     fns = {"rng": gen_rng, "vq": gen_vq, "dynamics": gen_dynamics, "toklam": gen_tokenizer_lam,
            "sampling": gen_sampling, "adamw": gen_adamw, "jasmine": gen_jasmine_summary,
-           "checkpoint": gen_checkpoint, "records": gen_records, "dit": gen_dit}
+           "checkpoint": gen_checkpoint, "records": gen_records, "dit": gen_dit, "mae": gen_mae}
     for w in which:
         fns[w]()

@@ -255,3 +255,20 @@ def test_dit_predict_loss_grads_sample(golden):
     _check_grads(P, g)
     z = M.dit_sample_frame(P, cfg, g["latents"][:, :2], act, steps=3, gen=R.stream(23, "dit-sample"))
     np.testing.assert_allclose(z, g["sample"], rtol=1e-10, atol=1e-12)
+
+
+def test_mae_forward_grads(golden):
+    """MAE tokenizer oracle (diffusion.py:50-103) against the reference's f64 masked forward."""
+    g = golden("mae_golden")
+    cfg = M.MaeCfg(model_dim=32, heads=2, ffn_dim=128, blocks=1, latent_dim=8, patch=4, height=8, width=8,
+                   max_frames=3)
+    init = M.init_mae(cfg, seed=5, dtype=np.float64)
+    for k, v in init.items():
+        np.testing.assert_array_equal(v, g[f"param.{k}"], err_msg=k)
+    P = M.params_to_torch(init)
+    recon, latents, loss = M.mae_forward(P, cfg, torch.tensor(g["unit"]), R.stream(25, "mae-mask"))
+    np.testing.assert_allclose(latents.detach().numpy(), g["latents"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(recon.detach().numpy(), g["recon"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(float(loss), float(g["loss"]), rtol=1e-11)
+    loss.backward()
+    _check_grads(P, g)
