@@ -97,3 +97,79 @@ def test_errors(case):
         dit.predict_clean(case["latents"], np.zeros((case["B"], case["T"])), case["act"][:, :2])
     with pytest.raises(ValueError):
         dit.sample_frame(case["latents"][:, :2], case["act"][:, :2], steps=0)
+
+
+MAEKW = dict(model_dim=512, heads=8, ffn_dim=2048, blocks=2, latent_dim=32, patch=16, height=64, width=64,
+             max_frames=16)
+
+
+@pytest.fixture(scope="module")
+def mae_case():
+    from paper_2510_27002_b200.diffusion import MaeConfig, MaeTokenizer
+    mae = MaeTokenizer(MaeConfig(**MAEKW), seed=6)
+    P = OM.params_to_torch(OM.init_mae(OM.MaeCfg(**MAEKW), seed=6))
+    frames = OR.stream(11, "mae-frames").integers(0, 256, size=(3, 6, 64, 64, 3)).astype(np.uint8)
+    return dict(mae=mae, P=P, frames=frames, unit=OM.frames_to_unit(frames))
+
+
+def test_mae_encode_decode_match_oracle(mae_case):
+    mae, P, unit = mae_case["mae"], mae_case["P"], mae_case["unit"]
+    for k, p in mae.params.items():
+        np.testing.assert_array_equal(p.data.cpu().numpy(), P[k].detach().numpy(), err_msg=k)
+    cfg = OM.MaeCfg(**MAEKW)
+    lat = mae.encode(mae_case["frames"]).numpy()  # uint8 in: unit conversion on device
+    with torch.no_grad():
+        lat_ref = OM.mae_encode(P, cfg, torch.tensor(unit)).numpy()
+        mask = OR.stream(12, "m").random((3, 6, 16)) < 0.5
+        lat_m_ref = OM.mae_encode(P, cfg, torch.tensor(unit), mask).numpy()
+        rec_ref = OM.mae_decode(P, cfg, torch.tensor(lat_ref)).numpy()
+    assert lat.shape == (3, 6, 16, 32)
+    assert _rel(lat, lat_ref) < TOL["bf16_logits_rel_l2"]
+    assert _rel(mae.encode(unit, mask=mask).numpy(), lat_m_ref) < TOL["bf16_logits_rel_l2"]
+    assert _rel(mae.decode(lat_ref).numpy(), rec_ref) < TOL["bf16_logits_rel_l2"]
+
+
+def test_mae_forward_backward_match_oracle(mae_case):
+    from paper_2510_27002_b200 import rng as R
+    mae, P = mae_case["mae"], mae_case["P"]
+    recon, lat, loss = mae.forward(mae_case["unit"], R.stream(13, "mae-step"))
+    r2, l2, loss2 = OM.mae_forward(P, OM.MaeCfg(**MAEKW), torch.tensor(mae_case["unit"]), OR.stream(13, "mae-step"))
+    assert _rel(lat.numpy(), l2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
+    assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
+    assert abs(float(loss.data) - float(loss2)) < max(TOL["bf16_loss_abs"], 1e-2 * float(loss2))
+    loss.backward()
+    loss2.backward()
+    bad = []
+    for k, p in mae.params.items():
+        if k.endswith(".k.b"):
+            continue
+        ref, got = P[k].grad.numpy(), p.grad.cpu().numpy()
+        if _cos(got, ref) < 0.995:
+            bad.append((k, _cos(got, ref), _rel(got, ref)))
+    assert not bad, bad
+
+
+def test_diffusion_rollout_matches_oracle_composition(case, mae_case):
+    """diffusion_rollout (diffusion.py:217-251): MAE encode -> per-frame DiT Euler sampling with
+    ground-truth action ids -> clip -> MAE decode, against the same pipeline from oracle pieces."""
+    from paper_2510_27002_b200 import rng as R
+    from paper_2510_27002_b200.diffusion import diffusion_rollout
+    mae, dit = mae_case["mae"], case["dit"]
+    cond = mae_case["frames"][:2, :3]
+    actions = [np.array([1, 4]), np.array([6, 0])]
+    out = diffusion_rollout(mae, dit, cond, actions, horizon=2, steps=3, rng=R.stream(14, "roll"))
+    assert out.shape == (2, 5, 64, 64, 3) and out.dtype == np.uint8
+    Pm, Pd = mae_case["P"], case["P"]
+    g = OR.stream(14, "roll")
+    with torch.no_grad():
+        lat = OM.mae_encode(Pm, OM.MaeCfg(**MAEKW), torch.tensor(OM.frames_to_unit(cond))).numpy()
+        hist = Pd["null_action"].detach().reshape(1, 1, 32) + torch.zeros(2, 2, 32)
+        for a in actions:
+            hist = torch.cat([hist, Pd["gt_action_embed"].detach()[torch.as_tensor(a)].reshape(2, 1, 32)], 1)
+            nxt = OM.dit_sample_frame(Pd, OM.DitCfg(**KW), lat, hist, steps=3, gen=g)
+            lat = np.concatenate([lat, nxt[:, None]], axis=1)
+        lat = np.clip(lat, -1.0 + 1e-6, 1.0 - 1e-6)
+        ref = OM.unit_to_frames(OM.mae_decode(Pm, OM.MaeCfg(**MAEKW), torch.tensor(lat)).numpy())
+    diff = np.abs(out.astype(np.int16) - ref.astype(np.int16))
+    assert diff[:, :3].mean() < 1.0  # re-decoded conditioning frames
+    assert diff.mean() < 2.0         # generated frames: bf16 chains through 2 x 3 model calls
