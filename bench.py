@@ -218,7 +218,59 @@ def secondary_configs(dev) -> dict:
                                         "(trainer.tokenizer_stage)"}
     out["pretrain_lam_stage"] = _pretrain_lam_stage(tok, lam, dev)
     out["play_act"] = _play_act(tok, lam, dev)
+    out["dit_train"] = _dit_train(dev)
     return out
+
+
+def _dit_train(dev) -> dict:
+    """ST-DiT diffusion-forcing train step at the reference's DitConfig defaults
+    (512 wide, 6 blocks, 16 latent patches -> S = 18, T = 16), B = 36: host tau / eps draws and
+    their H2D copy, forward, ramp-weighted loss, full backward, AdamW. Plus the small-frame
+    spatial attention kernels (K3s) alone at that shape, against their HBM roofline."""
+    import numpy as np
+    import torch
+
+    from paper_2510_27002_b200 import kernels as Kn
+    from paper_2510_27002_b200.diffusion import DitConfig, DitDynamics
+    from paper_2510_27002_b200.optim import adamw_init, adamw_step
+    from paper_2510_27002_b200.rng import stream
+
+    B, T, N = 36, FRAMES_T, 16
+    dit = DitDynamics(DitConfig(), seed=0)
+    lat = np.tanh(stream(3, "dit-bench").normal(size=(B, T, N, 32))).astype(np.float32)
+    act = (stream(4, "dit-bench").normal(size=(B, T - 1, 32)) * 0.1).astype(np.float32)
+    opt = adamw_init(dit.params)
+    k = [0]
+
+    def step():
+        loss = dit.loss(lat, act, stream(0, "dit", "step", k[0]))
+        loss.backward()
+        adamw_step(dit.params, {n: p.grad for n, p in dit.params.items()}, opt, 1e-4)
+        k[0] += 1
+
+    step()
+    ms = _events_ms(step, reps=3)
+    frames, S, H, D = B * T, N + 2, 8, 512
+    g = torch.Generator(device=dev).manual_seed(0)
+    qkv = torch.randn(frames * S, 3 * D, device=dev, generator=g).bfloat16()
+    o, _, lse = Kn.attn_spatial_fwd(qkv, frames, S, H)
+    do = torch.randn(frames * S, D, device=dev, generator=g).bfloat16()
+    dq = torch.empty_like(qkv)
+    fwd_us = 1e3 * _events_ms(lambda: Kn.attn_spatial_fwd(qkv, frames, S, H), reps=20)
+    bwd_us = 1e3 * _events_ms(lambda: Kn.attn_spatial_bwd(qkv, o, do, lse, frames, S, H, dqkv=dq), reps=20)
+    hbm = _peaks()["hbm_gbs"]
+    fwd_b = frames * S * (3 * D * 2 + D * 2 + H * 4)
+    bwd_b = frames * S * (3 * D * 2 + D * 2 + H * 4 + 3 * D * 2)
+    return {"metric": "DiT train frames/sec", "value": round(B * T / (ms / 1e3), 1), "unit": "frames/s",
+            "ms_per_step": round(ms, 2),
+            "config": "ST-DiT at DitConfig defaults (512 wide, 8 heads, 6 blocks, 16 latent patches, S = 18), "
+                      "B=36, T=16; host tau/eps draws + H2D, forward, loss, full backward, AdamW (eager)",
+            "attention_small": {"S": S, "frames": frames,
+                                "fwd_us": round(fwd_us, 1), "fwd_gbs": round(fwd_b / fwd_us / 1e3, 1),
+                                "fwd_frac_hbm": round(fwd_b / fwd_us / 1e3 / hbm, 3),
+                                "bwd_us": round(bwd_us, 1), "bwd_gbs": round(bwd_b / bwd_us / 1e3, 1),
+                                "bwd_frac_hbm": round(bwd_b / bwd_us / 1e3 / hbm, 3),
+                                "bytes": "fwd: qkv in, O + lse out; bwd: qkv, dO, lse in, dqkv out"}}
 
 
 def _play_act(tok, lam, dev) -> dict:

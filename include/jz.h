@@ -236,7 +236,7 @@ JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void
  * K4  causal temporal (inter-frame) attention (st.py:74-76, nn.py:103-105):
  * for every (b, s) the T rows (b, t, s) attend causally over t.  qkv/out as
  * above with rows ordered (b, t, s); lse f32 [B*S, H, T].  T <= 32, head_dim 64
- * (T > 16: two 16-row register tiles, model_dim <= 512 for the backward's shared memory).
+ * (T > 16: two 16-row register tiles; one CTA per (slot, group of up to 4 heads)).
  * ---------------------------------------------------------------------- */
 JZ_API int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, int H, int head_dim, void* out,
                                 float* lse, jz_stream_t stream);

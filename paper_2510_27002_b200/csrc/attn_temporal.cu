@@ -365,7 +365,8 @@ __global__ void __launch_bounds__(512) temporal_bwd_kernel(const __nv_bfloat16* 
 //    diffusion.py:164-180). Launched with B := frames, T := S_sp, S := 1, so a slot's rows are
 //    the frame's contiguous tokens and lse lands as [frame][H][S_sp], the K3 layout;
 //  - causal temporal attention with 16 < T <= 32 (st.py:74-76).
-// Per warp (= head): query tile qt against all NT key tiles in registers (m16n8k16), P / dS
+// One CTA per (slot, group of up to 4 heads); per warp (= head): query tile qt against all NT
+// key tiles in registers (m16n8k16), P / dS
 // tiles staged per warp in shared memory for the transposed dK / dV products. The backward
 // forms Delta = sum_j P_ij dP_ij from its fp32 registers, as the T <= 16 kernel does (the forward
 // output is not read). Tiles wholly above the causal
@@ -430,21 +431,24 @@ __global__ void __launch_bounds__(512) rowtile_fwd_kernel(const __nv_bfloat16* _
   extern __shared__ __align__(16) uint8_t smem_raw[];
   constexpr int R = 16 * NT;
   const int D = H * HD;
-  const int ld = 3 * D + 8;
+  const int hpc = blockDim.x / 32, h0 = blockIdx.y * hpc;  // this CTA's heads h0 .. h0 + hpc - 1
+  const int Dl = hpc * HD, ld = 3 * Dl + 8;
   const int64_t bs = blockIdx.x;
   const int64_t b = bs / S, s = bs - b * S;
-  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
-  stage_rows_n(sq, ld, R, qkv, 3 * D, 3 * D, b, T, S, s);
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [R][q | k | v of the CTA's heads]
+#pragma unroll
+  for (int part = 0; part < 3; ++part)
+    stage_rows_n(sq + part * Dl, ld, R, qkv + part * D + h0 * HD, 3 * D, Dl, b, T, S, s);
   cp_async_wait_all();
   __syncthreads();
-  const int h = warp_id(), L = lane_id();
+  const int w = warp_id(), h = h0 + w, L = lane_id();
   const int r0 = L >> 2, cq = 2 * (L & 3);
   float* lp = lse + (bs * H + h) * T;
 #pragma unroll
   for (int qt = 0; qt < NT; ++qt) {
     float sc[NT][2][4];
 #pragma unroll
-    for (int kt = 0; kt < NT; ++kt) xyT(sc[kt], sq + 16 * qt * ld + h * HD, ld, sq + 16 * kt * ld + D + h * HD, ld);
+    for (int kt = 0; kt < NT; ++kt) xyT(sc[kt], sq + 16 * qt * ld + w * HD, ld, sq + 16 * kt * ld + Dl + w * HD, ld);
     float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
     for (int kt = 0; kt < NT; ++kt)
@@ -479,10 +483,10 @@ __global__ void __launch_bounds__(512) rowtile_fwd_kernel(const __nv_bfloat16* _
     for (int kt = 0; kt < NT; ++kt) {
       uint32_t pa[4];
       c_to_a(pa, sc[kt]);
-      av_acc(pa, sq + 16 * kt * ld + 2 * D + h * HD, ld, o);
+      av_acc(pa, sq + 16 * kt * ld + 2 * Dl + w * HD, ld, o);
     }
     __syncwarp();  // this head's q rows of tile qt are consumed: O overwrites them in place
-    frag_to_smem(o, sq + 16 * qt * ld, ld, h * HD, 1.0f / l0, 1.0f / l1);
+    frag_to_smem(o, sq + 16 * qt * ld, ld, w * HD, 1.0f / l0, 1.0f / l1);
     if ((L & 3) == 0) {
       const int ra = 16 * qt + r0;
       if (ra < T) lp[ra] = m0 + logf(l0);
@@ -490,10 +494,11 @@ __global__ void __launch_bounds__(512) rowtile_fwd_kernel(const __nv_bfloat16* _
     }
   }
   __syncthreads();
-  const int c16 = D / 8;
+  const int c16 = Dl / 8;
   for (int i = threadIdx.x; i < T * c16; i += blockDim.x) {
     const int t = i / c16, c = i - t * c16;
-    *reinterpret_cast<uint4*>(out + ((b * T + t) * S + s) * D + 8 * c) = *reinterpret_cast<const uint4*>(sq + t * ld + 8 * c);
+    *reinterpret_cast<uint4*>(out + ((b * T + t) * S + s) * D + h0 * HD + 8 * c) =
+        *reinterpret_cast<const uint4*>(sq + t * ld + 8 * c);
   }
 }
 
@@ -507,24 +512,28 @@ __global__ void __launch_bounds__(512) rowtile_bwd_kernel(const __nv_bfloat16* _
   extern __shared__ __align__(16) uint8_t smem_raw[];
   constexpr int R = 16 * NT, LDR = R + 8;
   const int D = H * HD;
-  const int ldq = 3 * D + 8, ldo = D + 8;
+  const int hpc = blockDim.x / 32, h0 = blockIdx.y * hpc;  // this CTA's heads h0 .. h0 + hpc - 1
+  const int Dl = hpc * HD;
+  const int ldq = 3 * Dl + 8, ldo = Dl + 8;
   const int64_t bs = blockIdx.x;
   const int64_t b = bs / S, s = bs - b * S;
-  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sq = reinterpret_cast<__nv_bfloat16*>(smem_raw);  // [R][q | k | v of the CTA's heads]
   __nv_bfloat16* so = sq + R * ldq;  // dQ staging (each warp its own head's columns)
   __nv_bfloat16* sdo = so + R * ldo;
   __nv_bfloat16* sp_all = sdo + R * ldo;
-  stage_rows_n(sq, ldq, R, qkv, 3 * D, 3 * D, b, T, S, s);
-  stage_rows_n(sdo, ldo, R, dout, D, D, b, T, S, s);
+#pragma unroll
+  for (int part = 0; part < 3; ++part)
+    stage_rows_n(sq + part * Dl, ldq, R, qkv + part * D + h0 * HD, 3 * D, Dl, b, T, S, s);
+  stage_rows_n(sdo, ldo, R, dout + h0 * HD, D, Dl, b, T, S, s);
   cp_async_wait_all();
   __syncthreads();
-  const int h = warp_id(), L = lane_id();
-  __nv_bfloat16* sP = sp_all + h * 2 * R * LDR;
+  const int w = warp_id(), h = h0 + w, L = lane_id();
+  __nv_bfloat16* sP = sp_all + w * 2 * R * LDR;
   __nv_bfloat16* sdS = sP + R * LDR;
-  const __nv_bfloat16* q = sq + h * HD;
-  const __nv_bfloat16* k = sq + D + h * HD;
-  const __nv_bfloat16* v = sq + 2 * D + h * HD;
-  const __nv_bfloat16* dog = sdo + h * HD;
+  const __nv_bfloat16* q = sq + w * HD;
+  const __nv_bfloat16* k = sq + Dl + w * HD;
+  const __nv_bfloat16* v = sq + 2 * Dl + w * HD;
+  const __nv_bfloat16* dog = sdo + w * HD;
   const int r0 = L >> 2, cq = 2 * (L & 3);
   const float* lp = lse + (bs * H + h) * T;
 #pragma unroll
@@ -569,7 +578,7 @@ __global__ void __launch_bounds__(512) rowtile_bwd_kernel(const __nv_bfloat16* _
       c_to_a(a, dS[kt]);
       av_acc(a, k + 16 * kt * ldq, ldq, oq);  // dQ_qt += dS_(qt,kt) K_kt
     }
-    frag_to_smem(oq, so + 16 * qt * ldo, ldo, h * HD, scale, scale);
+    frag_to_smem(oq, so + 16 * qt * ldo, ldo, w * HD, scale, scale);
   }
   __syncwarp();
   // dK_kt = scale * sum_qt dS_(qt,kt)^T Q_qt, dV_kt = sum_qt P_(qt,kt)^T dO_qt; K and V are consumed
@@ -586,28 +595,32 @@ __global__ void __launch_bounds__(512) rowtile_bwd_kernel(const __nv_bfloat16* _
       load_a_trans(a, sP + 16 * qt * LDR + 16 * kt, LDR);
       av_acc(a, dog + 16 * qt * ldo, ldo, gv);
     }
-    frag_to_smem(gk, sq + 16 * kt * ldq, ldq, D + h * HD, scale, scale);
-    frag_to_smem(gv, sq + 16 * kt * ldq, ldq, 2 * D + h * HD, 1.0f, 1.0f);
+    frag_to_smem(gk, sq + 16 * kt * ldq, ldq, Dl + w * HD, scale, scale);
+    frag_to_smem(gv, sq + 16 * kt * ldq, ldq, 2 * Dl + w * HD, 1.0f, 1.0f);
   }
   __syncthreads();
-  // coalesced write-out of the T rows: dQ from the O buffer, dK | dV from the qkv buffer
-  const int c16 = 3 * D / 8, cq16 = D / 8;
+  // coalesced write-out of the T rows, the CTA's head columns of each of dq | dk | dv:
+  // dQ from the O buffer, dK | dV from the qkv buffer (local column c -> global part * D + h0 * HD)
+  const int c16 = 3 * Dl / 8, cq16 = Dl / 8;
   for (int i = threadIdx.x; i < T * c16; i += blockDim.x) {
     const int t = i / c16, c = i - t * c16;
-    const __nv_bfloat16* src = c < cq16 ? so + t * ldo + 8 * c : sq + t * ldq + 8 * c;
-    *reinterpret_cast<uint4*>(dqkv + ((b * T + t) * S + s) * (3 * D) + 8 * c) = *reinterpret_cast<const uint4*>(src);
+    const int part = c / cq16;
+    const __nv_bfloat16* src = part == 0 ? so + t * ldo + 8 * c : sq + t * ldq + 8 * c;
+    *reinterpret_cast<uint4*>(dqkv + ((b * T + t) * S + s) * (3 * D) + part * D + h0 * HD + 8 * (c - part * cq16)) =
+        *reinterpret_cast<const uint4*>(src);
   }
   if (colsum) {
-    float* part = colsum + bs * (3 * D);
-    for (int c2 = threadIdx.x; c2 < 3 * D / 2; c2 += blockDim.x) {
+    float* prow = colsum + bs * (3 * D);
+    for (int c2 = threadIdx.x; c2 < 3 * Dl / 2; c2 += blockDim.x) {
+      const int part = (2 * c2) / Dl;
       float s0 = 0.f, s1 = 0.f;
       for (int t = 0; t < T; ++t) {
-        const __nv_bfloat16* src = 2 * c2 < D ? so + t * ldo + 2 * c2 : sq + t * ldq + 2 * c2;
+        const __nv_bfloat16* src = part == 0 ? so + t * ldo + 2 * c2 : sq + t * ldq + 2 * c2;
         const float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(src));
         s0 += f.x;
         s1 += f.y;
       }
-      *reinterpret_cast<float2*>(part + 2 * c2) = make_float2(s0, s1);
+      *reinterpret_cast<float2*>(prow + part * D + h0 * HD + 2 * c2 - part * Dl) = make_float2(s0, s1);
     }
   }
 }
@@ -621,21 +634,27 @@ static int launch_rowtile(bool bwd, const void* qkv, const void* o, const void* 
   const float scale = 0.125f;
   const int64_t BS = B * S;
   if (BS == 0) return JZ_OK;
-  const int D = H * HD;
-  const int threads = 32 * H;
+  // heads per CTA: the largest divisor of H up to 4, so a frame (slot) spreads over H / hpc CTAs
+  // and several CTAs share an SM (fwd 4, bwd 2 at R = 32): loads of one overlap another's math
+  int hpc = 1;
+  for (int c = 4; c >= 1; --c)
+    if (H % c == 0) { hpc = c; break; }
+  const int Dl = hpc * HD;
+  const int threads = 32 * hpc;
+  const dim3 grid((unsigned)BS, (unsigned)(H / hpc));
   if (!bwd) {
-    const size_t smem = (size_t)R * (3 * D + 8) * 2;
+    const size_t smem = (size_t)R * (3 * Dl + 8) * 2;
     JZ_CHECK_ARG(smem <= kRowTileSmemMax, "row-tile attention: %d rows x %d heads exceed shared memory", T, H);
     JZ_CUDA_TRY(cudaFuncSetAttribute(rowtile_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    rowtile_fwd_kernel<NT><<<(unsigned)BS, threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), T, S, H,
+    rowtile_fwd_kernel<NT><<<grid, threads, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(qkv), T, S, H,
                                                                 causal, reinterpret_cast<__nv_bfloat16*>(out), lse,
                                                                 scale);
   } else {
-    const size_t smem = (size_t)R * (3 * D + 8) * 2 + (size_t)2 * R * (D + 8) * 2 + (size_t)H * 2 * R * (R + 8) * 2;
+    const size_t smem = (size_t)R * (3 * Dl + 8) * 2 + (size_t)2 * R * (Dl + 8) * 2 + (size_t)hpc * 2 * R * (R + 8) * 2;
     JZ_CHECK_ARG(smem <= kRowTileSmemMax, "row-tile attention backward: %d rows x %d heads exceed shared memory", T,
                  H);
     JZ_CUDA_TRY(cudaFuncSetAttribute(rowtile_bwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    rowtile_bwd_kernel<NT><<<(unsigned)BS, threads, smem, st>>>(
+    rowtile_bwd_kernel<NT><<<grid, threads, smem, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<const __nv_bfloat16*>(o),
         reinterpret_cast<const __nv_bfloat16*>(dout), lse, T, S, H, causal, reinterpret_cast<__nv_bfloat16*>(out),
         scale, colsum);

@@ -102,9 +102,6 @@ def check_supported(cfg: StConfig, S: int, T: int) -> None:
         raise ValueError(f"device spatial attention supports S in (256, 257) or S <= 32, got {S}")
     if T > 32:
         raise ValueError(f"device temporal attention supports T <= 32, got {T}")
-    if (S > 16 and S <= 32) or T > 16:
-        if cfg.model_dim > 512:
-            raise ValueError(f"device attention over 17..32 rows needs model_dim <= 512 (got {cfg.model_dim})")
 
 
 # --------------------------------------------------------------------------

@@ -269,18 +269,13 @@ def test_attn_temporal_long_clip(T):
         assert rel(dqkv[:, i * D:(i + 1) * D].float(), qf.grad[:, i * D:(i + 1) * D]) < 2e-2, "qkv"[i]
 
 
-@pytest.mark.parametrize("S,H", [(16, 8), (17, 8), (18, 8), (32, 8), (5, 2), (1, 4), (24, 16)])
+@pytest.mark.parametrize("S,H", [(16, 8), (17, 8), (18, 8), (32, 8), (5, 2), (1, 4), (24, 16), (18, 6), (9, 3)])
 def test_attn_spatial_small_fwd_bwd(S, H):
     """S <= 32 (patch-16 presets, MAE S = 16, ST-DiT S = 18): the register-tile kernel, non-causal."""
     frames = 37
     D = H * 64
     g = torch.Generator(device=dev).manual_seed(S * 31 + H)
     qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
-    if S > 16 and H > 8:  # the backward's shared memory bounds 17..32 rows to model_dim 512
-        with pytest.raises(ValueError, match="shared memory"):
-            out, _, lse = Kn.attn_spatial_fwd(qkv, frames, S, H)
-            Kn.attn_spatial_bwd(qkv, out, torch.zeros_like(out), lse, frames, S, H)
-        return
     out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
     assert out32 is None  # the small kernel's backward reads the bf16 output
     qf = qkv.float().requires_grad_(True)

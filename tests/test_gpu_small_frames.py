@@ -132,7 +132,6 @@ def test_envelope_errors():
     check_supported(StConfig(512, 8, 2048, 1), 18, 32)
     with pytest.raises(ValueError):
         check_supported(StConfig(512, 8, 2048, 1), 33, 16)
-    with pytest.raises(ValueError):
-        check_supported(StConfig(1024, 16, 4096, 1), 17, 16)
+    check_supported(StConfig(1024, 16, 4096, 1), 17, 16)
     with pytest.raises(ValueError):
         check_supported(StConfig(512, 8, 2048, 1), 257, 33)
