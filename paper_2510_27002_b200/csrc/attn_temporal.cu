@@ -21,7 +21,7 @@ namespace jz {
 namespace tp {
 
 constexpr int HD = 64;
-constexpr int LDP = 24;  // padded row pitch (elements) of the per-warp 16x16 P / dS tiles
+constexpr int LDP = 16;  // row pitch (elements) of the per-warp 16x16 P / dS tiles (unpadded: three backward CTAs per SM)
 
 JZ_DEV void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
