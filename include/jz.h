@@ -200,6 +200,11 @@ JZ_API int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, const fl
                             const float* pos_temporal, int64_t B, int T, int N, int D, int dl, int K,
                             int prepend, float* x, int* err, jz_stream_t stream);
 /* Workspace (floats) for jz_dyn_embed_bwd; K = vocabulary (token-table sort buffers). */
+/* Small embedding-table backward (autodiff.embedding backward, autodiff.py:344-364):
+ * dtable[k] (=|+=) sum_{i: ids[i]==k} dout[i] in increasing i (deterministic, no atomics).
+ * dout f32 [n, D]; err (may be NULL) is set to 1 when an id is outside [0, K). */
+JZ_API int jz_embedding_table_bwd(const float* dout, const int64_t* ids, int64_t n, int K, int D, float* dtable,
+                                  int accumulate, int* err, jz_stream_t stream);
 JZ_API int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend, int K);
 /* Deterministic backward of jz_dyn_embed_fwd (no float atomics).  d_latents may be NULL. */
 JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_t* mask,
@@ -357,7 +362,8 @@ JZ_API int jz_kv_fill(const void* qkv, void* cache, int64_t B, int T, int t0, in
  * n_keep best (conf desc, position asc) of each row become known.  dev_params (may be
  * NULL): device int64[13] {draw_base, n_keep, counter[4], key[2], buffer[4], buffer_pos}
  * read by the kernels instead of the host values (buffer_pos < 0: keep the host Philox
- * state), so one captured CUDA graph serves every refinement step of every frame. */
+ * state), so one captured CUDA graph serves every refinement step of every frame.
+ * K <= 2048 (any K; K % 32 != 0 runs a padded lane layout). */
 JZ_API int jz_maskgit_step(const float* logits, int64_t B, int N, int K, float temperature,
                            const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4,
                            int buffer_pos, uint64_t draw_base, int n_keep, const int64_t* dev_params,

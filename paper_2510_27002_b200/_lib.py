@@ -48,6 +48,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_adamw_step_dev": [_P, _P, _P, _P, _I64, _P, _P, _P],
     "jz_dyn_embed_fwd": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32,
                          _I32, _P, _P, _P],
+    "jz_embedding_table_bwd": [_P, _P, _I64, _I32, _I32, _P, _I32, _P, _P],
     "jz_dyn_embed_bwd_workspace": [_I64, _I32, _I32, _I32, _I32, _I32, _I32],
     "jz_dyn_embed_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32,
                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -483,6 +483,45 @@ extern "C" int jz_dyn_embed_fwd(const int64_t* tokens, const uint8_t* mask, cons
   return JZ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Small-table embedding backward (autodiff.embedding, autodiff.py:344-364): d_table[k] (+)= sum over
+// positions i with ids[i] == k of dout[i], in increasing i order.  One CTA per (row k, 128 dims):
+// the owner scans every id, so the sum has a fixed order (no atomics) -- meant for action tables
+// (gt_action_embed, a handful of rows, a few hundred ids per step).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) table_bwd_kernel(const float* __restrict__ dout, const int64_t* __restrict__ ids,
+                                                        int64_t n, int K, int D, float* __restrict__ dtab,
+                                                        int accumulate, int* __restrict__ err) {
+  const int k = blockIdx.x;
+  const int d = blockIdx.y * 128 + threadIdx.x;
+  __shared__ int64_t sid[256];
+  float acc = 0.f;
+  for (int64_t i0 = 0; i0 < n; i0 += 256) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 256; j += 128) {
+      const int64_t id = i0 + j < n ? ids[i0 + j] : -1;
+      sid[j] = id;
+      if (i0 + j < n && (id < 0 || id >= K) && err) atomicExch(err, 1);
+    }
+    __syncthreads();
+    const int m = (n - i0) < 256 ? (int)(n - i0) : 256;
+    if (d < D)
+      for (int j = 0; j < m; ++j)
+        if (sid[j] == k) acc += dout[(i0 + j) * D + d];
+  }
+  if (d < D) dtab[(int64_t)k * D + d] = accumulate ? dtab[(int64_t)k * D + d] + acc : acc;
+}
+
+extern "C" int jz_embedding_table_bwd(const float* dout, const int64_t* ids, int64_t n, int K, int D, float* dtable,
+                                      int accumulate, int* err, jz_stream_t s) {
+  JZ_CHECK_ARG(n >= 0 && K >= 1 && K <= 65535 && D >= 1, "table_bwd: bad sizes n=%lld K=%d D=%d", (long long)n, K, D);
+  auto st = reinterpret_cast<cudaStream_t>(s);
+  table_bwd_kernel<<<dim3((unsigned)K, (unsigned)((D + 127) / 128)), 128, 0, st>>>(dout, ids, n, K, D, dtable,
+                                                                                    accumulate, err);
+  JZ_LAUNCH_CHECK();
+  return JZ_OK;
+}
+
 // Workspace floats needed by jz_dyn_embed_bwd.
 extern "C" int64_t jz_dyn_embed_bwd_workspace(int64_t B, int T, int N, int D, int dl, int prepend, int K) {
   const int S = N + (prepend ? 1 : 0);

@@ -416,7 +416,9 @@ JZ_DEV void load_sampler_params(const int64_t* __restrict__ dev_params, PhiloxSt
   }
 }
 
-template <int PER>  // codes per lane
+// GUARD: K is not a multiple of 32 (small vocabularies, e.g. the reference's one-hot sampler
+// test); codes past K are padded with -inf, so they add 0 to the CDF and never win the argmax.
+template <int PER, bool GUARD = false>  // codes per lane
 __global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t rows, int K, float inv_temp,
                                       int greedy, PhiloxState st, uint64_t draw_base,
                                       const int64_t* __restrict__ dev_params, int64_t* __restrict__ cur,
@@ -428,7 +430,7 @@ __global__ void maskgit_sample_kernel(const float* __restrict__ logits, int64_t 
   const float* lr = logits + r * K + lane * PER;
   float v[PER];
 #pragma unroll
-  for (int i = 0; i < PER; ++i) v[i] = lr[i];
+  for (int i = 0; i < PER; ++i) v[i] = (!GUARD || lane * PER + i < K) ? lr[i] : -INFINITY;
   sample_row<PER>(v, r, lane, K, inv_temp, greedy, st, draw_base, cur, known, conf);
 }
 
@@ -575,7 +577,7 @@ extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, flo
                                const uint64_t* counter4, const uint64_t* key2, const uint64_t* buffer4, int buffer_pos,
                                uint64_t draw_base, int n_keep, const int64_t* dev_params, int64_t* cur,
                                uint8_t* known, float* conf, jz_stream_t s) {
-  JZ_CHECK_ARG(K % 32 == 0 && K / 32 <= 64, "maskgit: vocabulary %d unsupported (multiple of 32, <= 2048)", K);
+  JZ_CHECK_ARG(K >= 1 && K <= 2048, "maskgit: vocabulary %d unsupported (<= 2048)", K);
   JZ_CHECK_ARG(n_keep >= 0 && n_keep <= N, "maskgit: n_keep %d", n_keep);
   auto st = reinterpret_cast<cudaStream_t>(s);
   PhiloxState ps;
@@ -596,6 +598,17 @@ extern "C" int jz_maskgit_step(const float* logits, int64_t B, int N, int K, flo
   int64_t pgrid = (rows + kSampleWarps - 1) / kSampleWarps;
   if (pgrid > (int64_t)num_sms() * 4) pgrid = (int64_t)num_sms() * 4;
   const size_t psmem = (size_t)kSampleWarps * 2 * K * sizeof(float);
+  if (K % 32 != 0) {
+    const int per = (K + 31) / 32;
+#define MG(P) else if (per <= P) maskgit_sample_kernel<P, true><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf);
+    if (false) {}
+    MG(1) MG(2) MG(4) MG(8) MG(16) MG(32) MG(64)
+#undef MG
+    JZ_LAUNCH_CHECK();
+    maskgit_select_kernel<<<(unsigned)B, 256, N * sizeof(float), st>>>(conf, N, n_keep, dev_params, known);
+    JZ_LAUNCH_CHECK();
+    return JZ_OK;
+  }
   switch (K / 32) {
 #define MS_(P) maskgit_sample_kernel<P><<<grid, 256, 0, st>>>(logits, rows, K, inv_temp, greedy, ps, draw_base, dev_params, cur, known, conf);
 #define MS(P) case P: MS_(P) break;

@@ -141,7 +141,8 @@ class DitDynamics:
 
     def loss(self, latents: np.ndarray, action_latents, rng: np.random.Generator) -> Tensor:
         """diffusion.py:182-192: ramp-weighted x-prediction loss, per-frame tau ~ U(0, 1).
-        `.backward()` writes the gradients of every parameter (gt_action_embed: zero)."""
+        `.backward()` writes the gradients of every parameter; gt_action_embed's comes through
+        `action_latents` when it is `embedding(params["gt_action_embed"], ids)` (trainer.py:358-359)."""
         cfg, P = self.cfg, self.params
         latents = np.asarray(latents, dtype=np.float32)
         b, t = latents.shape[:2]
@@ -183,7 +184,12 @@ class DitDynamics:
                              db=G["noise_proj.b"])
             K.linear_f32_bwd(sv["z"], d_xlat, P["latent_embed.w"].data, dW=G["latent_embed.w"],
                              db=G["latent_embed.b"])
-            G["gt_action_embed"].zero_()  # rollout-only table: no gradient from the loss
+            G["gt_action_embed"].zero_()
+            if isinstance(action_latents, Tensor) and action_latents._backward is not None:
+                # embedding(dit.params["gt_action_embed"], actions) (trainer.py:358-359): frames 1..T-1
+                # of the conditioning are the action latents; the table gets their scatter
+                action_latents.grad = d_cond.view(b, t, -1)[:, 1:].contiguous()
+                action_latents.backward()
 
         return Tensor(loss, _backward=backward)
 

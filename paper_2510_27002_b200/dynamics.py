@@ -25,7 +25,7 @@ from . import _lib as L
 from . import kernels as K
 from .rng import PhiloxState, consume, stream
 from .st import StConfig, init_st_stack_arrays, st_backward, st_forward, st_param_groups
-from .tensor import ParamStore, Tensor, as_device, grad_buffers
+from .tensor import ParamStore, Tensor, as_device, embedding, grad_buffers
 
 
 class ConditioningMode(str, enum.Enum):
@@ -153,6 +153,8 @@ class DynamicsModel:
             if source_codebook is None:
                 raise ValueError("latent action indices need the LAM codebook")
             table = source_codebook if isinstance(source_codebook, Tensor) else Tensor(source_codebook)
+        if self.cfg.mode is ConditioningMode.GROUND_TRUTH:
+            return embedding(table, acts)  # differentiable: trains gt_action_embed (dynamics.py:95-96)
         if acts.size and (acts.min() < 0 or acts.max() >= table.shape[0]):
             raise IndexError(f"embedding ids out of range [0, {table.shape[0]})")
         idx = torch.as_tensor(acts.astype(np.int64), device=table.data.device)
@@ -227,7 +229,7 @@ class DynamicsModel:
                 mask_d = mask.to(torch.uint8).contiguous()
             else:
                 mask_d = as_device(np.asarray(mask, dtype=np.uint8))
-            count = mask_d.sum(dtype=torch.int32)
+            count = _count if _count is not None else mask_d.sum(dtype=torch.int32)
         if _count is not None:
             count = _count
         stats = _LazyStats(mask_d, count)
@@ -251,12 +253,12 @@ class DynamicsModel:
             K.dyn_embed_bwd(dx, f["tok"], mask_d, f["lat"], {k: v.data for k, v in P.items()}, G,
                             B=f["B"], T=f["T"], N=f["N"], D=cfg.model_dim, dl=cfg.action_latent_dim,
                             K=cfg.token_codes, prepend=self._prepend, d_latents=d_lat)
-            if _on_grads_done is not None:
-                _on_grads_done("embed")
             if need_lat_grad:
                 latents.grad = d_lat.view_as(latents.data)
                 if latents._backward is not None:
-                    latents.backward()
+                    latents.backward()  # e.g. the gt_action_embed scatter (dynamics.py:95-96)
+            if _on_grads_done is not None:  # after every write into this model's gradient buffer
+                _on_grads_done("embed")
 
         return Tensor(loss, _backward=backward), stats
 

@@ -411,6 +411,18 @@ def dyn_embed_bwd(dx, tokens, mask, latents, P: dict, G: dict, *, B, T, N, D, dl
            G["pos_temporal"].data_ptr(), _p(d_latents), ws.data_ptr(), _s())
 
 
+def embedding_table_bwd(dout: torch.Tensor, ids: torch.Tensor, dtable: torch.Tensor, accumulate: bool = False,
+                        err: torch.Tensor | None = None) -> None:
+    """dtable[k] (=|+=) sum_{ids[i]==k} dout[i] in index order (autodiff.py:344-364 embedding backward)."""
+    Kt, D = dtable.shape
+    if not dtable.is_contiguous():
+        raise ValueError("embedding_table_bwd: the table gradient must be contiguous")
+    ids = ids.reshape(-1).to(torch.int64).contiguous()
+    dout = dout.reshape(ids.numel(), D).to(F32).contiguous()
+    L.call("jz_embedding_table_bwd", dout.data_ptr(), ids.data_ptr(), ids.numel(), Kt, D, dtable.data_ptr(),
+           int(accumulate), _p(err), _s())
+
+
 def ce_fwd_bwd(logits: torch.Tensor, targets: torch.Tensor, mask: torch.Tensor | None, count: torch.Tensor,
                grad_scale: float = 1.0):
     rows, K = logits.shape
@@ -427,6 +439,10 @@ def finite_check(g: torch.Tensor, flag: torch.Tensor) -> None:
 
 
 def adamw(p, g, m, v, *, lr, b1, b2, omb1, omb2, bc1, bc2, eps, lrwd, flag=None) -> None:
+    """K13 over p[0..numel): every operand must be one dense contiguous block."""
+    for name, t in (("param", p), ("grad", g), ("m", m), ("v", v)):
+        if not t.is_contiguous() or t.numel() != p.numel():
+            raise ValueError(f"adamw: {name} must be contiguous with {p.numel()} elements")
     if DEVSTATE is not None:
         L.call("jz_adamw_step_dev", p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel(),
                DEVSTATE[1].data_ptr(), _p(flag), _s())

@@ -61,8 +61,9 @@ def adamw_init(params: dict, weight_decay: float = 0.0, beta1: float = 0.9, beta
             st.v[name] = store.view_of(st.v_flat, name)
     else:
         for name, p in params.items():
-            st.m[name] = torch.zeros_like(p.data)
-            st.v[name] = torch.zeros_like(p.data)
+            # contiguous moments even when p is a strided member of a fused block
+            st.m[name] = torch.zeros(p.data.shape, dtype=p.data.dtype, device=p.data.device)
+            st.v[name] = torch.zeros(p.data.shape, dtype=p.data.dtype, device=p.data.device)
     return st
 
 
@@ -92,7 +93,13 @@ def adamw_step(params: dict, grads: dict, state: AdamWState, lr: float, check: s
                 raise ValueError(f"gradient shape {tuple(g.shape)} != param shape {tuple(params[n].data.shape)} for {n!r}")
             K.finite_check(g.contiguous(), state.flag)
         for n in names:
-            K.adamw(params[n].data, grads[n].contiguous(), state.m[n], state.v[n], flag=state.flag, **sc)
+            p = params[n].data
+            if p.is_contiguous():
+                K.adamw(p, grads[n].contiguous(), state.m[n], state.v[n], flag=state.flag, **sc)
+            else:  # strided member of a fused q/k/v block: update a dense copy, write it back
+                pc = p.contiguous()
+                K.adamw(pc, grads[n].contiguous(), state.m[n], state.v[n], flag=state.flag, **sc)
+                p.copy_(pc)
     if check == "sync":
         state.raise_if_nonfinite()
 

@@ -16,68 +16,83 @@ from .rng import stream
 from .tensor import Tensor
 
 
-def _np_logits(model, tokens, latents, mask) -> np.ndarray:
-    out = model.logits(tokens, latents, mask=mask)
-    data = out.data if hasattr(out, "data") else out
-    if isinstance(data, torch.Tensor):
-        data = data.detach().cpu().numpy()
-    return np.asarray(data)
-
-
-def _sample_with_confidence(logits: np.ndarray, temperature: float, rng: np.random.Generator):
-    """dynamics.py:198-217."""
-    scaled = logits / max(temperature, 1e-8)
-    scaled = scaled - scaled.max(axis=-1, keepdims=True)
-    probs = np.exp(scaled)
-    probs /= probs.sum(axis=-1, keepdims=True)
-    if temperature < 1e-6:
-        sampled = np.argmax(logits, axis=-1)
-    else:
-        cdf = np.cumsum(probs, axis=-1)
-        u = rng.random(logits.shape[:-1] + (1,))
-        sampled = (u > cdf).sum(axis=-1)
-        sampled = np.minimum(sampled, logits.shape[-1] - 1)
-    conf = np.take_along_axis(probs, sampled[..., None], axis=-1)[..., 0]
-    return sampled.astype(np.int64), conf
+def _is_device_model(model) -> bool:
+    from .dynamics import DynamicsModel
+    return isinstance(model, DynamicsModel)
 
 
 def decode_frame(model, prev_tokens, action_latents, steps: int = 25, temperature: float = 1.0,
                  rng: np.random.Generator | None = None) -> np.ndarray:
-    from .dynamics import DynamicsModel
-    if isinstance(model, DynamicsModel) and model.cfg.mode.value != "additive":
+    """dynamics.py:156-194.  A DynamicsModel with a prepended action token decodes on the KV-cached
+    device path; any other model (additive conditioning, or a duck-typed stand-in with the
+    reference's cfg/params/logits surface, test_dynamics.py:143-170) runs the same device sampler
+    over full-clip logits (decode_frame_stepwise)."""
+    if _is_device_model(model) and model.cfg.mode.value != "additive":
         return decode_frame_device(model, prev_tokens, action_latents, steps, temperature, rng).cpu().numpy()
+    return decode_frame_stepwise(model, prev_tokens, action_latents, steps, temperature, rng).cpu().numpy()
+
+
+def decode_frame_stepwise(model, prev_tokens, action_latents, steps: int = 25, temperature: float = 1.0,
+                          rng: np.random.Generator | None = None) -> torch.Tensor:
+    """MaskGIT loop of dynamics.py:164-194 with K11 (jz_maskgit_step) doing the sampling, the
+    confidence and the top-n_keep reveal on the device every step; the logits of each step are a
+    full-clip forward of `model.logits` (device forward for a DynamicsModel; a duck-typed model's
+    host logits are copied in).  Draws: B*N uniforms per step from `rng` (none when greedy), in
+    the reference's order.  Returns cur (B, N) int64 in HBM."""
     if steps < 1:
         raise ValueError("steps must be >= 1")
     if rng is None:
         rng = stream(0, "maskgit-decode")
-    prev_tokens = np.asarray(prev_tokens)
-    b, t_prev, n = prev_tokens.shape
+    on_dev = _is_device_model(model)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    prev = prev_tokens.cpu().numpy() if isinstance(prev_tokens, torch.Tensor) else np.asarray(prev_tokens)
+    b, t_prev, n = prev.shape
     if action_latents.shape[1] != t_prev:
         raise ValueError(f"need {t_prev} action latents, got {action_latents.shape[1]}")
-    tokens = np.concatenate([prev_tokens, np.zeros((b, 1, n), dtype=prev_tokens.dtype)], axis=1)
-    known = np.zeros((b, n), dtype=bool)
-    cur = np.zeros((b, n), dtype=prev_tokens.dtype)
-    for s in range(1, steps + 1):
-        frac_masked = np.cos(np.pi / 2 * s / steps)
-        n_keep = n if s == steps else min(n, int(np.ceil(n * (1.0 - frac_masked))))
-        n_keep = max(n_keep, int(known[0].sum()))
-        tokens[:, -1] = cur
-        mask = np.zeros_like(tokens, dtype=bool)
-        mask[:, -1] = ~known
-        logits = _np_logits(model, tokens, action_latents, mask)[:, -1]
-        sampled, conf = _sample_with_confidence(logits, temperature, rng)
-        cur = np.where(known, cur, sampled)
-        conf = np.where(known, np.inf, conf)
-        order = np.lexsort((np.broadcast_to(np.arange(n), conf.shape), -conf), axis=-1)
-        new_known = np.zeros_like(known)
-        np.put_along_axis(new_known, order[:, :n_keep], True, axis=-1)
-        known = new_known
-    assert known.all(), "decode must leave zero masked positions"
+    K = int(model.cfg.token_codes)
+    tokens = np.concatenate([prev, np.zeros((b, 1, n), dtype=prev.dtype)], axis=1)
+    cur = torch.zeros(b, n, dtype=torch.int64, device=dev)
+    known = torch.zeros(b, n, dtype=torch.uint8, device=dev)
+    conf = torch.empty(b, n, dtype=torch.float32, device=dev)
+    if on_dev:
+        tok_d = torch.as_tensor(tokens).to(dev, torch.int64)
+        lat = action_latents if isinstance(action_latents, Tensor) else Tensor(np.asarray(action_latents))
+    greedy = temperature < 1e-6
+    for s, n_keep in enumerate(keep_counts(n, steps)):
+        if on_dev:
+            tok_d[:, -1] = cur
+            mask = torch.zeros(b, t_prev + 1, n, dtype=torch.uint8, device=dev)
+            mask[:, -1] = 1 - known
+            lg = model.logits(tok_d, lat, mask=mask).data[:, -1]
+        else:  # duck-typed stand-in: numpy in, its logits copied to the device sampler
+            tokens[:, -1] = cur.cpu().numpy()
+            mask = np.zeros(tokens.shape, dtype=bool)
+            mask[:, -1] = known.cpu().numpy() == 0
+            out = model.logits(tokens, action_latents, mask=mask)
+            lg = out.data if hasattr(out, "data") else out
+            lg = torch.as_tensor(np.asarray(lg.cpu() if isinstance(lg, torch.Tensor) else lg)[:, -1])
+        lg = lg.to(dev, torch.float32).contiguous()
+        z = (_C.c_uint64 * 4)()
+        if greedy:
+            _L.call("jz_maskgit_step", lg.data_ptr(), b, n, K, float(temperature), _C.addressof(z), _C.addressof(z),
+                    _C.addressof(z), 4, 0, n_keep, None, cur.data_ptr(), known.data_ptr(), conf.data_ptr(),
+                    _L.stream_ptr())
+        else:
+            st = _consume(rng, b * n)
+            ctr = (_C.c_uint64 * 4)(*st.counter)
+            key = (_C.c_uint64 * 2)(*st.key)
+            buf = (_C.c_uint64 * 4)(*st.buffer)
+            _L.call("jz_maskgit_step", lg.data_ptr(), b, n, K, float(temperature), _C.addressof(ctr),
+                    _C.addressof(key), _C.addressof(buf), int(st.buffer_pos), 0, n_keep, None, cur.data_ptr(),
+                    known.data_ptr(), conf.data_ptr(), _L.stream_ptr())
     return cur
 
 
 def rollout(tokenizer, dynamics, conditioning_frames, actions, horizon: int, steps: int = 25,
             temperature: float = 1.0, rng=None, source_codebook=None, prefix_action_latents=None):
+    """dynamics.py:220-260.  Device models with a prepended action token run rollout_device (KV
+    cache, graph-captured refinement steps); other models decode each frame with decode_frame's
+    device sampler."""
     from .dynamics import DynamicsModel
     from .tokenizer import VideoTokenizer, unit_to_frames
     if isinstance(dynamics, DynamicsModel) and isinstance(tokenizer, VideoTokenizer) \
@@ -106,8 +121,8 @@ def rollout(tokenizer, dynamics, conditioning_frames, actions, horizon: int, ste
             lat = action.data.reshape(b, 1, dlat)
         else:
             lat = dynamics.action_latents_for(np.asarray(action).reshape(b, 1), source_codebook).data
-        history = torch.cat([history, lat.to(history.device)], dim=1)
-        nxt = dynamics.decode_frame(tokens, Tensor(history), steps=steps, temperature=temperature, rng=rng)
+        history = torch.cat([history, lat.to(history.device, history.dtype)], dim=1)
+        nxt = decode_frame(dynamics, tokens, Tensor(history), steps=steps, temperature=temperature, rng=rng)
         tokens = np.concatenate([tokens, np.asarray(nxt)[:, None, :]], axis=1)
     unit = tokenizer.decode(tokens)
     return unit_to_frames(unit)

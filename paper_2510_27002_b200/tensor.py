@@ -137,6 +137,38 @@ class Tensor:
                 fn()
 
 
+def embedding(table: Tensor, ids) -> Tensor:
+    """autodiff.embedding (autodiff.py:350-364): row lookup `table[ids]`; the output's backward
+    scatters `out.grad` into `table.grad` with a deterministic owner-computes kernel. Gradients
+    here are per-step buffers, so the scatter overwrites (the reference accumulates into a fresh
+    p.grad = None each step, trainer.py:181-183)."""
+    from . import kernels as K
+    if isinstance(ids, torch.Tensor):
+        idx = ids.to(table.data.device, torch.int64)
+        if idx.numel():
+            lo, hi = int(idx.min()), int(idx.max())
+            if lo < 0 or hi >= table.shape[0]:
+                raise IndexError(f"embedding ids out of range [0, {table.shape[0]})")
+    else:
+        arr = np.asarray(ids)
+        if arr.size and (arr.min() < 0 or arr.max() >= table.shape[0]):
+            raise IndexError(f"embedding ids out of range [0, {table.shape[0]})")
+        idx = torch.as_tensor(arr.astype(np.int64)).to(table.data.device)
+    out = Tensor(table.data[idx])
+    if not table.requires_grad:
+        return out
+
+    def bw():
+        if out.grad is None:
+            return
+        if table.grad is None or tuple(table.grad.shape) != tuple(table.data.shape):
+            table.grad = torch.zeros_like(table.data)
+        K.embedding_table_bwd(out.grad, idx, table.grad)
+
+    out._backward = bw
+    return out
+
+
 def parameter(data) -> Tensor:
     return Tensor(data, requires_grad=True)
 

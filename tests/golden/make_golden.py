@@ -278,11 +278,71 @@ def gen_mae():
          **{f"param.{k}": v.data for k, v in mae.params.items()}, **grads)
 
 
+def gen_device_rollout():
+    """rollout (dynamics.py:220-260) through a real tokenizer at dims the device path runs
+    (model_dim 128, 2 heads of 64, patch 16 on 64x64 frames: N = 16), ground-truth and additive
+    conditioning.  to_logits.w is scaled by 40 so the MaskGIT picks are decided by clear margins
+    (bf16 vs fp32 logits then pick the same tokens); the scaling is part of the fixture."""
+    tcfg = TokenizerConfig(model_dim=128, heads=2, ffn_dim=512, blocks=1, codes=64, latent_dim=32,
+                           patch=16, height=64, width=64, max_frames=6)
+    tok = VideoTokenizer(tcfg, seed=6)
+    frames = R.stream(23, "dev-roll").integers(0, 256, size=(2, 4, 64, 64, 3)).astype(np.uint8)
+    out = {"frames": frames, "tokens": tok.encode(frames)}
+    base = dict(model_dim=128, heads=2, ffn_dim=512, blocks=1, token_codes=64, action_latent_dim=32,
+                patches_per_frame=16, max_frames=6)
+    for mode in (ConditioningMode.GROUND_TRUTH, ConditioningMode.ADDITIVE):
+        dyn = DynamicsModel(DynamicsConfig(**base, mode=mode), seed=7)
+        dyn.params["to_logits.w"].data *= np.float32(40.0)
+        if mode is ConditioningMode.GROUND_TRUTH:
+            actions, cb = [np.array([1, 3]), np.array([2, 0])], None
+        else:
+            cb = Tensor(R.stream(24, "dev-roll-cb").uniform(-0.5, 0.5, size=(6, 32)).astype(np.float32))
+            actions = [np.array([4, 1]), np.array([0, 5])]
+        roll = rollout(tok, dyn, frames, actions, horizon=2, steps=5, rng=R.stream(9, "dev-roll", mode.value),
+                       source_codebook=cb)
+        # the generated tokens, through the same public calls rollout makes (dynamics.py:243-258)
+        g = R.stream(9, "dev-roll", mode.value)
+        tokens = tok.encode(frames)
+        hist = Tensor(np.broadcast_to(dyn.params["null_action"].data, (2, 3, 32)).copy())
+        for a in actions:
+            lat = dyn.action_latents_for(a.reshape(2, 1), cb)
+            hist = Tensor(np.concatenate([hist.data, lat.data], axis=1))
+            nxt = dyn.decode_frame(tokens, hist, steps=5, rng=g)
+            tokens = np.concatenate([tokens, nxt[:, None]], axis=1)
+        from deskworld.tokenizer import unit_to_frames
+        assert np.array_equal(unit_to_frames(tok.decode(tokens)), roll)
+        out[f"{mode.value}.out"] = roll
+        out[f"{mode.value}.out_tokens"] = tokens
+        out[f"{mode.value}.actions"] = np.stack(actions)
+        if cb is not None:
+            out[f"{mode.value}.codebook"] = cb.data
+    save("device_rollout_golden", **out)
+
+
+def gen_configs():
+    """configs.py presets and the model configs derived from them (JSON)."""
+    import json
+    from deskworld.configs import PRESETS
+    res = {}
+    for name, cfg in PRESETS.items():
+        d = {"train": cfg.to_dict(), "tokenizer": dataclasses.asdict(cfg.tokenizer_cfg),
+             "lam": dataclasses.asdict(cfg.lam_cfg), "mae": dataclasses.asdict(cfg.mae_cfg),
+             "dit": dataclasses.asdict(cfg.dit_cfg)}
+        for cond in (None, "additive", "prepend"):
+            dc = dataclasses.asdict(cfg.dynamics_cfg(cond))
+            dc["mode"] = cfg.dynamics_cfg(cond).mode.value
+            d[f"dynamics.{cond}"] = dc
+        res[name] = d
+    (OUT / "configs_golden.json").write_text(json.dumps(res, indent=1, sort_keys=True))
+    print("wrote configs_golden.json")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "vq", "dynamics", "toklam", "sampling", "adamw", "jasmine", "checkpoint",
                              "records"]
     fns = {"rng": gen_rng, "vq": gen_vq, "dynamics": gen_dynamics, "toklam": gen_tokenizer_lam,
            "sampling": gen_sampling, "adamw": gen_adamw, "jasmine": gen_jasmine_summary,
-           "checkpoint": gen_checkpoint, "records": gen_records, "dit": gen_dit, "mae": gen_mae}
+           "checkpoint": gen_checkpoint, "records": gen_records, "dit": gen_dit, "mae": gen_mae,
+           "device_rollout": gen_device_rollout, "configs": gen_configs}
     for w in which:
         fns[w]()

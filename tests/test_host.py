@@ -213,3 +213,35 @@ def test_gloo_two_rank_bucketed_allreduce():
         p.join(timeout=60)
     expect = [float(i * 3) for i in range(10)]
     assert out[0] == expect and out[1] == expect
+
+
+def test_configs_mirror_reference_presets():
+    """configs.py mirror: every preset, its to_dict and every derived model config equal the
+    reference's (tests/golden/configs_golden.json, written by make_golden.py from deskworld)."""
+    import dataclasses
+    import json
+    from pathlib import Path
+
+    from paper_2510_27002_b200 import configs as C
+    gold = json.loads((Path(__file__).parent / "golden" / "configs_golden.json").read_text())
+    assert sorted(C.PRESETS) == sorted(gold)
+    for name, g in gold.items():
+        cfg = C.get_preset(name)
+        assert json.loads(json.dumps(cfg.to_dict())) == g["train"], name
+        assert C.TrainConfig.from_dict(cfg.to_dict()) == cfg
+        for key, derived in (("tokenizer", cfg.tokenizer_cfg), ("lam", cfg.lam_cfg), ("mae", cfg.mae_cfg),
+                             ("dit", cfg.dit_cfg)):
+            assert json.loads(json.dumps(dataclasses.asdict(derived))) == g[key], (name, key)
+        for cond in (None, "additive", "prepend"):
+            dc = cfg.dynamics_cfg(cond)
+            d = dataclasses.asdict(dc)
+            d["mode"] = dc.mode.value
+            assert json.loads(json.dumps(d)) == g[f"dynamics.{cond}"], (name, cond)
+    with pytest.raises(ValueError):
+        C.get_preset("nope")
+    with pytest.raises(ValueError):
+        C.TrainConfig(mode="bogus")
+    with pytest.raises(ValueError):
+        C.TrainConfig(seq_len=1)
+    with pytest.raises(ValueError):
+        C.TrainConfig(conditioning="sideways")
