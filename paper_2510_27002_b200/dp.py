@@ -26,17 +26,28 @@ import torch.distributed as dist
 
 
 def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
-    """torchrun env -> (rank, world, local_rank); initialises the process group once."""
+    """torchrun env -> (rank, world, device index); initialises the process group once.
+
+    One process per GPU over NCCL.  When there are more ranks than visible GPUs (JZ_DP_SHARED_GPU=1,
+    or world > device count) the ranks share devices round-robin and talk over gloo: NCCL refuses
+    two ranks on one device, gloo all-reduces CUDA tensors through host memory.  That mode exists to
+    run the multi-process step end to end on a single-GPU box; it is not a performance mode."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = local
+    if torch.cuda.is_available():
+        n = torch.cuda.device_count()
+        shared = os.environ.get("JZ_DP_SHARED_GPU", "0") == "1" or world > n
+        if shared:
+            dev = local % n
+            backend = backend or "gloo"
+        torch.cuda.set_device(dev)
     if world > 1 and not dist.is_initialized():
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if torch.cuda.is_available():
-            torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
-    return rank, world, local
+    return rank, world, dev
 
 
 def shard(global_batch: int, rank: int, world: int) -> tuple[int, int]:

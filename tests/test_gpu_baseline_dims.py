@@ -184,7 +184,8 @@ def test_c1_vq_indices_exact_on_oracle_latents(c1):
     mism = int((got != ref).sum())
     _report("c1", vq_mismatches_on_oracle_latents=mism, rows=int(got.size))
     assert _near_tie_ok(z, cb, got, ref)
-    np.testing.assert_array_equal(zq.cpu().numpy(), cb[got])
+    # straight-through value z + (z_q - z) in f32 (tokenizer.py:78), not z_q itself
+    np.testing.assert_array_equal(zq.cpu().numpy(), z + (cb[got] - z))
 
 
 def test_c1_tokenizer_forward_vs_oracle(c1):
@@ -257,7 +258,7 @@ def test_c5_decode_frame_jasmine_dims_vs_oracle():
     ref = OM.decode_frame(logits_fn, prev, lat, steps=25, gen=og)
     agree = float((got == ref).mean())
     _report("c5", token_agreement=agree)
-    assert agree >= TOL["decode_token_agreement_peaked"]
+    assert agree >= TOL["decode_token_agreement_jasmine_chain"]
     assert g.random() == og.random()
 
 

@@ -63,7 +63,7 @@ def test_loss_and_grads_match_oracle(case):
     dit, P = case["dit"], case["P"]
     loss = dit.loss(case["latents"], case["act"], R.stream(9, "dit-loss"))
     ref = OM.dit_loss(P, OM.DitCfg(**KW), case["latents"], torch.tensor(case["act"]), OR.stream(9, "dit-loss"))
-    assert abs(float(loss.data) - float(ref)) < max(TOL["bf16_loss_abs"], 1e-2 * float(ref))
+    assert abs(float(loss.data) - float(ref)) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(ref))
     loss.backward()
     ref.backward()
     bad = []
@@ -136,7 +136,7 @@ def test_mae_forward_backward_match_oracle(mae_case):
     r2, l2, loss2 = OM.mae_forward(P, OM.MaeCfg(**MAEKW), torch.tensor(mae_case["unit"]), OR.stream(13, "mae-step"))
     assert _rel(lat.numpy(), l2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
     assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
-    assert abs(float(loss.data) - float(loss2)) < max(TOL["bf16_loss_abs"], 1e-2 * float(loss2))
+    assert abs(float(loss.data) - float(loss2)) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(loss2))
     loss.backward()
     loss2.backward()
     bad = []
@@ -144,7 +144,7 @@ def test_mae_forward_backward_match_oracle(mae_case):
         if k.endswith(".k.b"):
             continue
         ref, got = P[k].grad.numpy(), p.grad.cpu().numpy()
-        if _cos(got, ref) < 0.995:
+        if _cos(got, ref) < TOL["bf16_grad_cosine_min_vq_models"]:
             bad.append((k, _cos(got, ref), _rel(got, ref)))
     assert not bad, bad
 

@@ -2,6 +2,8 @@
 PlayService, server.py:55-135): protocol and error codes, PNG frames, and the KV-cached session
 against stateless decode_frame calls on the same generator (the reference's semantics, which
 re-run the whole clip every act)."""
+import json
+from pathlib import Path
 import base64
 import io
 
@@ -12,6 +14,7 @@ import torch
 from oracle import rng as OR
 
 pytestmark = pytest.mark.gpu
+TOL = json.loads((Path(__file__).resolve().parent.parent / "fidelity_threshold.json").read_text())["parity"]
 
 DKW = dict(model_dim=128, heads=2, ffn_dim=512, blocks=2, token_codes=256, action_latent_dim=32,
            patches_per_frame=256, max_frames=6)
@@ -96,6 +99,6 @@ def test_play_session_kv_cache_matches_stateless_decode():
         else:
             # the session read K/V it appended through the single-frame path (a slide re-prefills):
             # equal to the full recompute within bf16 rounding, so only near-tie draws may differ
-            assert float((got == ref).float().mean()) >= 0.97, (k, float((got == ref).float().mean()))
+            assert float((got == ref).float().mean()) >= TOL["decode_token_agreement_peaked"], (k, float((got == ref).float().mean()))
         tokens = torch.cat([tokens, got[None, None]], dim=1)
     assert torch.equal(tokens, sess.tokens)

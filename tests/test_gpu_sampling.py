@@ -1,4 +1,6 @@
 """Device MaskGIT sampling: KV-cache exactness, sampler kernel vs the oracle, decode/rollout."""
+import json
+from pathlib import Path
 import numpy as np
 import pytest
 import torch
@@ -7,6 +9,7 @@ from oracle import model as OM
 from oracle import rng as OR
 
 pytestmark = pytest.mark.gpu
+TOL = json.loads((Path(__file__).resolve().parent.parent / "fidelity_threshold.json").read_text())["parity"]
 
 DKW = dict(model_dim=128, heads=2, ffn_dim=512, blocks=2, token_codes=256, action_latent_dim=32,
            patches_per_frame=256, max_frames=6)
@@ -35,7 +38,7 @@ def test_kv_cached_frame_logits_match_full_recompute():
     mask[:, -1] = (known == 0).cpu().numpy()
     full = m.logits(tokens, Tensor(lat), mask=mask).data[:, -1].reshape(B * 256, -1)
     rel = float((got - full).norm() / full.norm())
-    assert rel < 5e-3, rel
+    assert rel < TOL["kv_cache_logits_rel"], rel
 
 
 def test_sampler_kernel_vs_oracle():
@@ -102,7 +105,7 @@ def test_decode_frame_peaked_matches_oracle():
 
     og = OR.stream(18, "dec-rng")
     ref = OM.decode_frame(logits_fn, prev, lat, steps=5, gen=og)
-    assert (got == ref).mean() > 0.97
+    assert (got == ref).mean() >= TOL["decode_token_agreement_peaked"]
     assert g.random() == og.random()  # same number of draws consumed
 
 
@@ -162,7 +165,7 @@ def test_temporal_decode_kernel_vs_torch(D, t):
     vals = torch.cat([cv, v.unsqueeze(2)], 2)
     sc = torch.einsum("bshd,bsthd->bsht", q, keys) / 8.0
     ref = torch.einsum("bsht,bsthd->bshd", sc.softmax(-1), vals).reshape(B * S, D)
-    assert float((out.float() - ref).norm() / ref.norm()) < 8e-3
+    assert float((out.float() - ref).norm() / ref.norm()) < TOL["bf16_kernel_rel_l2"]
     assert torch.equal(cache[:, t], qkv.view(B, S, 3 * D)[:, :, D:])
     assert torch.equal(cache[:, :t], ref_cache[:, :t])
     # host frame index, no append: same output

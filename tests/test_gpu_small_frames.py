@@ -90,7 +90,7 @@ def test_tokenizer_patch16_forward_backward(frames):
     unit = OM.frames_to_unit(frames)
     recon, idx, losses = tok.forward(unit)
     _, i2, _ = OM.tok_forward(P, ocfg, torch.tensor(unit))
-    assert (idx == np.asarray(i2)).mean() > 0.99  # bf16 encoder: only near-tie codes may flip
+    assert (idx == np.asarray(i2)).mean() >= TOL["vq_index_agreement_bf16_encoder"]  # bf16 encoder: only near-tie codes may flip
     u = torch.tensor(unit)
     z_e = OM.tok_encode_latent(P, ocfg, u)
     z_q = P["codebook"][torch.as_tensor(idx)]
@@ -100,10 +100,10 @@ def test_tokenizer_patch16_forward_backward(frames):
     l2 = {"recon": rec, "codebook": cb, "commitment": commit, "total": rec + cb + ocfg.commitment_beta * commit}
     assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
     for k in ("recon", "codebook", "commitment", "total"):
-        assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
+        assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(l2[k])), k
     losses["total"].backward()
     l2["total"].backward()
-    bad = _grad_mismatches(tok.params, P, 0.995)
+    bad = _grad_mismatches(tok.params, P, TOL["bf16_grad_cosine_min_vq_models"])
     assert not bad, bad
 
 
@@ -120,10 +120,10 @@ def test_lam_patch16_forward_backward(frames):
     np.testing.assert_array_equal(idx, i2)
     assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
     for k in ("recon", "codebook", "commitment", "total"):
-        assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
+        assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(l2[k])), k
     losses["total"].backward()
     l2["total"].backward()
-    bad = _grad_mismatches(lam.params, P, 0.995)
+    bad = _grad_mismatches(lam.params, P, TOL["bf16_grad_cosine_min_vq_models"])
     assert not bad, bad
 
 

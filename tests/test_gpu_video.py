@@ -106,7 +106,7 @@ class TestTokenizer:
         idx = tok.encode(frames)
         ref = OM.tok_encode(P, ocfg, frames)
         # encoder runs in bf16: indices may legitimately flip where codes are nearly equidistant
-        assert (idx == ref).mean() > 0.97
+        assert (idx == ref).mean() >= TOL["vq_index_agreement_small_encoder"]
 
     def test_decode_and_forward(self, frames):
         from paper_2510_27002_b200.tokenizer import TokenizerConfig, VideoTokenizer
@@ -124,7 +124,7 @@ class TestTokenizer:
         with torch.no_grad():
             r2, i2, l2 = OM.tok_forward(P, ocfg, torch.tensor(unit))
         for k in ("recon", "codebook", "commitment", "total"):
-            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
+            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(l2[k])), k
 
     def test_forward_backward_vs_oracle(self, frames):
         """Tokenizer training step (trainer.py:211-223): losses and every parameter gradient."""
@@ -135,7 +135,7 @@ class TestTokenizer:
         unit = OM.frames_to_unit(frames)
         recon, idx, losses = tok.forward(unit)
         _, i2, _ = OM.tok_forward(P, ocfg, torch.tensor(unit))
-        assert (idx == np.asarray(i2)).mean() > 0.99  # bf16 encoder: only near-tie codes may flip
+        assert (idx == np.asarray(i2)).mean() >= TOL["vq_index_agreement_bf16_encoder"]  # bf16 encoder: only near-tie codes may flip
         # oracle step on OUR code indices (a flipped code moves a whole patch): tokenizer.py:58-79, 134-143
         u = torch.tensor(unit)
         z_e = OM.tok_encode_latent(P, ocfg, u)
@@ -146,7 +146,7 @@ class TestTokenizer:
         l2 = {"recon": rec, "codebook": cb, "commitment": commit, "total": rec + cb + ocfg.commitment_beta * commit}
         assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
         for k in ("recon", "codebook", "commitment", "total"):
-            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
+            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(l2[k])), k
         losses["total"].backward()
         l2["total"].backward()
         bad = []
@@ -155,7 +155,7 @@ class TestTokenizer:
             got = p.grad.cpu().numpy()
             if k.endswith(".k.b") or np.linalg.norm(ref) < 1e-9:
                 continue  # .k.b: exactly zero in exact arithmetic (softmax shift invariance)
-            if _cos(got, ref) < 0.995:
+            if _cos(got, ref) < TOL["bf16_grad_cosine_min_vq_models"]:
                 bad.append((k, _cos(got, ref), _rel(got, ref)))
         assert not bad, bad
 
@@ -183,7 +183,7 @@ class TestLam:
         np.testing.assert_array_equal(idx, i2)
         assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
         for k in ("recon", "codebook", "commitment", "total"):
-            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], 2e-2 * float(l2[k])), k
+            assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(l2[k])), k
         losses["total"].backward()
         l2["total"].backward()
         bad = []
@@ -194,7 +194,7 @@ class TestLam:
                 continue  # exactly zero in exact arithmetic (softmax shift invariance)
             if np.linalg.norm(ref) < 1e-9:
                 continue
-            if _cos(got, ref) < 0.995:
+            if _cos(got, ref) < TOL["bf16_grad_cosine_min_vq_models"]:
                 bad.append((k, _cos(got, ref), _rel(got, ref)))
         assert not bad, bad
 
@@ -240,7 +240,7 @@ class TestCotrain:
         ce2, _ = OM.dyn_loss(Pd, OM.DynCfg(**dkw), tokens, zq2, mask)
         total2 = ce2 + cb2 + beta * commit2
         np.testing.assert_array_equal(idx, np.asarray(i2))
-        assert abs(float(total.data) - float(total2)) < max(TOL["bf16_loss_abs"], 1e-2 * float(total2))
+        assert abs(float(total.data) - float(total2)) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(total2))
         total.backward()
         total2.backward()
         bad = []
@@ -252,7 +252,7 @@ class TestCotrain:
                     if k.startswith("dec") and model is lam:
                         assert np.linalg.norm(got) == 0, k  # decoder is not in the cotrain graph
                     continue
-                if _cos(got, ref) < 0.99:
+                if _cos(got, ref) < TOL["bf16_grad_cosine_min_cotrain"]:
                     bad.append((k, _cos(got, ref), _rel(got, ref)))
         assert not bad, bad
         with pytest.raises(NotImplementedError):
