@@ -103,11 +103,33 @@ class ClockSampler:
 
 
 def cpu_baseline(steps: int = 2) -> dict:
-    from oracle.bench_cpu import time_dynamics_step
+    from oracle.bench_cpu import host_info, time_dynamics_step
     r = time_dynamics_step(batch=1, steps=steps, warmup=1)
     return {"value": round(r["frames_per_s"], 4), "unit": UNIT, "cores": r["threads"], "kind": "port",
             "sample": f"oracle port (torch-CPU fp32 restatement of deskworld) dynamics train step, jasmine-base dims, "
-                      f"B=1 (16 frames), {steps} timed steps after 1 warm-up, {r['seconds_per_step']:.2f} s/step"}
+                      f"B=1 (16 frames), {steps} timed steps after 1 warm-up, {r['seconds_per_step']:.2f} s/step",
+            "host": host_info()}
+
+
+def cpu_baseline_secondary() -> dict:
+    """SURVEY §8d CPU timing plan for the other BASELINE configs (oracle port, all host cores):
+    C1 tokenizer forward at B=2, C2 LAM train step at B=1, C5 one generated frame at B=1."""
+    from oracle.bench_cpu import time_decode_frame, time_lam_step, time_tokenizer_fwd
+    out = {}
+    r = time_tokenizer_fwd(batch=2, steps=1, warmup=1)
+    out["tokenizer_fwd"] = {"value": round(r["frames_per_s"], 3), "unit": "frames/s", "cores": r["threads"],
+                            "kind": "port", "sample": f"C1 tokenizer forward + quantize, B=2 (32 frames), 1 timed "
+                                                      f"step after 1 warm-up, {r['seconds_per_step']:.2f} s"}
+    r = time_lam_step(batch=1, steps=1, warmup=1)
+    out["lam_train"] = {"value": round(r["frames_per_s"], 3), "unit": "frames/s", "cores": r["threads"],
+                        "kind": "port", "sample": f"C2 LAM forward + backward + AdamW, B=1 (16 frames), 1 timed "
+                                                  f"step after 1 warm-up, {r['seconds_per_step']:.2f} s"}
+    r = time_decode_frame(batch=1, context=10, steps=25)
+    out["sample"] = {"value": round(r["frames_per_s"], 4), "unit": "frames/s", "cores": r["threads"],
+                     "kind": "port", "sample": f"C5 one generated frame at B=1: 25 MaskGIT refinements, each the "
+                                               f"reference's full-clip forward over 10 context frames (mid-rollout), "
+                                               f"{r['seconds_per_frame']:.2f} s"}
+    return out
 
 
 def _events_ms(fn, reps: int = 1) -> float:
@@ -153,7 +175,9 @@ def secondary_configs(dev) -> dict:
                      "unit": "frames/s", "ms_per_rollout": round(ms, 1), "rollouts_ms": [round(r, 1) for r in runs],
                      "config": "C5: batch 64, 4 cond -> 12 generated frames, 25 MaskGIT steps, T=1, KV-cached "
                                "last-frame forward, tokenizer encode+decode included",
-                     "algorithmic_tflops": round(351.2e9 * gen / (ms / 1e3) / 1e12, 1)}
+                     "algorithmic_tflops": round(351.2e9 * gen / (ms / 1e3) / 1e12, 1),
+                     "roofline": _frac_line(351.2e9 * gen / (ms / 1e3),
+                                            "SURVEY §8d: 351.2 GFLOP per generated frame (KV-cached dynamics)")}
     # C2: LAM train step (forward, backward and AdamW: run_stage's step body), B=8, T=16
     from paper_2510_27002_b200.optim import WsdSchedule
     from paper_2510_27002_b200.trainer import lam_stage, tokenizer_stage
@@ -175,7 +199,9 @@ def secondary_configs(dev) -> dict:
                         "unit": "frames/s", "ms_per_step": round(ms2, 2),
                         "config": "C2: B=8, T=16, 6 codes; forward + backward + AdamW (trainer.lam_stage), "
                                   f"replayed as {'a CUDA graph' if lam_run is not lam_tr else 'eager steps'}",
-                        "model_tflops": round(53.37e9 * 8 * FRAMES_T / (ms2 / 1e3) / 1e12, 1)}
+                        "model_tflops": round(53.37e9 * 8 * FRAMES_T / (ms2 / 1e3) / 1e12, 1),
+                        "roofline": _frac_line(53.37e9 * 8 * FRAMES_T / (ms2 / 1e3),
+                                               "SURVEY §8d: 53.37 GFLOP per trained frame (3x forward)")}
     # C1: tokenizer forward (encode + VQ + decode + losses), B=2; static shapes, so the forward is
     # captured once as a CUDA graph (indices stay on device) and replayed
     fr2 = fr8[:2].clone()
@@ -198,7 +224,9 @@ def secondary_configs(dev) -> dict:
     out["tokenizer_fwd"] = {"metric": "tokenizer fwd+quantize frames/sec", "value": round(2 * FRAMES_T / (ms1 / 1e3), 1),
                             "unit": "frames/s", "ms_per_step": round(ms1, 2),
                             "eager_ms_per_step": round(ms1_eager, 2),
-                            "config": f"C1: B=2, T=16, 1024 codes; {c1_mode}"}
+                            "config": f"C1: B=2, T=16, 1024 codes; {c1_mode}",
+                            "roofline": _frac_line(18.35e9 * 2 * FRAMES_T / (ms1 / 1e3),
+                                                   "SURVEY §8d: 18.35 GFLOP per frame (encoder + decoder)")}
 
     # tokenizer training step: forward + full backward + AdamW, B=8
     tok_tr = tokenizer_stage(tok, WsdSchedule(peak_lr=3e-5, total_steps=200_000), seed=0)
@@ -220,6 +248,15 @@ def secondary_configs(dev) -> dict:
     out["play_act"] = _play_act(tok, lam, dev)
     out["dit_train"] = _dit_train(dev)
     return out
+
+
+def _frac_line(flops_per_s: float, basis: str) -> dict:
+    """Whole-model throughput against the bf16 tensor peak (these steps are GEMM-dominated)."""
+    pk = _peaks()
+    tf = flops_per_s / 1e12
+    return {"bound": "tensor", "achieved": round(tf, 1), "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
+            "frac": round(tf / pk["bf16_sustained"], 4), "basis": basis,
+            "peak_source": f"{pk['source']} bf16_tflops_sustained"}
 
 
 def _dit_train(dev) -> dict:
@@ -534,6 +571,13 @@ def main() -> None:
             extra = secondary_configs(dev)
         except Exception as exc:  # never sink the headline line
             extra = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+        if not args.no_cpu_baseline:
+            try:
+                for k, v in cpu_baseline_secondary().items():
+                    if isinstance(extra.get(k), dict):
+                        extra[k]["cpu_baseline"] = v
+            except Exception as exc:
+                extra["cpu_baseline_error"] = f"{type(exc).__name__}: {str(exc)[:200]}"
 
     peaks = _peaks()
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
