@@ -97,6 +97,31 @@ JZ_API int jz_gemm_bf16_colsum(const void* A, int64_t lda, int a_kmajor, const v
                                int64_t ldd2, float* colsum_part, jz_stream_t stream);
 
 
+/* LayerNorm fused into the K1 GEMM epilogue (nn.layer_norm, nn.py:35-40, and its backward), for
+ * N = 512 (one CTA pair computes both 256-column tiles of a 256-row block back to back, so each
+ * row's statistics close inside the pair; no separate LayerNorm pass over HBM).
+ *
+ * jz_gemm_bf16_ln_fwd: the residual projection and the next sub-layer's LayerNorm (st.py:73-79):
+ *   D f32 = resid + A.B + bias                       (the residual stream, as JZ_EPI_RESID)
+ *   xn bf16 = (D - mean) * rstd * gamma + beta       (two-pass statistics, biased variance, eps)
+ *   mean, rstd f32 [M]; skip_period > 0 drops rows r % skip_period == 0 from xn (compacted rows).
+ * jz_gemm_bf16_ln_bwd: the input-gradient GEMM of a LayerNorm-fed layer and the LayerNorm backward:
+ *   dy = A.B (gradient of xn); dres f32 (+)= LN_bwd(dy; x, mean, rstd, gamma); dres_bf16 copy (may be
+ *   NULL); dgamma = sum dy*xhat, dbeta = sum dy, dbias = sum dres (column sums, each may be NULL),
+ *   reduced deterministically from `part` f32 [3][nparts][512], nparts = jz_gemm_ln_bwd_parts(M).
+ * A must be K-major (activations); b_kmajor as in jz_gemm_bf16. */
+JZ_API int jz_gemm_bf16_ln_fwd(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor,
+                               float* D, int64_t ldd, int64_t M, int64_t N, int64_t K, const float* bias,
+                               const float* resid, int64_t ld_resid, const float* gamma, const float* beta,
+                               float eps, void* xn_bf16, float* mean, float* rstd, int64_t skip_period,
+                               jz_stream_t stream);
+JZ_API int64_t jz_gemm_ln_bwd_parts(int64_t M);
+JZ_API int jz_gemm_bf16_ln_bwd(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor,
+                               int64_t M, int64_t N, int64_t K, const float* x, const float* mean,
+                               const float* rstd, const float* gamma, float* dres, int accumulate,
+                               void* dres_bf16, float* part, int64_t nparts, float* dgamma, float* dbeta,
+                               float* dbias, jz_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * Column reductions (bias / LayerNorm-affine gradients; replaces the
  * _unbroadcast sums of autodiff.py:22-32).  Deterministic two-stage scheme:

@@ -42,6 +42,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 int make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
                  uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  return make_tmap_2d_sw(map, base, elem_bytes, inner, outer, pitch_elems, box_inner, box_outer, swizzle128 ? 128 : 0);
+}
+
+int make_tmap_2d_sw(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
+                    uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
   auto enc = encoder();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -53,7 +58,8 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t in
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                        : (swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu pitch=%llu box=%ux%u", (int)r,

@@ -48,6 +48,10 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64
 int make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
                  uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, bool swizzle128 = true);
 
+// explicit swizzle span in bytes: 0 (none), 64 or 128
+int make_tmap_2d_sw(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
+                    uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
 int num_sms();
 
 }  // namespace jz

@@ -77,6 +77,21 @@ struct GemmParams {
   float* colsum;  // optional per-32-row-block column sums of the bf16 output [ceil(M/32)][N]
   int tma_epi;    // 1: smem-staged epilogue, 0: direct per-thread stores (unaligned shapes)
   int store_tma;  // staged epilogue writes with TMA bulk stores (1) or coalesced st.global (0)
+  // LayerNorm-fused epilogues (kernel template LNX != 0; N = 512 = two 256-column pair tiles of
+  // the same rows, run back to back by one CTA pair so a row's statistics close in the pair):
+  //   LNX = 1  D f32 = aux + acc + bias (the residual stream), ln_out16 = LN(D) bf16, mean/rstd out
+  //   LNX = 2  LN backward of dy = acc: D f32 (the residual gradient) (+)= LN_bwd(dy; ln_x, mean,
+  //            rstd, gamma); D2 bf16 copy of D; per-warp column partials of dgamma/dbeta/colsum(D)
+  const float* ln_gamma;
+  const float* ln_beta;
+  float* ln_mean;
+  float* ln_rstd;
+  __nv_bfloat16* ln_out16;
+  float* ln_part;        // LNX = 2: [3][nparts][N]
+  int64_t ln_nparts;
+  int64_t ln_skip;       // LNX = 1: rows r % ln_skip == 0 get no LN output; output rows compacted
+  int ln_accumulate;     // LNX = 2: D += (1) or D = (0)
+  float ln_eps;
 };
 
 struct EpiMaps {
@@ -100,16 +115,20 @@ __device__ __forceinline__ void stg_write_rows(const uint8_t* stg, uint8_t* gbas
 
 // PAIR: a cluster of two CTAs runs one cta_group::2 MMA of M = 256; each CTA stages its own 128
 // rows of A and half of the BN columns of B, so operand bytes per MAC drop by a third.
-template <int BN, bool PAIR = false>
+// LNX (LayerNorm-fused epilogue): four 4 KB staging tiles per epilogue warp (prefetched fp32 input
+// tiles + output tiles), paid for with three operand stages instead of six.
+template <int BN, bool PAIR = false, int LNX = 0>
 struct GemmShape {
   static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = ((PAIR ? 192 : 200) * 1024) / STAGE_BYTES;
+  // per epilogue warp: 32 rows x 128 B tiles, 128B-swizzled (LNX 1: two fp32 + two bf16 tiles,
+  // LNX 2: four fp32 tiles)
+  static constexpr int STG_BYTES = LNX == 1 ? 12288 : (LNX == 2 ? 16384 : 4096);
+  static constexpr int STAGES_RAW = ((PAIR ? 192 : 200) * 1024 - 8 * (STG_BYTES - 4096)) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int STG_BYTES = 4096;  // per epilogue warp: 32 rows x 128 B, 128B-swizzled
   static constexpr int EW = epi_warps<PAIR>();
   static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EW * STG_BYTES + 1024 + BAR_BYTES + BN * 4;
@@ -325,11 +344,382 @@ JZ_DEV void epilogue_chunk(const GemmParams& p, int m, int n, float (&v)[32], fl
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR>
+// k-th output tile of a persistent CTA (pair).  LNX kernels run the two 256-column tiles of one
+// 256-row block back to back (tile 2 mb + n in accumulator buffer n), so the epilogue owns whole
+// 512-wide rows; everything else strides single tiles (split-K slabs innermost).
+template <int LNX>
+JZ_DEV bool tile_at(const GemmParams& p, int first, int stride, int it, int& tile, int& split) {
+  if constexpr (LNX != 0) {
+    const int mb = first + (it >> 1) * stride;
+    if (mb >= p.m_tiles) return false;
+    tile = 2 * mb + (it & 1);
+    split = 0;
+    return true;
+  } else {
+    const int u = first + it * stride;
+    if (u >= p.m_tiles * p.n_tiles * p.splits) return false;
+    tile = u / p.splits;
+    split = u % p.splits;
+    return true;
+  }
+}
+
+// Row-statistics exchange between the two epilogue warps that share a TMEM lane quarter
+// (column halves 0 and 1 of every 256-column tile): warp c1 posts its partial, warp c0 adds its
+// own and posts the total, both use that one total (bitwise-identical statistics for the row).
+JZ_DEV float2 ln_row_total(float* red, uint32_t quarter, int chalf, int lane, float a, float b) {
+  float* slot = red + quarter * 64;
+  const int bar = 2 + (int)quarter;
+  if (chalf == 1) {
+    slot[lane] = a;
+    slot[32 + lane] = b;
+  }
+  asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+  if (chalf == 0) {
+    a += slot[lane];
+    b += slot[32 + lane];
+    slot[lane] = a;
+    slot[32 + lane] = b;
+  }
+  asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+  if (chalf == 1) {
+    a = slot[lane];
+    b = slot[32 + lane];
+  }
+  return make_float2(a, b);
+}
+
+// Column sums of a warp's 32 rows x 32 columns (lane = row) through its 4 KB staging tile
+// (128B-swizzled rows: conflict-free row writes and column reads); returns column `lane`.
+JZ_DEV float ln_colsum32(uint8_t* stg, const float (&v)[32], int lane) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+        make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  __syncwarp();
+  float s = 0.f;
+  const int c = lane >> 2, w = (lane & 3) * 4;
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) s += *reinterpret_cast<const float*>(stg + r * 128 + ((c ^ (r & 7)) << 4) + w);
+  __syncwarp();
+  return s;
+}
+
+JZ_DEV void tmem_ld32f(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Staging-tile helpers (32 rows x 32 columns per warp; lane = row).  fp32 tiles: 128-byte rows,
+// 128B swizzle (16-byte chunk c of row r at c ^ (r & 7)); bf16 tiles: 64-byte rows, 64B swizzle
+// (chunk c at c ^ ((r >> 1) & 3)).  Row accesses by the 32 lanes are bank-conflict free.
+JZ_DEV void stg_row_f32_ld(const uint8_t* t, int r, float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 w = *reinterpret_cast<const float4*>(t + r * 128 + ((c ^ (r & 7)) << 4));
+    v[4 * c] = w.x; v[4 * c + 1] = w.y; v[4 * c + 2] = w.z; v[4 * c + 3] = w.w;
+  }
+}
+JZ_DEV void stg_row_f32_st(uint8_t* t, int r, const float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(t + r * 128 + ((c ^ (r & 7)) << 4)) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+JZ_DEV void stg_row_bf16_st(uint8_t* t, int r, const float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    *reinterpret_cast<uint4*>(t + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) =
+        make_uint4(pack_bf16(v[8 * c], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                   pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+}
+
+// acc[0] += v, then rotate left by one: after 8 calls every slot got its chunk's value in order
+JZ_DEV void rot_add(float (&acc)[8], float v) {
+  const float a0 = acc[0] + v;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) acc[i] = acc[i + 1];
+  acc[7] = a0;
+}
+
+// LNX epilogue of one CTA (8 warps; warp = lane quarter x column half), persistent over 256-row
+// blocks.  Per block: accumulator buffer n holds columns [256 n, 256 n + 256) of the block's rows;
+// a warp walks its 8 chunks of 32 columns (k = 4 n + cc).  Every global tile moves by TMA through
+// the warp's 4 staging tiles T0..T3, the next chunk's input tiles prefetched while this one computes.
+//  LNX = 1 (LayerNorm forward, nn.py:35-40, two-pass): pass A x = acc + bias + resid (T0/T1) -> D and
+//          back into TMEM, row sums; pass B centred squares (TMEM only); pass C (x - mean) rstd gamma
+//          + beta -> bf16 (two 2 KB tiles after T1) -> ln_out16.
+//  LNX = 2 (LayerNorm backward): pass A x (T0/T1): row sums of dxn = dy gamma and dxn xhat, column
+//          partials of dy xhat and dy (T2 scratch); pass B x, D (T0,T1 / T2,T3): dx = rstd (dxn -
+//          mean(dxn) - xhat mean(dxn xhat)) added to D (in place in its tile) -> D, bf16 copy -> D2
+//          (in the x tile), column partials of the new D.
+template <int LNX, bool PAIR>
+JZ_DEV void ln_epilogue(const GemmParams& p, const EpiMaps& em, uint32_t tmem_base, uint64_t* tfull_bar,
+                        uint64_t* tempty_bar, uint64_t* bars, float* red, uint8_t* stg, int first_unit,
+                        int unit_stride, uint32_t rank, int warp, int lane) {
+  constexpr int TM = PAIR ? 2 * BM : BM;
+  constexpr int TB = 4096;
+  const uint32_t quarter = warp & 3;
+  const int chalf = (warp - 2) >> 2;
+  const int N = p.N;  // 512
+  const float invN = 1.0f / (float)N;
+  uint32_t acc_phase = 0;
+  uint32_t bpar = 0;  // phase bit per staging barrier (bit = slot)
+  float pdg[8], pdb[8], pdr[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) pdg[k] = pdb[k] = pdr[k] = 0.f;
+  auto release = [&](int n) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (PAIR) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&tempty_bar[n]), 0));
+      else mbar_arrive_relaxed(&tempty_bar[n]);
+    }
+  };
+  auto col_of = [&](int k) { return (k >> 2) * 256 + chalf * 128 + (k & 3) * 32; };
+  auto tile = [&](int t) { return stg + t * TB; };
+  // previous async (TMA) stores and generic reads of the tiles are done before they are refilled
+  auto drain = [&]() {
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+  };
+  for (int mb = first_unit; mb < p.m_tiles; mb += unit_stride, acc_phase ^= 1) {
+    const int row0 = mb * TM + (int)rank * BM + (int)quarter * 32;
+    const int row = row0 + lane;
+    const bool live = row < p.M;
+    const uint32_t tq = tmem_base + ((quarter * 32) << 16) + chalf * 128;
+    // loads one or two fp32 tiles of chunk k into T(2 slot), T(2 slot + 1) on bars[slot]
+    auto load = [&](int k, int slot, const CUtensorMap* m0, uint8_t* d0, const CUtensorMap* m1, uint8_t* d1) {
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bars[slot], m1 ? 2 * TB : TB);
+        tma_load_2d(d0, m0, &bars[slot], col_of(k), row0);
+        if (m1) tma_load_2d(d1, m1, &bars[slot], col_of(k), row0);
+      }
+    };
+    auto wait_tiles = [&](int slot) {
+      mbar_wait(&bars[slot], (bpar >> slot) & 1u);
+      bpar ^= 1u << slot;
+    };
+    auto store = [&](const CUtensorMap* m, const uint8_t* src, int k) {
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tma_store_2d(m, src, col_of(k), row0);
+    };
+    if constexpr (LNX == 1) {
+      float s = 0.f;
+      drain();
+      load(0, 0, &em.aux, tile(0), nullptr, nullptr);
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int n = k >> 2, col = col_of(k);
+        if ((k & 3) == 0) {
+          mbar_wait(&tfull_bar[n], acc_phase);
+          tc_fence_after();
+        }
+        if (k + 1 < 8) {
+          drain();  // chunk k - 1's store out of this slot has read it
+          load(k + 1, (k + 1) & 1, &em.aux, tile((k + 1) & 1), nullptr, nullptr);
+        }
+        float x[32], r[32];
+        tmem_ld32f(tq + n * 256 + (k & 3) * 32, x);
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 b = __ldg(b4 + j);
+          x[4 * j] += b.x; x[4 * j + 1] += b.y; x[4 * j + 2] += b.z; x[4 * j + 3] += b.w;
+        }
+        wait_tiles(k & 1);
+        uint8_t* t = tile(k & 1);
+        stg_row_f32_ld(t, lane, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] += r[j];
+        stg_row_f32_st(t, lane, x);
+        store(&em.d, t, k);
+        if (lane == 0) bulk_commit();
+        if (live) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) s += (x[j] + x[j + 1]) + (x[j + 2] + x[j + 3]);
+        }
+        uint32_t* xu = reinterpret_cast<uint32_t*>(x);
+        tmem_st_32x32b_x16(tq + n * 256 + (k & 3) * 32, *reinterpret_cast<const uint32_t(*)[16]>(xu));
+        tmem_st_32x32b_x16(tq + n * 256 + (k & 3) * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(xu + 16));
+      }
+      tmem_st_wait();
+      const float mu = ln_row_total(red, quarter, chalf, lane, s, 0.f).x * invN;
+      float q = 0.f;
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        float x[32];
+        tmem_ld32f(tq + (k >> 2) * 256 + (k & 3) * 32, x);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float a = x[j] - mu, b = x[j + 1] - mu;
+          q += a * a + b * b;
+        }
+      }
+      const float var = ln_row_total(red, quarter, chalf, lane, live ? q : 0.f, 0.f).x * invN;
+      const float rs = 1.0f / sqrtf(var + p.ln_eps);
+      const bool skip = p.ln_skip > 0;
+      const bool out_ok = live && (!skip || (row % p.ln_skip) != 0);
+      const int64_t orow = skip ? row - row / p.ln_skip - 1 : row;
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int n = k >> 2, col = col_of(k);
+        float x[32];
+        tmem_ld32f(tq + n * 256 + (k & 3) * 32, x);
+        if ((k & 3) == 3) release(n);  // buffer n fully read: the next block's MMAs may overwrite it
+        const float4* g4 = reinterpret_cast<const float4*>(p.ln_gamma + col);
+        const float4* be4 = reinterpret_cast<const float4*>(p.ln_beta + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 g = __ldg(g4 + j), b = __ldg(be4 + j);
+          x[4 * j] = (x[4 * j] - mu) * rs * g.x + b.x;
+          x[4 * j + 1] = (x[4 * j + 1] - mu) * rs * g.y + b.y;
+          x[4 * j + 2] = (x[4 * j + 2] - mu) * rs * g.z + b.z;
+          x[4 * j + 3] = (x[4 * j + 3] - mu) * rs * g.w + b.w;
+        }
+        if (skip) {  // compacted rows (final LayerNorm dropping s = 0): per-row stores
+          if (out_ok) {
+            __nv_bfloat16* o16 = p.ln_out16 + orow * (int64_t)N + col;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(o16 + 8 * j) =
+                  make_uint4(pack_bf16(x[8 * j], x[8 * j + 1]), pack_bf16(x[8 * j + 2], x[8 * j + 3]),
+                             pack_bf16(x[8 * j + 4], x[8 * j + 5]), pack_bf16(x[8 * j + 6], x[8 * j + 7]));
+          }
+        } else {
+          if (lane == 0) bulk_wait_read1();  // chunk k - 2's store out of this tile has read it
+          __syncwarp();
+          uint8_t* t = stg + 2 * TB + (k & 1) * (TB / 2);  // 64-byte-row bf16 tiles
+          stg_row_bf16_st(t, lane, x);
+          store(&em.d2, t, k);
+          if (lane == 0) bulk_commit();
+        }
+      }
+      if (live && chalf == 0) {
+        p.ln_mean[row] = mu;
+        p.ln_rstd[row] = rs;
+      }
+    } else {
+      const bool has16 = p.D2 != nullptr;
+      const float mu = live ? p.ln_mean[row] : 0.f, rs = live ? p.ln_rstd[row] : 0.f;
+      float s1 = 0.f, s2 = 0.f;
+      drain();
+      load(0, 0, &em.aux, tile(0), nullptr, nullptr);
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int n = k >> 2, col = col_of(k);
+        if ((k & 3) == 0) {
+          mbar_wait(&tfull_bar[n], acc_phase);
+          tc_fence_after();
+        }
+        if (k + 1 < 8) load(k + 1, (k + 1) & 1, &em.aux, tile((k + 1) & 1), nullptr, nullptr);
+        float g[32], x[32];
+        tmem_ld32f(tq + n * 256 + (k & 3) * 32, g);
+        wait_tiles(k & 1);
+        stg_row_f32_ld(tile(k & 1), lane, x);
+        if (!live) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) g[j] = x[j] = 0.f;
+        }
+        const float4* g4 = reinterpret_cast<const float4*>(p.ln_gamma + col);
+        float gx[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 gm = __ldg(g4 + j);
+          const float gmv[4] = {gm.x, gm.y, gm.z, gm.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 4 * j + e;
+            const float xh = (x[i] - mu) * rs;
+            const float dn = g[i] * gmv[e];
+            s1 += dn;
+            s2 += dn * xh;
+            gx[i] = g[i] * xh;
+          }
+        }
+        __syncwarp();  // every lane has read its x row before the tile is refilled (next-next chunk)
+        // k-th column partial: the accumulators rotate by one slot per chunk (register-resident; a
+        // runtime index would put them in local memory), back in place after the 8 chunks
+        rot_add(pdg, ln_colsum32(tile(2), gx, lane));
+        rot_add(pdb, ln_colsum32(tile(2), g, lane));
+      }
+      const float2 tot = ln_row_total(red, quarter, chalf, lane, s1, s2);
+      const float m1 = tot.x * invN, m2 = tot.y * invN;
+      drain();
+      load(0, 0, &em.aux, tile(0), &em.d, tile(1));
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const int n = k >> 2, col = col_of(k);
+        if (k + 1 < 8) {
+          drain();  // chunk k - 1's stores out of the other slot have read it
+          const int sl = (k + 1) & 1;
+          load(k + 1, sl, &em.aux, tile(2 * sl), &em.d, tile(2 * sl + 1));
+        }
+        float g[32], x[32], o[32];
+        tmem_ld32f(tq + n * 256 + (k & 3) * 32, g);
+        if ((k & 3) == 3) release(n);
+        const int sl = k & 1;
+        uint8_t* tx = tile(2 * sl);
+        uint8_t* td = tile(2 * sl + 1);
+        wait_tiles(sl);
+        stg_row_f32_ld(tx, lane, x);
+        if (p.ln_accumulate) stg_row_f32_ld(td, lane, o);
+        else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = 0.f;
+        }
+        const float4* g4 = reinterpret_cast<const float4*>(p.ln_gamma + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 gm = __ldg(g4 + j);
+          const float gmv[4] = {gm.x, gm.y, gm.z, gm.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 4 * j + e;
+            const float xh = (x[i] - mu) * rs;
+            const float dn = g[i] * gmv[e];
+            o[i] += rs * (dn - m1 - xh * m2);
+          }
+        }
+        stg_row_f32_st(td, lane, o);
+        store(&em.d, td, k);
+        if (!live) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = 0.f;
+        }
+        rot_add(pdr, ln_colsum32(tx, o, lane));  // x tile is free: column-sum scratch
+        if (has16) {
+          stg_row_bf16_st(tx, lane, o);
+          store(&em.d2, tx, k);
+        }
+        if (lane == 0) bulk_commit();
+      }
+    }
+  }
+  if (lane == 0) bulk_wait0();
+  if constexpr (LNX == 2) {
+    // one partial row per (CTA, lane quarter); this warp owns columns chalf*128 + 256 n + 32 cc + lane
+    const int64_t prow = (int64_t)blockIdx.x * 4 + quarter;
+    const int64_t plane = p.ln_nparts * N;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int col = col_of(k) + lane;
+      p.ln_part[prow * N + col] = pdg[k];
+      p.ln_part[plane + prow * N + col] = pdb[k];
+      p.ln_part[2 * plane + prow * N + col] = pdr[k];
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, bool PAIR, int LNX = 0>
 __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ EpiMaps em, GemmParams p, float* ws) {
-  using S = GemmShape<BN, PAIR>;
+  using S = GemmShape<BN, PAIR, LNX>;
   constexpr int TM = PAIR ? 2 * BM : BM;  // rows per (pair) tile
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -343,8 +733,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
   uint64_t* empty_bar = full_bar + S::STAGES;
   uint64_t* tfull_bar = empty_bar + S::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
+  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps] ([2 kEpiWarps] for LNX)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + (LNX ? 2 : 1) * kEpiWarps);
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + S::BAR_BYTES);  // [BN]
 
   const uint32_t warp = warp_id();
@@ -373,7 +763,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], (PAIR ? 2 : 1) * kEpiWarps);  // one arrival per epilogue warp of the pair
     }
-    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
+    for (int i = 0; i < (LNX ? 2 : 1) * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -393,8 +783,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
       uint32_t phase = 0;
       // pair: every load signals the leader's full barrier, which expects both CTAs' bytes
       const uint32_t full0 = PAIR ? mapa_shared(smem_u32(&full_bar[0]), 0) : 0;
-      for (int u = first_unit; u < units; u += unit_stride) {
-        const int tile = u / p.splits, split = u % p.splits;
+      int tile, split;
+      for (int it = 0; tile_at<LNX>(p, first_unit, unit_stride, it, tile, split); ++it) {
         const int m0 = (tile / p.n_tiles) * TM + (int)rank * BM;
         const int nb0 = (tile % p.n_tiles) * BN + (int)rank * S::B_ROWS;
         const int kb0 = split * p.kb_per_split;
@@ -437,8 +827,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int ti = 0;
-      for (int u = first_unit; u < units; u += unit_stride, ++ti) {
-        const int split = u % p.splits;
+      int tile_, split;
+      for (int it = 0; tile_at<LNX>(p, first_unit, unit_stride, it, tile_, split); ++it, ++ti) {
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
         GPROF(0);
@@ -483,6 +873,9 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if constexpr (LNX != 0) {
+    ln_epilogue<LNX, PAIR>(p, em, tmem_base, tfull_bar, tempty_bar, aux_bar + 2 * (warp - 2), sbias,
+                           stg_base + (warp - 2) * S::STG_BYTES, first_unit, unit_stride, rank, (int)warp, (int)lane);
   } else {
     // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
     const uint32_t quarter = warp & 3;
@@ -792,18 +1185,18 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR>
+template <int BN, bool A_MN, bool B_MN, bool PAIR, int LNX = 0>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmParams& p,
                        float* ws, cudaStream_t stream) {
-  using S = GemmShape<BN, PAIR>;
+  using S = GemmShape<BN, PAIR, LNX>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN, PAIR>,
+    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
   });
   JZ_CUDA_TRY(attr_err);
-  const int units = p.m_tiles * p.n_tiles * p.splits;
+  const int units = LNX ? p.m_tiles : p.m_tiles * p.n_tiles * p.splits;
   if constexpr (PAIR) {
     const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
@@ -818,11 +1211,11 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    JZ_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, A_MN, B_MN, PAIR>, ta, tb, em, p, ws));
+    JZ_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX>, ta, tb, em, p, ws));
     count_launch();
   } else {
     const int grid = units < num_sms() ? units : num_sms();
-    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR><<<grid, gemm_threads<PAIR>(), S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
+    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX><<<grid, gemm_threads<PAIR>(), S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
     JZ_LAUNCH_CHECK();
   }
   return JZ_OK;
@@ -998,6 +1391,107 @@ static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, in
     JZ_LAUNCH_CHECK();
   }
   return JZ_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// LayerNorm-fused GEMMs (N = 512: one CTA pair owns whole rows, see ln_epilogue)
+// ---------------------------------------------------------------------------------------------
+static int ln_gemm_setup(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor,
+                         int64_t M, int64_t N, int64_t K, CUtensorMap& ta, CUtensorMap& tb, GemmParams& p) {
+  JZ_CHECK_ARG(N == 512, "LN-fused gemm: N must be 512 (got %lld)", (long long)N);
+  JZ_CHECK_ARG(M > BM && M < (1ll << 31) && K > 0 && K < (1ll << 31), "LN-fused gemm: M=%lld K=%lld", (long long)M,
+               (long long)K);
+  JZ_CHECK_ARG(a_kmajor == 1, "LN-fused gemm: A must be K-major (activations)");
+  JZ_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0 && ((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0,
+               "LN-fused gemm: operand alignment");
+  JZ_CHECK_ARG(pair_mode_enabled(), "LN-fused gemm needs CTA pairs (JZ_GEMM_PAIR=0 set)");
+  int rc = make_tmap_2d_bf16(&ta, A, K, M, lda, 64, 128);
+  if (rc) return rc;
+  if (b_kmajor) rc = make_tmap_2d_bf16(&tb, B, K, N, ldb, 64, 128);
+  else rc = make_tmap_2d_bf16(&tb, B, N, K, ldb, 64, 64);
+  if (rc) return rc;
+  memset(&p, 0, sizeof(p));
+  p.M = (int)M; p.N = (int)N; p.K = (int)K;
+  p.m_tiles = (int)((M + 2 * BM - 1) / (2 * BM));
+  p.n_tiles = 2;
+  p.kb_total = (int)((K + BK - 1) / BK);
+  p.kb_per_split = p.kb_total;
+  p.splits = 1;
+  return JZ_OK;
+}
+
+extern "C" int jz_gemm_bf16_ln_fwd(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor,
+                                   float* D, int64_t ldd, int64_t M, int64_t N, int64_t K, const float* bias,
+                                   const float* resid, int64_t ld_resid, const float* gamma, const float* beta,
+                                   float eps, void* xn_bf16, float* mean, float* rstd, int64_t skip_period,
+                                   jz_stream_t s) {
+  CUtensorMap ta, tb;
+  GemmParams p;
+  int rc = ln_gemm_setup(A, lda, a_kmajor, B, ldb, b_kmajor, M, N, K, ta, tb, p);
+  if (rc) return rc;
+  auto a16 = [](const void* q) { return ((uintptr_t)q % 16) == 0; };
+  JZ_CHECK_ARG(D && resid && bias && gamma && beta && xn_bf16 && mean && rstd, "LN-fused gemm fwd: null pointer");
+  JZ_CHECK_ARG(a16(D) && a16(resid) && a16(bias) && a16(gamma) && a16(beta) && a16(xn_bf16) && ldd % 4 == 0 &&
+                   ld_resid % 4 == 0, "LN-fused gemm fwd: 16-byte alignment");
+  p.epi = JZ_EPI_RESID;
+  p.D = D; p.ldd = ldd;
+  p.bias = bias;
+  p.aux = resid; p.ldaux = ld_resid;
+  p.ln_gamma = gamma; p.ln_beta = beta; p.ln_eps = eps;
+  p.ln_out16 = reinterpret_cast<__nv_bfloat16*>(xn_bf16);
+  p.ln_mean = mean; p.ln_rstd = rstd;
+  p.ln_skip = skip_period;
+  EpiMaps em;
+  memset(&em, 0, sizeof(em));
+  rc = make_tmap_2d(&em.aux, resid, 4, N, M, ld_resid, 32, 32);
+  if (!rc) rc = make_tmap_2d(&em.d, D, 4, N, M, ldd, 32, 32);
+  if (!rc && skip_period <= 0) rc = make_tmap_2d_sw(&em.d2, xn_bf16, 2, N, M, N, 32, 32, 64);
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  return b_kmajor ? launch_gemm<256, false, false, true, 1>(ta, tb, em, p, nullptr, st)
+                  : launch_gemm<256, false, true, true, 1>(ta, tb, em, p, nullptr, st);
+}
+
+extern "C" int64_t jz_gemm_ln_bwd_parts(int64_t M) {
+  const int64_t mt = (M + 2 * BM - 1) / (2 * BM);
+  const int64_t pairs = mt < num_sms() / 2 ? mt : num_sms() / 2;
+  return 2 * pairs * 4;
+}
+
+extern "C" int jz_gemm_bf16_ln_bwd(const void* A, int64_t lda, int a_kmajor, const void* B, int64_t ldb, int b_kmajor,
+                                   int64_t M, int64_t N, int64_t K, const float* x, const float* mean,
+                                   const float* rstd, const float* gamma, float* dres, int accumulate,
+                                   void* dres_bf16, float* part, int64_t nparts, float* dgamma, float* dbeta,
+                                   float* dbias, jz_stream_t s) {
+  CUtensorMap ta, tb;
+  GemmParams p;
+  int rc = ln_gemm_setup(A, lda, a_kmajor, B, ldb, b_kmajor, M, N, K, ta, tb, p);
+  if (rc) return rc;
+  auto a16 = [](const void* q) { return ((uintptr_t)q % 16) == 0; };
+  JZ_CHECK_ARG(x && mean && rstd && gamma && dres && part, "LN-fused gemm bwd: null pointer");
+  JZ_CHECK_ARG(a16(x) && a16(gamma) && a16(dres) && (dres_bf16 == nullptr || a16(dres_bf16)),
+               "LN-fused gemm bwd: 16-byte alignment");
+  JZ_CHECK_ARG(nparts == jz_gemm_ln_bwd_parts(M), "LN-fused gemm bwd: nparts %lld != %lld", (long long)nparts,
+               (long long)jz_gemm_ln_bwd_parts(M));
+  p.epi = JZ_EPI_F32;
+  p.D = dres; p.ldd = N;
+  p.aux = x; p.ldaux = N;
+  p.D2 = dres_bf16; p.ldd2 = N;
+  p.ln_gamma = gamma; p.ln_mean = const_cast<float*>(mean); p.ln_rstd = const_cast<float*>(rstd);
+  p.ln_part = part; p.ln_nparts = nparts;
+  p.ln_accumulate = accumulate;
+  EpiMaps em;
+  memset(&em, 0, sizeof(em));
+  rc = make_tmap_2d(&em.aux, x, 4, N, M, N, 32, 32);
+  if (!rc) rc = make_tmap_2d(&em.d, dres, 4, N, M, N, 32, 32);
+  if (!rc && dres_bf16 != nullptr) rc = make_tmap_2d_sw(&em.d2, dres_bf16, 2, N, M, N, 32, 32, 64);
+  if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  rc = b_kmajor ? launch_gemm<256, false, false, true, 2>(ta, tb, em, p, nullptr, st)
+                : launch_gemm<256, false, true, true, 2>(ta, tb, em, p, nullptr, st);
+  if (rc) return rc;
+  return jz_reduce_partials3(part, part + nparts * N, part + 2 * nparts * N, (int)nparts, N, dgamma, dbeta, dbias,
+                             0, s);
 }
 
 #ifdef JZ_GEMM_PROF

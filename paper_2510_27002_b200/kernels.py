@@ -7,6 +7,7 @@ arithmetic happens in libjz's sm_100a kernels.  There is no fallback path.
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import torch
@@ -78,6 +79,9 @@ class KernelTimer:
 
 
 TIMER: KernelTimer | None = None
+# LayerNorm fused into the GEMM epilogues where the shapes allow (JZ_LN_FUSION=0 runs the standalone
+# LayerNorm kernels instead: A/B comparisons and the parity tests of both paths)
+LN_FUSION = os.environ.get("JZ_LN_FUSION", "1") != "0"
 
 
 def _fam_begin():
@@ -188,6 +192,72 @@ def linear_dx(dy_bf16: torch.Tensor, w_bf16: torch.Tensor, *, epilogue=L.EPI_F32
         out = torch.empty(M, K_in, dtype=dt, device=dy_bf16.device)
     return gemm(dy_bf16, w_bf16, M=M, N=K_in, K=N, a_kmajor=True, b_kmajor=True, out=out, epilogue=epilogue,
                 aux=aux, out2=out2, ldb=w_bf16.stride(0), colsum=colsum)
+
+
+def _timed_call(name: str, flops: int, *args) -> None:
+    timed = TIMER is not None and TIMER.active
+    if timed:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+    L.call(name, *args)
+    if timed:
+        e1.record()
+        TIMER.events.append((e0, e1))
+        TIMER.flops += flops
+        TIMER.launches += 1
+
+
+LN_FUSED_N = 512  # the LayerNorm-fused GEMM epilogues own 512-wide rows (two 256-column pair tiles)
+# Measured policy (tools/check_ln_fused.py, M = 148032): the fused forward wins where the GEMM itself
+# is short (K = 512 residual projections: 176 vs 209 us per launch) and loses at K = 2048 (373 vs
+# 330 us: the epilogue's staging tiles leave four operand stages and half of its work exposed);
+# the fused backward loses at K = 1536 / 2048 (481 / 548 vs 404 / 452 us), so it runs only when
+# JZ_LN_FUSION_BWD=1.
+LN_FUSED_FWD_MAX_K = 512
+LN_FUSION_BWD = os.environ.get("JZ_LN_FUSION_BWD", "0") == "1"
+
+
+def ln_fusable(M: int, N: int, K: int | None = None, backward: bool = False) -> bool:
+    if not (LN_FUSION and N == LN_FUSED_N and M > 128):
+        return False
+    if backward:
+        return LN_FUSION_BWD
+    return K is None or K <= LN_FUSED_FWD_MAX_K
+
+
+def linear_fwd_ln(x_bf16: torch.Tensor, w_bf16: torch.Tensor, bias: torch.Tensor, resid: torch.Tensor,
+                  gamma: torch.Tensor, beta: torch.Tensor, *, eps: float = 1e-5, skip_period: int = 0):
+    """Residual projection + the next LayerNorm in one GEMM (jz_gemm_bf16_ln_fwd, N = 512):
+    -> (x f32 = resid + x_bf16 @ W + b, LN(x) bf16 (rows compacted by skip_period), mean, rstd)."""
+    M, K = x_bf16.shape
+    N = w_bf16.shape[1]
+    dev = x_bf16.device
+    out = torch.empty(M, N, dtype=F32, device=dev)
+    out_rows = M - (M // skip_period if skip_period else 0)
+    xn = torch.empty(out_rows, N, dtype=BF16, device=dev)
+    mean = torch.empty(M, dtype=F32, device=dev)
+    rstd = torch.empty(M, dtype=F32, device=dev)
+    _timed_call("jz_gemm_bf16_ln_fwd", 2 * M * N * K, x_bf16.data_ptr(), x_bf16.stride(0), 1, w_bf16.data_ptr(),
+                w_bf16.stride(0), 0, out.data_ptr(), N, M, N, K, bias.data_ptr(), resid.data_ptr(), resid.stride(0),
+                gamma.data_ptr(), beta.data_ptr(), eps, xn.data_ptr(), mean.data_ptr(), rstd.data_ptr(), skip_period,
+                _s())
+    return out, xn, mean, rstd
+
+
+def linear_dx_ln(dy_bf16: torch.Tensor, w_bf16: torch.Tensor, *, x: torch.Tensor, mean: torch.Tensor,
+                 rstd: torch.Tensor, gamma: torch.Tensor, dres: torch.Tensor, accumulate: bool = True,
+                 dres_bf16: torch.Tensor | None = None, dgamma=None, dbeta=None, dbias=None) -> None:
+    """Input gradient of a LayerNorm-fed layer + the LayerNorm backward in one GEMM
+    (jz_gemm_bf16_ln_bwd): dres (+)= LN_bwd(dy_bf16 @ W^T); dgamma / dbeta / dbias (colsum of dres)."""
+    M, Nout = dy_bf16.shape
+    K_in = w_bf16.shape[0]
+    nparts = L.load().jz_gemm_ln_bwd_parts(M)
+    part = scratch("ln_gemm_part", 3 * nparts * K_in)
+    _timed_call("jz_gemm_bf16_ln_bwd", 2 * M * K_in * Nout, dy_bf16.data_ptr(), dy_bf16.stride(0), 1,
+                w_bf16.data_ptr(), w_bf16.stride(0), 1, M, K_in, Nout, x.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                gamma.data_ptr(), dres.data_ptr(), int(accumulate), _p(dres_bf16), part.data_ptr(), nparts,
+                _p(dgamma), _p(dbeta), _p(dbias), _s())
 
 
 def linear_dw(x_bf16: torch.Tensor, dy_bf16: torch.Tensor, out_f32: torch.Tensor, *, accumulate=False,

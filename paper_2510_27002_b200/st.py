@@ -157,35 +157,69 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
     H = cfg.heads
     frames = B * T
     sh = _shadows(P, cfg, prefix)
+    rows = x.shape[0]
+    # LayerNorm fused into the residual projections' epilogues (jz_gemm_bf16_ln_fwd): a residual
+    # GEMM also emits the NEXT sub-layer's LayerNorm output.  kernels.ln_fusable holds the measured
+    # policy (the attention output projections fuse; the K = 2048 FFN down-projection does not)
+    fuse = K.ln_fusable(rows, cfg.model_dim, K=cfg.model_dim)           # after the attention projections
+    fuse_ffn = K.ln_fusable(rows, cfg.model_dim, K=cfg.ffn_dim)         # after the FFN down-projection
+    fuse_final = fuse_ffn and not final_f32
     blocks_ctx = []
+    nxt = None  # (xn, mean, rstd) of this block's spatial LayerNorm, from the previous block's epilogue
+    y = mf = rf = None
     for i in range(cfg.blocks):
         base = f"{prefix}.block{i}"
         w = sh[i]
         c = {"x_in": x}
         # spatial sub-layer (st.py:73)
-        xn, m1, r1 = K.layernorm_fwd(x, P[f"{base}.spatial.ln.g"].data, P[f"{base}.spatial.ln.b"].data)
+        if nxt is None:
+            xn, m1, r1 = K.layernorm_fwd(x, P[f"{base}.spatial.ln.g"].data, P[f"{base}.spatial.ln.b"].data)
+        else:
+            xn, m1, r1 = nxt
         qkv = K.linear_fwd(xn, w["spatial.wqkv"], w["spatial.bqkv"])
         ao, ao32, lse_s = K.attn_spatial_fwd(qkv, frames, S, H, keep_f32=save)
-        x1 = K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=L.EPI_RESID, aux=x)
+        if fuse:
+            x1, xn2, m2, r2 = K.linear_fwd_ln(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, x,
+                                               P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
+        else:
+            x1 = K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=L.EPI_RESID, aux=x)
+            xn2, m2, r2 = K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
         # temporal sub-layer (st.py:74-76)
-        xn2, m2, r2 = K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
         qkv2 = K.linear_fwd(xn2, w["temporal.wqkv"], w["temporal.bqkv"])
         ao2, lse_t = K.attn_temporal_fwd(qkv2, B, T, S, H)
-        x2 = K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=L.EPI_RESID, aux=x1)
+        if fuse:
+            x2, xn3, m3, r3 = K.linear_fwd_ln(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, x1,
+                                               P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
+        else:
+            x2 = K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=L.EPI_RESID, aux=x1)
+            xn3, m3, r3 = K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
         # FFN (st.py:77-79)
-        xn3, m3, r3 = K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
         # training saves gelu'(pre-activation) (f16) from the same tanh, so the backward epilogue
         # only multiplies; inference skips it
         hpre = torch.empty(xn3.shape[0], cfg.ffn_dim, dtype=torch.float16, device=x.device) if save else None
         h = K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data,
                          epilogue=L.EPI_GELU_DG if save else L.EPI_GELU, out2=hpre)
-        x3 = K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=L.EPI_RESID, aux=x2)
+        last = i == cfg.blocks - 1
+        nxt = None
+        if fuse_ffn and (not last or fuse_final):
+            lnp = f"{prefix}.block{i + 1}.spatial.ln" if not last else f"{prefix}.final_ln"
+            g_ln, b_ln = P[f"{lnp}.g"].data, P[f"{lnp}.b"].data
+            x3, xn_n, m_n, r_n = K.linear_fwd_ln(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, x2, g_ln, b_ln,
+                                                 skip_period=S if (last and final_skip) else 0)
+            if last:
+                y, mf, rf = xn_n, m_n, r_n
+            else:
+                nxt = (xn_n, m_n, r_n)
+        else:
+            x3 = K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=L.EPI_RESID, aux=x2)
         if save:
             c.update(xn=xn, m1=m1, r1=r1, qkv=qkv, ao=ao, ao32=ao32, lse_s=lse_s, x1=x1, xn2=xn2, m2=m2, r2=r2, qkv2=qkv2,
                      ao2=ao2, lse_t=lse_t, x2=x2, xn3=xn3, m3=m3, r3=r3, h=h, hpre=hpre)
             blocks_ctx.append(c)
         x = x3
-    if final_f32:
+    if y is not None:  # the final LayerNorm came out of the last FFN-down GEMM's epilogue
+        assert not final_f32
+    elif final_f32:
         y16, y32, mf, rf = K.layernorm_fwd(x, P[f"{prefix}.final_ln.g"].data, P[f"{prefix}.final_ln.b"].data,
                                            skip_period=S if final_skip else 0, out_f32=True, out_bf16=final_bf16)
         y = (y16, y32)
@@ -226,7 +260,8 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
     if on_done is not None:
         on_done("head_ln")
     # LN-backward inputs in bf16: the dX GEMMs write half the bytes and the HBM-bound LN pass reads half
-    dtmp = torch.empty(rows, d, dtype=K.BF16, device=dev)
+    fuse = K.ln_fusable(rows, d, backward=True)  # LayerNorm backward inside the dX GEMMs' epilogues
+    dtmp = None if fuse else torch.empty(rows, d, dtype=K.BF16, device=dev)
     dh = torch.empty(rows, cfg.ffn_dim, dtype=K.BF16, device=dev)
     dao = torch.empty(rows, d, dtype=K.BF16, device=dev)
     for i in reversed(range(nb)):
@@ -238,20 +273,17 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.linear_dx(dres_b, w["ffn.wdown"], epilogue=L.EPI_MUL_F16, out=dh, aux=c["hpre"],
                     colsum=G[f"{base}.ffn.up.b"])  # up-bias gradient from the epilogue's column sums
         K.linear_dw(c["xn3"], dh, G[f"{base}.ffn.up.w"])
-        K.linear_dx(dh, w["ffn.wup"], epilogue=L.EPI_BF16, out=dtmp)
-        K.layernorm_bwd(c["x2"], c["m3"], c["r3"], P[f"{base}.ffn.ln.g"].data, dtmp, dres, accumulate=True,
-                        dres_bf16=dres_b, dgamma=G[f"{base}.ffn.ln.g"], dbeta=G[f"{base}.ffn.ln.b"],
-                        dbias=G[f"{base}.temporal.o.b"])
+        _dx_layernorm(dh, w["ffn.wup"], c["x2"], c["m3"], c["r3"], P[f"{base}.ffn.ln.g"].data, dres, dtmp,
+                      dres_b, G[f"{base}.ffn.ln.g"], G[f"{base}.ffn.ln.b"], G[f"{base}.temporal.o.b"], fuse)
         # ---- temporal: x2 = x1 + attn_t(LN(x1)) Wo + bo
         K.linear_dw(c["ao2"], dres_b, G[f"{base}.temporal.o.w"])
         K.linear_dx(dres_b, w["temporal.wo"], epilogue=L.EPI_BF16, out=dao)
         gbt = gst.block_of(gst.grad_flat, f"{base}.temporal.q.b") if gst is not None else None
         dqkv = K.attn_temporal_bwd(c["qkv2"], c["ao2"], dao, c["lse_t"], B, T, S, H, colsum=gbt)
         _qkv_param_grads(dqkv, c["xn2"], G, f"{base}.temporal", d, gst, bias_done=gbt is not None)
-        K.linear_dx(dqkv, w["temporal.wqkv"], epilogue=L.EPI_BF16, out=dtmp)
-        K.layernorm_bwd(c["x1"], c["m2"], c["r2"], P[f"{base}.temporal.ln.g"].data, dtmp, dres, accumulate=True,
-                        dres_bf16=dres_b, dgamma=G[f"{base}.temporal.ln.g"], dbeta=G[f"{base}.temporal.ln.b"],
-                        dbias=G[f"{base}.spatial.o.b"])
+        _dx_layernorm(dqkv, w["temporal.wqkv"], c["x1"], c["m2"], c["r2"], P[f"{base}.temporal.ln.g"].data, dres,
+                      dtmp, dres_b, G[f"{base}.temporal.ln.g"], G[f"{base}.temporal.ln.b"], G[f"{base}.spatial.o.b"],
+                      fuse)
         # ---- spatial: x1 = x + attn_s(LN(x)) Wo + bo
         K.linear_dw(c["ao"], dres_b, G[f"{base}.spatial.o.w"])
         gbs = gst.block_of(gst.grad_flat, f"{base}.spatial.q.b") if gst is not None else None
@@ -266,16 +298,27 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
             gbs[d:2 * d].zero_()
             K.colsum_bf16(dqkv, gbs[:d], cols=d)
         _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst, bias_done=gbs is not None)
-        K.linear_dx(dqkv, w["spatial.wqkv"], epilogue=L.EPI_BF16, out=dtmp)
         prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
-        K.layernorm_bwd(c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dtmp, dres, accumulate=True,
-                        dres_bf16=dres_b if (i > 0 or want_dx_bf16) else None, dgamma=G[f"{base}.spatial.ln.g"],
-                        dbeta=G[f"{base}.spatial.ln.b"], dbias=prev_bias)
+        _dx_layernorm(dqkv, w["spatial.wqkv"], c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dres,
+                      dtmp, dres_b if (i > 0 or want_dx_bf16) else None, G[f"{base}.spatial.ln.g"],
+                      G[f"{base}.spatial.ln.b"], prev_bias, fuse)
         if on_done is not None:
             on_done(f"block{i}")
     if want_dx_bf16:
         return dres, dres_b
     return dres
+
+
+def _dx_layernorm(dy, w, x, mean, rstd, gamma, dres, dtmp, dres_b, dgamma, dbeta, dbias, fuse: bool) -> None:
+    """dres += LN_bwd(dy @ W^T) (nn.py:35-40 backward through the layer W feeds): one LN-fused GEMM,
+    or the dX GEMM then the standalone LayerNorm backward."""
+    if fuse:
+        K.linear_dx_ln(dy, w, x=x, mean=mean, rstd=rstd, gamma=gamma, dres=dres, accumulate=True, dres_bf16=dres_b,
+                       dgamma=dgamma, dbeta=dbeta, dbias=dbias)
+        return
+    K.linear_dx(dy, w, epilogue=L.EPI_BF16, out=dtmp)
+    K.layernorm_bwd(x, mean, rstd, gamma, dtmp, dres, accumulate=True, dres_bf16=dres_b, dgamma=dgamma, dbeta=dbeta,
+                    dbias=dbias)
 
 
 def _qkv_param_grads(dqkv: torch.Tensor, xn: torch.Tensor, G: dict, base: str, d: int, st=None,

@@ -161,3 +161,30 @@ def test_token_id_out_of_range_raises(jasmine_case):
         c["model"].loss(bad, Tensor(c["lat"]), None, mask=c["mask"])
     with pytest.raises(ValueError):
         c["model"].loss(c["tokens"], Tensor(c["lat"][:, :-1]), None, mask=c["mask"])
+
+
+@pytest.mark.parametrize("fused_bwd", [True, False])
+def test_grads_with_and_without_layernorm_fusion(jasmine_case, fused_bwd):
+    """The LayerNorm-fused GEMM epilogues (forward: attention output projections; backward: every
+    LayerNorm-fed dX GEMM when enabled) keep every gradient within the stated tolerance; the
+    standalone-kernel path (JZ_LN_FUSION=0) too."""
+    from paper_2510_27002_b200 import kernels as Kn
+    from paper_2510_27002_b200.tensor import Tensor
+    c = jasmine_case
+    saved = (Kn.LN_FUSION, Kn.LN_FUSION_BWD)
+    Kn.LN_FUSION, Kn.LN_FUSION_BWD = fused_bwd, fused_bwd
+    try:
+        loss, _ = c["model"].loss(c["tokens"], Tensor(c["lat"]), None, mask=c["mask"])
+        assert abs(float(loss.data) - c["loss_ref"]) < TOL["bf16_loss_abs"]
+        loss.backward()
+        bad = []
+        for k, p in c["model"].params.items():
+            if k.endswith(".k.b"):
+                continue
+            ref = c["P"][k].grad.numpy()
+            got = p.grad.cpu().numpy()
+            if _cos(got, ref) < TOL["bf16_grad_cosine_min"] or _rel(got, ref) > TOL["bf16_grad_rel_l2"]:
+                bad.append((k, _cos(got, ref), _rel(got, ref)))
+        assert not bad, bad
+    finally:
+        Kn.LN_FUSION, Kn.LN_FUSION_BWD = saved

@@ -413,3 +413,61 @@ def test_linear_f32_bwd_parallel_vs_reference_kernel(K, N, accumulate):
     ref = x.double().t() @ dy.double()
     base = torch.randn(K, N, device=dev, generator=torch.Generator(device=dev).manual_seed(2)).double()
     assert rel(dW1.double(), ref + (base if accumulate else 0)) < 1e-5
+
+
+@pytest.mark.parametrize("M", [148032, 1000, 300])
+def test_ln_fused_gemm_forward_matches_gemm_then_layernorm(M):
+    """jz_gemm_bf16_ln_fwd (residual projection + next LayerNorm in the epilogue) against the
+    separate RESID GEMM + LayerNorm kernels on the same bf16 operands (nn.py:35-40)."""
+    from paper_2510_27002_b200 import _lib as L
+    from paper_2510_27002_b200 import kernels as K
+    g = torch.Generator(device="cuda").manual_seed(M)
+    a = (torch.randn(M, 512, device="cuda", generator=g) * 0.5).bfloat16()
+    w = (torch.randn(512, 512, device="cuda", generator=g) * 0.05).bfloat16()
+    b = torch.randn(512, device="cuda", generator=g) * 0.1
+    res = torch.randn(M, 512, device="cuda", generator=g)
+    gm = 1 + 0.1 * torch.randn(512, device="cuda", generator=g)
+    be = 0.1 * torch.randn(512, device="cuda", generator=g)
+    x1, xn, mu, rs = K.linear_fwd_ln(a, w, b, res, gm, be)
+    ref_x = K.linear_fwd(a, w, b, epilogue=L.EPI_RESID, aux=res)
+    ref_xn, ref_mu, ref_rs = K.layernorm_fwd(ref_x, gm, be)
+    assert torch.equal(x1, ref_x)
+    assert float((mu - ref_mu).abs().max()) < 1e-6
+    assert float(((rs - ref_rs) / ref_rs).abs().max()) < 1e-5
+    assert float((xn.float() - ref_xn.float()).abs().max()) <= 2 ** -6 * float(ref_xn.float().abs().max())
+    if M % 257 == 0:  # compacted output (final LayerNorm dropping the action-token rows)
+        _, xs, _, _ = K.linear_fwd_ln(a, w, b, res, gm, be, skip_period=257)
+        ref_s, _, _ = K.layernorm_fwd(ref_x, gm, be, skip_period=257)
+        assert xs.shape == ref_s.shape
+        assert float((xs.float() - ref_s.float()).abs().max()) <= 2 ** -6 * float(ref_s.float().abs().max())
+
+
+@pytest.mark.parametrize("M,Kd", [(148032, 1536), (1000, 2048), (300, 512)])
+def test_ln_fused_gemm_backward_matches_fp32_reference(M, Kd):
+    """jz_gemm_bf16_ln_bwd (dX GEMM + LayerNorm backward in the epilogue) against a torch fp32
+    LayerNorm backward of the same GEMM output (autodiff of nn.py:35-40)."""
+    from paper_2510_27002_b200 import kernels as K
+    g = torch.Generator(device="cuda").manual_seed(M + Kd)
+    dy = (torch.randn(M, Kd, device="cuda", generator=g) * 0.1).bfloat16()
+    w = (torch.randn(512, Kd, device="cuda", generator=g) * 0.05).bfloat16()
+    x = torch.randn(M, 512, device="cuda", generator=g) * 2 + 0.3
+    gm = 1 + 0.1 * torch.randn(512, device="cuda", generator=g)
+    mean = x.mean(1)
+    rstd = 1 / torch.sqrt(x.var(1, unbiased=False) + 1e-5)
+    dres0 = torch.randn(M, 512, device="cuda", generator=g)
+    dres = dres0.clone()
+    dres_b = torch.empty(M, 512, device="cuda", dtype=torch.bfloat16)
+    dgam, dbet, dbias = (torch.empty(512, device="cuda") for _ in range(3))
+    K.linear_dx_ln(dy, w, x=x, mean=mean, rstd=rstd, gamma=gm, dres=dres, dres_bf16=dres_b, dgamma=dgam, dbeta=dbet,
+                   dbias=dbias)
+    gout = dy.float() @ w.float().t()  # gradient of the LayerNorm output
+    xr = x.clone().requires_grad_(True)
+    gr = gm.clone().requires_grad_(True)
+    br = torch.zeros(512, device="cuda", requires_grad=True)
+    torch.nn.functional.layer_norm(xr, (512,), gr, br, eps=1e-5).backward(gout)
+    ref = dres0 + xr.grad
+    rel = lambda p, q: float((p - q).norm() / q.norm())
+    assert rel(dres - dres0, xr.grad) < TOL["fp32_kernel_rel_l2"] * 100  # fp32 accumulation-order level
+    assert torch.equal(dres_b, dres.bfloat16())
+    assert rel(dgam, gr.grad) < 1e-4 and rel(dbet, br.grad) < 1e-4
+    assert rel(dbias, ref.sum(0)) < 1e-4
