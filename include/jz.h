@@ -272,6 +272,9 @@ JZ_API int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, int H,
                                 float* lse, jz_stream_t stream);
 /* colsum_part (nullable): fp32 [jz_attn_temporal_colsum_parts(B, S)][3*H*64], as the spatial one. */
 JZ_API int64_t jz_attn_temporal_colsum_parts(int64_t B, int S);
+/* partial rows the backward writes for these dims (use this one; the two-argument form is the
+ * register-tile kernels' count): T <= 16 runs the tcgen05 kernels, one partial row per CTA. */
+JZ_API int64_t jz_attn_temporal_colsum_parts_t(int64_t B, int S, int T, int H);
 /* out: the forward output; not read (Delta_t = sum_j P_tj dP_tj is formed from the kernel's fp32
  * P and dP registers, which removes the O read and the dP - Delta cancellation against a bf16 O);
  * kept for interface stability, may be NULL. */

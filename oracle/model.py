@@ -389,6 +389,36 @@ def lam_forward(P, cfg: LamCfg, unit):  # lam.py:120-129
     return recon, idx, {"recon": rec, "codebook": cb, "commitment": commit, "total": total}
 
 
+def lam_forward_with_indices(P, cfg: LamCfg, unit, idx):
+    """lam.py:120-129 with the code indices given (the VQ argmin replaced by `idx`; the losses and
+    the straight-through estimator exactly as vq_quantize forms them, tokenizer.py:58-79)."""
+    z_e = lam_encode_pre_vq(P, cfg, unit)
+    z_q = P["codebook"][torch.as_tensor(np.asarray(idx))]
+    cb, commit = mse(z_q, z_e.detach()), mse(z_e, z_q.detach())
+    z_q_st = z_e + (z_q.detach() - z_e.detach())
+    recon = lam_decode(P, cfg, unit[:, :-1], z_q_st)
+    rec = mse(recon, unit.detach()[:, 1:])
+    total = rec + cb + cfg.commitment_beta * commit
+    return recon, z_e, {"recon": rec, "codebook": cb, "commitment": commit, "total": total}
+
+
+def vq_mismatch_explained(z_dev, z_ref, codebook, idx_dev, idx_ref) -> int:
+    """Number of code mismatches NOT explained by the latent difference: with z' = z + e,
+    |z'-c|^2 - |z-c|^2 = 2 e.(z - c) + |e|^2, so a flip from c_r to c_o needs
+    |z-c_o|^2 - |z-c_r|^2 <= 2 |e| (|z-c_o| + |z-c_r|) + 2 |e|^2."""
+    zd = np.asarray(z_dev, dtype=np.float64).reshape(-1, np.shape(codebook)[-1])
+    zr = np.asarray(z_ref, dtype=np.float64).reshape(zd.shape)
+    cb = np.asarray(codebook, dtype=np.float64)
+    io, ir = np.asarray(idx_dev).reshape(-1), np.asarray(idx_ref).reshape(-1)
+    bad = 0
+    for r in np.nonzero(io != ir)[0]:
+        e = np.linalg.norm(zd[r] - zr[r])
+        do, dr = np.linalg.norm(zr[r] - cb[io[r]]), np.linalg.norm(zr[r] - cb[ir[r]])
+        if do ** 2 - dr ** 2 > 2 * e * (do + dr) + 2 * e ** 2:
+            bad += 1
+    return bad
+
+
 def init_dynamics(cfg: DynCfg, seed=0, dtype=np.float32) -> dict:  # dynamics.py:66-87
     g = orng.stream(seed, "dynamics-init")
     d = cfg.model_dim

@@ -61,6 +61,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_attn_spatial_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],
     "jz_attn_spatial_colsum_parts": [_I64],
     "jz_attn_temporal_colsum_parts": [_I64, _I32],
+    "jz_attn_temporal_colsum_parts_t": [_I64, _I32, _I32, _I32],
     "jz_attn_spatial_bwd_workspace_bytes": [_I64, _I32, _I32],
     "jz_attn_temporal_fwd": [_P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
     "jz_attn_temporal_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _P, _P, _P],
@@ -87,7 +88,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_maskgit_step": [_P, _I64, _I32, _I32, _F32, _P, _P, _P, _I32, _U64, _I32, _P, _P, _P, _P, _P],
 }
 _RESTYPE = {"jz_gemm_workspace_bytes": _I64, "jz_gemm_ln_bwd_parts": _I64, "jz_linear_f32_bwd_workspace": _I64, "jz_gemm_colsum_parts": _I64, "jz_attn_spatial_colsum_parts": _I64,
-            "jz_attn_temporal_colsum_parts": _I64, "jz_attn_spatial_bwd_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_assemble_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
+            "jz_attn_temporal_colsum_parts": _I64, "jz_attn_temporal_colsum_parts_t": _I64, "jz_attn_spatial_bwd_workspace_bytes": _I64, "jz_dyn_embed_bwd_workspace": _I64, "jz_assemble_bwd_workspace": _I64, "jz_last_error": C.c_char_p,
             "jz_build_info": C.c_char_p}
 
 

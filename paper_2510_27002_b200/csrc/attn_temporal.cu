@@ -14,6 +14,8 @@
 //
 // qkv bf16 [M, 3D] (cols [q | k | v], head h = cols 64h..64h+63 of each),
 // out bf16 [M, D], lse f32 [((b*S + s) * H + h) * T + t] (natural log).
+#include <stdlib.h>
+
 #include "common.h"
 #include "ptx.cuh"
 
@@ -671,11 +673,29 @@ static int dispatch_rowtile(bool bwd, const void* qkv, const void* o, const void
   return launch_rowtile<2>(bwd, qkv, o, dout, lse, B, T, S, H, causal, out, st, colsum);
 }
 
+int temporal_tc_fwd(const void* qkv, int64_t B, int T, int S, int H, void* out, float* lse, cudaStream_t st);
+int temporal_tc_bwd(const void* qkv, const void* dout, const float* lse, int64_t B, int T, int S, int H, void* dqkv,
+                    float* colsum, cudaStream_t st);
+int64_t temporal_tc_colsum_parts(int64_t B, int S, int H);
+
+// T <= 16 runs the tcgen05 kernels (attn_temporal_tc.cu) unless JZ_TEMPORAL_TC=0 selects the
+// register-tile (mma.sync) kernels below; 16 < T <= 32 runs the row-tile kernels.
+static bool temporal_tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("JZ_TEMPORAL_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int dispatch_temporal(bool bwd, const void* qkv, const void* o, const void* dout, float* lse, int64_t B,
                              int T, int S, int H, void* out, cudaStream_t st, float* colsum = nullptr) {
   JZ_CHECK_ARG(H >= 1 && H <= 16, "temporal attention: heads %d unsupported (<= 16)", H);
   JZ_CHECK_ARG(T >= 1 && T <= 32, "temporal attention: T=%d unsupported (<= 32)", T);
   if (T > 16) return dispatch_rowtile(bwd, qkv, o, dout, lse, B, T, S, H, 1, out, st, colsum);
+  if (temporal_tc_enabled() && B * S > 0)
+    return bwd ? temporal_tc_bwd(qkv, dout, lse, B, T, S, H, out, colsum, st)
+               : temporal_tc_fwd(qkv, B, T, S, H, out, lse, st);
   const float scale = 0.125f;  // 1/sqrt(64)
   const int64_t BS = B * S;
   if (BS == 0) return JZ_OK;
@@ -709,6 +729,11 @@ extern "C" int jz_attn_temporal_fwd(const void* qkv, int64_t B, int T, int S, in
 }
 
 extern "C" int64_t jz_attn_temporal_colsum_parts(int64_t B, int S) { return B * S; }
+
+extern "C" int64_t jz_attn_temporal_colsum_parts_t(int64_t B, int S, int T, int H) {
+  if (T <= 16 && temporal_tc_enabled()) return temporal_tc_colsum_parts(B, S, H);  // one partial row per CTA
+  return B * S;
+}
 
 extern "C" int jz_attn_temporal_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                                     int64_t B, int T, int S, int H, int head_dim, void* dqkv, float* colsum_part,

@@ -52,6 +52,10 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t in
 int make_tmap_2d_sw(CUtensorMap* map, const void* base, int elem_bytes, uint64_t inner, uint64_t outer,
                     uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 
+// 4-D bf16 tensor map, 128-byte swizzle; strides of dims 1..3 in bytes
+int make_tmap_4d_bf16(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
+                      const uint32_t box[4]);
+
 int num_sms();
 
 }  // namespace jz

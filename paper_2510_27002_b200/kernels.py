@@ -423,7 +423,7 @@ def attn_temporal_bwd(qkv, out, dout, lse, B: int, T: int, S: int, H: int, dqkv=
         dqkv = torch.empty_like(qkv)
     part, nparts = None, 0
     if colsum is not None:
-        nparts = L.load().jz_attn_temporal_colsum_parts(B, S)
+        nparts = L.load().jz_attn_temporal_colsum_parts_t(B, S, T, H)
         part = scratch("attn_colsum", nparts * 3 * H * 64)
     e0 = _fam_begin()
     L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), B, T, S, H, 64,

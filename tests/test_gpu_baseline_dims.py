@@ -199,6 +199,21 @@ def test_c1_tokenizer_forward_vs_oracle(c1):
              for k in ("recon", "codebook", "commitment", "total")}
     _report("c1", z_e_rel=rz, index_agreement=agree, recon_rel=rr, **{f"loss_rel_{k}": v for k, v in diffs.items()})
     assert rz < TOL["bf16_logits_rel_l2"]
+    # every code that differs from the oracle's must be explained by the bf16 encoder's latent
+    # error: with z' = z + e, |z'-c|^2 - |z-c|^2 = 2 e.(z - c) + |e|^2, so a flip from the oracle's
+    # code c_r to c_o needs gap = |z-c_o|^2 - |z-c_r|^2 <= 2 |e| (|z-c_o| + |z-c_r|) + 2 |e|^2
+    zo = z.reshape(-1, 32).astype(np.float64)
+    zr = c1["z_e"].reshape(-1, 32).astype(np.float64)
+    cbk = c1["P"]["codebook"].numpy().astype(np.float64)
+    io, ir = np.asarray(idx).reshape(-1), c1["idx"].reshape(-1)
+    unexplained = 0
+    for rrow in np.nonzero(io != ir)[0]:
+        e = np.linalg.norm(zo[rrow] - zr[rrow])
+        do, dr = np.linalg.norm(zr[rrow] - cbk[io[rrow]]), np.linalg.norm(zr[rrow] - cbk[ir[rrow]])
+        if do ** 2 - dr ** 2 > 2 * e * (do + dr) + 2 * e ** 2:
+            unexplained += 1
+    _report("c1", mismatches=int((io != ir).sum()), unexplained_mismatches=unexplained)
+    assert unexplained == 0
     assert agree >= TOL["vq_index_agreement_bf16_encoder"]
     assert rr < TOL["bf16_logits_rel_l2"]
     for k, v in diffs.items():
@@ -235,10 +250,19 @@ def test_c2_lam_forward_backward_vs_oracle():
 # C5: decode_frame at jasmine-base dims
 # ------------------------------------------------------------------------------------------------
 def test_c5_decode_frame_jasmine_dims_vs_oracle():
-    """One MaskGIT frame (25 steps, t = 4 context frames) at the C5 model dims.  to_logits is
-    scaled so the picks are decided by clear margins; the draws consumed must match exactly."""
+    """One MaskGIT frame (25 steps, t = 4 context frames) at the C5 model dims, to_logits scaled so
+    the picks are decided by clear margins.
+
+    Per step (teacher-forced on the oracle's trajectory): the device logits of the same clip state
+    pick the same token as the oracle's under the same uniform draws.  Whole chain: the device
+    decode_frame (KV cache + device sampler) consumes exactly the oracle's draws, and its tokens
+    agree with the oracle's; one early near-tie pick changes the context of every later step, so
+    the chain agreement floor is lower than the per-step one."""
+    import copy
+
     from paper_2510_27002_b200 import rng as R
     from paper_2510_27002_b200.dynamics import DynamicsConfig, DynamicsModel
+    from paper_2510_27002_b200.tensor import Tensor
     kw = dict(JB, blocks=6, token_codes=1024, action_latent_dim=32, patches_per_frame=256, max_frames=16)
     m = DynamicsModel(DynamicsConfig(**kw), seed=0)
     m.params["to_logits.w"].data.mul_(60.0)
@@ -247,19 +271,32 @@ def test_c5_decode_frame_jasmine_dims_vs_oracle():
     P["to_logits.w"].mul_(60.0)
     prev = OR.stream(5, "c5-prev").integers(0, 1024, size=(1, 4, 256))
     lat = (OR.stream(5, "c5-lat").normal(size=(1, 4, 32)) * 0.1).astype(np.float32)
-    g = R.stream(5, "c5-rng")
-    got = m.decode_frame(prev, lat, steps=25, rng=g)
+    og = OR.stream(5, "c5-rng")
+    step_hits = [0, 0]
 
     def logits_fn(tk, la, mask):
         with torch.no_grad():
-            return OM.dyn_logits(P, ocfg, tk, torch.tensor(la), mask).numpy()
+            ref = OM.dyn_logits(P, ocfg, tk, torch.tensor(la), mask).numpy()
+        dev = m.logits(tk, Tensor(la), mask=mask).numpy()
+        s_ref, _ = OM.sample_with_confidence(ref[:, -1], 1.0, copy.deepcopy(og))
+        s_dev, _ = OM.sample_with_confidence(dev[:, -1], 1.0, copy.deepcopy(og))
+        live = mask[:, -1]
+        step_hits[0] += int((s_ref == s_dev)[live].sum())
+        step_hits[1] += int(live.sum())
+        return ref
 
-    og = OR.stream(5, "c5-rng")
     ref = OM.decode_frame(logits_fn, prev, lat, steps=25, gen=og)
-    agree = float((got == ref).mean())
-    _report("c5", token_agreement=agree)
-    assert agree >= TOL["decode_token_agreement_jasmine_chain"]
-    assert g.random() == og.random()
+    g = R.stream(5, "c5-rng")
+    got = m.decode_frame(prev, lat, steps=25, rng=g)
+    og2 = OR.stream(5, "c5-rng")
+    OM.decode_frame(lambda tk, la, mask: np.zeros((1, tk.shape[1], 256, 1024), np.float32), prev, lat, steps=25,
+                    gen=og2)
+    step_agree = step_hits[0] / max(step_hits[1], 1)
+    chain = float((got == ref).mean())
+    _report("c5", step_agreement=step_agree, chain_token_agreement=chain)
+    assert step_agree >= TOL["decode_step_agreement_peaked"]
+    assert chain >= TOL["decode_token_agreement_jasmine_chain"]
+    assert g.random() == og2.random()  # the device decode consumed exactly the reference's draws
 
 
 # ------------------------------------------------------------------------------------------------

@@ -238,7 +238,12 @@ def test_attn_temporal_fwd_bwd(T):
     dqkv = Kn.attn_temporal_bwd(qkv, out, dout, lse, B, T, S, H, colsum=cs)
     cs_ref = torch.empty_like(cs)
     Kn.colsum_bf16(dqkv, cs_ref)
-    assert rel(cs, cs_ref) < 1e-5
+    # q / v bias gradients are the column sums of the written dq / dv; the key-bias gradient is
+    # exactly zero (a bias shared by every key shifts each softmax row by a constant): the tcgen05
+    # kernel writes 0 there, and the summed written dk is zero up to bf16 rounding noise
+    assert rel(cs[:D], cs_ref[:D]) < 1e-5 and rel(cs[2 * D:], cs_ref[2 * D:]) < 1e-5
+    assert float(cs[D:2 * D].abs().max()) == 0.0
+    assert float(cs_ref[D:2 * D].norm()) < 1e-2 * float(cs_ref[2 * D:].norm()) + 1e-3
     scale = float(qf.grad[:, 2 * D:].norm())
     for i in range(3):
         got, ref = dqkv[:, i * D:(i + 1) * D].float(), qf.grad[:, i * D:(i + 1) * D]

@@ -116,8 +116,15 @@ def test_lam_patch16_forward_backward(frames):
     P = OM.params_to_torch(OM.init_lam(ocfg, seed=5))
     unit = OM.frames_to_unit(frames)
     recon, idx, losses = lam.forward(unit)
-    r2, i2, l2 = OM.lam_forward(P, ocfg, torch.tensor(unit))
-    np.testing.assert_array_equal(idx, i2)
+    _, i2, _ = OM.lam_forward(P, ocfg, torch.tensor(unit))
+    # bf16 encoder: a code may flip only where the latent error explains it (6-code near-ties);
+    # the oracle step then runs on the device's codes (a flipped code moves a whole action)
+    with torch.no_grad():
+        z_ref = OM.lam_encode_pre_vq(P, ocfg, torch.tensor(unit)).numpy()
+    z_dev = lam._encode_pre_vq(unit).numpy()
+    assert OM.vq_mismatch_explained(z_dev, z_ref, P["codebook"].detach().numpy(), idx, i2) == 0
+    assert (np.asarray(idx) == np.asarray(i2)).mean() >= TOL["lam_code_agreement_bf16_encoder"]
+    r2, _, l2 = OM.lam_forward_with_indices(P, ocfg, torch.tensor(unit), idx)
     assert _rel(recon.numpy(), r2.detach().numpy()) < TOL["bf16_logits_rel_l2"]
     for k in ("recon", "codebook", "commitment", "total"):
         assert abs(float(losses[k].data) - float(l2[k])) < max(TOL["bf16_loss_abs"], TOL["bf16_loss_rel"] * float(l2[k])), k
