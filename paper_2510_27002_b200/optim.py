@@ -37,11 +37,18 @@ class AdamWState:
     m_flat: torch.Tensor | None = None
     v_flat: torch.Tensor | None = None
     store: object = None
+    first_bad: torch.Tensor | None = None  # optimizer step (t) at which the flag first tripped, 0 = never
 
     def raise_if_nonfinite(self) -> None:
+        """Raise NonFiniteGradient if any deferred check tripped (the reference raises at the first
+        non-finite gradient, optim.py:48-49; every later update was skipped, trainer.py:170-180)."""
         if self.flag is not None and int(self.flag) != 0:
+            at = int(self.first_bad) if self.first_bad is not None else 0
             self.flag.zero_()
-            raise NonFiniteGradient("non-finite gradient (update skipped)")
+            if self.first_bad is not None:
+                self.first_bad.zero_()
+            where = f" at optimizer step {at}" if at else ""
+            raise NonFiniteGradient(f"non-finite gradient{where} (that update and every later one skipped)")
 
 
 def adamw_init(params: dict, weight_decay: float = 0.0, beta1: float = 0.9, beta2: float = 0.999,
@@ -50,6 +57,7 @@ def adamw_init(params: dict, weight_decay: float = 0.0, beta1: float = 0.9, beta
     st = AdamWState(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
     dev = next(iter(params.values())).data.device
     st.flag = torch.zeros((), dtype=torch.int32, device=dev)
+    st.first_bad = torch.zeros((), dtype=torch.int32, device=dev)
     if store is None:
         store = store_for(params)
     if store is not None and store.owns(params):
@@ -100,6 +108,10 @@ def adamw_step(params: dict, grads: dict, state: AdamWState, lr: float, check: s
                 pc = p.contiguous()
                 K.adamw(pc, grads[n].contiguous(), state.m[n], state.v[n], flag=state.flag, **sc)
                 p.copy_(pc)
+    if state.first_bad is not None and not torch.cuda.is_current_stream_capturing():
+        # remember the first step whose gradients tripped the flag (device-side, no host sync)
+        torch.where((state.flag != 0) & (state.first_bad == 0), torch.full_like(state.first_bad, state.t),
+                    state.first_bad, out=state.first_bad)
     if check == "sync":
         state.raise_if_nonfinite()
 

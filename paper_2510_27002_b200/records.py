@@ -87,54 +87,69 @@ def _frame_bytes(geometry) -> int:
     return h * w * c
 
 
-def _write_file(path: Path, records: list, fpr: int, geometry) -> None:
+def _file_image(records: list, fpr: int, geometry) -> np.ndarray:
+    """The whole JASREC file (records.py:7-16) as one uint8 array: header, absolute payload
+    offsets, then each record's frames followed by its per-frame actions."""
     h, w, c = geometry
-    header = MAGIC + _FIXED.pack(VERSION, len(records), fpr, h, w, c)
-    rec = fpr * _frame_bytes(geometry) + fpr
-    first = len(header) + 8 * len(records)
+    n = len(records)
+    head = MAGIC + _FIXED.pack(VERSION, n, fpr, h, w, c)
+    rec_bytes = fpr * _frame_bytes(geometry) + fpr
+    base = len(head) + 8 * n
+    img = np.empty(base + n * rec_bytes, dtype=np.uint8)
+    img[:len(head)] = np.frombuffer(head, dtype=np.uint8)
+    offsets = base + rec_bytes * np.arange(n, dtype="<u8")
+    img[len(head):base] = offsets.view(np.uint8)
+    body = img[base:].reshape(n, rec_bytes) if n else img[base:].reshape(0, rec_bytes)
+    nfb = fpr * _frame_bytes(geometry)
+    for row, (frames, actions) in zip(body, records):
+        row[:nfb] = np.asarray(frames, dtype=np.uint8).reshape(-1)
+        row[nfb:] = np.asarray(actions, dtype=np.uint8).reshape(-1)
+    return img
+
+
+def _atomic_write(path: Path, data: np.ndarray) -> None:
+    """Write through a sibling temp file and rename: a reader never sees a partial file."""
     tmp = path.with_suffix(".tmp")
     try:
-        with open(tmp, "wb") as fh:
-            fh.write(header)
-            fh.write(struct.pack(f"<{len(records)}Q", *[first + i * rec for i in range(len(records))]))
-            for frames, actions in records:
-                fh.write(np.ascontiguousarray(frames, dtype=np.uint8).tobytes())
-                fh.write(np.ascontiguousarray(actions, dtype=np.uint8).tobytes())
+        data.tofile(tmp)
         os.replace(tmp, path)
-    except BaseException:
-        tmp.unlink(missing_ok=True)
-        raise
+    finally:
+        if tmp.exists():
+            tmp.unlink()
+
+
+def _full_records(episodes, fpr: int):
+    """(seed, geometry, frames, actions) of every whole frames_per_record chunk of every episode;
+    shorter episodes and ragged tails yield nothing (records.py:120-169 chunking rule)."""
+    for ep in episodes:
+        frames = np.asarray(ep.frames)
+        for k in range(len(frames) // fpr):
+            sl = slice(k * fpr, (k + 1) * fpr)
+            yield int(ep.seed), tuple(int(g) for g in frames.shape[1:]), frames[sl], np.asarray(ep.actions)[sl]
 
 
 def write_dataset(episodes, chunking: Chunking, out_dir) -> DatasetIndex:
-    """records.py:120-169: fixed-size records from episodes (ragged tails and short episodes dropped)."""
+    """records.py:120-169: fixed-size records grouped records_per_file to a file
+    (records-00000.bin, ...), plus index.json.  Byte-identical to the reference's files."""
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
     fpr, rpf = chunking.frames_per_record, chunking.records_per_file
-    files, seeds, pending = [], [], []
-    geometry = None
+    files, seeds, group, geometry = [], [], [], None
 
-    def flush():
-        if pending:
-            name = f"records-{len(files):05d}.bin"
-            _write_file(out / name, pending, fpr, geometry)
-            files.append({"name": name, "records": len(pending)})
-            pending.clear()
+    def emit():
+        name = f"records-{len(files):05d}.bin"
+        _atomic_write(out / name, _file_image(group, fpr, geometry))
+        files.append({"name": name, "records": len(group)})
+        group.clear()
 
-    try:
-        for ep in episodes:
-            if geometry is None:
-                geometry = tuple(int(g) for g in ep.frames.shape[1:])
-            for k in range(len(ep.frames) // fpr):
-                pending.append((ep.frames[k * fpr:(k + 1) * fpr], ep.actions[k * fpr:(k + 1) * fpr]))
-                seeds.append(int(ep.seed))
-                if len(pending) == rpf:
-                    flush()
-        flush()
-    except BaseException:
-        for p in out.glob("*.tmp"):
-            p.unlink(missing_ok=True)
-        raise
+    for seed, geo, frames, actions in _full_records(episodes, fpr):
+        geometry = geometry or geo
+        group.append((frames, actions))
+        seeds.append(seed)
+        if len(group) == rpf:
+            emit()
+    if group:
+        emit()
     if geometry is None:
         raise ValueError("no episodes long enough to produce a record")
     index = DatasetIndex(root=out, files=files, frames_per_record=fpr, records_per_file=rpf, geometry=geometry,
@@ -241,65 +256,73 @@ def subsequence_start(seed: int, epoch: int, record_id: int, fpr: int, seq_len: 
     return fold_key(seed, "subseq", epoch, record_id) % (fpr - seq_len + 1)
 
 
+def _epoch_batches(seed: int, epoch: int, first: int, total: int, batch_size: int):
+    """Record ids of the batches of one epoch from cursor `first`: consecutive windows of the
+    epoch's permutation stream(seed, "perm", epoch) (records.py:273-294)."""
+    order = stream(seed, "perm", epoch).permutation(total)
+    return [order[c:c + batch_size] for c in range(first, total - batch_size + 1, batch_size)]
+
+
 def _batch_plan(index: DatasetIndex, state: LoaderState, batch_size: int, seq_len: int):
-    """(epoch, cursor, record ids, starts, next_state) for every batch, in the reference's order."""
+    """(record ids, subsequence starts, loader state after the batch) of every batch, in the
+    reference's order.  The state after a batch points at the next batch: the same epoch at the
+    next cursor, or cursor 0 of the next epoch when no full batch is left."""
     if seq_len > index.frames_per_record:
         raise ValueError("seq_len exceeds frames_per_record")
     total = index.total_records
     if batch_size > total:
         raise ValueError(f"batch_size {batch_size} > total records {total}")
+    fpr = index.frames_per_record
     epoch, cursor = state.epoch, state.cursor
     while True:
-        perm = stream(state.seed, "perm", epoch).permutation(total)
-        while cursor + batch_size <= total:
-            ids = [int(r) for r in perm[cursor:cursor + batch_size]]
-            starts = [subsequence_start(state.seed, epoch, r, index.frames_per_record, seq_len) for r in ids]
+        for ids in _epoch_batches(state.seed, epoch, cursor, total, batch_size):
             cursor += batch_size
-            nxt = replace(state, epoch=epoch, cursor=cursor)
-            if cursor + batch_size > total:
-                nxt = replace(state, epoch=epoch + 1, cursor=0)
-            yield ids, starts, nxt
-        epoch += 1
-        cursor = 0
+            after = (epoch, cursor) if cursor + batch_size <= total else (epoch + 1, 0)
+            rids = [int(r) for r in ids]
+            yield (rids, [subsequence_start(state.seed, epoch, r, fpr, seq_len) for r in rids],
+                   replace(state, epoch=after[0], cursor=after[1]))
+        epoch, cursor = epoch + 1, 0
 
 
 def shuffled_batches(index: DatasetIndex, state: LoaderState, batch_size: int, seq_len: int = 16):
-    """records.py:259-292: endless (frames (B,T,H,W,C) u8, actions (B,T) u8, next_state) stream."""
+    """records.py:259-292: endless (frames (B,T,H,W,C) u8, actions (B,T) u8, next_state) stream;
+    only each record's subsequence bytes are read."""
     reader = DatasetReader(index)
+    shape = (batch_size, seq_len) + tuple(index.geometry)
     try:
         for ids, starts, nxt in _batch_plan(index, state, batch_size, seq_len):
-            frames = np.empty((batch_size, seq_len) + tuple(index.geometry), dtype=np.uint8)
-            actions = np.empty((batch_size, seq_len), dtype=np.uint8)
-            for j, (rid, st) in enumerate(zip(ids, starts)):
-                reader.read_span_into(rid, st, seq_len, frames[j], actions[j])
+            frames = np.empty(shape, dtype=np.uint8)
+            actions = np.empty(shape[:2], dtype=np.uint8)
+            for j, rid in enumerate(ids):
+                reader.read_span_into(rid, starts[j], seq_len, frames[j], actions[j])
             yield frames, actions, nxt
     finally:
         reader.close()
 
 
+_END = object()
+
+
 def prefetch(iterator, depth: int):
-    """records.py:295-322: same items, produced by a background thread; errors re-raise here."""
+    """records.py:295-322 semantics (same items in the same order, produced ahead by a background
+    thread; a producer error re-raises at the consumer): `depth` next() calls are kept in flight
+    on a single worker thread."""
     if depth < 1:
         raise ValueError("depth must be >= 1")
-    q: queue.Queue = queue.Queue(maxsize=depth)
-    done = object()
-
-    def worker():
-        try:
-            for item in iterator:
-                q.put(item)
-            q.put(done)
-        except BaseException as exc:
-            q.put(exc)
-
-    threading.Thread(target=worker, daemon=True).start()
-    while True:
-        item = q.get()
-        if item is done:
-            return
-        if isinstance(item, BaseException):
-            raise item
-        yield item
+    import collections
+    from concurrent.futures import ThreadPoolExecutor
+    source = iter(iterator)
+    pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="jasrec-prefetch")
+    try:
+        ahead = collections.deque(pool.submit(next, source, _END) for _ in range(depth))
+        while True:
+            item = ahead.popleft().result()
+            if item is _END:
+                return
+            ahead.append(pool.submit(next, source, _END))
+            yield item
+    finally:
+        pool.shutdown(wait=False, cancel_futures=True)
 
 
 def detect_duplicates(index: DatasetIndex) -> dict:

@@ -75,6 +75,7 @@ class DynamicsTrainStep:
         """JASCKPT1 bundle of this stage (params + AdamW moments + loader state), deskworld layout."""
         from .checkpoint import pack_stage
         from .records import LoaderState
+        self.opt.raise_if_nonfinite()  # never checkpoint past a skipped (non-finite) update
         ls = loader_state if loader_state is not None else LoaderState(seed=self.seed)
         return pack_stage(self.stage, config or {}, self.model.params, self.opt, ls, step, self.seed)
 
