@@ -117,7 +117,7 @@ __device__ __forceinline__ void stg_write_rows(const uint8_t* stg, uint8_t* gbas
 // rows of A and half of the BN columns of B, so operand bytes per MAC drop by a third.
 // LNX (LayerNorm-fused epilogue): four 4 KB staging tiles per epilogue warp (prefetched fp32 input
 // tiles + output tiles), paid for with three operand stages instead of six.
-template <int BN, bool PAIR = false, int LNX = 0>
+template <int BN, bool PAIR = false, int LNX = 0, bool DB = false>
 struct GemmShape {
   static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
   static constexpr int A_BYTES = BM * BK * 2;
@@ -125,7 +125,8 @@ struct GemmShape {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // per epilogue warp: 32 rows x 128 B tiles, 128B-swizzled (LNX 1: two fp32 + two bf16 tiles,
   // LNX 2: four fp32 tiles)
-  static constexpr int STG_BYTES = LNX == 1 ? 12288 : (LNX == 2 ? 16384 : 4096);
+  // DB: two 4 KB staging tiles per epilogue warp (aux prefetched one chunk ahead / two outputs in flight)
+  static constexpr int STG_BYTES = LNX == 1 ? 12288 : (LNX == 2 ? 16384 : (DB ? 8192 : 4096));
   static constexpr int STAGES_RAW = ((PAIR ? 192 : 200) * 1024 - 8 * (STG_BYTES - 4096)) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
@@ -715,11 +716,11 @@ JZ_DEV void ln_epilogue(const GemmParams& p, const EpiMaps& em, uint32_t tmem_ba
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR, int LNX = 0>
+template <int BN, bool A_MN, bool B_MN, bool PAIR, int LNX = 0, bool DB = false>
 __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ EpiMaps em, GemmParams p, float* ws) {
-  using S = GemmShape<BN, PAIR, LNX>;
+  using S = GemmShape<BN, PAIR, LNX, DB>;
   constexpr int TM = PAIR ? 2 * BM : BM;  // rows per (pair) tile
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -733,8 +734,8 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
   uint64_t* empty_bar = full_bar + S::STAGES;
   uint64_t* tfull_bar = empty_bar + S::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps] ([2 kEpiWarps] for LNX)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + (LNX ? 2 : 1) * kEpiWarps);
+  uint64_t* aux_bar = tempty_bar + 2;  // [kEpiWarps] ([2 kEpiWarps] for LNX / DB)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + ((LNX || DB) ? 2 : 1) * kEpiWarps);
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + S::BAR_BYTES);  // [BN]
 
   const uint32_t warp = warp_id();
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], (PAIR ? 2 : 1) * kEpiWarps);  // one arrival per epilogue warp of the pair
     }
-    for (int i = 0; i < (LNX ? 2 : 1) * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
+    for (int i = 0; i < ((LNX || DB) ? 2 : 1) * kEpiWarps; ++i) mbar_init(&aux_bar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -883,11 +884,29 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
     const int chalf = ew >> 2;                 // column slot of this warp
     constexpr int HALF = BN / (kEpiWarps / 4);  // columns per warp
     const int etid = threadIdx.x - 64;  // 0 .. 32*kEpiWarps-1
-    uint8_t* stg = stg_base + ew * S::STG_BYTES;
-    uint32_t apar = 0;
+    uint8_t* const stg_w = stg_base + ew * S::STG_BYTES;  // this warp's staging tile(s)
+    uint8_t* stg = stg_w;
+    uint32_t apar = 0;  // aux barrier phase bits (bit b: staging tile b under DB)
+    int q = 0;          // staged chunks done by this warp (DB: the aux of chunk q sits in tile q & 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool has_bias = p.bias != nullptr && p.splits == 1;
+    // DB with an aux operand: chunk q + 1's aux tile is loaded while chunk q computes.  The host
+    // enables DB only with N % BN == 0, so every warp has columns in every tile and the next
+    // processed chunk is always the next one in this sequence.
+    const bool db_aux = DB && p.tma_epi && p.splits == 1 && (p.epi == JZ_EPI_GELU_BWD || p.epi == JZ_EPI_MUL_F16);
+    constexpr int kChunks = HALF / 64;  // bf16-output chunks per tile per warp
+    auto aux_prefetch = [&](int u_next, int cc_next, int slot) {  // chunk cc_next of unit u_next -> tile slot
+      const int tile2 = u_next;  // splits == 1
+      const int m0_2 = (tile2 / p.n_tiles) * TM + (int)rank * BM, n0_2 = (tile2 % p.n_tiles) * BN;
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&aux_bar[2 * ew + slot], 4096);
+        tma_load_2d(stg_w + slot * 4096, &em.aux, &aux_bar[2 * ew + slot], n0_2 + chalf * HALF + cc_next * 64,
+                    m0_2 + (int)quarter * 32);
+      }
+    };
+    if (db_aux && first_unit < units) aux_prefetch(first_unit, 0, 0);
     // staged epilogue: bias comes straight from global (all lanes read the same address -> one
     // L1 broadcast per vector), so the epilogue warps never synchronise with each other
     const bool bias_vec = has_bias && (reinterpret_cast<uintptr_t>(p.bias) % 16 == 0) && (p.N % 4 == 0);
@@ -926,12 +945,24 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
           if (n >= p.N) break;  // warp-uniform
           const int cols_bytes = min(CW, p.N - n) * esz;
           PH_T(t_a);
-          if (p.store_tma) {
+          if (DB && db_aux) {
+            // this chunk's aux is in tile q & 1; refill the other tile with the next chunk's once
+            // the previous chunk's store has read it
+            stg = stg_w + (q & 1) * 4096;
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            if (cc + 1 < kChunks) aux_prefetch(u, cc + 1, (q + 1) & 1);
+            else if (u + unit_stride < units) aux_prefetch(u + unit_stride, 0, (q + 1) & 1);
+          } else if (DB && p.store_tma) {
+            stg = stg_w;  // GELU_DG: gelu' goes through tile 0, gelu through tile 1
+            if (lane == 0) bulk_wait_read1();  // the previous chunk's gelu' store has read tile 0
+            __syncwarp();
+          } else if (p.store_tma) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
           }
           PH_ADD(0, t_a);
-          if (need_aux && lane == 0) {
+          if (!DB && need_aux && lane == 0) {
             fence_proxy_async();  // generic reads of the previous chunk before the async-proxy write
             mbar_arrive_expect_tx(&aux_bar[ew], S::STG_BYTES);
             tma_load_2d(stg, &em.aux, &aux_bar[ew], n, row0);
@@ -981,8 +1012,14 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
               if (j < CW && n + j < p.N) v[j] += __ldg(p.bias + n + j);
           }
           if (need_aux) {
-            mbar_wait(&aux_bar[ew], apar);
-            apar ^= 1;
+            if (DB && db_aux) {
+              const int b = q & 1;
+              mbar_wait(&aux_bar[2 * ew + b], (apar >> b) & 1u);
+              apar ^= 1u << b;
+            } else {
+              mbar_wait(&aux_bar[ew], apar);
+              apar ^= 1;
+            }
             if (p.epi == JZ_EPI_MUL_F16) {
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
@@ -1044,7 +1081,12 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
                 uint32_t pk[32];
 #pragma unroll
                 for (int c = 0; c < 32; ++c) pk[c] = pack_bf16(v[2 * c], v[2 * c + 1]);
-                if (lane == 0) bulk_wait_read0();
+                if (DB) {
+                  stg = stg_w + 4096;  // tile 1: the previous chunk's gelu store has read it
+                  if (lane == 0) bulk_wait_read1();
+                } else if (lane == 0) {
+                  bulk_wait_read0();
+                }
                 __syncwarp();
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
@@ -1129,6 +1171,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
           }
           __syncwarp();
           PH_ADD(3, t_d);
+          ++q;
         }
       } else {
         // ---------- direct epilogue (unaligned shapes) ----------
@@ -1185,14 +1228,14 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR, int LNX = 0>
+template <int BN, bool A_MN, bool B_MN, bool PAIR, int LNX = 0, bool DB = false>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMaps& em, const GemmParams& p,
                        float* ws, cudaStream_t stream) {
-  using S = GemmShape<BN, PAIR, LNX>;
+  using S = GemmShape<BN, PAIR, LNX, DB>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX>,
+    attr_err = cudaFuncSetAttribute(gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX, DB>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
   });
   JZ_CUDA_TRY(attr_err);
@@ -1211,11 +1254,11 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const EpiMa
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    JZ_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX>, ta, tb, em, p, ws));
+    JZ_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX, DB>, ta, tb, em, p, ws));
     count_launch();
   } else {
     const int grid = units < num_sms() ? units : num_sms();
-    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX><<<grid, gemm_threads<PAIR>(), S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
+    gemm_bf16_kernel<BN, A_MN, B_MN, PAIR, LNX, DB><<<grid, gemm_threads<PAIR>(), S::SMEM_BYTES, stream>>>(ta, tb, em, p, ws);
     JZ_LAUNCH_CHECK();
   }
   return JZ_OK;
@@ -1239,6 +1282,14 @@ using namespace jz;
 static bool pair_mode_enabled() {
   static const bool on = [] {
     const char* e = getenv("JZ_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool db_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("JZ_GEMM_DB");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -1376,7 +1427,14 @@ static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, in
   if (colsum != nullptr)
     JZ_CHECK_ARG(p.tma_epi == 1 && (reinterpret_cast<uintptr_t>(colsum) % 8) == 0,
                  "gemm colsum: needs the staged epilogue (N %% 8 == 0, N > 64, aligned output) and an 8-byte aligned buffer");
-  if (BN == 256 && pair) rc = dispatch_major<256, true>(a_mn, b_mn, ta, tb, em, p, ws, stream);
+  // double-buffered epilogue staging for the aux-reading GELU-backward epilogues: the next chunk's
+  // aux tile loads while this one computes (MUL_F16 dX at M=148032, N=2048: 334.6 -> 326.7 us; the
+  // two-stores-in-flight variant for GELU_DG measured 389.6 -> 393.5 us and is not used)
+  const bool db = BN == 256 && pair && p.tma_epi && p.store_tma && p.splits == 1 && N % 256 == 0 && db_enabled() &&
+                  (epilogue == JZ_EPI_MUL_F16 || epilogue == JZ_EPI_GELU_BWD);
+  if (db && !a_mn && b_mn) rc = launch_gemm<256, false, true, true, 0, true>(ta, tb, em, p, ws, stream);
+  else if (db && !a_mn && !b_mn) rc = launch_gemm<256, false, false, true, 0, true>(ta, tb, em, p, ws, stream);
+  else if (BN == 256 && pair) rc = dispatch_major<256, true>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else if (BN == 256) rc = dispatch_major<256>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else if (BN == 128) rc = dispatch_major<128>(a_mn, b_mn, ta, tb, em, p, ws, stream);
   else rc = dispatch_major<64>(a_mn, b_mn, ta, tb, em, p, ws, stream);
