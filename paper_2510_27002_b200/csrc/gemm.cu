@@ -56,8 +56,11 @@ namespace jz {
 
 // epilogue warps: 2 per TMEM lane quarter (16 measured slower: register cap 96 + spills and one
 // fewer pipeline stage)
+#ifndef JZ_GEMM_EPI_WARPS
+#define JZ_GEMM_EPI_WARPS 8
+#endif
 template <bool PAIR>
-constexpr int epi_warps() { return 8; }
+constexpr int epi_warps() { return PAIR ? JZ_GEMM_EPI_WARPS : 8; }
 template <bool PAIR>
 constexpr int gemm_threads() { return 64 + 32 * epi_warps<PAIR>(); }
 constexpr int BM = 128;
