@@ -274,6 +274,88 @@ __global__ void __launch_bounds__(256) linear_f32_n32_kernel(const float* __rest
   }
 }
 
+// N = 32 forward, row-per-lane: a warp owns 32 rows (lane = row) and all 32 outputs of each in
+// registers.  x is staged per warp through shared memory in 32-column chunks (coalesced 512-byte
+// row segments in, padded rows so the per-lane column reads are conflict-free), and W [K][32] is
+// read as broadcast float4s: 9 shared loads per 32 FFMA (the warp-per-4-rows kernel above issued 8
+// loads per 16).  Per output the sum still runs over k in order with fmaf: bit-identical.
+constexpr int kLinV2Warps = 8;
+constexpr int kLinV2Kc = 16;             // x columns staged per step
+constexpr int kLinV2Pad = kLinV2Kc + 1;  // padded staging rows: conflict-free column reads
+constexpr int kLinV2Rows = 64;  // rows per warp: lane owns rows lane and lane + 32
+__global__ void __launch_bounds__(32 * kLinV2Warps) linear_f32_n32_rows_kernel(
+    const float* __restrict__ x, int64_t R, int K, const float* __restrict__ W, const float* __restrict__ b,
+    float* __restrict__ y, int accumulate) {
+  extern __shared__ float smem[];
+  float* sW = smem;                                  // [K][32]
+  float* sx = smem + (int64_t)K * 32;                // [warps][64 rows][kLinV2Pad]
+  for (int e = threadIdx.x * 4; e < K * 32; e += blockDim.x * 4)
+    *reinterpret_cast<float4*>(sW + e) = *reinterpret_cast<const float4*>(W + e);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* xs = sx + warp * kLinV2Rows * kLinV2Pad;
+  const int64_t groups = (R + kLinV2Rows - 1) / kLinV2Rows;
+  for (int64_t gidx = (int64_t)blockIdx.x * kLinV2Warps + warp; gidx < groups; gidx += (int64_t)gridDim.x * kLinV2Warps) {
+    const int64_t r0 = gidx * kLinV2Rows;
+    float a0[32], a1[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a0[j] = a1[j] = 0.f;
+    for (int k0 = 0; k0 < K; k0 += kLinV2Kc) {
+      // stage x[r0 .. r0+63][k0 .. k0+15]: each instruction moves 8 rows x 64 bytes
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = (lane >> 2) + 8 * i;
+        const int64_t row = r0 + rr < R ? r0 + rr : R - 1;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x + row * K + k0) + (lane & 3));
+        float* d = xs + rr * kLinV2Pad + 4 * (lane & 3);
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+      }
+      __syncwarp();
+#pragma unroll 2
+      for (int kk = 0; kk < kLinV2Kc; ++kk) {
+        const float x0 = xs[lane * kLinV2Pad + kk], x1 = xs[(lane + 32) * kLinV2Pad + kk];
+        const float4* wr = reinterpret_cast<const float4*>(sW + (k0 + kk) * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 w = wr[q];
+          a0[4 * q] = fmaf(x0, w.x, a0[4 * q]);
+          a0[4 * q + 1] = fmaf(x0, w.y, a0[4 * q + 1]);
+          a0[4 * q + 2] = fmaf(x0, w.z, a0[4 * q + 2]);
+          a0[4 * q + 3] = fmaf(x0, w.w, a0[4 * q + 3]);
+          a1[4 * q] = fmaf(x1, w.x, a1[4 * q]);
+          a1[4 * q + 1] = fmaf(x1, w.y, a1[4 * q + 1]);
+          a1[4 * q + 2] = fmaf(x1, w.z, a1[4 * q + 2]);
+          a1[4 * q + 3] = fmaf(x1, w.w, a1[4 * q + 3]);
+        }
+      }
+    }
+    // out: lane holds rows lane and lane + 32 (32 outputs each): write them as two 16-column halves
+    // transposed through the staging tile, so every store instruction covers 64-byte row segments
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kLinV2Kc; ++j) {
+        const float bj = b ? b[16 * hf + j] : 0.f;
+        xs[lane * kLinV2Pad + j] = a0[16 * hf + j] + bj;
+        xs[(lane + 32) * kLinV2Pad + j] = a1[16 * hf + j] + bj;
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int i = 0; i < kLinV2Rows / 2; ++i) {  // 2 rows x 16 columns per instruction
+        const int rr = 2 * i + (lane >> 4);
+        const int64_t r = r0 + rr;
+        if (r < R) {
+          float* dst = y + r * 32 + 16 * hf + (lane & 15);
+          const float v = xs[rr * kLinV2Pad + (lane & 15)];
+          *dst = accumulate ? *dst + v : v;
+        }
+      }
+    }
+  }
+}
+
 // dx = dy W^T for a K -> 32 projection (W [K][32], the latent projections' input gradient): W staged
 // transposed in shared memory, one warp per row with lane j holding dy[r][j] (shuffle-broadcast),
 // lane l computing columns l + 32 q.  Per output the sum runs over j in order (as linear_f32_dx_kernel).
@@ -529,7 +611,20 @@ extern "C" int jz_linear_f32(const float* x, int64_t R, int K, const float* W, i
                              int accumulate, jz_stream_t s) {
   const int64_t n = R * N;
   if (n == 0) return JZ_OK;
-  if (N == 32 && K % 4 == 0 && K <= 1024 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)W % 16) == 0) {
+  if (N == 32 && K % 32 == 0 && K <= 1024 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)W % 16) == 0) {
+    const size_t smem = (size_t)K * 32 * sizeof(float) + (size_t)kLinV2Warps * kLinV2Rows * kLinV2Pad * sizeof(float);
+    static std::once_flag once2;
+    static cudaError_t attr_err2 = cudaSuccess;
+    std::call_once(once2, [] {
+      attr_err2 = cudaFuncSetAttribute(linear_f32_n32_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       1024 * 32 * 4 + kLinV2Warps * kLinV2Rows * kLinV2Pad * 4);
+    });
+    JZ_CUDA_TRY(attr_err2);
+    int64_t grid = (R + kLinV2Rows * kLinV2Warps - 1) / (kLinV2Rows * kLinV2Warps);
+    if (grid > (int64_t)num_sms() * 2) grid = (int64_t)num_sms() * 2;  // two CTAs per SM
+    linear_f32_n32_rows_kernel<<<(unsigned)grid, 32 * kLinV2Warps, smem, reinterpret_cast<cudaStream_t>(s)>>>(
+        x, R, K, W, b, y, accumulate);
+  } else if (N == 32 && K % 4 == 0 && K <= 1024 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)W % 16) == 0) {
     const size_t smem = (size_t)K * 32 * sizeof(float);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
