@@ -244,9 +244,45 @@ def secondary_configs(dev) -> dict:
                               "unit": "frames/s", "ms_per_step": round(ms3, 2),
                               "config": "B=8, T=16, 1024 codes, recon + VQ losses, full backward + AdamW "
                                         "(trainer.tokenizer_stage)"}
+    out["tokenizer_fwd"]["fp32_kernels"] = _fp32_kernels(dev)
     out["pretrain_lam_stage"] = _pretrain_lam_stage(tok, lam, dev)
     out["play_act"] = _play_act(tok, lam, dev)
     out["dit_train"] = _dit_train(dev)
+    return out
+
+
+def _ffma_peak() -> tuple:
+    p = ROOT / "profiles" / "r02" / "ffma_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["ffma_tflops"]), "profiles/r02/ffma_peak.json (tools/ffma_peak.cu)"
+    return 72.3, "fallback: 148 SM x 128 FFMA x 2 x 1.965 GHz measured 72.3"
+
+
+def _fp32_kernels(dev) -> dict:
+    """The fp32 (CUDA-core FFMA) kernels of the tokenizer / LAM path at the pretrain_lam stage shape
+    (R = 36 x 16 x 256 latent rows): the fused VQ distance + argmin + gather (K = 1024 codes, dz = 32)
+    and the 512 -> 32 latent projection, event-timed, against the measured FFMA peak."""
+    import torch
+
+    from paper_2510_27002_b200 import kernels as Kn
+    R = 36 * FRAMES_T * PATCHES
+    g = torch.Generator(device=dev).manual_seed(0)
+    z = torch.randn(R, 32, device=dev, generator=g)
+    cb = torch.randn(1024, 32, device=dev, generator=g)
+    x = torch.randn(R, 512, device=dev, generator=g)
+    w = torch.randn(512, 32, device=dev, generator=g) * 0.05
+    b = torch.zeros(32, device=dev)
+    peak, src = _ffma_peak()
+    out = {}
+    for name, fn, flops in (("vq_fwd", lambda: Kn.vq_fwd(z, cb), 2.0 * R * 1024 * 32),
+                            ("latent_projection_512x32", lambda: Kn.linear_f32(x, w, b), 2.0 * R * 512 * 32)):
+        fn()
+        us = 1e3 * _events_ms(fn, reps=10)
+        tf = flops / us / 1e6
+        out[name] = {"us_per_launch": round(us, 1), "tflops": round(tf, 1), "frac_ffma_peak": round(tf / peak, 3)}
+    out["ffma_peak_tflops"] = peak
+    out["peak_source"] = src
+    out["shape"] = f"R = {R} latent rows (B=36 clips)"
     return out
 
 
