@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ out_f32, float* __restrict__ lse, int frames, int S, int H) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   FwdSmallSmem& sm = *reinterpret_cast<FwdSmallSmem*>(smem + F_END);
   const int D = H * 64;
   const int warp = warp_id(), lane = lane_id();
@@ -464,12 +464,13 @@ constexpr int B_END = B_ST + TILE;       // 212992
 // per-unit vector block written by spatial_delta_kernel, one per (frame, head), floats:
 constexpr int U_LSE2 = 0;     // [0, 260)   lse * log2(e) per query row
 constexpr int U_DV = 260;     // [260, 520) Delta = rowsum(dO o O) per query row
-constexpr int U_Q = 520;      // q, k, v, dO of token 256 (fp32, 64 each)
-constexpr int U_K = 584;
-constexpr int U_V = 648;
-constexpr int U_DO = 712;
-constexpr int U_PC = 776;     // p and dS of (query 256, key 256)
-constexpr int U_DC = 777;
+constexpr int U_PC = 520;     // p and dS of (query 256, key 256)
+constexpr int U_DC = 521;
+constexpr int kUvbHead = 524;   // lse2, Delta, corner: the part the v3 backward loads (2096 bytes)
+constexpr int U_Q = 524;      // q, k, v, dO of token 256 (fp32, 64 each)
+constexpr int U_K = 588;
+constexpr int U_V = 652;
+constexpr int U_DO = 716;
 constexpr int kUvbFloats = 780;  // 3120 bytes: 16-byte multiple for cp.async.bulk
 
 struct BwdSmallSmem {
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
                        int frames, int S, int H) {
   using namespace sp;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   BwdSmallSmem& sm = *reinterpret_cast<BwdSmallSmem*>(smem + B_END);
   const int D = H * 64;
   const int warp = warp_id(), lane = lane_id();
@@ -1026,6 +1027,11 @@ __global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const float* __re
   }
 }
 
+namespace jz {
+int spatial_bwd3_launch(const void* qkv, const void* dout, const float* uvb, int64_t frames, int S, int H, void* dqkv,
+                        float* colsum_part, cudaStream_t st);
+}
+
 extern "C" int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H) {
   (void)S;
   return frames * (int64_t)H * jz::sp::kUvbFloats * (int64_t)sizeof(float);
@@ -1068,6 +1074,12 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
     }
     JZ_LAUNCH_CHECK();
   }
+  static const int version = [] {
+    const char* e = getenv("JZ_SPATIAL_BWD");
+    return e ? atoi(e) : 3;
+  }();
+  if (version != 2)
+    return spatial_bwd3_launch(qkv, dout, uvb, frames, S, H, dqkv, colsum_part, reinterpret_cast<cudaStream_t>(s));
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {

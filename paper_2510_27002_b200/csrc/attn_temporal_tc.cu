@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
     temporal_tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_o,
                            float* __restrict__ lse, int B, int T, int S, int H, int NG) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars& bar = *reinterpret_cast<Bars*>(smem + F_END);
   const int D = H * 64;
   const int warp = warp_id(), lane = lane_id();
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
                            const __grid_constant__ CUtensorMap tm_dqkv, const float* __restrict__ lse,
                            float* __restrict__ colsum, int B, int T, int S, int H, int NG) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars& bar = *reinterpret_cast<Bars*>(smem + B_END);
   const int D = H * 64;
   const int warp = warp_id(), lane = lane_id();

@@ -729,8 +729,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
   const int first_unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int unit_stride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kEpiWarps = S::EW;
   uint8_t* stg_base = smem + S::STAGES * S::STAGE_BYTES;  // kEpiWarps x 4 KB (1024-aligned)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * S::STG_BYTES);
@@ -1157,20 +1156,35 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
               stg_write_rows(stg, dbase + (int64_t)row0 * dld + (int64_t)n * esz, dld, rows_ok, cols_bytes, lane);
           }
           if (p.colsum != nullptr && !f32out) {
-            // bias gradient of the next layer: column sums of this warp's 32 staged bf16 rows
-            // (lane -> columns 2 lane, 2 lane + 1), one fp32 partial row per 32-row block
-            const int ch = lane >> 2, wd = lane & 3;
-            float s0 = 0.f, s1 = 0.f;
-#pragma unroll 8
-            for (int r = 0; r < 32; ++r) {
-              if (r < rows_ok) {
-                const float2 f = unpack_bf16(*reinterpret_cast<const uint32_t*>(stg + r * 128 + ((ch ^ (r & 7)) << 4) + wd * 4));
-                s0 += f.x;
-                s1 += f.y;
+            // bias gradient of the next layer: column sums of this warp's 32 staged bf16 rows, one
+            // fp32 partial row per 32-row block.  Lane reads 16-byte chunk (lane & 7) of rows
+            // 4k + (lane >> 3); the four row groups are folded with two shuffles.
+            const int cch = lane & 7;
+            float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int rr = 4 * k + (lane >> 3);
+              if (rr < rows_ok) {
+                const uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 128 + ((cch ^ (rr & 7)) << 4));
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = unpack_bf16(ww[e]);
+                  cs[2 * e] += f.x;
+                  cs[2 * e + 1] += f.y;
+                }
               }
             }
-            if (rows_ok > 0 && 2 * lane < p.N - n)
-              *reinterpret_cast<float2*>(p.colsum + (int64_t)(row0 >> 5) * p.N + n + 2 * lane) = make_float2(s0, s1);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 8);
+              cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], 16);
+            }
+            if (rows_ok > 0 && lane < 8 && 8 * cch < p.N - n) {
+              float4* dst = reinterpret_cast<float4*>(p.colsum + (int64_t)(row0 >> 5) * p.N + n + 8 * cch);
+              dst[0] = make_float4(cs[0], cs[1], cs[2], cs[3]);
+              dst[1] = make_float4(cs[4], cs[5], cs[6], cs[7]);
+            }
           }
           __syncwarp();
           PH_ADD(3, t_d);
@@ -1428,8 +1442,8 @@ static int gemm_impl(const void* A, int64_t lda, int a_kmajor, const void* B, in
     }
   }
   if (colsum != nullptr)
-    JZ_CHECK_ARG(p.tma_epi == 1 && (reinterpret_cast<uintptr_t>(colsum) % 8) == 0,
-                 "gemm colsum: needs the staged epilogue (N %% 8 == 0, N > 64, aligned output) and an 8-byte aligned buffer");
+    JZ_CHECK_ARG(p.tma_epi == 1 && (reinterpret_cast<uintptr_t>(colsum) % 16) == 0,
+                 "gemm colsum: needs the staged epilogue (N %% 8 == 0, N > 64, aligned output) and a 16-byte aligned buffer");
   // double-buffered epilogue staging for the aux-reading GELU-backward epilogues: the next chunk's
   // aux tile loads while this one computes (MUL_F16 dX at M=148032, N=2048: 334.6 -> 326.7 us; the
   // two-stores-in-flight variant for GELU_DG measured 389.6 -> 393.5 us and is not used)

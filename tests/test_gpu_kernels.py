@@ -190,9 +190,11 @@ def _ref_attn(qkv, lead, L_, H, causal):
     return o, torch.logsumexp(s, -1)
 
 
-@pytest.mark.parametrize("S", [257, 256])
-def test_attn_spatial_fwd_bwd(S):
-    frames, H = 13, 8
+@pytest.mark.parametrize("S,frames", [(257, 13), (256, 13), (257, 40), (256, 40)])
+def test_attn_spatial_fwd_bwd(S, frames):
+    """frames = 40: 320 (frame, head) units on 148 CTAs, so every CTA pipelines 2-3 units through the
+    backward's staged input release and its per-unit barrier phases."""
+    H = 8
     D = H * 64
     g = torch.Generator(device=dev).manual_seed(S)
     qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
