@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   FwdSmallSmem& sm = *reinterpret_cast<FwdSmallSmem*>(smem + F_END);
   const int D = H * 64;
-  const int warp = warp_id(), lane = lane_id();
+  const int warp = __shfl_sync(0xffffffffu, (int)warp_id(), 0), lane = lane_id();  // warp-uniform
   const int units = frames * H;
   const bool has_tail = S > 256;
   const float c2 = 0.125f * 1.4426950408889634f;  // scale * log2(e)
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, sm.tmem_base, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   BwdSmallSmem& sm = *reinterpret_cast<BwdSmallSmem*>(smem + B_END);
   const int D = H * 64;
-  const int warp = warp_id(), lane = lane_id();
+  const int warp = __shfl_sync(0xffffffffu, (int)warp_id(), 0), lane = lane_id();  // warp-uniform
   const int units = frames * H;
   const bool has_tail = S > 256;
   const float scale = 0.125f;
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, sm.tmem_base, 0);
 
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------

@@ -91,12 +91,18 @@ JZ_DEV uint32_t sw128(uint32_t r, uint32_t c) { return r * 128 + ((c ^ (r & 7)) 
 #ifdef JZ_SPATIAL_BWD_PROF
 // per-unit timeline of CTA 0 (clock64 marks), read back with jz_attn_bwd3_prof_read
 __device__ unsigned long long g_tl[16][128];
+__device__ unsigned long long g_tw[4][10][2][32];  // units 0..3: per-block, per-warp (loaded, done)
+#define TW(x, k)                                                                                      \
+  do {                                                                                                 \
+    if (blockIdx.x == 0 && i < 4 && (threadIdx.x & 31) == 0) g_tw[i][x][k][threadIdx.x >> 5] = clock64(); \
+  } while (0)
 #define TL(slot)                                                             \
   do {                                                                       \
     if (blockIdx.x == 0 && i < 16 && (threadIdx.x & 31) == 0) g_tl[i][slot] = clock64(); \
   } while (0)
 #else
 #define TL(slot) do { } while (0)
+#define TW(x, k) do { } while (0)
 #endif
 
 #ifdef JZ_SPATIAL_BWD_DEBUG
@@ -280,10 +286,10 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
       const uint32_t pcol = tmem + (b ? C_RC : C_RA);
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
+        // P^T / dS^T of queries 16 ks .. 16 ks + 15: written by column group 16 ks / QW, packed bf16 pairs
         const uint32_t pa = pcol + QW * (ks / (QW / 16)) + 8 * (ks % (QW / 16));
         umma_bf16_ts_w(tmem + C_DV, pa, dsc(ado, qoff + ks * 2048, 8192), id_kv, (c > 0 || ks > 0));
-        umma_bf16_ss_w(tmem + C_DK, dsc(ads, c * TILE + ks * 32, 16), dsc(aq, qoff + ks * 2048, 8192), id_kv,
-                       (c > 0 || ks > 0));
+        umma_bf16_ts_w(tmem + C_DK, pa + QW / 2, dsc(aq, qoff + ks * 2048, 8192), id_kv, (c > 0 || ks > 0));
       }
       if (c & 1) {
         const int t = c >> 1;
@@ -454,6 +460,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         ld_cols(tP + QW * cg, vd);
         tmem_ld_wait();
         if (warp == W_PDS) TL(64 + x);
+        TW(x, 0);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.dp_free[b]);
@@ -477,6 +484,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         // P^T (bf16 pairs) over the first half of this warp's own S^T columns; dS^T into smem slot c
         if (warp == W_PDS) TL(74 + x);
         st_cols(tS + QW * cg, pp);
+        st_cols(tS + QW * cg + QW / 2, pd);  // dS^T for the dK MMA (A from TMEM); dQ reads the smem copy
         uint8_t* slot = smem + S_DS + c * TILE;
 #pragma unroll
         for (int k = 0; k < QW / 8; ++k)
@@ -489,6 +497,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (warp == W_PDS) TL(43 + x);
+        TW(x, 1);
         if (lane == 0) mbar_arrive(&sm.pds_full[b]);
       }
     }
@@ -735,6 +744,9 @@ int spatial_bwd3_launch(const void* qkv, const void* dout, const float* uvb, int
 }  // namespace jz
 
 #ifdef JZ_SPATIAL_BWD_PROF
+extern "C" int jz_attn_bwd3_tw_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, jz::g_tw, sizeof(unsigned long long) * 4 * 10 * 2 * 32) == cudaSuccess ? 0 : -3;
+}
 extern "C" int jz_attn_bwd3_prof_read(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, jz::g_tl, sizeof(unsigned long long) * 16 * 128) == cudaSuccess ? 0 : -3;
 }

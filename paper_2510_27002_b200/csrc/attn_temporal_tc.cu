@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars& bar = *reinterpret_cast<Bars*>(smem + F_END);
   const int D = H * 64;
-  const int warp = warp_id(), lane = lane_id();
+  const int warp = __shfl_sync(0xffffffffu, (int)warp_id(), 0), lane = lane_id();  // warp-uniform
   const int units = B * NG * H;
   const float c2 = 0.125f * 1.4426950408889634f;
 
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
   fence_proxy_async();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = bar.tmem_base;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, bar.tmem_base, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Bars& bar = *reinterpret_cast<Bars*>(smem + B_END);
   const int D = H * 64;
-  const int warp = warp_id(), lane = lane_id();
+  const int warp = __shfl_sync(0xffffffffu, (int)warp_id(), 0), lane = lane_id();  // warp-uniform
   const int units = B * NG * H;
   const float c2 = 0.125f * 1.4426950408889634f;
   constexpr uint32_t C_S = 0, C_DP = 128, C_DV = 256, C_DK = 320, C_DQ = 384;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
   fence_proxy_async();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = bar.tmem_base;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, bar.tmem_base, 0);
 
   if (warp == 0) {
     if (lane == 0) {

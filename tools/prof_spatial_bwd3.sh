@@ -40,6 +40,15 @@ for x in range(10):
     names[33 + x] = f"PDS blk {x} start"; names[43 + x] = f"PDS blk {x} done"
     names[64 + x] = f"PDS blk {x} loaded"; names[74 + x] = f"PDS blk {x} computed"; names[84 + x] = f"PDS blk {x} st waited"
     names[94 + x] = f"PDS blk {x} proxy fenced"
+tw = np.zeros(4 * 10 * 2 * 32, dtype=np.uint64)
+lib.jz_attn_bwd3_tw_read.argtypes = [C.c_void_p]
+assert lib.jz_attn_bwd3_tw_read(tw.ctypes.data) == 0
+tw = tw.reshape(4, 10, 2, 32).astype(np.int64)
+base = t[3, 3]
+for x in range(10):
+    ld = tw[3, x, 0, 2:18]; dn = tw[3, x, 1, 2:18]
+    if ld.min() > 0:
+        print(f"blk {x}: P/dS warps loaded {ld.min() - base}..{ld.max() - base}  done {dn.min() - base}..{dn.max() - base}  (warp order of done: {list(np.argsort(dn) + 2)})")
 for u in (3,):
     base = t[u, 3]
     print(f"unit {u}: period {t[u + 1, 3] - base} cycles (MMA block-0 issue to next unit's)")
