@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + ((LNX || DB) ? 2 : 1) * kEpiWarps);
   float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full_bar) + S::BAR_BYTES);  // [BN]
 
-  const uint32_t warp = warp_id();
+  const uint32_t warp = __shfl_sync(0xffffffffu, warp_id(), 0);  // warp-uniform (uniform-datapath MMA operands)
   const uint32_t lane = lane_id();
 #ifdef JZ_GEMM_PROF
   const int dbg_ = g_gemm_dbg;
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(gemm_threads<PAIR>(), 1)
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
   const int units = p.m_tiles * p.n_tiles * p.splits;
 
