@@ -195,6 +195,16 @@ JZ_DEV void umma_bf16_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uin
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// smem (matrix descriptor) -> TMEM copy of 128 rows x 256 bits; warp-wide, one elected lane issues
+JZ_DEV void tmem_cp_128x256b_w(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
+      "}\n" ::"r"(taddr),
+      "l"(sdesc));
+}
 JZ_DEV void umma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n"

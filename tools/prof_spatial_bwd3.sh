@@ -4,7 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 if [ "$1" != "--run" ]; then
   mkdir -p paper_2510_27002_b200/lib/dbg
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -DJZ_SPATIAL_BWD_PROF -Iinclude \
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -DJZ_SPATIAL_BWD_PROF $EXTRA -Iinclude \
     -c paper_2510_27002_b200/csrc/attn_spatial_bwd.cu -o paper_2510_27002_b200/lib/dbg/attn_spatial_bwd.o
   objs=""
   for f in paper_2510_27002_b200/lib/obj/*.o; do b=$(basename $f); [ "$b" = attn_spatial_bwd.o ] || objs="$objs $f"; done
