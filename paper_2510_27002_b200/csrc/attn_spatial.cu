@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         return ((uint64_t)dhi << 32) | (addr4 + (off >> 4) + ((lbo >> 4) << 16));
       };
       const uint32_t q4 = smem_u32(smem + F_Q) >> 4, k4 = smem_u32(smem + F_K) >> 4, v4 = smem_u32(smem + F_V) >> 4;
-      const uint32_t p4[2] = {smem_u32(smem + F_P0) >> 4, smem_u32(smem + F_P1) >> 4};
       int i = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         const uint32_t par = i & 1;
@@ -144,10 +143,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int t = 0; t < 2; ++t) {
           mbar_wait(&sm.p_full[t], par);
           tc_fence_after();
+          // O_t (cols 256t + 128 ..) += P_t V: P from TMEM (bf16 pairs over the first 128 S columns)
 #pragma unroll
           for (int ks = 0; ks < 16; ++ks)
-            umma_bf16_ss_w(tmem + 256 * t, dsc(p4[t], (ks >> 2) * TILE + (ks & 3) * 32, 16),
-                           dsc(v4, ks * 2048, 8192), idesc_o, ks > 0);
+            umma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + 8 * ks, dsc(v4, ks * 2048, 8192), idesc_o, ks > 0);
           umma_commit_w(&sm.o_full[t]);
         }
         umma_commit_w(&sm.v_free);
@@ -216,21 +215,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const float2 pr = unpack_bf16(pk[j / 2]);  // normalise with the probabilities the MMA sees
           sum += pr.x + pr.y;
         }
-        // keys 32c..32c+31 -> atom (c/2), 16B chunks (c%2)*4 .. +3
-        uint8_t* atom = pbuf + (c >> 1) * TILE;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t chunk = (c & 1) * 4 + q;
-          *reinterpret_cast<uint4*>(atom + sw128(r, chunk)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
+        // keys 32c..32c+31 -> TMEM columns 16c..16c+15 as bf16 pairs (S columns already loaded)
+        tmem_st_32x32b_x16(taddr + 16 * c, pk);
       }
       const float plast = has_tail ? ex2(s_last * c2 - mb) : 0.f;
       sum += plast;
-      fence_proxy_async();
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
-      // O epilogue: stage O (bf16 atom + two fp32 atoms) in this tile's P buffer, TMA-store it
+      // O epilogue: stage O (bf16 atom + two fp32 atoms) in this tile's staging buffer, TMA-store it
       mbar_wait(&sm.o_full[t], par);
       tc_fence_after();
       const float inv = 1.0f / sum;
@@ -240,7 +233,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(taddr + 32 * c, v);
+        tmem_ld_32x32b_x32(taddr + 128 + 32 * c, v);
         tmem_ld_wait();
         float o[32];
 #pragma unroll
