@@ -60,14 +60,20 @@ constexpr int kUvbHead = 524;    // floats loaded per unit
 constexpr int kUvbStride = 780;  // floats per unit in the workspace
 
 // TMEM columns
-constexpr uint32_t C_RA = 0, C_RB = 64, C_RC = 128;  // S^T slots A / C (alternating), dP^T slot B
-constexpr uint32_t C_DV = 192, C_DK = 256, C_DQ = 320, C_CT = 448;
+// S^T ring of three 64-column slots (block g uses slot g % 3), one dP^T slot; the gradient MMAs of
+// block g are issued two blocks later, so S^T / dP^T of the next block are computed ahead of them
+constexpr uint32_t C_RB = 64;  // dP^T slot
+constexpr uint32_t C_DV = 256, C_DK = 320, C_DQ = 384;
+JZ_DEV uint32_t sslot(uint32_t g) {
+  const uint32_t m = g % 3;
+  return m == 0 ? 0u : (m == 1 ? 128u : 192u);
+}
 
 struct Small {
   uint64_t full_a, full_b, full_c, full_d, free_a, free_b, free_cd;
-  uint64_t sdp_full[2], dp_free[2], pds_full[2];
+  uint64_t sdp_full[2], dp_free[2], pds_full[3];
   uint64_t dkdv_full, dkdv_free, dq_full[2], dq_free[2], ds_free[2];
-  uint64_t ct_full[2], ct_free, uvb_free[2], vec_ready, prow_full[2];
+  uint64_t uvb_free[2], vec_ready, prow_full[2];
   uint32_t tmem_base;
   alignas(16) float uvb[2][kUvbHead];
   alignas(16) __nv_bfloat16 vec[4][64];  // row 0 of the tail tiles: q256, do256, k256, v256
@@ -201,15 +207,14 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.sdp_full[b], 1);
       mbar_init(&sm.dp_free[b], kPds);
-      mbar_init(&sm.pds_full[b], kPds);
       mbar_init(&sm.dq_full[b], 1);
       mbar_init(&sm.dq_free[b], 4);
       mbar_init(&sm.ds_free[b], 1);
-      mbar_init(&sm.ct_full[b], 1);
       mbar_init(&sm.uvb_free[b], 1);
     }
     mbar_init(&sm.dkdv_full, 1); mbar_init(&sm.dkdv_free, 4);
-    mbar_init(&sm.ct_free, 4); mbar_init(&sm.vec_ready, 1);
+    for (int b = 0; b < 3; ++b) mbar_init(&sm.pds_full[b], kPds);
+    mbar_init(&sm.vec_ready, 1);
     mbar_init(&sm.prow_full[0], 4); mbar_init(&sm.prow_full[1], 4);
     fence_barrier_init();
   }
@@ -269,8 +274,8 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
     auto grad = [&](int i, int x) {
       int j, c;
       blk(x, tail, j, c);
-      const uint32_t g = (uint32_t)(NB * i + x), b = g & 1;
-      MBAR_WAIT(&sm.pds_full[b], (g >> 1) & 1);
+      const uint32_t g = (uint32_t)(NB * i + x);
+      MBAR_WAIT(&sm.pds_full[g % 3], (g / 3) & 1);
       tc_fence_after();
       TL(23 + x);
       if (c == 4) return;  // query-256 block: its row sums are CUDA-core work
@@ -283,20 +288,17 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         tc_fence_after();
       }
       const uint32_t qoff = (c >> 1) * TILE + (c & 1) * 8192;  // rows 64c.. of Q / dO
-      const uint32_t pcol = tmem + (b ? C_RC : C_RA);
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        // P^T / dS^T of queries 16 ks .. 16 ks + 15: written by column group 16 ks / QW, packed bf16 pairs
-        const uint32_t pa = pcol + QW * (ks / (QW / 16)) + 8 * (ks % (QW / 16));
-        umma_bf16_ts_w(tmem + C_DV, pa, dsc(ado, qoff + ks * 2048, 8192), id_kv, (c > 0 || ks > 0));
-        umma_bf16_ts_w(tmem + C_DK, pa + QW / 2, dsc(aq, qoff + ks * 2048, 8192), id_kv, (c > 0 || ks > 0));
-      }
+      const uint32_t pcol = tmem + sslot(g);
+      // P^T / dS^T of queries 16 ks .. 16 ks + 15: column group ks (QW = 16), packed bf16 pairs
+      static_assert(QW == 16, "batched gradient MMAs assume 16 query columns per P/dS warp");
+      umma4x2_bf16_ts_w(tmem + C_DV, pcol, dsc(ado, qoff, 8192), tmem + C_DK, pcol + QW / 2, dsc(aq, qoff, 8192), 16,
+                        2048 >> 4, id_kv, c > 0);
       if (c & 1) {
         const int t = c >> 1;
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          umma_bf16_ss_w(tmem + C_DQ + 64 * t, dsc(ads, 2 * t * TILE + ks * 2048, TILE),
-                         dsc(ak, j * TILE + ks * 2048, 8192), id_q, (j > 0 || ks > 0));
+        umma4_bf16_ss_w(tmem + C_DQ + 64 * t, dsc(ads, 2 * t * TILE, TILE), dsc(ak, j * TILE, 8192), 2048 >> 4,
+                        2048 >> 4, id_q, j > 0);
+        umma4_bf16_ss_w(tmem + C_DQ + 64 * t, dsc(ads, 2 * t * TILE + 4 * 2048, TILE),
+                        dsc(ak, j * TILE + 4 * 2048, 8192), 2048 >> 4, 2048 >> 4, id_q, 1);
         umma_commit_w(&sm.ds_free[t]);
       }
       if (c == 3) umma_commit_w(&sm.dkdv_full);
@@ -310,23 +312,12 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         umma_commit_w(&sm.dq_full[1]);
       }
     };
-    // key 256 against query tile t: D1 = Q_t K4^T, D2 = dO_t V4^T (N = 16, column 0 is key 256)
-    auto col_tail = [&](int t) {
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        umma_bf16_ss_w(tmem + C_CT + 32 * t, dsc(aq, t * TILE + kk * 32, 16), dsc(at, T_K * 2048 + kk * 32, 16),
-                       id_s16, kk > 0);
-        umma_bf16_ss_w(tmem + C_CT + 32 * t + 16, dsc(ado, t * TILE + kk * 32, 16),
-                       dsc(at, T_V * 2048 + kk * 32, 16), id_s16, kk > 0);
-      }
-      umma_commit_w(&sm.ct_full[t]);
-    };
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       MBAR_WAIT(&sm.full_a, i & 1);
       MBAR_WAIT(&sm.full_b, i & 1);
       tc_fence_after();
-      bool wc = false, wd = false, ct1 = !tail;
+      bool wc = false, wd = false;
       for (int x = 0; x < NB; ++x) {
         int j, c;
         blk(x, tail, j, c);
@@ -341,44 +332,28 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
           wd = true;
           tc_fence_after();
         }
-        const uint32_t dS = tmem + (b ? C_RC : C_RA), dP = tmem + C_RB;
+        const uint32_t dS = tmem + sslot(g), dP = tmem + C_RB;
         TL(3 + x);
-        // S^T: the slot's previous P^T was read by grad(g - 2), issued earlier by this warp (in-order pipe)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          if (c == 4)
-            umma_bf16_ss_w(dS, dsc(ak, j * TILE + kk * 32, 16), dsc(at, T_Q * 2048 + kk * 32, 16), id_s16, kk > 0);
-          else
-            umma_bf16_ss_w(dS, dsc(ak, j * TILE + kk * 32, 16),
-                           dsc(aq, (c >> 1) * TILE + (c & 1) * 8192 + kk * 32, 16), id_s, kk > 0);
-        }
+        // S^T: the slot's previous P^T (block g - 3) was read by grad(g - 3), issued earlier by this
+        // warp (in-order pipe)
+        if (c == 4)
+          umma4_bf16_ss_w(dS, dsc(ak, j * TILE, 16), dsc(at, T_Q * 2048, 16), 2, 2, id_s16, 0);
+        else
+          umma4_bf16_ss_w(dS, dsc(ak, j * TILE, 16), dsc(aq, (c >> 1) * TILE + (c & 1) * 8192, 16), 2, 2, id_s, 0);
         if (g > 0) {  // dP^T slot: the P/dS warps have loaded block g - 1
           MBAR_WAIT(&sm.dp_free[(g - 1) & 1], ((g - 1) >> 1) & 1);
           tc_fence_after();
         }
         TL(13 + x);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          if (c == 4)
-            umma_bf16_ss_w(dP, dsc(av, j * TILE + kk * 32, 16), dsc(at, T_DO * 2048 + kk * 32, 16), id_s16, kk > 0);
-          else
-            umma_bf16_ss_w(dP, dsc(av, j * TILE + kk * 32, 16),
-                           dsc(ado, (c >> 1) * TILE + (c & 1) * 8192 + kk * 32, 16), id_s, kk > 0);
-        }
+        if (c == 4)
+          umma4_bf16_ss_w(dP, dsc(av, j * TILE, 16), dsc(at, T_DO * 2048, 16), 2, 2, id_s16, 0);
+        else
+          umma4_bf16_ss_w(dP, dsc(av, j * TILE, 16), dsc(ado, (c >> 1) * TILE + (c & 1) * 8192, 16), 2, 2, id_s, 0);
         umma_commit_w(&sm.sdp_full[b]);
-        if (tail && x == 0) {
-          if (i > 0) {
-            MBAR_WAIT(&sm.ct_free, (i - 1) & 1);
-            tc_fence_after();
-          }
-          col_tail(0);
-        }
-        if (!ct1 && wc) {
-          col_tail(1);
-          ct1 = true;
-        }
-        if (x > 0) grad(i, x - 1);
+        if (x >= 2) grad(i, x - 2);  // two blocks behind: S^T / dP^T of block x run ahead of them
       }
+      // unit end: the last two blocks' gradients (their commits release the next unit's inputs)
+      grad(i, NB - 2);
       grad(i, NB - 1);
     }
   } else if (warp < W_HELP) {
@@ -396,7 +371,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         int j, c;
         blk(x, tail, j, c);
         const uint32_t g = (uint32_t)(NB * i + x), b = g & 1;
-        const uint32_t tS = lbase + (b ? C_RC : C_RA), tP = lbase + C_RB;
+        const uint32_t tS = lbase + sslot(g), tP = lbase + C_RB;
         if (c < 4 && (c & 1) == 0 && 2 * i + j > 0) MBAR_WAIT(&sm.ds_free[c >> 1], (2 * i + j - 1) & 1);
         MBAR_WAIT(&sm.sdp_full[b], (g >> 1) & 1);
         tc_fence_after();
@@ -452,7 +427,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
           }
           __syncwarp();
           if (warp == W_PDS) TL(43 + x);
-          if (lane == 0) mbar_arrive(&sm.pds_full[b]);
+          if (lane == 0) mbar_arrive(&sm.pds_full[g % 3]);
           continue;
         }
         uint32_t vs[QW], vd[QW];
@@ -498,7 +473,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         __syncwarp();
         if (warp == W_PDS) TL(43 + x);
         TW(x, 1);
-        if (lane == 0) mbar_arrive(&sm.pds_full[b]);
+        if (lane == 0) mbar_arrive(&sm.pds_full[g % 3]);
       }
     }
   } else {
@@ -587,18 +562,33 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
           if (lane == 0) mbar_arrive(&sm.vec_ready);
         }
         MBAR_WAIT(&sm.vec_ready, i & 1);
-        // key 256 against the queries of both tiles (this thread: queries r and 128 + r)
-        MBAR_WAIT(&sm.ct_full[0], i & 1);
-        MBAR_WAIT(&sm.ct_full[1], i & 1);
-        tc_fence_after();
-        const float s0 = __uint_as_float(tmem_ld_32x32b_x1(lbase + C_CT));
-        const float d0 = __uint_as_float(tmem_ld_32x32b_x1(lbase + C_CT + 16));
-        const float s1 = __uint_as_float(tmem_ld_32x32b_x1(lbase + C_CT + 32));
-        const float d1 = __uint_as_float(tmem_ld_32x32b_x1(lbase + C_CT + 48));
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.ct_free);
+        // key 256 against the queries of both tiles (this thread: queries r and 128 + r): s = q . k256,
+        // dp = dO . v256 from the staged Q / dO rows (these tiles are read below anyway)
+        MBAR_WAIT(&sm.full_b, i & 1);
+        MBAR_WAIT(&sm.full_c, i & 1);
+        float s0 = 0.f, d0 = 0.f, s1 = 0.f, d1 = 0.f;
+#pragma unroll 2
+        for (int cc = 0; cc < 8; ++cc) {
+          const uint4 kw = *reinterpret_cast<const uint4*>(&sm.vec[T_K][8 * cc]);
+          const uint4 vw = *reinterpret_cast<const uint4*>(&sm.vec[T_V][8 * cc]);
+          const uint4 q0 = *reinterpret_cast<const uint4*>(smem + S_Q + sw128(r, cc));
+          const uint4 q1 = *reinterpret_cast<const uint4*>(smem + S_Q + TILE + sw128(r, cc));
+          const uint4 g0 = *reinterpret_cast<const uint4*>(smem + S_DO + sw128(r, cc));
+          const uint4 g1 = *reinterpret_cast<const uint4*>(smem + S_DO + TILE + sw128(r, cc));
+          const uint32_t ka[4] = {kw.x, kw.y, kw.z, kw.w}, va[4] = {vw.x, vw.y, vw.z, vw.w};
+          const uint32_t qa[4] = {q0.x, q0.y, q0.z, q0.w}, qb[4] = {q1.x, q1.y, q1.z, q1.w};
+          const uint32_t ga[4] = {g0.x, g0.y, g0.z, g0.w}, gb[4] = {g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 kf = unpack_bf16(ka[e]), vf = unpack_bf16(va[e]);
+            const float2 x0 = unpack_bf16(qa[e]), x1 = unpack_bf16(qb[e]);
+            const float2 y0 = unpack_bf16(ga[e]), y1 = unpack_bf16(gb[e]);
+            s0 += x0.x * kf.x + x0.y * kf.y;
+            s1 += x1.x * kf.x + x1.y * kf.y;
+            d0 += y0.x * vf.x + y0.y * vf.y;
+            d1 += y1.x * vf.x + y1.y * vf.y;
+          }
+        }
         const float p0 = ex2(s0 * c2 - uv[U_LSE2 + r]);
         const float p1 = ex2(s1 * c2 - uv[U_LSE2 + 128 + r]);
         dsc0 = p0 * (d0 - uv[U_DV + r]);

@@ -195,6 +195,53 @@ JZ_DEV void umma_bf16_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uin
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// Four K-steps into one accumulator (K-major A and B advanced by `astep` / `bstep` descriptor units
+// per step) from one elected lane: the first step overwrites when `acc0` is 0.
+JZ_DEV void umma4_bf16_ss_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t astep, uint32_t bstep,
+                            uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "add.s64 a1, %1, %3; add.s64 a2, a1, %3; add.s64 a3, a2, %3;\n"
+      "add.s64 b1, %2, %4; add.s64 b2, b1, %4; add.s64 b3, b2, %4;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %5, 1;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "l"((uint64_t)astep), "l"((uint64_t)bstep), "r"(idesc), "r"(acc0));
+}
+
+// Two accumulators, four K-steps each, interleaved, A from TMEM (columns advanced by `atstep`),
+// B from shared memory (descriptor advanced by `bstep`): D0 += A0 B0, D1 += A1 B1 step by step.
+JZ_DEV void umma4x2_bf16_ts_w(uint32_t d0, uint32_t a0, uint64_t b0, uint32_t d1, uint32_t a1, uint64_t b1,
+                              uint32_t atstep, uint32_t bstep, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 x1, x2, x3, y1, y2, y3;\n"
+      ".reg .b64 u1, u2, u3, v1, v2, v3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %9, 0;\n"
+      "add.u32 x1, %1, %6; add.u32 x2, x1, %6; add.u32 x3, x2, %6;\n"
+      "add.u32 y1, %4, %6; add.u32 y2, y1, %6; add.u32 y3, y2, %6;\n"
+      "add.s64 u1, %2, %7; add.s64 u2, u1, %7; add.s64 u3, u2, %7;\n"
+      "add.s64 v1, %5, %7; add.s64 v2, v1, %7; add.s64 v3, v2, %7;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %8, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], [%4], %5, %8, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x1], u1, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], [y1], v1, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x2], u2, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], [y2], v2, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x3], u3, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], [y3], v3, %8, 1;\n"
+      "}\n" ::"r"(d0),
+      "r"(a0), "l"(b0), "r"(d1), "r"(a1), "l"(b1), "r"(atstep), "l"((uint64_t)bstep), "r"(idesc), "r"(acc0));
+}
+
 // smem (matrix descriptor) -> TMEM copy of 128 rows x 256 bits; warp-wide, one elected lane issues
 JZ_DEV void tmem_cp_128x256b_w(uint32_t taddr, uint64_t sdesc) {
   asm volatile(
