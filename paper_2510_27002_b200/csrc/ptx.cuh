@@ -215,6 +215,26 @@ JZ_DEV void umma4_bf16_ss_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uin
       "l"(adesc), "l"(bdesc), "l"((uint64_t)astep), "l"((uint64_t)bstep), "r"(idesc), "r"(acc0));
 }
 
+// Four K-steps into one accumulator, A from TMEM (columns advanced by `atstep`), B from shared memory.
+JZ_DEV void umma4_bf16_ts_w(uint32_t tmem_d, uint32_t a0, uint64_t bdesc, uint32_t atstep, uint32_t bstep,
+                            uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 x1, x2, x3;\n"
+      ".reg .b64 u1, u2, u3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "add.u32 x1, %1, %3; add.u32 x2, x1, %3; add.u32 x3, x2, %3;\n"
+      "add.s64 u1, %2, %4; add.s64 u2, u1, %4; add.s64 u3, u2, %4;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x1], u1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x2], u2, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x3], u3, %5, 1;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(a0), "l"(bdesc), "r"(atstep), "l"((uint64_t)bstep), "r"(idesc), "r"(acc0));
+}
+
 // Two accumulators, four K-steps each, interleaved, A from TMEM (columns advanced by `atstep`),
 // B from shared memory (descriptor advanced by `bstep`): D0 += A0 B0, D1 += A1 B1 step by step.
 JZ_DEV void umma4x2_bf16_ts_w(uint32_t d0, uint32_t a0, uint64_t b0, uint32_t d1, uint32_t a1, uint64_t b1,
