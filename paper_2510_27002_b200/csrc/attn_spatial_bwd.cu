@@ -243,6 +243,14 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
           tma_load_2d(smem + S_TAIL + T_K * 2048, &tm_qkv16, &sm.full_a, D + h * 64, row0 + 256);
           tma_load_2d(smem + S_TAIL + T_V * 2048, &tm_qkv16, &sm.full_a, 2 * D + h * 64, row0 + 256);
         }
+        // the rest of this unit's tiles are loaded once the previous unit releases them (late in that
+        // unit): pull them into L2 now so those loads are L2 hits
+        tma_prefetch_2d(&tm_qkv, h * 64, row0);
+        tma_prefetch_2d(&tm_do, h * 64, row0);
+        tma_prefetch_2d(&tm_qkv, h * 64, row0 + 128);
+        tma_prefetch_2d(&tm_do, h * 64, row0 + 128);
+        tma_prefetch_2d(&tm_qkv, D + h * 64, row0 + 128);
+        tma_prefetch_2d(&tm_qkv, 2 * D + h * 64, row0 + 128);
         if (i > 0) MBAR_WAIT(&sm.free_b, (i - 1) & 1);
         TL(1);
         mbar_arrive_expect_tx(&sm.full_b, 2 * TILE);
@@ -486,7 +494,10 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
     uint8_t* stg = smem + S_STG + hw * 4096;
     // TMEM row block (64 fp32 columns) -> sc * (acc + coef * vec) -> bf16 -> this warp's staging
     // rows (128B swizzle) -> TMA store; plus the column sums of the 32 rows (QKV bias gradient)
-    auto epi = [&](uint32_t col, float coef, const __nv_bfloat16* vec, float sc, int gcol, int64_t grow, float* part) {
+    // zero_sum: the columns sum to exactly 0 over the frame (dK: every dS row sums to 0), so the
+    // partial row is written as 0 without reading the tile back
+    auto epi = [&](uint32_t col, float coef, const __nv_bfloat16* vec, float sc, int gcol, int64_t grow, float* part,
+                   bool zero_sum = false) {
       if (lane == 0) bulk_wait_read0();
       __syncwarp();
 #pragma unroll
@@ -513,7 +524,13 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
         tma_store_2d(&tm_dq, stg, gcol, (int)grow);
         bulk_commit();
       }
-      if (part != nullptr) {
+      if (part != nullptr && zero_sum) {
+        if (lane < 8) {
+          float4* dst = reinterpret_cast<float4*>(part + gcol + 8 * lane);
+          dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+          dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else if (part != nullptr) {
         const int cch = lane & 7;
         float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -633,7 +650,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
       tc_fence_after();
       if (hw == 0) TL(55);
       epi(C_DV, tail ? sm.p_row[r] : 0.f, do256, 1.f, 2 * D + h * 64, rw, part0);
-      epi(C_DK, tail ? sm.ds_row[r] : 0.f, q256, scale, D + h * 64, rw, part0);
+      epi(C_DK, tail ? sm.ds_row[r] : 0.f, q256, scale, D + h * 64, rw, part0, true);
       if (hw == 0) TL(56);
       tc_fence_before();
       __syncwarp();
@@ -653,7 +670,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
       tc_fence_after();
       if (hw == 0) TL(59);
       epi(C_DV, tail ? sm.p_row[128 + r] : 0.f, do256, 1.f, 2 * D + h * 64, rw + 128, part1);
-      epi(C_DK, tail ? sm.ds_row[128 + r] : 0.f, q256, scale, D + h * 64, rw + 128, part1);
+      epi(C_DK, tail ? sm.ds_row[128 + r] : 0.f, q256, scale, D + h * 64, rw + 128, part1, true);
       if (hw == 0) TL(60);
       tc_fence_before();
       __syncwarp();
@@ -684,7 +701,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
           dqkv[(row0 + 256) * ld3 + D + h * 64 + d] = bk;
           dqkv[(row0 + 256) * ld3 + 2 * D + h * 64 + d] = bv;
           if (pr) {
-            pr[D] = __bfloat162float(bk);
+            pr[D] = 0.f;  // the k-bias gradient is exactly 0 (see epi's zero_sum)
             pr[2 * D] = __bfloat162float(bv);
           }
         } else if (pr) {  // S = 256: no token 256, its partial row is zero

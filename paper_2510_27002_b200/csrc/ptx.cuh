@@ -104,6 +104,13 @@ JZ_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_
       : "memory");
 }
 
+// L2 prefetch of a 2-D tensor-map box (no shared-memory destination, no barrier)
+JZ_DEV void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 JZ_DEV void tma_store_4d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),

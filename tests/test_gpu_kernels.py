@@ -214,7 +214,11 @@ def test_attn_spatial_fwd_bwd(S, frames):
     assert torch.isfinite(dqkv.float()).all()
     cs_ref = torch.empty_like(cs)
     Kn.colsum_bf16(dqkv, cs_ref)  # fused bias-gradient column sums == a pass over the written dqkv
-    assert rel(cs, cs_ref) < 1e-5
+    # q / v: the column sums of the written dq / dv; k: exactly 0 (every dS row sums to 0 over the
+    # S keys, so a bias shared by all keys has no gradient), the summed written dk is rounding noise
+    assert rel(cs[:D], cs_ref[:D]) < 1e-5 and rel(cs[2 * D:], cs_ref[2 * D:]) < 1e-5
+    assert float(cs[D:2 * D].abs().max()) == 0.0
+    assert float(cs_ref[D:2 * D].norm()) < 1e-2 * float(cs_ref[2 * D:].norm()) + 1e-3
     for i in range(3):
         got, ref = dqkv[:, i * D:(i + 1) * D], qf.grad[:, i * D:(i + 1) * D]
         assert rel(got, ref) < 2e-2, "qkv"[i]
