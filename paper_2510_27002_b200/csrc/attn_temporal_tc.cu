@@ -198,16 +198,14 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
       mbar_wait(&bar.full[st], (i / kFStages) & 1);
       mbar_wait(&bar.d[buf], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16_ss_w(tmem + 128 * buf, dsc(q4, kk * 32, 16), dsc(k4, kk * 32, 16), id_s, kk > 0);
+      umma4_bf16_ss_w(tmem + 128 * buf, dsc(q4, 0, 16), dsc(k4, 0, 16), 2, 2, id_s, 0);
       umma_commit_w(&bar.a[buf]);
       mbar_wait(&bar.b, i & 1);
       tc_fence_after();
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-        umma_bf16_ss_w(tmem + 256 + 64 * buf, dsc(p4, (ks >> 2) * TILE + (ks & 3) * 32, 16), dsc(v4, ks * 2048, 8192),
-                       id_o, ks > 0);
+      for (int hk = 0; hk < 2; ++hk)
+        umma4_bf16_ss_w(tmem + 256 + 64 * buf, dsc(p4, hk * TILE, 16), dsc(v4, hk * 4 * 2048, 8192), 2, 2048 >> 4, id_o,
+                        hk);
       umma_commit_w(&bar.c[buf]);
       umma_commit_w(&bar.empty[st]);
     }
@@ -354,23 +352,19 @@ __global__ void __launch_bounds__(ttc::kThreads, 1)
       mbar_wait(&bar.full[st], (i / kBStages) & 1);
       tc_fence_after();
       // S / dP columns are free: this thread already waited on b for the previous unit
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        umma_bf16_ss_w(tmem + C_S, dsc(q4, kk * 32, 16), dsc(k4, kk * 32, 16), id_s, kk > 0);
-        umma_bf16_ss_w(tmem + C_DP, dsc(do4, kk * 32, 16), dsc(v4, kk * 32, 16), id_s, kk > 0);
-      }
+      umma4x2_bf16_ss_w(tmem + C_S, dsc(q4, 0, 16), dsc(k4, 0, 16), tmem + C_DP, dsc(do4, 0, 16), dsc(v4, 0, 16), 2, 2,
+                        id_s, 0);
       umma_commit_w(&bar.a[0]);
       mbar_wait(&bar.b, i & 1);                // P / dS staged (S / dP read)
       mbar_wait(&bar.d[0], (i & 1) ^ 1);       // the previous unit's gradients left TMEM
       tc_fence_after();
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
+      for (int hk = 0; hk < 2; ++hk) {
         // contraction over queries (16 rows = 2048 bytes per step); P^T / dS^T are MN-major reads
-        umma_bf16_ss_w(tmem + C_DV, dsc(p4, ks * 2048, TILE), dsc(do4, ks * 2048, 8192), id_t, ks > 0);
-        umma_bf16_ss_w(tmem + C_DK, dsc(ds4, ks * 2048, TILE), dsc(q4, ks * 2048, 8192), id_t, ks > 0);
-        // contraction over keys: dS K-major (atom ks / 4), K rows MN-major
-        umma_bf16_ss_w(tmem + C_DQ, dsc(ds4, (ks >> 2) * TILE + (ks & 3) * 32, 16), dsc(k4, ks * 2048, 8192), id_q,
-                       ks > 0);
+        umma4x2_bf16_ss_w(tmem + C_DV, dsc(p4, hk * 4 * 2048, TILE), dsc(do4, hk * 4 * 2048, 8192), tmem + C_DK,
+                          dsc(ds4, hk * 4 * 2048, TILE), dsc(q4, hk * 4 * 2048, 8192), 2048 >> 4, 2048 >> 4, id_t, hk);
+        // contraction over keys: dS K-major (atom hk), K rows MN-major
+        umma4_bf16_ss_w(tmem + C_DQ, dsc(ds4, hk * TILE, 16), dsc(k4, hk * 4 * 2048, 8192), 2, 2048 >> 4, id_q, hk);
       }
       umma_commit_w(&bar.c[0]);
       umma_commit_w(&bar.empty[st]);

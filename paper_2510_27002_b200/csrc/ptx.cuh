@@ -222,6 +222,33 @@ JZ_DEV void umma4_bf16_ss_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uin
       "l"(adesc), "l"(bdesc), "l"((uint64_t)astep), "l"((uint64_t)bstep), "r"(idesc), "r"(acc0));
 }
 
+// Two accumulators, four K-steps each, interleaved, both operands from shared memory (descriptors
+// advanced by `astep` / `bstep` units per step): D0 += A0 B0, D1 += A1 B1.
+JZ_DEV void umma4x2_bf16_ss_w(uint32_t d0, uint64_t a0, uint64_t b0, uint32_t d1, uint64_t a1, uint64_t b1,
+                              uint32_t astep, uint32_t bstep, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b64 x1, x2, x3, y1, y2, y3, u1, u2, u3, v1, v2, v3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %9, 0;\n"
+      "add.s64 x1, %1, %6; add.s64 x2, x1, %6; add.s64 x3, x2, %6;\n"
+      "add.s64 y1, %4, %6; add.s64 y2, y1, %6; add.s64 y3, y2, %6;\n"
+      "add.s64 u1, %2, %7; add.s64 u2, u1, %7; add.s64 u3, u2, %7;\n"
+      "add.s64 v1, %5, %7; add.s64 v2, v1, %7; add.s64 v3, v2, %7;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %8, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], %4, %5, %8, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x1, u1, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], y1, v1, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x2, u2, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], y2, v2, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x3, u3, %8, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%3], y3, v3, %8, 1;\n"
+      "}\n" ::"r"(d0),
+      "l"(a0), "l"(b0), "r"(d1), "l"(a1), "l"(b1), "l"((uint64_t)astep), "l"((uint64_t)bstep), "r"(idesc),
+      "r"(acc0));
+}
+
 // Four K-steps into one accumulator, A from TMEM (columns advanced by `atstep`), B from shared memory.
 JZ_DEV void umma4_bf16_ts_w(uint32_t tmem_d, uint32_t a0, uint64_t bdesc, uint32_t atstep, uint32_t bstep,
                             uint32_t idesc, uint32_t acc0) {
