@@ -14,7 +14,8 @@ from pathlib import Path
 
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libjz.so"
+# JZ_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("JZ_LIB_PATH") or Path(__file__).resolve().parent / "lib" / "libjz.so")
 
 JZ_OK, JZ_EINVAL, JZ_EINDEX, JZ_ECUDA, JZ_EUNSUPPORTED, JZ_ENONFINITE = 0, -1, -2, -3, -4, -5
 
