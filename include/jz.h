@@ -243,22 +243,24 @@ JZ_API int jz_dyn_embed_bwd(const float* dx, const int64_t* tokens, const uint8_
 /* ------------------------------------------------------------------------
  * K3  spatial (intra-frame) attention, tcgen05/TMEM + TMA (st.py:73,
  * nn.py:80-110, causal=False).  qkv bf16 [frames*S, 3*H*64] (q|k|v, head h =
- * cols 64h..), out bf16 [frames*S, H*64], out_f32 (optional, may be NULL) the
- * same in fp32, lse f32 [frames, H, S] (natural-log softmax normaliser).
+ * cols 64h..), out bf16 [frames*S, H*64], out_lo (optional, may be NULL) bf16 the
+ * rounding residual O - bf16(O) of the fp32 output (out + out_lo carries O to ~16
+ * mantissa bits for the backward's Delta), lse f32 [frames, H, S] (natural-log softmax
+ * normaliser).
  * S in {256, 257}, head_dim 64.
  * ---------------------------------------------------------------------- */
 JZ_API int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
-                               float* out_f32, float* lse, jz_stream_t stream);
-/* dqkv bf16 [frames*S, 3*H*64] (fully overwritten).  out_f32 is the forward's fp32
- * output: Delta_i = dO_i . O_i is formed from it (first launch, into per-(frame, head)
- * vector blocks in `workspace`, with lse and the token-256 vectors) so
+                               void* out_lo, float* lse, jz_stream_t stream);
+/* dqkv bf16 [frames*S, 3*H*64] (fully overwritten).  out / out_lo are the forward's output
+ * and residual: Delta_i = dO_i . (out + out_lo)_i is formed from them (first launch, into
+ * per-(frame, head) vector blocks in `workspace`, with lse and the token-256 vectors) so
  * dP - Delta does not cancel against the bf16 rounding of O.  workspace: caller-owned,
  * jz_attn_spatial_bwd_workspace_bytes(frames, S, H) bytes, 16-byte aligned. */
 JZ_API int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, int H);
 /* colsum_part (nullable): fp32 [jz_attn_spatial_colsum_parts(frames)][3*H*64] partial column sums
  * of dqkv (the QKV bias gradient after jz_reduce_partials), written instead of re-reading dqkv. */
 JZ_API int64_t jz_attn_spatial_colsum_parts(int64_t frames);
-JZ_API int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
+JZ_API int jz_attn_spatial_bwd(const void* qkv, const void* out, const void* out_lo, const void* dout, const float* lse,
                                int64_t frames, int S, int H, int head_dim, void* dqkv, void* workspace,
                                float* colsum_part, jz_stream_t stream);
 

@@ -59,7 +59,7 @@ PROTOTYPES: dict[str, list] = {
     "jz_dyn_embed_bwd": [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I32,
                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "jz_attn_spatial_fwd": [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],
-    "jz_attn_spatial_bwd": [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],
+    "jz_attn_spatial_bwd": [_P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P],
     "jz_attn_spatial_colsum_parts": [_I64],
     "jz_attn_temporal_colsum_parts": [_I64, _I32],
     "jz_attn_temporal_colsum_parts_t": [_I64, _I32, _I32, _I32],

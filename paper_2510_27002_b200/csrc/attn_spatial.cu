@@ -61,9 +61,9 @@ using namespace sp;
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
     spatial_fwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_row,
-                       const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_o32,
+                       const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_olo,
                        const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
-                       float* __restrict__ out_f32, float* __restrict__ lse, int frames, int S, int H) {
+                       __nv_bfloat16* __restrict__ out_lo, float* __restrict__ lse, int frames, int S, int H) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   FwdSmallSmem& sm = *reinterpret_cast<FwdSmallSmem*>(smem + F_END);
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tma_prefetch_desc(&tm);
     tma_prefetch_desc(&tm_row);
     tma_prefetch_desc(&tm_o);
-    if (out_f32) tma_prefetch_desc(&tm_o32);
+    if (out_lo) tma_prefetch_desc(&tm_olo);
   }
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.qk_full, 1); mbar_init(&sm.v_full, 1);
@@ -223,13 +223,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
-      // O epilogue: stage O (bf16 atom + two fp32 atoms) in this tile's staging buffer, TMA-store it
+      // O epilogue: stage O (bf16) and, for the backward's Delta, its rounding residual O - bf16(O)
+      // (bf16: O to ~16 bits) in this tile's staging buffer, TMA-store both
       mbar_wait(&sm.o_full[t], par);
       tc_fence_after();
       const float inv = 1.0f / sum;
       const uint8_t* vrow = sm.vrow;
       uint8_t* o16 = pbuf;             // [128 rows][64 bf16], 128B swizzle
-      uint8_t* o32 = pbuf + TILE;      // two [128 rows][32 f32] atoms
+      uint8_t* olo = pbuf + TILE;      // [128 rows][64 bf16] residual
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
@@ -248,11 +249,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           *reinterpret_cast<uint4*>(o16 + sw128(r, 4 * c + q)) =
               make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
                          pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
-        if (out_f32) {
+        if (out_lo) {
+          uint32_t lo[16];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(o32 + c * TILE + sw128(r, q)) =
-                make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          for (int e = 0; e < 16; ++e) {
+            const float2 hi = unpack_bf16(pack_bf16(o[2 * e], o[2 * e + 1]));
+            lo[e] = pack_bf16(o[2 * e] - hi.x, o[2 * e + 1] - hi.y);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(olo + sw128(r, 4 * c + q)) = make_uint4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
         }
       }
       mbar_arrive(&sm.v_free);  // done with value row 256
@@ -260,10 +266,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       named_bar(1 + t, 128);
       if (wtid == 0) {
         tma_store_2d(&tm_o, o16, h * 64, (int)(row0 + 128 * t));
-        if (out_f32) {
-          tma_store_2d(&tm_o32, o32, h * 64, (int)(row0 + 128 * t));
-          tma_store_2d(&tm_o32, o32 + TILE, h * 64 + 32, (int)(row0 + 128 * t));
-        }
+        if (out_lo) tma_store_2d(&tm_olo, olo, h * 64, (int)(row0 + 128 * t));
         bulk_commit();
       }
       lse[((int64_t)f * H + h) * S + 128 * t + r] = mx * 0.125f + logf(sum);
@@ -372,7 +375,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         o0 /= sum;
         o1 /= sum;
         *reinterpret_cast<uint32_t*>(out + (row0 + 256) * D + h * 64 + 2 * dpair) = pack_bf16(o0, o1);
-        if (out_f32) *reinterpret_cast<float2*>(out_f32 + (row0 + 256) * D + h * 64 + 2 * dpair) = make_float2(o0, o1);
+        if (out_lo) {
+          const float2 hi = unpack_bf16(pack_bf16(o0, o1));
+          *reinterpret_cast<uint32_t*>(out_lo + (row0 + 256) * D + h * 64 + 2 * dpair) = pack_bf16(o0 - hi.x, o1 - hi.y);
+        }
         if (tid == 0) lse[((int64_t)f * H + h) * S + 256] = mx * 0.125f + logf(sum);
       }
       named_bar(3, kFwdTailThreads);
@@ -391,17 +397,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 using namespace jz;
 
 extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H, int head_dim, void* out,
-                                   float* out_f32, float* lse, jz_stream_t s) {
+                                   void* out_lo, float* lse, jz_stream_t s) {
   JZ_CHECK_ARG(head_dim == 64, "spatial attention: head_dim %d unsupported (64)", head_dim);
   JZ_CHECK_ARG(S == 256 || S == 257, "spatial attention: sequence length %d unsupported (256 or 257)", S);
   JZ_CHECK_ARG(frames >= 1 && frames * H < (1ll << 31), "spatial attention: frames");
   const int D = H * 64;
-  CUtensorMap tm, tm_row, tm_o, tm_o32;
+  CUtensorMap tm, tm_row, tm_o, tm_olo;
   int rc = make_tmap_2d_bf16(&tm, qkv, 3 * D, frames * S, 3 * D, 64, 128);
   if (!rc) rc = make_tmap_2d(&tm_row, qkv, 2, 3 * D, frames * S, 3 * D, 64, 1, /*swizzle128=*/false);
   if (!rc) rc = make_tmap_2d_bf16(&tm_o, out, D, frames * S, D, 64, 128);
-  if (!rc && out_f32) rc = make_tmap_2d(&tm_o32, out_f32, 4, D, frames * S, D, 32, 128);
-  if (!out_f32) tm_o32 = tm_o;
+  if (!rc && out_lo) rc = make_tmap_2d_bf16(&tm_olo, out_lo, D, frames * S, D, 64, 128);
+  if (!out_lo) tm_olo = tm_o;
   if (rc) return rc;
   static bool attr_done = false;
   if (!attr_done) {
@@ -411,8 +417,8 @@ extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H
   const int64_t units = frames * H;
   const int grid = (int)(units < num_sms() ? units : num_sms());
   spatial_fwd_kernel<<<grid, kFwdThreads, F_SMEM, reinterpret_cast<cudaStream_t>(s)>>>(
-      tm, tm_row, tm_o, tm_o32, reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out),
-      out_f32, lse, (int)frames, S, H);
+      tm, tm_row, tm_o, tm_olo, reinterpret_cast<const __nv_bfloat16*>(qkv), reinterpret_cast<__nv_bfloat16*>(out),
+      reinterpret_cast<__nv_bfloat16*>(out_lo), lse, (int)frames, S, H);
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
@@ -921,7 +927,7 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
 
 
 // Per-unit vector blocks for the backward (layout sp::U_*): Delta_i = rowsum(dO_i o O_i) per head (dO
-// the bf16 tensor the MMAs consume, O the forward's fp32 copy), lse_i * log2(e) for every row, and for
+// the bf16 tensor the MMAs consume, O = the forward's bf16 output + its bf16 rounding residual), lse_i * log2(e) for every row, and for
 // token 256 its q, k, v, dO vectors (fp32) and the (256, 256) entry p = exp(q.k / 8 - lse),
 // dS = p (dO.v - Delta).  CTA (frame f, chunk c) owns rows [64 c, 64 c + 64) of the frame, so a
 // launch has frames * ceil(S / 64) CTAs (one CTA per frame walking 257 rows was latency-bound at small
@@ -929,7 +935,8 @@ __global__ void __launch_bounds__(sp::kBwdThreads2, 1)
 constexpr int kUvbMaxH = 16;
 constexpr int kUvbRows = 64;
 template <int NC>  // D / 128 column chunks per lane
-__global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const float* __restrict__ out,
+__global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const __nv_bfloat16* __restrict__ out,
+                                                               const __nv_bfloat16* __restrict__ out_lo,
                                                                const __nv_bfloat16* __restrict__ dout,
                                                                const __nv_bfloat16* __restrict__ qkv,
                                                                const float* __restrict__ lse, int64_t frames, int S,
@@ -957,10 +964,12 @@ __global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const float* __re
       for (int c = 0; c < NC; ++c) {
         {
           const int col = 128 * c + 4 * lane;
-          const float4 ov = __ldg(reinterpret_cast<const float4*>(out + row * D + col));
+          const uint2 hv = __ldg(reinterpret_cast<const uint2*>(out + row * D + col));
+          const uint2 lv = __ldg(reinterpret_cast<const uint2*>(out_lo + row * D + col));
           const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dout + row * D + col));
+          const float2 h0 = unpack_bf16(hv.x), h1 = unpack_bf16(hv.y), l0 = unpack_bf16(lv.x), l1 = unpack_bf16(lv.y);
           const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
-          acc[k][c] = ov.x * g0.x + ov.y * g0.y + ov.z * g1.x + ov.w * g1.y;
+          acc[k][c] = (h0.x + l0.x) * g0.x + (h0.y + l0.y) * g0.y + (h1.x + l1.x) * g1.x + (h1.y + l1.y) * g1.y;
         }
       }
     }
@@ -1032,7 +1041,7 @@ extern "C" int64_t jz_attn_spatial_bwd_workspace_bytes(int64_t frames, int S, in
 
 extern "C" int64_t jz_attn_spatial_colsum_parts(int64_t frames) { return frames * 9; }
 
-extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const void* dout, const float* lse,
+extern "C" int jz_attn_spatial_bwd(const void* qkv, const void* out, const void* out_lo, const void* dout, const float* lse,
                                    int64_t frames, int S, int H, int head_dim, void* dqkv, void* workspace,
                                    float* colsum_part, jz_stream_t s) {
   using namespace jz;
@@ -1052,18 +1061,21 @@ extern "C" int jz_attn_spatial_bwd(const void* qkv, const float* out_f32, const 
     const int64_t blocks = frames * ((S + kUvbRows - 1) / kUvbRows);
     JZ_CHECK_ARG(blocks < (1ll << 31), "spatial attention bwd: too many frames");
     JZ_CHECK_ARG(H % 2 == 0, "spatial attention bwd: an even head count is required (D multiple of 128)");
+    JZ_CHECK_ARG(out != nullptr && out_lo != nullptr, "spatial attention bwd: the forward's output and its residual are required");
+    auto oh = reinterpret_cast<const __nv_bfloat16*>(out);
+    auto ol = reinterpret_cast<const __nv_bfloat16*>(out_lo);
     auto dd = reinterpret_cast<const __nv_bfloat16*>(dout);
     auto qq = reinterpret_cast<const __nv_bfloat16*>(qkv);
     auto st_ = reinterpret_cast<cudaStream_t>(s);
     switch (D / 128) {
-      case 1: spatial_uvb_rows_kernel<1><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      case 2: spatial_uvb_rows_kernel<2><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      case 3: spatial_uvb_rows_kernel<3><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      case 4: spatial_uvb_rows_kernel<4><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      case 5: spatial_uvb_rows_kernel<5><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      case 6: spatial_uvb_rows_kernel<6><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      case 7: spatial_uvb_rows_kernel<7><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
-      default: spatial_uvb_rows_kernel<8><<<(unsigned)blocks, 256, 0, st_>>>(out_f32, dd, qq, lse, frames, S, H, uvb); break;
+      case 1: spatial_uvb_rows_kernel<1><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      case 2: spatial_uvb_rows_kernel<2><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      case 3: spatial_uvb_rows_kernel<3><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      case 4: spatial_uvb_rows_kernel<4><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      case 5: spatial_uvb_rows_kernel<5><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      case 6: spatial_uvb_rows_kernel<6><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      case 7: spatial_uvb_rows_kernel<7><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
+      default: spatial_uvb_rows_kernel<8><<<(unsigned)blocks, 256, 0, st_>>>(oh, ol, dd, qq, lse, frames, S, H, uvb); break;
     }
     JZ_LAUNCH_CHECK();
   }

@@ -349,9 +349,10 @@ def layernorm_bwd(x, mean, rstd, g, dy, dres, *, accumulate: bool, dres_bf16=Non
 SMALL_S = 32  # spatial sequence lengths served by the register-tile kernel (K3s)
 
 
-def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: bool = True):
-    """-> (out bf16, out fp32 or None, lse).  S <= 32 runs the register-tile kernel (K3s), whose
-    backward takes the bf16 output: no fp32 copy is written then."""
+def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_lo: bool = True):
+    """-> (out bf16, out_lo bf16 or None, lse).  out_lo = O - bf16(O), the rounding residual of the fp32
+    output (out + out_lo carries O to ~16 mantissa bits for the backward's Delta).  S <= 32 runs the
+    register-tile kernel (K3s), whose backward forms Delta from its in-register P and dP: no residual."""
     D = H * 64
     out = torch.empty(frames * S, D, dtype=BF16, device=qkv.device)
     if S <= SMALL_S:
@@ -360,47 +361,49 @@ def attn_spatial_fwd(qkv: torch.Tensor, frames: int, S: int, H: int, keep_f32: b
         L.call("jz_attn_spatial_small_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), lse.data_ptr(), _s())
         _fam_end(e0, "spatial_small_fwd", 4 * frames * H * S * S * 64, frames * S * (3 * D * 2 + D * 2 + H * 4))
         return out, None, lse
-    out32 = torch.empty(frames * S, D, dtype=F32, device=qkv.device) if keep_f32 else None
+    out_lo = torch.empty(frames * S, D, dtype=BF16, device=qkv.device) if keep_lo else None
     lse = torch.empty(frames, H, S, dtype=F32, device=qkv.device)
     e0 = _fam_begin()
-    L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), _p(out32), lse.data_ptr(), _s())
-    # algorithmic work: QK^T and PV over S x S per (frame, head); qkv in, O bf16 (+ fp32) and lse out
+    L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), _p(out_lo), lse.data_ptr(), _s())
+    # algorithmic work: QK^T and PV over S x S per (frame, head); qkv in, O bf16 (+ residual) and lse out
     _fam_end(e0, "spatial_fwd", 4 * frames * H * S * S * 64,
-             frames * S * (3 * D * 2 + D * 2 + (D * 4 if keep_f32 else 0) + H * 4))
-    return out, out32, lse
+             frames * S * (3 * D * 2 + D * 2 + (D * 2 if keep_lo else 0) + H * 4))
+    return out, out_lo, lse
 
 
-def attn_spatial_bwd(qkv, out_f32, dout, lse, frames: int, S: int, H: int, dqkv=None, colsum=None):
+def attn_spatial_bwd(qkv, out, dout, lse, frames: int, S: int, H: int, dqkv=None, colsum=None, out_lo=None):
     """colsum (fp32 [3*H*64], optional): also the column sums of dqkv (QKV bias gradient).
-    out_f32: the forward's fp32 output (S in {256, 257}) or its bf16 output (S <= 32)."""
+    out: the forward's bf16 output; out_lo: its residual (required for S in {256, 257})."""
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
     if S <= SMALL_S:
-        if out_f32.dtype != BF16:
+        if out.dtype != BF16:
             raise ValueError("small-frame spatial attention backward takes the bf16 forward output")
         part, nparts = None, 0
         if colsum is not None:
             nparts = frames
             part = scratch("attn_colsum", nparts * 3 * H * 64)
         e0 = _fam_begin()
-        L.call("jz_attn_spatial_small_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames,
+        L.call("jz_attn_spatial_small_bwd", qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames,
                S, H, 64, dqkv.data_ptr(), _p(part), _s())
         D = H * 64
         _fam_end(e0, "spatial_small_bwd", 10 * frames * H * S * S * 64, frames * S * (3 * D * 2 + D * 2 + 3 * D * 2))
         if colsum is not None:
             reduce_partials(part, nparts, 3 * H * 64, colsum)
         return dqkv
+    if out_lo is None:
+        raise ValueError("spatial attention backward needs the forward's residual (attn_spatial_fwd(keep_lo=True))")
     ws = scratch("attn_uvb", L.load().jz_attn_spatial_bwd_workspace_bytes(frames, S, H) // 4)
     part, nparts = None, 0
     if colsum is not None:
         nparts = L.load().jz_attn_spatial_colsum_parts(frames)
         part = scratch("attn_colsum", nparts * 3 * H * 64)
     e0 = _fam_begin()
-    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out_f32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
-           64, dqkv.data_ptr(), ws.data_ptr(), _p(part), _s())
-    # 2.5x the forward FLOPs (S, dP, dV, dK, dQ); bytes: qkv, dO (twice: Delta pass + MMAs), O fp32 in, dqkv out
+    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out.data_ptr(), out_lo.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+           frames, S, H, 64, dqkv.data_ptr(), ws.data_ptr(), _p(part), _s())
+    # 2.5x the forward FLOPs (S, dP, dV, dK, dQ); bytes: qkv, dO (twice: Delta pass + MMAs), O + residual in, dqkv out
     D = H * 64
-    _fam_end(e0, "spatial_bwd", 10 * frames * H * S * S * 64, frames * S * (3 * D * 2 + 2 * D * 2 + D * 4 + 3 * D * 2))
+    _fam_end(e0, "spatial_bwd", 10 * frames * H * S * S * 64, frames * S * (3 * D * 2 + 2 * D * 2 + 2 * D * 2 + 3 * D * 2))
     if colsum is not None:
         reduce_partials(part, nparts, 3 * H * 64, colsum)
     return dqkv

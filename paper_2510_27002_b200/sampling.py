@@ -202,7 +202,7 @@ class FrameDecoder:
         H, S = self.H, self.S
         xn, _, _ = _K.layernorm_fwd(x, P[f"{base}.spatial.ln.g"].data, P[f"{base}.spatial.ln.b"].data)
         qkv = _K.linear_fwd(xn, w["spatial.wqkv"], w["spatial.bqkv"])
-        ao, _, _ = _K.attn_spatial_fwd(qkv, B * T, S, H, keep_f32=False)
+        ao, _, _ = _K.attn_spatial_fwd(qkv, B * T, S, H, keep_lo=False)
         x1 = _K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=_L.EPI_RESID, aux=x)
         xn2, _, _ = _K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
         qkv2 = _K.linear_fwd(xn2, w["temporal.wqkv"], w["temporal.bqkv"])

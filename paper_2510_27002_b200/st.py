@@ -177,7 +177,7 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
         else:
             xn, m1, r1 = nxt
         qkv = K.linear_fwd(xn, w["spatial.wqkv"], w["spatial.bqkv"])
-        ao, ao32, lse_s = K.attn_spatial_fwd(qkv, frames, S, H, keep_f32=save)
+        ao, ao_lo, lse_s = K.attn_spatial_fwd(qkv, frames, S, H, keep_lo=save)
         if fuse:
             x1, xn2, m2, r2 = K.linear_fwd_ln(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, x,
                                                P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
@@ -213,7 +213,7 @@ def st_forward(x: torch.Tensor, P: dict, cfg: StConfig, prefix: str, *, B: int, 
         else:
             x3 = K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=L.EPI_RESID, aux=x2)
         if save:
-            c.update(xn=xn, m1=m1, r1=r1, qkv=qkv, ao=ao, ao32=ao32, lse_s=lse_s, x1=x1, xn2=xn2, m2=m2, r2=r2, qkv2=qkv2,
+            c.update(xn=xn, m1=m1, r1=r1, qkv=qkv, ao=ao, ao_lo=ao_lo, lse_s=lse_s, x1=x1, xn2=xn2, m2=m2, r2=r2, qkv2=qkv2,
                      ao2=ao2, lse_t=lse_t, x2=x2, xn3=xn3, m3=m3, r3=r3, h=h, hpre=hpre)
             blocks_ctx.append(c)
         x = x3
@@ -288,10 +288,10 @@ def st_backward(ctx: dict, dy: torch.Tensor, P: dict, G: dict, cfg: StConfig, pr
         K.linear_dw(c["ao"], dres_b, G[f"{base}.spatial.o.w"])
         gbs = gst.block_of(gst.grad_flat, f"{base}.spatial.q.b") if gst is not None else None
         K.linear_dx(dres_b, w["spatial.wo"], epilogue=L.EPI_BF16, out=dao)
-        o_saved = c["ao32"] if c["ao32"] is not None else c["ao"]  # bf16 O for S <= 32
         # the QKV bias gradient from the attention backward's own column-sum partials of dqkv (one
         # fused pass; measured 54 us per block faster than the dO-GEMM column sums + a q pass)
-        dqkv = K.attn_spatial_bwd(c["qkv"], o_saved, dao, c["lse_s"], frames, S, H, dqkv=dqkv, colsum=gbs)
+        dqkv = K.attn_spatial_bwd(c["qkv"], c["ao"], dao, c["lse_s"], frames, S, H, dqkv=dqkv, colsum=gbs,
+                                  out_lo=c["ao_lo"])
         _qkv_param_grads(dqkv, c["xn"], G, f"{base}.spatial", d, gst, bias_done=gbs is not None)
         prev_bias = G[f"{prefix}.block{i - 1}.ffn.down.b"] if i > 0 else None
         _dx_layernorm(dqkv, w["spatial.wqkv"], c["x_in"], c["m1"], c["r1"], P[f"{base}.spatial.ln.g"].data, dres,

@@ -198,19 +198,21 @@ def test_attn_spatial_fwd_bwd(S, frames):
     D = H * 64
     g = torch.Generator(device=dev).manual_seed(S)
     qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
-    out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+    out, out_lo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
     qf = qkv.float().requires_grad_(True)
     o_ref, lse_ref = _ref_attn(qf.reshape(frames, S, 3 * D), (frames,), S, H, False)
     assert rel(out.reshape(frames, S, D), o_ref) < 1e-2
-    assert rel(out32.reshape(frames, S, D), o_ref) < 1e-2
+    o_full = (out.float() + out_lo.float()).reshape(frames, S, D)  # the residual carries O past bf16
+    assert rel(o_full, o_ref) < 1e-2
+    assert float((out_lo.float().abs() - out.float().abs() * 2.0 ** -8).clamp_min(0).max()) == 0.0
     assert rel(out.reshape(frames, S, D)[:, -1], o_ref[:, -1]) < 1e-2  # the CUDA-core 257th row
     assert rel(lse, lse_ref) < 1e-4
     go = torch.randn(o_ref.shape, device=dev, generator=g)
     o_ref.backward(go)
     dqkv = torch.full_like(qkv, float("nan"))
     cs = torch.full((3 * D,), float("nan"), device=dev)
-    Kn.attn_spatial_bwd(qkv, out32, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
-                        colsum=cs)
+    Kn.attn_spatial_bwd(qkv, out, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
+                        colsum=cs, out_lo=out_lo)
     assert torch.isfinite(dqkv.float()).all()
     cs_ref = torch.empty_like(cs)
     Kn.colsum_bf16(dqkv, cs_ref)  # fused bias-gradient column sums == a pass over the written dqkv
@@ -290,8 +292,8 @@ def test_attn_spatial_small_fwd_bwd(S, H):
     D = H * 64
     g = torch.Generator(device=dev).manual_seed(S * 31 + H)
     qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
-    out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
-    assert out32 is None  # the small kernel's backward reads the bf16 output
+    out, out_lo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
+    assert out_lo is None  # the small kernel's backward reads the bf16 output
     qf = qkv.float().requires_grad_(True)
     o_ref, lse_ref = _ref_attn(qf.reshape(frames, S, 3 * D), (frames,), S, H, False)
     assert rel(out.reshape(frames, S, D), o_ref) < 1e-2

@@ -12,7 +12,7 @@ for S in (257, 256):
     frames, H, D = 576, 8, 512
     qkv = torch.randn(frames * S, 3 * D, device="cuda").bfloat16()
     for keep in (True, False):
-        fn = lambda: Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=keep)
+        fn = lambda: Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=keep)
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -22,4 +22,4 @@ for S in (257, 256):
             fn()
         b.record()
         torch.cuda.synchronize()
-        print(f"S={S} fwd keep_f32={keep}: {a.elapsed_time(b) / 20 * 1e3:.1f} us ({pathlib.Path(sys.argv[1]).name if len(sys.argv) > 1 else 'default'})", flush=True)
+        print(f"S={S} fwd keep_lo={keep}: {a.elapsed_time(b) / 20 * 1e3:.1f} us ({pathlib.Path(sys.argv[1]).name if len(sys.argv) > 1 else 'default'})", flush=True)

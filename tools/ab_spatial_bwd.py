@@ -42,15 +42,15 @@ for S in (257, 256):
     D = H * 64
     g = torch.Generator(device=dev).manual_seed(S)
     qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
-    out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+    out, olo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
     qf = qkv.float().requires_grad_(True)
     o = ref_attn(qf, frames, S, H)
     go = torch.randn(o.shape, device=dev, generator=g)
     o.backward(go)
     dqkv = torch.full_like(qkv, float("nan"))
     cs = torch.full((3 * D,), float("nan"), device=dev)
-    Kn.attn_spatial_bwd(qkv, out32, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
-                        colsum=cs)
+    Kn.attn_spatial_bwd(qkv, out, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
+                        colsum=cs, out_lo=olo)
     torch.cuda.synchronize()
     cs_ref = torch.empty_like(cs)
     Kn.colsum_bf16(dqkv, cs_ref)
@@ -63,11 +63,11 @@ for S in (257, 256):
     # timing at B = 36
     frames = 576
     qkv = torch.randn(frames * S, 3 * D, device=dev).bfloat16()
-    out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+    out, olo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
     dO = torch.randn(frames * S, D, device=dev).bfloat16()
     dq = torch.empty_like(qkv)
     cs = torch.empty(3 * D, device=dev)
-    fn = lambda: Kn.attn_spatial_bwd(qkv, out32, dO, lse, frames, S, H, dqkv=dq, colsum=cs)
+    fn = lambda: Kn.attn_spatial_bwd(qkv, out, dO, lse, frames, S, H, dqkv=dq, colsum=cs, out_lo=olo)
     for _ in range(3):
         fn()
     torch.cuda.synchronize()

@@ -12,7 +12,7 @@ D = H * 64
 M = frames * S
 g = torch.Generator(device="cuda").manual_seed(0)
 qkv = torch.randn(M, 3 * D, device="cuda", generator=g).bfloat16()
-o, o32, lse = K.attn_spatial_fwd(qkv, frames, S, H)
+o, olo, lse = K.attn_spatial_fwd(qkv, frames, S, H)
 dres_b = (torch.randn(M, D, device="cuda", generator=g) * 0.1).bfloat16()
 wo = (torch.randn(D, D, device="cuda", generator=g) * 0.05).bfloat16()
 dao = torch.empty(M, D, device="cuda", dtype=torch.bfloat16)
@@ -22,14 +22,14 @@ gb = torch.empty(3 * D, device="cuda")
 
 def a():
     K.linear_dx(dres_b, wo, epilogue=L.EPI_BF16, out=dao, colsum=gb[2 * D:])
-    K.attn_spatial_bwd(qkv, o32, dao, lse, frames, S, H, dqkv=dq)
+    K.attn_spatial_bwd(qkv, o, dao, lse, frames, S, H, dqkv=dq, out_lo=olo)
     gb[D:2 * D].zero_()
     K.colsum_bf16(dq, gb[:D], cols=D)
 
 
 def b():
     K.linear_dx(dres_b, wo, epilogue=L.EPI_BF16, out=dao)
-    K.attn_spatial_bwd(qkv, o32, dao, lse, frames, S, H, dqkv=dq, colsum=gb)
+    K.attn_spatial_bwd(qkv, o, dao, lse, frames, S, H, dqkv=dq, colsum=gb, out_lo=olo)
 
 
 def t(fn, n=10):

@@ -26,14 +26,14 @@ for S in (256, 257):
     D = H * 64
     qkv = torch.randn(frames * S, 3 * D, device=dev).bfloat16()
     out = torch.empty(frames * S, D, device=dev, dtype=torch.bfloat16)
-    o32 = torch.empty(frames * S, D, device=dev)
+    olo = torch.empty(frames * S, D, device=dev, dtype=torch.bfloat16)
     lse = torch.empty(frames, H, S, device=dev)
     dq = torch.empty_like(qkv)
     WS = torch.empty(frames * H * 780, device='cuda')
-    f = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
+    f = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), olo.data_ptr(), lse.data_ptr(), L.stream_ptr())
     f2 = lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), None, lse.data_ptr(), L.stream_ptr())
-    bw = lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
+    bw = lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out.data_ptr(), olo.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
     fl = 4 * frames * H * S * S * 64
-    for name, fn, mult in (("fwd+f32", f, 1), ("fwd", f2, 1), ("bwd", bw, 2.5)):
+    for name, fn, mult in (("fwd+residual", f, 1), ("fwd", f2, 1), ("bwd", bw, 2.5)):
         us = timeit(fn)
         print(f"S={S} {name}: {us:.1f} us  {mult * fl / us / 1e6:.0f} TFLOP/s", flush=True)

@@ -85,8 +85,8 @@ if "spatial_bwd" in sys.argv:
         qkv = (torch.randn(frames * S, 3 * D, device=dev) * 1.5).bfloat16()
         out = torch.empty(frames * S, D, device=dev, dtype=torch.bfloat16)
         lse = torch.empty(frames, H, S, device=dev)
-        out32 = torch.empty(frames * S, D, device=dev)
-        L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), out32.data_ptr(), lse.data_ptr(), L.stream_ptr())
+        olo = torch.empty(frames * S, D, device=dev, dtype=torch.bfloat16)
+        L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), olo.data_ptr(), lse.data_ptr(), L.stream_ptr())
         qkv_f = qkv.float().requires_grad_(True)
         o_r, _ = ref_attn(qkv_f.reshape(frames, S, 3 * D), (frames,), S, H, False)
         go = torch.randn_like(o_r)
@@ -94,7 +94,7 @@ if "spatial_bwd" in sys.argv:
         dref = qkv_f.grad
         dout = go.reshape(frames * S, D).bfloat16().contiguous()
         dqkv = torch.full_like(qkv, float("nan"))
-        L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out32.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
+        L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out.data_ptr(), olo.data_ptr(), dout.data_ptr(), lse.data_ptr(), frames, S, H,
                64, dqkv.data_ptr(), torch.empty(frames * H * 780, device=dev).data_ptr(), None, L.stream_ptr())
         torch.cuda.synchronize()
         for i, nm in enumerate("qkv"):
@@ -121,8 +121,8 @@ D = H * 64
 qkv = torch.randn(frames * S, 3 * D, device=dev).bfloat16()
 out = torch.empty(frames * S, D, device=dev, dtype=torch.bfloat16)
 lse = torch.empty(frames, H, S, device=dev)
-out32 = torch.empty(frames * S, D, device=dev)
-us = timeit(lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), out32.data_ptr(), lse.data_ptr(), L.stream_ptr()))
+olo = torch.empty(frames * S, D, device=dev, dtype=torch.bfloat16)
+us = timeit(lambda: L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), olo.data_ptr(), lse.data_ptr(), L.stream_ptr()))
 fl = 4 * frames * H * S * S * 64
 print(f"spatial fwd B36: {us:.1f} us  {fl / us / 1e6:.0f} TFLOP/s", flush=True)
 lse_t = torch.empty(36 * S, H, 16, device=dev)
@@ -133,7 +133,7 @@ WS = torch.empty(frames * H * 780, device='cuda')
 us = timeit(lambda: L.call("jz_attn_temporal_bwd", qkv.data_ptr(), out.data_ptr(), out.data_ptr(), lse_t.data_ptr(), 36, 16, S, H, 64, dq.data_ptr(), None, L.stream_ptr()))
 print(f"temporal bwd B36: {us:.1f} us  {(qkv.numel() * 4 + out.numel() * 4) / us / 1e3:.0f} GB/s", flush=True)
 if "spatial_bwd" in sys.argv:
-    us = timeit(lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr()))
+    us = timeit(lambda: L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out.data_ptr(), olo.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr()))
     print(f"spatial bwd B36: {us:.1f} us  {2.5 * fl / us / 1e6:.0f} TFLOP/s", flush=True)
 print("ALL OK" if ok else "SOME FAILED")
 sys.exit(0 if ok else 1)

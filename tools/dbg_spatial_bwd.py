@@ -11,10 +11,10 @@ frames = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 257
 H, D = 8, 512
 qkv = torch.randn(frames * S, 3 * D, device="cuda").bfloat16()
-out, out32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+out, olo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
 dO = torch.randn(frames * S, D, device="cuda").bfloat16()
 dq = torch.full_like(qkv, float("nan"))
 cs = torch.empty(3 * D, device="cuda")
-Kn.attn_spatial_bwd(qkv, out32, dO, lse, frames, S, H, dqkv=dq, colsum=cs)
+Kn.attn_spatial_bwd(qkv, out, dO, lse, frames, S, H, dqkv=dq, colsum=cs, out_lo=olo)
 torch.cuda.synchronize()
 print("ok", frames, S, bool(torch.isfinite(dq.float()).all()))

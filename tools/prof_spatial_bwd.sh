@@ -18,13 +18,13 @@ frames, S, H = 576, int(os.environ.get("S", "257")), 8
 D = H * 64
 qkv = torch.randn(frames * S, 3 * D, device="cuda").bfloat16()
 out = torch.empty(frames * S, D, device="cuda", dtype=torch.bfloat16)
-o32 = torch.empty(frames * S, D, device="cuda")
+olo = torch.empty(frames * S, D, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(frames, H, S, device="cuda")
 dq = torch.empty_like(qkv)
 WS = torch.empty(frames * H * 780, device='cuda')
-L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), o32.data_ptr(), lse.data_ptr(), L.stream_ptr())
+L.call("jz_attn_spatial_fwd", qkv.data_ptr(), frames, S, H, 64, out.data_ptr(), olo.data_ptr(), lse.data_ptr(), L.stream_ptr())
 for _ in range(3):
-    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), o32.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
+    L.call("jz_attn_spatial_bwd", qkv.data_ptr(), out.data_ptr(), olo.data_ptr(), out.data_ptr(), lse.data_ptr(), frames, S, H, 64, dq.data_ptr(), WS.data_ptr(), None, L.stream_ptr())
 torch.cuda.synchronize()
 buf = np.zeros(64 * 32, dtype=np.uint64)
 lib.jz_attn_prof_read.argtypes = [C.c_void_p]

@@ -21,11 +21,11 @@ L.ensure_device()
 S = int(os.environ.get("S", "257"))
 frames, H, D = 576, 8, 512
 qkv = torch.randn(frames * S, 3 * D, device="cuda").bfloat16()
-out, o32, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_f32=True)
+out, olo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
 dO = torch.randn(frames * S, D, device="cuda").bfloat16()
 dq = torch.empty_like(qkv); cs = torch.empty(3 * D, device="cuda")
 for _ in range(3):
-    Kn.attn_spatial_bwd(qkv, o32, dO, lse, frames, S, H, dqkv=dq, colsum=cs)
+    Kn.attn_spatial_bwd(qkv, out, dO, lse, frames, S, H, dqkv=dq, colsum=cs, out_lo=olo)
 torch.cuda.synchronize()
 lib = L.load()
 buf = np.zeros(16 * 128, dtype=np.uint64)
