@@ -71,6 +71,23 @@ JZ_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with back-off: a failed try_wait puts the thread to sleep for `ns` before polling again, so
+// warps that wait long (load producers, epilogue warps) do not take issue slots from the compute
+// warps on their scheduler.
+JZ_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t addr = smem_u32(bar);
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor)
 // ----------------------------------------------------------------------------
