@@ -953,24 +953,28 @@ __global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const __nv_bfloat
     const int h = e / kUvbRows, q = c0 + e % kUvbRows;
     if (q < S) uvb[(f * H + h) * kUvbFloats + U_LSE2 + q] = __ldg(lse + (f * H + h) * S + q) * 1.4426950408889634f;
   }
+  constexpr int NC2 = NC / 2;  // 256-column chunks: lane reads 8 consecutive columns (16-byte loads)
   for (int k0 = 0; k0 < kUvbRows / 8; k0 += 2) {
-    float acc[2][NC];
+    float acc[2][NC2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int sidx = c0 + warp * (kUvbRows / 8) + k0 + k;
       if (sidx >= S) continue;
       const int64_t row = f * S + sidx;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        {
-          const int col = 128 * c + 4 * lane;
-          const uint2 hv = __ldg(reinterpret_cast<const uint2*>(out + row * D + col));
-          const uint2 lv = __ldg(reinterpret_cast<const uint2*>(out_lo + row * D + col));
-          const uint2 gv = __ldg(reinterpret_cast<const uint2*>(dout + row * D + col));
-          const float2 h0 = unpack_bf16(hv.x), h1 = unpack_bf16(hv.y), l0 = unpack_bf16(lv.x), l1 = unpack_bf16(lv.y);
-          const float2 g0 = unpack_bf16(gv.x), g1 = unpack_bf16(gv.y);
-          acc[k][c] = (h0.x + l0.x) * g0.x + (h0.y + l0.y) * g0.y + (h1.x + l1.x) * g1.x + (h1.y + l1.y) * g1.y;
+      for (int c = 0; c < NC2; ++c) {
+        const int col = 256 * c + 8 * lane;
+        const uint4 hv = __ldg(reinterpret_cast<const uint4*>(out + row * D + col));
+        const uint4 lv = __ldg(reinterpret_cast<const uint4*>(out_lo + row * D + col));
+        const uint4 gv = __ldg(reinterpret_cast<const uint4*>(dout + row * D + col));
+        const uint32_t hh[4] = {hv.x, hv.y, hv.z, hv.w}, ll[4] = {lv.x, lv.y, lv.z, lv.w}, gg[4] = {gv.x, gv.y, gv.z, gv.w};
+        float a = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 h2 = unpack_bf16(hh[e]), l2 = unpack_bf16(ll[e]), g2 = unpack_bf16(gg[e]);
+          a += (h2.x + l2.x) * g2.x + (h2.y + l2.y) * g2.y;
         }
+        acc[k][c] = a;
       }
     }
 #pragma unroll
@@ -978,17 +982,15 @@ __global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const __nv_bfloat
       const int sidx = c0 + warp * (kUvbRows / 8) + k0 + k;
       if (sidx >= S) continue;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        {
-          float a = acc[k][c];
+      for (int c = 0; c < NC2; ++c) {
+        float a = acc[k][c];
 #pragma unroll
-          for (int m = 8; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);  // 16 lanes = one head
-          const int h = (128 * c + 4 * lane) >> 6;
-          if ((lane & 15) == 0) uvb[(f * H + h) * kUvbFloats + U_DV + sidx] = a;
-          acc[k][c] = a;
-        }
+        for (int m = 4; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);  // 8 lanes = one head
+        const int h = (256 * c + 8 * lane) >> 6;
+        if ((lane & 7) == 0) uvb[(f * H + h) * kUvbFloats + U_DV + sidx] = a;
       }
       if (sidx == 256) {  // token 256: its vectors and the (256, 256) entry, per head
+        __syncwarp();  // Delta[256] of every head written above by this warp
         const int64_t row = f * S + sidx;
         const __nv_bfloat16* qr = qkv + row * 3 * (int64_t)D;
 #pragma unroll
@@ -1020,7 +1022,7 @@ __global__ void __launch_bounds__(256) spatial_uvb_rows_kernel(const __nv_bfloat
             if ((lane & 15) == 0) {
               const float p = exp2f(sk * c2 - __ldg(lse + (f * H + h) * S + 256) * 1.4426950408889634f);
               ub[U_PC] = p;
-              ub[U_DC] = p * (dpv - acc[k][c]);
+              ub[U_DC] = p * (dpv - ub[U_DV + 256]);
             }
           }
         }
