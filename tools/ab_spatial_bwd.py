@@ -1,17 +1,18 @@
 import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))  # noqa: E402
-"""A/B of the spatial attention backward versions (JZ_SPATIAL_BWD=2 / 3): accuracy against torch fp32 at
-frames=40 (several units per CTA) and event timing at B=36 (576 frames x 8 heads), S = 256 and 257.
-usage: python tools/ab_spatial_bwd.py            (spawns one process per version)"""
+"""Spatial attention backward: accuracy against torch fp32 at frames=40 (several units per CTA) and
+event timing at B=36 (576 frames x 8 heads), S = 256 and 257, for the default library and any
+alternative builds given as JZ_LIB_PATH values.
+usage: python tools/ab_spatial_bwd.py [LIB ...]          (spawns one process per library)"""
 import json
 import math
 import os
 import subprocess
 
-if len(sys.argv) == 1:
-    for v in ("2", "3"):
-        env = dict(os.environ, JZ_SPATIAL_BWD=v)
+if len(sys.argv) == 1 or sys.argv[1] != "run":
+    for lib in [""] + sys.argv[1:]:
+        env = dict(os.environ, JZ_LIB_PATH=lib) if lib else dict(os.environ)
         out = subprocess.run([sys.executable, __file__, "run"], env=env, capture_output=True, text=True)
-        print(f"--- JZ_SPATIAL_BWD={v}", out.returncode)
+        print(f"--- {lib or 'default library'}", out.returncode)
         print(out.stdout[-3000:], out.stderr[-3000:])
     sys.exit(0)
 
