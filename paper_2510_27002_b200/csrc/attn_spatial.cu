@@ -20,29 +20,43 @@ namespace jz {
 
 namespace sp {
 
-constexpr int kFwdTailWarps = 4;  // query row 256 (S = 257) on CUDA cores, keys split 4 ways
+constexpr int kFwdTailWarps = 4;  // query row 256 / key column 256 (S = 257) on CUDA cores
 constexpr int kFwdTailThreads = 32 * kFwdTailWarps;
-constexpr int kFwdThreads = 320 + kFwdTailThreads;  // w0 TMA, w1 MMA, w2-5 tile 0, w6-9 tile 1, w10.. tail row
+constexpr int kFwdThreads = 320 + kFwdTailThreads;  // w0 TMA, w1 MMA, w2-5 tile 0, w6-9 tile 1, w10.. tail
 constexpr int TILE = 16384;    // 128 rows x 128 B
 // forward smem map (bytes, from a 1024-aligned base)
-constexpr int F_Q = 0;                 // 2 tiles
-constexpr int F_K = F_Q + 2 * TILE;    // 2 tiles (256 keys)
-constexpr int F_V = F_K + 2 * TILE;    // 2 tiles
-constexpr int F_P0 = F_V + 2 * TILE;   // 4 atoms
-constexpr int F_P1 = F_P0 + 4 * TILE;  // 4 atoms
-constexpr int F_END = F_P1 + 4 * TILE; // 229376
-constexpr int F_SMEM = F_END + 1024 + 2048;
+constexpr int F_Q = 0;                  // 2 tiles (query tiles 0 / 1)
+constexpr int F_K = F_Q + 2 * TILE;     // 2 slots x 2 tiles (256 keys), slot = unit parity
+constexpr int F_V = F_K + 4 * TILE;     // 2 tiles
+constexpr int F_ST = F_V + 2 * TILE;    // per query tile: O staging + residual staging (2 tiles each)
+constexpr int F_VX = F_ST + 4 * TILE;    // value rows 256..271 for the PV MMA's 17th K-step: row 0 = v_256
+                                         // (TMA, with V), rows 1..15 stay zero
+constexpr int F_ONES = F_VX + 2048;      // 16 rows x 128 B of bf16 1.0: the row-sum columns of the PV MMA
+constexpr int F_END = F_ONES + 2048;     // 200704
+constexpr int kFwdSmall = 8192;
+constexpr int F_SMEM = F_END + kFwdSmall + 1024;
 
 struct FwdSmallSmem {
-  uint64_t qk_full, v_full, qk_free, v_free;
+  uint64_t q_full[2], q_free[2], k_full[2], k_free[2], v_full, v_free;
   uint64_t s_full[2], p_full[2], o_full[2], tmem_free[2];
+  uint64_t exp_turn[2];  // the two softmax warpgroups take turns on the exponentials
   uint32_t tmem_base;
-  alignas(128) uint8_t krow[128];  // key 256 of the unit (TMA, arrives with Q/K)
-  alignas(128) uint8_t vrow[128];  // value 256 of the unit (TMA, arrives with V)
+  alignas(128) uint8_t krow[2][128];  // key 256 of the unit (TMA, arrives with K), slot = unit parity
   float tail_s[260];
   float tail_red[2 * kFwdTailWarps];
 };
-static_assert(sizeof(FwdSmallSmem) <= 2048, "forward small smem budget");
+static_assert(sizeof(FwdSmallSmem) <= kFwdSmall, "forward small smem budget");
+
+#ifdef JZ_SPATIAL_FWD_PROF
+// per-unit timeline of CTA 0 (clock64 marks), read back with jz_attn_fwd_prof_read
+__device__ unsigned long long g_ftl[16][64];
+#define FTL(slot)                                                                      \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && i < 16 && (threadIdx.x & 31) == 0) g_ftl[i][slot] = clock64(); \
+  } while (0)
+#else
+#define FTL(slot) do { } while (0)
+#endif
 
 JZ_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -52,13 +66,45 @@ JZ_DEV float ex2(float x) {
   return y;
 }
 
+JZ_DEV float fmax3(float a, float b, float c) {
+  float y;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
+  return y;
+}
+
 // byte offset of (row r, 16-byte chunk c in 0..7) inside a 128B-swizzled 128-row tile
 JZ_DEV uint32_t sw128(uint32_t r, uint32_t c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+// dot product of a 64-wide bf16 row held as 8 16-byte chunks (row r of a swizzled tile) with an
+// unswizzled 64-wide bf16 row; four partial sums
+JZ_DEV float dot64_tile_row(const uint8_t* tile, uint32_t r, const uint8_t* row) {
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 w = *reinterpret_cast<const uint4*>(tile + sw128(r, c));
+    const uint4 kw = *reinterpret_cast<const uint4*>(row + (c << 4));
+    const uint32_t qa[4] = {w.x, w.y, w.z, w.w}, ka[4] = {kw.x, kw.y, kw.z, kw.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = unpack_bf16(qa[e]), y = unpack_bf16(ka[e]);
+      a[e] = fmaf(x.x, y.x, a[e]);
+      a[e] = fmaf(x.y, y.y, a[e]);
+    }
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
 
 }  // namespace sp
 
 using namespace sp;
 
+// One CTA per SM walks (frame, head) units. Query tile t (rows 128t..128t+127) belongs to softmax
+// warpgroup t; S_t = Q_t K^T (128 x 256 fp32) sits in TMEM columns 256t..256t+255, P overwrites its
+// first 128 columns as bf16 pairs and O_t = P_t V accumulates in columns 256t+128..256t+191.
+// The two warpgroups take turns on the exponentials (exp_turn), so one warpgroup's max pass, PV
+// wait and epilogue overlap the other's MUFU-bound exponential pass. K is double-buffered by unit
+// parity so the next unit's scores can start while this unit's second tile is still in flight.
+// S = 257: the tail warps form query row 256 and the key-256 column on CUDA cores.
 __global__ void __launch_bounds__(kFwdThreads, 1)
     spatial_fwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_row,
                        const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_olo,
@@ -72,6 +118,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int units = frames * H;
   const bool has_tail = S > 256;
   const float c2 = 0.125f * 1.4426950408889634f;  // scale * log2(e)
+  const int ntail = has_tail ? kFwdTailThreads : 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
@@ -80,286 +127,363 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (out_lo) tma_prefetch_desc(&tm_olo);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(&sm.qk_full, 1); mbar_init(&sm.v_full, 1);
-    // Q/K and V smem (+ rows 256) are released by the MMA commit, both softmax warpgroups and the tail
-    mbar_init(&sm.qk_free, 1 + 256 + (has_tail ? kFwdTailThreads : 0));
-    mbar_init(&sm.v_free, 1 + 256 + (has_tail ? kFwdTailThreads : 0));
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&sm.s_full[t], 1); mbar_init(&sm.p_full[t], 128);
-      mbar_init(&sm.o_full[t], 1); mbar_init(&sm.tmem_free[t], 128);
+      mbar_init(&sm.q_full[t], 1);
+      mbar_init(&sm.q_free[t], 1 + (has_tail ? 128 : 0));  // S_t MMA commit (+ warpgroup t: key-256 column)
+      mbar_init(&sm.k_full[t], 1);
+      mbar_init(&sm.k_free[t], 1 + ntail + (has_tail ? 256 : 0));  // S_1 MMA commit + tail warps (+ softmax: key row 256)
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.o_full[t], 1);
+      mbar_init(&sm.tmem_free[t], 128);
+      mbar_init(&sm.exp_turn[t], 4);
     }
+    mbar_init(&sm.v_full, 1);
+    mbar_init(&sm.v_free, 1 + ntail);  // PV_1 MMA commit + tail warps
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  for (int e = threadIdx.x; e < 2048 / 16; e += blockDim.x)
+  {
+    *reinterpret_cast<uint4*>(smem + F_ONES + 16 * e) = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+    *reinterpret_cast<uint4*>(smem + F_VX + 16 * e) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  fence_proxy_async();  // generic writes of the ones tile before the tensor core reads it
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, sm.tmem_base, 0);
 
   if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       int i = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
         const int f = u / H, h = u % H;
         const int row0 = f * S;
-        mbar_wait(&sm.qk_free, (i & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.qk_full, 4 * TILE + (has_tail ? 128 : 0));
-        if (has_tail) tma_load_2d(sm.krow, &tm_row, &sm.qk_full, D + h * 64, row0 + 256);
-        tma_load_2d(smem + F_Q, &tm, &sm.qk_full, h * 64, row0);
-        tma_load_2d(smem + F_Q + TILE, &tm, &sm.qk_full, h * 64, row0 + 128);
-        tma_load_2d(smem + F_K, &tm, &sm.qk_full, D + h * 64, row0);
-        tma_load_2d(smem + F_K + TILE, &tm, &sm.qk_full, D + h * 64, row0 + 128);
+        const int ks = i & 1;
+        // in order of release: Q_0 (after S_0 of the previous unit), K slot (two units back), Q_1, V
+        mbar_wait(&sm.q_free[0], (i & 1) ^ 1);
+        FTL(30);
+        mbar_arrive_expect_tx(&sm.q_full[0], TILE);
+        tma_load_2d(smem + F_Q, &tm, &sm.q_full[0], h * 64, row0);
+        mbar_wait(&sm.k_free[ks], ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.k_full[ks], 2 * TILE + (has_tail ? 128 : 0));
+        if (has_tail) tma_load_2d(sm.krow[ks], &tm_row, &sm.k_full[ks], D + h * 64, row0 + 256);
+        tma_load_2d(smem + F_K + ks * 2 * TILE, &tm, &sm.k_full[ks], D + h * 64, row0);
+        tma_load_2d(smem + F_K + ks * 2 * TILE + TILE, &tm, &sm.k_full[ks], D + h * 64, row0 + 128);
+        mbar_wait(&sm.q_free[1], (i & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.q_full[1], TILE);
+        tma_load_2d(smem + F_Q + TILE, &tm, &sm.q_full[1], h * 64, row0 + 128);
         mbar_wait(&sm.v_free, (i & 1) ^ 1);
+        FTL(31);
         mbar_arrive_expect_tx(&sm.v_full, 2 * TILE + (has_tail ? 128 : 0));
-        if (has_tail) tma_load_2d(sm.vrow, &tm_row, &sm.v_full, 2 * D + h * 64, row0 + 256);
+        if (has_tail) tma_load_2d(smem + F_VX, &tm_row, &sm.v_full, 2 * D + h * 64, row0 + 256);
         tma_load_2d(smem + F_V, &tm, &sm.v_full, 2 * D + h * 64, row0);
         tma_load_2d(smem + F_V + TILE, &tm, &sm.v_full, 2 * D + h * 64, row0 + 128);
       }
     }
   } else if (warp == 1) {
-    // the whole warp runs the loop (convergent: uniform operands); one elected lane issues
-    {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(128, 256, false, false);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(128, 64, false, true);
-      // SW128 descriptors share one high word; low word = (address >> 4) | (LBO >> 4) << 16
-      const uint32_t dhi = (uint32_t)(sdesc_sw128(0, 0, 1024) >> 32);
-      auto dsc = [dhi](uint32_t addr4, uint32_t off, uint32_t lbo) -> uint64_t {
-        return ((uint64_t)dhi << 32) | (addr4 + (off >> 4) + ((lbo >> 4) << 16));
-      };
-      const uint32_t q4 = smem_u32(smem + F_Q) >> 4, k4 = smem_u32(smem + F_K) >> 4, v4 = smem_u32(smem + F_V) >> 4;
-      int i = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-        const uint32_t par = i & 1;
-        mbar_wait(&sm.qk_full, par);
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&sm.tmem_free[t], par ^ 1);
-          tc_fence_after();
+    // ------------------------------ MMA issuer (whole warp, uniform operands) ------------------------------
+    // Issue order follows the steady-state event order: S_0(i), PV_1(i-1), S_1(i), PV_0(i).
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 256, false, false);
+    // PV with N = 80: dims 0..63 from V, dims 64..79 from the all-ones tile (every one of those
+    // output columns is the row sum of the bf16 P the MMA multiplies)
+    constexpr uint32_t idesc_o = idesc_bf16_f32(128, 80, false, true);
+    const uint32_t dhi = (uint32_t)(sdesc_sw128(0, 0, 1024) >> 32);
+    auto dsc = [dhi](uint32_t addr4, uint32_t off, uint32_t lbo) -> uint64_t {
+      return ((uint64_t)dhi << 32) | (addr4 + (off >> 4) + ((lbo >> 4) << 16));
+    };
+    const uint32_t q4 = smem_u32(smem + F_Q) >> 4, k4 = smem_u32(smem + F_K) >> 4, v4 = smem_u32(smem + F_V) >> 4;
+    constexpr uint32_t ones_off = F_ONES - F_V;
+    const uint32_t vx4 = smem_u32(smem + F_VX) >> 4;
+    auto issue_s = [&](int i, int t) {
+      const int ks = i & 1;
+      mbar_wait(&sm.q_full[t], i & 1);
+      mbar_wait(&sm.tmem_free[t], (i & 1) ^ 1);
+      tc_fence_after();
+      FTL(1 + t);
+      umma4_bf16_ss_w(tmem + 256 * t, dsc(q4, t * TILE, 16), dsc(k4, ks * 2 * TILE, 16), 2, 2, idesc_s, 0);
+      umma_commit_w(&sm.s_full[t]);
+      umma_commit_w(&sm.q_free[t]);
+    };
+    auto issue_pv = [&](int i, int t) {
+      mbar_wait(&sm.p_full[t], i & 1);
+      tc_fence_after();
+      FTL(4 + t);
+      // O_t (cols 256t + 128 ..) = P_t V: P from TMEM (bf16 pairs over the first 128 S columns)
+      // the second 64-dim atom of B sits LBO bytes after the step's V rows: LBO points every step at
+      // the ones tile (the step adds 2048 B to the address and removes it from LBO)
+      const uint64_t bstep = (uint64_t)((int64_t)(2048 >> 4) - ((int64_t)(2048 >> 4) << 16));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16_ss_w(tmem + 256 * t, dsc(q4, t * TILE + kk * 32, 16), dsc(k4, kk * 32, 16), idesc_s, kk > 0);
-          umma_commit_w(&sm.s_full[t]);
-        }
-        umma_commit_w(&sm.qk_free);
-        mbar_wait(&sm.v_full, par);
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&sm.p_full[t], par);
-          tc_fence_after();
-          // O_t (cols 256t + 128 ..) += P_t V: P from TMEM (bf16 pairs over the first 128 S columns)
-#pragma unroll
-          for (int ks = 0; ks < 16; ++ks)
-            umma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + 8 * ks, dsc(v4, ks * 2048, 8192), idesc_o, ks > 0);
-          umma_commit_w(&sm.o_full[t]);
-        }
+      for (int g = 0; g < 4; ++g)
+        umma4_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + 32 * g, dsc(v4, g * 4 * 2048, ones_off - g * 4 * 2048), 8,
+                        bstep, idesc_o, g > 0);
+      // S = 257: key 256 as a 17th K-step (P of keys 256..271 = (p_256, 0, ..) at columns 208..215,
+      // value rows 256..271 = (v_256, 0, ..)); its p also lands in the ones columns' row sum
+      if (has_tail) umma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + 208, dsc(vx4, 0, F_ONES - F_VX), idesc_o, 1);
+      umma_commit_w(&sm.o_full[t]);
+    };
+    int i = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      mbar_wait(&sm.k_full[i & 1], (i >> 1) & 1);
+      FTL(0);
+      issue_s(i, 0);
+      if (i > 0) {
+        issue_pv(i - 1, 1);
         umma_commit_w(&sm.v_free);
       }
+      issue_s(i, 1);
+      umma_commit_w(&sm.k_free[i & 1]);
+      mbar_wait(&sm.v_full, i & 1);
+      FTL(3);
+      issue_pv(i, 0);
+    }
+    if (i > 0) {
+      issue_pv(i - 1, 1);
+      umma_commit_w(&sm.v_free);
     }
   } else if (warp < 10) {
-    // softmax/epilogue warpgroup g owns query tile t = g; TMEM lane quarter = warp % 4
+    // ------------------------------ softmax / epilogue warpgroups ------------------------------
     const int t = (warp - 2) >> 2;
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;  // query row within the tile
     const int wtid = threadIdx.x - 64 - 128 * t;
+    const uint32_t taddr = tmem + ((quarter * 32) << 16) + 256 * t;
+    uint8_t* o16 = smem + F_ST + t * 2 * TILE;  // [128 rows][64 bf16], 128B swizzle
+    uint8_t* olo = o16 + TILE;                   // [128 rows][64 bf16] residual
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const uint32_t par = i & 1;
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
-      // previous unit's TMA stores must have finished reading this tile's P buffer
-      if (wtid == 0) bulk_wait_read0();
-      named_bar(1 + t, 128);
-      mbar_wait(&sm.s_full[t], par);  // also implies Q/K (and key 256) landed in smem
-      // score against the 257th key (CUDA cores): q row from the staged Q tile, k row 256 from smem
+      // S = 257: the score against key 256 (q_r . k_256) on CUDA cores while S_t is computed
       float s_last = -INFINITY;
       if (has_tail) {
-        const uint8_t* qt = smem + F_Q + t * TILE;
-        const uint8_t* kr = sm.krow;
-        float a = 0.f;
+        mbar_wait(&sm.k_full[i & 1], (i >> 1) & 1);
+        mbar_wait(&sm.q_full[t], par);
+        s_last = dot64_tile_row(smem + F_Q + t * TILE, r, sm.krow[i & 1]);
+        mbar_arrive(&sm.q_free[t]);      // done with the Q tile
+        mbar_arrive(&sm.k_free[i & 1]);  // and with key row 256
+      }
+      if (quarter == 2) FTL(8 + t);
+      mbar_wait(&sm.s_full[t], par);
+      if (quarter == 2) FTL(10 + t);
+      // take the turn on the exponentials: warpgroup 1 after warpgroup 0 of the same unit,
+      // warpgroup 0 after warpgroup 1 of the previous unit
+      if (t == 1) mbar_wait(&sm.exp_turn[0], par);
+      else if (i > 0) mbar_wait(&sm.exp_turn[1], par ^ 1);
+      if (quarter == 2) FTL(12 + t);
+      tc_fence_after();
+      // One pass over S: the exponent offset m is the maximum of the first 64 keys (and key 256);
+      // a later chunk only moves it when its maximum exceeds m by more than 2^32 in probability,
+      // rescaling the probabilities already written. Any offset within that range gives the same
+      // bf16 probabilities relative to each other (the row sum comes from the PV MMA's ones columns,
+      // lse = m + log(sum)), so the max pass is not needed.
+      float m = s_last, mb = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[64];
+        tmem_ld_32x32b_x32(taddr + 64 * c, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld_32x32b_x32(taddr + 64 * c + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        tmem_ld_wait();
+        float m4[4] = {__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3])};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 w = *reinterpret_cast<const uint4*>(qt + sw128(r, c));
-          const uint4 kw = *reinterpret_cast<const uint4*>(kr + ((c ^ 0) << 4));
-          const uint32_t qa[4] = {w.x, w.y, w.z, w.w}, ka[4] = {kw.x, kw.y, kw.z, kw.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 x = unpack_bf16(qa[e]), y = unpack_bf16(ka[e]);
-            a += x.x * y.x + x.y * y.y;
+        for (int j = 4; j < 64; j += 8) {
+          m4[0] = fmax3(m4[0], __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+          m4[1] = fmax3(m4[1], __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+          if (j + 4 < 64) {
+            m4[2] = fmax3(m4[2], __uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+            m4[3] = fmax3(m4[3], __uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
           }
         }
-        s_last = a;
-      }
-      mbar_arrive(&sm.qk_free);  // done with the Q tile and key row 256
-      tc_fence_after();
-      const uint32_t taddr = tmem + ((quarter * 32) << 16) + 256 * t;
-      float mx = s_last;
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(taddr + 32 * c, v);
-        tmem_ld_wait();
+        const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        if (c == 0) {
+          m = fmaxf(m, cm);
+          mb = m * c2;
+        } else if (__any_sync(0xffffffffu, (cm - m) * c2 > 32.f)) {
+          // rare: rescale the probabilities of chunks 0..c-1 (warp-uniform branch: the TMEM
+          // accesses are warp-collective; rows that keep their offset scale by 1)
+          const float mn = (cm - m) * c2 > 32.f ? cm : m;
+          const float fs = ex2((m - mn) * c2);
+          tmem_st_wait();
+          for (int cc = 0; cc < 2 * c; ++cc) {
+            uint32_t w[16];
+            tmem_ld_32x32b_x16(taddr + 16 * cc, w);
+            tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(v[j]));
-      }
-      const float mb = mx * c2;
-      float sum = 0.f;
-      uint8_t* pbuf = smem + (t ? F_P1 : F_P0);
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(taddr + 32 * c, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const float p0 = ex2(__uint_as_float(v[j]) * c2 - mb);
-          const float p1 = ex2(__uint_as_float(v[j + 1]) * c2 - mb);
-          pk[j / 2] = pack_bf16(p0, p1);
-          const float2 pr = unpack_bf16(pk[j / 2]);  // normalise with the probabilities the MMA sees
-          sum += pr.x + pr.y;
+            for (int e = 0; e < 16; ++e) {
+              const float2 x = unpack_bf16(w[e]);
+              w[e] = pack_bf16(x.x * fs, x.y * fs);
+            }
+            tmem_st_32x32b_x16(taddr + 16 * cc, w);
+          }
+          m = mn;
+          mb = m * c2;
         }
-        // keys 32c..32c+31 -> TMEM columns 16c..16c+15 as bf16 pairs (S columns already loaded)
-        tmem_st_32x32b_x16(taddr + 16 * c, pk);
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(v[j]), c2, -mb));
+          const float p1 = ex2(fmaf(__uint_as_float(v[j + 1]), c2, -mb));
+          pk[j / 2] = pack_bf16(p0, p1);
+        }
+        // keys 64c..64c+63 -> TMEM columns 32c..32c+31 as bf16 pairs (S columns already loaded)
+        tmem_st_32x32b_x16(taddr + 32 * c, *reinterpret_cast<uint32_t(*)[16]>(pk));
+        tmem_st_32x32b_x16(taddr + 32 * c + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
       }
-      const float plast = has_tail ? ex2(s_last * c2 - mb) : 0.f;
-      sum += plast;
+      const float mx = m;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.exp_turn[t]);
+      if (has_tail) {  // key 256: (p_256, 0) and zeros over the 17th K-step's columns 208..215
+        const uint32_t px[8] = {pack_bf16(ex2(s_last * c2 - mb), 0.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        tmem_st_32x32b_x8(taddr + 208, px);
+      }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
+      if (quarter == 2) FTL(16 + t);
       // O epilogue: stage O (bf16) and, for the backward's Delta, its rounding residual O - bf16(O)
-      // (bf16: O to ~16 bits) in this tile's staging buffer, TMA-store both
+      // (bf16: O to ~16 bits), TMA-store both
+      float sum;
+      if (wtid == 0) bulk_wait_read0();  // the previous unit's stores have read the staging tiles
+      named_bar(1 + t, 128);
       mbar_wait(&sm.o_full[t], par);
+      if (quarter == 2) FTL(18 + t);
       tc_fence_after();
-      const float inv = 1.0f / sum;
-      const uint8_t* vrow = sm.vrow;
-      uint8_t* o16 = pbuf;             // [128 rows][64 bf16], 128B swizzle
-      uint8_t* olo = pbuf + TILE;      // [128 rows][64 bf16] residual
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(taddr + 128 + 32 * c, v);
+      {
+        uint32_t v[64];
+        tmem_ld_32x32b_x32(taddr + 128, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld_32x32b_x32(taddr + 160, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        const uint32_t srow = tmem_ld_32x32b_x1(taddr + 192);  // sum of the bf16 P row (MMA, fp32)
         tmem_ld_wait();
-        float o[32];
+        tc_fence_before();
+        mbar_arrive_relaxed(&sm.tmem_free[t]);  // only TMEM reads precede (tcgen05.wait::ld done)
+        sum = __uint_as_float(srow);
+        const float inv = 1.0f / sum;
+        if (quarter == 2) FTL(22 + t);
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const float2 vl = has_tail ? unpack_bf16(*reinterpret_cast<const uint32_t*>(vrow + 2 * (32 * c + j)))
-                                     : make_float2(0.f, 0.f);
-          o[j] = (__uint_as_float(v[j]) + plast * vl.x) * inv;
-          o[j + 1] = (__uint_as_float(v[j + 1]) + plast * vl.y) * inv;
-        }
+        for (int q = 0; q < 8; ++q) {
+          float o[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(o16 + sw128(r, 4 * c + q)) =
-              make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
-                         pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
-        if (out_lo) {
-          uint32_t lo[16];
+          for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(v[8 * q + e]) * inv;
+          uint32_t hi[4];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 hi = unpack_bf16(pack_bf16(o[2 * e], o[2 * e + 1]));
-            lo[e] = pack_bf16(o[2 * e] - hi.x, o[2 * e + 1] - hi.y);
+          for (int e = 0; e < 4; ++e) hi[e] = pack_bf16(o[2 * e], o[2 * e + 1]);
+          *reinterpret_cast<uint4*>(o16 + sw128(r, q)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          if (out_lo) {
+            uint32_t lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 hf = unpack_bf16(hi[e]);
+              lo[e] = pack_bf16(o[2 * e] - hf.x, o[2 * e + 1] - hf.y);
+            }
+            *reinterpret_cast<uint4*>(olo + sw128(r, q)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(olo + sw128(r, 4 * c + q)) = make_uint4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
         }
       }
-      mbar_arrive(&sm.v_free);  // done with value row 256
+      if (quarter == 2) FTL(24 + t);
       fence_proxy_async();
       named_bar(1 + t, 128);
+      if (quarter == 2) FTL(26 + t);
       if (wtid == 0) {
         tma_store_2d(&tm_o, o16, h * 64, (int)(row0 + 128 * t));
         if (out_lo) tma_store_2d(&tm_olo, olo, h * 64, (int)(row0 + 128 * t));
         bulk_commit();
       }
       lse[((int64_t)f * H + h) * S + 128 * t + r] = mx * 0.125f + logf(sum);
-      tc_fence_before();
-      mbar_arrive_relaxed(&sm.tmem_free[t]);  // only TMEM reads precede (tcgen05.wait::ld done)
+      if (quarter == 2) FTL(20 + t);
     }
   } else if (has_tail) {
-    // tail warps: query row 256 on CUDA cores, reading K/V from the staged smem tiles
+    // ------------------------------ tail warps (S = 257) ------------------------------
+    // query row 256 against every key on CUDA cores (the key-256 column is formed by the softmax
+    // warps, key 256's value row rides on the PV MMA)
     const int tid = threadIdx.x - 320;  // 0 .. kFwdTailThreads - 1
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const uint32_t par = i & 1;
+      const int ks = i & 1;
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
       const __nv_bfloat16* q = qkv + (row0 + 256) * 3 * D + h * 64;
-      float qf[64];
+      uint4 qw[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) qw[c] = reinterpret_cast<const uint4*>(q)[c];
+      const uint32_t qpair = *reinterpret_cast<const uint32_t*>(q + 2 * lane);  // dims 2 lane, 2 lane + 1
+      if (tid == 0) FTL(40);
+      mbar_wait(&sm.k_full[ks], (i >> 1) & 1);
+      if (tid == 0) FTL(41);
+      // scores against keys tid and 128 + tid (four partial sums each), key 256 by warp 10
+      const uint8_t* kt = smem + F_K + ks * 2 * TILE;
+      float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        uint4 w = reinterpret_cast<const uint4*>(q)[c];
-        float2 a = unpack_bf16(w.x), b = unpack_bf16(w.y), cc = unpack_bf16(w.z), d = unpack_bf16(w.w);
-        qf[8 * c] = a.x; qf[8 * c + 1] = a.y; qf[8 * c + 2] = b.x; qf[8 * c + 3] = b.y;
-        qf[8 * c + 4] = cc.x; qf[8 * c + 5] = cc.y; qf[8 * c + 6] = d.x; qf[8 * c + 7] = d.y;
-      }
-      // key 256 from global, keys 0..255 from the swizzled K tile
-      float mx = -INFINITY;
-      mbar_wait(&sm.qk_full, par);
-      if (tid == 0) {
-        const uint4* kp = reinterpret_cast<const uint4*>(sm.krow);
-        float a = 0.f;
+        const uint4 w0 = *reinterpret_cast<const uint4*>(kt + sw128(tid, c));
+        const uint4 w1 = *reinterpret_cast<const uint4*>(kt + TILE + sw128(tid, c));
+        const uint32_t qa[4] = {qw[c].x, qw[c].y, qw[c].z, qw[c].w};
+        const uint32_t k0[4] = {w0.x, w0.y, w0.z, w0.w}, k1[4] = {w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 w = kp[c];
-          float2 x0 = unpack_bf16(w.x), x1 = unpack_bf16(w.y), x2 = unpack_bf16(w.z), x3 = unpack_bf16(w.w);
-          a += qf[8 * c] * x0.x + qf[8 * c + 1] * x0.y + qf[8 * c + 2] * x1.x + qf[8 * c + 3] * x1.y +
-               qf[8 * c + 4] * x2.x + qf[8 * c + 5] * x2.y + qf[8 * c + 6] * x3.x + qf[8 * c + 7] * x3.y;
+        for (int e = 0; e < 4; ++e) {
+          const float2 x = unpack_bf16(qa[e]), y0 = unpack_bf16(k0[e]), y1 = unpack_bf16(k1[e]);
+          a0[e] = fmaf(x.y, y0.y, fmaf(x.x, y0.x, a0[e]));
+          a1[e] = fmaf(x.y, y1.y, fmaf(x.x, y1.x, a1[e]));
         }
-        sm.tail_s[256] = a;
-        mx = a;
       }
-      for (int k = tid; k < 256; k += kFwdTailThreads) {
-        const uint8_t* kt = smem + F_K + (k >> 7) * TILE;
-        float a = 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 w = *reinterpret_cast<const uint4*>(kt + sw128(k & 127, c));
-          float2 x0 = unpack_bf16(w.x), x1 = unpack_bf16(w.y), x2 = unpack_bf16(w.z), x3 = unpack_bf16(w.w);
-          a += qf[8 * c] * x0.x + qf[8 * c + 1] * x0.y + qf[8 * c + 2] * x1.x + qf[8 * c + 3] * x1.y +
-               qf[8 * c + 4] * x2.x + qf[8 * c + 5] * x2.y + qf[8 * c + 6] * x3.x + qf[8 * c + 7] * x3.y;
-        }
-        sm.tail_s[k] = a;
-        mx = fmaxf(mx, a);
+      const float s0 = (a0[0] + a0[1]) + (a0[2] + a0[3]);
+      const float s1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+      float s256 = -INFINITY;
+      if (warp == 10) {
+        const float2 x = unpack_bf16(qpair), y = unpack_bf16(*reinterpret_cast<const uint32_t*>(sm.krow[ks] + 4 * lane));
+        s256 = warp_sum(fmaf(x.y, y.y, x.x * y.x));
       }
-      mbar_arrive(&sm.qk_free);
-      mx = warp_max(mx);
+      mbar_arrive(&sm.k_free[ks]);
+      float mx = warp_max(fmax3(s0, s1, s256));
       if (lane == 0) sm.tail_red[warp - 10] = mx;
       named_bar(3, kFwdTailThreads);
-      mx = sm.tail_red[0];
-#pragma unroll
-      for (int w = 1; w < kFwdTailWarps; ++w) mx = fmaxf(mx, sm.tail_red[w]);
+      mx = fmaxf(fmaxf(sm.tail_red[0], sm.tail_red[1]), fmaxf(sm.tail_red[2], sm.tail_red[3]));
       const float mb = mx * c2;
-      float sum = 0.f;
-      for (int k = tid; k < S; k += kFwdTailThreads) {
-        const float p = ex2(sm.tail_s[k] * c2 - mb);
-        sm.tail_s[k] = p;
-        sum += p;
+      const float p0 = ex2(s0 * c2 - mb), p1 = ex2(s1 * c2 - mb);
+      sm.tail_s[tid] = p0;
+      sm.tail_s[128 + tid] = p1;
+      float sum = p0 + p1;
+      if (tid == 0) {
+        const float p256 = ex2(s256 * c2 - mb);
+        sm.tail_s[256] = p256;
+        sum += p256;
       }
       sum = warp_sum(sum);
       if (lane == 0) sm.tail_red[kFwdTailWarps + warp - 10] = sum;
       named_bar(3, kFwdTailThreads);
-      sum = 0.f;
-#pragma unroll
-      for (int w = 0; w < kFwdTailWarps; ++w) sum += sm.tail_red[kFwdTailWarps + w];
-      // o[d] for d = 2*(tid&31) .. +1, keys split into kFwdTailWarps parts by warp
+      sum = (sm.tail_red[kFwdTailWarps] + sm.tail_red[kFwdTailWarps + 1]) +
+            (sm.tail_red[kFwdTailWarps + 2] + sm.tail_red[kFwdTailWarps + 3]);
+      // o[d] for d = 2 lane, 2 lane + 1; keys split into kFwdTailWarps parts by warp; even / odd keys
+      // accumulate separately
       constexpr int KP = 256 / kFwdTailWarps;
-      const int dpair = tid & 31, part = tid >> 5;
-      float o0 = 0.f, o1 = 0.f;
+      const int dpair = lane, part = tid >> 5;
+      float oa0 = 0.f, oa1 = 0.f, ob0 = 0.f, ob1 = 0.f;
+      if (tid == 0) FTL(44);
       mbar_wait(&sm.v_full, par);
+      if (tid == 0) FTL(45);
       const uint32_t chunk = dpair >> 2, within = (dpair & 3) * 4;
+      const uint8_t* vt = smem + F_V + (part >> 1) * TILE;  // a part's 64 keys lie in one tile
 #pragma unroll 8
-      for (int k = part * KP; k < part * KP + KP; ++k) {
-        const uint8_t* vt = smem + F_V + (k >> 7) * TILE;
-        const float2 v = unpack_bf16(*reinterpret_cast<const uint32_t*>(vt + sw128(k & 127, chunk) + within));
-        const float p = sm.tail_s[k];
-        o0 += p * v.x;
-        o1 += p * v.y;
+      for (int k = (part * KP) & 127; k < ((part * KP) & 127) + KP; k += 2) {
+        const float2 va = unpack_bf16(*reinterpret_cast<const uint32_t*>(vt + sw128(k, chunk) + within));
+        const float2 vb = unpack_bf16(*reinterpret_cast<const uint32_t*>(vt + sw128(k + 1, chunk) + within));
+        const float2 pp = *reinterpret_cast<const float2*>(sm.tail_s + (part >> 1) * 128 + k);
+        oa0 = fmaf(pp.x, va.x, oa0);
+        oa1 = fmaf(pp.x, va.y, oa1);
+        ob0 = fmaf(pp.y, vb.x, ob0);
+        ob1 = fmaf(pp.y, vb.y, ob1);
       }
-      if (part == kFwdTailWarps - 1) {  // value row 256, read before this thread releases V
-        const float2 vl = unpack_bf16(*reinterpret_cast<const uint32_t*>(sm.vrow + 4 * dpair));
+      float o0 = oa0 + ob0, o1 = oa1 + ob1;
+      if (part == kFwdTailWarps - 1) {  // value row 256 (row 0 of the PV MMA's 17th K-step tile)
+        const float2 vl = unpack_bf16(*reinterpret_cast<const uint32_t*>(smem + F_VX + 4 * dpair));
         const float p256 = sm.tail_s[256];
-        o0 += p256 * vl.x;
-        o1 += p256 * vl.y;
+        o0 = fmaf(p256, vl.x, o0);
+        o1 = fmaf(p256, vl.y, o1);
       }
       mbar_arrive(&sm.v_free);
+      if (tid == 0) FTL(46);
       named_bar(3, kFwdTailThreads);  // every part is done reading the probabilities in tail_s
       if (part > 0) {                 // partial outputs of parts 1.. into tail_s
         sm.tail_s[(part - 1) * 64 + 2 * dpair] = o0;
@@ -422,6 +546,12 @@ extern "C" int jz_attn_spatial_fwd(const void* qkv, int64_t frames, int S, int H
   JZ_LAUNCH_CHECK();
   return JZ_OK;
 }
+
+#ifdef JZ_SPATIAL_FWD_PROF
+extern "C" int jz_attn_fwd_prof_read(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, jz::g_ftl, sizeof(jz::g_ftl)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // ============================================================================
 // Backward: the tcgen05 kernel is csrc/attn_spatial_bwd.cu (v3); this file keeps the pass that

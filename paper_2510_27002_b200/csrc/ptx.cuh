@@ -267,7 +267,9 @@ JZ_DEV void umma4x2_bf16_ss_w(uint32_t d0, uint64_t a0, uint64_t b0, uint32_t d1
 }
 
 // Four K-steps into one accumulator, A from TMEM (columns advanced by `atstep`), B from shared memory.
-JZ_DEV void umma4_bf16_ts_w(uint32_t tmem_d, uint32_t a0, uint64_t bdesc, uint32_t atstep, uint32_t bstep,
+// `bstep` is added to the whole 64-bit descriptor, so a step may move the address and LBO fields
+// in opposite directions (two's-complement step).
+JZ_DEV void umma4_bf16_ts_w(uint32_t tmem_d, uint32_t a0, uint64_t bdesc, uint32_t atstep, uint64_t bstep,
                             uint32_t idesc, uint32_t acc0) {
   asm volatile(
       "{\n"

@@ -227,6 +227,36 @@ def test_attn_spatial_fwd_bwd(S, frames):
         assert rel(got.reshape(frames, S, D)[:, -1], ref.reshape(frames, S, D)[:, -1]) < 2e-2, "qkv"[i]
 
 
+@pytest.mark.parametrize("S", [257, 256])
+def test_attn_spatial_fwd_score_spread(S):
+    """Rows whose dominant key lies in a later 64-key chunk, by far more than 2^32 in probability
+    (the one-pass forward softmax rescales the probabilities it already wrote), and for S = 257 rows
+    dominated by key 256."""
+    H, frames = 8, 4
+    D = H * 64
+    g = torch.Generator(device=dev).manual_seed(7 + S)
+    x = torch.randn(frames * S, 3 * D, device=dev, generator=g)
+    q = x[:, :D].view(frames, S, H, 64)
+    k = x[:, D:2 * D].view(frames, S, H, 64)
+    q[0, 0:32, 0] = 4.0   # key 200 (chunk 3) against queries 0..31: scores 128 above the rest
+    k[0, 200, 0] = 4.0
+    q[1, 100:140, 3] = -3.0  # key 70 (chunk 1) against queries across both query tiles
+    k[1, 70, 3] = -3.0
+    if S == 257:
+        q[2, 5:9, 1] = 4.0  # key 256 (CUDA cores + the PV MMA's 17th K-step)
+        k[2, 256, 1] = 4.0
+    qkv = x.bfloat16()
+    out, out_lo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
+    o_ref, lse_ref = _ref_attn(qkv.float().reshape(frames, S, 3 * D), (frames,), S, H, False)
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
+    assert rel(out.reshape(frames, S, D), o_ref) < 1e-2
+    assert rel((out.float() + out_lo.float()).reshape(frames, S, D), o_ref) < 1e-2
+    assert rel(lse, lse_ref) < 1e-4
+    for f, rows, h in ((0, slice(0, 32), 0), (1, slice(100, 140), 3)) + (((2, slice(5, 9), 1),) if S == 257 else ()):
+        o = out.reshape(frames, S, H, 64)[f, rows, h].float()
+        assert rel(o, o_ref.reshape(frames, S, H, 64)[f, rows, h]) < 1e-2
+
+
 @pytest.mark.parametrize("T", [16, 5, 1])
 def test_attn_temporal_fwd_bwd(T):
     B, S, H = 2, 257, 8
