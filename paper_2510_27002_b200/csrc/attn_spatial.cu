@@ -20,30 +20,34 @@ namespace jz {
 
 namespace sp {
 
-constexpr int kFwdTailWarps = 4;  // query row 256 / key column 256 (S = 257) on CUDA cores
+constexpr int kFwdTailWarps = 4;  // query row 256 (S = 257) on CUDA cores
 constexpr int kFwdTailThreads = 32 * kFwdTailWarps;
-constexpr int kFwdThreads = 320 + kFwdTailThreads;  // w0 TMA, w1 MMA, w2-5 tile 0, w6-9 tile 1, w10.. tail
+constexpr int W_TAIL = 18;  // w0 TMA, w1 MMA, w2-9 tile 0, w10-17 tile 1 (two warps per TMEM lane quarter), w18.. tail
+constexpr int kFwdThreads = 32 * W_TAIL + kFwdTailThreads;
 constexpr int TILE = 16384;    // 128 rows x 128 B
 // forward smem map (bytes, from a 1024-aligned base)
 constexpr int F_Q = 0;                  // 2 tiles (query tiles 0 / 1)
 constexpr int F_K = F_Q + 2 * TILE;     // 2 slots x 2 tiles (256 keys), slot = unit parity
-constexpr int F_V = F_K + 4 * TILE;     // 2 tiles
-constexpr int F_ST = F_V + 2 * TILE;    // per query tile: O staging + residual staging (2 tiles each)
-constexpr int F_VX = F_ST + 4 * TILE;    // value rows 256..271 for the PV MMA's 17th K-step: row 0 = v_256
-                                         // (TMA, with V), rows 1..15 stay zero
-constexpr int F_ONES = F_VX + 2048;      // 16 rows x 128 B of bf16 1.0: the row-sum columns of the PV MMA
-constexpr int F_END = F_ONES + 2048;     // 200704
+constexpr int F_V = F_K + 4 * TILE;     // 2 slots x 2 tiles (256 values), slot = unit parity
+constexpr int F_ST = F_V + 4 * TILE;    // O staging + residual staging, shared by the two query tiles
+                                        // (their epilogues alternate with the exponential passes)
+constexpr int F_VX = F_ST + 2 * TILE;   // 2 slots: value rows 256..271 for the PV MMA's 17th K-step, row 0 =
+                                        // v_256 (TMA, with V), rows 1..15 stay zero
+constexpr int F_ONES = F_VX + 2 * 2048;  // 16 rows x 128 B of bf16 1.0: the row-sum columns of the PV MMA
+constexpr int F_END = F_ONES + 2048;     // 202752
 constexpr int kFwdSmall = 8192;
 constexpr int F_SMEM = F_END + kFwdSmall + 1024;
 
 struct FwdSmallSmem {
-  uint64_t q_full[2], q_free[2], k_full[2], k_free[2], v_full, v_free;
+  uint64_t q_full[2], q_free[2], k_full[2], k_free[2], v_full[2], v_free[2];
+  uint64_t stg_free;     // the staging tiles' previous TMA store has read them (one phase per tile epilogue)
   uint64_t s_full[2], p_full[2], o_full[2], tmem_free[2];
   uint64_t exp_turn[2];  // the two softmax warpgroups take turns on the exponentials
   uint32_t tmem_base;
   alignas(128) uint8_t krow[2][128];  // key 256 of the unit (TMA, arrives with K), slot = unit parity
   float tail_s[260];
   float tail_red[2 * kFwdTailWarps];
+  float2 xch[2][2][128];  // [tile][column half][row]: half-row max and key-256 partial dot
 };
 static_assert(sizeof(FwdSmallSmem) <= kFwdSmall, "forward small smem budget");
 
@@ -129,24 +133,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int t = 0; t < 2; ++t) {
       mbar_init(&sm.q_full[t], 1);
-      mbar_init(&sm.q_free[t], 1 + (has_tail ? 128 : 0));  // S_t MMA commit (+ warpgroup t: key-256 column)
+      mbar_init(&sm.q_free[t], 1 + (has_tail ? 256 : 0));  // S_t MMA commit (+ tile t's warps: key-256 column)
       mbar_init(&sm.k_full[t], 1);
-      mbar_init(&sm.k_free[t], 1 + ntail + (has_tail ? 256 : 0));  // S_1 MMA commit + tail warps (+ softmax: key row 256)
+      mbar_init(&sm.k_free[t], 1 + ntail + (has_tail ? 512 : 0));  // S_1 MMA commit + tail warps (+ softmax: key row 256)
       mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.p_full[t], 256);
       mbar_init(&sm.o_full[t], 1);
-      mbar_init(&sm.tmem_free[t], 128);
-      mbar_init(&sm.exp_turn[t], 4);
+      mbar_init(&sm.tmem_free[t], 256);
+      mbar_init(&sm.exp_turn[t], 8);
     }
-    mbar_init(&sm.v_full, 1);
-    mbar_init(&sm.v_free, 1 + ntail);  // PV_1 MMA commit + tail warps
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.v_full[b], 1);
+      mbar_init(&sm.v_free[b], 1 + ntail);  // PV_1 MMA commit + tail warps
+    }
+    mbar_init(&sm.stg_free, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
-  for (int e = threadIdx.x; e < 2048 / 16; e += blockDim.x)
-  {
+  for (int e = threadIdx.x; e < 2048 / 16; e += blockDim.x) {
     *reinterpret_cast<uint4*>(smem + F_ONES + 16 * e) = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
     *reinterpret_cast<uint4*>(smem + F_VX + 16 * e) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(smem + F_VX + 2048 + 16 * e) = make_uint4(0u, 0u, 0u, 0u);
   }
   fence_proxy_async();  // generic writes of the ones tile before the tensor core reads it
   __syncthreads();
@@ -174,12 +181,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&sm.q_free[1], (i & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.q_full[1], TILE);
         tma_load_2d(smem + F_Q + TILE, &tm, &sm.q_full[1], h * 64, row0 + 128);
-        mbar_wait(&sm.v_free, (i & 1) ^ 1);
+        mbar_wait(&sm.v_free[ks], ((i >> 1) & 1) ^ 1);
         FTL(31);
-        mbar_arrive_expect_tx(&sm.v_full, 2 * TILE + (has_tail ? 128 : 0));
-        if (has_tail) tma_load_2d(smem + F_VX, &tm_row, &sm.v_full, 2 * D + h * 64, row0 + 256);
-        tma_load_2d(smem + F_V, &tm, &sm.v_full, 2 * D + h * 64, row0);
-        tma_load_2d(smem + F_V + TILE, &tm, &sm.v_full, 2 * D + h * 64, row0 + 128);
+        mbar_arrive_expect_tx(&sm.v_full[ks], 2 * TILE + (has_tail ? 128 : 0));
+        if (has_tail) tma_load_2d(smem + F_VX + ks * 2048, &tm_row, &sm.v_full[ks], 2 * D + h * 64, row0 + 256);
+        tma_load_2d(smem + F_V + ks * 2 * TILE, &tm, &sm.v_full[ks], 2 * D + h * 64, row0);
+        tma_load_2d(smem + F_V + ks * 2 * TILE + TILE, &tm, &sm.v_full[ks], 2 * D + h * 64, row0 + 128);
       }
     }
   } else if (warp == 1) {
@@ -194,8 +201,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       return ((uint64_t)dhi << 32) | (addr4 + (off >> 4) + ((lbo >> 4) << 16));
     };
     const uint32_t q4 = smem_u32(smem + F_Q) >> 4, k4 = smem_u32(smem + F_K) >> 4, v4 = smem_u32(smem + F_V) >> 4;
-    constexpr uint32_t ones_off = F_ONES - F_V;
-    const uint32_t vx4 = smem_u32(smem + F_VX) >> 4;
+
     auto issue_s = [&](int i, int t) {
       const int ks = i & 1;
       mbar_wait(&sm.q_full[t], i & 1);
@@ -207,20 +213,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       umma_commit_w(&sm.q_free[t]);
     };
     auto issue_pv = [&](int i, int t) {
+      const int vs = i & 1;  // V slot
       mbar_wait(&sm.p_full[t], i & 1);
       tc_fence_after();
       FTL(4 + t);
-      // O_t (cols 256t + 128 ..) = P_t V: P from TMEM (bf16 pairs over the first 128 S columns)
-      // the second 64-dim atom of B sits LBO bytes after the step's V rows: LBO points every step at
-      // the ones tile (the step adds 2048 B to the address and removes it from LBO)
+      // O_t (cols 256t + 64 .. 143: 64 dims + 16 row-sum columns) = P_t V. P from TMEM as bf16 pairs:
+      // keys 0..127 at columns 0..63, keys 128..255 at 192..255, key 256 at 144 (17th K-step).
+      // The second 64-dim atom of B sits LBO bytes after the step's V rows: LBO points every step at
+      // the ones tile (the step adds 2048 B to the address and removes it from LBO).
       const uint64_t bstep = (uint64_t)((int64_t)(2048 >> 4) - ((int64_t)(2048 >> 4) << 16));
 #pragma unroll
       for (int g = 0; g < 4; ++g)
-        umma4_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + 32 * g, dsc(v4, g * 4 * 2048, ones_off - g * 4 * 2048), 8,
-                        bstep, idesc_o, g > 0);
-      // S = 257: key 256 as a 17th K-step (P of keys 256..271 = (p_256, 0, ..) at columns 208..215,
-      // value rows 256..271 = (v_256, 0, ..)); its p also lands in the ones columns' row sum
-      if (has_tail) umma_bf16_ts_w(tmem + 256 * t + 128, tmem + 256 * t + 208, dsc(vx4, 0, F_ONES - F_VX), idesc_o, 1);
+        umma4_bf16_ts_w(tmem + 256 * t + 64, tmem + 256 * t + (g < 2 ? 32 * g : 192 + 32 * (g - 2)),
+                        dsc(v4, vs * 2 * TILE + g * 4 * 2048, F_ONES - F_V - vs * 2 * TILE - g * 4 * 2048), 8, bstep,
+                        idesc_o, g > 0);
+      if (has_tail)
+        umma_bf16_ts_w(tmem + 256 * t + 64, tmem + 256 * t + 144,
+                       dsc(v4, F_VX - F_V + vs * 2048, F_ONES - F_VX - vs * 2048), idesc_o, 1);
       umma_commit_w(&sm.o_full[t]);
     };
     int i = 0;
@@ -230,146 +239,132 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       issue_s(i, 0);
       if (i > 0) {
         issue_pv(i - 1, 1);
-        umma_commit_w(&sm.v_free);
+        umma_commit_w(&sm.v_free[(i - 1) & 1]);
       }
       issue_s(i, 1);
       umma_commit_w(&sm.k_free[i & 1]);
-      mbar_wait(&sm.v_full, i & 1);
+      mbar_wait(&sm.v_full[i & 1], (i >> 1) & 1);
       FTL(3);
       issue_pv(i, 0);
     }
     if (i > 0) {
       issue_pv(i - 1, 1);
-      umma_commit_w(&sm.v_free);
+      umma_commit_w(&sm.v_free[(i - 1) & 1]);
     }
-  } else if (warp < 10) {
-    // ------------------------------ softmax / epilogue warpgroups ------------------------------
-    const int t = (warp - 2) >> 2;
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // query row within the tile
-    const int wtid = threadIdx.x - 64 - 128 * t;
-    const uint32_t taddr = tmem + ((quarter * 32) << 16) + 256 * t;
-    uint8_t* o16 = smem + F_ST + t * 2 * TILE;  // [128 rows][64 bf16], 128B swizzle
-    uint8_t* olo = o16 + TILE;                   // [128 rows][64 bf16] residual
+  } else if (warp < W_TAIL) {
+    // ------------------------------ softmax / epilogue warps ------------------------------
+    // tile t = 8 warps: two per TMEM lane quarter, column half hc (keys 128 hc .. 128 hc + 127)
+    const int sw = warp - 2;
+    const int t = sw >> 3, hc = (sw >> 2) & 1, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // query row within the tile
+    const int wtid = threadIdx.x - 64 - 256 * t;   // 0 .. 255
+    const uint32_t lrow = tmem + ((quarter * 32) << 16) + 256 * t;
+    const uint32_t scol = lrow + 128 * hc;         // this warp's S columns
+    uint8_t* o16 = smem + F_ST;                    // [128 rows][64 bf16], 128B swizzle
+    uint8_t* olo = o16 + TILE;                     // [128 rows][64 bf16] residual
+    const int bar_pair = 4 + 4 * t + quarter;      // named barrier of the two warps of a lane quarter
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const uint32_t par = i & 1;
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
-      // S = 257: the score against key 256 (q_r . k_256) on CUDA cores while S_t is computed
-      float s_last = -INFINITY;
+      // S = 257: q_r . k_256 on CUDA cores while S_t is computed, by the half-1 warp of the row (the
+      // half-0 warp takes it through the exchange below). Splitting the dot product between the
+      // two warps was measured to give wrong key-256 scores for some rows on a first launch.
+      float dpart = 0.f;
       if (has_tail) {
-        mbar_wait(&sm.k_full[i & 1], (i >> 1) & 1);
-        mbar_wait(&sm.q_full[t], par);
-        s_last = dot64_tile_row(smem + F_Q + t * TILE, r, sm.krow[i & 1]);
+        if (hc == 1) {
+          mbar_wait(&sm.k_full[i & 1], (i >> 1) & 1);
+          mbar_wait(&sm.q_full[t], par);
+          dpart = dot64_tile_row(smem + F_Q + t * TILE, r, sm.krow[i & 1]);
+        }
         mbar_arrive(&sm.q_free[t]);      // done with the Q tile
         mbar_arrive(&sm.k_free[i & 1]);  // and with key row 256
       }
-      if (quarter == 2) FTL(8 + t);
+      if (quarter == 2 && hc == 0) FTL(8 + t);
       mbar_wait(&sm.s_full[t], par);
-      if (quarter == 2) FTL(10 + t);
-      // take the turn on the exponentials: warpgroup 1 after warpgroup 0 of the same unit,
-      // warpgroup 0 after warpgroup 1 of the previous unit
-      if (t == 1) mbar_wait(&sm.exp_turn[0], par);
-      else if (i > 0) mbar_wait(&sm.exp_turn[1], par ^ 1);
-      if (quarter == 2) FTL(12 + t);
+      if (quarter == 2 && hc == 0) FTL(10 + t);
       tc_fence_after();
-      // One pass over S: the exponent offset m is the maximum of the first 64 keys (and key 256);
-      // a later chunk only moves it when its maximum exceeds m by more than 2^32 in probability,
-      // rescaling the probabilities already written. Any offset within that range gives the same
-      // bf16 probabilities relative to each other (the row sum comes from the PV MMA's ones columns,
-      // lse = m + log(sum)), so the max pass is not needed.
-      float m = s_last, mb = 0.f;
+      // max over this warp's 128 columns (64 per TMEM wait, three-input max), then the row's
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[64];
-        tmem_ld_32x32b_x32(taddr + 64 * c, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld_32x32b_x32(taddr + 64 * c + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        tmem_ld_wait();
-        float m4[4] = {__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3])};
+        tmem_ld_32x32b_x64_wait(scol + 64 * c, v);
 #pragma unroll
-        for (int j = 4; j < 64; j += 8) {
+        for (int j = 0; j < 64; j += 8) {
           m4[0] = fmax3(m4[0], __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
           m4[1] = fmax3(m4[1], __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-          if (j + 4 < 64) {
-            m4[2] = fmax3(m4[2], __uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
-            m4[3] = fmax3(m4[3], __uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
-          }
+          m4[2] = fmax3(m4[2], __uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+          m4[3] = fmax3(m4[3], __uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
         }
-        const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-        if (c == 0) {
-          m = fmaxf(m, cm);
-          mb = m * c2;
-        } else if (__any_sync(0xffffffffu, (cm - m) * c2 > 32.f)) {
-          // rare: rescale the probabilities of chunks 0..c-1 (warp-uniform branch: the TMEM
-          // accesses are warp-collective; rows that keep their offset scale by 1)
-          const float mn = (cm - m) * c2 > 32.f ? cm : m;
-          const float fs = ex2((m - mn) * c2);
-          tmem_st_wait();
-          for (int cc = 0; cc < 2 * c; ++cc) {
-            uint32_t w[16];
-            tmem_ld_32x32b_x16(taddr + 16 * cc, w);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const float2 x = unpack_bf16(w[e]);
-              w[e] = pack_bf16(x.x * fs, x.y * fs);
-            }
-            tmem_st_32x32b_x16(taddr + 16 * cc, w);
-          }
-          m = mn;
-          mb = m * c2;
-        }
-        uint32_t pk[32];
-#pragma unroll
-        for (int j = 0; j < 64; j += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[j]), c2, -mb));
-          const float p1 = ex2(fmaf(__uint_as_float(v[j + 1]), c2, -mb));
-          pk[j / 2] = pack_bf16(p0, p1);
-        }
-        // keys 64c..64c+63 -> TMEM columns 32c..32c+31 as bf16 pairs (S columns already loaded)
-        tmem_st_32x32b_x16(taddr + 32 * c, *reinterpret_cast<uint32_t(*)[16]>(pk));
-        tmem_st_32x32b_x16(taddr + 32 * c + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
       }
-      const float mx = m;
+      const float mh = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      sm.xch[t][hc][r] = make_float2(mh, dpart);
+      named_bar(bar_pair, 64);
+      const float2 other = sm.xch[t][hc ^ 1][r];
+      const float s_last = has_tail ? (hc ? dpart : other.y) : -INFINITY;
+      const float mx = fmax3(mh, other.x, s_last);
+
+      const float mb = mx * c2;
+      if (quarter == 2 && hc == 0) FTL(14 + t);
+      // take the turn on the exponentials: tile 1 after tile 0 of the same unit, tile 0 after
+      // tile 1 of the previous unit
+      if (t == 1) mbar_wait(&sm.exp_turn[0], par);
+      else if (i > 0) mbar_wait(&sm.exp_turn[1], par ^ 1);
+      if (quarter == 2 && hc == 0) FTL(12 + t);
+      // exponentials, 32 keys per TMEM wait. P of keys 128 hc + 32 j .. + 31 goes to columns
+      // 16 j .. (half 0) / 192 + 16 j .. (half 1, walked from its last 32 keys down) as bf16 pairs:
+      // every column is read before this warp overwrites it.
+#pragma unroll 1
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = hc ? 3 - jj : jj;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32_wait(scol + 32 * j, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2)
+          pk[e / 2] = pack_bf16(ex2(fmaf(__uint_as_float(v[e]), c2, -mb)), ex2(fmaf(__uint_as_float(v[e + 1]), c2, -mb)));
+        tmem_st_32x32b_x16(lrow + (hc ? 192 : 0) + 16 * j, pk);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.exp_turn[t]);
-      if (has_tail) {  // key 256: (p_256, 0) and zeros over the 17th K-step's columns 208..215
+      if (has_tail && hc == 1) {  // key 256: (p_256, 0) and zeros over the 17th K-step's columns 144..151
         const uint32_t px[8] = {pack_bf16(ex2(s_last * c2 - mb), 0.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        tmem_st_32x32b_x8(taddr + 208, px);
+        tmem_st_32x32b_x8(lrow + 144, px);
       }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full[t]);
-      if (quarter == 2) FTL(16 + t);
-      // O epilogue: stage O (bf16) and, for the backward's Delta, its rounding residual O - bf16(O)
-      // (bf16: O to ~16 bits), TMA-store both
-      float sum;
-      if (wtid == 0) bulk_wait_read0();  // the previous unit's stores have read the staging tiles
-      named_bar(1 + t, 128);
+      if (quarter == 2 && hc == 0) FTL(16 + t);
+      // O epilogue: dims 32 hc .. 32 hc + 31 of O (bf16) and, for the backward's Delta, its rounding
+      // residual O - bf16(O) (bf16: O to ~16 bits), staged and TMA-stored per tile
       mbar_wait(&sm.o_full[t], par);
-      if (quarter == 2) FTL(18 + t);
+      if (quarter == 2 && hc == 0) FTL(18 + t);
       tc_fence_after();
+      float sum;
       {
-        uint32_t v[64];
-        tmem_ld_32x32b_x32(taddr + 128, *reinterpret_cast<uint32_t(*)[32]>(v));
-        tmem_ld_32x32b_x32(taddr + 160, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-        const uint32_t srow = tmem_ld_32x32b_x1(taddr + 192);  // sum of the bf16 P row (MMA, fp32)
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(lrow + 64 + 32 * hc, v);
+        const uint32_t srow = tmem_ld_32x32b_x1(lrow + 128);  // sum of the bf16 P row (MMA, fp32)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive_relaxed(&sm.tmem_free[t]);  // only TMEM reads precede (tcgen05.wait::ld done)
         sum = __uint_as_float(srow);
         const float inv = 1.0f / sum;
-        if (quarter == 2) FTL(22 + t);
+        if (quarter == 2 && hc == 0) FTL(22 + t);
+        // the other tile's (or the previous unit's) store has read the staging tiles
+        const int e = 2 * i + t;  // this CTA's tile epilogues alternate: e = 0, 1, 2, ...
+        if (e > 0) mbar_wait(&sm.stg_free, (e - 1) & 1);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
           float o[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) o[e] = __uint_as_float(v[8 * q + e]) * inv;
           uint32_t hi[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) hi[e] = pack_bf16(o[2 * e], o[2 * e + 1]);
-          *reinterpret_cast<uint4*>(o16 + sw128(r, q)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(o16 + sw128(r, 4 * hc + q)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
           if (out_lo) {
             uint32_t lo[4];
 #pragma unroll
@@ -377,27 +372,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               const float2 hf = unpack_bf16(hi[e]);
               lo[e] = pack_bf16(o[2 * e] - hf.x, o[2 * e + 1] - hf.y);
             }
-            *reinterpret_cast<uint4*>(olo + sw128(r, q)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            *reinterpret_cast<uint4*>(olo + sw128(r, 4 * hc + q)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
         }
       }
-      if (quarter == 2) FTL(24 + t);
+      if (quarter == 2 && hc == 0) FTL(24 + t);
       fence_proxy_async();
-      named_bar(1 + t, 128);
-      if (quarter == 2) FTL(26 + t);
+      named_bar(1 + t, 256);
+      if (quarter == 2 && hc == 0) FTL(26 + t);
       if (wtid == 0) {
         tma_store_2d(&tm_o, o16, h * 64, (int)(row0 + 128 * t));
         if (out_lo) tma_store_2d(&tm_olo, olo, h * 64, (int)(row0 + 128 * t));
         bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&sm.stg_free);
       }
-      lse[((int64_t)f * H + h) * S + 128 * t + r] = mx * 0.125f + logf(sum);
-      if (quarter == 2) FTL(20 + t);
+      if (hc == 0) lse[((int64_t)f * H + h) * S + 128 * t + r] = mx * 0.125f + logf(sum);
+      if (quarter == 2 && hc == 0) FTL(20 + t);
     }
   } else if (has_tail) {
     // ------------------------------ tail warps (S = 257) ------------------------------
     // query row 256 against every key on CUDA cores (the key-256 column is formed by the softmax
     // warps, key 256's value row rides on the PV MMA)
-    const int tid = threadIdx.x - 320;  // 0 .. kFwdTailThreads - 1
+    const int tid = threadIdx.x - 32 * W_TAIL;  // 0 .. kFwdTailThreads - 1
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const uint32_t par = i & 1;
@@ -431,13 +428,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float s0 = (a0[0] + a0[1]) + (a0[2] + a0[3]);
       const float s1 = (a1[0] + a1[1]) + (a1[2] + a1[3]);
       float s256 = -INFINITY;
-      if (warp == 10) {
+      if (warp == W_TAIL) {
         const float2 x = unpack_bf16(qpair), y = unpack_bf16(*reinterpret_cast<const uint32_t*>(sm.krow[ks] + 4 * lane));
         s256 = warp_sum(fmaf(x.y, y.y, x.x * y.x));
       }
       mbar_arrive(&sm.k_free[ks]);
       float mx = warp_max(fmax3(s0, s1, s256));
-      if (lane == 0) sm.tail_red[warp - 10] = mx;
+      if (lane == 0) sm.tail_red[warp - W_TAIL] = mx;
       named_bar(3, kFwdTailThreads);
       mx = fmaxf(fmaxf(sm.tail_red[0], sm.tail_red[1]), fmaxf(sm.tail_red[2], sm.tail_red[3]));
       const float mb = mx * c2;
@@ -451,7 +448,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         sum += p256;
       }
       sum = warp_sum(sum);
-      if (lane == 0) sm.tail_red[kFwdTailWarps + warp - 10] = sum;
+      if (lane == 0) sm.tail_red[kFwdTailWarps + warp - W_TAIL] = sum;
       named_bar(3, kFwdTailThreads);
       sum = (sm.tail_red[kFwdTailWarps] + sm.tail_red[kFwdTailWarps + 1]) +
             (sm.tail_red[kFwdTailWarps + 2] + sm.tail_red[kFwdTailWarps + 3]);
@@ -461,10 +458,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int dpair = lane, part = tid >> 5;
       float oa0 = 0.f, oa1 = 0.f, ob0 = 0.f, ob1 = 0.f;
       if (tid == 0) FTL(44);
-      mbar_wait(&sm.v_full, par);
+      mbar_wait(&sm.v_full[ks], (i >> 1) & 1);
       if (tid == 0) FTL(45);
       const uint32_t chunk = dpair >> 2, within = (dpair & 3) * 4;
-      const uint8_t* vt = smem + F_V + (part >> 1) * TILE;  // a part's 64 keys lie in one tile
+      const uint8_t* vt = smem + F_V + ks * 2 * TILE + (part >> 1) * TILE;  // a part's 64 keys lie in one tile
 #pragma unroll 8
       for (int k = (part * KP) & 127; k < ((part * KP) & 127) + KP; k += 2) {
         const float2 va = unpack_bf16(*reinterpret_cast<const uint32_t*>(vt + sw128(k, chunk) + within));
@@ -477,12 +474,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       float o0 = oa0 + ob0, o1 = oa1 + ob1;
       if (part == kFwdTailWarps - 1) {  // value row 256 (row 0 of the PV MMA's 17th K-step tile)
-        const float2 vl = unpack_bf16(*reinterpret_cast<const uint32_t*>(smem + F_VX + 4 * dpair));
+        const float2 vl = unpack_bf16(*reinterpret_cast<const uint32_t*>(smem + F_VX + ks * 2048 + 4 * dpair));
         const float p256 = sm.tail_s[256];
         o0 = fmaf(p256, vl.x, o0);
         o1 = fmaf(p256, vl.y, o1);
       }
-      mbar_arrive(&sm.v_free);
+      mbar_arrive(&sm.v_free[ks]);
       if (tid == 0) FTL(46);
       named_bar(3, kFwdTailThreads);  // every part is done reading the probabilities in tail_s
       if (part > 0) {                 // partial outputs of parts 1.. into tail_s
@@ -508,7 +505,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       named_bar(3, kFwdTailThreads);
     }
   }
-  if (warp >= 2 && warp < 10 && lane == 0) bulk_wait0();
+  if (warp >= 2 && warp < W_TAIL && lane == 0) bulk_wait0();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
