@@ -145,6 +145,126 @@ __global__ void __launch_bounds__(256) vq_fwd4_kernel(const float* __restrict__ 
   if (row_sq) row_sq[r] = se;
 }
 
+// R rows per thread (rows r, r + 256, .. of the CTA's 256 R), CP codes per step: every staged code
+// is read from shared memory once for R rows, so the broadcast loads no longer bound the FFMA pipe
+// (one LDS.128 per 4 R FFMAs instead of four). Each (row, code) distance keeps vq_fwd_kernel's
+// sequential i order and codes are compared in index order per row, so the result is
+// bit-identical. 2 z_i is kept instead of z_i (z_i = 0.5 * (2 z_i) exactly).
+template <int DZ, int R, int CP, int kChunk>
+__global__ void __launch_bounds__(256, R >= 4 ? 1 : 2) vq_fwd4r_kernel(const float* __restrict__ z, int64_t rows,
+                                                                       const float* __restrict__ cb, int K,
+                                                                       int64_t* __restrict__ idx,
+                                                                       float* __restrict__ zq_st,
+                                                                       float* __restrict__ row_sq) {
+  constexpr int V = DZ / 4;
+  extern __shared__ float4 vq_smem[];  // kChunk codes (float4 x V each), then kChunk squared norms
+  float4* sc = vq_smem;
+  float* scc = reinterpret_cast<float*>(vq_smem + kChunk * V);
+  const int64_t rb = (int64_t)blockIdx.x * (256 * R) + threadIdx.x;
+  float z2[R][DZ];
+  float zz[R];
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int64_t r = rb + 256 * h;
+    zz[h] = 0.f;
+#pragma unroll
+    for (int i = 0; i < DZ; ++i) {
+      const float x = r < rows ? z[r * DZ + i] : 0.f;
+      zz[h] += x * x;
+      z2[h][i] = 2.0f * x;
+    }
+  }
+  float best[R];
+  int bi[R];
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    best[h] = INFINITY;
+    bi[h] = 0;
+  }
+  for (int k0 = 0; k0 < K; k0 += kChunk) {
+    const int kn = min(kChunk, K - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kn * V; e += blockDim.x)
+      sc[e] = *reinterpret_cast<const float4*>(cb + (int64_t)k0 * DZ + 4 * e);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kn; k += blockDim.x) {
+      float cc = 0.f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 c4 = sc[k * V + v];
+        cc += c4.x * c4.x; cc += c4.y * c4.y; cc += c4.z * c4.z; cc += c4.w * c4.w;
+      }
+      scc[k] = cc;
+    }
+    __syncthreads();
+    int k = 0;
+    for (; k + CP <= kn; k += CP) {
+      float d[CP][R];  // codes k .. k + CP - 1 x rows
+#pragma unroll
+      for (int c = 0; c < CP; ++c)
+#pragma unroll
+        for (int h = 0; h < R; ++h) d[c][h] = 0.f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+          const float4 p = sc[(k + c) * V + v];
+#pragma unroll
+          for (int h = 0; h < R; ++h) {
+            d[c][h] += z2[h][4 * v] * p.x; d[c][h] += z2[h][4 * v + 1] * p.y;
+            d[c][h] += z2[h][4 * v + 2] * p.z; d[c][h] += z2[h][4 * v + 3] * p.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CP; ++c) {
+        const float cc = scc[k + c];
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          const float e = (zz[h] - d[c][h]) + cc;
+          if (e < best[h]) { best[h] = e; bi[h] = k0 + k + c; }
+        }
+      }
+    }
+    for (; k < kn; ++k) {
+      float d0[R];
+#pragma unroll
+      for (int h = 0; h < R; ++h) d0[h] = 0.f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float4 p = sc[k * V + v];
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          d0[h] += z2[h][4 * v] * p.x; d0[h] += z2[h][4 * v + 1] * p.y;
+          d0[h] += z2[h][4 * v + 2] * p.z; d0[h] += z2[h][4 * v + 3] * p.w;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < R; ++h) {
+        const float e0 = (zz[h] - d0[h]) + scc[k];
+        if (e0 < best[h]) { best[h] = e0; bi[h] = k0 + k; }
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int64_t r = rb + 256 * h;
+    if (r >= rows) continue;
+    idx[r] = bi[h];
+    float se = 0.f;
+#pragma unroll
+    for (int i = 0; i < DZ; ++i) {
+      const float zi = 0.5f * z2[h][i];
+      const float q = cb[(int64_t)bi[h] * DZ + i];
+      const float diff = q - zi;
+      se += diff * diff;
+      if (zq_st) zq_st[r * DZ + i] = zi + diff;
+    }
+    if (row_sq) row_sq[r] = se;
+  }
+}
+
+
 // dz = g + commit_coef * (z - c_idx)
 __global__ void vq_bwd_z_kernel(const float* __restrict__ z, const float* __restrict__ cb,
                                 const int64_t* __restrict__ idx, const float* __restrict__ g, int64_t rows, int dz,
@@ -233,7 +353,14 @@ extern "C" int jz_vq_fwd(const float* z, int64_t rows, int dz, const float* code
     case 8: vq_fwd_kernel<8><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;
     case 16: vq_fwd_kernel<16><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;
     case 32:
-      if (((uintptr_t)codebook % 16) == 0) vq_fwd4_kernel<32><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq);
+      // several rows per thread while that still gives about a CTA per SM; one row for small batches
+      if (((uintptr_t)codebook % 16) == 0 && rows >= (int64_t)num_sms() * 1024 * 7 / 8) {
+        vq_fwd4r_kernel<32, 4, 4, 256><<<(unsigned)((rows + 1023) / 1024), 256, 256 * (32 * 4 + 4), st>>>(
+            z, rows, codebook, K, idx, zq_st, row_sq);
+      } else if (((uintptr_t)codebook % 16) == 0 && rows >= (int64_t)num_sms() * 512)
+        vq_fwd4r_kernel<32, 2, 2, 256><<<(unsigned)((rows + 511) / 512), 256, 256 * (32 * 4 + 4), st>>>(
+            z, rows, codebook, K, idx, zq_st, row_sq);
+      else if (((uintptr_t)codebook % 16) == 0) vq_fwd4_kernel<32><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq);
       else vq_fwd_kernel<32><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq);
       break;
     default: vq_fwd_kernel<64><<<grid, 256, 0, st>>>(z, rows, codebook, K, idx, zq_st, row_sq); break;

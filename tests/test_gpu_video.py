@@ -82,6 +82,24 @@ class TestVqKernel:
         assert _near_tie_ok(z, cb, idx.cpu().numpy(), ref)
 
 
+    @pytest.mark.parametrize("rows", [80000, 140000])
+    def test_multi_row_kernel_bit_identical(self, rows):
+        """Above 148 x 512 rows jz_vq_fwd runs two rows per thread, above ~148 x 896 four; both must
+        equal the one-row kernel (used for fewer rows) bit for bit: indices, z_q and squared errors."""
+        from paper_2510_27002_b200 import kernels as K
+        g = torch.Generator(device="cuda").manual_seed(11)
+        cb = torch.randn(1024, 32, device="cuda", generator=g) * 0.3
+        z = torch.randn(rows, 32, device="cuda", generator=g) * 0.3
+        for h, c in enumerate((513, 2, 1023, 0)):  # exact hits in every row slot of a thread
+            z[7 + 256 * h] = cb[c]
+        big = K.vq_fwd(z, cb)
+        parts = [K.vq_fwd(z[a:a + 40000].contiguous(), cb) for a in range(0, rows, 40000)]
+        for k in range(3):
+            got, ref = big[k], torch.cat([p[k] for p in parts])
+            assert torch.equal(got, ref), k
+        assert [big[0][7 + 256 * h].item() for h in range(4)] == [513, 2, 1023, 0]
+
+
 TOKKW = dict(model_dim=128, heads=2, ffn_dim=512, blocks=1, codes=64, latent_dim=32, patch=4, height=64, width=64,
              max_frames=4)
 
