@@ -428,6 +428,33 @@ def test_dyn_embed_fwd_modes(prepend, D, dl):
     assert int(err.item()) == 1
 
 
+@pytest.mark.parametrize("R", [147456, 9000])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_linear_f32_n32_rows_kernel_bit_identical(R, accumulate):
+    """The 512 -> 32 fp32 latent projection: the two-rows-per-lane kernel and the thread-per-output
+    kernel (reached through a 4-byte-misaligned x) both sum over k in order with fmaf, so their
+    outputs are bit-identical."""
+    K = 512
+    g = torch.Generator(device=dev).manual_seed(R + accumulate)
+    x = torch.randn(R, K, device=dev, generator=g)
+    W = torch.randn(K, 32, device=dev, generator=g)
+    b = torch.randn(32, device=dev, generator=g)
+    base = torch.randn(R, 32, device=dev, generator=g)
+    outs = []
+    for mode in ("fast", "scalar"):
+        y = base.clone()
+        xm = x
+        if mode == "scalar":
+            mis = torch.empty(R * K + 1, device=dev)
+            mis[1:].copy_(x.flatten())
+            xm = mis[1:].view(R, K)  # 4-byte aligned only: the thread-per-output kernel
+        Kn.linear_f32(xm, W, b, out=y, accumulate=bool(accumulate))
+        outs.append(y)
+    assert torch.equal(outs[0], outs[1])
+    ref = x.double() @ W.double() + b.double() + (base.double() if accumulate else 0)
+    assert rel(outs[0].double(), ref) < 1e-6
+
+
 @pytest.mark.parametrize("K,N", [(512, 32), (32, 512), (48, 32)])
 @pytest.mark.parametrize("accumulate", [0, 1])
 def test_linear_f32_bwd_parallel_vs_reference_kernel(K, N, accumulate):
