@@ -23,7 +23,8 @@ namespace sp {
 constexpr int kFwdTailWarps = 4;  // query row 256 (S = 257) on CUDA cores
 constexpr int kFwdTailThreads = 32 * kFwdTailWarps;
 constexpr int W_TAIL = 18;  // w0 TMA, w1 MMA, w2-9 tile 0, w10-17 tile 1 (two warps per TMEM lane quarter), w18.. tail
-constexpr int kFwdThreads = 32 * W_TAIL + kFwdTailThreads;
+constexpr int W_STORE = W_TAIL + kFwdTailWarps;  // the O / residual TMA store warp
+constexpr int kFwdThreads = 32 * (W_STORE + 1);
 constexpr int TILE = 16384;    // 128 rows x 128 B
 // forward smem map (bytes, from a 1024-aligned base)
 constexpr int F_Q = 0;                  // 2 tiles (query tiles 0 / 1)
@@ -40,6 +41,7 @@ constexpr int F_SMEM = F_END + kFwdSmall + 1024;
 
 struct FwdSmallSmem {
   uint64_t q_full[2], q_free[2], k_full[2], k_free[2], v_full[2], v_free[2];
+  uint64_t stg_full;     // a tile's O / residual rows are staged (one phase per tile epilogue)
   uint64_t stg_free;     // the staging tiles' previous TMA store has read them (one phase per tile epilogue)
   uint64_t s_full[2], p_full[2], o_full[2], tmem_free[2];
   uint64_t exp_turn[2];  // the two softmax warpgroups take turns on the exponentials
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&sm.v_full[b], 1);
       mbar_init(&sm.v_free[b], 1 + ntail);  // PV_1 MMA commit + tail warps
     }
+    mbar_init(&sm.stg_full, 8);  // lane 0 of the tile's 8 warps
     mbar_init(&sm.stg_free, 1);
     fence_barrier_init();
   }
@@ -257,7 +260,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int sw = warp - 2;
     const int t = sw >> 3, hc = (sw >> 2) & 1, quarter = warp & 3;
     const int r = quarter * 32 + lane;             // query row within the tile
-    const int wtid = threadIdx.x - 64 - 256 * t;   // 0 .. 255
     const uint32_t lrow = tmem + ((quarter * 32) << 16) + 256 * t;
     const uint32_t scol = lrow + 128 * hc;         // this warp's S columns
     uint8_t* o16 = smem + F_ST;                    // [128 rows][64 bf16], 128B swizzle
@@ -267,7 +269,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
       const uint32_t par = i & 1;
       const int f = u / H, h = u % H;
-      const int64_t row0 = (int64_t)f * S;
       // S = 257: q_r . k_256 on CUDA cores while S_t is computed, by the half-1 warp of the row (the
       // half-0 warp takes it through the exchange below). Splitting the dot product between the
       // two warps was measured to give wrong key-256 scores for some rows on a first launch.
@@ -377,27 +378,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       if (quarter == 2 && hc == 0) FTL(24 + t);
-      fence_proxy_async();
-      named_bar(1 + t, 256);
+      fence_proxy_async();  // generic staging writes before the store warp's bulk copy reads them
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.stg_full);
       if (quarter == 2 && hc == 0) FTL(26 + t);
-      if (wtid == 0) {
-        tma_store_2d(&tm_o, o16, h * 64, (int)(row0 + 128 * t));
-        if (out_lo) tma_store_2d(&tm_olo, olo, h * 64, (int)(row0 + 128 * t));
-        bulk_commit();
-        bulk_wait_read0();
-        mbar_arrive(&sm.stg_free);
-      }
       if (hc == 0) lse[((int64_t)f * H + h) * S + 128 * t + r] = mx * 0.125f + logf(sum);
       if (quarter == 2 && hc == 0) FTL(20 + t);
     }
-  } else if (has_tail) {
+  } else if (warp < W_STORE && has_tail) {
     // ------------------------------ tail warps (S = 257) ------------------------------
     // query row 256 against every key on CUDA cores (the key-256 column is formed by the softmax
     // warps, key 256's value row rides on the PV MMA)
     const int tid = threadIdx.x - 32 * W_TAIL;  // 0 .. kFwdTailThreads - 1
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-      const uint32_t par = i & 1;
       const int ks = i & 1;
       const int f = u / H, h = u % H;
       const int64_t row0 = (int64_t)f * S;
@@ -504,8 +498,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       named_bar(3, kFwdTailThreads);
     }
+  } else if (warp == W_STORE && lane == 0) {
+    // ------------------------------ store warp ------------------------------
+    // the tile epilogues alternate (stg_free): store tile 0 then tile 1 of every unit, and release
+    // the staging once the bulk copies have read it, so no softmax warp waits on a store
+    int e = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int f = u / H, h = u % H;
+      for (int t = 0; t < 2; ++t, ++e) {
+        mbar_wait(&sm.stg_full, e & 1);
+        const int row = f * S + 128 * t;
+        tma_store_2d(&tm_o, smem + F_ST, h * 64, row);
+        if (out_lo) tma_store_2d(&tm_olo, smem + F_ST + TILE, h * 64, row);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&sm.stg_free);
+      }
+    }
+    bulk_wait0();
   }
-  if (warp >= 2 && warp < W_TAIL && lane == 0) bulk_wait0();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
