@@ -317,16 +317,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // exponentials, 32 keys per TMEM wait. P of keys 128 hc + 32 j .. + 31 goes to columns
       // 16 j .. (half 0) / 192 + 16 j .. (half 1, walked from its last 32 keys down) as bf16 pairs:
       // every column is read before this warp overwrites it.
-#pragma unroll 1
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = hc ? 3 - jj : jj;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32_wait(scol + 32 * j, v);
-        uint32_t pk[16];
+      {
+        // the next 32 columns load while these are exponentiated
+        uint32_t va[32], vb[32];
+        tmem_ld_32x32b_x32(scol + 32 * (hc ? 3 : 0), va);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2)
-          pk[e / 2] = pack_bf16(ex2(fmaf(__uint_as_float(v[e]), c2, -mb)), ex2(fmaf(__uint_as_float(v[e + 1]), c2, -mb)));
-        tmem_st_32x32b_x16(lrow + (hc ? 192 : 0) + 16 * j, pk);
+        for (int jj = 0; jj < 4; jj += 2) {
+          const int j0 = hc ? 3 - jj : jj, j1 = hc ? 2 - jj : jj + 1;
+          uint32_t pk[16];
+          tmem_ld_wait();
+          tmem_ld_32x32b_x32(scol + 32 * j1, vb);
+#pragma unroll
+          for (int e = 0; e < 32; e += 2)
+            pk[e / 2] = pack_bf16(ex2(fmaf(__uint_as_float(va[e]), c2, -mb)), ex2(fmaf(__uint_as_float(va[e + 1]), c2, -mb)));
+          tmem_st_32x32b_x16(lrow + (hc ? 192 : 0) + 16 * j0, pk);
+          tmem_ld_wait();
+          if (jj + 2 < 4) tmem_ld_32x32b_x32(scol + 32 * (hc ? 1 - jj : jj + 2), va);
+#pragma unroll
+          for (int e = 0; e < 32; e += 2)
+            pk[e / 2] = pack_bf16(ex2(fmaf(__uint_as_float(vb[e]), c2, -mb)), ex2(fmaf(__uint_as_float(vb[e + 1]), c2, -mb)));
+          tmem_st_32x32b_x16(lrow + (hc ? 192 : 0) + 16 * j1, pk);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.exp_turn[t]);
