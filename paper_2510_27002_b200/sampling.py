@@ -203,8 +203,14 @@ class FrameDecoder:
         xn, _, _ = _K.layernorm_fwd(x, P[f"{base}.spatial.ln.g"].data, P[f"{base}.spatial.ln.b"].data)
         qkv = _K.linear_fwd(xn, w["spatial.wqkv"], w["spatial.bqkv"])
         ao, _, _ = _K.attn_spatial_fwd(qkv, B * T, S, H, keep_lo=False)
-        x1 = _K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=_L.EPI_RESID, aux=x)
-        xn2, _, _ = _K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
+        # the attention output projections emit the next LayerNorm from their epilogue, as in training
+        fuse = _K.ln_fusable(B * T * S, self.D, K=self.D)
+        if fuse:
+            x1, xn2, _, _ = _K.linear_fwd_ln(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, x,
+                                             P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
+        else:
+            x1 = _K.linear_fwd(ao, w["spatial.wo"], P[f"{base}.spatial.o.b"].data, epilogue=_L.EPI_RESID, aux=x)
+            xn2, _, _ = _K.layernorm_fwd(x1, P[f"{base}.temporal.ln.g"].data, P[f"{base}.temporal.ln.b"].data)
         qkv2 = _K.linear_fwd(xn2, w["temporal.wqkv"], w["temporal.bqkv"])
         mode, arg = temporal
         if mode == "full":
@@ -217,8 +223,12 @@ class FrameDecoder:
             _L.call("jz_attn_temporal_decode", qkv2.data_ptr(), self.cache[i].data_ptr(), B, t,
                     None if dev_t is None else dev_t.data_ptr(), self.t_max, S, H, int(append), ao2.data_ptr(),
                     _L.stream_ptr())
-        x2 = _K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=_L.EPI_RESID, aux=x1)
-        xn3, _, _ = _K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
+        if fuse:
+            x2, xn3, _, _ = _K.linear_fwd_ln(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, x1,
+                                             P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
+        else:
+            x2 = _K.linear_fwd(ao2, w["temporal.wo"], P[f"{base}.temporal.o.b"].data, epilogue=_L.EPI_RESID, aux=x1)
+            xn3, _, _ = _K.layernorm_fwd(x2, P[f"{base}.ffn.ln.g"].data, P[f"{base}.ffn.ln.b"].data)
         h = _K.linear_fwd(xn3, w["ffn.wup"], P[f"{base}.ffn.up.b"].data, epilogue=_L.EPI_GELU)
         return _K.linear_fwd(h, w["ffn.wdown"], P[f"{base}.ffn.down.b"].data, epilogue=_L.EPI_RESID, aux=x2)
 
