@@ -421,10 +421,11 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
             else sm.part_dq[quarter][dim] += a;
           }
           if (j == 1) {
-            // dQ_256 = scale (sum_k dS[256, k] K_k + dS[256, 256] k256)
-            named_bar(1, 32 * kPds);
-            const int pt = threadIdx.x - 32 * W_PDS;
-            if (pt < 64) {
+            // dQ_256 = scale (sum_k dS[256, k] K_k + dS[256, 256] k256): the dims of column group cg
+            // are summed over the four lane quarters by that group's warps alone
+            named_bar(4 + cg, 128);
+            const int pt = QW * cg + lane;
+            if (quarter == 0 && lane < QW) {
               MBAR_WAIT(&sm.vec_ready, i & 1);
               float acc = sm.part_dq[0][pt] + sm.part_dq[1][pt] + sm.part_dq[2][pt] + sm.part_dq[3][pt];
               acc = scale * (acc + uv[U_DC] * __bfloat162float(sm.vec[T_K][pt]));
