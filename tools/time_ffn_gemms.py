@@ -4,7 +4,9 @@ import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().par
 import torch
 
 from paper_2510_27002_b200 import _lib as L
-from paper_2510_27002_b200 import kernels as Kn
+if len(sys.argv) > 1 and sys.argv[1].endswith(".so"):
+    L.LIB_PATH = pathlib.Path(sys.argv[1]).resolve()
+from paper_2510_27002_b200 import kernels as Kn  # noqa: E402
 
 L.ensure_device()
 M, d, f = 148032, 512, 2048
@@ -36,6 +38,5 @@ def t(fn, n=20):
 up = t(lambda: Kn.linear_fwd(xn, wup, bf_, epilogue=L.EPI_GELU_DG, out2=hd, out=hh))
 dn = t(lambda: Kn.linear_dx(dres, wdn, epilogue=L.EPI_MUL_F16, out=dh, aux=hd))
 dnc = t(lambda: Kn.linear_dx(dres, wdn, epilogue=L.EPI_MUL_F16, out=dh, aux=hd, colsum=cs))
-print(f"GELU_DG up {up:.1f} us | MUL_F16 dX {dn:.1f} us | MUL_F16 dX + colsum {dnc:.1f} us")
-ref_h = hh.clone(); ref_d = hd.clone(); ref_dh = dh.clone()
-torch.save({"h": ref_h.cpu(), "d": ref_d.cpu(), "dh": ref_dh.cpu(), "cs": cs.cpu()}, f"/tmp/ffn_{sys.argv[1] if len(sys.argv) > 1 else 'x'}.pt")
+print(f"GELU_DG up {up:.1f} us | MUL_F16 dX {dn:.1f} us | MUL_F16 dX + colsum {dnc:.1f} us "
+      f"({pathlib.Path(sys.argv[1]).name if len(sys.argv) > 1 else 'default'})")
