@@ -272,13 +272,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // S = 257: q_r . k_256 on CUDA cores while S_t is computed, by the half-1 warp of the row (the
       // half-0 warp takes it through the exchange below). Splitting the dot product between the
       // two warps was measured to give wrong key-256 scores for some rows on a first launch.
+      // Both warps wait for the tiles before arriving on their release barriers: an arrival for
+      // unit i + 2 must not land in the K slot's phase of unit i (the tail warps may still be
+      // reading that slot), and waiting for k_full of this unit guarantees that phase completed.
       float dpart = 0.f;
       if (has_tail) {
-        if (hc == 1) {
-          mbar_wait(&sm.k_full[i & 1], (i >> 1) & 1);
-          mbar_wait(&sm.q_full[t], par);
-          dpart = dot64_tile_row(smem + F_Q + t * TILE, r, sm.krow[i & 1]);
-        }
+        mbar_wait(&sm.k_full[i & 1], (i >> 1) & 1);
+        mbar_wait(&sm.q_full[t], par);
+        if (hc == 1) dpart = dot64_tile_row(smem + F_Q + t * TILE, r, sm.krow[i & 1]);
         mbar_arrive(&sm.q_free[t]);      // done with the Q tile
         mbar_arrive(&sm.k_free[i & 1]);  // and with key row 256
       }
