@@ -6,9 +6,10 @@
 //
 // S = 257 does not tile (256 patch tokens + the prepended action token,
 // dynamics.py:118): tokens 0..255 run on the tensor cores as two 128-row query
-// tiles against one 256-key tile; the 257th key is folded into each row's
-// softmax on CUDA cores, and the 257th query row is computed by two "tail" warps
-// on CUDA cores — exactly, no padding waste.
+// tiles against one 256-key tile; the 257th key's score is formed on CUDA cores
+// and its value row rides on the PV MMA as a 17th K-step, and the 257th query row
+// is computed by four "tail" warps on CUDA cores — exactly, no padding waste
+// (SURVEY §7.4.1).
 //
 // qkv bf16 [M, 3D] (row = frame*S + s), out bf16 [M, D], lse f32 [frame][H][S].
 #include <mutex>
@@ -104,13 +105,14 @@ JZ_DEV float dot64_tile_row(const uint8_t* tile, uint32_t r, const uint8_t* row)
 
 using namespace sp;
 
-// One CTA per SM walks (frame, head) units. Query tile t (rows 128t..128t+127) belongs to softmax
-// warpgroup t; S_t = Q_t K^T (128 x 256 fp32) sits in TMEM columns 256t..256t+255, P overwrites its
-// first 128 columns as bf16 pairs and O_t = P_t V accumulates in columns 256t+128..256t+191.
-// The two warpgroups take turns on the exponentials (exp_turn), so one warpgroup's max pass, PV
-// wait and epilogue overlap the other's MUFU-bound exponential pass. K is double-buffered by unit
-// parity so the next unit's scores can start while this unit's second tile is still in flight.
-// S = 257: the tail warps form query row 256 and the key-256 column on CUDA cores.
+// One CTA per SM walks (frame, head) units. Query tile t (rows 128t..128t+127) belongs to 8 softmax
+// warps (two per TMEM lane quarter, one per 128-key half); S_t = Q_t K^T (128 x 256 fp32) sits in
+// TMEM columns 256t..256t+255. P is written back as bf16 pairs (keys 0..127 at columns 0..63,
+// keys 128..255 at 192..255, key 256 at 144) and O_t = P_t [V | 1] accumulates 64 dims + 16
+// row-sum columns at 64..143. The two tiles take turns on the exponentials (exp_turn), so one
+// tile's max pass, PV wait and epilogue overlap the other's MUFU-bound exponential pass. K and V
+// are double-buffered by unit parity; a store warp issues the O / residual TMA stores.
+// S = 257: the half-1 warps form the key-256 scores, the tail warps query row 256.
 __global__ void __launch_bounds__(kFwdThreads, 1)
     spatial_fwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_row,
                        const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_olo,
