@@ -372,8 +372,6 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
     const uint32_t lbase = tmem + ((quarter * 32) << 16);
     int i = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-      const int f = u / H, h = u % H;
-      const int64_t row0 = (int64_t)f * S;
       const float* uv = sm.uvb[i & 1];
       for (int x = 0; x < NB; ++x) {
         int j, c;
@@ -400,40 +398,7 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.prow_full[j]);  // one phase per unit and key half
           }
-          // dQ_256 partial over this warp's 32 keys, dims [QW cg, QW cg + QW)
-          float v[QW];
-          const uint8_t* krow = smem + S_K + j * TILE;
-#pragma unroll
-          for (int k = 0; k < QW / 8; ++k) {
-            const uint4 w = *reinterpret_cast<const uint4*>(krow + sw128(r, (QW / 8) * cg + k));
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 kf = unpack_bf16(ww[e]);
-              v[8 * k + 2 * e] = ds * kf.x;
-              v[8 * k + 2 * e + 1] = ds * kf.y;
-            }
-          }
-          const float a = warp_reduce_scatter<QW>(v, lane);
-          const int dim = QW * cg + (QW == 32 ? lane : (lane >> 1));
-          if (QW == 32 || (lane & 1) == 0) {
-            if (j == 0) sm.part_dq[quarter][dim] = a;
-            else sm.part_dq[quarter][dim] += a;
-          }
-          if (j == 1) {
-            // dQ_256 = scale (sum_k dS[256, k] K_k + dS[256, 256] k256): the dims of column group cg
-            // are summed over the four lane quarters by that group's warps alone
-            named_bar(4 + cg, 128);
-            const int pt = QW * cg + lane;
-            if (quarter == 0 && lane < QW) {
-              MBAR_WAIT(&sm.vec_ready, i & 1);
-              float acc = sm.part_dq[0][pt] + sm.part_dq[1][pt] + sm.part_dq[2][pt] + sm.part_dq[3][pt];
-              acc = scale * (acc + uv[U_DC] * __bfloat162float(sm.vec[T_K][pt]));
-              const __nv_bfloat16 bq = __float2bfloat16_rn(acc);
-              dqkv[(row0 + 256) * ld3 + h * 64 + pt] = bq;
-              if (colsum) colsum[((int64_t)f * 9 + 8) * ld3 + h * 64 + pt] = __bfloat162float(bq);
-            }
-          }
+          // (the dQ_256 row, sum_k dS[256, k] K_k, is formed by the helper warps from ds_row)
           __syncwarp();
           if (warp == W_PDS) TL(43 + x);
           if (lane == 0) mbar_arrive(&sm.pds_full[g % 3]);
@@ -634,8 +599,29 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
           sm.part_ct[quarter][(pass >> 1) * 64 + 32 * half + lane] = a;
         }
       }
+      if (tail) {
+        // dQ_256 partials: sum_k dS[256, k] K_k over keys 64 hw .. 64 hw + 63 (lane: dims 2 lane,
+        // 2 lane + 1), once the P/dS warps have written both key halves' ds_row; K is still staged
+        MBAR_WAIT(&sm.prow_full[0], i & 1);
+        MBAR_WAIT(&sm.prow_full[1], i & 1);
+        const uint8_t* kt = smem + S_K + (hw >> 1) * TILE;
+        const float* dsr = sm.ds_row + 64 * hw;
+        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll 8
+        for (int kk = 0; kk < 64; kk += 2) {
+          const int k = 64 * (hw & 1) + kk;
+          const float2 ka = unpack_bf16(*reinterpret_cast<const uint32_t*>(kt + sw128(k, lane >> 2) + 4 * (lane & 3)));
+          const float2 kb = unpack_bf16(*reinterpret_cast<const uint32_t*>(kt + sw128(k + 1, lane >> 2) + 4 * (lane & 3)));
+          const float2 d = *reinterpret_cast<const float2*>(dsr + kk);
+          a0 = fmaf(d.x, ka.x, a0);
+          a1 = fmaf(d.x, ka.y, a1);
+          b0 = fmaf(d.y, kb.x, b0);
+          b1 = fmaf(d.y, kb.y, b1);
+        }
+        *reinterpret_cast<float2*>(&sm.part_dq[hw][2 * lane]) = make_float2(a0 + b0, a1 + b1);
+      }
       __syncwarp();
-      if (lane == 0) {  // done with the tail rows (A), Q_0 / dO_0 (B), Q_1 / dO_1 (C)
+      if (lane == 0) {  // done with the tail rows (A), Q_0 / dO_0 (B), Q_1 / dO_1 (C), K_1 (D)
         mbar_arrive(&sm.free_a);
         mbar_arrive(&sm.free_b);
         mbar_arrive(&sm.free_cd);
@@ -685,12 +671,18 @@ __global__ void __launch_bounds__(sb::kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.dq_free[1]);
-      // ---- token 256: dK_256, dV_256 (dQ_256 comes from the P/dS warps) ----
+      // ---- token 256: dQ_256, dK_256, dV_256 ----
       named_bar(2, 128);
       if (ht < 64) {
         const int d = ht;
         float* pr = colsum ? colsum + ((int64_t)f * 9 + 8) * ld3 + h * 64 + d : nullptr;
         if (tail) {
+          // dQ_256 = scale (sum_k dS[256, k] K_k + dS[256, 256] k256)
+          float aq = (sm.part_dq[0][d] + sm.part_dq[1][d]) + (sm.part_dq[2][d] + sm.part_dq[3][d]);
+          aq = scale * (aq + uv[U_DC] * __bfloat162float(sm.vec[T_K][d]));
+          const __nv_bfloat16 bq = __float2bfloat16_rn(aq);
+          dqkv[(row0 + 256) * ld3 + h * 64 + d] = bq;
+          if (pr) pr[0] = __bfloat162float(bq);
           float sk = uv[U_DC] * __bfloat162float(sm.vec[T_Q][d]);
           float sv = uv[U_PC] * __bfloat162float(sm.vec[T_DO][d]);
 #pragma unroll
