@@ -227,6 +227,32 @@ def test_attn_spatial_fwd_bwd(S, frames):
         assert rel(got.reshape(frames, S, D)[:, -1], ref.reshape(frames, S, D)[:, -1]) < 2e-2, "qkv"[i]
 
 
+@pytest.mark.parametrize("S,frames", [(257, 1), (256, 1), (257, 19), (257, 37), (256, 149)])
+def test_attn_spatial_unit_counts(S, frames):
+    """Unit counts around the CTA grid (8 heads: 8 .. 1192 units on 148 CTAs, so CTAs run 0 to 9
+    units and the K / V slots, the alternating tile epilogues and the tail warps wrap several
+    times): forward (with and without the residual) and backward against torch fp32."""
+    H = 8
+    D = H * 64
+    g = torch.Generator(device=dev).manual_seed(S * 1000 + frames)
+    qkv = (torch.randn(frames * S, 3 * D, device=dev, generator=g) * 1.5).bfloat16()
+    out, out_lo, lse = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=True)
+    out2, _, lse2 = Kn.attn_spatial_fwd(qkv, frames, S, H, keep_lo=False)
+    assert torch.equal(out, out2) and torch.equal(lse, lse2)
+    qf = qkv.float().requires_grad_(True)
+    o_ref, lse_ref = _ref_attn(qf.reshape(frames, S, 3 * D), (frames,), S, H, False)
+    assert rel(out.reshape(frames, S, D), o_ref) < 1e-2
+    assert rel(lse, lse_ref) < 2e-4
+    go = torch.randn(o_ref.shape, device=dev, generator=g)
+    o_ref.backward(go)
+    dqkv = torch.full_like(qkv, float("nan"))
+    Kn.attn_spatial_bwd(qkv, out, go.reshape(frames * S, D).bfloat16().contiguous(), lse, frames, S, H, dqkv=dqkv,
+                        out_lo=out_lo)
+    assert torch.isfinite(dqkv.float()).all()
+    for i in range(3):
+        assert rel(dqkv[:, i * D:(i + 1) * D], qf.grad[:, i * D:(i + 1) * D]) < 2e-2, "qkv"[i]
+
+
 @pytest.mark.parametrize("S", [257, 256])
 def test_attn_spatial_run_to_run_bitwise(S):
     """Spatial attention forward (O, its residual, lse) and backward (dq/dk/dv, bias column sums) are
