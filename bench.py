@@ -593,6 +593,18 @@ def main() -> None:
     ms_e2e = max_over_ranks(e2.elapsed_time(e3)) / args.steps
     e2e_value = frames_per_step / (ms_e2e / 1e3)
     h2d = tokens_h.numel() * tokens_h.element_size() + lat_h.numel() * lat_h.element_size()
+    # the device-resident loop once more, after the e2e loop: on a power-capped box the clock drifts
+    # between back-to-back loops, and |value - value_repeat| is that run-to-run spread (it can exceed
+    # the ~1.25 MB / step H2D cost the e2e loop adds)
+    sync_all()
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record()
+    for _ in range(args.steps):
+        runner.step(step, tokens_d, lat_d)
+        step += 1
+    e5.record()
+    sync_all()
+    value_repeat = frames_per_step / (max_over_ranks(e4.elapsed_time(e5)) / args.steps / 1e3)
 
     # ---- secondary BASELINE configs (rank 0, N=1): C5 sampling, C2 LAM step, C1 tokenizer fwd ----
     extra = {}
@@ -670,6 +682,8 @@ def main() -> None:
                            "l2": "working set ~20 GB per step >> 126 MB L2 (no flush needed)"},
                 "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": 4},
+                "value_repeat": round(value_repeat, 1),
+                "run_to_run_spread_pct": round(100 * abs(value - value_repeat) / value, 2),
                 "gpu_launches": int(launches),
                 "roofline": roofline,
                 "model_tflops": round(step_flops / (ms / 1e3) / 1e12, 1),
